@@ -1,0 +1,181 @@
+/*
+ * zcgraph.h -- C ABI of the B200-native EMOGI zero-copy traversal library
+ * (libzcgraph_b200.so, built from paper_2006_06890_b200/csrc/).
+ *
+ * The reference (arxiv 2006.06890, package `zcgraph`, pure Python) has no FFI
+ * layer; its boundary is the Python library API.  Each entry point below
+ * replaces one reference interface, cited as path:line relative to
+ * /root/reference/pkg/src/zcgraph/:
+ *
+ *   zc_graph_create   <- CsrGraph (csr.py:34-77) + validate (csr.py:80-105):
+ *                        the caller's CSR arrays become a handle whose edge /
+ *                        weight lists live in pinned mapped host memory
+ *                        (ZC_PLACE_ZEROCOPY), managed memory (ZC_PLACE_UVM) or
+ *                        HBM (ZC_PLACE_HBM); offsets and all per-vertex state
+ *                        live in HBM.
+ *   zc_bfs            <- bfs(g, source, strategy, ...)   traversal.py:98-120
+ *   zc_sssp           <- sssp(g, source, strategy, ...)  traversal.py:123-151
+ *   zc_cc             <- cc(g, strategy, ...)            traversal.py:154-179
+ *   zc_run_log        <- TraversalResult.traversed_edges traversal.py:26-45,63-65
+ *   zc_run_traffic    <- TraversalResult.per_iteration_traffic (the modelled
+ *                        request histogram, coalesce.py:44-85,165-207)
+ *   strategy ids      <- AccessStrategy                  access.py:28-31
+ *   ZC_UNREACHED_*    <- UNREACHED_LEVEL / UNREACHED_DIST traversal.py:22-23
+ *
+ * Conventions
+ *   - Every function returning int returns ZC_OK (0) on success and a
+ *     negative ZC_E* code otherwise; zc_last_error() then returns a message
+ *     (thread-local, valid until the next call on that thread).
+ *   - ZC_EINVAL is returned for exactly the conditions the reference raises
+ *     ValueError for (source out of range, missing / negative weights, CC on
+ *     a directed graph, invariant violations); the Python wrapper maps it to
+ *     ValueError and every other code to RuntimeError.
+ *   - Results are written as int64 into caller-owned buffers of length V
+ *     (the reference's result dtype).  Calls on one handle are serialised by
+ *     the caller; different handles may be used from different threads.
+ *   - No torch / C++ types cross this boundary.
+ */
+#ifndef ZCGRAPH_H_
+#define ZCGRAPH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZC_ABI_VERSION 1
+
+/* status codes */
+#define ZC_OK 0
+#define ZC_EINVAL (-1)   /* reference ValueError conditions */
+#define ZC_ECUDA (-2)    /* CUDA runtime / driver error */
+#define ZC_ENOMEM (-3)   /* host or device allocation failed */
+#define ZC_ESTATE (-4)   /* API misuse (null handle, wrong placement, ...) */
+
+/* access strategies (access.py:28-31, report.py:31-35 names) */
+#define ZC_NAIVE 0          /* "naive": thread per frontier vertex          */
+#define ZC_MERGED 1         /* "merged": warp per vertex, 32-element steps  */
+#define ZC_MERGED_ALIGNED 2 /* "merged-aligned": first step floored to 128 B */
+
+/* where the edge / weight lists live */
+#define ZC_PLACE_ZEROCOPY 0 /* cudaHostAlloc(Mapped|Portable) or cudaHostRegister */
+#define ZC_PLACE_UVM 1      /* cudaMallocManaged + cudaMemAdviseSetReadMostly     */
+#define ZC_PLACE_HBM 2      /* cudaMalloc: in-HBM control run                     */
+
+/* zc_graph_desc.flags */
+#define ZC_F_DIRECTED 1u        /* CsrGraph.directed (csr.py:45)                     */
+#define ZC_F_REGISTER 2u        /* ZEROCOPY: cudaHostRegister the caller's edge /
+                                   weight buffers in place instead of copying; they
+                                   must outlive the handle, be 128 B aligned and
+                                   already have the device element width          */
+#define ZC_F_UVM_PREFETCH 4u    /* UVM: cudaMemPrefetchAsync the lists before runs   */
+#define ZC_F_NO_VALIDATE 8u     /* skip the O(V+E) invariant check (trusted input)   */
+
+/* unreached markers in the int64 results (traversal.py:22-23) */
+#define ZC_UNREACHED_LEVEL (-1LL)
+#define ZC_UNREACHED_DIST (0x7fffffffffffffffLL)
+
+typedef struct zc_graph zc_graph;
+
+typedef struct zc_graph_desc {
+  uint64_t num_vertices;       /* V (device path requires V < 2^32 - 1)        */
+  uint64_t num_edges;          /* E                                            */
+  const int64_t *offsets;      /* V+1 entries, offsets[0]=0, offsets[V]=E      */
+  const void *edges;           /* E entries of src_edge_bytes each             */
+  const void *weights;         /* NULL or E entries of src_weight_bytes each   */
+  uint32_t src_edge_bytes;     /* width of the caller's edge array: 4 or 8     */
+  uint32_t src_weight_bytes;   /* width of the caller's weight array: 4 or 8   */
+  uint32_t edge_elem_bytes;    /* CsrGraph.edge_elem_bytes: 4 or 8 (device)    */
+  uint32_t weight_elem_bytes;  /* CsrGraph.weight_elem_bytes: 4 or 8 (device)  */
+  int32_t placement;           /* ZC_PLACE_*                                   */
+  int32_t device;              /* CUDA device ordinal                          */
+  uint32_t flags;              /* ZC_F_*                                       */
+  uint32_t reserved;
+} zc_graph_desc;
+
+/* Per-run statistics.  traversed_edges / frontier sizes per iteration are
+ * retrieved with zc_run_log (the count can exceed any fixed array). */
+typedef struct zc_stats {
+  uint64_t iterations;             /* TraversalResult.iterations            */
+  uint64_t total_traversed_edges;  /* sum of traversed_edges                */
+  uint64_t max_frontier;           /* largest frontier                      */
+  double kernel_ms;                /* device time of the traversal loop     */
+  double total_ms;                 /* host wall time of the whole call      */
+  double d2h_ms;                   /* device time of the result download    */
+  uint64_t h2d_bytes;              /* bytes copied host->device in the call */
+  uint64_t d2h_bytes;              /* bytes copied device->host in the call */
+  uint64_t launches;               /* kernels launched by the call          */
+  uint64_t reserved[7];
+} zc_stats;
+
+const char *zc_last_error(void);
+int zc_abi_version(void);
+int zc_device_count(int *count);
+
+/* Graph handle lifecycle. */
+int zc_graph_create(const zc_graph_desc *desc, zc_graph **out);
+void zc_graph_destroy(zc_graph *g);
+/* Host pointers of the handle's edge / weight lists (pinned, managed or a
+ * host shadow for HBM placement) -- used by checkers and generators. */
+int zc_graph_host_lists(zc_graph *g, void **edges, void **weights, const int64_t **offsets);
+int zc_graph_info(const zc_graph *g, uint64_t *num_vertices, uint64_t *num_edges,
+                  uint32_t *edge_elem_bytes, uint32_t *weight_elem_bytes,
+                  int32_t *placement, uint32_t *flags);
+
+/* Traversals (reference traversal.py:98-179).  out: caller buffer, V int64. */
+int zc_bfs(zc_graph *g, uint64_t source, int strategy, int64_t *out, zc_stats *stats);
+int zc_sssp(zc_graph *g, uint64_t source, int strategy, int64_t *out, zc_stats *stats);
+int zc_cc(zc_graph *g, int strategy, int64_t *out, zc_stats *stats);
+
+/* Per-iteration log of the handle's most recent run: traversed_edges[k] =
+ * sum of frontier degrees of iteration k (traversal.py:63-65) and the
+ * frontier size.  Copies min(capacity, iterations) entries; either pointer
+ * may be NULL. */
+int zc_run_log(const zc_graph *g, uint64_t *traversed_edges, uint64_t *frontier_sizes,
+               uint64_t capacity);
+
+/* Per-handle run options. */
+#define ZC_OPT_TRAFFIC_MODEL 1u /* also evaluate the reference's request model
+                                   (coalesce.py:165-207) on every frontier */
+int zc_set_options(zc_graph *g, uint32_t options);
+
+/* Modelled request histogram of the most recent run (needs
+ * ZC_OPT_TRAFFIC_MODEL): for iteration k, hist[8k+i] = edge-list requests of
+ * (i+1)*32 bytes and hist[8k+4+i] = weight-list requests (SSSP), i = 0..3 --
+ * TrafficStats.hist of traversal.py:66-73.  Copies min(capacity, iterations)
+ * iterations. */
+int zc_run_traffic(const zc_graph *g, uint64_t *hist, uint64_t capacity);
+
+/* Pinned host memory for result buffers (D2H at link speed). */
+void *zc_host_alloc(size_t bytes);
+void zc_host_free(void *p);
+
+/* Native synthetic graph generators.  The graph is
+ * generated on `device`, written straight into a new handle with the given
+ * placement; deterministic in (parameters, seed).
+ *   rmat:    R-MAT / Kronecker (a,b,c; d = 1-a-b-c), 2^scale vertices,
+ *            edge_factor * 2^scale arcs, Feistel vertex permutation,
+ *            duplicates / self loops kept; symmetrize!=0 adds reverse arcs
+ *            (csr.py:350-359 semantics, lists sorted by destination).
+ *   uniform: out-degree in [min_degree, max_degree], destinations uniform
+ *            without in-list duplicates (csr.py:248-282 semantics).
+ *   weights (both): uniform integers in [wlow, whigh] when wlow <= whigh,
+ *            none when wlow > whigh. */
+int zc_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                     uint64_t seed, int symmetrize, int64_t wlow, int64_t whigh,
+                     int32_t placement, int32_t device, zc_graph **out);
+int zc_generate_uniform(uint64_t num_vertices, uint32_t min_degree, uint32_t max_degree,
+                        uint64_t seed, int64_t wlow, int64_t whigh, int32_t placement,
+                        int32_t device, zc_graph **out);
+
+/* Host-link probe: pinned cudaMemcpy H2D GB/s and a zero-copy streaming
+ * read kernel GB/s over `bytes` of pinned memory (the denominators). */
+int zc_link_probe(int32_t device, uint64_t bytes, int iters, double *memcpy_h2d_gbs,
+                  double *zerocopy_read_gbs, double *hbm_read_gbs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZCGRAPH_H_ */

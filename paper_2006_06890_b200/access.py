@@ -1,0 +1,35 @@
+"""Access strategies (reference access.py:28-37).
+
+The strategy selects which CUDA expansion kernel runs; it never changes the
+results (the reference's strategy-independence contract).
+"""
+from __future__ import annotations
+
+from enum import Enum
+
+WARP_LANES = 32
+LINE_BYTES = 128
+SECTOR_BYTES = 32
+
+
+class AccessStrategy(Enum):
+    NAIVE = "naive"
+    MERGED = "merged"
+    MERGED_ALIGNED = "merged-aligned"
+
+
+_IDS = {"naive": 0, "merged": 1, "merged-aligned": 2}
+
+
+def strategy_id(strategy) -> int:
+    """C-ABI id of a strategy given as our enum, the reference's enum or its name."""
+    name = getattr(strategy, "value", strategy)
+    try:
+        return _IDS[name]
+    except (KeyError, TypeError):
+        raise ValueError(f"unknown strategy {strategy!r}") from None
+
+
+def aligned_start(start_elem: int, elem_bytes: int) -> int:
+    """First element of the 128-byte line holding start_elem (access.py:34-37)."""
+    return start_elem & ~(LINE_BYTES // elem_bytes - 1)

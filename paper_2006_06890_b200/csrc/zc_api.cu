@@ -1,0 +1,637 @@
+// Host graph store + C ABI (include/zcgraph.h).
+//
+// One handle = one CSR graph resident on one GPU:
+//   * edge / weight lists: pinned mapped host memory read zero-copy by the
+//     kernels (EMOGI), or managed memory with
+//     cudaMemAdviseSetReadMostly (the paper's UVM baseline), or
+//     plain HBM (control run);
+//   * offsets and every per-vertex array: HBM, allocated once at create and
+//     reused by every traversal (no allocation on the run path).
+// The traversal drivers restate traversal.py:98-179 as a host loop over
+// levels: expand (zc_kernels.cu) -> compact -> read two counters.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/zcgraph.h"
+#include "zc_graph.cuh"
+#include "zc_internal.cuh"
+
+namespace zc {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+// Run fn(lo, hi) over [0, n) on all host cores.
+template <typename F>
+static void parallel_for(uint64_t n, F fn) {
+  unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+  if (n < (1u << 16)) nt = 1;
+  if (nt == 1) {
+    fn(uint64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const uint64_t chunk = (n + nt - 1) / nt;
+  for (unsigned t = 0; t < nt; ++t) {
+    const uint64_t lo = std::min(n, t * chunk), hi = std::min(n, lo + chunk);
+    if (lo < hi) th.emplace_back(fn, lo, hi);
+  }
+  for (auto& x : th) x.join();
+}
+
+// Copy n elements of width sw from src into dst of width dw.
+static void convert_copy(void* dst, uint32_t dw, const void* src, uint32_t sw, uint64_t n) {
+  parallel_for(n, [&](uint64_t lo, uint64_t hi) {
+    if (dw == sw) {
+      memcpy(static_cast<char*>(dst) + lo * dw, static_cast<const char*>(src) + lo * sw,
+             (hi - lo) * dw);
+      return;
+    }
+    for (uint64_t i = lo; i < hi; ++i) {
+      uint64_t x = sw == 8 ? static_cast<const uint64_t*>(src)[i]
+                           : static_cast<const uint32_t*>(src)[i];
+      if (dw == 8) static_cast<uint64_t*>(dst)[i] = x;
+      else static_cast<uint32_t*>(dst)[i] = static_cast<uint32_t>(x);
+    }
+  });
+}
+
+static double now_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace zc
+
+using namespace zc;
+
+namespace {
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+void zc::free_graph(zc_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  auto free_list = [&](void*& h, bool registered, void*& hbm) {
+    if (h) {
+      if (registered) cudaHostUnregister(h);
+      else if (g->placement == ZC_PLACE_UVM) cudaFree(h);
+      else cudaFreeHost(h);
+    }
+    h = nullptr;
+    if (hbm) cudaFree(hbm);
+    hbm = nullptr;
+  };
+  free_list(g->h_edges, g->edges_registered, g->hbm_edges);
+  free_list(g->h_weights, g->weights_registered, g->hbm_weights);
+  if (g->h_off) cudaFreeHost(g->h_off);
+  cudaFree(g->d_off);
+  cudaFree(g->d_state);
+  cudaFree(g->d_flags);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(g->d_front[i]);
+    cudaFree(g->d_fval[i]);
+  }
+  cudaFree(g->d_tiles);
+  cudaFree(g->d_big);
+  cudaFree(g->d_big_prefix);
+  cudaFree(g->d_ctr);
+  if (g->h_ctr) cudaFreeHost(g->h_ctr);
+  if (g->h_small) cudaFreeHost(g->h_small);
+  for (auto& e : g->ev)
+    if (e) cudaEventDestroy(e);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+namespace {
+// Host-side invariant check (csr.py:80-105) on the caller's arrays.
+int validate_desc(const zc_graph_desc* d, bool* negative_weight) {
+  const uint64_t nv = d->num_vertices, ne = d->num_edges;
+  if (d->edge_elem_bytes != 4 && d->edge_elem_bytes != 8) {
+    set_error("edge_elem_bytes must be 4 or 8, got " + std::to_string(d->edge_elem_bytes));
+    return ZC_EINVAL;
+  }
+  if (d->weight_elem_bytes != 4 && d->weight_elem_bytes != 8) {
+    set_error("weight_elem_bytes must be 4 or 8, got " + std::to_string(d->weight_elem_bytes));
+    return ZC_EINVAL;
+  }
+  if (d->src_edge_bytes != 4 && d->src_edge_bytes != 8) {
+    set_error("src_edge_bytes must be 4 or 8");
+    return ZC_EINVAL;
+  }
+  if (d->weights && d->src_weight_bytes != 4 && d->src_weight_bytes != 8) {
+    set_error("src_weight_bytes must be 4 or 8");
+    return ZC_EINVAL;
+  }
+  if (nv >= 0xffffffffull) {
+    set_error("device path supports fewer than 2^32-1 vertices");
+    return ZC_EINVAL;
+  }
+  if (!d->offsets || (ne && !d->edges)) {
+    set_error("offsets / edges must not be NULL");
+    return ZC_EINVAL;
+  }
+  if (d->placement < ZC_PLACE_ZEROCOPY || d->placement > ZC_PLACE_HBM) {
+    set_error("unknown placement");
+    return ZC_EINVAL;
+  }
+  *negative_weight = false;
+  if (d->flags & ZC_F_NO_VALIDATE) return ZC_OK;
+  const int64_t* off = d->offsets;
+  if (off[0] != 0) {
+    set_error("offsets[0] must be 0");
+    return ZC_EINVAL;
+  }
+  if (static_cast<uint64_t>(off[nv]) != ne) {
+    set_error("offsets[-1]=" + std::to_string(off[nv]) + " does not match num_edges=" +
+              std::to_string(ne));
+    return ZC_EINVAL;
+  }
+  std::atomic<int> bad_off{0}, bad_edge{0}, neg_w{0}, big_w{0};
+  parallel_for(nv, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t v = lo; v < hi; ++v)
+      if (off[v + 1] < off[v]) {
+        bad_off = 1;
+        return;
+      }
+  });
+  if (bad_off) {
+    set_error("offsets must be non-decreasing");
+    return ZC_EINVAL;
+  }
+  parallel_for(ne, [&](uint64_t lo, uint64_t hi) {
+    int b = 0;
+    if (d->src_edge_bytes == 8) {
+      const int64_t* e = static_cast<const int64_t*>(d->edges);
+      for (uint64_t i = lo; i < hi; ++i) b |= (e[i] < 0) | (static_cast<uint64_t>(e[i]) >= nv);
+    } else {
+      const uint32_t* e = static_cast<const uint32_t*>(d->edges);
+      for (uint64_t i = lo; i < hi; ++i) b |= (e[i] >= nv);
+    }
+    if (b) bad_edge = 1;
+    if (d->weights) {
+      int n = 0, big = 0;
+      if (d->src_weight_bytes == 8) {
+        const int64_t* w = static_cast<const int64_t*>(d->weights);
+        for (uint64_t i = lo; i < hi; ++i) {
+          n |= w[i] < 0;
+          big |= (d->weight_elem_bytes == 4) & (w[i] > 0xffffffffll);
+        }
+      }
+      if (n) neg_w = 1;
+      if (big) big_w = 1;
+    }
+  });
+  if (bad_edge) {
+    set_error("edge destination out of range");
+    return ZC_EINVAL;
+  }
+  if (big_w) {
+    set_error("weight does not fit the 4-byte weight element width");
+    return ZC_EINVAL;
+  }
+  *negative_weight = neg_w != 0;
+  return ZC_OK;
+}
+
+// Place one list (edges or weights) according to the handle's placement.
+int place_list(zc_graph* g, const void* src, uint32_t sw, uint32_t dw, uint64_t n, void** h,
+               bool* registered, const void** dptr, void** hbm) {
+  const size_t bytes = std::max<size_t>(n * dw, kLineBytes);
+  *registered = false;
+  if (g->placement == ZC_PLACE_ZEROCOPY && (g->flags & ZC_F_REGISTER)) {
+    if (sw != dw || (reinterpret_cast<uintptr_t>(src) % kLineBytes)) {
+      set_error("ZC_F_REGISTER needs 128-byte aligned lists already at the element width");
+      return ZC_EINVAL;
+    }
+    void* p = const_cast<void*>(src);
+    cudaError_t e = cudaHostRegister(p, n * dw, cudaHostRegisterMapped | cudaHostRegisterReadOnly);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      ZC_CUDA_TRY(cudaHostRegister(p, n * dw, cudaHostRegisterMapped));
+    }
+    *h = p;
+    *registered = true;
+    void* d = nullptr;
+    ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, p, 0));
+    *dptr = d;
+    return ZC_OK;
+  }
+  if (g->placement == ZC_PLACE_UVM) {
+    void* p = nullptr;
+    ZC_CUDA_TRY(cudaMallocManaged(&p, bytes, cudaMemAttachGlobal));
+    *h = p;
+    if (src && n) convert_copy(p, dw, src, sw, n);
+    ZC_CUDA_TRY(cudaMemAdvise(p, bytes, cudaMemAdviseSetReadMostly, g->device));
+    *dptr = p;
+    return ZC_OK;
+  }
+  // pinned mapped host buffer (zero-copy list, or the host shadow of HBM)
+  void* p = nullptr;
+  ZC_CUDA_TRY(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  *h = p;
+  if (src && n) convert_copy(p, dw, src, sw, n);
+  if (g->placement == ZC_PLACE_HBM) {
+    ZC_CUDA_TRY(cudaMalloc(hbm, bytes));
+    ZC_CUDA_TRY(cudaMemcpy(*hbm, p, n * dw, cudaMemcpyHostToDevice));
+    *dptr = *hbm;
+  } else {
+    void* d = nullptr;
+    ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, p, 0));
+    *dptr = d;
+  }
+  return ZC_OK;
+}
+
+}  // namespace
+
+int zc::alloc_state(zc_graph* g) {
+  const uint64_t nv = g->nv;
+  const uint64_t n1 = std::max<uint64_t>(nv, 1);
+  g->ntiles = std::max<uint64_t>((nv + kTileVerts - 1) / kTileVerts, 1);
+  g->vpad = g->ntiles * kTileVerts;
+  ZC_CUDA_TRY(cudaMalloc(&g->d_off, (nv + 1) * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMemcpy(g->d_off, g->h_off, (nv + 1) * sizeof(uint64_t),
+                         cudaMemcpyHostToDevice));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_state, n1 * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_flags, g->vpad));
+  ZC_CUDA_TRY(cudaMemset(g->d_flags, 0, g->vpad));
+  for (int i = 0; i < 2; ++i) {
+    ZC_CUDA_TRY(cudaMalloc(&g->d_front[i], n1 * sizeof(uint32_t)));
+    ZC_CUDA_TRY(cudaMalloc(&g->d_fval[i], n1 * sizeof(uint64_t)));
+  }
+  ZC_CUDA_TRY(cudaMalloc(&g->d_tiles, g->ntiles * sizeof(uint32_t)));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_big, n1 * sizeof(uint32_t)));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_big_prefix, (n1 + 1) * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_ctr, kCtrCount * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaHostAlloc(&g->h_ctr, kCtrCount * sizeof(uint64_t), cudaHostAllocDefault));
+  ZC_CUDA_TRY(cudaHostAlloc(&g->h_small, 4 * sizeof(uint64_t), cudaHostAllocDefault));
+  ZC_CUDA_TRY(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  for (auto& e : g->ev) ZC_CUDA_TRY(cudaEventCreate(&e));
+  cudaDeviceProp prop;
+  ZC_CUDA_TRY(cudaGetDeviceProperties(&prop, g->device));
+  g->num_sms = prop.multiProcessorCount;
+  return ZC_OK;
+}
+
+int zc::finish_create(zc_graph* g) {
+  if (g->placement == ZC_PLACE_UVM && (g->flags & ZC_F_UVM_PREFETCH) && g->ne) {
+    ZC_CUDA_TRY(cudaMemPrefetchAsync(g->h_edges, g->ne * g->eb, g->device, g->stream));
+    if (g->h_weights)
+      ZC_CUDA_TRY(cudaMemPrefetchAsync(g->h_weights, g->ne * g->wb, g->device, g->stream));
+  }
+  ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  return ZC_OK;
+}
+
+int zc::adopt_device_list(zc_graph* g, void* d_src, uint32_t w, uint64_t n, void** h,
+                          const void** dptr, void** hbm) {
+  const size_t bytes = std::max<size_t>(n * w, kLineBytes);
+  if (g->placement == ZC_PLACE_UVM) {
+    void* p = nullptr;
+    ZC_CUDA_TRY(cudaMallocManaged(&p, bytes, cudaMemAttachGlobal));
+    *h = p;
+    ZC_CUDA_TRY(cudaMemcpy(p, d_src, n * w, cudaMemcpyDefault));
+    ZC_CUDA_TRY(cudaFree(d_src));
+    // start cold: pages resident on the host, read-mostly on the GPU
+    ZC_CUDA_TRY(cudaMemPrefetchAsync(p, bytes, cudaCpuDeviceId, 0));
+    ZC_CUDA_TRY(cudaDeviceSynchronize());
+    ZC_CUDA_TRY(cudaMemAdvise(p, bytes, cudaMemAdviseSetReadMostly, g->device));
+    *dptr = p;
+    return ZC_OK;
+  }
+  void* p = nullptr;
+  ZC_CUDA_TRY(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  *h = p;
+  ZC_CUDA_TRY(cudaMemcpy(p, d_src, n * w, cudaMemcpyDeviceToHost));
+  if (g->placement == ZC_PLACE_HBM) {
+    *hbm = d_src;
+    *dptr = d_src;
+  } else {
+    ZC_CUDA_TRY(cudaFree(d_src));
+    void* d = nullptr;
+    ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, p, 0));
+    *dptr = d;
+  }
+  return ZC_OK;
+}
+
+namespace {
+
+// One traversal (traversal.py:98-179) on the handle.
+int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stats* stats) {
+  const double t0 = now_ms();
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (strategy < kNaive || strategy > kMergedAligned) {
+    set_error("unknown access strategy " + std::to_string(strategy));
+    return ZC_EINVAL;
+  }
+  if (algo != kCc && src >= g->nv) {  // traversal.py:93-95
+    set_error("source " + std::to_string(src) + " out of range for " + std::to_string(g->nv) +
+              " vertices");
+    return ZC_EINVAL;
+  }
+  if (algo == kSssp) {  // traversal.py:133-136
+    if (!g->has_weights) {
+      set_error("sssp requires edge weights");
+      return ZC_EINVAL;
+    }
+    if (g->ne && g->negative_weight) {
+      set_error("sssp requires non-negative weights");
+      return ZC_EINVAL;
+    }
+  }
+  if (algo == kCc && (g->flags & ZC_F_DIRECTED)) {  // traversal.py:163-165
+    set_error("connected components require an undirected graph "
+              "(load with directed=False or symmetrize first)");
+    return ZC_EINVAL;
+  }
+  if (!out && g->nv) {
+    set_error("null output buffer");
+    return ZC_EINVAL;
+  }
+  DeviceGuard dg(g->device);
+  cudaStream_t st = g->stream;
+  uint64_t launches = 0;
+  g->log_trav.clear();
+  g->log_front.clear();
+  g->log_hist.clear();
+  const bool model = (g->options & ZC_OPT_TRAFFIC_MODEL) != 0;
+
+  ZC_CUDA_TRY(cudaMemsetAsync(g->d_flags, 0, g->vpad, st));
+  ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr, 0, kCtrCount * sizeof(uint64_t), st));
+  ZC_CUDA_TRY(launch_init(algo, g->d_state, g->nv, g->d_front[0], g->d_fval[0], st, &launches));
+  uint64_t n = 0, trav = 0;
+  uint64_t h2d = 0;
+  if (algo == kCc) {
+    n = g->nv;
+    trav = g->ne;
+  } else {
+    // frontier = [src], value 0, state[src] = 0
+    g->h_small[0] = src;
+    g->h_small[1] = 0;
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->d_front[0], &g->h_small[0], sizeof(uint32_t),
+                                cudaMemcpyHostToDevice, st));
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->d_fval[0], &g->h_small[1], sizeof(uint64_t),
+                                cudaMemcpyHostToDevice, st));
+    const size_t sb = algo == kSssp ? 8 : 4;
+    ZC_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(g->d_state) + src * sb, &g->h_small[1], sb,
+                                cudaMemcpyHostToDevice, st));
+    h2d += 4 + 8 + sb;
+    n = 1;
+    trav = g->h_off[src + 1] - g->h_off[src];
+  }
+  ZC_CUDA_TRY(cudaEventRecord(g->ev[0], st));
+  int cur = 0;
+  uint64_t iters = 0, total_trav = 0, max_front = 0;
+  while (n > 0) {
+    ++iters;
+    g->log_trav.push_back(trav);
+    g->log_front.push_back(n);
+    total_trav += trav;
+    max_front = std::max(max_front, n);
+    if (model)
+      ZC_CUDA_TRY(launch_traffic_model(strategy, g->eb, g->wb, algo == kSssp, g->d_front[cur], n,
+                                       g->d_off, g->d_ctr, g->num_sms, st, &launches));
+    ExpandArgs a;
+    a.front = g->d_front[cur];
+    a.fval = g->d_fval[cur];
+    a.n = n;
+    a.off = g->d_off;
+    a.edges = g->d_edges;
+    a.weights = g->d_weights;
+    a.state = g->d_state;
+    a.flags = g->d_flags;
+    a.iter = static_cast<uint32_t>(iters);
+    a.big = g->d_big;
+    a.big_prefix = g->d_big_prefix;
+    a.ctr = g->d_ctr;
+    ZC_CUDA_TRY(launch_expand(strategy, algo, g->eb, g->wb, a, g->num_sms, st, &launches));
+    CompactArgs c;
+    c.flags = g->d_flags;
+    c.nv = g->nv;
+    c.ntiles = g->ntiles;
+    c.tiles = g->d_tiles;
+    c.front_out = g->d_front[cur ^ 1];
+    c.fval_out = g->d_fval[cur ^ 1];
+    c.off = g->d_off;
+    c.state = g->d_state;
+    c.ctr = g->d_ctr;
+    ZC_CUDA_TRY(launch_compact(algo, c, st, &launches));
+    const size_t nctr = model ? kCtrCount : 2;
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, nctr * sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, st));
+    if (model)
+      ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr + kCtrHist, 0, 8 * sizeof(uint64_t), st));
+    ZC_CUDA_TRY(cudaStreamSynchronize(st));
+    n = g->h_ctr[kCtrNext];
+    trav = g->h_ctr[kCtrTrav];
+    if (model) g->log_hist.insert(g->log_hist.end(), g->h_ctr + kCtrHist, g->h_ctr + kCtrHist + 8);
+    cur ^= 1;
+  }
+  ZC_CUDA_TRY(cudaEventRecord(g->ev[1], st));
+  // widen into an int64 staging buffer (free fval slot) and download
+  int64_t* d_out = reinterpret_cast<int64_t*>(g->d_fval[0]);
+  ZC_CUDA_TRY(launch_widen(algo, g->d_state, g->nv, d_out, st, &launches));
+  if (g->nv)
+    ZC_CUDA_TRY(cudaMemcpyAsync(out, d_out, g->nv * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
+  ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    stats->iterations = iters;
+    stats->total_traversed_edges = total_trav;
+    stats->max_frontier = max_front;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]);
+    stats->kernel_ms = ms;
+    cudaEventElapsedTime(&ms, g->ev[1], g->ev[2]);
+    stats->d2h_ms = ms;
+    stats->h2d_bytes = h2d;
+    stats->d2h_bytes = g->nv * sizeof(int64_t) + iters * (model ? kCtrCount : 2) * sizeof(uint64_t);
+    stats->launches = launches;
+    stats->total_ms = now_ms() - t0;
+  }
+  return ZC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* zc_last_error(void) { return g_err.c_str(); }
+int zc_abi_version(void) { return ZC_ABI_VERSION; }
+
+int zc_device_count(int* count) {
+  ZC_CUDA_TRY(cudaGetDeviceCount(count));
+  return ZC_OK;
+}
+
+int zc_graph_create(const zc_graph_desc* d, zc_graph** out) {
+  if (!d || !out) {
+    set_error("null argument");
+    return ZC_ESTATE;
+  }
+  *out = nullptr;
+  bool neg = false;
+  int rc = validate_desc(d, &neg);
+  if (rc) return rc;
+  int ndev = 0;
+  ZC_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (d->device < 0 || d->device >= ndev) {
+    set_error("device " + std::to_string(d->device) + " not present (" + std::to_string(ndev) +
+              " visible)");
+    return ZC_EINVAL;
+  }
+  DeviceGuard dg(d->device);
+  zc_graph* g = new zc_graph();
+  g->nv = d->num_vertices;
+  g->ne = d->num_edges;
+  g->eb = d->edge_elem_bytes;
+  g->wb = d->weight_elem_bytes;
+  g->placement = d->placement;
+  g->device = d->device;
+  g->flags = d->flags;
+  g->has_weights = d->weights != nullptr;
+  g->negative_weight = neg;
+  auto fail = [&](int code) {
+    free_graph(g);
+    return code;
+  };
+  if (cudaHostAlloc(&g->h_off, (g->nv + 1) * sizeof(int64_t), cudaHostAllocDefault) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    set_error("cannot allocate pinned offsets");
+    return fail(ZC_ENOMEM);
+  }
+  convert_copy(g->h_off, 8, d->offsets, 8, g->nv + 1);
+  rc = place_list(g, d->edges, d->src_edge_bytes, g->eb, g->ne, &g->h_edges,
+                  &g->edges_registered, &g->d_edges, &g->hbm_edges);
+  if (rc) return fail(rc);
+  if (g->has_weights) {
+    rc = place_list(g, d->weights, d->src_weight_bytes, g->wb, g->ne, &g->h_weights,
+                    &g->weights_registered, &g->d_weights, &g->hbm_weights);
+    if (rc) return fail(rc);
+  }
+  rc = alloc_state(g);
+  if (rc) return fail(rc);
+  rc = finish_create(g);
+  if (rc) return fail(rc);
+  *out = g;
+  return ZC_OK;
+}
+
+void zc_graph_destroy(zc_graph* g) { free_graph(g); }
+
+int zc_graph_host_lists(zc_graph* g, void** edges, void** weights, const int64_t** offsets) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (edges) *edges = g->h_edges;
+  if (weights) *weights = g->h_weights;
+  if (offsets) *offsets = g->h_off;
+  return ZC_OK;
+}
+
+int zc_graph_info(const zc_graph* g, uint64_t* nv, uint64_t* ne, uint32_t* eb, uint32_t* wb,
+                  int32_t* placement, uint32_t* flags) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (nv) *nv = g->nv;
+  if (ne) *ne = g->ne;
+  if (eb) *eb = g->eb;
+  if (wb) *wb = g->has_weights ? g->wb : 0;
+  if (placement) *placement = g->placement;
+  if (flags) *flags = g->flags;
+  return ZC_OK;
+}
+
+int zc_bfs(zc_graph* g, uint64_t source, int strategy, int64_t* out, zc_stats* stats) {
+  return run(g, kBfs, source, strategy, out, stats);
+}
+int zc_sssp(zc_graph* g, uint64_t source, int strategy, int64_t* out, zc_stats* stats) {
+  return run(g, kSssp, source, strategy, out, stats);
+}
+int zc_cc(zc_graph* g, int strategy, int64_t* out, zc_stats* stats) {
+  return run(g, kCc, 0, strategy, out, stats);
+}
+
+int zc_run_log(const zc_graph* g, uint64_t* trav, uint64_t* front, uint64_t cap) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  const uint64_t n = std::min<uint64_t>(cap, g->log_trav.size());
+  if (trav) std::copy(g->log_trav.begin(), g->log_trav.begin() + n, trav);
+  if (front) std::copy(g->log_front.begin(), g->log_front.begin() + n, front);
+  return ZC_OK;
+}
+
+int zc_set_options(zc_graph* g, uint32_t options) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (options & ~ZC_OPT_TRAFFIC_MODEL) {
+    set_error("unknown option bits");
+    return ZC_EINVAL;
+  }
+  g->options = options;
+  return ZC_OK;
+}
+
+int zc_run_traffic(const zc_graph* g, uint64_t* hist, uint64_t cap) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (!(g->options & ZC_OPT_TRAFFIC_MODEL)) {
+    set_error("traffic model not enabled (zc_set_options)");
+    return ZC_ESTATE;
+  }
+  const uint64_t n = std::min<uint64_t>(cap, g->log_hist.size() / 8);
+  if (hist) std::copy(g->log_hist.begin(), g->log_hist.begin() + 8 * n, hist);
+  return ZC_OK;
+}
+
+void* zc_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("cudaHostAlloc failed");
+    return nullptr;
+  }
+  return p;
+}
+
+void zc_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,524 @@
+// Native synthetic graph generators.
+//
+// The reference generators (csr.py:248-317) are numpy loops that need ~20 s
+// at 2^20 vertices and cannot reach scale 27; these run on the GPU, write the
+// CSR straight into a handle and are deterministic in (parameters, seed)
+// through a counter-based hash (no sequential RNG state).
+//
+// R-MAT / Kronecker (GAP "kron", Graph500 parameters a,b,c = .57,.19,.19):
+// the source bit of each of the `scale` levels is Bernoulli(c+d) and,
+// given it, the destination bit is Bernoulli(b/(a+b)) or Bernoulli(d/(c+d)).
+// Pass 1 draws every arc's source and counts out-degrees, pass 2 scans them
+// into offsets, pass 3 draws each list's destinations in CSR order -- the
+// arc multiset has exactly the R-MAT distribution and no sort is needed.
+// Vertex ids are scrambled by a keyed Feistel bijection (GAP permutes ids).
+// Duplicates and self loops are kept, as the reference does.
+// Symmetrize appends the reverse arcs (csr.py:350-359 semantics, no dedup);
+// lists are then sorted ascending like the reference's lexsort.
+//
+// Uniform (csr.py:270-282 semantics): out-degree uniform in
+// [min_degree, max_degree], destinations uniform with no duplicate inside a
+// list (rejection, as csr.py:248-267).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+
+#include "zc_graph.cuh"
+#include "zc_internal.cuh"
+
+namespace zc {
+namespace {
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t hash3(uint64_t seed, uint64_t stream, uint64_t i) {
+  return mix64(mix64(seed ^ (stream * 0xd1b54a32d192ed03ull)) + i);
+}
+
+// Keyed Feistel bijection on [0, 2^bits) with cycle walking.
+struct Feistel {
+  uint32_t half;  // bits per half (domain 2^(2*half) >= 2^bits)
+  uint32_t bits;
+  uint64_t key;
+  __device__ __forceinline__ uint64_t f(uint64_t x, int r) const {
+    return hash3(key, 100 + r, x) & ((1ull << half) - 1);
+  }
+  __device__ __forceinline__ uint64_t round_fwd(uint64_t x) const {
+    uint64_t l = x >> half, r = x & ((1ull << half) - 1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t nl = r, nr = l ^ f(r, k);
+      l = nl;
+      r = nr;
+    }
+    return (l << half) | r;
+  }
+  __device__ __forceinline__ uint64_t round_inv(uint64_t x) const {
+    uint64_t l = x >> half, r = x & ((1ull << half) - 1);
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
+      const uint64_t pr = l, pl = r ^ f(l, k);
+      l = pl;
+      r = pr;
+    }
+    return (l << half) | r;
+  }
+  __device__ __forceinline__ uint64_t fwd(uint64_t x) const {
+    do x = round_fwd(x); while (x >> bits);
+    return x;
+  }
+  __device__ __forceinline__ uint64_t inv(uint64_t x) const {
+    do x = round_inv(x); while (x >> bits);
+    return x;
+  }
+};
+
+struct RmatParams {
+  uint32_t scale;
+  uint32_t thr_src;   // P(src bit = 1) = c + d, 16-bit fixed point
+  uint32_t thr_dst0;  // P(dst bit = 1 | src bit 0) = b / (a + b)
+  uint32_t thr_dst1;  // P(dst bit = 1 | src bit 1) = d / (c + d)
+  uint64_t seed;
+  Feistel perm;
+};
+
+__device__ __forceinline__ uint64_t rmat_src(const RmatParams& p, uint64_t arc) {
+  uint64_t s = 0, h = 0;
+  for (uint32_t l = 0; l < p.scale; ++l) {
+    if ((l & 3) == 0) h = hash3(p.seed, 1 + (l >> 2), arc);
+    const uint32_t u = static_cast<uint32_t>(h >> ((l & 3) * 16)) & 0xffffu;
+    s |= static_cast<uint64_t>(u < p.thr_src) << l;
+  }
+  return s;
+}
+
+__device__ __forceinline__ uint64_t rmat_dst(const RmatParams& p, uint64_t src_old,
+                                             uint64_t key) {
+  uint64_t d = 0, h = 0;
+  for (uint32_t l = 0; l < p.scale; ++l) {
+    if ((l & 3) == 0) h = hash3(p.seed, 32 + (l >> 2), key);
+    const uint32_t u = static_cast<uint32_t>(h >> ((l & 3) * 16)) & 0xffffu;
+    const uint32_t thr = (src_old >> l) & 1 ? p.thr_dst1 : p.thr_dst0;
+    d |= static_cast<uint64_t>(u < thr) << l;
+  }
+  return d;
+}
+
+__global__ void k_rmat_count(RmatParams p, uint64_t narcs, uint32_t* deg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < narcs;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = p.perm.fwd(rmat_src(p, i));
+    atomicAdd(deg + s, 1u);
+  }
+}
+
+// Warp per (permuted) vertex: its list in CSR order, lanes strided over k.
+template <typename ET>
+__global__ void k_rmat_fill(RmatParams p, uint64_t nv, const uint64_t* off, ET* edges) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t v = gw; v < nv; v += nw) {
+    const uint64_t s = off[v], e = off[v + 1];
+    if (s == e) continue;
+    const uint64_t src_old = p.perm.inv(v);
+    for (uint64_t k = s + lane; k < e; k += 32) {
+      const uint64_t d_old = rmat_dst(p, src_old, (v << 24) ^ (k - s) ^ (k << 40));
+      edges[k] = static_cast<ET>(p.perm.fwd(d_old));
+    }
+  }
+}
+
+// Symmetrize: sym list of x = out-list of x followed by the sources of its
+// in-arcs, then sorted.  cursor[x] starts at out_deg[x].
+template <typename ET>
+__global__ void k_sym_copy_out(uint64_t nv, const uint64_t* off, const ET* edges,
+                               const uint64_t* soff, ET* sedges) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t v = gw; v < nv; v += nw) {
+    const uint64_t s = off[v], e = off[v + 1], t = soff[v];
+    for (uint64_t k = s + lane; k < e; k += 32) sedges[t + (k - s)] = edges[k];
+  }
+}
+
+template <typename ET>
+__global__ void k_sym_scatter_in(uint64_t nv, const uint64_t* off, const ET* edges,
+                                 const uint64_t* soff, uint32_t* cursor, ET* sedges) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t v = gw; v < nv; v += nw) {
+    const uint64_t s = off[v], e = off[v + 1];
+    for (uint64_t k = s + lane; k < e; k += 32) {
+      const uint64_t d = edges[k];
+      const uint32_t pos = atomicAdd(cursor + d, 1u);
+      sedges[soff[d] + pos] = static_cast<ET>(v);
+    }
+  }
+}
+
+template <typename ET>
+__global__ void k_count_in(uint64_t ne, const ET* edges, uint32_t* deg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(deg + edges[i], 1u);
+}
+
+__global__ void k_deg_from_off(uint64_t nv, const uint64_t* off, uint32_t* deg) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x)
+    deg[v] = static_cast<uint32_t>(off[v + 1] - off[v]);
+}
+
+// Sort every list ascending.  Lists up to 32 elements: one warp-level
+// odd-even pass per list in registers; up to kSortSmem elements: one CTA with
+// shared-memory bitonic sort; longer lists are handled by k_sort_long.
+constexpr int kSortSmem = 4096;
+
+template <typename ET>
+__global__ void k_sort_short(uint64_t nv, const uint64_t* off, ET* edges) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t v = gw; v < nv; v += nw) {
+    const uint64_t s = off[v], e = off[v + 1], n = e - s;
+    if (n < 2 || n > 32) continue;
+    ET x = lane < n ? edges[s + lane] : static_cast<ET>(~0ull);
+    // bitonic sort across the 32 lanes
+    for (int k = 2; k <= 32; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const ET y = __shfl_xor_sync(0xffffffffu, x, j);
+        const bool up = (lane & k) == 0;
+        const bool lower = (lane & j) == 0;
+        const ET lo = x < y ? x : y, hi = x < y ? y : x;
+        x = (lower == up) ? lo : hi;
+      }
+    }
+    if (lane < n) edges[s + lane] = x;
+  }
+}
+
+template <typename ET>
+__global__ void __launch_bounds__(1024) k_sort_mid(uint64_t nv, const uint64_t* off, ET* edges) {
+  __shared__ ET sh[kSortSmem];
+  for (uint64_t v = blockIdx.x; v < nv; v += gridDim.x) {
+    const uint64_t s = off[v], e = off[v + 1], n = e - s;
+    if (n <= 32 || n > kSortSmem) continue;
+    uint32_t m = 64;
+    while (m < n) m <<= 1;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)
+      sh[i] = i < n ? edges[s + i] : static_cast<ET>(~0ull);
+    __syncthreads();
+    for (uint32_t k = 2; k <= m; k <<= 1) {
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+          const uint32_t p = i ^ j;
+          if (p > i) {
+            const ET a = sh[i], b = sh[p];
+            const bool up = (i & k) == 0;
+            if ((a > b) == up) {
+              sh[i] = b;
+              sh[p] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) edges[s + i] = sh[i];
+    __syncthreads();
+  }
+}
+
+// Long lists (> kSortSmem): counting sort by value through a per-list
+// histogram would need V-sized scratch; instead sort in place with a
+// global-memory bitonic network per list (rare: hubs only).
+template <typename ET>
+__global__ void k_sort_long_step(ET* data, uint64_t n, uint64_t m, uint64_t j, uint64_t k) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = i ^ j;
+    if (p > i) {
+      const ET a = i < n ? data[i] : static_cast<ET>(~0ull);
+      const ET b = p < n ? data[p] : static_cast<ET>(~0ull);
+      const bool up = (i & k) == 0;
+      if ((a > b) == up) {
+        if (i < n) data[i] = b;
+        if (p < n) data[p] = a;
+      }
+    }
+  }
+}
+
+template <typename ET>
+__global__ void k_uniform_fill(uint64_t nv, uint64_t seed, const uint64_t* off, ET* edges) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = off[v], e = off[v + 1];
+    uint64_t attempt = 0;
+    for (uint64_t k = s; k < e; ++k) {
+      uint64_t d;
+      bool dup;
+      do {
+        d = hash3(seed, 2, (k << 8) ^ attempt++) % nv;
+        dup = false;
+        for (uint64_t t = s; t < k; ++t) dup |= (static_cast<uint64_t>(edges[t]) == d);
+      } while (dup);
+      edges[k] = static_cast<ET>(d);
+    }
+  }
+}
+
+__global__ void k_uniform_deg(uint64_t nv, uint64_t seed, uint32_t lo, uint32_t hi, uint32_t* deg) {
+  const uint64_t span = static_cast<uint64_t>(hi) - lo + 1;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x)
+    deg[v] = lo + static_cast<uint32_t>(hash3(seed, 1, v) % span);
+}
+
+__global__ void k_weights(uint64_t ne, uint64_t seed, int64_t lo, int64_t hi, uint32_t* w) {
+  const uint64_t span = static_cast<uint64_t>(hi - lo) + 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    w[i] = static_cast<uint32_t>(lo + static_cast<int64_t>(hash3(seed, 3, i) % span));
+}
+
+constexpr int kGenGrid = 148 * 16;
+
+// deg (u32, device) -> offsets into g->h_off (pinned) and g's device offsets.
+int offsets_from_degrees(zc_graph* g, uint32_t* d_deg, uint64_t nv, uint64_t** d_off_out) {
+  uint64_t* d_off = nullptr;
+  ZC_CUDA_TRY(cudaMalloc(&d_off, (nv + 1) * sizeof(uint64_t)));
+  const size_t tb = scan_tmp_bytes(nv);
+  void* tmp = nullptr;
+  ZC_CUDA_TRY(cudaMalloc(&tmp, tb));
+  ZC_CUDA_TRY(scan_u32_to_u64(d_deg, d_off, nv, tmp, tb, 0));
+  ZC_CUDA_TRY(cudaFree(tmp));
+  if (!g->h_off) {
+    if (cudaHostAlloc(&g->h_off, (nv + 1) * sizeof(int64_t), cudaHostAllocDefault) !=
+        cudaSuccess) {
+      set_error("cannot allocate pinned offsets");
+      return ZC_ENOMEM;
+    }
+  }
+  ZC_CUDA_TRY(cudaMemcpy(g->h_off, d_off, (nv + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  *d_off_out = d_off;
+  return ZC_OK;
+}
+
+template <typename ET>
+int sort_lists(uint64_t nv, const uint64_t* d_off, const int64_t* h_off, ET* edges) {
+  k_sort_short<ET><<<kGenGrid, 256>>>(nv, d_off, edges);
+  k_sort_mid<ET><<<kGenGrid, 1024>>>(nv, d_off, edges);
+  ZC_CUDA_TRY(cudaGetLastError());
+  for (uint64_t v = 0; v < nv; ++v) {
+    const uint64_t n = h_off[v + 1] - h_off[v];
+    if (n <= static_cast<uint64_t>(kSortSmem)) continue;
+    uint64_t m = 1;
+    while (m < n) m <<= 1;
+    ET* data = edges + h_off[v];
+    for (uint64_t k = 2; k <= m; k <<= 1)
+      for (uint64_t j = k >> 1; j > 0; j >>= 1)
+        k_sort_long_step<ET><<<std::min<uint64_t>((m + 255) / 256, kGenGrid), 256>>>(data, n, m,
+                                                                                       j, k);
+  }
+  ZC_CUDA_TRY(cudaGetLastError());
+  return ZC_OK;
+}
+
+zc_graph* new_handle(int32_t placement, int32_t device, uint32_t flags) {
+  zc_graph* g = new zc_graph();
+  g->placement = placement;
+  g->device = device;
+  g->flags = flags;
+  g->eb = 4;
+  g->wb = 4;
+  return g;
+}
+
+int attach_weights(zc_graph* g, uint64_t seed, int64_t wlow, int64_t whigh) {
+  if (wlow > whigh) return ZC_OK;
+  uint32_t* d_w = nullptr;
+  ZC_CUDA_TRY(cudaMalloc(&d_w, std::max<uint64_t>(g->ne, 32) * sizeof(uint32_t)));
+  if (g->ne) k_weights<<<kGenGrid, 256>>>(g->ne, seed, wlow, whigh, d_w);
+  ZC_CUDA_TRY(cudaGetLastError());
+  g->has_weights = true;
+  return adopt_device_list(g, d_w, 4, g->ne, &g->h_weights, &g->d_weights, &g->hbm_weights);
+}
+
+int check_common(int32_t placement, int32_t device, int64_t wlow, int64_t whigh) {
+  int ndev = 0;
+  ZC_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) {
+    set_error("device not present");
+    return ZC_EINVAL;
+  }
+  if (placement < ZC_PLACE_ZEROCOPY || placement > ZC_PLACE_HBM) {
+    set_error("unknown placement");
+    return ZC_EINVAL;
+  }
+  if (wlow <= whigh && (wlow < 0 || whigh > 0xffffffffll)) {
+    set_error("weights must lie in [0, 2^32)");
+    return ZC_EINVAL;
+  }
+  return ZC_OK;
+}
+
+int generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uint64_t seed,
+                  int symmetrize, int64_t wlow, int64_t whigh, int32_t placement, int32_t device,
+                  zc_graph** out) {
+  *out = nullptr;
+  int rc = check_common(placement, device, wlow, whigh);
+  if (rc) return rc;
+  const double d = 1.0 - a - b - c;
+  if (scale < 1 || scale > 31 || ef < 1 || a <= 0 || b < 0 || c < 0 || d < 0) {
+    set_error("rmat needs 1 <= scale <= 31, edge_factor >= 1, a > 0, b, c, 1-a-b-c >= 0");
+    return ZC_EINVAL;
+  }
+  cudaSetDevice(device);
+  const uint64_t nv = 1ull << scale;
+  const uint64_t narcs = static_cast<uint64_t>(ef) << scale;
+  if (symmetrize && 2 * narcs / nv > 0xffffffffull) {
+    set_error("degree overflow");
+    return ZC_EINVAL;
+  }
+  RmatParams p;
+  p.scale = scale;
+  p.thr_src = static_cast<uint32_t>((c + d) * 65536.0 + 0.5);
+  p.thr_dst0 = static_cast<uint32_t>(b / (a + b) * 65536.0 + 0.5);
+  p.thr_dst1 = (c + d) > 0 ? static_cast<uint32_t>(d / (c + d) * 65536.0 + 0.5) : 0;
+  p.seed = seed;
+  p.perm.bits = scale;
+  p.perm.half = (scale + 1) / 2;
+  p.perm.key = mix64(seed ^ 0x5eedull);
+
+  zc_graph* g = new_handle(placement, device, symmetrize ? 0u : ZC_F_DIRECTED);
+  auto fail = [&](int code) {
+    free_graph(g);
+    return code;
+  };
+  g->nv = nv;
+  uint32_t* d_deg = nullptr;
+  uint64_t* d_off = nullptr;
+  uint32_t* d_edges = nullptr;
+  if (cudaMalloc(&d_deg, nv * sizeof(uint32_t)) != cudaSuccess) return fail(ZC_ENOMEM);
+  cudaMemset(d_deg, 0, nv * sizeof(uint32_t));
+  k_rmat_count<<<kGenGrid, 256>>>(p, narcs, d_deg);
+  if ((rc = offsets_from_degrees(g, d_deg, nv, &d_off))) return fail(rc);
+  if (cudaMalloc(&d_edges, std::max<uint64_t>(narcs, 32) * sizeof(uint32_t)) != cudaSuccess)
+    return fail(ZC_ENOMEM);
+  k_rmat_fill<uint32_t><<<kGenGrid, 256>>>(p, nv, d_off, d_edges);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    set_error(std::string("rmat fill: ") + cudaGetErrorString(cudaGetLastError()));
+    return fail(ZC_ECUDA);
+  }
+  g->ne = narcs;
+  if (symmetrize) {
+    // symmetric degree = out-degree + in-degree; cursor[x] starts at out-degree
+    uint32_t* d_cursor = nullptr;
+    uint32_t* d_sedges = nullptr;
+    uint64_t* d_soff = nullptr;
+    if (cudaMalloc(&d_cursor, nv * sizeof(uint32_t)) != cudaSuccess) return fail(ZC_ENOMEM);
+    k_deg_from_off<<<kGenGrid, 256>>>(nv, d_off, d_deg);
+    k_count_in<uint32_t><<<kGenGrid, 256>>>(narcs, d_edges, d_deg);
+    if ((rc = offsets_from_degrees(g, d_deg, nv, &d_soff))) return fail(rc);
+    k_deg_from_off<<<kGenGrid, 256>>>(nv, d_off, d_cursor);
+    if (cudaMalloc(&d_sedges, std::max<uint64_t>(2 * narcs, 32) * sizeof(uint32_t)) !=
+        cudaSuccess)
+      return fail(ZC_ENOMEM);
+    k_sym_copy_out<uint32_t><<<kGenGrid, 256>>>(nv, d_off, d_edges, d_soff, d_sedges);
+    k_sym_scatter_in<uint32_t><<<kGenGrid, 256>>>(nv, d_off, d_edges, d_soff, d_cursor, d_sedges);
+    if ((rc = sort_lists<uint32_t>(nv, d_soff, g->h_off, d_sedges))) return fail(rc);
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+      set_error(std::string("symmetrize: ") + cudaGetErrorString(cudaGetLastError()));
+      return fail(ZC_ECUDA);
+    }
+    cudaFree(d_cursor);
+    cudaFree(d_edges);
+    cudaFree(d_off);
+    d_edges = d_sedges;
+    d_off = d_soff;
+    g->ne = 2 * narcs;
+  }
+  cudaFree(d_deg);
+  g->eb = 4;
+  if ((rc = adopt_device_list(g, d_edges, 4, g->ne, &g->h_edges, &g->d_edges, &g->hbm_edges)))
+    return fail(rc);
+  cudaFree(d_off);
+  if ((rc = attach_weights(g, seed ^ 0x77ull, wlow, whigh))) return fail(rc);
+  if ((rc = alloc_state(g))) return fail(rc);
+  if ((rc = finish_create(g))) return fail(rc);
+  *out = g;
+  return ZC_OK;
+}
+
+int generate_uniform(uint64_t nv, uint32_t dmin, uint32_t dmax, uint64_t seed, int64_t wlow,
+                     int64_t whigh, int32_t placement, int32_t device, zc_graph** out) {
+  *out = nullptr;
+  int rc = check_common(placement, device, wlow, whigh);
+  if (rc) return rc;
+  // csr.py:273-274 precondition, plus the native generator's list cap
+  if (!(dmin <= dmax && dmax < nv) || nv >= 0xffffffffull || dmax > 256) {
+    set_error("require 0 <= min_degree <= max_degree < num_vertices, max_degree <= 256");
+    return ZC_EINVAL;
+  }
+  cudaSetDevice(device);
+  zc_graph* g = new_handle(placement, device, ZC_F_DIRECTED);
+  auto fail = [&](int code) {
+    free_graph(g);
+    return code;
+  };
+  g->nv = nv;
+  uint32_t* d_deg = nullptr;
+  uint64_t* d_off = nullptr;
+  uint32_t* d_edges = nullptr;
+  if (cudaMalloc(&d_deg, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)) != cudaSuccess)
+    return fail(ZC_ENOMEM);
+  k_uniform_deg<<<kGenGrid, 256>>>(nv, seed, dmin, dmax, d_deg);
+  if ((rc = offsets_from_degrees(g, d_deg, nv, &d_off))) return fail(rc);
+  g->ne = static_cast<uint64_t>(g->h_off[nv]);
+  if (cudaMalloc(&d_edges, std::max<uint64_t>(g->ne, 32) * sizeof(uint32_t)) != cudaSuccess)
+    return fail(ZC_ENOMEM);
+  k_uniform_fill<uint32_t><<<kGenGrid, 128>>>(nv, seed, d_off, d_edges);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    set_error(std::string("uniform fill: ") + cudaGetErrorString(cudaGetLastError()));
+    return fail(ZC_ECUDA);
+  }
+  cudaFree(d_deg);
+  cudaFree(d_off);
+  if ((rc = adopt_device_list(g, d_edges, 4, g->ne, &g->h_edges, &g->d_edges, &g->hbm_edges)))
+    return fail(rc);
+  if ((rc = attach_weights(g, seed ^ 0x77ull, wlow, whigh))) return fail(rc);
+  if ((rc = alloc_state(g))) return fail(rc);
+  if ((rc = finish_create(g))) return fail(rc);
+  *out = g;
+  return ZC_OK;
+}
+
+}  // namespace
+}  // namespace zc
+
+extern "C" int zc_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b,
+                                double c, uint64_t seed, int symmetrize, int64_t wlow,
+                                int64_t whigh, int32_t placement, int32_t device,
+                                zc_graph** out) {
+  if (!out) return ZC_ESTATE;
+  return zc::generate_rmat(scale, edge_factor, a, b, c, seed, symmetrize, wlow, whigh, placement,
+                           device, out);
+}
+
+extern "C" int zc_generate_uniform(uint64_t num_vertices, uint32_t min_degree, uint32_t max_degree,
+                                   uint64_t seed, int64_t wlow, int64_t whigh, int32_t placement,
+                                   int32_t device, zc_graph** out) {
+  if (!out) return ZC_ESTATE;
+  return zc::generate_uniform(num_vertices, min_degree, max_degree, seed, wlow, whigh, placement,
+                              device, out);
+}

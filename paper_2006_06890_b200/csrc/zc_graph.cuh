@@ -1,0 +1,63 @@
+// Definition of the graph handle shared by the C-ABI (zc_api.cu) and the
+// native generators (zc_gen.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/zcgraph.h"
+#include "zc_internal.cuh"
+
+struct zc_graph {
+  uint64_t nv = 0, ne = 0;
+  uint32_t eb = 4, wb = 4;
+  int32_t placement = ZC_PLACE_ZEROCOPY;
+  int32_t device = 0;
+  uint32_t flags = 0;
+  int num_sms = 148;
+  bool has_weights = false;
+  bool negative_weight = false;
+  // host side
+  int64_t* h_off = nullptr;  // pinned copy of the offsets (V+1)
+  void* h_edges = nullptr;   // pinned / managed / pinned shadow
+  void* h_weights = nullptr;
+  bool edges_registered = false, weights_registered = false;
+  // device-visible lists
+  const void* d_edges = nullptr;
+  const void* d_weights = nullptr;
+  void* hbm_edges = nullptr;
+  void* hbm_weights = nullptr;
+  // HBM state
+  uint64_t* d_off = nullptr;
+  void* d_state = nullptr;
+  uint8_t* d_flags = nullptr;
+  uint64_t vpad = 0, ntiles = 0;
+  uint32_t* d_front[2] = {nullptr, nullptr};
+  uint64_t* d_fval[2] = {nullptr, nullptr};
+  uint32_t* d_tiles = nullptr;
+  uint32_t* d_big = nullptr;
+  uint64_t* d_big_prefix = nullptr;
+  uint64_t* d_ctr = nullptr;
+  uint64_t* h_ctr = nullptr;    // pinned
+  uint64_t* h_small = nullptr;  // pinned staging for the source / initial values
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // last run's per-iteration log
+  std::vector<uint64_t> log_trav, log_front;
+  std::vector<uint64_t> log_hist;  // 8 per iteration (ZC_OPT_TRAFFIC_MODEL)
+  uint32_t options = 0;
+};
+
+
+namespace zc {
+// zc_api.cu
+void free_graph(zc_graph* g);
+int alloc_state(zc_graph* g);
+int finish_create(zc_graph* g);  // prefetch (UVM) + sync
+// Adopt a list generated in HBM (d_src, n elements of width w) into the
+// handle's placement; frees d_src unless it becomes the HBM copy.
+int adopt_device_list(zc_graph* g, void* d_src, uint32_t w, uint64_t n, void** h,
+                      const void** dptr, void** hbm);
+}  // namespace zc

@@ -1,0 +1,112 @@
+// Internal declarations shared by the zcgraph B200 translation units.
+//
+// Layout in HBM (per handle, allocated once at create, reused by every run):
+//   off      u64[V+1]      CSR vertex list (the paper keeps it on the GPU,
+//                          PAPER.md:452-455)
+//   state    u64[V]        BFS: u32 level[V] (0xffffffff = unreached);
+//                          SSSP: u64 dist[V] (UINT64_MAX = unreached);
+//                          CC: u32 label[V]
+//   flags    u8[Vpad]      "improved / discovered this iteration" marks,
+//                          Vpad = V rounded up to the compaction tile
+//   front    u32[V] x2     frontier (sorted ascending, like traversal.py:117/150)
+//   fval     u64[V] x2     start-of-iteration value of each frontier vertex
+//                          (Jacobi snapshot, traversal.py:147,175)
+//   tiles    u32[ntiles]   per-tile counts / offsets of the compaction
+//   big      u32[V] + u64[V+1]  frontier slots whose lists are split across
+//                          warps (degree-binned scheduling) + step prefix
+//   ctr      u64[8]        device counters (next size, traversed sum, ...)
+// Edge / weight lists: pinned mapped host memory (zero-copy), managed memory
+// (UVM) or HBM (control), all 128-byte aligned.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace zc {
+
+constexpr int kWarp = 32;
+constexpr int kLineBytes = 128;
+constexpr int kTileThreads = 256;
+constexpr int kTileVerts = kTileThreads * 16;  // 16 flag bytes (one uint4) per thread
+constexpr uint32_t kUnreached32 = 0xffffffffu;
+constexpr uint64_t kUnreached64 = ~0ull;
+// A frontier vertex whose list needs more than kBigSteps warp steps is not
+// expanded by its chunk warp but queued and split across all warps.
+constexpr uint32_t kBigSteps = 16;
+
+enum Strategy : int { kNaive = 0, kMerged = 1, kMergedAligned = 2 };
+enum Algo : int { kBfs = 0, kSssp = 1, kCc = 2 };
+
+// device counter slots
+enum Ctr : int {
+  kCtrNext = 0,      // size of the next frontier
+  kCtrTrav = 1,      // sum of degrees of the next frontier
+  kCtrBig = 2,       // entries in the big-list queue
+  kCtrBigSteps = 3,  // total warp steps of the big-list queue
+  kCtrHist = 8,      // 8..11 modelled edge requests of 1..4 sectors, 12..15 weights
+  kCtrCount = 16
+};
+
+struct ExpandArgs {
+  const uint32_t* front;  // frontier vertex ids
+  const uint64_t* fval;   // snapshot values (SSSP dist / CC label)
+  uint64_t n;             // frontier size
+  const uint64_t* off;    // CSR offsets (HBM)
+  const void* edges;      // edge list (zero-copy / managed / HBM)
+  const void* weights;    // weight list (SSSP)
+  void* state;            // level / dist / label
+  uint8_t* flags;         // next-frontier marks
+  uint32_t iter;          // BFS: level assigned to newly reached vertices
+  uint32_t* big;          // big-list queue: frontier slots
+  uint64_t* big_prefix;   // exclusive prefix of big-list steps (nbig+1)
+  uint64_t* ctr;          // device counters
+};
+
+struct CompactArgs {
+  uint8_t* flags;
+  uint64_t nv;
+  uint64_t ntiles;
+  uint32_t* tiles;          // per-tile counts, then offsets
+  uint32_t* front_out;
+  uint64_t* fval_out;
+  const uint64_t* off;
+  const void* state;
+  uint64_t* ctr;
+};
+
+// Launchers (zc_kernels.cu).  All launch on `st`; return cudaError_t.
+cudaError_t launch_expand(int strategy, int algo, int edge_bytes, int weight_bytes,
+                          const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t* launches);
+// The reference's request model (coalesce.py:165-207) of one frontier,
+// accumulated into ctr[kCtrHist..kCtrHist+7].
+cudaError_t launch_traffic_model(int strategy, int edge_bytes, int weight_bytes, bool weights,
+                                 const uint32_t* front, uint64_t n, const uint64_t* off,
+                                 uint64_t* ctr, int num_sms, cudaStream_t st, uint64_t* launches);
+cudaError_t launch_compact(int algo, const CompactArgs& c, cudaStream_t st, uint64_t* launches);
+cudaError_t launch_init(int algo, void* state, uint64_t nv, uint32_t* front, uint64_t* fval,
+                        cudaStream_t st, uint64_t* launches);
+cudaError_t launch_widen(int algo, const void* state, uint64_t nv, int64_t* out, cudaStream_t st,
+                         uint64_t* launches);
+cudaError_t launch_check_edges(const void* edges, int edge_bytes, uint64_t ne, uint64_t nv,
+                               uint64_t* bad, cudaStream_t st);
+
+// Exclusive scan of u32 counts into u64 offsets (n+1 outputs), device-wide.
+cudaError_t scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp,
+                            size_t tmp_bytes, cudaStream_t st);
+size_t scan_tmp_bytes(uint64_t n);
+
+// error plumbing (zc_api.cu)
+void set_error(const std::string& msg);
+
+}  // namespace zc
+
+#define ZC_CUDA_TRY(expr)                                                              \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess) {                                                           \
+      ::zc::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+      return ZC_ECUDA;                                                                 \
+    }                                                                                  \
+  } while (0)

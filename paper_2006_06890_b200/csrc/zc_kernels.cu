@@ -1,0 +1,848 @@
+// Traversal kernels for sm_100a: frontier expansion under the three EMOGI
+// access strategies, frontier compaction, init / widen helpers.
+//
+// The lane -> element maps follow the reference access engine exactly
+// (/root/reference/pkg/src/zcgraph/access.py):
+//   naive           access.py:146-156, 195-216: lane i of warp w carries
+//                   frontier[32w+i]; each lane walks its own list one element
+//                   per step.
+//   merged          access.py:70-97, 171-192: one warp per list, step k covers
+//                   elements [s+32k, s+32k+32) & [s,e).
+//   merged-aligned  same with the first window floored to a 128-byte line:
+//                   a = s & ~0x1F (4-byte elements) / s & ~0xF (8-byte),
+//                   access.py:34-37; lanes outside [s,e) are masked.
+// Weight reads (SSSP) reuse the edge windows (access.py:100-106, 183).
+//
+// What is B200-specific here (not in the reference, which has no GPU code):
+//   * a warp owns a chunk of 32 consecutive frontier slots, loads their
+//     (v, s, e, value) with one coalesced gather and then walks the flattened
+//     sequence of their warp steps, keeping kUnroll independent 128-byte
+//     line requests in flight per warp (memory-level parallelism for the
+//     ~1-2 us PCIe round trip);
+//   * lists longer than kBigSteps steps are queued and their steps are spread
+//     evenly over every warp of the grid (degree-binned scheduling, so a
+//     Kronecker hub does not serialise one warp);
+//   * Jacobi semantics of the reference SSSP / CC (cand computed from the
+//     start-of-iteration values, traversal.py:147,175) are kept by carrying
+//     each frontier vertex's value in the frontier itself; results, iteration
+//     counts and per-iteration traversed edges equal the reference's.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "zc_internal.cuh"
+
+namespace zc {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kExpandThreads = 256;
+constexpr int kUnroll = 4;
+
+// ---------------------------------------------------------------- loads
+// Edge / weight reads: the lists are read exactly once per expansion, so
+// keep them out of L1 (.L1::no_allocate).  Works for host-mapped (sysmem),
+// managed and device pointers alike.
+__device__ __forceinline__ uint32_t ld_list(const uint32_t* p) {
+  uint32_t v;
+  asm("ld.global.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_list(const uint64_t* p) {
+  uint64_t v;
+  asm("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+// ---------------------------------------------------------------- visitors
+// Apply one traversed edge (v -> w, weight wt) whose source carries the
+// start-of-iteration value `val`.
+template <int ALGO>
+struct Visit;
+
+template <>
+struct Visit<kBfs> {
+  // traversal.py:116-118: unvisited neighbours get level = iteration.
+  static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
+                                               uint64_t) {
+    uint32_t* level = static_cast<uint32_t*>(a.state);
+    if (level[w] == kUnreached32) {
+      level[w] = a.iter;
+      a.flags[w] = 1;
+    }
+  }
+};
+
+template <>
+struct Visit<kSssp> {
+  // traversal.py:146-150: cand = dist_old[v] + w; dist = min(dist, cand);
+  // improved vertices form the next frontier.
+  static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t wt,
+                                               uint64_t val) {
+    unsigned long long* dist = static_cast<unsigned long long*>(a.state);
+    const unsigned long long cand = val + wt;
+    if (cand < dist[w]) {
+      const unsigned long long old = atomicMin(dist + w, cand);
+      if (cand < old) a.flags[w] = 1;
+    }
+  }
+};
+
+template <>
+struct Visit<kCc> {
+  // traversal.py:174-178: cand = label_old[v]; label = min(label, cand).
+  static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
+                                               uint64_t val) {
+    unsigned* label = static_cast<unsigned*>(a.state);
+    const unsigned cand = static_cast<unsigned>(val);
+    if (cand < label[w]) {
+      const unsigned old = atomicMin(label + w, cand);
+      if (cand < old) a.flags[w] = 1;
+    }
+  }
+};
+
+template <typename ET>
+struct LineElems {
+  static constexpr uint64_t value = kLineBytes / sizeof(ET);
+};
+
+template <int STRAT, typename ET>
+__device__ __forceinline__ uint64_t window_base(uint64_t s) {
+  if (STRAT == kMergedAligned) return s & ~(LineElems<ET>::value - 1);
+  return s;
+}
+
+// ------------------------------------------------ merged / merged-aligned
+// Tier 1: a warp takes 32 consecutive frontier slots, then walks the
+// flattened sequence of their 32-element windows, kUnroll windows (= kUnroll
+// independent line requests) at a time.  Lists needing more than kBigSteps
+// windows are handed to tier 2.
+template <int STRAT, int ALGO, typename ET, typename WT>
+__global__ void __launch_bounds__(kExpandThreads) k_expand_warp(ExpandArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * kExpandThreads + threadIdx.x) >> 5;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * kExpandThreads) >> 5;
+  const ET* __restrict__ E = static_cast<const ET*>(a.edges);
+  const WT* __restrict__ W = static_cast<const WT*>(a.weights);
+
+  for (uint64_t c0 = gw * kWarp; c0 < a.n; c0 += nw * kWarp) {
+    const uint64_t j = c0 + lane;
+    uint64_t s = 0, e = 0, val = 0;
+    uint32_t nst = 0;
+    if (j < a.n) {
+      const uint32_t v = a.front[j];
+      s = a.off[v];
+      e = a.off[v + 1];
+      if (ALGO != kBfs) val = a.fval[j];
+      if (e > s) {
+        const uint64_t steps = (e - window_base<STRAT, ET>(s) + kWarp - 1) / kWarp;
+        if (steps > kBigSteps) {
+          const unsigned long long slot = atomicAdd(
+              reinterpret_cast<unsigned long long*>(a.ctr + kCtrBig), 1ull);
+          a.big[slot] = static_cast<uint32_t>(j);
+          a.big_prefix[slot] = steps;
+        } else {
+          nst = static_cast<uint32_t>(steps);
+        }
+      }
+    }
+    // warp-inclusive scan of the per-slot window counts
+    uint32_t incl = nst;
+#pragma unroll
+    for (int d = 1; d < kWarp; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    const uint32_t excl = incl - nst;
+    const uint32_t total = __shfl_sync(kFull, incl, kWarp - 1);
+    const uint64_t base = window_base<STRAT, ET>(s);
+
+    for (uint32_t q0 = 0; q0 < total; q0 += kUnroll) {
+      ET dst[kUnroll];
+      WT wt[kUnroll];
+      uint64_t sval[kUnroll];
+      bool ok[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t q = q0 + u;
+        ok[u] = false;
+        sval[u] = 0;
+        if (q < total) {  // warp-uniform
+          // owner slot of window q: highest lane whose exclusive prefix <= q
+          const unsigned m = __ballot_sync(kFull, excl <= q);
+          const int k = 31 - __clz(m);
+          const uint64_t bk = __shfl_sync(kFull, base, k);
+          const uint64_t sk = __shfl_sync(kFull, s, k);
+          const uint64_t ek = __shfl_sync(kFull, e, k);
+          const uint32_t t = q - __shfl_sync(kFull, excl, k);
+          if (ALGO != kBfs) sval[u] = __shfl_sync(kFull, val, k);
+          const uint64_t idx = bk + static_cast<uint64_t>(t) * kWarp + lane;
+          ok[u] = idx >= sk && idx < ek;
+          if (ok[u]) {
+            dst[u] = ld_list(E + idx);
+            if (ALGO == kSssp) wt[u] = ld_list(W + idx);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (ok[u]) Visit<ALGO>::apply(a, dst[u], ALGO == kSssp ? uint64_t(wt[u]) : 0, sval[u]);
+      }
+    }
+  }
+}
+
+// Tier 2: every warp takes an equal contiguous range of the big lists'
+// flattened window sequence.  The windows are the same as tier 1's.
+template <int STRAT, int ALGO, typename ET, typename WT>
+__global__ void __launch_bounds__(kExpandThreads) k_expand_big(ExpandArgs a) {
+  const uint64_t nbig = a.ctr[kCtrBig];
+  if (nbig == 0) return;
+  const uint64_t total = a.big_prefix[nbig];
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * kExpandThreads + threadIdx.x) >> 5;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * kExpandThreads) >> 5;
+  uint64_t per = (total + nw - 1) / nw;
+  per = (per + kUnroll - 1) / kUnroll * kUnroll;
+  const uint64_t q_begin = gw * per;
+  if (q_begin >= total) return;
+  const uint64_t q_end = min(total, q_begin + per);
+  const ET* __restrict__ E = static_cast<const ET*>(a.edges);
+  const WT* __restrict__ W = static_cast<const WT*>(a.weights);
+
+  // entry i owning q_begin: last i with prefix[i] <= q_begin
+  uint64_t lo = 0, hi = nbig;  // invariant prefix[lo] <= q < prefix[hi]
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (a.big_prefix[mid] <= q_begin) lo = mid; else hi = mid;
+  }
+  uint64_t i = lo;
+  uint64_t p_i = a.big_prefix[i], p_next = a.big_prefix[i + 1];
+  uint64_t s, e, b, val = 0;
+  auto load_entry = [&](uint64_t ent) {
+    const uint32_t j = a.big[ent];
+    const uint32_t v = a.front[j];
+    s = a.off[v];
+    e = a.off[v + 1];
+    b = window_base<STRAT, ET>(s);
+    if (ALGO != kBfs) val = a.fval[j];
+  };
+  load_entry(i);
+
+  for (uint64_t q0 = q_begin; q0 < q_end; q0 += kUnroll) {
+    ET dst[kUnroll];
+    WT wt[kUnroll];
+    uint64_t sval[kUnroll];
+    bool ok[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t q = q0 + u;
+      ok[u] = false;
+      sval[u] = val;
+      if (q < q_end) {
+        while (q >= p_next) {  // warp-uniform
+          ++i;
+          p_i = p_next;
+          p_next = a.big_prefix[i + 1];
+          load_entry(i);
+        }
+        sval[u] = val;
+        const uint64_t idx = b + (q - p_i) * kWarp + lane;
+        ok[u] = idx >= s && idx < e;
+        if (ok[u]) {
+          dst[u] = ld_list(E + idx);
+          if (ALGO == kSssp) wt[u] = ld_list(W + idx);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (ok[u]) Visit<ALGO>::apply(a, dst[u], ALGO == kSssp ? uint64_t(wt[u]) : 0, sval[u]);
+    }
+  }
+}
+
+// In-place exclusive scan of the big-list step counts (single CTA; the
+// queue holds only lists longer than kBigSteps windows).
+__global__ void __launch_bounds__(1024) k_big_scan(uint64_t* prefix, const uint64_t* ctr) {
+  const uint64_t n = ctr[kCtrBig];
+  if (n == 0) return;
+  __shared__ uint64_t warp_sums[32];
+  const int tid = threadIdx.x;
+  const uint64_t chunk = (n + blockDim.x - 1) / blockDim.x;
+  const uint64_t lo = min(n, tid * chunk), hi = min(n, lo + chunk);
+  uint64_t sum = 0;
+  for (uint64_t k = lo; k < hi; ++k) sum += prefix[k];
+  // block exclusive scan of `sum`
+  uint64_t incl = sum;
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t t = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += t;
+  }
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t ws = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+    uint64_t wi = ws;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t t = __shfl_up_sync(kFull, wi, d);
+      if (lane >= d) wi += t;
+    }
+    warp_sums[lane] = wi - ws;
+  }
+  __syncthreads();
+  uint64_t run = warp_sums[wid] + incl - sum;
+  for (uint64_t k = lo; k < hi; ++k) {
+    const uint64_t c = prefix[k];
+    prefix[k] = run;
+    run += c;
+  }
+  if (hi == n && lo < hi) prefix[n] = run;
+}
+
+// ------------------------------------------------------------------ naive
+// access.py:195-216: thread per frontier vertex, lockstep one element per
+// step.  Slot j is lane j%32 of warp j/32 in the first grid-stride round.
+template <int ALGO, typename ET, typename WT>
+__global__ void __launch_bounds__(kExpandThreads) k_expand_naive(ExpandArgs a) {
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * kExpandThreads + threadIdx.x;
+  const uint64_t nt = static_cast<uint64_t>(gridDim.x) * kExpandThreads;
+  const ET* __restrict__ E = static_cast<const ET*>(a.edges);
+  const WT* __restrict__ W = static_cast<const WT*>(a.weights);
+  for (uint64_t j = tid; j < a.n; j += nt) {
+    const uint32_t v = a.front[j];
+    const uint64_t s = a.off[v], e = a.off[v + 1];
+    const uint64_t val = ALGO != kBfs ? a.fval[j] : 0;
+    for (uint64_t k = s; k < e; ++k) {
+      const ET w = ld_list(E + k);
+      const uint64_t wt = ALGO == kSssp ? uint64_t(ld_list(W + k)) : 0;
+      Visit<ALGO>::apply(a, w, wt, val);
+    }
+  }
+}
+
+// ------------------------------------------------------------ traffic model
+// Device restatement of the reference's request model (coalesce.py:88-207):
+// every warp memory instruction is split into runs of consecutive touched
+// 32-byte sectors inside one 128-byte line; each run is one request of
+// 32/64/96/128 bytes.  No cache is modelled.  It reads only the
+// frontier and the offsets (HBM), never the lists themselves.
+
+// Requests of one contiguous element window [lo, hi) of width eb.
+__device__ __forceinline__ void model_window(uint64_t lo, uint64_t hi, uint32_t eb,
+                                             uint32_t* cnt) {
+  const uint64_t first = lo * eb / 32, last = (hi * eb - 1) / 32;
+  for (uint64_t line = first >> 2; line <= (last >> 2); ++line) {
+    const uint64_t a = max(first, line << 2), b = min(last, (line << 2) + 3);
+    cnt[b - a] += 1;
+  }
+}
+
+__device__ __forceinline__ void flush_counts(uint32_t* cnt, uint64_t* ctr, int slot0) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    unsigned long long c = cnt[i];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(kFull, c, d);
+    if ((threadIdx.x & 31) == 0 && c)
+      atomicAdd(reinterpret_cast<unsigned long long*>(ctr + slot0 + i), c);
+  }
+}
+
+// merged / merged-aligned: windows of access.py:171-192, one per warp step.
+template <int STRAT>
+__global__ void __launch_bounds__(256) k_model_merged(const uint32_t* front, uint64_t n,
+                                                      const uint64_t* off, uint32_t eb,
+                                                      uint32_t wb, int weights, uint64_t* ctr) {
+  uint32_t ce[4] = {0, 0, 0, 0}, cw[4] = {0, 0, 0, 0};
+  const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t tid0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t rounds = (n + nt - 1) / nt;  // keep the warp converged for the shuffles
+  for (uint64_t r = 0; r < rounds; ++r) {
+    const uint64_t j = tid0 + r * nt;
+    if (j >= n) continue;
+    const uint32_t v = front[j];
+    const uint64_t s = off[v], e = off[v + 1];
+    if (e <= s) continue;
+    const uint64_t a = STRAT == kMergedAligned ? (s & ~(uint64_t)(kLineBytes / eb - 1)) : s;
+    for (uint64_t base = a; base < e; base += kWarp) {
+      const uint64_t lo = max(base, s), hi = min(base + kWarp, e);
+      model_window(lo, hi, eb, ce);
+      if (weights) model_window(lo, hi, wb, cw);
+    }
+  }
+  flush_counts(ce, ctr, kCtrHist);
+  if (weights) flush_counts(cw, ctr, kCtrHist + 4);
+}
+
+// Runs of one warp step: each lane holds one sector id (or ~0 if masked).
+__device__ __forceinline__ void model_lanes(uint64_t sec, uint32_t* cnt) {
+  const int lane = threadIdx.x & 31;
+  // bitonic sort of the 32 sector ids across the warp (ascending)
+  for (int k = 2; k <= 32; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t o = __shfl_xor_sync(kFull, sec, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      const uint64_t lo = sec < o ? sec : o, hi = sec < o ? o : sec;
+      sec = (lower == up) ? lo : hi;
+    }
+  }
+  const uint64_t prev = __shfl_up_sync(kFull, sec, 1);
+  const bool valid = sec != ~0ull;
+  const bool uniq = valid && (lane == 0 || prev != sec);
+  const unsigned umask = __ballot_sync(kFull, uniq);
+  // previous unique sector (for run breaks): nearest unique lane below
+  const unsigned below = umask & ((1u << lane) - 1);
+  const int pl = below ? 31 - __clz(below) : -1;
+  const uint64_t psec = __shfl_sync(kFull, sec, pl < 0 ? 0 : pl);
+  const bool start = uniq && (pl < 0 || psec + 1 != sec || (psec >> 2) != (sec >> 2));
+  const unsigned smask = __ballot_sync(kFull, start);
+  if (start) {
+    const unsigned above = smask & ~((2u << lane) - 1);  // starts after this lane
+    const int next = above ? __ffs(above) - 1 : 32;
+    const unsigned span = (next == 32 ? 0xffffffffu : ((1u << next) - 1)) & ~((1u << lane) - 1);
+    cnt[__popc(umask & span) - 1] += 1;
+  }
+}
+
+// naive: access.py:195-216 -- lane i of warp w is frontier[32w+i], lanes
+// step through their lists in lockstep; edge and weight accesses are
+// separate instructions (coalesce.py:182-191).
+__global__ void __launch_bounds__(256) k_model_naive(const uint32_t* front, uint64_t n,
+                                                     const uint64_t* off, uint32_t eb,
+                                                     uint32_t wb, int weights, uint64_t* ctr) {
+  uint32_t ce[4] = {0, 0, 0, 0}, cw[4] = {0, 0, 0, 0};
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t w = gw; w * kWarp < n; w += nw) {
+    const uint64_t j = w * kWarp + lane;
+    uint64_t s = 0, d = 0;
+    if (j < n) {
+      const uint32_t v = front[j];
+      s = off[v];
+      d = off[v + 1] - s;
+    }
+    uint64_t steps = d;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t x = __shfl_xor_sync(kFull, steps, o);
+      steps = x > steps ? x : steps;
+    }
+    for (uint64_t k = 0; k < steps; ++k) {
+      const bool act = k < d;
+      const unsigned am = __ballot_sync(kFull, act);
+      if (__popc(am) == 1) {  // one lane left: one 1-sector request per step
+        const int only = __ffs(am) - 1;
+        const uint64_t rem = __shfl_sync(kFull, d, only) - k;
+        if (lane == 0) {
+          ce[0] += static_cast<uint32_t>(rem);
+          if (weights) cw[0] += static_cast<uint32_t>(rem);
+        }
+        break;
+      }
+      model_lanes(act ? (s + k) * eb / 32 : ~0ull, ce);
+      if (weights) model_lanes(act ? (s + k) * wb / 32 : ~0ull, cw);
+    }
+  }
+  flush_counts(ce, ctr, kCtrHist);
+  if (weights) flush_counts(cw, ctr, kCtrHist + 4);
+}
+
+// ------------------------------------------------------------ compaction
+// Next frontier = marked vertices in ascending order (the reference's
+// frontiers are sorted: np.unique / np.flatnonzero, traversal.py:116,150,178).
+// Three passes over 4096-vertex tiles: count, scan, write (+ snapshot value,
+// + degree sum for traversed_edges, + clearing of the marks).
+
+__device__ __forceinline__ uint32_t block_reduce_u32(uint32_t x, uint32_t* sh) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) x += __shfl_down_sync(kFull, x, d);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sh[wid] = x;
+  __syncthreads();
+  uint32_t r = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r += sh[w];
+  return r;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_tile_count(CompactArgs c) {
+  __shared__ uint32_t sh[kTileThreads / 32];
+  for (uint64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
+    const uint4 f = reinterpret_cast<const uint4*>(c.flags)[t * kTileThreads + threadIdx.x];
+    uint32_t cnt = __popc(f.x) + __popc(f.y) + __popc(f.z) + __popc(f.w);
+    cnt = block_reduce_u32(cnt, sh);
+    if (threadIdx.x == 0) c.tiles[t] = cnt;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_tile_scan(CompactArgs c) {
+  __shared__ uint64_t warp_sums[32];
+  const int tid = threadIdx.x;
+  const uint64_t n = c.ntiles;
+  const uint64_t chunk = (n + blockDim.x - 1) / blockDim.x;
+  const uint64_t lo = min(n, tid * chunk), hi = min(n, lo + chunk);
+  uint64_t sum = 0;
+  for (uint64_t k = lo; k < hi; ++k) sum += c.tiles[k];
+  uint64_t incl = sum;
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t t = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += t;
+  }
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const uint64_t ws = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+    uint64_t wi = ws;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t t = __shfl_up_sync(kFull, wi, d);
+      if (lane >= d) wi += t;
+    }
+    warp_sums[lane] = wi - ws;
+    if (lane == 31) {
+      c.ctr[kCtrNext] = wi;  // grand total
+      c.ctr[kCtrTrav] = 0;
+      c.ctr[kCtrBig] = 0;
+    }
+  }
+  __syncthreads();
+  uint64_t run = warp_sums[wid] + incl - sum;
+  for (uint64_t k = lo; k < hi; ++k) {
+    const uint32_t cnt = c.tiles[k];
+    c.tiles[k] = static_cast<uint32_t>(run);  // frontier positions fit u32 (V < 2^32)
+    run += cnt;
+  }
+}
+
+template <int ALGO>
+__global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
+  __shared__ uint32_t warp_tot[kTileThreads / 32];
+  __shared__ unsigned long long deg_sh[kTileThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
+    uint4* fp = reinterpret_cast<uint4*>(c.flags) + t * kTileThreads + threadIdx.x;
+    const uint4 f = *fp;
+    const uint32_t words[4] = {f.x, f.y, f.z, f.w};
+    const uint32_t cnt = __popc(f.x) + __popc(f.y) + __popc(f.z) + __popc(f.w);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t x = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += x;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (int w = 0; w < wid; ++w) before += warp_tot[w];
+    uint64_t pos = static_cast<uint64_t>(c.tiles[t]) + before + incl - cnt;
+    unsigned long long deg = 0;
+    if (cnt) {
+      const uint64_t v0 = t * kTileVerts + static_cast<uint64_t>(threadIdx.x) * 16;
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        if ((words[b >> 2] >> ((b & 3) * 8)) & 0xffu) {
+          const uint64_t v = v0 + b;
+          c.front_out[pos] = static_cast<uint32_t>(v);
+          if (ALGO == kSssp) c.fval_out[pos] = static_cast<const uint64_t*>(c.state)[v];
+          if (ALGO == kCc) c.fval_out[pos] = static_cast<const uint32_t*>(c.state)[v];
+          deg += c.off[v + 1] - c.off[v];
+          ++pos;
+        }
+      }
+      *fp = make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) deg += __shfl_down_sync(kFull, deg, d);
+    if (lane == 0) deg_sh[wid] = deg;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long tot = 0;
+      for (int w = 0; w < kTileThreads / 32; ++w) tot += deg_sh[w];
+      if (tot) atomicAdd(reinterpret_cast<unsigned long long*>(c.ctr + kCtrTrav), tot);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- helpers
+__global__ void k_init_cc(uint32_t* label, uint64_t nv, uint32_t* front, uint64_t* fval) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    label[v] = static_cast<uint32_t>(v);
+    front[v] = static_cast<uint32_t>(v);
+    fval[v] = v;
+  }
+}
+
+template <int ALGO>
+__global__ void k_widen(const void* state, uint64_t nv, int64_t* out) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    if (ALGO == kBfs) {
+      const uint32_t x = static_cast<const uint32_t*>(state)[v];
+      out[v] = x == kUnreached32 ? -1ll : static_cast<int64_t>(x);
+    } else if (ALGO == kSssp) {
+      const uint64_t x = static_cast<const uint64_t*>(state)[v];
+      out[v] = x == kUnreached64 ? INT64_MAX : static_cast<int64_t>(x);
+    } else {
+      out[v] = static_cast<const uint32_t*>(state)[v];
+    }
+  }
+}
+
+template <typename ET>
+__global__ void k_check_edges(const ET* edges, uint64_t ne, uint64_t nv,
+                              unsigned long long* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (static_cast<uint64_t>(edges[i]) >= nv) atomicAdd(bad, 1ull);
+  }
+}
+
+// ------------------------------------------------- device-wide u32 -> u64 scan
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr uint64_t kScanChunk = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* in, uint64_t n,
+                                                              uint64_t* part) {
+  __shared__ unsigned long long sh[kScanThreads / 32];
+  const uint64_t b = blockIdx.x;
+  const uint64_t base = b * kScanChunk + threadIdx.x * (uint64_t)kScanItems;
+  unsigned long long sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < n) sum += in[base + i];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) sum += __shfl_down_sync(kFull, sum, d);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kScanThreads / 32; ++w) t += sh[w];
+    part[b] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_partials(uint64_t* part, uint64_t nb) {
+  __shared__ uint64_t warp_sums[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t chunk = (nb + blockDim.x - 1) / blockDim.x;
+  const uint64_t lo = min(nb, tid * chunk), hi = min(nb, lo + chunk);
+  uint64_t sum = 0;
+  for (uint64_t k = lo; k < hi; ++k) sum += part[k];
+  uint64_t incl = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t t = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += t;
+  }
+  if (lane == 31) warp_sums[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const uint64_t ws = warp_sums[lane];
+    uint64_t wi = ws;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t t = __shfl_up_sync(kFull, wi, d);
+      if (lane >= d) wi += t;
+    }
+    warp_sums[lane] = wi - ws;
+  }
+  __syncthreads();
+  uint64_t run = warp_sums[wid] + incl - sum;
+  for (uint64_t k = lo; k < hi; ++k) {
+    const uint64_t c = part[k];
+    part[k] = run;
+    run += c;
+  }
+  if (hi == nb && lo < hi) part[nb] = run;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* in, uint64_t n,
+                                                            const uint64_t* part, uint64_t* out) {
+  __shared__ unsigned long long warp_tot[kScanThreads / 32];
+  const uint64_t b = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t base = b * kScanChunk + threadIdx.x * (uint64_t)kScanItems;
+  uint32_t vals[kScanItems];
+  unsigned long long sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    vals[i] = base + i < n ? in[base + i] : 0;
+    sum += vals[i];
+  }
+  unsigned long long incl = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long t = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += t;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  unsigned long long run = part[b] + incl - sum;
+  for (int w = 0; w < wid; ++w) run += warp_tot[w];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) out[base + i] = run;
+    run += vals[i];
+  }
+  if (b == gridDim.x - 1 && threadIdx.x == kScanThreads - 1) out[n] = part[gridDim.x];
+}
+
+int grid_for(uint64_t work, int threads, int num_sms, int per_sm) {
+  uint64_t g = (work + threads - 1) / threads;
+  const uint64_t cap = static_cast<uint64_t>(num_sms) * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+template <int STRAT, int ALGO, typename ET, typename WT>
+cudaError_t expand_t(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t* launches) {
+  // 8 resident 256-thread CTAs per SM = 64 warps/SM (full occupancy).
+  const int per_sm = 2048 / kExpandThreads;
+  if (STRAT == kNaive) {
+    const int g = grid_for(a.n, kExpandThreads, num_sms, per_sm);
+    k_expand_naive<ALGO, ET, WT><<<g, kExpandThreads, 0, st>>>(a);
+    *launches += 1;
+    return cudaGetLastError();
+  }
+  const int g = grid_for((a.n + kWarp - 1) / kWarp * kWarp, kExpandThreads, num_sms, per_sm);
+  k_expand_warp<STRAT, ALGO, ET, WT><<<g, kExpandThreads, 0, st>>>(a);
+  k_big_scan<<<1, 1024, 0, st>>>(a.big_prefix, a.ctr);
+  k_expand_big<STRAT, ALGO, ET, WT>
+      <<<num_sms * per_sm, kExpandThreads, 0, st>>>(a);
+  *launches += 3;
+  return cudaGetLastError();
+}
+
+template <int STRAT, int ALGO>
+cudaError_t expand_w(int eb, int wb, const ExpandArgs& a, int num_sms, cudaStream_t st,
+                     uint64_t* l) {
+  if (eb == 4) {
+    if (ALGO == kSssp && wb == 8) return expand_t<STRAT, ALGO, uint32_t, uint64_t>(a, num_sms, st, l);
+    return expand_t<STRAT, ALGO, uint32_t, uint32_t>(a, num_sms, st, l);
+  }
+  if (ALGO == kSssp && wb == 8) return expand_t<STRAT, ALGO, uint64_t, uint64_t>(a, num_sms, st, l);
+  return expand_t<STRAT, ALGO, uint64_t, uint32_t>(a, num_sms, st, l);
+}
+
+template <int STRAT>
+cudaError_t expand_a(int algo, int eb, int wb, const ExpandArgs& a, int num_sms, cudaStream_t st,
+                     uint64_t* l) {
+  switch (algo) {
+    case kBfs: return expand_w<STRAT, kBfs>(eb, wb, a, num_sms, st, l);
+    case kSssp: return expand_w<STRAT, kSssp>(eb, wb, a, num_sms, st, l);
+    default: return expand_w<STRAT, kCc>(eb, wb, a, num_sms, st, l);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_expand(int strategy, int algo, int edge_bytes, int weight_bytes,
+                          const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t* launches) {
+  if (a.n == 0) return cudaSuccess;
+  switch (strategy) {
+    case kNaive: return expand_a<kNaive>(algo, edge_bytes, weight_bytes, a, num_sms, st, launches);
+    case kMerged: return expand_a<kMerged>(algo, edge_bytes, weight_bytes, a, num_sms, st, launches);
+    default:
+      return expand_a<kMergedAligned>(algo, edge_bytes, weight_bytes, a, num_sms, st, launches);
+  }
+}
+
+cudaError_t launch_traffic_model(int strategy, int edge_bytes, int weight_bytes, bool weights,
+                                 const uint32_t* front, uint64_t n, const uint64_t* off,
+                                 uint64_t* ctr, int num_sms, cudaStream_t st, uint64_t* launches) {
+  if (n == 0) return cudaSuccess;
+  const int g = grid_for(n, 256, num_sms, 8);
+  if (strategy == kNaive)
+    k_model_naive<<<g, 256, 0, st>>>(front, n, off, edge_bytes, weight_bytes, weights, ctr);
+  else if (strategy == kMerged)
+    k_model_merged<kMerged><<<g, 256, 0, st>>>(front, n, off, edge_bytes, weight_bytes, weights,
+                                               ctr);
+  else
+    k_model_merged<kMergedAligned><<<g, 256, 0, st>>>(front, n, off, edge_bytes, weight_bytes,
+                                                      weights, ctr);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact(int algo, const CompactArgs& c, cudaStream_t st, uint64_t* launches) {
+  const int g = static_cast<int>(c.ntiles < (1u << 20) ? c.ntiles : (1u << 20));
+  k_tile_count<<<g, kTileThreads, 0, st>>>(c);
+  k_tile_scan<<<1, 1024, 0, st>>>(c);
+  switch (algo) {
+    case kBfs: k_tile_write<kBfs><<<g, kTileThreads, 0, st>>>(c); break;
+    case kSssp: k_tile_write<kSssp><<<g, kTileThreads, 0, st>>>(c); break;
+    default: k_tile_write<kCc><<<g, kTileThreads, 0, st>>>(c); break;
+  }
+  *launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init(int algo, void* state, uint64_t nv, uint32_t* front, uint64_t* fval,
+                        cudaStream_t st, uint64_t* launches) {
+  if (algo == kCc) {
+    if (nv == 0) return cudaSuccess;
+    const int g = grid_for(nv, 256, 148, 16);
+    k_init_cc<<<g, 256, 0, st>>>(static_cast<uint32_t*>(state), nv, front, fval);
+    *launches += 1;
+    return cudaGetLastError();
+  }
+  const size_t bytes = nv * (algo == kSssp ? 8 : 4);
+  return cudaMemsetAsync(state, 0xff, bytes, st);
+}
+
+cudaError_t launch_widen(int algo, const void* state, uint64_t nv, int64_t* out, cudaStream_t st,
+                         uint64_t* launches) {
+  if (nv == 0) return cudaSuccess;
+  const int g = grid_for(nv, 256, 148, 16);
+  switch (algo) {
+    case kBfs: k_widen<kBfs><<<g, 256, 0, st>>>(state, nv, out); break;
+    case kSssp: k_widen<kSssp><<<g, 256, 0, st>>>(state, nv, out); break;
+    default: k_widen<kCc><<<g, 256, 0, st>>>(state, nv, out); break;
+  }
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_edges(const void* edges, int edge_bytes, uint64_t ne, uint64_t nv,
+                               uint64_t* bad, cudaStream_t st) {
+  if (ne == 0) return cudaSuccess;
+  const int g = grid_for(ne, 256, 148, 16);
+  if (edge_bytes == 4)
+    k_check_edges<uint32_t><<<g, 256, 0, st>>>(static_cast<const uint32_t*>(edges), ne, nv,
+                                               reinterpret_cast<unsigned long long*>(bad));
+  else
+    k_check_edges<uint64_t><<<g, 256, 0, st>>>(static_cast<const uint64_t*>(edges), ne, nv,
+                                               reinterpret_cast<unsigned long long*>(bad));
+  return cudaGetLastError();
+}
+
+size_t scan_tmp_bytes(uint64_t n) {
+  const uint64_t nb = (n + kScanChunk - 1) / kScanChunk;
+  return (nb + 1) * sizeof(uint64_t);
+}
+
+cudaError_t scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp,
+                            size_t tmp_bytes, cudaStream_t st) {
+  if (n == 0) return cudaMemsetAsync(out, 0, sizeof(uint64_t), st);
+  const uint64_t nb = (n + kScanChunk - 1) / kScanChunk;
+  if (tmp_bytes < (nb + 1) * sizeof(uint64_t)) return cudaErrorInvalidValue;
+  uint64_t* part = static_cast<uint64_t*>(tmp);
+  k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, st>>>(in, n, part);
+  k_scan_partials<<<1, 1024, 0, st>>>(part, nb);
+  k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, st>>>(in, n, part, out);
+  return cudaGetLastError();
+}
+
+}  // namespace zc

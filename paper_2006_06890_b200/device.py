@@ -1,0 +1,297 @@
+"""Device-resident graph handles (the B200 host graph store).
+
+``DeviceGraph`` owns one ``zc_graph`` handle of the C ABI: the edge / weight
+lists live in pinned mapped host memory (``placement="zerocopy"``, EMOGI),
+in managed memory with read-mostly advice (``"uvm"``, the paper's baseline,
+PAPER.md:593) or in HBM (``"hbm"``, control run); offsets and all per-vertex
+state live in HBM.  Building a handle pins and copies the lists once;
+:func:`device_graph` caches it per (graph object, placement, device) so the
+reference-style ``bfs(g, ...)`` calls reuse it (CsrGraph is immutable by
+convention, reference csr.py:36).
+
+The native generators build handles directly on the GPU
+(:func:`generate_rmat`, :func:`generate_uniform_device`).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+import weakref
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from .csr import CsrGraph
+
+
+# ------------------------------------------------------------ pinned results
+class _PinnedPool:
+    """Recycles pinned host buffers of result arrays (D2H at link speed
+    without paying cudaHostAlloc on every call)."""
+
+    def __init__(self, cap_bytes: int = 8 << 30):
+        self.free: dict[int, list[int]] = {}
+        self.pooled = 0
+        self.cap = cap_bytes
+        self.lock = threading.Lock()
+
+    def get(self, nbytes: int) -> int:
+        with self.lock:
+            lst = self.free.get(nbytes)
+            if lst:
+                self.pooled -= nbytes
+                return lst.pop()
+        ptr = N.lib().zc_host_alloc(max(nbytes, 8))
+        if not ptr:
+            raise MemoryError(N.last_error())
+        return ptr
+
+    def put(self, nbytes: int, ptr: int) -> None:
+        with self.lock:
+            if self.pooled + nbytes <= self.cap:
+                self.free.setdefault(nbytes, []).append(ptr)
+                self.pooled += nbytes
+                return
+        N.lib().zc_host_free(ptr)
+
+
+_POOL = _PinnedPool()
+
+
+class _PinnedArrayOwner:
+    """numpy base object of a pinned array; returns the buffer to the pool."""
+
+    def __init__(self, count: int, dtype):
+        dt = np.dtype(dtype)
+        self.nbytes = count * dt.itemsize
+        self.ptr = _POOL.get(self.nbytes)
+        self.__array_interface__ = {"shape": (count,), "typestr": dt.str,
+                                    "data": (self.ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            _POOL.put(self.nbytes, self.ptr)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def pinned_empty(count: int, dtype=np.int64) -> np.ndarray:
+    """Uninitialised numpy array in pinned (page-locked) host memory."""
+    return np.asarray(_PinnedArrayOwner(count, dtype))
+
+
+# --------------------------------------------------------------- the handle
+def _list_arg(arr) -> tuple[np.ndarray, int]:
+    """Contiguous array with 4- or 8-byte integer elements + its width."""
+    a = np.asarray(arr)
+    if a.dtype.kind not in "iu":
+        a = a.astype(np.int64)
+    if a.dtype.itemsize not in (4, 8):
+        a = a.astype(np.int64)
+    return np.ascontiguousarray(a), a.dtype.itemsize
+
+
+class DeviceGraph:
+    """A CSR graph resident for traversal on one GPU."""
+
+    def __init__(self, g=None, placement: str = "zerocopy", device: int = 0, *,
+                 register: bool = False, uvm_prefetch: bool = False, validate: bool = True,
+                 _handle: Optional[int] = None):
+        if placement not in N.PLACEMENTS:
+            raise ValueError(f"placement must be one of {sorted(N.PLACEMENTS)}")
+        self.placement = placement
+        self.device = device
+        self._h = None
+        self._keep = None
+        self._lock = threading.Lock()
+        lib = N.lib()
+        if _handle is not None:
+            self._h = C.c_void_p(_handle)
+        else:
+            offsets = np.ascontiguousarray(np.asarray(g.offsets), dtype=np.int64)
+            edges, eb_src = _list_arg(g.edges)
+            weights, wb_src = (None, 8) if g.weights is None else _list_arg(g.weights)
+            d = N.GraphDesc()
+            d.num_vertices, d.num_edges = g.num_vertices, g.num_edges
+            d.offsets = offsets.ctypes.data
+            d.edges = edges.ctypes.data if edges.size else None
+            d.weights = None if weights is None else (weights.ctypes.data or None)
+            d.src_edge_bytes, d.src_weight_bytes = eb_src, wb_src
+            d.edge_elem_bytes, d.weight_elem_bytes = g.edge_elem_bytes, g.weight_elem_bytes
+            d.placement, d.device = N.PLACEMENTS[placement], device
+            d.flags = ((N.ZC_F_DIRECTED if g.directed else 0)
+                       | (N.ZC_F_REGISTER if register else 0)
+                       | (N.ZC_F_UVM_PREFETCH if uvm_prefetch else 0)
+                       | (0 if validate else N.ZC_F_NO_VALIDATE))
+            h = C.c_void_p()
+            N.check(lib.zc_graph_create(C.byref(d), C.byref(h)))
+            self._h = h
+            if register:  # the registered caller buffers must outlive the handle
+                self._keep = (edges, weights)
+        nv, ne = C.c_uint64(), C.c_uint64()
+        eb, wb, pl, fl = C.c_uint32(), C.c_uint32(), C.c_int32(), C.c_uint32()
+        N.check(lib.zc_graph_info(self._h, C.byref(nv), C.byref(ne), C.byref(eb), C.byref(wb),
+                                  C.byref(pl), C.byref(fl)))
+        self.num_vertices, self.num_edges = nv.value, ne.value
+        self.edge_elem_bytes = eb.value
+        self.weight_elem_bytes = wb.value or 4
+        self.has_weights = wb.value != 0
+        self.directed = bool(fl.value & N.ZC_F_DIRECTED)
+        self._options = 0
+
+    # -- lifecycle
+    def close(self) -> None:
+        if self._h is not None and self._h.value:
+            N.lib().zc_graph_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self) -> C.c_void_p:
+        if self._h is None:
+            raise RuntimeError("DeviceGraph is closed")
+        return self._h
+
+    # -- host views of the handle's own memory (valid while the handle lives)
+    def host_arrays(self):
+        e, w, o = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        N.check(N.lib().zc_graph_host_lists(self.handle, C.byref(e), C.byref(w), C.byref(o)))
+        nv, ne = self.num_vertices, self.num_edges
+        off = np.ctypeslib.as_array((C.c_int64 * (nv + 1)).from_address(o.value))
+        et = C.c_uint32 if self.edge_elem_bytes == 4 else C.c_uint64
+        edges = (np.ctypeslib.as_array((et * ne).from_address(e.value)) if ne
+                 else np.zeros(0, np.uint32))
+        weights = None
+        if self.has_weights:
+            wt = C.c_uint32 if self.weight_elem_bytes == 4 else C.c_uint64
+            weights = (np.ctypeslib.as_array((wt * ne).from_address(w.value)) if ne
+                       else np.zeros(0, np.uint32))
+        return off, edges, weights
+
+    def as_csr(self) -> CsrGraph:
+        """CsrGraph whose arrays are views of this handle's host memory."""
+        off, edges, weights = self.host_arrays()
+        g = CsrGraph(self.num_vertices, self.num_edges, off, edges, weights,
+                     self.edge_elem_bytes, self.weight_elem_bytes, self.directed)
+        g._device_graph_owner = self  # keep the memory alive with the view
+        return g
+
+    # -- run plumbing
+    def set_traffic_model(self, on: bool) -> None:
+        opt = N.ZC_OPT_TRAFFIC_MODEL if on else 0
+        if opt != self._options:
+            N.check(N.lib().zc_set_options(self.handle, opt))
+            self._options = opt
+
+    def run(self, algo: str, source: int, strategy_id: int, traffic: bool = False):
+        """Run one traversal; returns (values int64[V] pinned, Stats, traversed, frontier, hist)."""
+        lib = N.lib()
+        with self._lock:
+            self.set_traffic_model(traffic)
+            out = pinned_empty(self.num_vertices, np.int64)
+            st = N.Stats()
+            ptr = out.ctypes.data
+            if algo == "bfs":
+                rc = lib.zc_bfs(self.handle, source, strategy_id, ptr, C.byref(st))
+            elif algo == "sssp":
+                rc = lib.zc_sssp(self.handle, source, strategy_id, ptr, C.byref(st))
+            elif algo == "cc":
+                rc = lib.zc_cc(self.handle, strategy_id, ptr, C.byref(st))
+            else:
+                raise ValueError(f"unknown algorithm {algo!r}")
+            N.check(rc)
+            it = st.iterations
+            trav = np.zeros(it, np.uint64)
+            front = np.zeros(it, np.uint64)
+            N.check(lib.zc_run_log(self.handle, trav.ctypes.data, front.ctypes.data, it))
+            hist = None
+            if traffic:
+                hist = np.zeros((it, 8), np.uint64)
+                N.check(lib.zc_run_traffic(self.handle, hist.ctypes.data, it))
+        return out, st, trav, front, hist
+
+
+# id(graph) -> (weakref to graph, {key: DeviceGraph}); CsrGraph defines __eq__
+# without __hash__ (like the reference), so it cannot key a WeakKeyDictionary.
+_CACHE: dict = {}
+_CACHE_LOCK = threading.Lock()
+
+
+def _drop(gid: int) -> None:
+    with _CACHE_LOCK:
+        entry = _CACHE.pop(gid, None)
+    if entry:
+        for dg in entry[1].values():
+            dg.close()
+
+
+def device_graph(g, placement: str = "zerocopy", device: int = 0) -> DeviceGraph:
+    """The cached DeviceGraph of a CsrGraph (or g itself if already one)."""
+    if isinstance(g, DeviceGraph):
+        return g
+    owner = getattr(g, "_device_graph_owner", None)
+    if isinstance(owner, DeviceGraph) and owner.placement == placement and owner.device == device:
+        return owner
+    key = (placement, device, g.num_vertices, g.num_edges, g.edge_elem_bytes,
+           g.weight_elem_bytes, bool(g.directed), id(g.offsets), id(g.edges), id(g.weights))
+    gid = id(g)
+    with _CACHE_LOCK:
+        entry = _CACHE.get(gid)
+        if entry is None or entry[0]() is not g:
+            entry = (weakref.ref(g, lambda _r, gid=gid: _drop(gid)), {})
+            _CACHE[gid] = entry
+        per = entry[1]
+        dg = per.get(key)
+        if dg is None:
+            dg = DeviceGraph(g, placement, device)
+            per.clear()  # one live handle per graph object (memory is large)
+            per[key] = dg
+    return dg
+
+
+def release(g) -> None:
+    """Drop the cached device handle of g (frees pinned / HBM memory)."""
+    _drop(id(g))
+
+
+# --------------------------------------------------------------- generators
+def generate_rmat(scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
+                  c: float = 0.19, seed: int = 27, *, symmetrize: bool = False,
+                  weights: Optional[tuple[int, int]] = None, placement: str = "zerocopy",
+                  device: int = 0) -> DeviceGraph:
+    """R-MAT / Kronecker graph generated on the GPU straight into a handle."""
+    lo, hi = weights if weights is not None else (1, 0)
+    h = C.c_void_p()
+    N.check(N.lib().zc_generate_rmat(scale, edge_factor, a, b, c, seed, int(symmetrize), lo, hi,
+                                     N.PLACEMENTS[placement], device, C.byref(h)))
+    return DeviceGraph(placement=placement, device=device, _handle=h.value)
+
+
+def generate_uniform_device(num_vertices: int, min_degree: int, max_degree: int,
+                            seed: int = 3, *, weights: Optional[tuple[int, int]] = None,
+                            placement: str = "zerocopy", device: int = 0) -> DeviceGraph:
+    """Uniform random graph (generate_uniform semantics) generated on the GPU."""
+    lo, hi = weights if weights is not None else (1, 0)
+    h = C.c_void_p()
+    N.check(N.lib().zc_generate_uniform(num_vertices, min_degree, max_degree, seed, lo, hi,
+                                        N.PLACEMENTS[placement], device, C.byref(h)))
+    return DeviceGraph(placement=placement, device=device, _handle=h.value)
+
+
+def link_probe(device: int = 0, nbytes: int = 1 << 30, iters: int = 5) -> dict:
+    """Measured host-link and HBM read bandwidths (GB/s)."""
+    m, z, h = C.c_double(), C.c_double(), C.c_double()
+    N.check(N.lib().zc_link_probe(device, nbytes, iters, C.byref(m), C.byref(z), C.byref(h)))
+    return {"memcpy_h2d_gbs": m.value, "zerocopy_read_gbs": z.value, "hbm_read_gbs": h.value}

@@ -1,0 +1,125 @@
+"""BFS / SSSP / CC over zero-copy CSR on a B200 -- drop-in for the reference's
+traversal entry points (/root/reference/pkg/src/zcgraph/traversal.py:98-179).
+
+Same signatures, same argument checks (same ValueError conditions and
+messages), same ``TraversalResult`` (int64 values with -1 / INT64_MAX for
+unreached, iteration count, per-iteration traversed edges, per-iteration
+modelled traffic).  The work runs in the CUDA library through the C ABI;
+there is no CPU path.  Extra keyword-only arguments select the placement of
+the edge list (``placement="zerocopy" | "uvm" | "hbm"``) and the GPU.
+"""
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from .access import AccessStrategy, strategy_id
+from .device import DeviceGraph, device_graph
+from .traffic import TrafficStats
+
+UNREACHED_LEVEL = -1
+UNREACHED_DIST = np.iinfo(np.int64).max
+
+
+@dataclass
+class TraversalResult:
+    """Reference traversal.py:26-45, plus the device run statistics."""
+
+    algo: str
+    values: np.ndarray
+    iterations: int
+    per_iteration_traffic: list
+    traversed_edges: list
+    flags: tuple = ()
+    page_streams: Optional[list] = None
+    frontier_sizes: list = field(default_factory=list)
+    kernel_ms: float = 0.0
+    total_ms: float = 0.0
+    d2h_ms: float = 0.0
+    launches: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+    @property
+    def total_traffic(self) -> TrafficStats:
+        total = TrafficStats.zero()
+        for s in self.per_iteration_traffic:
+            total = total.merged_with(s)
+        return total
+
+    @property
+    def total_traversed_edges(self) -> int:
+        return sum(self.traversed_edges)
+
+
+def _check_source(g, source: int) -> None:
+    # traversal.py:93-95
+    if not 0 <= source < g.num_vertices:
+        raise ValueError(f"source {source} out of range for {g.num_vertices} vertices")
+
+
+def _has_weights(g) -> bool:
+    if isinstance(g, DeviceGraph):
+        return g.has_weights
+    return g.weights is not None
+
+
+def _run(algo: str, g, source: int, strategy, collect_traffic: bool, want_pages: bool,
+         placement: str, device: int) -> TraversalResult:
+    sid = strategy_id(strategy)
+    if want_pages:
+        # The page streams feed the reference's LRU page-migration simulator
+        # (uvm.py), which this build replaces with a real managed-memory run.
+        raise NotImplementedError(
+            "page streams are a simulator artefact; run with placement='uvm' for the real "
+            "cudaMallocManaged comparison")
+    dg = device_graph(g, placement, device)
+    out, st, trav, front, hist = dg.run(algo, int(source), sid, traffic=collect_traffic)
+    if hist is not None:
+        per_iter = [TrafficStats.from_size_counts(h[:4] + h[4:]) for h in hist.astype(np.int64)]
+    else:
+        per_iter = [TrafficStats.zero() for _ in range(st.iterations)]
+    return TraversalResult(
+        algo=algo, values=out, iterations=int(st.iterations), per_iteration_traffic=per_iter,
+        traversed_edges=[int(x) for x in trav], frontier_sizes=[int(x) for x in front],
+        kernel_ms=st.kernel_ms, total_ms=st.total_ms, d2h_ms=st.d2h_ms,
+        launches=int(st.launches), h2d_bytes=int(st.h2d_bytes), d2h_bytes=int(st.d2h_bytes))
+
+
+def bfs(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traffic: bool = True,
+        want_pages: bool = False, page_bytes: int = 4096, placement: str = "zerocopy",
+        device: int = 0) -> TraversalResult:
+    """Unweighted hop distances from source; unreached vertices get -1.
+
+    One iteration per level including the final empty expansion, so
+    iterations = max reached level + 1 (reference traversal.py:98-120).
+    """
+    _check_source(g, source)
+    return _run("bfs", g, source, strategy, collect_traffic, want_pages, placement, device)
+
+
+def sssp(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traffic: bool = True,
+         want_pages: bool = False, page_bytes: int = 4096, placement: str = "zerocopy",
+         device: int = 0) -> TraversalResult:
+    """Exact shortest distances by frontier-restricted (Jacobi) relaxation
+    (reference traversal.py:123-151); unreached vertices get INT64_MAX."""
+    _check_source(g, source)
+    if not _has_weights(g):
+        raise ValueError("sssp requires edge weights")
+    if not isinstance(g, DeviceGraph) and g.num_edges and int(np.min(g.weights)) < 0:
+        raise ValueError("sssp requires non-negative weights")
+    return _run("sssp", g, source, strategy, collect_traffic, want_pages, placement, device)
+
+
+def cc(g, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traffic: bool = True,
+       want_pages: bool = False, page_bytes: int = 4096, placement: str = "zerocopy",
+       device: int = 0) -> TraversalResult:
+    """Connected-component labels (min vertex id) by minimum-label propagation,
+    all vertices active at the start (reference traversal.py:154-179)."""
+    if g.directed:
+        raise ValueError("connected components require an undirected graph "
+                         "(load with directed=False or symmetrize first)")
+    return _run("cc", g, 0, strategy, collect_traffic, want_pages, placement, device)

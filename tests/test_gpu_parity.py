@@ -1,0 +1,165 @@
+"""Parity of the CUDA path (through the C ABI) with the reference's outputs and
+the CPU oracle.  Bit-exact: values (int64), iteration counts and per-iteration
+traversed-edge counts; modelled traffic histograms too.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from fixtures import crc, goldens, small_cases, traffic_cases
+
+import paper_2006_06890_b200 as zc
+
+pytestmark = pytest.mark.gpu
+
+STRATS = list(zc.AccessStrategy)
+CASES = small_cases()
+
+
+def _run(c, strategy, placement="zerocopy", traffic=False):
+    fn = {"bfs": lambda: zc.bfs(c.graph, c.source, strategy, collect_traffic=traffic,
+                                placement=placement),
+          "sssp": lambda: zc.sssp(c.graph, c.source, strategy, collect_traffic=traffic,
+                                  placement=placement),
+          "cc": lambda: zc.cc(c.graph, strategy, collect_traffic=traffic,
+                              placement=placement)}[c.algo]
+    return fn()
+
+
+@pytest.mark.parametrize("strategy", STRATS, ids=[s.value for s in STRATS])
+def test_small_graphs_match_reference(strategy):
+    bad = []
+    for c in CASES:
+        r = _run(c, strategy)
+        if not (np.array_equal(r.values, c.values) and r.iterations == c.iterations
+                and r.traversed_edges == c.traversed):
+            bad.append((c.index, c.tag))
+    assert not bad, f"{len(bad)} mismatches, first {bad[:8]}"
+
+
+@pytest.mark.parametrize("placement", ["uvm", "hbm"])
+def test_small_graphs_other_placements(placement):
+    bad = []
+    for c in CASES[::3]:
+        r = _run(c, zc.AccessStrategy.MERGED_ALIGNED, placement)
+        if not (np.array_equal(r.values, c.values) and r.iterations == c.iterations):
+            bad.append((c.index, c.tag))
+        zc.release(c.graph)
+    assert not bad, bad[:8]
+
+
+def test_traffic_model_matches_reference():
+    bad = []
+    for idx, sid, hist in traffic_cases():
+        c = CASES[idx]
+        r = _run(c, STRATS[sid], traffic=True)
+        got = np.array([[t.hist[s] for s in (32, 64, 96, 128)] for t in r.per_iteration_traffic],
+                       np.int64).reshape(-1, 4)
+        if not np.array_equal(got, hist):
+            bad.append((idx, c.tag, STRATS[sid].value))
+    assert not bad, f"{len(bad)} traffic mismatches, first {bad[:8]}"
+
+
+def _mid(name, g):
+    gold = goldens()[name]
+    gw = zc.with_uniform_weights(g)
+    gu = zc.symmetrized(g)
+    for s in STRATS:
+        for algo, graph in (("bfs", g), ("sssp", gw), ("cc", gu)):
+            if algo == "cc":
+                r = zc.cc(graph, s, collect_traffic=False)
+            else:
+                r = getattr(zc, algo)(graph, gold["src"], s, collect_traffic=False)
+            assert crc(r.values) == gold[algo]["crc"], (algo, s)
+            assert r.iterations == gold[algo]["iterations"], (algo, s)
+            assert r.traversed_edges == gold[algo]["traversed_edges"], (algo, s)
+
+
+def test_uniform_2p16_all_strategies():
+    _mid("uniform_2p16_d16", zc.generate_uniform(2 ** 16, 16, 16, seed=3))
+
+
+def test_powerlaw_100k_all_strategies():
+    _mid("powerlaw_100k_d8", zc.generate_powerlaw(100000, 8.0, 2.0, seed=3))
+
+
+def test_config1_goldens():
+    """Config 1: uniform 2^20 deg 16 seed 3 -- BFS src 0 crc 171fbc8b (8
+    levels), SSSP 2e5f7c3e (16 iterations), CC 1ad2bc45 (6 iterations)."""
+    g = zc.generate_uniform(2 ** 20, 16, 16, seed=3)
+    gold = goldens()["c1"]
+    r = zc.bfs(g, 0, collect_traffic=False)
+    assert crc(r.values) == gold["bfs"]["crc"] == "171fbc8b"
+    assert r.traversed_edges == gold["bfs"]["traversed_edges"]
+    for s, rec in gold["bfs_sources"].items():
+        assert crc(zc.bfs(g, int(s), collect_traffic=False).values) == rec["crc"]
+    gw = zc.with_uniform_weights(g)
+    r = zc.sssp(gw, 0, collect_traffic=False)
+    assert crc(r.values) == gold["sssp"]["crc"] and r.iterations == 16
+    r = zc.cc(zc.symmetrized(g), collect_traffic=False)
+    assert crc(r.values) == gold["cc"]["crc"] and r.iterations == 6
+
+
+@pytest.mark.parametrize("symmetrize", [False, True])
+def test_rmat_generator_vs_oracle(symmetrize):
+    dg = zc.generate_rmat(16, 16, seed=5, symmetrize=symmetrize, weights=(8, 72))
+    g = dg.as_csr()
+    zc.validate(g)
+    assert g.num_edges == (2 if symmetrize else 1) * 16 * 2 ** 16
+    src = int(zc.pick_sources(g, 1)[0])
+    algos = [("cc", None)] if symmetrize else [("bfs", src), ("sssp", src)]
+    for algo, s in algos:
+        ref = oracle.run(algo, g, s or 0, threads=8)
+        for st in STRATS:
+            r = zc.cc(dg, st, collect_traffic=False) if algo == "cc" else \
+                getattr(zc, algo)(dg, s, st, collect_traffic=False)
+            assert np.array_equal(r.values, ref.values), (algo, st)
+            assert r.iterations == ref.iterations and r.traversed_edges == ref.traversed_edges
+
+
+def test_rmat_generator_deterministic_and_symmetric():
+    a = zc.generate_rmat(14, 8, seed=9)
+    b = zc.generate_rmat(14, 8, seed=9)
+    ga, gb = a.as_csr(), b.as_csr()
+    assert np.array_equal(ga.offsets, gb.offsets) and np.array_equal(ga.edges, gb.edges)
+    s = zc.generate_rmat(14, 8, seed=9, symmetrize=True).as_csr()
+    ref = zc.symmetrized(ga)  # reference csr.py:350-359 semantics
+    assert np.array_equal(s.offsets, ref.offsets)
+    assert np.array_equal(np.asarray(s.edges, np.int64), ref.edges)
+
+
+def test_uniform_generator_device():
+    dg = zc.generate_uniform_device(50000, 16, 16, seed=4, weights=(8, 72))
+    g = dg.as_csr()
+    zc.validate(g)
+    assert np.all(np.diff(g.offsets) == 16)
+    lists = np.sort(np.asarray(g.edges).reshape(-1, 16), axis=1)
+    assert not np.any(lists[:, 1:] == lists[:, :-1])  # no in-list duplicates
+    assert int(g.weights.min()) >= 8 and int(g.weights.max()) <= 72
+    ref = oracle.sssp(g, 0, threads=8)
+    r = zc.sssp(dg, 0, collect_traffic=False)
+    assert np.array_equal(r.values, ref.values) and r.iterations == ref.iterations
+
+
+def test_edge_cases():
+    empty = zc.CsrGraph(0, 0, np.zeros(1, np.int64), np.zeros(0, np.int64), directed=False)
+    r = zc.cc(empty, collect_traffic=False)
+    assert r.values.size == 0 and r.iterations == 0
+    single = zc.CsrGraph(1, 1, np.array([0, 1]), np.array([0]), weights=np.array([0]))
+    assert zc.bfs(single, 0).values.tolist() == [0]
+    assert zc.sssp(single, 0).values.tolist() == [0]
+    # a hub whose list spans many lines, unaligned start: big-list path
+    n = 40000
+    off = np.array([0, 3] + [3 + n] * (n - 1), np.int64)
+    edges = np.concatenate([[1, 2, 3], np.arange(1, n + 1) % n]).astype(np.int64)
+    g = zc.CsrGraph(n, int(off[-1]), off, edges)
+    for s in STRATS:
+        r = zc.bfs(g, 1, s, collect_traffic=False)
+        assert np.array_equal(r.values, oracle.bfs(g, 1).values)
+
+
+def test_link_probe_sane():
+    p = zc.link_probe(nbytes=256 << 20, iters=3)
+    assert 5 < p["memcpy_h2d_gbs"] < 200
+    assert 1 < p["zerocopy_read_gbs"] < 200
+    assert p["hbm_read_gbs"] > 500
