@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark: EMOGI zero-copy BFS on a Kronecker scale-27 graph (BASELINE.json
+configs[1]: ~2.1 B directed arcs, edge list in pinned host memory, 1x B200,
+naive vs merged vs merged+aligned vs UVM).
+
+Metric: GTEPS = traversed edges (sum of frontier degrees, the reference's
+traversed_edges, traversal.py:63-65) / second, whole job.  One step = one BFS
+from the next of pick_sources(g, 64, seed=7).
+
+  value  device time (CUDA events on the library stream) of the traversal
+         loop, graph resident in its placement (edges in pinned host memory)
+  e2e    the same through the public API (paper_2006_06890_b200.bfs on a
+         DeviceGraph): source H2D, traversal, D2H of the int64 levels into
+         pinned host memory -- host wall clock
+  roofline  dominant kernel = the expansion kernels (the zero-copy edge
+         stream): algorithmic bytes = traversed edges x 4 B, over their
+         CUDA-event time, against PCIe Gen5 x16 (63.0 GB/s per direction)
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+Under torchrun (N>1) each rank generates and traverses its own replica
+(scaling "weak"); rank 0 prints the JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PCIE_GEN5_X16_GBS = 63.0  # 32 GT/s x 16 lanes x 128/130 / 8, per direction
+METRIC = "BFS GTEPS (Kronecker scale-27, edge list zero-copy in pinned host memory)"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--scale", type=int, default=27)
+    p.add_argument("--edge-factor", type=int, default=16)
+    p.add_argument("--seed", type=int, default=27)
+    p.add_argument("--strategy", default="merged-aligned")
+    p.add_argument("--no-variants", action="store_true",
+                   help="skip the naive / merged / UVM / HBM comparison runs")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-threads", type=int, default=0)
+    return p.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) >= 7 and parts[0].isdigit():
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        busy = [r for r in rows if r[6].isdigit() and int(r[6]) > 0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(int(r[0]) for r in busy),
+                "sm_max_mhz": max(int(r[1]) for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_setup(n_gpus: int):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world: int, device: int):
+    import torch
+    torch.cuda.synchronize(device)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        torch.cuda.synchronize(device)
+
+
+def max_over_ranks(x: float, world: int, device: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{device}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int, device: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{device}")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def load_ncu_summary() -> dict:
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return json.load(fh)
+    return {}
+
+
+def cpu_baseline(g, sources, threads: int, budget_s: float = 25.0) -> dict:
+    """The oracle port (oracle/zc_oracle.c, OpenMP) on the same graph: BFS from
+    the bench sources until ~budget_s of CPU work."""
+    import oracle
+    done, edges, t_total = 0, 0, 0.0
+    for s in sources:
+        t0 = time.perf_counter()
+        r = oracle.bfs(g, int(s), threads=threads)
+        t_total += time.perf_counter() - t0
+        edges += sum(r.traversed_edges)
+        done += 1
+        if t_total > budget_s:
+            break
+    return {"value": edges / t_total / 1e9, "unit": "GTEPS", "cores": threads, "kind": "port",
+            "sample": f"{done} full BFS run(s) of the oracle port (OpenMP C restatement of "
+                      f"traversal.py:98-120) on the same in-memory graph, {threads} threads",
+            "seconds": t_total}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_setup(args.gpus)
+    import numpy as np
+
+    if args.impl == "reference" and world > 1 and rank != 0:
+        return  # the CPU reference arm runs on rank 0 only
+    import paper_2006_06890_b200 as zc
+    import torch
+
+    device = local
+    torch.cuda.set_device(device)
+    config = {"workload": f"BFS, Kronecker (R-MAT a=.57 b=.19 c=.19) scale {args.scale}, "
+                          f"edge factor {args.edge_factor}, "
+                          f"{args.edge_factor << args.scale} directed arcs, u32 edges in "
+                          "pinned host memory (zero-copy)",
+              "graph": f"kron{args.scale}", "scale": args.scale, "edge_factor": args.edge_factor,
+              "seed": args.seed + rank, "strategy": args.strategy, "placement": "zerocopy",
+              "sources": "pick_sources(g, 64, seed=7)",
+              "l2": "inputs larger than L2 (8 GiB edge list in host memory, 512 MiB level "
+                    "array)",
+              "parallelism": f"replicas{world}" if world > 1 else "single"}
+
+    t0 = time.time()
+    dg = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed + rank, device=device)
+    gen_s = time.time() - t0
+    g = dg.as_csr()
+    sources = zc.pick_sources(g, 64, seed=7)
+
+    if args.impl == "reference":
+        threads = args.cpu_threads or os.cpu_count()
+        import oracle
+        per = []
+        edges = 0
+        for i in range(args.warmup + args.steps):
+            s = int(sources[i % len(sources)])
+            t1 = time.perf_counter()
+            r = oracle.bfs(g, s, threads=threads)
+            dt = time.perf_counter() - t1
+            if i >= args.warmup:
+                per.append(dt)
+                edges += sum(r.traversed_edges)
+        total = sum(per)
+        val = edges / total / 1e9
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GTEPS",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                "config": config,
+                "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": threads, "kind": "port",
+                                 "sample": f"{args.steps} full BFS runs of the oracle port "
+                                           "(OpenMP C restatement of traversal.py:98-120; the "
+                                           "reference itself is a Python package that cannot "
+                                           "run on the GPU box)"},
+                "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    strat = args.strategy
+    probe = zc.link_probe(device=device, nbytes=1 << 30, iters=5)
+
+    # warm-up (untimed)
+    for i in range(args.warmup):
+        zc.bfs(dg, int(sources[i % 64]), strat, collect_traffic=False)
+
+    # timed region 1: device time of the traversal loop (value)
+    barrier(world, device)
+    kernel_ms = expand_ms = 0.0
+    trav = launches = 0
+    with ClockSampler(device) as clk:
+        for i in range(args.steps):
+            r = zc.bfs(dg, int(sources[(args.warmup + i) % 64]), strat, collect_traffic=False)
+            kernel_ms += r.kernel_ms
+            expand_ms += r.expand_ms
+            trav += r.total_traversed_edges
+            launches += r.launches
+    barrier(world, device)
+    kernel_ms_max = max_over_ranks(kernel_ms, world, device)
+    trav_all = sum_over_ranks(trav, world, device)
+    value = trav_all / (kernel_ms_max * 1e-3) / 1e9
+
+    # timed region 2: end to end through the public API (host wall clock)
+    barrier(world, device)
+    t1 = time.perf_counter()
+    e2e_trav = h2d = d2h = 0
+    for i in range(args.steps):
+        r = zc.bfs(dg, int(sources[(args.warmup + i) % 64]), strat, collect_traffic=False)
+        e2e_trav += r.total_traversed_edges
+        h2d += r.h2d_bytes
+        d2h += r.d2h_bytes
+        del r
+    barrier(world, device)
+    wall = max_over_ranks(time.perf_counter() - t1, world, device)
+    e2e_value = sum_over_ranks(e2e_trav, world, device) / wall / 1e9
+
+    achieved = trav * 4 / (expand_ms * 1e-3) / 1e9  # GB/s of the expansion kernels
+    ncu = load_ncu_summary().get("bfs_expand", {})
+    line = {
+        "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": kernel_ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": config,
+        "e2e": {"value": e2e_value, "unit": "GTEPS",
+                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+                "ms_per_step": wall / args.steps * 1e3},
+        "gpu_launches": launches,
+        "roofline": {"bound": "host-link", "achieved": achieved,
+                     "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
+                     "frac": achieved / PCIE_GEN5_X16_GBS,
+                     "traffic": ncu.get("dram_bytes_per_launch"),
+                     "kernel": "k_expand_warp + k_expand_big (zero-copy edge stream)",
+                     "algorithmic_bytes": "traversed edges x 4 B (u32 edge list)",
+                     "peak_kind": "PCIe Gen5 x16 theoretical per direction",
+                     "measured_peaks_gbs": probe,
+                     "frac_of_measured_memcpy": achieved / probe["memcpy_h2d_gbs"],
+                     "sysmem_bytes_per_launch": ncu.get("sysmem_bytes_per_launch")},
+        "clocks": clk.summary(),
+        "graph": {"vertices": dg.num_vertices, "arcs": dg.num_edges, "gen_s": gen_s,
+                  "traversed_edges_per_step": trav / args.steps},
+    }
+
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = args.cpu_threads or os.cpu_count()
+        line["cpu_baseline"] = cpu_baseline(g, sources, threads)
+
+    if rank == 0 and not args.no_variants and world == 1:
+        line["variants"] = variants(zc, args, dg, sources, device)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def _gteps(zc, dg, sources, strategy, reps=1, evict=False):
+    best = None
+    for i in range(reps):
+        if evict:
+            zc.evict(dg)
+        r = zc.bfs(dg, int(sources[i % 64]), strategy, collect_traffic=False)
+        cur = {"gteps": r.total_traversed_edges / (r.kernel_ms * 1e-3) / 1e9,
+               "kernel_ms": r.kernel_ms, "expand_gbs":
+                   r.total_traversed_edges * 4 / (r.expand_ms * 1e-3) / 1e9}
+        if best is None or cur["gteps"] > best["gteps"]:
+            best = cur
+    return best
+
+
+def variants(zc, args, dg, sources, device) -> dict:
+    """configs[1]'s comparison: naive vs merged vs merged+aligned (zero-copy),
+    UVM (cold, merged+aligned) and the in-HBM control."""
+    out = {}
+    for s in ("naive", "merged", "merged-aligned"):
+        out[f"zerocopy/{s}"] = _gteps(zc, dg, sources, s, reps=2)
+    dg.close()
+    for placement in ("uvm", "hbm"):
+        h = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, device=device,
+                             placement=placement)
+        out[f"{placement}/merged-aligned"] = _gteps(zc, h, sources, "merged-aligned", reps=2,
+                                                    evict=placement == "uvm")
+        h.close()
+    zc_ = out["zerocopy/merged-aligned"]["gteps"]
+    out["speedup_vs_uvm"] = zc_ / out["uvm/merged-aligned"]["gteps"]
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -107,7 +107,9 @@ typedef struct zc_stats {
   uint64_t h2d_bytes;              /* bytes copied host->device in the call */
   uint64_t d2h_bytes;              /* bytes copied device->host in the call */
   uint64_t launches;               /* kernels launched by the call          */
-  uint64_t reserved[7];
+  double expand_ms;                /* device time of the expansion kernels
+                                      (the zero-copy edge stream) alone     */
+  uint64_t reserved[6];
 } zc_stats;
 
 const char *zc_last_error(void);
@@ -135,6 +137,14 @@ int zc_cc(zc_graph *g, int strategy, int64_t *out, zc_stats *stats);
  * may be NULL. */
 int zc_run_log(const zc_graph *g, uint64_t *traversed_edges, uint64_t *frontier_sizes,
                uint64_t capacity);
+
+/* Device time (ms, CUDA events on the handle's stream) of each iteration's
+ * expansion kernels in the most recent run. */
+int zc_run_profile(const zc_graph *g, double *expand_ms, uint64_t capacity);
+
+/* UVM placement: migrate the lists back to host memory so the next run
+ * starts cold (the paper's UVM timing).  No-op otherwise. */
+int zc_graph_evict(zc_graph *g);
 
 /* Per-handle run options. */
 #define ZC_OPT_TRAFFIC_MODEL 1u /* also evaluate the reference's request model

@@ -12,7 +12,7 @@ from .access import LINE_BYTES, SECTOR_BYTES, WARP_LANES, AccessStrategy
 from .csr import (CsrGraph, DegreeCdf, degree_cdf, generate_powerlaw, generate_uniform,
                   load_csr_binary, pick_sources, store_csr_binary, symmetrized, validate,
                   with_uniform_weights)
-from .device import (DeviceGraph, device_graph, generate_rmat, generate_uniform_device,
+from .device import (DeviceGraph, device_graph, evict, generate_rmat, generate_uniform_device,
                      link_probe, pinned_empty, release)
 from .traffic import TrafficStats
 from .traversal import UNREACHED_DIST, UNREACHED_LEVEL, TraversalResult, bfs, cc, sssp
@@ -22,7 +22,7 @@ __version__ = "0.1.0"
 __all__ = [
     "AccessStrategy", "CsrGraph", "DegreeCdf", "DeviceGraph", "LINE_BYTES", "SECTOR_BYTES",
     "TrafficStats", "TraversalResult", "UNREACHED_DIST", "UNREACHED_LEVEL", "WARP_LANES",
-    "bfs", "cc", "degree_cdf", "device_graph", "generate_powerlaw", "generate_rmat",
+    "bfs", "cc", "degree_cdf", "device_graph", "evict", "generate_powerlaw", "generate_rmat",
     "generate_uniform", "generate_uniform_device", "link_probe", "load_csr_binary",
     "pick_sources", "pinned_empty", "release", "sssp", "store_csr_binary", "symmetrized",
     "validate", "with_uniform_weights",

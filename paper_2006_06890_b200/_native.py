@@ -26,6 +26,7 @@ EXPORTED = (
     "zc_graph_destroy", "zc_graph_host_lists", "zc_graph_info", "zc_bfs", "zc_sssp",
     "zc_cc", "zc_run_log", "zc_host_alloc", "zc_host_free", "zc_generate_rmat",
     "zc_generate_uniform", "zc_link_probe", "zc_set_options", "zc_run_traffic",
+    "zc_run_profile", "zc_graph_evict",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -46,7 +47,7 @@ class Stats(C.Structure):
         ("iterations", C.c_uint64), ("total_traversed_edges", C.c_uint64),
         ("max_frontier", C.c_uint64), ("kernel_ms", C.c_double), ("total_ms", C.c_double),
         ("d2h_ms", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
-        ("launches", C.c_uint64), ("reserved", C.c_uint64 * 7),
+        ("launches", C.c_uint64), ("expand_ms", C.c_double), ("reserved", C.c_uint64 * 6),
     ]
 
 
@@ -74,6 +75,8 @@ def _declare(lib: C.CDLL) -> None:
         "zc_cc": (C.c_int, [P, C.c_int, P, C.POINTER(Stats)]),
         "zc_run_log": (C.c_int, [P, P, P, u64]),
         "zc_set_options": (C.c_int, [P, u32]),
+        "zc_run_profile": (C.c_int, [P, P, u64]),
+        "zc_graph_evict": (C.c_int, [P]),
         "zc_run_traffic": (C.c_int, [P, P, u64]),
         "zc_host_alloc": (P, [C.c_size_t]),
         "zc_host_free": (None, [P]),

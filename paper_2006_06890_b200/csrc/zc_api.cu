@@ -119,6 +119,7 @@ void zc::free_graph(zc_graph* g) {
   if (g->h_small) cudaFreeHost(g->h_small);
   for (auto& e : g->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : g->iter_ev) cudaEventDestroy(e);
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
 }
@@ -379,6 +380,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
   g->log_trav.clear();
   g->log_front.clear();
   g->log_hist.clear();
+  g->log_expand_ms.clear();
   const bool model = (g->options & ZC_OPT_TRAFFIC_MODEL) != 0;
 
   ZC_CUDA_TRY(cudaMemsetAsync(g->d_flags, 0, g->vpad, st));
@@ -429,7 +431,14 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     a.big = g->d_big;
     a.big_prefix = g->d_big_prefix;
     a.ctr = g->d_ctr;
+    while (g->iter_ev.size() < 2 * iters) {
+      cudaEvent_t e;
+      ZC_CUDA_TRY(cudaEventCreate(&e));
+      g->iter_ev.push_back(e);
+    }
+    ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (iters - 1)], st));
     ZC_CUDA_TRY(launch_expand(strategy, algo, g->eb, g->wb, a, g->num_sms, st, &launches));
+    ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (iters - 1) + 1], st));
     CompactArgs c;
     c.flags = g->d_flags;
     c.nv = g->nv;
@@ -460,6 +469,13 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     ZC_CUDA_TRY(cudaMemcpyAsync(out, d_out, g->nv * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
   ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  double expand_ms = 0;
+  for (uint64_t k = 0; k < iters; ++k) {
+    float e = 0;
+    cudaEventElapsedTime(&e, g->iter_ev[2 * k], g->iter_ev[2 * k + 1]);
+    g->log_expand_ms.push_back(e);
+    expand_ms += e;
+  }
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     stats->iterations = iters;
@@ -473,6 +489,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     stats->h2d_bytes = h2d;
     stats->d2h_bytes = g->nv * sizeof(int64_t) + iters * (model ? kCtrCount : 2) * sizeof(uint64_t);
     stats->launches = launches;
+    stats->expand_ms = expand_ms;
     stats->total_ms = now_ms() - t0;
   }
   return ZC_OK;
@@ -590,6 +607,30 @@ int zc_run_log(const zc_graph* g, uint64_t* trav, uint64_t* front, uint64_t cap)
   const uint64_t n = std::min<uint64_t>(cap, g->log_trav.size());
   if (trav) std::copy(g->log_trav.begin(), g->log_trav.begin() + n, trav);
   if (front) std::copy(g->log_front.begin(), g->log_front.begin() + n, front);
+  return ZC_OK;
+}
+
+int zc_run_profile(const zc_graph* g, double* expand_ms, uint64_t cap) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  const uint64_t n = std::min<uint64_t>(cap, g->log_expand_ms.size());
+  if (expand_ms) std::copy(g->log_expand_ms.begin(), g->log_expand_ms.begin() + n, expand_ms);
+  return ZC_OK;
+}
+
+int zc_graph_evict(zc_graph* g) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (g->placement != ZC_PLACE_UVM || !g->ne) return ZC_OK;
+  DeviceGuard dg(g->device);
+  ZC_CUDA_TRY(cudaMemPrefetchAsync(g->h_edges, g->ne * g->eb, cudaCpuDeviceId, g->stream));
+  if (g->h_weights)
+    ZC_CUDA_TRY(cudaMemPrefetchAsync(g->h_weights, g->ne * g->wb, cudaCpuDeviceId, g->stream));
+  ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
   return ZC_OK;
 }
 

@@ -238,21 +238,27 @@ __global__ void __launch_bounds__(1024) k_sort_mid(uint64_t nv, const uint64_t* 
   }
 }
 
-// Long lists (> kSortSmem): counting sort by value through a per-list
-// histogram would need V-sized scratch; instead sort in place with a
-// global-memory bitonic network per list (rare: hubs only).
+// Long lists (> kSortSmem, hubs only): bitonic network over a padded copy
+// in global memory (the pads must be materialised: intermediate stages move
+// them through the whole power-of-two range).
 template <typename ET>
-__global__ void k_sort_long_step(ET* data, uint64_t n, uint64_t m, uint64_t j, uint64_t k) {
+__global__ void k_pad_copy(const ET* src, uint64_t n, uint64_t m, ET* dst) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = i < n ? src[i] : static_cast<ET>(~0ull);
+}
+
+template <typename ET>
+__global__ void k_sort_long_step(ET* data, uint64_t m, uint64_t j, uint64_t k) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t p = i ^ j;
     if (p > i) {
-      const ET a = i < n ? data[i] : static_cast<ET>(~0ull);
-      const ET b = p < n ? data[p] : static_cast<ET>(~0ull);
+      const ET a = data[i], b = data[p];
       const bool up = (i & k) == 0;
       if ((a > b) == up) {
-        if (i < n) data[i] = b;
-        if (p < n) data[p] = a;
+        data[i] = b;
+        data[p] = a;
       }
     }
   }
@@ -319,16 +325,32 @@ int sort_lists(uint64_t nv, const uint64_t* d_off, const int64_t* h_off, ET* edg
   k_sort_short<ET><<<kGenGrid, 256>>>(nv, d_off, edges);
   k_sort_mid<ET><<<kGenGrid, 1024>>>(nv, d_off, edges);
   ZC_CUDA_TRY(cudaGetLastError());
+  uint64_t mmax = 0;
   for (uint64_t v = 0; v < nv; ++v) {
     const uint64_t n = h_off[v + 1] - h_off[v];
-    if (n <= static_cast<uint64_t>(kSortSmem)) continue;
-    uint64_t m = 1;
-    while (m < n) m <<= 1;
-    ET* data = edges + h_off[v];
-    for (uint64_t k = 2; k <= m; k <<= 1)
-      for (uint64_t j = k >> 1; j > 0; j >>= 1)
-        k_sort_long_step<ET><<<std::min<uint64_t>((m + 255) / 256, kGenGrid), 256>>>(data, n, m,
-                                                                                       j, k);
+    if (n > static_cast<uint64_t>(kSortSmem)) {
+      uint64_t m = 1;
+      while (m < n) m <<= 1;
+      mmax = std::max(mmax, m);
+    }
+  }
+  if (mmax) {
+    ET* tmp = nullptr;
+    ZC_CUDA_TRY(cudaMalloc(&tmp, mmax * sizeof(ET)));
+    for (uint64_t v = 0; v < nv; ++v) {
+      const uint64_t n = h_off[v + 1] - h_off[v];
+      if (n <= static_cast<uint64_t>(kSortSmem)) continue;
+      uint64_t m = 1;
+      while (m < n) m <<= 1;
+      ET* data = edges + h_off[v];
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((m + 255) / 256, kGenGrid));
+      k_pad_copy<ET><<<grid, 256>>>(data, n, m, tmp);
+      for (uint64_t k = 2; k <= m; k <<= 1)
+        for (uint64_t j = k >> 1; j > 0; j >>= 1) k_sort_long_step<ET><<<grid, 256>>>(tmp, m, j, k);
+      ZC_CUDA_TRY(cudaMemcpyAsync(data, tmp, n * sizeof(ET), cudaMemcpyDeviceToDevice, 0));
+    }
+    ZC_CUDA_TRY(cudaDeviceSynchronize());
+    ZC_CUDA_TRY(cudaFree(tmp));
   }
   ZC_CUDA_TRY(cudaGetLastError());
   return ZC_OK;

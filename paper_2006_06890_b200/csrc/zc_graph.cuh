@@ -47,6 +47,8 @@ struct zc_graph {
   // last run's per-iteration log
   std::vector<uint64_t> log_trav, log_front;
   std::vector<uint64_t> log_hist;  // 8 per iteration (ZC_OPT_TRAFFIC_MODEL)
+  std::vector<double> log_expand_ms;
+  std::vector<cudaEvent_t> iter_ev;  // 2 per iteration, grown on demand
   uint32_t options = 0;
 };
 

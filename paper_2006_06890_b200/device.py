@@ -188,6 +188,16 @@ class DeviceGraph:
         g._device_graph_owner = self  # keep the memory alive with the view
         return g
 
+    def evict(self) -> None:
+        """UVM: move the lists back to host memory so the next run is cold."""
+        N.check(N.lib().zc_graph_evict(self.handle))
+
+    def expand_profile(self, iterations: int) -> np.ndarray:
+        """Per-iteration device time (ms) of the expansion kernels of the last run."""
+        out = np.zeros(iterations, np.float64)
+        N.check(N.lib().zc_run_profile(self.handle, out.ctypes.data, iterations))
+        return out
+
     # -- run plumbing
     def set_traffic_model(self, on: bool) -> None:
         opt = N.ZC_OPT_TRAFFIC_MODEL if on else 0
@@ -288,6 +298,10 @@ def generate_uniform_device(num_vertices: int, min_degree: int, max_degree: int,
     N.check(N.lib().zc_generate_uniform(num_vertices, min_degree, max_degree, seed, lo, hi,
                                         N.PLACEMENTS[placement], device, C.byref(h)))
     return DeviceGraph(placement=placement, device=device, _handle=h.value)
+
+
+def evict(dg: DeviceGraph) -> None:
+    dg.evict()
 
 
 def link_probe(device: int = 0, nbytes: int = 1 << 30, iters: int = 5) -> dict:

@@ -39,6 +39,7 @@ class TraversalResult:
     kernel_ms: float = 0.0
     total_ms: float = 0.0
     d2h_ms: float = 0.0
+    expand_ms: float = 0.0
     launches: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
@@ -85,7 +86,7 @@ def _run(algo: str, g, source: int, strategy, collect_traffic: bool, want_pages:
     return TraversalResult(
         algo=algo, values=out, iterations=int(st.iterations), per_iteration_traffic=per_iter,
         traversed_edges=[int(x) for x in trav], frontier_sizes=[int(x) for x in front],
-        kernel_ms=st.kernel_ms, total_ms=st.total_ms, d2h_ms=st.d2h_ms,
+        kernel_ms=st.kernel_ms, total_ms=st.total_ms, d2h_ms=st.d2h_ms, expand_ms=st.expand_ms,
         launches=int(st.launches), h2d_bytes=int(st.h2d_bytes), d2h_bytes=int(st.d2h_bytes))
 
 

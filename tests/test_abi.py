@@ -51,7 +51,7 @@ def test_abi_version_and_error_plumbing():
 
 def test_struct_layout_matches_header():
     assert ctypes.sizeof(_native.GraphDesc) == 8 * 5 + 4 * 8
-    assert ctypes.sizeof(_native.Stats) == 8 * 3 + 8 * 3 + 8 * 3 + 8 * 7
+    assert ctypes.sizeof(_native.Stats) == 8 * 3 + 8 * 3 + 8 * 3 + 8 + 8 * 6
 
 
 def test_host_side_value_errors_match_reference():
