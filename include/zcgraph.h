@@ -185,6 +185,14 @@ int zc_generate_uniform(uint64_t num_vertices, uint32_t min_degree, uint32_t max
 int zc_link_probe(int32_t device, uint64_t bytes, int iters, double *memcpy_h2d_gbs,
                   double *zerocopy_read_gbs, double *hbm_read_gbs);
 
+/* Read microbenchmark (the paper's zero-copy toy kernel):
+ * warps read chunk_bytes contiguous bytes per request at consecutive
+ * (pattern 0) or random (pattern 1) chunk-aligned offsets of a `bytes`
+ * buffer allocated by cudaHostAlloc (alloc 0), transparent-huge-page
+ * mmap + cudaHostRegister (alloc 1) or cudaMalloc (alloc 2). */
+int zc_read_probe(int32_t device, uint64_t bytes, int pattern, uint32_t chunk_bytes, int alloc,
+                  int iters, double *gbs);
+
 #ifdef __cplusplus
 }
 #endif

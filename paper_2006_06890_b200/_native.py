@@ -26,7 +26,7 @@ EXPORTED = (
     "zc_graph_destroy", "zc_graph_host_lists", "zc_graph_info", "zc_bfs", "zc_sssp",
     "zc_cc", "zc_run_log", "zc_host_alloc", "zc_host_free", "zc_generate_rmat",
     "zc_generate_uniform", "zc_link_probe", "zc_set_options", "zc_run_traffic",
-    "zc_run_profile", "zc_graph_evict",
+    "zc_run_profile", "zc_graph_evict", "zc_read_probe",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -86,6 +86,7 @@ def _declare(lib: C.CDLL) -> None:
                                           C.POINTER(P)]),
         "zc_link_probe": (C.c_int, [i32, u64, C.c_int, C.POINTER(dbl), C.POINTER(dbl),
                                     C.POINTER(dbl)]),
+        "zc_read_probe": (C.c_int, [i32, u64, C.c_int, u32, C.c_int, C.c_int, C.POINTER(dbl)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

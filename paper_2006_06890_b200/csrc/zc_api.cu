@@ -110,9 +110,13 @@ void zc::free_graph(zc_graph* g) {
   for (int i = 0; i < 2; ++i) {
     cudaFree(g->d_front[i]);
     cudaFree(g->d_fval[i]);
+    cudaFree(g->d_fs[i]);
+    cudaFree(g->d_fd[i]);
   }
   cudaFree(g->d_tiles);
-  cudaFree(g->d_big);
+  cudaFree(g->d_big_s);
+  cudaFree(g->d_big_e);
+  cudaFree(g->d_big_val);
   cudaFree(g->d_big_prefix);
   cudaFree(g->d_ctr);
   if (g->h_ctr) cudaFreeHost(g->h_ctr);
@@ -280,9 +284,13 @@ int zc::alloc_state(zc_graph* g) {
   for (int i = 0; i < 2; ++i) {
     ZC_CUDA_TRY(cudaMalloc(&g->d_front[i], n1 * sizeof(uint32_t)));
     ZC_CUDA_TRY(cudaMalloc(&g->d_fval[i], n1 * sizeof(uint64_t)));
+    ZC_CUDA_TRY(cudaMalloc(&g->d_fs[i], n1 * sizeof(uint64_t)));
+    ZC_CUDA_TRY(cudaMalloc(&g->d_fd[i], n1 * sizeof(uint32_t)));
   }
   ZC_CUDA_TRY(cudaMalloc(&g->d_tiles, g->ntiles * sizeof(uint32_t)));
-  ZC_CUDA_TRY(cudaMalloc(&g->d_big, n1 * sizeof(uint32_t)));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_big_s, n1 * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_big_e, n1 * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_big_val, n1 * sizeof(uint64_t)));
   ZC_CUDA_TRY(cudaMalloc(&g->d_big_prefix, (n1 + 1) * sizeof(uint64_t)));
   ZC_CUDA_TRY(cudaMalloc(&g->d_ctr, kCtrCount * sizeof(uint64_t)));
   ZC_CUDA_TRY(cudaHostAlloc(&g->h_ctr, kCtrCount * sizeof(uint64_t), cudaHostAllocDefault));
@@ -385,24 +393,20 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
 
   ZC_CUDA_TRY(cudaMemsetAsync(g->d_flags, 0, g->vpad, st));
   ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr, 0, kCtrCount * sizeof(uint64_t), st));
-  ZC_CUDA_TRY(launch_init(algo, g->d_state, g->nv, g->d_front[0], g->d_fval[0], st, &launches));
+  ZC_CUDA_TRY(launch_init(algo, g->d_state, g->nv, src, g->d_off, g->d_front[0], g->d_fval[0],
+                          g->d_fs[0], g->d_fd[0], st, &launches));
   uint64_t n = 0, trav = 0;
   uint64_t h2d = 0;
   if (algo == kCc) {
     n = g->nv;
     trav = g->ne;
   } else {
-    // frontier = [src], value 0, state[src] = 0
-    g->h_small[0] = src;
+    // state[src] = 0 (the frontier [src] was written by launch_init)
     g->h_small[1] = 0;
-    ZC_CUDA_TRY(cudaMemcpyAsync(g->d_front[0], &g->h_small[0], sizeof(uint32_t),
-                                cudaMemcpyHostToDevice, st));
-    ZC_CUDA_TRY(cudaMemcpyAsync(g->d_fval[0], &g->h_small[1], sizeof(uint64_t),
-                                cudaMemcpyHostToDevice, st));
     const size_t sb = algo == kSssp ? 8 : 4;
     ZC_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(g->d_state) + src * sb, &g->h_small[1], sb,
                                 cudaMemcpyHostToDevice, st));
-    h2d += 4 + 8 + sb;
+    h2d += sb;
     n = 1;
     trav = g->h_off[src + 1] - g->h_off[src];
   }
@@ -420,6 +424,8 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
                                        g->d_off, g->d_ctr, g->num_sms, st, &launches));
     ExpandArgs a;
     a.front = g->d_front[cur];
+    a.fs = g->d_fs[cur];
+    a.fd = g->d_fd[cur];
     a.fval = g->d_fval[cur];
     a.n = n;
     a.off = g->d_off;
@@ -428,7 +434,9 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     a.state = g->d_state;
     a.flags = g->d_flags;
     a.iter = static_cast<uint32_t>(iters);
-    a.big = g->d_big;
+    a.big_s = g->d_big_s;
+    a.big_e = g->d_big_e;
+    a.big_val = g->d_big_val;
     a.big_prefix = g->d_big_prefix;
     a.ctr = g->d_ctr;
     while (g->iter_ev.size() < 2 * iters) {
@@ -445,6 +453,8 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     c.ntiles = g->ntiles;
     c.tiles = g->d_tiles;
     c.front_out = g->d_front[cur ^ 1];
+    c.fs_out = g->d_fs[cur ^ 1];
+    c.fd_out = g->d_fd[cur ^ 1];
     c.fval_out = g->d_fval[cur ^ 1];
     c.off = g->d_off;
     c.state = g->d_state;
@@ -627,11 +637,19 @@ int zc_graph_evict(zc_graph* g) {
   }
   if (g->placement != ZC_PLACE_UVM || !g->ne) return ZC_OK;
   DeviceGuard dg(g->device);
-  ZC_CUDA_TRY(cudaMemPrefetchAsync(g->h_edges, g->ne * g->eb, cudaCpuDeviceId, g->stream));
-  if (g->h_weights)
-    ZC_CUDA_TRY(cudaMemPrefetchAsync(g->h_weights, g->ne * g->wb, cudaCpuDeviceId, g->stream));
-  ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
-  return ZC_OK;
+  // Read-mostly pages keep their GPU duplicate across a prefetch to the
+  // host, so collapse the duplicates first, migrate, then re-advise.
+  auto cold = [&](void* p, size_t bytes) -> int {
+    ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
+    ZC_CUDA_TRY(cudaMemAdvise(p, bytes, cudaMemAdviseUnsetReadMostly, g->device));
+    ZC_CUDA_TRY(cudaMemPrefetchAsync(p, bytes, cudaCpuDeviceId, g->stream));
+    ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
+    ZC_CUDA_TRY(cudaMemAdvise(p, bytes, cudaMemAdviseSetReadMostly, g->device));
+    return ZC_OK;
+  };
+  int rc = cold(g->h_edges, g->ne * g->eb);
+  if (rc == ZC_OK && g->h_weights) rc = cold(g->h_weights, g->ne * g->wb);
+  return rc;
 }
 
 int zc_set_options(zc_graph* g, uint32_t options) {

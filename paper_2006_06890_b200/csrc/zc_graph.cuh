@@ -36,8 +36,12 @@ struct zc_graph {
   uint64_t vpad = 0, ntiles = 0;
   uint32_t* d_front[2] = {nullptr, nullptr};
   uint64_t* d_fval[2] = {nullptr, nullptr};
+  uint64_t* d_fs[2] = {nullptr, nullptr};
+  uint32_t* d_fd[2] = {nullptr, nullptr};
   uint32_t* d_tiles = nullptr;
-  uint32_t* d_big = nullptr;
+  uint64_t* d_big_s = nullptr;
+  uint64_t* d_big_e = nullptr;
+  uint64_t* d_big_val = nullptr;
   uint64_t* d_big_prefix = nullptr;
   uint64_t* d_ctr = nullptr;
   uint64_t* h_ctr = nullptr;    // pinned

@@ -11,9 +11,13 @@
 //   front    u32[V] x2     frontier (sorted ascending, like traversal.py:117/150)
 //   fval     u64[V] x2     start-of-iteration value of each frontier vertex
 //                          (Jacobi snapshot, traversal.py:147,175)
+//   fs, fd   u64[V], u32[V] x2  list start / degree of each frontier vertex
+//                          (written by the compaction: expansion needs no
+//                          dependent offsets gather)
 //   tiles    u32[ntiles]   per-tile counts / offsets of the compaction
-//   big      u32[V] + u64[V+1]  frontier slots whose lists are split across
-//                          warps (degree-binned scheduling) + step prefix
+//   big_*    u64[V] x3 + u64[V+1]  lists split across all warps
+//                          (degree-binned scheduling): start, end, value,
+//                          exclusive prefix of their window counts
 //   ctr      u64[8]        device counters (next size, traversed sum, ...)
 // Edge / weight lists: pinned mapped host memory (zero-copy), managed memory
 // (UVM) or HBM (control), all 128-byte aligned.
@@ -51,6 +55,8 @@ enum Ctr : int {
 
 struct ExpandArgs {
   const uint32_t* front;  // frontier vertex ids
+  const uint64_t* fs;     // list start of each frontier vertex
+  const uint32_t* fd;     // degree of each frontier vertex
   const uint64_t* fval;   // snapshot values (SSSP dist / CC label)
   uint64_t n;             // frontier size
   const uint64_t* off;    // CSR offsets (HBM)
@@ -59,7 +65,9 @@ struct ExpandArgs {
   void* state;            // level / dist / label
   uint8_t* flags;         // next-frontier marks
   uint32_t iter;          // BFS: level assigned to newly reached vertices
-  uint32_t* big;          // big-list queue: frontier slots
+  uint64_t* big_s;        // big-list queue: list start,
+  uint64_t* big_e;        //   list end,
+  uint64_t* big_val;      //   snapshot value
   uint64_t* big_prefix;   // exclusive prefix of big-list steps (nbig+1)
   uint64_t* ctr;          // device counters
 };
@@ -70,6 +78,8 @@ struct CompactArgs {
   uint64_t ntiles;
   uint32_t* tiles;          // per-tile counts, then offsets
   uint32_t* front_out;
+  uint64_t* fs_out;
+  uint32_t* fd_out;
   uint64_t* fval_out;
   const uint64_t* off;
   const void* state;
@@ -85,7 +95,8 @@ cudaError_t launch_traffic_model(int strategy, int edge_bytes, int weight_bytes,
                                  const uint32_t* front, uint64_t n, const uint64_t* off,
                                  uint64_t* ctr, int num_sms, cudaStream_t st, uint64_t* launches);
 cudaError_t launch_compact(int algo, const CompactArgs& c, cudaStream_t st, uint64_t* launches);
-cudaError_t launch_init(int algo, void* state, uint64_t nv, uint32_t* front, uint64_t* fval,
+cudaError_t launch_init(int algo, void* state, uint64_t nv, uint64_t src, const uint64_t* off,
+                        uint32_t* front, uint64_t* fval, uint64_t* fs, uint32_t* fd,
                         cudaStream_t st, uint64_t* launches);
 cudaError_t launch_widen(int algo, const void* state, uint64_t nv, int64_t* out, cudaStream_t st,
                          uint64_t* launches);

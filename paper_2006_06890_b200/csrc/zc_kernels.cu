@@ -113,10 +113,48 @@ __device__ __forceinline__ uint64_t window_base(uint64_t s) {
 }
 
 // ------------------------------------------------ merged / merged-aligned
-// Tier 1: a warp takes 32 consecutive frontier slots, then walks the
-// flattened sequence of their 32-element windows, kUnroll windows (= kUnroll
-// independent line requests) at a time.  Lists needing more than kBigSteps
-// windows are handed to tier 2.
+// A batch of kUnroll windows of one warp: each lane holds the element it
+// loaded from each window (ok = lane inside the list).
+template <int ALGO, typename ET, typename WT>
+struct Batch {
+  ET dst[kUnroll];
+  WT wt[kUnroll];
+  uint64_t sval[kUnroll];
+  bool ok[kUnroll];
+};
+
+template <int ALGO, typename ET, typename WT>
+__device__ __forceinline__ void visit_batch(const ExpandArgs& a, const Batch<ALGO, ET, WT>& b) {
+#pragma unroll
+  for (int u = 0; u < kUnroll; ++u)
+    if (b.ok[u]) Visit<ALGO>::apply(a, b.dst[u], ALGO == kSssp ? uint64_t(b.wt[u]) : 0, b.sval[u]);
+}
+
+// Per-lane metadata of one 32-slot chunk of the frontier.
+struct Chunk {
+  uint64_t s, e, val;
+  uint32_t nst;
+};
+
+template <int STRAT, int ALGO, typename ET>
+__device__ __forceinline__ Chunk load_chunk(const ExpandArgs& a, uint64_t c0, int lane) {
+  Chunk c{0, 0, 0, 0};
+  const uint64_t j = c0 + lane;
+  if (j < a.n) {
+    c.s = a.fs[j];
+    c.e = c.s + a.fd[j];
+    if (ALGO != kBfs) c.val = a.fval[j];
+  }
+  return c;
+}
+
+// Tier 1: a warp takes 32 consecutive frontier slots (their list start and
+// degree were written by the compaction, so no dependent offsets gather),
+// then walks the flattened sequence of their 32-element windows, kUnroll
+// windows at a time, issuing the loads of batch k+1 before visiting batch k
+// (so the HBM-side visit overlaps the next PCIe round trip) and prefetching
+// the next chunk's metadata.  Lists needing more than kBigSteps windows go to
+// the tier-2 queue.
 template <int STRAT, int ALGO, typename ET, typename WT>
 __global__ void __launch_bounds__(kExpandThreads) k_expand_warp(ExpandArgs a) {
   const int lane = threadIdx.x & 31;
@@ -125,25 +163,24 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_warp(ExpandArgs a) {
   const ET* __restrict__ E = static_cast<const ET*>(a.edges);
   const WT* __restrict__ W = static_cast<const WT*>(a.weights);
 
-  for (uint64_t c0 = gw * kWarp; c0 < a.n; c0 += nw * kWarp) {
-    const uint64_t j = c0 + lane;
-    uint64_t s = 0, e = 0, val = 0;
+  uint64_t c0 = gw * kWarp;
+  Chunk nextc = load_chunk<STRAT, ALGO, ET>(a, c0, lane);
+  for (; c0 < a.n; c0 += nw * kWarp) {
+    const Chunk c = nextc;
+    if (c0 + nw * kWarp < a.n) nextc = load_chunk<STRAT, ALGO, ET>(a, c0 + nw * kWarp, lane);
     uint32_t nst = 0;
-    if (j < a.n) {
-      const uint32_t v = a.front[j];
-      s = a.off[v];
-      e = a.off[v + 1];
-      if (ALGO != kBfs) val = a.fval[j];
-      if (e > s) {
-        const uint64_t steps = (e - window_base<STRAT, ET>(s) + kWarp - 1) / kWarp;
-        if (steps > kBigSteps) {
-          const unsigned long long slot = atomicAdd(
-              reinterpret_cast<unsigned long long*>(a.ctr + kCtrBig), 1ull);
-          a.big[slot] = static_cast<uint32_t>(j);
-          a.big_prefix[slot] = steps;
-        } else {
-          nst = static_cast<uint32_t>(steps);
-        }
+    const uint64_t base = window_base<STRAT, ET>(c.s);
+    if (c.e > c.s) {
+      const uint64_t steps = (c.e - base + kWarp - 1) / kWarp;
+      if (steps > kBigSteps) {
+        const unsigned long long slot =
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.ctr + kCtrBig), 1ull);
+        a.big_s[slot] = c.s;
+        a.big_e[slot] = c.e;
+        if (ALGO != kBfs) a.big_val[slot] = c.val;
+        a.big_prefix[slot] = steps;
+      } else {
+        nst = static_cast<uint32_t>(steps);
       }
     }
     // warp-inclusive scan of the per-slot window counts
@@ -155,45 +192,45 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_warp(ExpandArgs a) {
     }
     const uint32_t excl = incl - nst;
     const uint32_t total = __shfl_sync(kFull, incl, kWarp - 1);
-    const uint64_t base = window_base<STRAT, ET>(s);
 
-    for (uint32_t q0 = 0; q0 < total; q0 += kUnroll) {
-      ET dst[kUnroll];
-      WT wt[kUnroll];
-      uint64_t sval[kUnroll];
-      bool ok[kUnroll];
+    auto issue = [&](Batch<ALGO, ET, WT>& b, uint32_t q0) {
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const uint32_t q = q0 + u;
-        ok[u] = false;
-        sval[u] = 0;
+        b.ok[u] = false;
+        b.sval[u] = 0;
         if (q < total) {  // warp-uniform
           // owner slot of window q: highest lane whose exclusive prefix <= q
           const unsigned m = __ballot_sync(kFull, excl <= q);
           const int k = 31 - __clz(m);
           const uint64_t bk = __shfl_sync(kFull, base, k);
-          const uint64_t sk = __shfl_sync(kFull, s, k);
-          const uint64_t ek = __shfl_sync(kFull, e, k);
+          const uint64_t sk = __shfl_sync(kFull, c.s, k);
+          const uint64_t ek = __shfl_sync(kFull, c.e, k);
           const uint32_t t = q - __shfl_sync(kFull, excl, k);
-          if (ALGO != kBfs) sval[u] = __shfl_sync(kFull, val, k);
+          if (ALGO != kBfs) b.sval[u] = __shfl_sync(kFull, c.val, k);
           const uint64_t idx = bk + static_cast<uint64_t>(t) * kWarp + lane;
-          ok[u] = idx >= sk && idx < ek;
-          if (ok[u]) {
-            dst[u] = ld_list(E + idx);
-            if (ALGO == kSssp) wt[u] = ld_list(W + idx);
+          b.ok[u] = idx >= sk && idx < ek;
+          if (b.ok[u]) {
+            b.dst[u] = ld_list(E + idx);
+            if (ALGO == kSssp) b.wt[u] = ld_list(W + idx);
           }
         }
       }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        if (ok[u]) Visit<ALGO>::apply(a, dst[u], ALGO == kSssp ? uint64_t(wt[u]) : 0, sval[u]);
-      }
+    };
+    if (total == 0) continue;
+    Batch<ALGO, ET, WT> cur, nxt;
+    issue(cur, 0);
+    for (uint32_t q0 = 0; q0 < total; q0 += kUnroll) {
+      if (q0 + kUnroll < total) issue(nxt, q0 + kUnroll);
+      visit_batch<ALGO, ET, WT>(a, cur);
+      cur = nxt;
     }
   }
 }
 
 // Tier 2: every warp takes an equal contiguous range of the big lists'
-// flattened window sequence.  The windows are the same as tier 1's.
+// flattened window sequence (same windows as tier 1), software-pipelined
+// the same way.
 template <int STRAT, int ALGO, typename ET, typename WT>
 __global__ void __launch_bounds__(kExpandThreads) k_expand_big(ExpandArgs a) {
   const uint64_t nbig = a.ctr[kCtrBig];
@@ -218,47 +255,42 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_big(ExpandArgs a) {
   }
   uint64_t i = lo;
   uint64_t p_i = a.big_prefix[i], p_next = a.big_prefix[i + 1];
-  uint64_t s, e, b, val = 0;
-  auto load_entry = [&](uint64_t ent) {
-    const uint32_t j = a.big[ent];
-    const uint32_t v = a.front[j];
-    s = a.off[v];
-    e = a.off[v + 1];
-    b = window_base<STRAT, ET>(s);
-    if (ALGO != kBfs) val = a.fval[j];
-  };
-  load_entry(i);
+  uint64_t s = a.big_s[i], e = a.big_e[i];
+  uint64_t b = window_base<STRAT, ET>(s);
+  uint64_t val = ALGO != kBfs ? a.big_val[i] : 0;
 
-  for (uint64_t q0 = q_begin; q0 < q_end; q0 += kUnroll) {
-    ET dst[kUnroll];
-    WT wt[kUnroll];
-    uint64_t sval[kUnroll];
-    bool ok[kUnroll];
+  auto issue = [&](Batch<ALGO, ET, WT>& bt, uint64_t q0) {
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const uint64_t q = q0 + u;
-      ok[u] = false;
-      sval[u] = val;
+      bt.ok[u] = false;
+      bt.sval[u] = val;
       if (q < q_end) {
         while (q >= p_next) {  // warp-uniform
           ++i;
           p_i = p_next;
           p_next = a.big_prefix[i + 1];
-          load_entry(i);
+          s = a.big_s[i];
+          e = a.big_e[i];
+          b = window_base<STRAT, ET>(s);
+          if (ALGO != kBfs) val = a.big_val[i];
         }
-        sval[u] = val;
+        bt.sval[u] = val;
         const uint64_t idx = b + (q - p_i) * kWarp + lane;
-        ok[u] = idx >= s && idx < e;
-        if (ok[u]) {
-          dst[u] = ld_list(E + idx);
-          if (ALGO == kSssp) wt[u] = ld_list(W + idx);
+        bt.ok[u] = idx >= s && idx < e;
+        if (bt.ok[u]) {
+          bt.dst[u] = ld_list(E + idx);
+          if (ALGO == kSssp) bt.wt[u] = ld_list(W + idx);
         }
       }
     }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (ok[u]) Visit<ALGO>::apply(a, dst[u], ALGO == kSssp ? uint64_t(wt[u]) : 0, sval[u]);
-    }
+  };
+  Batch<ALGO, ET, WT> cur, nxt;
+  issue(cur, q_begin);
+  for (uint64_t q0 = q_begin; q0 < q_end; q0 += kUnroll) {
+    if (q0 + kUnroll < q_end) issue(nxt, q0 + kUnroll);
+    visit_batch<ALGO, ET, WT>(a, cur);
+    cur = nxt;
   }
 }
 
@@ -313,8 +345,7 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_naive(ExpandArgs a) {
   const ET* __restrict__ E = static_cast<const ET*>(a.edges);
   const WT* __restrict__ W = static_cast<const WT*>(a.weights);
   for (uint64_t j = tid; j < a.n; j += nt) {
-    const uint32_t v = a.front[j];
-    const uint64_t s = a.off[v], e = a.off[v + 1];
+    const uint64_t s = a.fs[j], e = s + a.fd[j];
     const uint64_t val = ALGO != kBfs ? a.fval[j] : 0;
     for (uint64_t k = s; k < e; ++k) {
       const ET w = ld_list(E + k);
@@ -550,10 +581,13 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
       for (int b = 0; b < 16; ++b) {
         if ((words[b >> 2] >> ((b & 3) * 8)) & 0xffu) {
           const uint64_t v = v0 + b;
+          const uint64_t s0 = c.off[v], d0 = c.off[v + 1] - s0;
           c.front_out[pos] = static_cast<uint32_t>(v);
+          c.fs_out[pos] = s0;
+          c.fd_out[pos] = static_cast<uint32_t>(d0);
           if (ALGO == kSssp) c.fval_out[pos] = static_cast<const uint64_t*>(c.state)[v];
           if (ALGO == kCc) c.fval_out[pos] = static_cast<const uint32_t*>(c.state)[v];
-          deg += c.off[v + 1] - c.off[v];
+          deg += d0;
           ++pos;
         }
       }
@@ -573,13 +607,26 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
 }
 
 // ---------------------------------------------------------------- helpers
-__global__ void k_init_cc(uint32_t* label, uint64_t nv, uint32_t* front, uint64_t* fval) {
+__global__ void k_init_cc(uint32_t* label, uint64_t nv, uint32_t* front, uint64_t* fval,
+                          const uint64_t* off, uint64_t* fs, uint32_t* fd) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
        v += (uint64_t)gridDim.x * blockDim.x) {
     label[v] = static_cast<uint32_t>(v);
     front[v] = static_cast<uint32_t>(v);
     fval[v] = v;
+    const uint64_t s0 = off[v];
+    fs[v] = s0;
+    fd[v] = static_cast<uint32_t>(off[v + 1] - s0);
   }
+}
+
+// frontier = [src] with its list bounds (BFS / SSSP)
+__global__ void k_init_source(uint64_t src, const uint64_t* off, uint32_t* front, uint64_t* fval,
+                              uint64_t* fs, uint32_t* fd) {
+  front[0] = static_cast<uint32_t>(src);
+  fval[0] = 0;
+  fs[0] = off[src];
+  fd[0] = static_cast<uint32_t>(off[src + 1] - off[src]);
 }
 
 template <int ALGO>
@@ -789,17 +836,22 @@ cudaError_t launch_compact(int algo, const CompactArgs& c, cudaStream_t st, uint
   return cudaGetLastError();
 }
 
-cudaError_t launch_init(int algo, void* state, uint64_t nv, uint32_t* front, uint64_t* fval,
+cudaError_t launch_init(int algo, void* state, uint64_t nv, uint64_t src, const uint64_t* off,
+                        uint32_t* front, uint64_t* fval, uint64_t* fs, uint32_t* fd,
                         cudaStream_t st, uint64_t* launches) {
   if (algo == kCc) {
     if (nv == 0) return cudaSuccess;
     const int g = grid_for(nv, 256, 148, 16);
-    k_init_cc<<<g, 256, 0, st>>>(static_cast<uint32_t*>(state), nv, front, fval);
+    k_init_cc<<<g, 256, 0, st>>>(static_cast<uint32_t*>(state), nv, front, fval, off, fs, fd);
     *launches += 1;
     return cudaGetLastError();
   }
   const size_t bytes = nv * (algo == kSssp ? 8 : 4);
-  return cudaMemsetAsync(state, 0xff, bytes, st);
+  cudaError_t e = cudaMemsetAsync(state, 0xff, bytes, st);
+  if (e != cudaSuccess) return e;
+  k_init_source<<<1, 1, 0, st>>>(src, off, front, fval, fs, fd);
+  *launches += 1;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_widen(int algo, const void* state, uint64_t nv, int64_t* out, cudaStream_t st,

@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string.h>
+#include <sys/mman.h>
+
 #include <algorithm>
 #include <string>
 
@@ -41,8 +44,124 @@ __global__ void __launch_bounds__(256) k_stream_read(const uint4* __restrict__ p
   if (acc == 0x12345678u) atomicAdd(sink, 1ull);
 }
 
+// Read microbenchmark (the paper's zero-copy toy kernel):
+// every warp reads `chunk` contiguous bytes per request (32..512, lanes
+// masked beyond it) at either consecutive (pattern 0) or pseudo-random
+// (pattern 1) chunk-aligned offsets; kU requests in flight per warp.
+template <int kU>
+__global__ void __launch_bounds__(256) k_chunk_read(const uint32_t* __restrict__ p, uint64_t nchunks,
+                                                    uint32_t chunk_words, int random,
+                                                    uint64_t total_reqs,
+                                                    unsigned long long* sink) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t acc = 0;
+  for (uint64_t r0 = gw * kU; r0 < total_reqs; r0 += nw * kU) {
+    uint32_t v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      uint64_t r = r0 + u;
+      v[u] = 0;
+      if (r < total_reqs) {
+        uint64_t c = r % nchunks;
+        if (random) {
+          uint64_t z = r * 0x9e3779b97f4a7c15ull;
+          z ^= z >> 31;
+          z *= 0xbf58476d1ce4e5b9ull;
+          z ^= z >> 29;
+          c = z % nchunks;
+        }
+        for (uint32_t w = lane; w < chunk_words; w += 32) {
+          uint32_t x;
+          asm volatile("ld.global.L1::no_allocate.u32 %0, [%1];"
+                       : "=r"(x) : "l"(p + c * chunk_words + w));
+          v[u] ^= x;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) acc ^= v[u];
+  }
+  if (acc == 0x12345678u) atomicAdd(sink, 1ull);
+}
+
 }  // namespace
 }  // namespace zc
+
+// alloc: 0 = cudaHostAlloc(Mapped), 1 = THP (madvise) + cudaHostRegister,
+// 2 = device memory.  Returns GB/s of useful bytes in *gbs.
+extern "C" int zc_read_probe(int32_t device, uint64_t bytes, int pattern, uint32_t chunk_bytes,
+                             int alloc, int iters, double* gbs) {
+  using namespace zc;
+  cudaSetDevice(device);
+  if (chunk_bytes < 4 || chunk_bytes % 4 || chunk_bytes > 4096) {
+    set_error("chunk_bytes must be a multiple of 4 in [4, 4096]");
+    return ZC_EINVAL;
+  }
+  bytes = std::max<uint64_t>(bytes / 4096 * 4096, 1 << 22);
+  void* h = nullptr;
+  const void* dp = nullptr;
+  bool registered = false;
+  if (alloc == 0) {
+    ZC_CUDA_TRY(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(h, 1, bytes);
+    void* d = nullptr;
+    ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, h, 0));
+    dp = d;
+  } else if (alloc == 1) {
+    const size_t huge = 2u << 20;
+    bytes = (bytes + huge - 1) / huge * huge;
+    void* m = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (m == MAP_FAILED) {
+      set_error("mmap failed");
+      return ZC_ENOMEM;
+    }
+    madvise(m, bytes, MADV_HUGEPAGE);
+    memset(m, 1, bytes);
+    h = m;
+    ZC_CUDA_TRY(cudaHostRegister(h, bytes, cudaHostRegisterMapped));
+    registered = true;
+    void* d = nullptr;
+    ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, h, 0));
+    dp = d;
+  } else {
+    void* d = nullptr;
+    ZC_CUDA_TRY(cudaMalloc(&d, bytes));
+    ZC_CUDA_TRY(cudaMemset(d, 1, bytes));
+    dp = d;
+  }
+  unsigned long long* sink = nullptr;
+  ZC_CUDA_TRY(cudaMalloc(&sink, sizeof(unsigned long long)));
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  const uint64_t nchunks = bytes / chunk_bytes;
+  const uint64_t reqs = nchunks;  // one pass worth of requests
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int grid = nsm * 8;
+  k_chunk_read<4><<<grid, 256>>>(static_cast<const uint32_t*>(dp), nchunks, chunk_bytes / 4,
+                                 pattern, reqs, sink);
+  cudaEventRecord(a);
+  for (int k = 0; k < std::max(iters, 1); ++k)
+    k_chunk_read<4><<<grid, 256>>>(static_cast<const uint32_t*>(dp), nchunks, chunk_bytes / 4,
+                                   pattern, reqs, sink);
+  cudaEventRecord(b);
+  ZC_CUDA_TRY(cudaEventSynchronize(b));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  *gbs = static_cast<double>(reqs) * chunk_bytes * std::max(iters, 1) / (ms * 1e6);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  if (alloc == 0) cudaFreeHost(h);
+  else if (alloc == 1) {
+    if (registered) cudaHostUnregister(h);
+    munmap(h, bytes);
+  } else cudaFree(const_cast<void*>(dp));
+  return ZC_OK;
+}
 
 extern "C" int zc_link_probe(int32_t device, uint64_t bytes, int iters, double* memcpy_gbs,
                              double* zc_gbs, double* hbm_gbs) {

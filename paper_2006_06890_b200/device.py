@@ -304,6 +304,16 @@ def evict(dg: DeviceGraph) -> None:
     dg.evict()
 
 
+def read_probe(nbytes: int, chunk_bytes: int, random: bool, alloc: str = "pinned",
+               device: int = 0, iters: int = 3) -> float:
+    """GB/s of warps reading chunk_bytes per request (zero-copy toy kernel)."""
+    a = {"pinned": 0, "thp": 1, "hbm": 2}[alloc]
+    out = C.c_double()
+    N.check(N.lib().zc_read_probe(device, nbytes, int(random), chunk_bytes, a, iters,
+                                  C.byref(out)))
+    return out.value
+
+
 def link_probe(device: int = 0, nbytes: int = 1 << 30, iters: int = 5) -> dict:
     """Measured host-link and HBM read bandwidths (GB/s)."""
     m, z, h = C.c_double(), C.c_double(), C.c_double()
