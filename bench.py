@@ -52,6 +52,10 @@ def parse():
                    help="skip the naive / merged / UVM / HBM comparison runs")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
+    # test hooks for the partitioned path on a 1-GPU box
+    p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    p.add_argument("--device-override", type=int, default=-1)
+    p.add_argument("--force-partitioned", action="store_true")
     return p.parse_args()
 
 
@@ -107,45 +111,52 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def dist_setup(n_gpus: int):
+def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if args.device_override >= 0:
+        local = args.device_override
+    if world > 1 or args.force_partitioned:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     return rank, world, local
 
 
 def barrier(world: int, device: int):
     import torch
     torch.cuda.synchronize(device)
-    if world > 1:
+    import torch.distributed as dist
+    if dist.is_initialized():
         import torch.distributed as dist
         dist.barrier()
         torch.cuda.synchronize(device)
 
 
-def max_over_ranks(x: float, world: int, device: int) -> float:
-    if world == 1:
-        return x
+def _reduce(x: float, op_name: str) -> float:
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{device}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return x
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if dist.get_backend() == "gloo":
+        dev = torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=getattr(dist.ReduceOp, op_name))
     return float(t.item())
+
+
+def max_over_ranks(x: float, world: int, device: int) -> float:
+    return _reduce(x, "MAX")
 
 
 def sum_over_ranks(x: float, world: int, device: int) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{device}")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    return _reduce(x, "SUM")
 
 
 def load_ncu_summary() -> dict:
@@ -177,7 +188,7 @@ def cpu_baseline(g, sources, threads: int, budget_s: float = 25.0) -> dict:
 
 def main():
     args = parse()
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup(args)
     import numpy as np
 
     if args.impl == "reference" and world > 1 and rank != 0:
@@ -198,41 +209,16 @@ def main():
                     "array)",
               "parallelism": f"replicas{world}" if world > 1 else "single"}
 
+    if args.impl == "reference":
+        return main_reference(args, world, device, config)
+    if world > 1 or args.force_partitioned:
+        return main_partitioned(args, rank, world, device, config)
+
     t0 = time.time()
     dg = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed + rank, device=device)
     gen_s = time.time() - t0
     g = dg.as_csr()
     sources = zc.pick_sources(g, 64, seed=7)
-
-    if args.impl == "reference":
-        threads = args.cpu_threads or os.cpu_count()
-        import oracle
-        per = []
-        edges = 0
-        for i in range(args.warmup + args.steps):
-            s = int(sources[i % len(sources)])
-            t1 = time.perf_counter()
-            r = oracle.bfs(g, s, threads=threads)
-            dt = time.perf_counter() - t1
-            if i >= args.warmup:
-                per.append(dt)
-                edges += sum(r.traversed_edges)
-        total = sum(per)
-        val = edges / total / 1e9
-        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GTEPS",
-                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-                "config": config,
-                "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": threads, "kind": "port",
-                                 "sample": f"{args.steps} full BFS runs of the oracle port "
-                                           "(OpenMP C restatement of traversal.py:98-120; the "
-                                           "reference itself is a Python package that cannot "
-                                           "run on the GPU box)"},
-                "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return
 
     strat = args.strategy
     probe = zc.link_probe(device=device, nbytes=1 << 30, iters=5)
@@ -306,6 +292,133 @@ def main():
         line["variants"] = variants(zc, args, dg, sources, device)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def main_reference(args, world, device, config):
+    """--impl reference: the reference's algorithm on the host cores -- the
+    oracle port (oracle/zc_oracle.c, OpenMP restatement of traversal.py:98-120;
+    the reference itself is a Python package absent from the GPU box) -- on
+    this arm's workload (same graph: scale 27 + log2(N), same sources).  Rank 0
+    only; the input graph is built by the GPU generator (not timed)."""
+    import numpy as np
+    import oracle
+    import paper_2006_06890_b200 as zc
+
+    scale = args.scale + max(0, int(round(np.log2(world))))
+    threads = args.cpu_threads or os.cpu_count()
+    dg = zc.generate_rmat(scale, args.edge_factor, seed=args.seed, device=device)
+    g = dg.as_csr()
+    sources = zc.pick_sources(g, 64, seed=7)
+    per, edges = [], 0
+    for i in range(args.warmup + args.steps):
+        t1 = time.perf_counter()
+        r = oracle.bfs(g, int(sources[i % 64]), threads=threads)
+        dt = time.perf_counter() - t1
+        if i >= args.warmup:
+            per.append(dt)
+            edges += sum(r.traversed_edges)
+    total = sum(per)
+    val = edges / total / 1e9
+    cfg = dict(config)
+    cfg.update({"graph": f"kron{scale}", "scale": scale})
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GTEPS",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": cfg,
+            "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": threads, "kind": "port",
+                             "sample": f"{args.steps} full BFS runs (after {args.warmup} warm-up) "
+                                       "of the oracle port on the whole graph"},
+            "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    dg.close()
+
+
+def main_partitioned(args, rank, world, device, config):
+    """N>1: weak scaling -- Kronecker scale 27 + log2(N) (K29 at N=4, BASELINE
+    configs[4]), vertex-range partitioned, each rank streaming its own 2^31-arc
+    slice over its own host link; NCCL reduce-scatter of the u8 frontier flags
+    (MAX) over NVLink every level."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2006_06890_b200 as zc
+    from paper_2006_06890_b200.multi import (exchange_buffers, generate_rmat_part,
+                                             run_partition)
+
+    scale = args.scale + max(0, int(round(np.log2(world))))
+    stage = args.backend == "gloo"
+    t0 = time.time()
+    part = generate_rmat_part(scale, world, rank, args.edge_factor, seed=args.seed,
+                              device=device)
+    gen_s = time.time() - t0
+    # sources: pick_sources semantics on rank 0's range, broadcast
+    src = torch.zeros(64, dtype=torch.int64)
+    if rank == 0:
+        src = torch.from_numpy(zc.pick_sources(part.graph_view(), 64, seed=7).astype(np.int64))
+    src = src.to(torch.device("cpu") if stage else torch.device("cuda", device))
+    dist.broadcast(src, 0)
+    sources = src.cpu().numpy()
+    bufs = exchange_buffers("bfs", world, part.stride, torch.device("cuda", device))
+    strat = args.strategy
+
+    def one(i, fetch):
+        return run_partition(part, "bfs", int(sources[i % 64]), strat, stage_host=stage,
+                             fetch=fetch, buffers=bufs)
+
+    for i in range(args.warmup):
+        one(i, False)
+    barrier(world, device)
+    trav = 0
+    expand_ms = 0.0
+    with ClockSampler(device) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for i in range(args.steps):
+            r = one(args.warmup + i, False)
+            trav += r.total_traversed_edges
+        ev1.record()
+        torch.cuda.synchronize(device)
+    barrier(world, device)
+    loop_ms = max_over_ranks(ev0.elapsed_time(ev1), world, device)
+    value = trav / (loop_ms * 1e-3) / 1e9  # traversed edges are global (summed over ranks)
+
+    barrier(world, device)
+    t1 = time.perf_counter()
+    d2h = 0
+    for i in range(args.steps):
+        r = one(args.warmup + i, True)
+        d2h += r.values.nbytes
+        del r
+    barrier(world, device)
+    wall = max_over_ranks(time.perf_counter() - t1, world, device)
+    e2e_value = trav / wall / 1e9
+    cfg = dict(config)
+    cfg.update({"workload": f"BFS, Kronecker (R-MAT a=.57 b=.19 c=.19) scale {scale}, edge factor "
+                            f"{args.edge_factor}, {args.edge_factor << scale} directed arcs, "
+                            f"vertex-range partitioned over {world} ranks (edge-balanced), each "
+                            "rank's u32 edge slice zero-copy in pinned host memory",
+                "graph": f"kron{scale}", "scale": scale, "seed": args.seed,
+                "parallelism": f"vertex-partition{world}",
+                "exchange": "per level: reduce-scatter of u8 flags (MAX), all-reduce of counts",
+                "backend": args.backend})
+    line = {"metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": loop_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": cfg,
+            "e2e": {"value": e2e_value, "unit": "GTEPS", "h2d_bytes_per_step": 8,
+                    "d2h_bytes_per_step": int(sum_over_ranks(d2h, world, device)) // args.steps,
+                    "ms_per_step": wall / args.steps * 1e3},
+            "gpu_launches": None,
+            "clocks": clk.summary(),
+            "graph": {"vertices": 1 << scale, "arcs": args.edge_factor << scale,
+                      "local_arcs_rank0": part.graph_view().num_edges, "gen_s": gen_s,
+                      "traversed_edges_per_step": trav / args.steps}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    part.close()
 
 
 def _gteps(zc, dg, sources, strategy, reps=1, evict=False):

@@ -185,6 +185,44 @@ int zc_generate_uniform(uint64_t num_vertices, uint32_t min_degree, uint32_t max
 int zc_link_probe(int32_t device, uint64_t bytes, int iters, double *memcpy_h2d_gbs,
                   double *zerocopy_read_gbs, double *hbm_read_gbs);
 
+/* ---------------------------------------------------------------------------
+ * Vertex-range partitions (multi-GPU; no reference counterpart --
+ * the paper lists multi-GPU as future work).
+ * Rank k owns global vertices [bounds[k], bounds[k+1]) and holds only their
+ * lists (offsets rebased to its edge slice, destinations global), streamed
+ * over its own host link.  One iteration = zc_part_expand (writes candidates
+ * for ANY global vertex into the caller's device exchange buffer of
+ * nparts*stride slots; global w of part j -> slot j*stride + w - bounds[j]),
+ * a reduce-scatter of that buffer by the caller (BFS: u8 flags, MAX; SSSP:
+ * int64 candidate distances, MIN, none = INT64_MAX; CC: int32 candidate
+ * labels, MIN, none = INT32_MAX), and
+ * zc_part_apply with this rank's reduced slice.  Iterates, per-iteration
+ * traversed edges (summed over ranks) and results equal the single-graph run.
+ * ------------------------------------------------------------------------- */
+typedef struct zc_part_info {
+  uint64_t global_vertices;
+  uint64_t stride;         /* slots per part in the exchange buffer (>= max range) */
+  const uint64_t *bounds;  /* nparts + 1 range starts, bounds[nparts] = global V */
+  uint32_t nparts, part;
+} zc_part_info;
+
+/* local: this part's CSR (V = its range, offsets rebased, global destinations). */
+int zc_part_create(const zc_graph_desc *local, const zc_part_info *info, zc_graph **out);
+size_t zc_part_exchange_elem_bytes(int algo); /* algo: 0 bfs, 1 sssp, 2 cc */
+int zc_part_begin(zc_graph *g, int algo, uint64_t source, int strategy, uint64_t *n_local,
+                  uint64_t *traversed_local);
+int zc_part_expand(zc_graph *g, void *exchange /* device pointer */);
+int zc_part_apply(zc_graph *g, const void *mine /* device pointer, stride slots */,
+                  uint64_t *n_next, uint64_t *traversed_next);
+int zc_part_result(zc_graph *g, int64_t *out_local /* range size */, zc_stats *stats);
+/* Part `part` of the directed graph zc_generate_rmat builds with the same
+ * parameters (same arcs, same list order), edge-balanced across nparts;
+ * bounds (nparts+1) receives the vertex ranges of all parts. */
+int zc_generate_rmat_part(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                          uint64_t seed, int64_t wlow, int64_t whigh, uint32_t nparts,
+                          uint32_t part, int32_t placement, int32_t device, uint64_t *bounds,
+                          zc_graph **out);
+
 /* Read microbenchmark (the paper's zero-copy toy kernel):
  * warps read chunk_bytes contiguous bytes per request at consecutive
  * (pattern 0) or random (pattern 1) chunk-aligned offsets of a `bytes`

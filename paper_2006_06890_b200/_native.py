@@ -26,7 +26,9 @@ EXPORTED = (
     "zc_graph_destroy", "zc_graph_host_lists", "zc_graph_info", "zc_bfs", "zc_sssp",
     "zc_cc", "zc_run_log", "zc_host_alloc", "zc_host_free", "zc_generate_rmat",
     "zc_generate_uniform", "zc_link_probe", "zc_set_options", "zc_run_traffic",
-    "zc_run_profile", "zc_graph_evict", "zc_read_probe",
+    "zc_run_profile", "zc_graph_evict", "zc_read_probe", "zc_part_create",
+    "zc_part_exchange_elem_bytes", "zc_part_begin", "zc_part_expand", "zc_part_apply",
+    "zc_part_result", "zc_generate_rmat_part",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -49,6 +51,11 @@ class Stats(C.Structure):
         ("d2h_ms", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
         ("launches", C.c_uint64), ("expand_ms", C.c_double), ("reserved", C.c_uint64 * 6),
     ]
+
+
+class PartInfo(C.Structure):
+    _fields_ = [("global_vertices", C.c_uint64), ("stride", C.c_uint64),
+                ("bounds", C.c_void_p), ("nparts", C.c_uint32), ("part", C.c_uint32)]
 
 
 _lib = None
@@ -87,6 +94,14 @@ def _declare(lib: C.CDLL) -> None:
         "zc_link_probe": (C.c_int, [i32, u64, C.c_int, C.POINTER(dbl), C.POINTER(dbl),
                                     C.POINTER(dbl)]),
         "zc_read_probe": (C.c_int, [i32, u64, C.c_int, u32, C.c_int, C.c_int, C.POINTER(dbl)]),
+        "zc_part_create": (C.c_int, [C.POINTER(GraphDesc), C.POINTER(PartInfo), C.POINTER(P)]),
+        "zc_part_exchange_elem_bytes": (C.c_size_t, [C.c_int]),
+        "zc_part_begin": (C.c_int, [P, C.c_int, u64, C.c_int, C.POINTER(u64), C.POINTER(u64)]),
+        "zc_part_expand": (C.c_int, [P, P]),
+        "zc_part_apply": (C.c_int, [P, P, C.POINTER(u64), C.POINTER(u64)]),
+        "zc_part_result": (C.c_int, [P, P, C.POINTER(Stats)]),
+        "zc_generate_rmat_part": (C.c_int, [u32, u32, dbl, dbl, dbl, u64, i64, i64, u32, u32, i32,
+                                            i32, P, C.POINTER(P)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

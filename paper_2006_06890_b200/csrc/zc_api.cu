@@ -119,6 +119,7 @@ void zc::free_graph(zc_graph* g) {
   cudaFree(g->d_big_val);
   cudaFree(g->d_big_prefix);
   cudaFree(g->d_ctr);
+  cudaFree(g->d_part_lo);
   if (g->h_ctr) cudaFreeHost(g->h_ctr);
   if (g->h_small) cudaFreeHost(g->h_small);
   for (auto& e : g->ev)
@@ -130,8 +131,9 @@ void zc::free_graph(zc_graph* g) {
 
 namespace {
 // Host-side invariant check (csr.py:80-105) on the caller's arrays.
-int validate_desc(const zc_graph_desc* d, bool* negative_weight) {
+int validate_desc(const zc_graph_desc* d, bool* negative_weight, uint64_t dest_limit = 0) {
   const uint64_t nv = d->num_vertices, ne = d->num_edges;
+  const uint64_t dl = dest_limit ? dest_limit : nv;  // edge destinations must be < dl
   if (d->edge_elem_bytes != 4 && d->edge_elem_bytes != 8) {
     set_error("edge_elem_bytes must be 4 or 8, got " + std::to_string(d->edge_elem_bytes));
     return ZC_EINVAL;
@@ -148,7 +150,7 @@ int validate_desc(const zc_graph_desc* d, bool* negative_weight) {
     set_error("src_weight_bytes must be 4 or 8");
     return ZC_EINVAL;
   }
-  if (nv >= 0xffffffffull) {
+  if (nv >= 0xffffffffull || dl >= 0xffffffffull) {
     set_error("device path supports fewer than 2^32-1 vertices");
     return ZC_EINVAL;
   }
@@ -188,10 +190,10 @@ int validate_desc(const zc_graph_desc* d, bool* negative_weight) {
     int b = 0;
     if (d->src_edge_bytes == 8) {
       const int64_t* e = static_cast<const int64_t*>(d->edges);
-      for (uint64_t i = lo; i < hi; ++i) b |= (e[i] < 0) | (static_cast<uint64_t>(e[i]) >= nv);
+      for (uint64_t i = lo; i < hi; ++i) b |= (e[i] < 0) | (static_cast<uint64_t>(e[i]) >= dl);
     } else {
       const uint32_t* e = static_cast<const uint32_t*>(d->edges);
-      for (uint64_t i = lo; i < hi; ++i) b |= (e[i] >= nv);
+      for (uint64_t i = lo; i < hi; ++i) b |= (e[i] >= dl);
     }
     if (b) bad_edge = 1;
     if (d->weights) {
@@ -300,6 +302,19 @@ int zc::alloc_state(zc_graph* g) {
   cudaDeviceProp prop;
   ZC_CUDA_TRY(cudaGetDeviceProperties(&prop, g->device));
   g->num_sms = prop.multiProcessorCount;
+  return ZC_OK;
+}
+
+int zc::init_partition(zc_graph* g, const zc_part_info* info) {
+  DeviceGuard dg(g->device);
+  g->nparts = info->nparts;
+  g->part = info->part;
+  g->global_nv = info->global_vertices;
+  g->lo = info->bounds[info->part];
+  g->stride = info->stride;
+  ZC_CUDA_TRY(cudaMalloc(&g->d_part_lo, (info->nparts + 1) * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMemcpy(g->d_part_lo, info->bounds, (info->nparts + 1) * sizeof(uint64_t),
+                         cudaMemcpyHostToDevice));
   return ZC_OK;
 }
 
@@ -517,14 +532,14 @@ int zc_device_count(int* count) {
   return ZC_OK;
 }
 
-int zc_graph_create(const zc_graph_desc* d, zc_graph** out) {
+static int create_impl(const zc_graph_desc* d, zc_graph** out, uint64_t dest_limit) {
   if (!d || !out) {
     set_error("null argument");
     return ZC_ESTATE;
   }
   *out = nullptr;
   bool neg = false;
-  int rc = validate_desc(d, &neg);
+  int rc = validate_desc(d, &neg, dest_limit);
   if (rc) return rc;
   int ndev = 0;
   ZC_CUDA_TRY(cudaGetDeviceCount(&ndev));
@@ -571,7 +586,215 @@ int zc_graph_create(const zc_graph_desc* d, zc_graph** out) {
   return ZC_OK;
 }
 
+int zc_graph_create(const zc_graph_desc* d, zc_graph** out) { return create_impl(d, out, 0); }
+
 void zc_graph_destroy(zc_graph* g) { free_graph(g); }
+
+// ------------------------------------------------------------ partitions
+int zc_part_create(const zc_graph_desc* local, const zc_part_info* info, zc_graph** out) {
+  if (!info || !info->bounds || !info->nparts || info->part >= info->nparts) {
+    set_error("invalid partition info");
+    return ZC_EINVAL;
+  }
+  const uint64_t gv = info->global_vertices;
+  for (uint32_t k = 0; k < info->nparts; ++k) {
+    if (info->bounds[k] > info->bounds[k + 1] ||
+        info->bounds[k + 1] - info->bounds[k] > info->stride) {
+      set_error("partition bounds must be non-decreasing with ranges <= stride");
+      return ZC_EINVAL;
+    }
+  }
+  if (info->bounds[0] != 0 || info->bounds[info->nparts] != gv ||
+      info->bounds[info->part + 1] - info->bounds[info->part] != local->num_vertices) {
+    set_error("partition bounds do not match the global / local vertex counts");
+    return ZC_EINVAL;
+  }
+  int rc = create_impl(local, out, gv ? gv : 1);
+  if (rc) return rc;
+  rc = init_partition(*out, info);
+  if (rc) {
+    free_graph(*out);
+    *out = nullptr;
+  }
+  return rc;
+}
+
+size_t zc_part_exchange_elem_bytes(int algo) {
+  return algo == kBfs ? 1 : algo == kSssp ? 8 : 4;
+}
+
+int zc_part_begin(zc_graph* g, int algo, uint64_t src, int strategy, uint64_t* n_local,
+                  uint64_t* trav_local) {
+  if (!g || !g->nparts) {
+    set_error("not a partition handle");
+    return ZC_ESTATE;
+  }
+  if (algo < kBfs || algo > kCc || strategy < kNaive || strategy > kMergedAligned) {
+    set_error("unknown algorithm or strategy");
+    return ZC_EINVAL;
+  }
+  if (algo != kCc && src >= g->global_nv) {
+    set_error("source " + std::to_string(src) + " out of range for " +
+              std::to_string(g->global_nv) + " vertices");
+    return ZC_EINVAL;
+  }
+  if (algo == kSssp && !g->has_weights) {
+    set_error("sssp requires edge weights");
+    return ZC_EINVAL;
+  }
+  if (algo == kSssp && g->negative_weight) {
+    set_error("sssp requires non-negative weights");
+    return ZC_EINVAL;
+  }
+  if (algo == kCc && (g->flags & ZC_F_DIRECTED)) {
+    set_error("connected components require an undirected graph "
+              "(load with directed=False or symmetrize first)");
+    return ZC_EINVAL;
+  }
+  if (algo == kCc && g->global_nv > 0x7fffffffull) {
+    set_error("partitioned cc supports fewer than 2^31 vertices");
+    return ZC_EINVAL;
+  }
+  DeviceGuard dg(g->device);
+  cudaStream_t st = g->stream;
+  g->p_algo = algo;
+  g->p_strategy = strategy;
+  g->p_iter = 0;
+  g->p_cur = 0;
+  g->p_launches = 0;
+  g->log_trav.clear();
+  g->log_front.clear();
+  g->log_expand_ms.clear();
+  ZC_CUDA_TRY(cudaMemsetAsync(g->d_flags, 0, g->vpad, st));
+  ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr, 0, kCtrCount * sizeof(uint64_t), st));
+  const bool owned = algo != kCc && src >= g->lo && src < g->lo + g->nv;
+  const uint64_t lsrc = owned ? src - g->lo : 0;
+  ZC_CUDA_TRY(launch_init(algo, g->d_state, g->nv, lsrc, g->d_off, g->d_front[0], g->d_fval[0],
+                          g->d_fs[0], g->d_fd[0], st, &g->p_launches, g->lo, owned));
+  uint64_t n = 0, trav = 0;
+  if (algo == kCc) {
+    n = g->nv;
+    trav = g->ne;
+  } else if (owned) {
+    g->h_small[1] = 0;
+    const size_t sb = algo == kSssp ? 8 : 4;
+    ZC_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(g->d_state) + lsrc * sb, &g->h_small[1], sb,
+                                cudaMemcpyHostToDevice, st));
+    n = 1;
+    trav = g->h_off[lsrc + 1] - g->h_off[lsrc];
+  }
+  ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  g->p_n = n;
+  if (n_local) *n_local = n;
+  if (trav_local) *trav_local = trav;
+  return ZC_OK;
+}
+
+int zc_part_expand(zc_graph* g, void* exch) {
+  if (!g || !g->nparts || g->p_algo < 0) {
+    set_error("zc_part_begin first");
+    return ZC_ESTATE;
+  }
+  DeviceGuard dg(g->device);
+  cudaStream_t st = g->stream;
+  const int algo = g->p_algo;
+  ZC_CUDA_TRY(launch_fill_exchange(algo, exch, g->nparts * g->stride, st, &g->p_launches));
+  ++g->p_iter;
+  g->log_front.push_back(g->p_n);
+  while (g->iter_ev.size() < 2 * g->p_iter) {
+    cudaEvent_t e;
+    ZC_CUDA_TRY(cudaEventCreate(&e));
+    g->iter_ev.push_back(e);
+  }
+  ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (g->p_iter - 1)], st));
+  ExpandArgs a{};
+  a.front = g->d_front[g->p_cur];
+  a.fs = g->d_fs[g->p_cur];
+  a.fd = g->d_fd[g->p_cur];
+  a.fval = g->d_fval[g->p_cur];
+  a.n = g->p_n;
+  a.off = g->d_off;
+  a.edges = g->d_edges;
+  a.weights = g->d_weights;
+  a.state = g->d_state;
+  a.flags = g->d_flags;
+  a.iter = static_cast<uint32_t>(g->p_iter);
+  a.big_s = g->d_big_s;
+  a.big_e = g->d_big_e;
+  a.big_val = g->d_big_val;
+  a.big_prefix = g->d_big_prefix;
+  a.ctr = g->d_ctr;
+  a.exch = exch;
+  a.part_lo = g->d_part_lo;
+  a.nparts = g->nparts;
+  a.stride = g->stride;
+  ZC_CUDA_TRY(launch_expand(g->p_strategy, algo + kPartAlgo, g->eb, g->wb, a, g->num_sms, st,
+                            &g->p_launches));
+  ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (g->p_iter - 1) + 1], st));
+  ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr + kCtrBig, 0, sizeof(uint64_t), st));
+  ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, g->iter_ev[2 * (g->p_iter - 1)], g->iter_ev[2 * (g->p_iter - 1) + 1]);
+  g->log_expand_ms.push_back(ms);
+  return ZC_OK;
+}
+
+int zc_part_apply(zc_graph* g, const void* mine, uint64_t* n_next, uint64_t* trav_next) {
+  if (!g || !g->nparts || g->p_algo < 0 || g->p_iter == 0) {
+    set_error("zc_part_expand first");
+    return ZC_ESTATE;
+  }
+  DeviceGuard dg(g->device);
+  cudaStream_t st = g->stream;
+  const int algo = g->p_algo;
+  ZC_CUDA_TRY(launch_part_apply(algo, mine, g->nv, g->d_state, g->d_flags,
+                                static_cast<uint32_t>(g->p_iter), st, &g->p_launches));
+  CompactArgs c;
+  c.flags = g->d_flags;
+  c.nv = g->nv;
+  c.ntiles = g->ntiles;
+  c.tiles = g->d_tiles;
+  c.front_out = g->d_front[g->p_cur ^ 1];
+  c.fs_out = g->d_fs[g->p_cur ^ 1];
+  c.fd_out = g->d_fd[g->p_cur ^ 1];
+  c.fval_out = g->d_fval[g->p_cur ^ 1];
+  c.off = g->d_off;
+  c.state = g->d_state;
+  c.ctr = g->d_ctr;
+  ZC_CUDA_TRY(launch_compact(algo, c, st, &g->p_launches));
+  ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                              st));
+  ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  g->p_n = g->h_ctr[kCtrNext];
+  g->p_cur ^= 1;
+  if (n_next) *n_next = g->h_ctr[kCtrNext];
+  if (trav_next) *trav_next = g->h_ctr[kCtrTrav];
+  return ZC_OK;
+}
+
+int zc_part_result(zc_graph* g, int64_t* out, zc_stats* stats) {
+  if (!g || !g->nparts || g->p_algo < 0) {
+    set_error("zc_part_begin first");
+    return ZC_ESTATE;
+  }
+  DeviceGuard dg(g->device);
+  cudaStream_t st = g->stream;
+  int64_t* d_out = reinterpret_cast<int64_t*>(g->d_fval[g->p_cur ^ 1]);
+  ZC_CUDA_TRY(launch_widen(g->p_algo, g->d_state, g->nv, d_out, st, &g->p_launches));
+  if (g->nv)
+    ZC_CUDA_TRY(cudaMemcpyAsync(out, d_out, g->nv * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    stats->iterations = g->p_iter;
+    stats->launches = g->p_launches;
+    double ex = 0;
+    for (double x : g->log_expand_ms) ex += x;
+    stats->expand_ms = ex;
+    stats->d2h_bytes = g->nv * sizeof(int64_t);
+  }
+  return ZC_OK;
+}
 
 int zc_graph_host_lists(zc_graph* g, void** edges, void** weights, const int64_t** offsets) {
   if (!g) {

@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <string>
+#include <vector>
 
 #include "zc_graph.cuh"
 #include "zc_internal.cuh"
@@ -119,14 +120,17 @@ __global__ void k_rmat_count(RmatParams p, uint64_t narcs, uint32_t* deg) {
 }
 
 // Warp per (permuted) vertex: its list in CSR order, lanes strided over k.
+// vbase: global id of local vertex 0 (partition generation fills one range).
 template <typename ET>
-__global__ void k_rmat_fill(RmatParams p, uint64_t nv, const uint64_t* off, ET* edges) {
+__global__ void k_rmat_fill(RmatParams p, uint64_t nv, const uint64_t* off, ET* edges,
+                            uint64_t vbase = 0) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t v = gw; v < nv; v += nw) {
-    const uint64_t s = off[v], e = off[v + 1];
+  for (uint64_t lv = gw; lv < nv; lv += nw) {
+    const uint64_t s = off[lv], e = off[lv + 1];
     if (s == e) continue;
+    const uint64_t v = vbase + lv;
     const uint64_t src_old = p.perm.inv(v);
     for (uint64_t k = s + lane; k < e; k += 32) {
       const uint64_t d_old = rmat_dst(p, src_old, (v << 24) ^ (k - s) ^ (k << 40));
@@ -290,11 +294,12 @@ __global__ void k_uniform_deg(uint64_t nv, uint64_t seed, uint32_t lo, uint32_t 
     deg[v] = lo + static_cast<uint32_t>(hash3(seed, 1, v) % span);
 }
 
-__global__ void k_weights(uint64_t ne, uint64_t seed, int64_t lo, int64_t hi, uint32_t* w) {
+__global__ void k_weights(uint64_t ne, uint64_t seed, int64_t lo, int64_t hi, uint32_t* w,
+                          uint64_t ebase = 0) {
   const uint64_t span = static_cast<uint64_t>(hi - lo) + 1;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne;
        i += (uint64_t)gridDim.x * blockDim.x)
-    w[i] = static_cast<uint32_t>(lo + static_cast<int64_t>(hash3(seed, 3, i) % span));
+    w[i] = static_cast<uint32_t>(lo + static_cast<int64_t>(hash3(seed, 3, ebase + i) % span));
 }
 
 constexpr int kGenGrid = 148 * 16;
@@ -366,14 +371,19 @@ zc_graph* new_handle(int32_t placement, int32_t device, uint32_t flags) {
   return g;
 }
 
-int attach_weights(zc_graph* g, uint64_t seed, int64_t wlow, int64_t whigh) {
+int attach_weights_range(zc_graph* g, uint64_t seed, int64_t wlow, int64_t whigh,
+                         uint64_t ebase) {
   if (wlow > whigh) return ZC_OK;
   uint32_t* d_w = nullptr;
   ZC_CUDA_TRY(cudaMalloc(&d_w, std::max<uint64_t>(g->ne, 32) * sizeof(uint32_t)));
-  if (g->ne) k_weights<<<kGenGrid, 256>>>(g->ne, seed, wlow, whigh, d_w);
+  if (g->ne) k_weights<<<kGenGrid, 256>>>(g->ne, seed, wlow, whigh, d_w, ebase);
   ZC_CUDA_TRY(cudaGetLastError());
   g->has_weights = true;
   return adopt_device_list(g, d_w, 4, g->ne, &g->h_weights, &g->d_weights, &g->hbm_weights);
+}
+
+int attach_weights(zc_graph* g, uint64_t seed, int64_t wlow, int64_t whigh) {
+  return attach_weights_range(g, seed, wlow, whigh, 0);
 }
 
 int check_common(int32_t placement, int32_t device, int64_t wlow, int64_t whigh) {
@@ -391,6 +401,125 @@ int check_common(int32_t placement, int32_t device, int64_t wlow, int64_t whigh)
     set_error("weights must lie in [0, 2^32)");
     return ZC_EINVAL;
   }
+  return ZC_OK;
+}
+
+RmatParams rmat_params(uint32_t scale, double a, double b, double c, uint64_t seed) {
+  const double d = 1.0 - a - b - c;
+  RmatParams p;
+  p.scale = scale;
+  p.thr_src = static_cast<uint32_t>((c + d) * 65536.0 + 0.5);
+  p.thr_dst0 = static_cast<uint32_t>(b / (a + b) * 65536.0 + 0.5);
+  p.thr_dst1 = (c + d) > 0 ? static_cast<uint32_t>(d / (c + d) * 65536.0 + 0.5) : 0;
+  p.seed = seed;
+  p.perm.bits = scale;
+  p.perm.half = (scale + 1) / 2;
+  p.perm.key = mix64(seed ^ 0x5eedull);
+  return p;
+}
+
+// One edge-balanced vertex range of the directed R-MAT graph generate_rmat
+// would build with the same parameters (the same arcs, lists and order).
+int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c, uint64_t seed,
+                       int64_t wlow, int64_t whigh, uint32_t nparts, uint32_t part,
+                       int32_t placement, int32_t device, uint64_t* bounds, zc_graph** out) {
+  *out = nullptr;
+  int rc = check_common(placement, device, wlow, whigh);
+  if (rc) return rc;
+  if (scale < 1 || scale > 31 || ef < 1 || a <= 0 || b < 0 || c < 0 || 1.0 - a - b - c < 0 ||
+      nparts < 1 || part >= nparts || !bounds) {
+    set_error("invalid rmat partition parameters");
+    return ZC_EINVAL;
+  }
+  cudaSetDevice(device);
+  const uint64_t nv = 1ull << scale;
+  const uint64_t narcs = static_cast<uint64_t>(ef) << scale;
+  const RmatParams p = rmat_params(scale, a, b, c, seed);
+  // global degrees -> global offsets (identical on every rank)
+  uint32_t* d_deg = nullptr;
+  uint64_t* d_goff = nullptr;
+  if (cudaMalloc(&d_deg, nv * sizeof(uint32_t)) != cudaSuccess) {
+    set_error("out of device memory");
+    return ZC_ENOMEM;
+  }
+  cudaMemset(d_deg, 0, nv * sizeof(uint32_t));
+  k_rmat_count<<<kGenGrid, 256>>>(p, narcs, d_deg);
+  ZC_CUDA_TRY(cudaMalloc(&d_goff, (nv + 1) * sizeof(uint64_t)));
+  {
+    const size_t tb = scan_tmp_bytes(nv);
+    void* tmp = nullptr;
+    ZC_CUDA_TRY(cudaMalloc(&tmp, tb));
+    ZC_CUDA_TRY(scan_u32_to_u64(d_deg, d_goff, nv, tmp, tb, 0));
+    ZC_CUDA_TRY(cudaFree(tmp));
+  }
+  ZC_CUDA_TRY(cudaFree(d_deg));
+  // edge-balanced bounds: first vertex whose offset reaches E*k/nparts
+  std::vector<uint64_t> cut(nparts + 1);
+  cut[0] = 0;
+  cut[nparts] = nv;
+  for (uint32_t k = 1; k < nparts; ++k) {
+    const uint64_t target = static_cast<uint64_t>(static_cast<double>(narcs) * k / nparts);
+    uint64_t lo = 0, hi = nv;  // smallest v with goff[v] >= target
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) / 2;
+      uint64_t val = 0;
+      ZC_CUDA_TRY(cudaMemcpy(&val, d_goff + mid, sizeof(val), cudaMemcpyDeviceToHost));
+      if (val >= target) hi = mid; else lo = mid + 1;
+    }
+    cut[k] = std::max(lo, cut[k - 1]);
+  }
+  for (uint32_t k = 0; k <= nparts; ++k) bounds[k] = cut[k];
+  const uint64_t lo = cut[part], hi = cut[part + 1], nl = hi - lo;
+  uint64_t e0 = 0, e1 = 0;
+  ZC_CUDA_TRY(cudaMemcpy(&e0, d_goff + lo, sizeof(e0), cudaMemcpyDeviceToHost));
+  ZC_CUDA_TRY(cudaMemcpy(&e1, d_goff + hi, sizeof(e1), cudaMemcpyDeviceToHost));
+
+  zc_graph* g = new_handle(placement, device, ZC_F_DIRECTED);
+  auto fail = [&](int code) {
+    cudaFree(d_goff);
+    free_graph(g);
+    return code;
+  };
+  g->nv = nl;
+  g->ne = e1 - e0;
+  if (cudaHostAlloc(&g->h_off, (nl + 1) * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess) {
+    set_error("cannot allocate pinned offsets");
+    return fail(ZC_ENOMEM);
+  }
+  ZC_CUDA_TRY(cudaMemcpy(g->h_off, d_goff + lo, (nl + 1) * sizeof(uint64_t),
+                         cudaMemcpyDeviceToHost));
+  for (uint64_t v = 0; v <= nl; ++v) g->h_off[v] -= static_cast<int64_t>(e0);
+  uint64_t* d_loff = nullptr;
+  uint32_t* d_edges = nullptr;
+  if (cudaMalloc(&d_loff, (nl + 1) * sizeof(uint64_t)) != cudaSuccess ||
+      cudaMalloc(&d_edges, std::max<uint64_t>(g->ne, 32) * sizeof(uint32_t)) != cudaSuccess) {
+    set_error("out of device memory");
+    return fail(ZC_ENOMEM);
+  }
+  ZC_CUDA_TRY(cudaMemcpy(d_loff, g->h_off, (nl + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  cudaFree(d_goff);
+  d_goff = nullptr;
+  k_rmat_fill<uint32_t><<<kGenGrid, 256>>>(p, nl, d_loff, d_edges, lo);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    set_error(std::string("rmat fill: ") + cudaGetErrorString(cudaGetLastError()));
+    return fail(ZC_ECUDA);
+  }
+  cudaFree(d_loff);
+  if ((rc = adopt_device_list(g, d_edges, 4, g->ne, &g->h_edges, &g->d_edges, &g->hbm_edges)))
+    return fail(rc);
+  if ((rc = attach_weights_range(g, seed ^ 0x77ull, wlow, whigh, e0))) return fail(rc);
+  if ((rc = alloc_state(g))) return fail(rc);
+  zc_part_info info;
+  info.global_vertices = nv;
+  info.bounds = bounds;
+  info.nparts = nparts;
+  info.part = part;
+  uint64_t stride = 1;
+  for (uint32_t k = 0; k < nparts; ++k) stride = std::max(stride, cut[k + 1] - cut[k]);
+  info.stride = stride;
+  if ((rc = init_partition(g, &info))) return fail(rc);
+  if ((rc = finish_create(g))) return fail(rc);
+  *out = g;
   return ZC_OK;
 }
 
@@ -412,15 +541,7 @@ int generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uin
     set_error("degree overflow");
     return ZC_EINVAL;
   }
-  RmatParams p;
-  p.scale = scale;
-  p.thr_src = static_cast<uint32_t>((c + d) * 65536.0 + 0.5);
-  p.thr_dst0 = static_cast<uint32_t>(b / (a + b) * 65536.0 + 0.5);
-  p.thr_dst1 = (c + d) > 0 ? static_cast<uint32_t>(d / (c + d) * 65536.0 + 0.5) : 0;
-  p.seed = seed;
-  p.perm.bits = scale;
-  p.perm.half = (scale + 1) / 2;
-  p.perm.key = mix64(seed ^ 0x5eedull);
+  const RmatParams p = rmat_params(scale, a, b, c, seed);
 
   zc_graph* g = new_handle(placement, device, symmetrize ? 0u : ZC_F_DIRECTED);
   auto fail = [&](int code) {
@@ -543,4 +664,13 @@ extern "C" int zc_generate_uniform(uint64_t num_vertices, uint32_t min_degree, u
   if (!out) return ZC_ESTATE;
   return zc::generate_uniform(num_vertices, min_degree, max_degree, seed, wlow, whigh, placement,
                               device, out);
+}
+
+extern "C" int zc_generate_rmat_part(uint32_t scale, uint32_t edge_factor, double a, double b,
+                                     double c, uint64_t seed, int64_t wlow, int64_t whigh,
+                                     uint32_t nparts, uint32_t part, int32_t placement,
+                                     int32_t device, uint64_t* bounds, zc_graph** out) {
+  if (!out) return ZC_ESTATE;
+  return zc::generate_rmat_part(scale, edge_factor, a, b, c, seed, wlow, whigh, nparts, part,
+                                placement, device, bounds, out);
 }

@@ -54,6 +54,13 @@ struct zc_graph {
   std::vector<double> log_expand_ms;
   std::vector<cudaEvent_t> iter_ev;  // 2 per iteration, grown on demand
   uint32_t options = 0;
+  // vertex-range partition (multi-GPU); nparts == 0 for a whole graph
+  uint32_t nparts = 0, part = 0;
+  uint64_t global_nv = 0, lo = 0, stride = 0;
+  uint64_t* d_part_lo = nullptr;  // nparts + 1
+  // stepped run state (zc_part_begin / expand / apply)
+  int p_algo = -1, p_strategy = 0, p_cur = 0;
+  uint64_t p_iter = 0, p_n = 0, p_launches = 0;
 };
 
 
@@ -62,6 +69,7 @@ namespace zc {
 void free_graph(zc_graph* g);
 int alloc_state(zc_graph* g);
 int finish_create(zc_graph* g);  // prefetch (UVM) + sync
+int init_partition(zc_graph* g, const zc_part_info* info);
 // Adopt a list generated in HBM (d_src, n elements of width w) into the
 // handle's placement; frees d_src unless it becomes the HBM copy.
 int adopt_device_list(zc_graph* g, void* d_src, uint32_t w, uint64_t n, void** h,

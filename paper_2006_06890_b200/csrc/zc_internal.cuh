@@ -36,12 +36,26 @@ constexpr int kTileThreads = 256;
 constexpr int kTileVerts = kTileThreads * 16;  // 16 flag bytes (one uint4) per thread
 constexpr uint32_t kUnreached32 = 0xffffffffu;
 constexpr uint64_t kUnreached64 = ~0ull;
+// "no candidate" in the partition exchange buffers: signed maxima, so the
+// buffers reduce correctly as int64 / int32 MIN in NCCL and gloo.
+constexpr uint64_t kExchNone64 = 0x7fffffffffffffffull;
+constexpr uint32_t kExchNone32 = 0x7fffffffu;
 // A frontier vertex whose list needs more than kBigSteps warp steps is not
 // expanded by its chunk warp but queued and split across all warps.
 constexpr uint32_t kBigSteps = 16;
 
 enum Strategy : int { kNaive = 0, kMerged = 1, kMergedAligned = 2 };
 enum Algo : int { kBfs = 0, kSssp = 1, kCc = 2 };
+// Partitioned (multi-GPU) variants: the visit writes candidates for any
+// global vertex into the exchange buffer instead of updating local state.
+constexpr int kPartAlgo = 3;  // algo + kPartAlgo
+template <int A>
+struct AlgoTraits {
+  static constexpr int base = A % kPartAlgo;
+  static constexpr bool part = A >= kPartAlgo;
+  static constexpr bool has_val = base != kBfs;  // frontier carries a value
+  static constexpr bool weighted = base == kSssp;
+};
 
 // device counter slots
 enum Ctr : int {
@@ -70,6 +84,12 @@ struct ExpandArgs {
   uint64_t* big_val;      //   snapshot value
   uint64_t* big_prefix;   // exclusive prefix of big-list steps (nbig+1)
   uint64_t* ctr;          // device counters
+  // partitioned mode: exchange buffer of nparts * stride slots; global
+  // vertex w of part k lives in slot k * stride + (w - part_lo[k])
+  void* exch;
+  const uint64_t* part_lo;  // nparts + 1 range starts (device)
+  uint32_t nparts;
+  uint64_t stride;
 };
 
 struct CompactArgs {
@@ -97,7 +117,15 @@ cudaError_t launch_traffic_model(int strategy, int edge_bytes, int weight_bytes,
 cudaError_t launch_compact(int algo, const CompactArgs& c, cudaStream_t st, uint64_t* launches);
 cudaError_t launch_init(int algo, void* state, uint64_t nv, uint64_t src, const uint64_t* off,
                         uint32_t* front, uint64_t* fval, uint64_t* fs, uint32_t* fd,
-                        cudaStream_t st, uint64_t* launches);
+                        cudaStream_t st, uint64_t* launches, uint64_t label_base = 0,
+                        bool with_source = true);
+// Partitioned mode: owner-side merge of this part's reduced exchange slice
+// (BFS: flags / SSSP: u64 candidates / CC: u32 candidates) into the local
+// state, marking improved vertices for the compaction.
+cudaError_t launch_fill_exchange(int algo, void* x, uint64_t n, cudaStream_t st,
+                                 uint64_t* launches);
+cudaError_t launch_part_apply(int algo, const void* mine, uint64_t nlocal, void* state,
+                              uint8_t* flags, uint32_t iter, cudaStream_t st, uint64_t* launches);
 cudaError_t launch_widen(int algo, const void* state, uint64_t nv, int64_t* out, cudaStream_t st,
                          uint64_t* launches);
 cudaError_t launch_check_edges(const void* edges, int edge_bytes, uint64_t ne, uint64_t nv,

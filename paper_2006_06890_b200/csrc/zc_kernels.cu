@@ -101,6 +101,44 @@ struct Visit<kCc> {
   }
 };
 
+// Slot of global vertex w in the exchange buffer (partitioned mode).
+__device__ __forceinline__ uint64_t part_slot(const ExpandArgs& a, uint64_t w) {
+  uint32_t lo = 0, hi = a.nparts;  // part_lo[lo] <= w < part_lo[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a.part_lo[mid] <= w) lo = mid; else hi = mid;
+  }
+  return lo * a.stride + (w - a.part_lo[lo]);
+}
+
+template <>
+struct Visit<kBfs + kPartAlgo> {
+  static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
+                                               uint64_t) {
+    static_cast<uint8_t*>(a.exch)[part_slot(a, w)] = 1;
+  }
+};
+
+template <>
+struct Visit<kSssp + kPartAlgo> {
+  static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t wt,
+                                               uint64_t val) {
+    unsigned long long* x = static_cast<unsigned long long*>(a.exch) + part_slot(a, w);
+    const unsigned long long cand = val + wt;
+    if (cand < *x) atomicMin(x, cand);
+  }
+};
+
+template <>
+struct Visit<kCc + kPartAlgo> {
+  static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
+                                               uint64_t val) {
+    unsigned* x = static_cast<unsigned*>(a.exch) + part_slot(a, w);
+    const unsigned cand = static_cast<unsigned>(val);
+    if (cand < *x) atomicMin(x, cand);
+  }
+};
+
 template <typename ET>
 struct LineElems {
   static constexpr uint64_t value = kLineBytes / sizeof(ET);
@@ -127,7 +165,9 @@ template <int ALGO, typename ET, typename WT>
 __device__ __forceinline__ void visit_batch(const ExpandArgs& a, const Batch<ALGO, ET, WT>& b) {
 #pragma unroll
   for (int u = 0; u < kUnroll; ++u)
-    if (b.ok[u]) Visit<ALGO>::apply(a, b.dst[u], ALGO == kSssp ? uint64_t(b.wt[u]) : 0, b.sval[u]);
+    if (b.ok[u])
+      Visit<ALGO>::apply(a, b.dst[u], AlgoTraits<ALGO>::weighted ? uint64_t(b.wt[u]) : 0,
+                         b.sval[u]);
 }
 
 // Per-lane metadata of one 32-slot chunk of the frontier.
@@ -143,7 +183,7 @@ __device__ __forceinline__ Chunk load_chunk(const ExpandArgs& a, uint64_t c0, in
   if (j < a.n) {
     c.s = a.fs[j];
     c.e = c.s + a.fd[j];
-    if (ALGO != kBfs) c.val = a.fval[j];
+    if (AlgoTraits<ALGO>::has_val) c.val = a.fval[j];
   }
   return c;
 }
@@ -177,7 +217,7 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_warp(ExpandArgs a) {
             atomicAdd(reinterpret_cast<unsigned long long*>(a.ctr + kCtrBig), 1ull);
         a.big_s[slot] = c.s;
         a.big_e[slot] = c.e;
-        if (ALGO != kBfs) a.big_val[slot] = c.val;
+        if (AlgoTraits<ALGO>::has_val) a.big_val[slot] = c.val;
         a.big_prefix[slot] = steps;
       } else {
         nst = static_cast<uint32_t>(steps);
@@ -207,12 +247,12 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_warp(ExpandArgs a) {
           const uint64_t sk = __shfl_sync(kFull, c.s, k);
           const uint64_t ek = __shfl_sync(kFull, c.e, k);
           const uint32_t t = q - __shfl_sync(kFull, excl, k);
-          if (ALGO != kBfs) b.sval[u] = __shfl_sync(kFull, c.val, k);
+          if (AlgoTraits<ALGO>::has_val) b.sval[u] = __shfl_sync(kFull, c.val, k);
           const uint64_t idx = bk + static_cast<uint64_t>(t) * kWarp + lane;
           b.ok[u] = idx >= sk && idx < ek;
           if (b.ok[u]) {
             b.dst[u] = ld_list(E + idx);
-            if (ALGO == kSssp) b.wt[u] = ld_list(W + idx);
+            if (AlgoTraits<ALGO>::weighted) b.wt[u] = ld_list(W + idx);
           }
         }
       }
@@ -257,7 +297,7 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_big(ExpandArgs a) {
   uint64_t p_i = a.big_prefix[i], p_next = a.big_prefix[i + 1];
   uint64_t s = a.big_s[i], e = a.big_e[i];
   uint64_t b = window_base<STRAT, ET>(s);
-  uint64_t val = ALGO != kBfs ? a.big_val[i] : 0;
+  uint64_t val = AlgoTraits<ALGO>::has_val ? a.big_val[i] : 0;
 
   auto issue = [&](Batch<ALGO, ET, WT>& bt, uint64_t q0) {
 #pragma unroll
@@ -273,14 +313,14 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_big(ExpandArgs a) {
           s = a.big_s[i];
           e = a.big_e[i];
           b = window_base<STRAT, ET>(s);
-          if (ALGO != kBfs) val = a.big_val[i];
+          if (AlgoTraits<ALGO>::has_val) val = a.big_val[i];
         }
         bt.sval[u] = val;
         const uint64_t idx = b + (q - p_i) * kWarp + lane;
         bt.ok[u] = idx >= s && idx < e;
         if (bt.ok[u]) {
           bt.dst[u] = ld_list(E + idx);
-          if (ALGO == kSssp) bt.wt[u] = ld_list(W + idx);
+          if (AlgoTraits<ALGO>::weighted) bt.wt[u] = ld_list(W + idx);
         }
       }
     }
@@ -346,10 +386,10 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_naive(ExpandArgs a) {
   const WT* __restrict__ W = static_cast<const WT*>(a.weights);
   for (uint64_t j = tid; j < a.n; j += nt) {
     const uint64_t s = a.fs[j], e = s + a.fd[j];
-    const uint64_t val = ALGO != kBfs ? a.fval[j] : 0;
+    const uint64_t val = AlgoTraits<ALGO>::has_val ? a.fval[j] : 0;
     for (uint64_t k = s; k < e; ++k) {
       const ET w = ld_list(E + k);
-      const uint64_t wt = ALGO == kSssp ? uint64_t(ld_list(W + k)) : 0;
+      const uint64_t wt = AlgoTraits<ALGO>::weighted ? uint64_t(ld_list(W + k)) : 0;
       Visit<ALGO>::apply(a, w, wt, val);
     }
   }
@@ -608,12 +648,12 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
 
 // ---------------------------------------------------------------- helpers
 __global__ void k_init_cc(uint32_t* label, uint64_t nv, uint32_t* front, uint64_t* fval,
-                          const uint64_t* off, uint64_t* fs, uint32_t* fd) {
+                          const uint64_t* off, uint64_t* fs, uint32_t* fd, uint64_t base) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
        v += (uint64_t)gridDim.x * blockDim.x) {
-    label[v] = static_cast<uint32_t>(v);
+    label[v] = static_cast<uint32_t>(base + v);
     front[v] = static_cast<uint32_t>(v);
-    fval[v] = v;
+    fval[v] = base + v;
     const uint64_t s0 = off[v];
     fs[v] = s0;
     fd[v] = static_cast<uint32_t>(off[v + 1] - s0);
@@ -627,6 +667,43 @@ __global__ void k_init_source(uint64_t src, const uint64_t* off, uint32_t* front
   fval[0] = 0;
   fs[0] = off[src];
   fd[0] = static_cast<uint32_t>(off[src + 1] - off[src]);
+}
+
+__global__ void k_fill_exchange(void* x, uint64_t n, int elem_bytes) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (elem_bytes == 8) static_cast<uint64_t*>(x)[i] = kExchNone64;
+    else static_cast<uint32_t*>(x)[i] = kExchNone32;
+  }
+}
+
+template <int ALGO>
+__global__ void k_part_apply(const void* mine, uint64_t n, void* state, uint8_t* flags,
+                             uint32_t iter) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    if (ALGO == kBfs) {
+      uint32_t* level = static_cast<uint32_t*>(state);
+      if (static_cast<const uint8_t*>(mine)[v] && level[v] == kUnreached32) {
+        level[v] = iter;
+        flags[v] = 1;
+      }
+    } else if (ALGO == kSssp) {
+      uint64_t* dist = static_cast<uint64_t*>(state);
+      const uint64_t m = static_cast<const uint64_t*>(mine)[v];
+      if (m != kExchNone64 && m < dist[v]) {
+        dist[v] = m;
+        flags[v] = 1;
+      }
+    } else {
+      uint32_t* label = static_cast<uint32_t*>(state);
+      const uint32_t m = static_cast<const uint32_t*>(mine)[v];
+      if (m < label[v]) {
+        label[v] = m;
+        flags[v] = 1;
+      }
+    }
+  }
 }
 
 template <int ALGO>
@@ -775,11 +852,12 @@ cudaError_t expand_t(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t
 template <int STRAT, int ALGO>
 cudaError_t expand_w(int eb, int wb, const ExpandArgs& a, int num_sms, cudaStream_t st,
                      uint64_t* l) {
+  constexpr bool W = AlgoTraits<ALGO>::weighted;
   if (eb == 4) {
-    if (ALGO == kSssp && wb == 8) return expand_t<STRAT, ALGO, uint32_t, uint64_t>(a, num_sms, st, l);
+    if (W && wb == 8) return expand_t<STRAT, ALGO, uint32_t, uint64_t>(a, num_sms, st, l);
     return expand_t<STRAT, ALGO, uint32_t, uint32_t>(a, num_sms, st, l);
   }
-  if (ALGO == kSssp && wb == 8) return expand_t<STRAT, ALGO, uint64_t, uint64_t>(a, num_sms, st, l);
+  if (W && wb == 8) return expand_t<STRAT, ALGO, uint64_t, uint64_t>(a, num_sms, st, l);
   return expand_t<STRAT, ALGO, uint64_t, uint32_t>(a, num_sms, st, l);
 }
 
@@ -789,7 +867,10 @@ cudaError_t expand_a(int algo, int eb, int wb, const ExpandArgs& a, int num_sms,
   switch (algo) {
     case kBfs: return expand_w<STRAT, kBfs>(eb, wb, a, num_sms, st, l);
     case kSssp: return expand_w<STRAT, kSssp>(eb, wb, a, num_sms, st, l);
-    default: return expand_w<STRAT, kCc>(eb, wb, a, num_sms, st, l);
+    case kCc: return expand_w<STRAT, kCc>(eb, wb, a, num_sms, st, l);
+    case kBfs + kPartAlgo: return expand_w<STRAT, kBfs + kPartAlgo>(eb, wb, a, num_sms, st, l);
+    case kSssp + kPartAlgo: return expand_w<STRAT, kSssp + kPartAlgo>(eb, wb, a, num_sms, st, l);
+    default: return expand_w<STRAT, kCc + kPartAlgo>(eb, wb, a, num_sms, st, l);
   }
 }
 
@@ -838,18 +919,43 @@ cudaError_t launch_compact(int algo, const CompactArgs& c, cudaStream_t st, uint
 
 cudaError_t launch_init(int algo, void* state, uint64_t nv, uint64_t src, const uint64_t* off,
                         uint32_t* front, uint64_t* fval, uint64_t* fs, uint32_t* fd,
-                        cudaStream_t st, uint64_t* launches) {
+                        cudaStream_t st, uint64_t* launches, uint64_t label_base,
+                        bool with_source) {
   if (algo == kCc) {
     if (nv == 0) return cudaSuccess;
     const int g = grid_for(nv, 256, 148, 16);
-    k_init_cc<<<g, 256, 0, st>>>(static_cast<uint32_t*>(state), nv, front, fval, off, fs, fd);
+    k_init_cc<<<g, 256, 0, st>>>(static_cast<uint32_t*>(state), nv, front, fval, off, fs, fd,
+                                 label_base);
     *launches += 1;
     return cudaGetLastError();
   }
   const size_t bytes = nv * (algo == kSssp ? 8 : 4);
   cudaError_t e = cudaMemsetAsync(state, 0xff, bytes, st);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || !with_source) return e;
   k_init_source<<<1, 1, 0, st>>>(src, off, front, fval, fs, fd);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_exchange(int algo, void* x, uint64_t n, cudaStream_t st,
+                                 uint64_t* launches) {
+  if (algo == kBfs) return cudaMemsetAsync(x, 0, n, st);
+  if (n == 0) return cudaSuccess;
+  const int g = grid_for(n, 256, 148, 16);
+  k_fill_exchange<<<g, 256, 0, st>>>(x, n, algo == kSssp ? 8 : 4);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_part_apply(int algo, const void* mine, uint64_t nlocal, void* state,
+                              uint8_t* flags, uint32_t iter, cudaStream_t st, uint64_t* launches) {
+  if (nlocal == 0) return cudaSuccess;
+  const int g = grid_for(nlocal, 256, 148, 16);
+  switch (algo) {
+    case kBfs: k_part_apply<kBfs><<<g, 256, 0, st>>>(mine, nlocal, state, flags, iter); break;
+    case kSssp: k_part_apply<kSssp><<<g, 256, 0, st>>>(mine, nlocal, state, flags, iter); break;
+    default: k_part_apply<kCc><<<g, 256, 0, st>>>(mine, nlocal, state, flags, iter); break;
+  }
   *launches += 1;
   return cudaGetLastError();
 }

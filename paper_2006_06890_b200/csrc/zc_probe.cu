@@ -65,7 +65,17 @@ __global__ void __launch_bounds__(256) k_chunk_read(const uint32_t* __restrict__
       v[u] = 0;
       if (r < total_reqs) {
         uint64_t c = r % nchunks;
-        if (random) {
+        if (random == 2) {  // one contiguous stream per warp
+          const uint64_t per = (total_reqs + nw - 1) / nw;
+          const uint64_t wi = r / kU / nw, lane_u = r % kU;  // r = (wi*nw + gw)*kU + u
+          c = (gw * per + wi * kU + lane_u) % nchunks;
+        } else if (random == 3) {  // one contiguous stream per CTA, warps interleaved
+          const uint64_t wpc = blockDim.x >> 5, ncta = gridDim.x;
+          const uint64_t per = (total_reqs + ncta - 1) / ncta;
+          const uint64_t wi = r / kU / nw, lane_u = r % kU;
+          const uint64_t wl = gw % wpc;
+          c = (blockIdx.x * per + (wi * wpc + wl) * kU + lane_u) % nchunks;
+        } else if (random) {
           uint64_t z = r * 0x9e3779b97f4a7c15ull;
           z ^= z >> 31;
           z *= 0xbf58476d1ce4e5b9ull;

@@ -304,7 +304,7 @@ def evict(dg: DeviceGraph) -> None:
     dg.evict()
 
 
-def read_probe(nbytes: int, chunk_bytes: int, random: bool, alloc: str = "pinned",
+def read_probe(nbytes: int, chunk_bytes: int, random, alloc: str = "pinned",
                device: int = 0, iters: int = 3) -> float:
     """GB/s of warps reading chunk_bytes per request (zero-copy toy kernel)."""
     a = {"pinned": 0, "thp": 1, "hbm": 2}[alloc]

@@ -1,0 +1,298 @@
+"""Vertex-range partitioned BFS / SSSP / CC across GPUs.
+
+One process per GPU (``torch.distributed``, NCCL over NVLink).  Rank k owns
+the global vertices [bounds[k], bounds[k+1]) -- ranges cut so every rank
+holds ~E/p edges -- and keeps only their lists in its pinned host memory, so
+each GPU streams its own edge slice over its own host link.  Per iteration:
+
+1. ``expand``: the rank's CUDA kernels read its frontier's lists (zero-copy)
+   and write a candidate for every touched global vertex into a dense
+   exchange buffer of ``nparts * stride`` slots (BFS: u8 "discovered" flags;
+   SSSP: int64 candidate distances; CC: int32 candidate labels);
+2. ``reduce_scatter`` (MAX for the flags -- NCCL has no bitwise OR --, MIN
+   for distances / labels) delivers to every owner the merged candidates of
+   its own range;
+3. ``apply``: the owner merges them into its state (Jacobi: candidates were
+   computed from start-of-iteration values) and compacts its next frontier;
+4. ``all_reduce`` of (frontier size, traversed edges) decides termination.
+
+Because every step is the reference's level-synchronous / Jacobi iteration
+(traversal.py:98-179), values, iteration counts and per-iteration traversed
+edges (summed over ranks) are identical to the single-GPU run.
+
+The reference has no multi-device code (PAPER.md:1051-1054 lists
+multi-GPU as future work).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Protocol, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .access import strategy_id
+from .csr import CsrGraph
+
+ALGO_IDS = {"bfs": 0, "sssp": 1, "cc": 2}
+# exchange element types (numpy names; torch dtypes resolved lazily)
+EXCH_NP = {"bfs": np.uint8, "sssp": np.int64, "cc": np.int32}
+EXCH_NONE = {"bfs": 0, "sssp": np.iinfo(np.int64).max, "cc": np.iinfo(np.int32).max}
+
+
+def edge_balanced_bounds(offsets: np.ndarray, nparts: int) -> np.ndarray:
+    """nparts+1 vertex boundaries cutting the CSR at ~E*k/nparts edges."""
+    off = np.asarray(offsets)
+    nv = off.size - 1
+    ne = int(off[-1])
+    if nparts < 1:
+        raise ValueError("nparts must be >= 1")
+    targets = (np.arange(1, nparts, dtype=np.float64) * ne / nparts).astype(np.int64)
+    cuts = np.searchsorted(off, targets, side="left")
+    bounds = np.concatenate(([0], np.minimum(cuts, nv), [nv])).astype(np.uint64)
+    return np.maximum.accumulate(bounds)
+
+
+def exchange_stride(bounds: np.ndarray) -> int:
+    return max(1, int(np.max(np.diff(np.asarray(bounds, dtype=np.int64)))))
+
+
+def local_part(g, bounds: np.ndarray, part: int) -> CsrGraph:
+    """Part `part` of g: its vertex range, offsets rebased, global destinations."""
+    lo, hi = int(bounds[part]), int(bounds[part + 1])
+    off = np.asarray(g.offsets)
+    e0, e1 = int(off[lo]), int(off[hi])
+    loc_off = (off[lo:hi + 1] - e0).astype(np.int64)
+    edges = np.asarray(g.edges)[e0:e1]
+    weights = None if g.weights is None else np.asarray(g.weights)[e0:e1]
+    return CsrGraph(hi - lo, e1 - e0, loc_off, edges, weights, g.edge_elem_bytes,
+                    g.weight_elem_bytes, g.directed)
+
+
+class Engine(Protocol):
+    """One partition's traversal steps (CUDA: CudaPartition; tests: a numpy model)."""
+
+    lo: int
+    num_local: int
+
+    def begin(self, algo: str, source: int, strategy) -> tuple[int, int]: ...
+    def expand(self, exch) -> None: ...
+    def apply(self, mine) -> tuple[int, int]: ...
+    def result(self) -> np.ndarray: ...
+
+
+class CudaPartition:
+    """One vertex range of a graph on one GPU (zc_part_* of the C ABI)."""
+
+    def __init__(self, g_local, bounds: np.ndarray, part: int, placement: str = "zerocopy",
+                 device: int = 0, validate: bool = True, _handle: Optional[int] = None):
+        self.bounds = np.ascontiguousarray(bounds, dtype=np.uint64)
+        self.nparts = self.bounds.size - 1
+        self.part = part
+        self.lo = int(self.bounds[part])
+        self.num_local = int(self.bounds[part + 1]) - self.lo
+        self.stride = exchange_stride(self.bounds)
+        self.device = device
+        self.global_vertices = int(self.bounds[-1])
+        self.stats = N.Stats()
+        if _handle is not None:
+            self._h = C.c_void_p(_handle)
+            return
+        from .device import _list_arg
+        offsets = np.ascontiguousarray(np.asarray(g_local.offsets), dtype=np.int64)
+        edges, eb_src = _list_arg(g_local.edges)
+        weights, wb_src = (None, 8) if g_local.weights is None else _list_arg(g_local.weights)
+        d = N.GraphDesc()
+        d.num_vertices, d.num_edges = g_local.num_vertices, g_local.num_edges
+        d.offsets = offsets.ctypes.data
+        d.edges = edges.ctypes.data if edges.size else None
+        d.weights = None if weights is None else (weights.ctypes.data or None)
+        d.src_edge_bytes, d.src_weight_bytes = eb_src, wb_src
+        d.edge_elem_bytes, d.weight_elem_bytes = g_local.edge_elem_bytes, g_local.weight_elem_bytes
+        d.placement, d.device = N.PLACEMENTS[placement], device
+        d.flags = ((N.ZC_F_DIRECTED if g_local.directed else 0)
+                   | (0 if validate else N.ZC_F_NO_VALIDATE))
+        info = N.PartInfo()
+        info.global_vertices = self.global_vertices
+        info.stride = self.stride
+        info.bounds = self.bounds.ctypes.data
+        info.nparts, info.part = self.nparts, part
+        h = C.c_void_p()
+        N.check(N.lib().zc_part_create(C.byref(d), C.byref(info), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            N.lib().zc_graph_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def begin(self, algo: str, source: int, strategy) -> tuple[int, int]:
+        n, t = C.c_uint64(), C.c_uint64()
+        N.check(N.lib().zc_part_begin(self._h, ALGO_IDS[algo], int(source), strategy_id(strategy),
+                                      C.byref(n), C.byref(t)))
+        return n.value, t.value
+
+    def expand(self, exch) -> None:
+        N.check(N.lib().zc_part_expand(self._h, exch.data_ptr()))
+
+    def apply(self, mine) -> tuple[int, int]:
+        n, t = C.c_uint64(), C.c_uint64()
+        N.check(N.lib().zc_part_apply(self._h, mine.data_ptr(), C.byref(n), C.byref(t)))
+        return n.value, t.value
+
+    def graph_view(self):
+        """DeviceGraph-style host views (offsets, edges, weights) of this part."""
+        from .device import DeviceGraph
+        dg = DeviceGraph.__new__(DeviceGraph)
+        dg._h = self._h
+        nv, ne = C.c_uint64(), C.c_uint64()
+        eb, wb, pl, fl = C.c_uint32(), C.c_uint32(), C.c_int32(), C.c_uint32()
+        N.check(N.lib().zc_graph_info(self._h, C.byref(nv), C.byref(ne), C.byref(eb), C.byref(wb),
+                                      C.byref(pl), C.byref(fl)))
+        dg.num_vertices, dg.num_edges = nv.value, ne.value
+        dg.edge_elem_bytes, dg.weight_elem_bytes = eb.value, wb.value or 4
+        dg.has_weights = wb.value != 0
+        dg.directed = bool(fl.value & N.ZC_F_DIRECTED)
+        off, edges, weights = DeviceGraph.host_arrays(dg)
+        dg._h = None  # the view does not own the handle
+        return CsrGraph(dg.num_vertices, dg.num_edges, off, edges, weights, dg.edge_elem_bytes,
+                        dg.weight_elem_bytes, dg.directed)
+
+    def result(self) -> np.ndarray:
+        from .device import pinned_empty
+        out = pinned_empty(self.num_local, np.int64)
+        N.check(N.lib().zc_part_result(self._h, out.ctypes.data, C.byref(self.stats)))
+        return out
+
+
+def generate_rmat_part(scale: int, nparts: int, part: int, edge_factor: int = 16,
+                       a: float = 0.57, b: float = 0.19, c: float = 0.19, seed: int = 27, *,
+                       weights=None, placement: str = "zerocopy", device: int = 0
+                       ) -> CudaPartition:
+    """This rank's edge-balanced part of generate_rmat(scale, ...) (same arcs),
+    generated on the GPU straight into a partition handle."""
+    lo, hi = weights if weights is not None else (1, 0)
+    bounds = np.zeros(nparts + 1, np.uint64)
+    h = C.c_void_p()
+    N.check(N.lib().zc_generate_rmat_part(scale, edge_factor, a, b, c, seed, lo, hi, nparts, part,
+                                          N.PLACEMENTS[placement], device, bounds.ctypes.data,
+                                          C.byref(h)))
+    return CudaPartition(None, bounds, part, placement, device, _handle=h.value)
+
+
+@dataclass
+class PartResult:
+    """This rank's share of a partitioned traversal."""
+
+    algo: str
+    lo: int
+    values: np.ndarray          # int64 values of the owned range
+    iterations: int             # global (same on every rank)
+    traversed_edges: list       # global, summed over ranks
+    frontier_sizes: list = field(default_factory=list)  # global
+
+    @property
+    def total_traversed_edges(self) -> int:
+        return sum(self.traversed_edges)
+
+
+def _torch_dtype(algo: str):
+    import torch
+    return {"bfs": torch.uint8, "sssp": torch.int64, "cc": torch.int32}[algo]
+
+
+def run_partition(engine: Engine, algo: str, source: int, strategy, *, group=None,
+                  tensor_device=None, stage_host: bool = False, fetch: bool = True,
+                  buffers=None) -> PartResult:
+    """SPMD driver: call on every rank of `group` with that rank's engine.
+
+    stage_host: run the collectives on host copies of the exchange buffers
+    (gloo; lets several ranks share one GPU in tests).  fetch=False skips the
+    download of the owned values (timing of the traversal loop alone).
+    buffers: reusable (exch, mine) tensors from exchange_buffers().
+    """
+    import torch
+    import torch.distributed as dist
+
+    if algo not in ALGO_IDS:
+        raise ValueError(f"unknown algorithm {algo!r}")
+    nparts = dist.get_world_size(group)
+    stride = engine.stride
+    dev = tensor_device if tensor_device is not None else torch.device("cuda", engine.device)
+    if buffers is None:
+        buffers = exchange_buffers(algo, nparts, stride, dev)
+    exch, mine = buffers
+    if stage_host:
+        h_exch, h_mine = exch.cpu(), mine.cpu()
+    op = dist.ReduceOp.MAX if algo == "bfs" else dist.ReduceOp.MIN
+    cdev = torch.device("cpu") if stage_host else dev
+    counts = torch.zeros(2, dtype=torch.int64, device=cdev)
+
+    def global_counts(n: int, t: int) -> tuple[int, int]:
+        counts[0], counts[1] = n, t
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+        return int(counts[0]), int(counts[1])
+
+    n, t = global_counts(*engine.begin(algo, source, strategy))
+    iters, trav, front = 0, [], []
+    while n > 0:
+        iters += 1
+        trav.append(t)
+        front.append(n)
+        engine.expand(exch)                      # device work done when this returns
+        if stage_host:
+            h_exch.copy_(exch)
+            dist.reduce_scatter_tensor(h_mine, h_exch, op=op, group=group)
+            mine.copy_(h_mine)
+        else:
+            dist.reduce_scatter_tensor(mine, exch, op=op, group=group)
+        if dev.type == "cuda":
+            torch.cuda.current_stream(dev).synchronize()
+        n, t = global_counts(*engine.apply(mine))
+    values = engine.result() if fetch else None
+    return PartResult(algo, engine.lo, values, iters, trav, front)
+
+
+def exchange_buffers(algo: str, nparts: int, stride: int, device):
+    """(exchange, owned-slice) tensors for run_partition."""
+    import torch
+    dt = _torch_dtype(algo)
+    return (torch.empty(nparts * stride, dtype=dt, device=device),
+            torch.empty(stride, dtype=dt, device=device))
+
+
+def run_partitions_local(engines: Sequence[Engine], algo: str, source: int, strategy
+                         ) -> tuple[np.ndarray, int, list]:
+    """All partitions in one process (one device): the reduce-scatter becomes a
+    host-driven reduction over the stacked exchange buffers.  Used to validate
+    the partitioned kernels on a single GPU."""
+    import torch
+
+    p = len(engines)
+    stride = engines[0].stride
+    dev = torch.device("cuda", engines[0].device)
+    dt = _torch_dtype(algo)
+    bufs = [torch.empty(p * stride, dtype=dt, device=dev) for _ in range(p)]
+    nt = [e.begin(algo, source, strategy) for e in engines]
+    n, t = sum(x[0] for x in nt), sum(x[1] for x in nt)
+    iters, trav = 0, []
+    while n > 0:
+        iters += 1
+        trav.append(t)
+        for e, b in zip(engines, bufs):
+            e.expand(b)
+        st = torch.stack(bufs)
+        red = st.max(dim=0).values if algo == "bfs" else st.min(dim=0).values
+        slices = [red[k * stride:(k + 1) * stride].contiguous() for k in range(p)]
+        torch.cuda.synchronize(dev)
+        nt = [e.apply(sl) for e, sl in zip(engines, slices)]
+        n, t = sum(x[0] for x in nt), sum(x[1] for x in nt)
+    values = np.concatenate([e.result() for e in engines]) if engines else np.zeros(0, np.int64)
+    return values, iters, trav

@@ -163,3 +163,45 @@ def test_link_probe_sane():
     assert 5 < p["memcpy_h2d_gbs"] < 200
     assert 1 < p["zerocopy_read_gbs"] < 200
     assert p["hbm_read_gbs"] > 500
+
+
+# ------------------------------------------------------------ partitions
+from paper_2006_06890_b200.multi import (CudaPartition, edge_balanced_bounds, generate_rmat_part,
+                                         local_part, run_partitions_local)
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3])
+def test_cuda_partitions_match_reference(nparts):
+    """Several CUDA partitions on one GPU, host-side reduction in place of the
+    reduce-scatter: identical values / iterations / traversed edges."""
+    bad = []
+    for c in [c for c in CASES if c.tag.startswith(("c8_", "pl_", "e8_")) or c.index < 11]:
+        b = edge_balanced_bounds(c.graph.offsets, nparts)
+        engines = [CudaPartition(local_part(c.graph, b, k), b, k) for k in range(nparts)]
+        for s in STRATS:
+            vals, iters, trav = run_partitions_local(engines, c.algo, max(c.source, 0), s)
+            if not (np.array_equal(vals, c.values) and iters == c.iterations
+                    and trav == c.traversed):
+                bad.append((c.tag, c.index, s.value))
+        for e in engines:
+            e.close()
+    assert not bad, bad[:8]
+
+
+def test_rmat_partition_generator_matches_whole_graph():
+    whole = zc.generate_rmat(16, 16, seed=11, weights=(8, 72)).as_csr()
+    parts = [generate_rmat_part(16, 4, k, seed=11, weights=(8, 72)) for k in range(4)]
+    b = parts[0].bounds
+    assert np.array_equal(b, edge_balanced_bounds(whole.offsets, 4))
+    for k, p in enumerate(parts):
+        ref = local_part(whole, b, k)
+        got = p.graph_view()
+        assert np.array_equal(got.offsets, ref.offsets)
+        assert np.array_equal(np.asarray(got.edges), np.asarray(ref.edges))
+        assert np.array_equal(np.asarray(got.weights), np.asarray(ref.weights))
+    src = int(zc.pick_sources(whole, 1)[0])
+    for algo in ("bfs", "sssp"):
+        ref = oracle.run(algo, whole, src, threads=8)
+        vals, iters, trav = run_partitions_local(parts, algo, src, "merged-aligned")
+        assert np.array_equal(vals, ref.values) and iters == ref.iterations
+        assert trav == ref.traversed_edges
