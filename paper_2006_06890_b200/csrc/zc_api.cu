@@ -11,6 +11,7 @@
 // levels: expand (zc_kernels.cu) -> compact -> read two counters.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -62,6 +63,20 @@ static void convert_copy(void* dst, uint32_t dw, const void* src, uint32_t sw, u
       else static_cast<uint32_t*>(dst)[i] = static_cast<uint32_t>(x);
     }
   });
+}
+
+void tune_params(ExpandArgs* a) {
+  int u = 4, c = 0, sched = 0;
+  if (const char* t = getenv("ZC_TUNE")) {  // read per run: experiments vary it in-process
+    const char* p = strstr(t, "unroll=");
+    if (p) u = atoi(p + 7);
+    p = strstr(t, "ctas=");
+    if (p) c = atoi(p + 5);
+    sched = strstr(t, "sched=chunk") != nullptr;
+  }
+  a->unroll = u;
+  a->ctas_per_sm = c;
+  a->chunk_sched = sched;
 }
 
 static double now_ms() {
@@ -120,6 +135,9 @@ void zc::free_graph(zc_graph* g) {
   cudaFree(g->d_big_prefix);
   cudaFree(g->d_ctr);
   cudaFree(g->d_part_lo);
+  cudaFree(g->d_wcnt);
+  cudaFree(g->d_wpre);
+  cudaFree(g->d_scan_tmp);
   if (g->h_ctr) cudaFreeHost(g->h_ctr);
   if (g->h_small) cudaFreeHost(g->h_small);
   for (auto& e : g->ev)
@@ -295,6 +313,10 @@ int zc::alloc_state(zc_graph* g) {
   ZC_CUDA_TRY(cudaMalloc(&g->d_big_val, n1 * sizeof(uint64_t)));
   ZC_CUDA_TRY(cudaMalloc(&g->d_big_prefix, (n1 + 1) * sizeof(uint64_t)));
   ZC_CUDA_TRY(cudaMalloc(&g->d_ctr, kCtrCount * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_wcnt, n1 * sizeof(uint32_t)));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_wpre, (n1 + 1) * sizeof(uint64_t)));
+  g->scan_tmp_bytes = scan_tmp_bytes(n1);
+  ZC_CUDA_TRY(cudaMalloc(&g->d_scan_tmp, g->scan_tmp_bytes));
   ZC_CUDA_TRY(cudaHostAlloc(&g->h_ctr, kCtrCount * sizeof(uint64_t), cudaHostAllocDefault));
   ZC_CUDA_TRY(cudaHostAlloc(&g->h_small, 4 * sizeof(uint64_t), cudaHostAllocDefault));
   ZC_CUDA_TRY(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
@@ -437,7 +459,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     if (model)
       ZC_CUDA_TRY(launch_traffic_model(strategy, g->eb, g->wb, algo == kSssp, g->d_front[cur], n,
                                        g->d_off, g->d_ctr, g->num_sms, st, &launches));
-    ExpandArgs a;
+    ExpandArgs a{};
     a.front = g->d_front[cur];
     a.fs = g->d_fs[cur];
     a.fd = g->d_fd[cur];
@@ -454,6 +476,11 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     a.big_val = g->d_big_val;
     a.big_prefix = g->d_big_prefix;
     a.ctr = g->d_ctr;
+    a.wcnt = g->d_wcnt;
+    a.wpre = g->d_wpre;
+    a.scan_tmp = g->d_scan_tmp;
+    a.scan_tmp_bytes = g->scan_tmp_bytes;
+    tune_params(&a);
     while (g->iter_ev.size() < 2 * iters) {
       cudaEvent_t e;
       ZC_CUDA_TRY(cudaEventCreate(&e));
@@ -728,6 +755,11 @@ int zc_part_expand(zc_graph* g, void* exch) {
   a.part_lo = g->d_part_lo;
   a.nparts = g->nparts;
   a.stride = g->stride;
+  a.wcnt = g->d_wcnt;
+  a.wpre = g->d_wpre;
+  a.scan_tmp = g->d_scan_tmp;
+  a.scan_tmp_bytes = g->scan_tmp_bytes;
+  tune_params(&a);
   ZC_CUDA_TRY(launch_expand(g->p_strategy, algo + kPartAlgo, g->eb, g->wb, a, g->num_sms, st,
                             &g->p_launches));
   ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (g->p_iter - 1) + 1], st));

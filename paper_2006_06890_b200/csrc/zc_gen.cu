@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cub/device/device_segmented_sort.cuh>
+
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -133,7 +135,7 @@ __global__ void k_rmat_fill(RmatParams p, uint64_t nv, const uint64_t* off, ET* 
     const uint64_t v = vbase + lv;
     const uint64_t src_old = p.perm.inv(v);
     for (uint64_t k = s + lane; k < e; k += 32) {
-      const uint64_t d_old = rmat_dst(p, src_old, (v << 24) ^ (k - s) ^ (k << 40));
+      const uint64_t d_old = rmat_dst(p, src_old, (v << 32) | (k - s));
       edges[k] = static_cast<ET>(p.perm.fwd(d_old));
     }
   }
@@ -182,9 +184,9 @@ __global__ void k_deg_from_off(uint64_t nv, const uint64_t* off, uint32_t* deg) 
     deg[v] = static_cast<uint32_t>(off[v + 1] - off[v]);
 }
 
-// Sort every list ascending.  Lists up to 32 elements: one warp-level
-// odd-even pass per list in registers; up to kSortSmem elements: one CTA with
-// shared-memory bitonic sort; longer lists are handled by k_sort_long.
+// Sort every list ascending.  Lists up to 32 elements: warp bitonic sort in
+// registers; up to kSortSmem elements: one CTA with a shared-memory bitonic
+// sort; longer lists: CUB segmented sort (sort_lists).
 constexpr int kSortSmem = 4096;
 
 template <typename ET>
@@ -242,30 +244,14 @@ __global__ void __launch_bounds__(1024) k_sort_mid(uint64_t nv, const uint64_t* 
   }
 }
 
-// Long lists (> kSortSmem, hubs only): bitonic network over a padded copy
-// in global memory (the pads must be materialised: intermediate stages move
-// them through the whole power-of-two range).
+// Copy sorted segments [b, e) of src back into dst (warp per segment).
 template <typename ET>
-__global__ void k_pad_copy(const ET* src, uint64_t n, uint64_t m, ET* dst) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    dst[i] = i < n ? src[i] : static_cast<ET>(~0ull);
-}
-
-template <typename ET>
-__global__ void k_sort_long_step(ET* data, uint64_t m, uint64_t j, uint64_t k) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t p = i ^ j;
-    if (p > i) {
-      const ET a = data[i], b = data[p];
-      const bool up = (i & k) == 0;
-      if ((a > b) == up) {
-        data[i] = b;
-        data[p] = a;
-      }
-    }
-  }
+__global__ void k_copy_segments(const ET* src, ET* dst, const int* b, const int* e, int nseg) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t k = gw; k < static_cast<uint64_t>(nseg); k += nw)
+    for (int i = b[k] + lane; i < e[k]; i += 32) dst[i] = src[i];
 }
 
 template <typename ET>
@@ -330,32 +316,49 @@ int sort_lists(uint64_t nv, const uint64_t* d_off, const int64_t* h_off, ET* edg
   k_sort_short<ET><<<kGenGrid, 256>>>(nv, d_off, edges);
   k_sort_mid<ET><<<kGenGrid, 1024>>>(nv, d_off, edges);
   ZC_CUDA_TRY(cudaGetLastError());
-  uint64_t mmax = 0;
+  // Long lists (hubs): CUB segmented sort, batched so every call covers at
+  // most 2^30 keys (CUB takes int sizes), then copied back segment-wise.
+  std::vector<uint64_t> seg_b, seg_e;
   for (uint64_t v = 0; v < nv; ++v) {
     const uint64_t n = h_off[v + 1] - h_off[v];
     if (n > static_cast<uint64_t>(kSortSmem)) {
-      uint64_t m = 1;
-      while (m < n) m <<= 1;
-      mmax = std::max(mmax, m);
+      seg_b.push_back(h_off[v]);
+      seg_e.push_back(h_off[v + 1]);
     }
   }
-  if (mmax) {
-    ET* tmp = nullptr;
-    ZC_CUDA_TRY(cudaMalloc(&tmp, mmax * sizeof(ET)));
-    for (uint64_t v = 0; v < nv; ++v) {
-      const uint64_t n = h_off[v + 1] - h_off[v];
-      if (n <= static_cast<uint64_t>(kSortSmem)) continue;
-      uint64_t m = 1;
-      while (m < n) m <<= 1;
-      ET* data = edges + h_off[v];
-      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((m + 255) / 256, kGenGrid));
-      k_pad_copy<ET><<<grid, 256>>>(data, n, m, tmp);
-      for (uint64_t k = 2; k <= m; k <<= 1)
-        for (uint64_t j = k >> 1; j > 0; j >>= 1) k_sort_long_step<ET><<<grid, 256>>>(tmp, m, j, k);
-      ZC_CUDA_TRY(cudaMemcpyAsync(data, tmp, n * sizeof(ET), cudaMemcpyDeviceToDevice, 0));
+  const uint64_t kSpan = 1ull << 30;
+  size_t i0 = 0;
+  while (i0 < seg_b.size()) {
+    size_t i1 = i0 + 1;
+    while (i1 < seg_b.size() && seg_e[i1] - seg_b[i0] <= kSpan) ++i1;
+    const uint64_t base = seg_b[i0], span = seg_e[i1 - 1] - base;
+    const int nseg = static_cast<int>(i1 - i0);
+    std::vector<int> hb(nseg), he(nseg);
+    for (int k = 0; k < nseg; ++k) {
+      hb[k] = static_cast<int>(seg_b[i0 + k] - base);
+      he[k] = static_cast<int>(seg_e[i0 + k] - base);
     }
+    int *db = nullptr, *de = nullptr;
+    ET* out = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    ZC_CUDA_TRY(cudaMalloc(&db, nseg * sizeof(int)));
+    ZC_CUDA_TRY(cudaMalloc(&de, nseg * sizeof(int)));
+    ZC_CUDA_TRY(cudaMemcpy(db, hb.data(), nseg * sizeof(int), cudaMemcpyHostToDevice));
+    ZC_CUDA_TRY(cudaMemcpy(de, he.data(), nseg * sizeof(int), cudaMemcpyHostToDevice));
+    ZC_CUDA_TRY(cudaMalloc(&out, span * sizeof(ET)));
+    ZC_CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, edges + base, out,
+                                                   static_cast<int>(span), nseg, db, de));
+    ZC_CUDA_TRY(cudaMalloc(&tmp, tmp_bytes));
+    ZC_CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, edges + base, out,
+                                                   static_cast<int>(span), nseg, db, de));
+    k_copy_segments<ET><<<kGenGrid, 256>>>(out, edges + base, db, de, nseg);
     ZC_CUDA_TRY(cudaDeviceSynchronize());
-    ZC_CUDA_TRY(cudaFree(tmp));
+    cudaFree(db);
+    cudaFree(de);
+    cudaFree(out);
+    cudaFree(tmp);
+    i0 = i1;
   }
   ZC_CUDA_TRY(cudaGetLastError());
   return ZC_OK;

@@ -44,6 +44,10 @@ struct zc_graph {
   uint64_t* d_big_val = nullptr;
   uint64_t* d_big_prefix = nullptr;
   uint64_t* d_ctr = nullptr;
+  uint32_t* d_wcnt = nullptr;  // per-slot window counts (CTA sweep)
+  uint64_t* d_wpre = nullptr;  // their exclusive prefix
+  void* d_scan_tmp = nullptr;
+  size_t scan_tmp_bytes = 0;
   uint64_t* h_ctr = nullptr;    // pinned
   uint64_t* h_small = nullptr;  // pinned staging for the source / initial values
   cudaStream_t stream = nullptr;

@@ -90,7 +90,19 @@ struct ExpandArgs {
   const uint64_t* part_lo;  // nparts + 1 range starts (device)
   uint32_t nparts;
   uint64_t stride;
+  // CTA-sweep scheduling: per-slot window counts, their exclusive prefix
+  uint32_t* wcnt;
+  uint64_t* wpre;  // n + 1
+  void* scan_tmp;
+  size_t scan_tmp_bytes;
+  // launch tuning (host side only; ZC_TUNE environment variable)
+  int unroll;
+  int ctas_per_sm;
+  int chunk_sched;  // 1: the per-warp chunk + big-list scheduler instead of the sweep
 };
+
+// ZC_TUNE="unroll=8,ctas=6,sched=chunk": expansion tuning knobs for experiments.
+void tune_params(ExpandArgs* a);
 
 struct CompactArgs {
   uint8_t* flags;

@@ -153,18 +153,19 @@ __device__ __forceinline__ uint64_t window_base(uint64_t s) {
 // ------------------------------------------------ merged / merged-aligned
 // A batch of kUnroll windows of one warp: each lane holds the element it
 // loaded from each window (ok = lane inside the list).
-template <int ALGO, typename ET, typename WT>
+template <int ALGO, typename ET, typename WT, int U>
 struct Batch {
-  ET dst[kUnroll];
-  WT wt[kUnroll];
-  uint64_t sval[kUnroll];
-  bool ok[kUnroll];
+  ET dst[U];
+  WT wt[U];
+  uint64_t sval[U];
+  bool ok[U];
 };
 
-template <int ALGO, typename ET, typename WT>
-__device__ __forceinline__ void visit_batch(const ExpandArgs& a, const Batch<ALGO, ET, WT>& b) {
+template <int ALGO, typename ET, typename WT, int U>
+__device__ __forceinline__ void visit_batch(const ExpandArgs& a,
+                                            const Batch<ALGO, ET, WT, U>& b) {
 #pragma unroll
-  for (int u = 0; u < kUnroll; ++u)
+  for (int u = 0; u < U; ++u)
     if (b.ok[u])
       Visit<ALGO>::apply(a, b.dst[u], AlgoTraits<ALGO>::weighted ? uint64_t(b.wt[u]) : 0,
                          b.sval[u]);
@@ -195,7 +196,7 @@ __device__ __forceinline__ Chunk load_chunk(const ExpandArgs& a, uint64_t c0, in
 // (so the HBM-side visit overlaps the next PCIe round trip) and prefetching
 // the next chunk's metadata.  Lists needing more than kBigSteps windows go to
 // the tier-2 queue.
-template <int STRAT, int ALGO, typename ET, typename WT>
+template <int STRAT, int ALGO, typename ET, typename WT, int U>
 __global__ void __launch_bounds__(kExpandThreads) k_expand_warp(ExpandArgs a) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * kExpandThreads + threadIdx.x) >> 5;
@@ -233,9 +234,9 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_warp(ExpandArgs a) {
     const uint32_t excl = incl - nst;
     const uint32_t total = __shfl_sync(kFull, incl, kWarp - 1);
 
-    auto issue = [&](Batch<ALGO, ET, WT>& b, uint32_t q0) {
+    auto issue = [&](Batch<ALGO, ET, WT, U>& b, uint32_t q0) {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+      for (int u = 0; u < U; ++u) {
         const uint32_t q = q0 + u;
         b.ok[u] = false;
         b.sval[u] = 0;
@@ -258,11 +259,11 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_warp(ExpandArgs a) {
       }
     };
     if (total == 0) continue;
-    Batch<ALGO, ET, WT> cur, nxt;
+    Batch<ALGO, ET, WT, U> cur, nxt;
     issue(cur, 0);
-    for (uint32_t q0 = 0; q0 < total; q0 += kUnroll) {
-      if (q0 + kUnroll < total) issue(nxt, q0 + kUnroll);
-      visit_batch<ALGO, ET, WT>(a, cur);
+    for (uint32_t q0 = 0; q0 < total; q0 += U) {
+      if (q0 + U < total) issue(nxt, q0 + U);
+      visit_batch<ALGO, ET, WT, U>(a, cur);
       cur = nxt;
     }
   }
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_warp(ExpandArgs a) {
 // Tier 2: every warp takes an equal contiguous range of the big lists'
 // flattened window sequence (same windows as tier 1), software-pipelined
 // the same way.
-template <int STRAT, int ALGO, typename ET, typename WT>
+template <int STRAT, int ALGO, typename ET, typename WT, int U>
 __global__ void __launch_bounds__(kExpandThreads) k_expand_big(ExpandArgs a) {
   const uint64_t nbig = a.ctr[kCtrBig];
   if (nbig == 0) return;
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_big(ExpandArgs a) {
   const uint64_t gw = (static_cast<uint64_t>(blockIdx.x) * kExpandThreads + threadIdx.x) >> 5;
   const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * kExpandThreads) >> 5;
   uint64_t per = (total + nw - 1) / nw;
-  per = (per + kUnroll - 1) / kUnroll * kUnroll;
+  per = (per + U - 1) / U * U;
   const uint64_t q_begin = gw * per;
   if (q_begin >= total) return;
   const uint64_t q_end = min(total, q_begin + per);
@@ -299,9 +300,9 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_big(ExpandArgs a) {
   uint64_t b = window_base<STRAT, ET>(s);
   uint64_t val = AlgoTraits<ALGO>::has_val ? a.big_val[i] : 0;
 
-  auto issue = [&](Batch<ALGO, ET, WT>& bt, uint64_t q0) {
+  auto issue = [&](Batch<ALGO, ET, WT, U>& bt, uint64_t q0) {
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint64_t q = q0 + u;
       bt.ok[u] = false;
       bt.sval[u] = val;
@@ -325,12 +326,132 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_big(ExpandArgs a) {
       }
     }
   };
-  Batch<ALGO, ET, WT> cur, nxt;
+  Batch<ALGO, ET, WT, U> cur, nxt;
   issue(cur, q_begin);
-  for (uint64_t q0 = q_begin; q0 < q_end; q0 += kUnroll) {
-    if (q0 + kUnroll < q_end) issue(nxt, q0 + kUnroll);
-    visit_batch<ALGO, ET, WT>(a, cur);
+  for (uint64_t q0 = q_begin; q0 < q_end; q0 += U) {
+    if (q0 + U < q_end) issue(nxt, q0 + U);
+    visit_batch<ALGO, ET, WT, U>(a, cur);
     cur = nxt;
+  }
+}
+
+// ------------------------------------------------- CTA sweep (default)
+// Scheduling measured on B200 (tools/read_probe.py): zero-copy reads reach
+// the link rate only while the number of concurrently streamed address
+// regions stays around one per CTA (~1.2 K); one stream per warp (~9.5 K)
+// caps at ~35 GB/s -- the GPU/IOMMU translation reach.  So every CTA takes
+// an equal contiguous range of the frontier's flattened window sequence
+// (windows are equal-cost line requests, so static ranges balance) and its
+// 8 warps take interleaved batches of U windows inside it: the CTA streams
+// ~4 KB at a time through its region.  Windows (lane -> element maps) are
+// exactly those of the strategy; only their schedule changes.
+constexpr int kSweepThreads = 256;
+constexpr int kSweepWarps = kSweepThreads / 32;
+constexpr int kStage = 256;  // frontier slots staged in shared memory at a time
+
+template <int STRAT, typename ET>
+__global__ void k_window_counts(const uint64_t* fs, const uint32_t* fd, uint64_t n,
+                                uint32_t* wcnt) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = fs[j], d = fd[j];
+    wcnt[j] = d ? static_cast<uint32_t>((s + d - window_base<STRAT, ET>(s) + kWarp - 1) / kWarp)
+                : 0u;
+  }
+}
+
+template <int STRAT, int ALGO, typename ET, typename WT, int U>
+__global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
+  __shared__ uint64_t sh_s[kStage], sh_e[kStage], sh_v[kStage];
+  __shared__ uint64_t sh_w[kStage + 1];
+  __shared__ uint64_t sh_j;
+  const uint64_t n = a.n;
+  const uint64_t T = a.wpre[n];
+  const uint64_t G = gridDim.x, b = blockIdx.x;
+  const uint64_t Wb = T / G * b + min(b, T % G);
+  const uint64_t We = Wb + T / G + (b < T % G ? 1 : 0);
+  if (Wb >= We) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const ET* __restrict__ E = static_cast<const ET*>(a.edges);
+  const WT* __restrict__ Wt = static_cast<const WT*>(a.weights);
+
+  // slot owning window Wb: the last j with wpre[j] <= Wb (32-ary search)
+  if (warp == 0) {
+    uint64_t lo = 0, hi = n;  // wpre[lo] <= Wb < wpre[hi] (wpre[n] = T > Wb)
+    while (hi - lo > 1) {
+      const uint64_t step = (hi - lo + 31) / 32;
+      const uint64_t probe = lo + step * (lane + 1);
+      const bool le = probe < hi && a.wpre[probe] <= Wb;
+      const unsigned m = __ballot_sync(kFull, le);
+      const int k = m ? 31 - __clz(m) : -1;  // predicates are monotone in the lane
+      const uint64_t nlo = k >= 0 ? lo + step * (k + 1) : lo;
+      hi = min(hi, nlo + step);
+      lo = nlo;
+    }
+    if (lane == 0) sh_j = lo;
+  }
+  __syncthreads();
+  uint64_t j = sh_j;
+  uint64_t W = Wb;
+  while (W < We) {
+    // stage slots [j, j + kStage)
+    for (int i = threadIdx.x; i <= kStage; i += kSweepThreads) {
+      const uint64_t jj = j + i;
+      sh_w[i] = jj <= n ? a.wpre[jj] : T;
+      if (i < kStage && jj < n) {
+        const uint64_t s0 = a.fs[jj];
+        sh_s[i] = s0;
+        sh_e[i] = s0 + a.fd[jj];
+        if (AlgoTraits<ALGO>::has_val) sh_v[i] = a.fval[jj];
+      }
+    }
+    __syncthreads();
+    const uint64_t Wend = min(We, sh_w[kStage]);
+
+    int k = 0;  // per-warp slot cursor, monotone within this stage
+    auto issue = [&](Batch<ALGO, ET, WT, U>& bt, uint64_t q0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t q = q0 + u;
+        bt.ok[u] = false;
+        bt.sval[u] = 0;
+        if (q < Wend) {  // warp-uniform
+          if (u == 0) {  // binary search for the batch head, then walk
+            int lo = 0, hi = kStage;  // sh_w[lo] <= q < sh_w[hi]
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if (sh_w[mid] <= q) lo = mid; else hi = mid;
+            }
+            k = lo;
+          } else {
+            while (sh_w[k + 1] <= q) ++k;
+          }
+          const uint64_t s0 = sh_s[k], e0 = sh_e[k];
+          if (AlgoTraits<ALGO>::has_val) bt.sval[u] = sh_v[k];
+          const uint64_t idx = window_base<STRAT, ET>(s0) + (q - sh_w[k]) * kWarp + lane;
+          bt.ok[u] = idx >= s0 && idx < e0;
+          if (bt.ok[u]) {
+            bt.dst[u] = ld_list(E + idx);
+            if (AlgoTraits<ALGO>::weighted) bt.wt[u] = ld_list(Wt + idx);
+          }
+        }
+      }
+    };
+    // warps interleave batches of U windows: warp w takes [W + (i*8 + w)*U, +U)
+    uint64_t q0 = W + static_cast<uint64_t>(warp) * U;
+    if (q0 < Wend) {
+      Batch<ALGO, ET, WT, U> cur, nxt;
+      issue(cur, q0);
+      for (; q0 < Wend; q0 += kSweepWarps * U) {
+        const uint64_t qn = q0 + kSweepWarps * U;
+        if (qn < Wend) issue(nxt, qn);
+        visit_batch<ALGO, ET, WT, U>(a, cur);
+        cur = nxt;
+      }
+    }
+    __syncthreads();
+    W = Wend;
+    j += kStage;
   }
 }
 
@@ -830,23 +951,58 @@ int grid_for(uint64_t work, int threads, int num_sms, int per_sm) {
   return static_cast<int>(g);
 }
 
+template <typename K>
+int resident_ctas(K kernel, int threads, int num_sms) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  return num_sms * (per_sm > 0 ? per_sm : 1);
+}
+
+template <int STRAT, int ALGO, typename ET, typename WT, int U>
+cudaError_t expand_sweep(const ExpandArgs& a, int num_sms, cudaStream_t st,
+                         uint64_t* launches) {
+  // window counts -> global exclusive prefix (wpre[n] = total windows)
+  const int g1 = grid_for(a.n, 256, num_sms, 16);
+  k_window_counts<STRAT, ET><<<g1, 256, 0, st>>>(a.fs, a.fd, a.n, a.wcnt);
+  cudaError_t e = scan_u32_to_u64(a.wcnt, a.wpre, a.n, a.scan_tmp, a.scan_tmp_bytes, st);
+  if (e != cudaSuccess) return e;
+  static int grid = 0;  // per instantiation: all CTAs resident at once
+  if (!grid) grid = resident_ctas(k_expand_sweep<STRAT, ALGO, ET, WT, U>, kSweepThreads, num_sms);
+  const int g = a.ctas_per_sm > 0 ? num_sms * a.ctas_per_sm : grid;
+  k_expand_sweep<STRAT, ALGO, ET, WT, U><<<g, kSweepThreads, 0, st>>>(a);
+  *launches += 5;
+  return cudaGetLastError();
+}
+
+template <int STRAT, int ALGO, typename ET, typename WT, int U>
+cudaError_t expand_u(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t* launches) {
+  if (!a.chunk_sched) return expand_sweep<STRAT, ALGO, ET, WT, U>(a, num_sms, st, launches);
+  // default: 8 resident 256-thread CTAs per SM = 64 warps/SM (register-limited below)
+  const int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm : 2048 / kExpandThreads;
+  const int g = grid_for((a.n + kWarp - 1) / kWarp * kWarp, kExpandThreads, num_sms, per_sm);
+  k_expand_warp<STRAT, ALGO, ET, WT, U><<<g, kExpandThreads, 0, st>>>(a);
+  k_big_scan<<<1, 1024, 0, st>>>(a.big_prefix, a.ctr);
+  k_expand_big<STRAT, ALGO, ET, WT, U><<<num_sms * per_sm, kExpandThreads, 0, st>>>(a);
+  *launches += 3;
+  return cudaGetLastError();
+}
+
 template <int STRAT, int ALGO, typename ET, typename WT>
 cudaError_t expand_t(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t* launches) {
-  // 8 resident 256-thread CTAs per SM = 64 warps/SM (full occupancy).
-  const int per_sm = 2048 / kExpandThreads;
   if (STRAT == kNaive) {
+    const int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm : 2048 / kExpandThreads;
     const int g = grid_for(a.n, kExpandThreads, num_sms, per_sm);
     k_expand_naive<ALGO, ET, WT><<<g, kExpandThreads, 0, st>>>(a);
     *launches += 1;
     return cudaGetLastError();
   }
-  const int g = grid_for((a.n + kWarp - 1) / kWarp * kWarp, kExpandThreads, num_sms, per_sm);
-  k_expand_warp<STRAT, ALGO, ET, WT><<<g, kExpandThreads, 0, st>>>(a);
-  k_big_scan<<<1, 1024, 0, st>>>(a.big_prefix, a.ctr);
-  k_expand_big<STRAT, ALGO, ET, WT>
-      <<<num_sms * per_sm, kExpandThreads, 0, st>>>(a);
-  *launches += 3;
-  return cudaGetLastError();
+  // tuning variants (ZC_TUNE=unroll=N) for the BFS / u32 merged-aligned path
+  if constexpr (STRAT == kMergedAligned && AlgoTraits<ALGO>::base == kBfs &&
+                sizeof(ET) == 4 && sizeof(WT) == 4) {
+    if (a.unroll == 2) return expand_u<STRAT, ALGO, ET, WT, 2>(a, num_sms, st, launches);
+    if (a.unroll == 8) return expand_u<STRAT, ALGO, ET, WT, 8>(a, num_sms, st, launches);
+  }
+  return expand_u<STRAT, ALGO, ET, WT, kUnroll>(a, num_sms, st, launches);
 }
 
 template <int STRAT, int ALGO>
