@@ -439,18 +439,34 @@ def variants(zc, args, dg, sources, device) -> dict:
     """configs[1]'s comparison: naive vs merged vs merged+aligned (zero-copy),
     UVM (cold, merged+aligned) and the in-HBM control."""
     out = {}
-    for s in ("naive", "merged", "merged-aligned"):
+    for s in ("naive", "merged", "merged-aligned", "packed"):
         # naive walks each hub list with one thread (seconds per BFS): one rep
         out[f"zerocopy/{s}"] = _gteps(zc, dg, sources, s, reps=1 if s == "naive" else 2)
     dg.close()
+    import torch
     for placement in ("uvm", "hbm"):
         h = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, device=device,
                              placement=placement)
         out[f"{placement}/merged-aligned"] = _gteps(zc, h, sources, "merged-aligned", reps=2,
                                                     evict=placement == "uvm")
+        if placement == "uvm":
+            # the reference's UVM capacity default: 25% of the dataset
+            # (report.py:151-153) -- ballast HBM so only that much stays free
+            dataset = h.num_edges * h.edge_elem_bytes
+            free, _ = torch.cuda.mem_get_info(device)
+            ballast_bytes = max(0, free - dataset // 4 - (256 << 20))
+            ballast = torch.empty(ballast_bytes, dtype=torch.uint8, device=f"cuda:{device}")
+            r = _gteps(zc, h, sources, "merged-aligned", reps=2, evict=True)
+            r["free_hbm_bytes"] = torch.cuda.mem_get_info(device)[0]
+            out["uvm_cap25/merged-aligned"] = r
+            del ballast
+            torch.cuda.empty_cache()
         h.close()
     zc_ = out["zerocopy/merged-aligned"]["gteps"]
     out["speedup_vs_uvm"] = zc_ / out["uvm/merged-aligned"]["gteps"]
+    out["speedup_vs_uvm_cap25"] = zc_ / out["uvm_cap25/merged-aligned"]["gteps"]
+    out["packed_speedup_vs_uvm_cap25"] = (out["zerocopy/packed"]["gteps"]
+                                          / out["uvm_cap25/merged-aligned"]["gteps"])
     return out
 
 

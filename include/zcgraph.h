@@ -58,6 +58,9 @@ extern "C" {
 #define ZC_NAIVE 0          /* "naive": thread per frontier vertex          */
 #define ZC_MERGED 1         /* "merged": warp per vertex, 32-element steps  */
 #define ZC_MERGED_ALIGNED 2 /* "merged-aligned": first step floored to 128 B */
+#define ZC_PACKED 3         /* B200 extension (not in the reference): windows are
+                               aligned 32-element blocks of the union of the
+                               frontier's lists, each fetched once           */
 
 /* where the edge / weight lists live */
 #define ZC_PLACE_ZEROCOPY 0 /* cudaHostAlloc(Mapped|Portable) or cudaHostRegister */

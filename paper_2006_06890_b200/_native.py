@@ -13,7 +13,7 @@ import threading
 from ._build import LIB_PATH
 
 ZC_OK, ZC_EINVAL, ZC_ECUDA, ZC_ENOMEM, ZC_ESTATE = 0, -1, -2, -3, -4
-ZC_NAIVE, ZC_MERGED, ZC_MERGED_ALIGNED = 0, 1, 2
+ZC_NAIVE, ZC_MERGED, ZC_MERGED_ALIGNED, ZC_PACKED = 0, 1, 2, 3
 ZC_PLACE_ZEROCOPY, ZC_PLACE_UVM, ZC_PLACE_HBM = 0, 1, 2
 ZC_F_DIRECTED, ZC_F_REGISTER, ZC_F_UVM_PREFETCH, ZC_F_NO_VALIDATE = 1, 2, 4, 8
 ABI_VERSION = 1

@@ -18,7 +18,10 @@ class AccessStrategy(Enum):
     MERGED_ALIGNED = "merged-aligned"
 
 
-_IDS = {"naive": 0, "merged": 1, "merged-aligned": 2}
+# "packed" is a B200 extension beyond the reference's three (include/zcgraph.h
+# ZC_PACKED): windows are the aligned 32-element blocks of the union of the
+# frontier's lists, fetched once each.  Results are identical.
+_IDS = {"naive": 0, "merged": 1, "merged-aligned": 2, "packed": 3}
 
 
 def strategy_id(strategy) -> int:

@@ -122,6 +122,7 @@ void zc::free_graph(zc_graph* g) {
   cudaFree(g->d_off);
   cudaFree(g->d_state);
   cudaFree(g->d_flags);
+  cudaFree(g->d_visited);
   for (int i = 0; i < 2; ++i) {
     cudaFree(g->d_front[i]);
     cudaFree(g->d_fval[i]);
@@ -300,6 +301,7 @@ int zc::alloc_state(zc_graph* g) {
                          cudaMemcpyHostToDevice));
   ZC_CUDA_TRY(cudaMalloc(&g->d_state, n1 * sizeof(uint64_t)));
   ZC_CUDA_TRY(cudaMalloc(&g->d_flags, g->vpad));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_visited, g->vpad / 8));
   ZC_CUDA_TRY(cudaMemset(g->d_flags, 0, g->vpad));
   for (int i = 0; i < 2; ++i) {
     ZC_CUDA_TRY(cudaMalloc(&g->d_front[i], n1 * sizeof(uint32_t)));
@@ -391,8 +393,13 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     set_error("null graph handle");
     return ZC_ESTATE;
   }
-  if (strategy < kNaive || strategy > kMergedAligned) {
+  if (strategy < kNaive || strategy > kPacked) {
     set_error("unknown access strategy " + std::to_string(strategy));
+    return ZC_EINVAL;
+  }
+  if (strategy == kPacked && (g->options & ZC_OPT_TRAFFIC_MODEL)) {
+    set_error("the request model is defined for the reference's three strategies "
+              "(naive, merged, merged-aligned), not for packed");
     return ZC_EINVAL;
   }
   if (algo != kCc && src >= g->nv) {  // traversal.py:93-95
@@ -444,6 +451,13 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     ZC_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(g->d_state) + src * sb, &g->h_small[1], sb,
                                 cudaMemcpyHostToDevice, st));
     h2d += sb;
+    if (algo == kBfs) {  // visited bitmap = {src}
+      ZC_CUDA_TRY(cudaMemsetAsync(g->d_visited, 0, g->vpad / 8, st));
+      g->h_small[2] = 1ull << (src & 31);
+      ZC_CUDA_TRY(cudaMemcpyAsync(g->d_visited + (src >> 5), &g->h_small[2], sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice, st));
+      h2d += sizeof(uint32_t);
+    }
     n = 1;
     trav = g->h_off[src + 1] - g->h_off[src];
   }
@@ -470,6 +484,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     a.weights = g->d_weights;
     a.state = g->d_state;
     a.flags = g->d_flags;
+    a.visited = g->d_visited;
     a.iter = static_cast<uint32_t>(iters);
     a.big_s = g->d_big_s;
     a.big_e = g->d_big_e;
@@ -656,7 +671,7 @@ int zc_part_begin(zc_graph* g, int algo, uint64_t src, int strategy, uint64_t* n
     set_error("not a partition handle");
     return ZC_ESTATE;
   }
-  if (algo < kBfs || algo > kCc || strategy < kNaive || strategy > kMergedAligned) {
+  if (algo < kBfs || algo > kCc || strategy < kNaive || strategy > kPacked) {
     set_error("unknown algorithm or strategy");
     return ZC_EINVAL;
   }

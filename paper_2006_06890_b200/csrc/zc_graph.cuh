@@ -33,6 +33,7 @@ struct zc_graph {
   uint64_t* d_off = nullptr;
   void* d_state = nullptr;
   uint8_t* d_flags = nullptr;
+  uint32_t* d_visited = nullptr;
   uint64_t vpad = 0, ntiles = 0;
   uint32_t* d_front[2] = {nullptr, nullptr};
   uint64_t* d_fval[2] = {nullptr, nullptr};

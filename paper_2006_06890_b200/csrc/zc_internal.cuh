@@ -6,6 +6,7 @@
 //   state    u64[V]        BFS: u32 level[V] (0xffffffff = unreached);
 //                          SSSP: u64 dist[V] (UINT64_MAX = unreached);
 //                          CC: u32 label[V]
+//   visited  u32[V/32]     BFS visited bitmap (L2-resident filter for level[])
 //   flags    u8[Vpad]      "improved / discovered this iteration" marks,
 //                          Vpad = V rounded up to the compaction tile
 //   front    u32[V] x2     frontier (sorted ascending, like traversal.py:117/150)
@@ -44,7 +45,10 @@ constexpr uint32_t kExchNone32 = 0x7fffffffu;
 // expanded by its chunk warp but queued and split across all warps.
 constexpr uint32_t kBigSteps = 16;
 
-enum Strategy : int { kNaive = 0, kMerged = 1, kMergedAligned = 2 };
+enum Strategy : int { kNaive = 0, kMerged = 1, kMergedAligned = 2, kPacked = 3 };
+// kPacked (B200 extension, not one of the paper's three): a window is an
+// aligned 32-element block touched by any frontier list, fetched once for all
+// the lists that share it (see k_window_counts / k_expand_sweep).
 enum Algo : int { kBfs = 0, kSssp = 1, kCc = 2 };
 // Partitioned (multi-GPU) variants: the visit writes candidates for any
 // global vertex into the exchange buffer instead of updating local state.
@@ -78,6 +82,7 @@ struct ExpandArgs {
   const void* weights;    // weight list (SSSP)
   void* state;            // level / dist / label
   uint8_t* flags;         // next-frontier marks
+  uint32_t* visited;      // BFS visited bitmap ((V + 31) / 32 words)
   uint32_t iter;          // BFS: level assigned to newly reached vertices
   uint64_t* big_s;        // big-list queue: list start,
   uint64_t* big_e;        //   list end,

@@ -61,12 +61,15 @@ struct Visit;
 
 template <>
 struct Visit<kBfs> {
-  // traversal.py:116-118: unvisited neighbours get level = iteration.
+  // traversal.py:116-118: unvisited neighbours get level = iteration.  The
+  // check goes to a visited bitmap (V/8 bytes, L2-resident) instead of the
+  // level array, and the atomicOr elects the one writer of each new level.
   static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
                                                uint64_t) {
-    uint32_t* level = static_cast<uint32_t*>(a.state);
-    if (level[w] == kUnreached32) {
-      level[w] = a.iter;
+    uint32_t* word = a.visited + (w >> 5);
+    const uint32_t bit = 1u << (w & 31);
+    if (!(*word & bit) && !(atomicOr(word, bit) & bit)) {
+      static_cast<uint32_t*>(a.state)[w] = a.iter;
       a.flags[w] = 1;
     }
   }
@@ -147,6 +150,7 @@ struct LineElems {
 template <int STRAT, typename ET>
 __device__ __forceinline__ uint64_t window_base(uint64_t s) {
   if (STRAT == kMergedAligned) return s & ~(LineElems<ET>::value - 1);
+  if (STRAT == kPacked) return s & ~static_cast<uint64_t>(kWarp - 1);
   return s;
 }
 
@@ -349,14 +353,33 @@ constexpr int kSweepThreads = 256;
 constexpr int kSweepWarps = kSweepThreads / 32;
 constexpr int kStage = 256;  // frontier slots staged in shared memory at a time
 
+// Windows per frontier slot.  Packed: the slot's 32-element blocks minus its
+// first block when the nearest earlier non-empty slot of the same aligned
+// group of kStage slots (one shared-memory stage of the sweep) already
+// touches it -- so every block is fetched once per group and the lists that
+// share it are always staged together.
 template <int STRAT, typename ET>
 __global__ void k_window_counts(const uint64_t* fs, const uint32_t* fd, uint64_t n,
                                 uint32_t* wcnt) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t s = fs[j], d = fd[j];
-    wcnt[j] = d ? static_cast<uint32_t>((s + d - window_base<STRAT, ET>(s) + kWarp - 1) / kWarp)
-                : 0u;
+    if (!d) {
+      wcnt[j] = 0;
+      continue;
+    }
+    uint64_t w = (s + d - window_base<STRAT, ET>(s) + kWarp - 1) / kWarp;
+    if (STRAT == kPacked) {
+      const uint64_t group0 = j - j % kStage;
+      for (uint64_t i = j; i > group0; --i) {
+        const uint32_t di = fd[i - 1];
+        if (di) {
+          w -= ((fs[i - 1] + di - 1) / kWarp) == (s / kWarp);
+          break;
+        }
+      }
+    }
+    wcnt[j] = static_cast<uint32_t>(w);
   }
 }
 
@@ -388,7 +411,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
       hi = min(hi, nlo + step);
       lo = nlo;
     }
-    if (lane == 0) sh_j = lo;
+    if (lane == 0) sh_j = lo - lo % kStage;  // stages are aligned groups of kStage slots
   }
   __syncthreads();
   uint64_t j = sh_j;
@@ -407,6 +430,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
     }
     __syncthreads();
     const uint64_t Wend = min(We, sh_w[kStage]);
+    const int stage_n = static_cast<int>(n - j < kStage ? n - j : kStage);  // staged slots
 
     int k = 0;  // per-warp slot cursor, monotone within this stage
     auto issue = [&](Batch<ALGO, ET, WT, U>& bt, uint64_t q0) {
@@ -427,9 +451,25 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
             while (sh_w[k + 1] <= q) ++k;
           }
           const uint64_t s0 = sh_s[k], e0 = sh_e[k];
-          if (AlgoTraits<ALGO>::has_val) bt.sval[u] = sh_v[k];
-          const uint64_t idx = window_base<STRAT, ET>(s0) + (q - sh_w[k]) * kWarp + lane;
-          bt.ok[u] = idx >= s0 && idx < e0;
+          uint64_t idx;
+          if (STRAT == kPacked) {
+            // block t of slot k's new blocks; the lane's element may belong to
+            // any staged list that shares the block: search its owner
+            const uint64_t fb = s0 / kWarp;
+            const bool shared = (sh_w[k + 1] - sh_w[k]) < ((e0 - 1) / kWarp - fb + 1);
+            idx = (fb + shared + (q - sh_w[k])) * kWarp + lane;
+            int lo = 0, hi = stage_n;  // last m with sh_s[m] <= idx
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if (sh_s[mid] <= idx) lo = mid; else hi = mid;
+            }
+            bt.ok[u] = idx >= sh_s[lo] && idx < sh_e[lo];
+            if (AlgoTraits<ALGO>::has_val) bt.sval[u] = sh_v[lo];
+          } else {
+            if (AlgoTraits<ALGO>::has_val) bt.sval[u] = sh_v[k];
+            idx = window_base<STRAT, ET>(s0) + (q - sh_w[k]) * kWarp + lane;
+            bt.ok[u] = idx >= s0 && idx < e0;
+          }
           if (bt.ok[u]) {
             bt.dst[u] = ld_list(E + idx);
             if (AlgoTraits<ALGO>::weighted) bt.wt[u] = ld_list(Wt + idx);
@@ -976,7 +1016,8 @@ cudaError_t expand_sweep(const ExpandArgs& a, int num_sms, cudaStream_t st,
 
 template <int STRAT, int ALGO, typename ET, typename WT, int U>
 cudaError_t expand_u(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t* launches) {
-  if (!a.chunk_sched) return expand_sweep<STRAT, ALGO, ET, WT, U>(a, num_sms, st, launches);
+  if (!a.chunk_sched || STRAT == kPacked)
+    return expand_sweep<STRAT, ALGO, ET, WT, U>(a, num_sms, st, launches);
   // default: 8 resident 256-thread CTAs per SM = 64 warps/SM (register-limited below)
   const int per_sm = a.ctas_per_sm > 0 ? a.ctas_per_sm : 2048 / kExpandThreads;
   const int g = grid_for((a.n + kWarp - 1) / kWarp * kWarp, kExpandThreads, num_sms, per_sm);
@@ -1038,6 +1079,7 @@ cudaError_t launch_expand(int strategy, int algo, int edge_bytes, int weight_byt
   switch (strategy) {
     case kNaive: return expand_a<kNaive>(algo, edge_bytes, weight_bytes, a, num_sms, st, launches);
     case kMerged: return expand_a<kMerged>(algo, edge_bytes, weight_bytes, a, num_sms, st, launches);
+    case kPacked: return expand_a<kPacked>(algo, edge_bytes, weight_bytes, a, num_sms, st, launches);
     default:
       return expand_a<kMergedAligned>(algo, edge_bytes, weight_bytes, a, num_sms, st, launches);
   }

@@ -13,6 +13,9 @@ import paper_2006_06890_b200 as zc
 pytestmark = pytest.mark.gpu
 
 STRATS = list(zc.AccessStrategy)
+# the reference's three + the B200 "packed" extension (identical results)
+ALL = STRATS + ["packed"]
+ALL_IDS = [getattr(s, "value", s) for s in ALL]
 CASES = small_cases()
 
 
@@ -26,7 +29,7 @@ def _run(c, strategy, placement="zerocopy", traffic=False):
     return fn()
 
 
-@pytest.mark.parametrize("strategy", STRATS, ids=[s.value for s in STRATS])
+@pytest.mark.parametrize("strategy", ALL, ids=ALL_IDS)
 def test_small_graphs_match_reference(strategy):
     bad = []
     for c in CASES:
@@ -64,7 +67,7 @@ def _mid(name, g):
     gold = goldens()[name]
     gw = zc.with_uniform_weights(g)
     gu = zc.symmetrized(g)
-    for s in STRATS:
+    for s in ALL:
         for algo, graph in (("bfs", g), ("sssp", gw), ("cc", gu)):
             if algo == "cc":
                 r = zc.cc(graph, s, collect_traffic=False)
@@ -110,7 +113,7 @@ def test_rmat_generator_vs_oracle(symmetrize):
     algos = [("cc", None)] if symmetrize else [("bfs", src), ("sssp", src)]
     for algo, s in algos:
         ref = oracle.run(algo, g, s or 0, threads=8)
-        for st in STRATS:
+        for st in ALL:
             r = zc.cc(dg, st, collect_traffic=False) if algo == "cc" else \
                 getattr(zc, algo)(dg, s, st, collect_traffic=False)
             assert np.array_equal(r.values, ref.values), (algo, st)
@@ -153,9 +156,32 @@ def test_edge_cases():
     off = np.array([0, 3] + [3 + n] * (n - 1), np.int64)
     edges = np.concatenate([[1, 2, 3], np.arange(1, n + 1) % n]).astype(np.int64)
     g = zc.CsrGraph(n, int(off[-1]), off, edges)
-    for s in STRATS:
+    for s in ALL:
         r = zc.bfs(g, 1, s, collect_traffic=False)
         assert np.array_equal(r.values, oracle.bfs(g, 1).values)
+
+
+def test_packed_many_empty_and_shared_blocks():
+    """Dense runs of tiny / empty lists sharing blocks, across the 256-slot
+    stage groups (packed windows and their owner search)."""
+    rng = np.random.default_rng(3)
+    n = 20000
+    deg = rng.choice([0, 0, 1, 2, 3, 40], size=n)
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum(deg, out=off[1:])
+    edges = rng.integers(0, n, off[-1])
+    w = rng.integers(0, 9, off[-1])
+    g = zc.CsrGraph(n, int(off[-1]), off, edges, w)
+    gu = zc.symmetrized(g)
+    src = int(np.flatnonzero(deg)[0])
+    for algo, graph in (("bfs", g), ("sssp", g), ("cc", gu)):
+        ref = oracle.run(algo, graph, src, threads=8)
+        r = zc.cc(graph, "packed", collect_traffic=False) if algo == "cc" else \
+            getattr(zc, algo)(graph, src, "packed", collect_traffic=False)
+        assert np.array_equal(r.values, ref.values), algo
+        assert r.iterations == ref.iterations and r.traversed_edges == ref.traversed_edges
+    with pytest.raises(ValueError, match="request model"):
+        zc.bfs(g, src, "packed")  # collect_traffic=True: model undefined for packed
 
 
 def test_link_probe_sane():
@@ -178,7 +204,7 @@ def test_cuda_partitions_match_reference(nparts):
     for c in [c for c in CASES if c.tag.startswith(("c8_", "pl_", "e8_")) or c.index < 11]:
         b = edge_balanced_bounds(c.graph.offsets, nparts)
         engines = [CudaPartition(local_part(c.graph, b, k), b, k) for k in range(nparts)]
-        for s in STRATS:
+        for s in ALL:
             vals, iters, trav = run_partitions_local(engines, c.algo, max(c.source, 0), s)
             if not (np.array_equal(vals, c.values) and iters == c.iterations
                     and trav == c.traversed):

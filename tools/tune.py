@@ -8,6 +8,7 @@ ap.add_argument("--scale", type=int, default=27)
 ap.add_argument("--algo", default="bfs")
 ap.add_argument("--configs", default="sched=chunk;;unroll=2;unroll=8;ctas=4;ctas=6")
 ap.add_argument("--strategy", default="merged-aligned")
+ap.add_argument("--strategies", default="")
 a = ap.parse_args()
 t = time.time()
 if a.algo == "sssp":
@@ -18,7 +19,11 @@ print(f"gen {time.time()-t:.1f}s V={dg.num_vertices} E={dg.num_edges}", flush=Tr
 src = int(zc.pick_sources(dg.as_csr(), 64, seed=7)[0])
 eb = 8 if a.algo == "sssp" else 4
 ref = None
-for cfg in a.configs.split(";"):
+runs = [(c, a.strategy) for c in a.configs.split(";")]
+if a.strategies:
+    runs = [("", s) for s in a.strategies.split(",")]
+for cfg, strategy in runs:
+    a.strategy = strategy
     os.environ["ZC_TUNE"] = cfg
     best = None
     for rep in range(3):
@@ -32,7 +37,7 @@ for cfg in a.configs.split(";"):
     prof = dg.expand_profile(best.iterations)
     top = sorted(range(best.iterations), key=lambda k: -prof[k])[:3]
     lv = " ".join(f"L{k}:{best.traversed_edges[k]*eb/prof[k]/1e6:.1f}GB/s/{prof[k]:.1f}ms" for k in top)
-    print(f"[{cfg or 'default'}] iters={best.iterations} kernel={best.kernel_ms:.2f}ms "
+    print(f"[{strategy} {cfg or 'default'}] iters={best.iterations} kernel={best.kernel_ms:.2f}ms "
           f"GTEPS={best.total_traversed_edges/best.kernel_ms/1e6:.3f} "
           f"link={best.total_traversed_edges*eb/best.expand_ms/1e6:.2f}GB/s same={same} | {lv}",
           flush=True)
