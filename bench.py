@@ -47,10 +47,14 @@ def parse():
     p.add_argument("--scale", type=int, default=27)
     p.add_argument("--edge-factor", type=int, default=16)
     p.add_argument("--seed", type=int, default=27)
-    p.add_argument("--strategy", default="merged-aligned")
+    # packed: merged-aligned line windows merged across adjacent frontier lists
+    # (B200 extension, bit-identical results); variants report all four
+    p.add_argument("--strategy", default="packed")
     p.add_argument("--no-variants", action="store_true",
                    help="skip the naive / merged / UVM / HBM comparison runs")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-configs", action="store_true",
+                   help="skip the SSSP-U27 / CC-K27 lines (BASELINE configs[2], configs[3])")
     p.add_argument("--cpu-threads", type=int, default=0)
     # test hooks for the partitioned path on a 1-GPU box
     p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
@@ -273,7 +277,7 @@ def main():
                      "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
                      "frac": achieved / PCIE_GEN5_X16_GBS,
                      "traffic": ncu.get("dram_bytes_per_launch"),
-                     "kernel": "k_expand_warp + k_expand_big (zero-copy edge stream)",
+                     "kernel": "k_expand_sweep (zero-copy edge stream)",
                      "algorithmic_bytes": "traversed edges x 4 B (u32 edge list)",
                      "peak_kind": "PCIe Gen5 x16 theoretical per direction",
                      "measured_peaks_gbs": probe,
@@ -290,6 +294,9 @@ def main():
 
     if rank == 0 and not args.no_variants and world == 1:
         line["variants"] = variants(zc, args, dg, sources, device)
+    if rank == 0 and not args.no_configs and world == 1:
+        dg.close()
+        line["configs"] = other_configs(zc, args, device)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -433,6 +440,52 @@ def _gteps(zc, dg, sources, strategy, reps=1, evict=False):
         if best is None or cur["gteps"] > best["gteps"]:
             best = cur
     return best
+
+
+def other_configs(zc, args, device) -> dict:
+    """BASELINE configs[2] (SSSP, u32 weights, uniform scale 27, edges + weights
+    zero-copy) and configs[3] (CC, Kronecker scale 27 symmetrized = 2^32 arcs),
+    one source / run each after a warm-up, merged-aligned and packed."""
+    out = {}
+    import oracle
+    u = zc.generate_uniform_device(1 << args.scale, 16, 16, seed=args.seed, weights=(8, 72),
+                                   device=device)
+    src = int(zc.pick_sources(u.as_csr(), 1, seed=7)[0])
+    for s in ("merged-aligned", "packed"):
+        zc.sssp(u, src, s, collect_traffic=False)
+        r = zc.sssp(u, src, s, collect_traffic=False)
+        out[f"sssp_uniform{args.scale}/{s}"] = {
+            "work_gteps": r.total_traversed_edges / (r.kernel_ms * 1e-3) / 1e9,
+            "kernel_ms": r.kernel_ms, "iterations": r.iterations,
+            "link_gbs": r.total_traversed_edges * 8 / (r.expand_ms * 1e-3) / 1e9,
+            "work_edges": r.total_traversed_edges}
+    t0 = time.perf_counter()
+    ref = oracle.sssp(u.as_csr(), src, threads=os.cpu_count())
+    out[f"sssp_uniform{args.scale}/cpu_port_work_gteps"] = (
+        sum(ref.traversed_edges) / (time.perf_counter() - t0) / 1e9)
+    out[f"sssp_uniform{args.scale}/bit_exact_vs_oracle"] = bool(
+        (r.values == ref.values).all() and r.iterations == ref.iterations)
+    u.close()
+    t0 = time.time()
+    k = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, symmetrize=True,
+                         device=device)
+    gen_s = time.time() - t0
+    for s in ("merged-aligned", "packed"):
+        zc.cc(k, s, collect_traffic=False)
+        r = zc.cc(k, s, collect_traffic=False)
+        out[f"cc_kron{args.scale}_sym/{s}"] = {
+            "work_gteps": r.total_traversed_edges / (r.kernel_ms * 1e-3) / 1e9,
+            "kernel_ms": r.kernel_ms, "iterations": r.iterations,
+            "link_gbs": r.total_traversed_edges * 4 / (r.expand_ms * 1e-3) / 1e9,
+            "work_edges": r.total_traversed_edges, "arcs": k.num_edges, "gen_s": gen_s}
+    t0 = time.perf_counter()
+    ref = oracle.cc(k.as_csr(), threads=os.cpu_count())
+    out[f"cc_kron{args.scale}_sym/cpu_port_work_gteps"] = (
+        sum(ref.traversed_edges) / (time.perf_counter() - t0) / 1e9)
+    out[f"cc_kron{args.scale}_sym/bit_exact_vs_oracle"] = bool(
+        (r.values == ref.values).all() and r.iterations == ref.iterations)
+    k.close()
+    return out
 
 
 def variants(zc, args, dg, sources, device) -> dict:
