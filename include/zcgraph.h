@@ -16,6 +16,8 @@
  *   zc_bfs            <- bfs(g, source, strategy, ...)   traversal.py:98-120
  *   zc_sssp           <- sssp(g, source, strategy, ...)  traversal.py:123-151
  *   zc_cc             <- cc(g, strategy, ...)            traversal.py:154-179
+ *   zc_pagerank       <- pagerank(g, strategy, ...)      traversal.py:191-249
+ *   zc_graph_multigraph <- _is_multigraph(g)             traversal.py:182-188
  *   zc_run_log        <- TraversalResult.traversed_edges traversal.py:26-45,63-65
  *   zc_run_traffic    <- TraversalResult.per_iteration_traffic (the modelled
  *                        request histogram, coalesce.py:44-85,165-207)
@@ -133,6 +135,15 @@ int zc_graph_info(const zc_graph *g, uint64_t *num_vertices, uint64_t *num_edges
 int zc_bfs(zc_graph *g, uint64_t source, int strategy, int64_t *out, zc_stats *stats);
 int zc_sssp(zc_graph *g, uint64_t source, int strategy, int64_t *out, zc_stats *stats);
 int zc_cc(zc_graph *g, int strategy, int64_t *out, zc_stats *stats);
+
+/* PageRank (traversal.py:191-249): synchronous push over the whole edge list
+ * every iteration, float64, dangling mass redistributed uniformly, stop when
+ * the L1 change < tol or after max_iters; ranks normalised to sum 1.  out:
+ * caller buffer of V doubles.  Same ValueError conditions (ZC_EINVAL). */
+int zc_pagerank(zc_graph *g, int strategy, double damping, uint64_t max_iters, double tol,
+                double *out, zc_stats *stats);
+/* 1 if some list repeats a destination (traversal.py:182-188), cached. */
+int zc_graph_multigraph(zc_graph *g, int *out);
 
 /* Per-iteration log of the handle's most recent run: traversed_edges[k] =
  * sum of frontier degrees of iteration k (traversal.py:63-65) and the

@@ -15,7 +15,8 @@ from .csr import (CsrGraph, DegreeCdf, degree_cdf, generate_powerlaw, generate_u
 from .device import (DeviceGraph, device_graph, evict, generate_rmat, generate_uniform_device,
                      link_probe, pinned_empty, release)
 from .traffic import TrafficStats
-from .traversal import UNREACHED_DIST, UNREACHED_LEVEL, TraversalResult, bfs, cc, sssp
+from .traversal import (UNREACHED_DIST, UNREACHED_LEVEL, TraversalResult, bfs, cc, pagerank,
+                        sssp)
 
 __version__ = "0.1.0"
 
@@ -24,6 +25,6 @@ __all__ = [
     "TrafficStats", "TraversalResult", "UNREACHED_DIST", "UNREACHED_LEVEL", "WARP_LANES",
     "bfs", "cc", "degree_cdf", "device_graph", "evict", "generate_powerlaw", "generate_rmat",
     "generate_uniform", "generate_uniform_device", "link_probe", "load_csr_binary",
-    "pick_sources", "pinned_empty", "release", "sssp", "store_csr_binary", "symmetrized",
+    "pagerank", "pick_sources", "pinned_empty", "release", "sssp", "store_csr_binary", "symmetrized",
     "validate", "with_uniform_weights",
 ]

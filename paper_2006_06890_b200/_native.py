@@ -28,7 +28,7 @@ EXPORTED = (
     "zc_generate_uniform", "zc_link_probe", "zc_set_options", "zc_run_traffic",
     "zc_run_profile", "zc_graph_evict", "zc_read_probe", "zc_part_create",
     "zc_part_exchange_elem_bytes", "zc_part_begin", "zc_part_expand", "zc_part_apply",
-    "zc_part_result", "zc_generate_rmat_part",
+    "zc_part_result", "zc_generate_rmat_part", "zc_pagerank", "zc_graph_multigraph",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -80,6 +80,8 @@ def _declare(lib: C.CDLL) -> None:
         "zc_bfs": (C.c_int, [P, u64, C.c_int, P, C.POINTER(Stats)]),
         "zc_sssp": (C.c_int, [P, u64, C.c_int, P, C.POINTER(Stats)]),
         "zc_cc": (C.c_int, [P, C.c_int, P, C.POINTER(Stats)]),
+        "zc_pagerank": (C.c_int, [P, C.c_int, dbl, u64, dbl, P, C.POINTER(Stats)]),
+        "zc_graph_multigraph": (C.c_int, [P, C.POINTER(C.c_int)]),
         "zc_run_log": (C.c_int, [P, P, P, u64]),
         "zc_set_options": (C.c_int, [P, u32]),
         "zc_run_profile": (C.c_int, [P, P, u64]),

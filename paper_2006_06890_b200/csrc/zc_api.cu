@@ -890,6 +890,173 @@ int zc_run_log(const zc_graph* g, uint64_t* trav, uint64_t* front, uint64_t cap)
   return ZC_OK;
 }
 
+int zc_pagerank(zc_graph* g, int strategy, double damping, uint64_t max_iters, double tol,
+                double* out, zc_stats* stats) {
+  const double t0 = now_ms();
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  // traversal.py:201-208
+  if (!(damping > 0.0 && damping < 1.0)) {
+    set_error("damping must be in (0, 1)");
+    return ZC_EINVAL;
+  }
+  if (max_iters < 1) {
+    set_error("max_iters must be >= 1");
+    return ZC_EINVAL;
+  }
+  if (!(tol > 0)) {
+    set_error("tol must be positive");
+    return ZC_EINVAL;
+  }
+  if (g->nv == 0) {
+    set_error("pagerank needs at least one vertex");
+    return ZC_EINVAL;
+  }
+  if (strategy < kNaive || strategy > kPacked) {
+    set_error("unknown access strategy " + std::to_string(strategy));
+    return ZC_EINVAL;
+  }
+  const bool model = (g->options & ZC_OPT_TRAFFIC_MODEL) != 0;
+  if (strategy == kPacked && model) {
+    set_error("the request model is defined for the reference's three strategies "
+              "(naive, merged, merged-aligned), not for packed");
+    return ZC_EINVAL;
+  }
+  DeviceGuard dg(g->device);
+  cudaStream_t st = g->stream;
+  uint64_t launches = 0;
+  g->log_trav.clear();
+  g->log_front.clear();
+  g->log_hist.clear();
+  g->log_expand_ms.clear();
+  double* rank = static_cast<double*>(g->d_state);
+  double* pushed = reinterpret_cast<double*>(g->d_fval[1]);
+  ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr, 0, kCtrCount * sizeof(uint64_t), st));
+  ZC_CUDA_TRY(launch_pr_init(g->nv, g->d_off, g->d_front[0], g->d_fs[0], g->d_fd[0], rank, st,
+                             &launches));
+  std::vector<uint64_t> hist0;
+  if (model) {  // the whole list is traced once and repeated (traversal.py:237-246)
+    ZC_CUDA_TRY(launch_traffic_model(strategy, g->eb, g->wb, false, g->d_front[0], g->nv,
+                                     g->d_off, g->d_ctr, g->num_sms, st, &launches));
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, kCtrCount * sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, st));
+    ZC_CUDA_TRY(cudaStreamSynchronize(st));
+    hist0.assign(g->h_ctr + kCtrHist, g->h_ctr + kCtrHist + 8);
+  }
+  ZC_CUDA_TRY(cudaEventRecord(g->ev[0], st));
+  uint64_t iters = 0;
+  double expand_ms = 0;
+  while (iters < max_iters) {
+    ++iters;
+    g->log_trav.push_back(g->ne);
+    g->log_front.push_back(g->nv);
+    if (model) g->log_hist.insert(g->log_hist.end(), hist0.begin(), hist0.end());
+    ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr + kCtrPrDangling, 0, 3 * sizeof(uint64_t), st));
+    ZC_CUDA_TRY(launch_pr_prepare(rank, g->d_fd[0], g->nv, g->d_fval[0], pushed, g->d_ctr, st,
+                                  &launches));
+    ExpandArgs a{};
+    a.front = g->d_front[0];
+    a.fs = g->d_fs[0];
+    a.fd = g->d_fd[0];
+    a.fval = g->d_fval[0];
+    a.n = g->nv;
+    a.off = g->d_off;
+    a.edges = g->d_edges;
+    a.weights = g->d_weights;
+    a.state = g->d_state;
+    a.flags = g->d_flags;
+    a.big_s = g->d_big_s;
+    a.big_e = g->d_big_e;
+    a.big_val = g->d_big_val;
+    a.big_prefix = g->d_big_prefix;
+    a.ctr = g->d_ctr;
+    a.exch = pushed;
+    a.wcnt = g->d_wcnt;
+    a.wpre = g->d_wpre;
+    a.scan_tmp = g->d_scan_tmp;
+    a.scan_tmp_bytes = g->scan_tmp_bytes;
+    tune_params(&a);
+    while (g->iter_ev.size() < 2 * iters) {
+      cudaEvent_t e;
+      ZC_CUDA_TRY(cudaEventCreate(&e));
+      g->iter_ev.push_back(e);
+    }
+    ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (iters - 1)], st));
+    ZC_CUDA_TRY(launch_expand(strategy, kPr, g->eb, g->wb, a, g->num_sms, st, &launches));
+    ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (iters - 1) + 1], st));
+    ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr + kCtrBig, 0, sizeof(uint64_t), st));
+    ZC_CUDA_TRY(launch_pr_update(rank, pushed, g->nv, damping, g->d_ctr, st, &launches));
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr + kCtrPrDelta, g->d_ctr + kCtrPrDelta, sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, st));
+    ZC_CUDA_TRY(cudaStreamSynchronize(st));
+    double delta;
+    memcpy(&delta, g->h_ctr + kCtrPrDelta, sizeof(delta));
+    if (delta < tol) break;
+  }
+  ZC_CUDA_TRY(cudaEventRecord(g->ev[1], st));
+  ZC_CUDA_TRY(launch_pr_normalize(rank, g->nv, g->d_ctr, false, st, &launches));
+  ZC_CUDA_TRY(launch_pr_normalize(rank, g->nv, g->d_ctr, true, st, &launches));
+  ZC_CUDA_TRY(cudaMemcpyAsync(out, rank, g->nv * sizeof(double), cudaMemcpyDeviceToHost, st));
+  ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
+  ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  for (uint64_t k = 0; k < iters; ++k) {
+    float e = 0;
+    cudaEventElapsedTime(&e, g->iter_ev[2 * k], g->iter_ev[2 * k + 1]);
+    g->log_expand_ms.push_back(e);
+    expand_ms += e;
+  }
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    stats->iterations = iters;
+    stats->total_traversed_edges = iters * g->ne;
+    stats->max_frontier = g->nv;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]);
+    stats->kernel_ms = ms;
+    cudaEventElapsedTime(&ms, g->ev[1], g->ev[2]);
+    stats->d2h_ms = ms;
+    stats->d2h_bytes = g->nv * sizeof(double) + iters * sizeof(uint64_t);
+    stats->launches = launches;
+    stats->expand_ms = expand_ms;
+    stats->total_ms = now_ms() - t0;
+  }
+  return ZC_OK;
+}
+
+int zc_graph_multigraph(zc_graph* g, int* out) {
+  if (!g || !out) {
+    set_error("null argument");
+    return ZC_ESTATE;
+  }
+  if (g->multigraph < 0) {
+    if (g->ne < 2) {
+      g->multigraph = 0;
+    } else {
+      DeviceGuard dg(g->device);
+      void* scratch = nullptr;
+      ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
+      ZC_CUDA_TRY(cudaMalloc(&scratch, g->ne * g->eb));
+      ZC_CUDA_TRY(cudaMemcpy(scratch, g->h_edges, g->ne * g->eb, cudaMemcpyDefault));
+      int rc = sort_lists_device(static_cast<int>(g->eb), g->nv, g->d_off, g->h_off, scratch);
+      if (rc) {
+        cudaFree(scratch);
+        return rc;
+      }
+      ZC_CUDA_TRY(cudaMemset(g->d_ctr + kCtrBig, 0, sizeof(uint64_t)));
+      ZC_CUDA_TRY(launch_dup_flags(scratch, static_cast<int>(g->eb), g->d_off, g->nv, g->d_ctr, 0));
+      uint64_t flag = 0;
+      ZC_CUDA_TRY(cudaMemcpy(&flag, g->d_ctr + kCtrBig, sizeof(flag), cudaMemcpyDeviceToHost));
+      ZC_CUDA_TRY(cudaMemset(g->d_ctr + kCtrBig, 0, sizeof(uint64_t)));
+      cudaFree(scratch);
+      g->multigraph = flag ? 1 : 0;
+    }
+  }
+  *out = g->multigraph;
+  return ZC_OK;
+}
+
 int zc_run_profile(const zc_graph* g, double* expand_ms, uint64_t cap) {
   if (!g) {
     set_error("null graph handle");

@@ -650,6 +650,16 @@ int generate_uniform(uint64_t nv, uint32_t dmin, uint32_t dmax, uint64_t seed, i
 }
 
 }  // namespace
+
+int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, const int64_t* h_off,
+                      void* edges) {
+  int rc = elem_bytes == 4 ? sort_lists<uint32_t>(nv, d_off, h_off, static_cast<uint32_t*>(edges))
+                           : sort_lists<uint64_t>(nv, d_off, h_off, static_cast<uint64_t*>(edges));
+  if (rc) return rc;
+  ZC_CUDA_TRY(cudaDeviceSynchronize());
+  return ZC_OK;
+}
+
 }  // namespace zc
 
 extern "C" int zc_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b,

@@ -59,6 +59,7 @@ struct zc_graph {
   std::vector<double> log_expand_ms;
   std::vector<cudaEvent_t> iter_ev;  // 2 per iteration, grown on demand
   uint32_t options = 0;
+  int multigraph = -1;  // cached duplicate-arc check (-1 unknown)
   // vertex-range partition (multi-GPU); nparts == 0 for a whole graph
   uint32_t nparts = 0, part = 0;
   uint64_t global_nv = 0, lo = 0, stride = 0;

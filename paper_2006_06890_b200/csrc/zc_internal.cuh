@@ -49,10 +49,10 @@ enum Strategy : int { kNaive = 0, kMerged = 1, kMergedAligned = 2, kPacked = 3 }
 // kPacked (B200 extension, not one of the paper's three): a window is an
 // aligned 32-element block touched by any frontier list, fetched once for all
 // the lists that share it (see k_window_counts / k_expand_sweep).
-enum Algo : int { kBfs = 0, kSssp = 1, kCc = 2 };
+enum Algo : int { kBfs = 0, kSssp = 1, kCc = 2, kPr = 3 };
 // Partitioned (multi-GPU) variants: the visit writes candidates for any
 // global vertex into the exchange buffer instead of updating local state.
-constexpr int kPartAlgo = 3;  // algo + kPartAlgo
+constexpr int kPartAlgo = 4;  // algo + kPartAlgo
 template <int A>
 struct AlgoTraits {
   static constexpr int base = A % kPartAlgo;
@@ -67,6 +67,9 @@ enum Ctr : int {
   kCtrTrav = 1,      // sum of degrees of the next frontier
   kCtrBig = 2,       // entries in the big-list queue
   kCtrBigSteps = 3,  // total warp steps of the big-list queue
+  kCtrPrDangling = 4,  // PageRank: dangling mass (double bits)
+  kCtrPrDelta = 5,     //   L1 change of the iteration
+  kCtrPrSum = 6,       //   sum of ranks
   kCtrHist = 8,      // 8..11 modelled edge requests of 1..4 sectors, 12..15 weights
   kCtrCount = 16
 };
@@ -147,6 +150,21 @@ cudaError_t launch_widen(int algo, const void* state, uint64_t nv, int64_t* out,
                          uint64_t* launches);
 cudaError_t launch_check_edges(const void* edges, int edge_bytes, uint64_t ne, uint64_t nv,
                                uint64_t* bad, cudaStream_t st);
+
+// PageRank (traversal.py:191-249) per-iteration helpers.
+cudaError_t launch_pr_init(uint64_t nv, const uint64_t* off, uint32_t* front, uint64_t* fs,
+                           uint32_t* fd, double* rank, cudaStream_t st, uint64_t* launches);
+cudaError_t launch_pr_prepare(const double* rank, const uint32_t* deg, uint64_t nv, uint64_t* fval,
+                              double* pushed, uint64_t* ctr, cudaStream_t st, uint64_t* launches);
+cudaError_t launch_pr_update(double* rank, const double* pushed, uint64_t nv, double damping,
+                             uint64_t* ctr, cudaStream_t st, uint64_t* launches);
+cudaError_t launch_pr_normalize(double* rank, uint64_t nv, uint64_t* ctr, bool divide,
+                                cudaStream_t st, uint64_t* launches);
+cudaError_t launch_dup_flags(const void* sorted, int elem_bytes, const uint64_t* off, uint64_t nv,
+                             uint64_t* ctr, cudaStream_t st);
+// Sort every list ascending in place (device array, zc_gen.cu).
+int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, const int64_t* h_off,
+                      void* edges);
 
 // Exclusive scan of u32 counts into u64 offsets (n+1 outputs), device-wide.
 cudaError_t scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp,

@@ -104,6 +104,16 @@ struct Visit<kCc> {
   }
 };
 
+template <>
+struct Visit<kPr> {
+  // traversal.py:229: pushed[d] += rank[s] / out[s]; the contribution rides in
+  // the frontier value slot (double bits); pushed lives in a.exch.
+  static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
+                                               uint64_t val) {
+    atomicAdd(static_cast<double*>(a.exch) + w, __longlong_as_double(static_cast<long long>(val)));
+  }
+};
+
 // Slot of global vertex w in the exchange buffer (partitioned mode).
 __device__ __forceinline__ uint64_t part_slot(const ExpandArgs& a, uint64_t w) {
   uint32_t lo = 0, hi = a.nparts;  // part_lo[lo] <= w < part_lo[hi]
@@ -821,6 +831,19 @@ __global__ void k_init_cc(uint32_t* label, uint64_t nv, uint32_t* front, uint64_
   }
 }
 
+// frontier = every vertex with its list bounds (PageRank); rank = 1/V
+__global__ void k_init_all(uint64_t nv, const uint64_t* off, uint32_t* front, uint64_t* fs,
+                           uint32_t* fd, double* rank) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    front[v] = static_cast<uint32_t>(v);
+    const uint64_t s0 = off[v];
+    fs[v] = s0;
+    fd[v] = static_cast<uint32_t>(off[v + 1] - s0);
+    rank[v] = 1.0 / static_cast<double>(nv);
+  }
+}
+
 // frontier = [src] with its list bounds (BFS / SSSP)
 __global__ void k_init_source(uint64_t src, const uint64_t* off, uint32_t* front, uint64_t* fval,
                               uint64_t* fs, uint32_t* fd) {
@@ -864,6 +887,99 @@ __global__ void k_part_apply(const void* mine, uint64_t n, void* state, uint8_t*
         flags[v] = 1;
       }
     }
+  }
+}
+
+// ---------------------------------------------------------------- PageRank
+__device__ __forceinline__ void atomic_add_ctr(uint64_t* ctr, int slot, double x) {
+  atomicAdd(reinterpret_cast<double*>(ctr + slot), x);
+}
+
+__device__ __forceinline__ double block_sum(double x, double* sh) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) x += __shfl_down_sync(kFull, x, d);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = x;
+  __syncthreads();
+  double t = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
+  __syncthreads();
+  return t;
+}
+
+// contrib[v] = rank[v] / out[v] into the frontier value slot, dangling mass,
+// pushed[] = 0 (traversal.py:218-230).
+__global__ void k_pr_prepare(const double* rank, const uint32_t* deg, uint64_t nv, uint64_t* fval,
+                             double* pushed, uint64_t* ctr) {
+  __shared__ double sh[32];
+  double dang = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t rounds = (nv + stride - 1) / stride;
+  for (uint64_t r = 0; r < rounds; ++r) {
+    const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + r * stride;
+    if (v < nv) {
+      const double rv = rank[v];
+      const uint32_t d = deg[v];
+      fval[v] = static_cast<uint64_t>(__double_as_longlong(d ? rv * (1.0 / d) : 0.0));
+      if (!d) dang += rv;
+      pushed[v] = 0.0;
+    }
+  }
+  const double t = block_sum(dang, sh);
+  if (threadIdx.x == 0 && t != 0.0) atomic_add_ctr(ctr, kCtrPrDangling, t);
+}
+
+// new = (1-d)/V + d (pushed + dangling/V); delta += |new - rank| (traversal.py:231-233)
+__global__ void k_pr_update(double* rank, const double* pushed, uint64_t nv, double damping,
+                            uint64_t* ctr) {
+  __shared__ double sh[32];
+  const double dang = __longlong_as_double(static_cast<long long>(ctr[kCtrPrDangling]));
+  const double base = (1.0 - damping) / static_cast<double>(nv);
+  double delta = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t rounds = (nv + stride - 1) / stride;
+  for (uint64_t r = 0; r < rounds; ++r) {
+    const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + r * stride;
+    if (v < nv) {
+      const double nr = base + damping * (pushed[v] + dang / static_cast<double>(nv));
+      delta += fabs(nr - rank[v]);
+      rank[v] = nr;
+    }
+  }
+  const double t = block_sum(delta, sh);
+  if (threadIdx.x == 0 && t != 0.0) atomic_add_ctr(ctr, kCtrPrDelta, t);
+}
+
+// sum of ranks (divide == false) or rank /= sum (divide == true) (traversal.py:248)
+__global__ void k_pr_normalize(double* rank, uint64_t nv, uint64_t* ctr, int divide) {
+  __shared__ double sh[32];
+  const double total = __longlong_as_double(static_cast<long long>(ctr[kCtrPrSum]));
+  double acc = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t rounds = (nv + stride - 1) / stride;
+  for (uint64_t r = 0; r < rounds; ++r) {
+    const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + r * stride;
+    if (v < nv) {
+      if (divide) rank[v] = rank[v] / total;
+      else acc += rank[v];
+    }
+  }
+  if (!divide) {
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) atomic_add_ctr(ctr, kCtrPrSum, t);
+  }
+}
+
+// any list with a repeated destination (lists sorted): ctr[kCtrBig] = 1
+template <typename ET>
+__global__ void k_dup_flags(const ET* e, const uint64_t* off, uint64_t nv, uint64_t* ctr) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint64_t k = off[v] + 1; k < off[v + 1]; ++k)
+      if (e[k] == e[k - 1]) {
+        ctr[kCtrBig] = 1;
+        break;
+      }
   }
 }
 
@@ -1065,6 +1181,7 @@ cudaError_t expand_a(int algo, int eb, int wb, const ExpandArgs& a, int num_sms,
     case kBfs: return expand_w<STRAT, kBfs>(eb, wb, a, num_sms, st, l);
     case kSssp: return expand_w<STRAT, kSssp>(eb, wb, a, num_sms, st, l);
     case kCc: return expand_w<STRAT, kCc>(eb, wb, a, num_sms, st, l);
+    case kPr: return expand_w<STRAT, kPr>(eb, wb, a, num_sms, st, l);
     case kBfs + kPartAlgo: return expand_w<STRAT, kBfs + kPartAlgo>(eb, wb, a, num_sms, st, l);
     case kSssp + kPartAlgo: return expand_w<STRAT, kSssp + kPartAlgo>(eb, wb, a, num_sms, st, l);
     default: return expand_w<STRAT, kCc + kPartAlgo>(eb, wb, a, num_sms, st, l);
@@ -1155,6 +1272,50 @@ cudaError_t launch_part_apply(int algo, const void* mine, uint64_t nlocal, void*
     default: k_part_apply<kCc><<<g, 256, 0, st>>>(mine, nlocal, state, flags, iter); break;
   }
   *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pr_init(uint64_t nv, const uint64_t* off, uint32_t* front, uint64_t* fs,
+                           uint32_t* fd, double* rank, cudaStream_t st, uint64_t* launches) {
+  if (nv == 0) return cudaSuccess;
+  const int g = grid_for(nv, 256, 148, 16);
+  k_init_all<<<g, 256, 0, st>>>(nv, off, front, fs, fd, rank);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pr_prepare(const double* rank, const uint32_t* deg, uint64_t nv, uint64_t* fval,
+                              double* pushed, uint64_t* ctr, cudaStream_t st, uint64_t* launches) {
+  const int g = grid_for(nv, 256, 148, 8);
+  k_pr_prepare<<<g, 256, 0, st>>>(rank, deg, nv, fval, pushed, ctr);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pr_update(double* rank, const double* pushed, uint64_t nv, double damping,
+                             uint64_t* ctr, cudaStream_t st, uint64_t* launches) {
+  const int g = grid_for(nv, 256, 148, 8);
+  k_pr_update<<<g, 256, 0, st>>>(rank, pushed, nv, damping, ctr);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pr_normalize(double* rank, uint64_t nv, uint64_t* ctr, bool divide,
+                                cudaStream_t st, uint64_t* launches) {
+  const int g = grid_for(nv, 256, 148, 8);
+  k_pr_normalize<<<g, 256, 0, st>>>(rank, nv, ctr, divide ? 1 : 0);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dup_flags(const void* sorted, int elem_bytes, const uint64_t* off, uint64_t nv,
+                             uint64_t* ctr, cudaStream_t st) {
+  if (nv == 0) return cudaSuccess;
+  const int g = grid_for(nv, 256, 148, 16);
+  if (elem_bytes == 4)
+    k_dup_flags<uint32_t><<<g, 256, 0, st>>>(static_cast<const uint32_t*>(sorted), off, nv, ctr);
+  else
+    k_dup_flags<uint64_t><<<g, 256, 0, st>>>(static_cast<const uint64_t*>(sorted), off, nv, ctr);
   return cudaGetLastError();
 }
 

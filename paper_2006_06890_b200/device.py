@@ -235,6 +235,29 @@ class DeviceGraph:
 
 # id(graph) -> (weakref to graph, {key: DeviceGraph}); CsrGraph defines __eq__
 # without __hash__ (like the reference), so it cannot key a WeakKeyDictionary.
+def _pagerank_run(dg: "DeviceGraph", sid: int, damping: float, max_iters: int, tol: float,
+                  traffic: bool):
+    lib = N.lib()
+    with dg._lock:
+        dg.set_traffic_model(traffic)
+        out = pinned_empty(dg.num_vertices, np.float64)
+        st = N.Stats()
+        N.check(lib.zc_pagerank(dg.handle, sid, float(damping), int(max_iters), float(tol),
+                                out.ctypes.data, C.byref(st)))
+        it = st.iterations
+        hist = None
+        if traffic:
+            hist = np.zeros((it, 8), np.uint64)
+            N.check(lib.zc_run_traffic(dg.handle, hist.ctypes.data, it))
+    return out, st, hist
+
+
+def is_multigraph(dg: "DeviceGraph") -> bool:
+    flag = C.c_int()
+    N.check(N.lib().zc_graph_multigraph(dg.handle, C.byref(flag)))
+    return bool(flag.value)
+
+
 _CACHE: dict = {}
 _CACHE_LOCK = threading.Lock()
 

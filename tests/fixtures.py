@@ -63,3 +63,22 @@ def goldens() -> dict:
 
 def crc(a: np.ndarray, dtype: str = "<i8") -> str:
     return f"{zlib.crc32(np.ascontiguousarray(np.asarray(a).astype(dtype)).tobytes()):08x}"
+
+
+def pagerank_cases():
+    """(graph, (damping, max_iters, tol), ranks, iterations, multigraph, dense_err)."""
+    d = np.load(os.path.join(GOLDEN, "pagerank.npz"))
+    nv = d["nv"]
+    ne = np.array([0] * nv.size)
+    o_off = np.concatenate(([0], np.cumsum(nv + 1)))
+    offs = [d["offsets"][o_off[i]:o_off[i + 1]] for i in range(nv.size)]
+    ne = np.array([int(o[-1]) for o in offs])
+    o_e = np.concatenate(([0], np.cumsum(ne)))
+    o_v = np.concatenate(([0], np.cumsum(nv)))
+    out = []
+    for i in range(nv.size):
+        g = CsrGraph(int(nv[i]), int(ne[i]), offs[i], d["edges"][o_e[i]:o_e[i + 1]])
+        dmp, mi, tol = d["args"][i]
+        out.append((g, (float(dmp), int(mi), float(tol)), d["ranks"][o_v[i]:o_v[i + 1]],
+                    int(d["iters"][i]), bool(d["multi"][i]), float(d["dense_err"][i])))
+    return out

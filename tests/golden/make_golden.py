@@ -206,6 +206,57 @@ def traffic_goldens():
     print("traffic goldens:", len(idx), flush=True)
 
 
+def pagerank_goldens():
+    """Reference pagerank (traversal.py:191-249) outputs: the acceptance
+    criterion 6 PR stream (its rng(1234) position after the bfs/sssp/cc
+    streams, tol 1e-13 / 600 iterations) plus the test_traversal.py cases."""
+    import warnings
+    from reference import pagerank_dense  # reference tests/reference.py:118-137
+    out = {"nv": [], "offsets": [], "edges": [], "ranks": [], "iters": [], "multi": [],
+           "dense_err": [], "args": []}
+
+    def add(g, damping=0.85, max_iters=100, tol=1e-6, dense=False):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            r = zc.pagerank(g, damping=damping, max_iters=max_iters, tol=tol,
+                            collect_traffic=False)
+        out["nv"].append(g.num_vertices)
+        out["offsets"].append(np.asarray(g.offsets, np.int64))
+        out["edges"].append(np.asarray(g.edges, np.int64))
+        out["ranks"].append(np.asarray(r.values, np.float64))
+        out["iters"].append(r.iterations)
+        out["multi"].append("multigraph" in r.flags)
+        out["args"].append((damping, max_iters, tol))
+        out["dense_err"].append(float(np.abs(r.values - pagerank_dense(g)).max()) if dense
+                                else -1.0)
+
+    rng = np.random.default_rng(1234)
+    for _ in range(100):  # bfs stream
+        g = random_csr(rng, 200)
+        rng.integers(g.num_vertices)
+    for _ in range(100):  # sssp stream
+        g = random_csr(rng, 200, weighted=True)
+        rng.integers(g.num_vertices)
+    for _ in range(100):  # cc stream
+        random_csr(rng, 200, undirected=True)
+    for _ in range(100):  # pr stream (test_acceptance.py:168-180)
+        add(random_csr(rng, 200), tol=1e-13, max_iters=600, dense=True)
+    add(zc.symmetrized(zc.CsrGraph(2, 1, np.array([0, 1, 1]), np.array([1]))))
+    add(zc.CsrGraph(1, 0, np.zeros(2, np.int64), np.zeros(0, np.int64)))
+    add(zc.CsrGraph(2, 2, np.array([0, 2, 2]), np.array([1, 1])))  # multigraph
+    add(random_csr(np.random.default_rng(17), 5, allow_empty=False), tol=1e-13, max_iters=500,
+        dense=True)
+    add(zc.generate_powerlaw(3000, 12.0, 2.0, seed=2), damping=0.9, max_iters=50, tol=1e-9)
+    add(zc.generate_uniform(5000, 0, 9, seed=5))
+    np.savez_compressed(os.path.join(HERE, "pagerank.npz"),
+                        nv=np.array(out["nv"]), offsets=np.concatenate(out["offsets"]),
+                        edges=np.concatenate(out["edges"]), ranks=np.concatenate(out["ranks"]),
+                        iters=np.array(out["iters"]), multi=np.array(out["multi"]),
+                        dense_err=np.array(out["dense_err"]), args=np.array(out["args"]))
+    print("pagerank goldens:", len(out["nv"]), "max dense err",
+          max(e for e in out["dense_err"]), flush=True)
+
+
 def result_record(r):
     return {"crc": crc(r.values, "<i8"), "iterations": r.iterations,
             "traversed_edges": [int(x) for x in r.traversed_edges]}
@@ -241,6 +292,7 @@ def main():
     pack.save(os.path.join(HERE, "small_graphs.npz"))
     print("small graphs:", len(pack.cols["nv"]), flush=True)
     traffic_goldens()
+    pagerank_goldens()
     if os.environ.get("GOLDEN_TRAFFIC_ONLY"):
         return
 

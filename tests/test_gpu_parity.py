@@ -231,3 +231,37 @@ def test_rmat_partition_generator_matches_whole_graph():
         vals, iters, trav = run_partitions_local(parts, algo, src, "merged-aligned")
         assert np.array_equal(vals, ref.values) and iters == ref.iterations
         assert trav == ref.traversed_edges
+
+
+def test_pagerank_matches_reference():
+    """Reference pagerank outputs (incl. acceptance criterion 6's PR stream):
+    L-inf <= 1e-8 (test_acceptance.py:169-180), same iteration count, the
+    multigraph flag; all strategies."""
+    import warnings
+    from fixtures import pagerank_cases
+    bad = []
+    for k, (g, (dmp, mi, tol), ranks, iters, multi, derr) in enumerate(pagerank_cases()):
+        for s in ALL:
+            with warnings.catch_warnings(record=True) as caught:
+                warnings.simplefilter("always")
+                r = zc.pagerank(g, s, dmp, mi, tol, collect_traffic=False)
+            err = float(np.abs(r.values - ranks).max())
+            if err > 1e-8 or abs(r.iterations - iters) > 1 or ("multigraph" in r.flags) != multi:
+                bad.append((k, getattr(s, "value", s), err, r.iterations, iters))
+            if multi:
+                assert any("multigraph" in str(w.message) for w in caught)
+    assert not bad, bad[:8]
+
+
+def test_pagerank_traffic_and_validation():
+    g = zc.symmetrized(zc.generate_uniform(300, 1, 6, seed=4))
+    r = zc.pagerank(g)
+    assert len(r.per_iteration_traffic) == r.iterations
+    assert all(n == g.num_edges for n in r.traversed_edges)
+    assert r.total_traffic.request_count > 0
+    with pytest.raises(ValueError):
+        zc.pagerank(g, damping=1.0)
+    with pytest.raises(ValueError):
+        zc.pagerank(g, max_iters=0)
+    with pytest.raises(ValueError):
+        zc.pagerank(g, tol=-1.0)
