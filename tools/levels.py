@@ -10,10 +10,15 @@ ap.add_argument("--ef", type=int, default=16)
 ap.add_argument("--algo", default="bfs")
 ap.add_argument("--strategies", default="merged-aligned,merged")
 ap.add_argument("--placement", default="zerocopy")
+ap.add_argument("--uniform", action="store_true")
 a = ap.parse_args()
 t = time.time()
-dg = zc.generate_rmat(a.scale, a.ef, seed=27, symmetrize=a.algo == "cc",
-                      weights=(8, 72) if a.algo == "sssp" else None, placement=a.placement)
+if a.algo == "sssp" and a.uniform:
+    dg = zc.generate_uniform_device(1 << a.scale, 16, 16, seed=27, weights=(8, 72),
+                                    placement=a.placement)
+else:
+    dg = zc.generate_rmat(a.scale, a.ef, seed=27, symmetrize=a.algo == "cc",
+                          weights=(8, 72) if a.algo == "sssp" else None, placement=a.placement)
 print(f"gen {time.time()-t:.1f}s V={dg.num_vertices} E={dg.num_edges}", flush=True)
 src = int(zc.pick_sources(dg.as_csr(), 64, seed=7)[0])
 eb = 8 if a.algo == "sssp" else 4
