@@ -292,11 +292,16 @@ def main():
         threads = args.cpu_threads or os.cpu_count()
         line["cpu_baseline"] = cpu_baseline(g, sources, threads)
 
+    # configs before the UVM variants: managed-memory runs leave the process
+    # slower on later zero-copy work (measured), so UVM goes last
     if rank == 0 and not args.no_variants and world == 1:
-        line["variants"] = variants(zc, args, dg, sources, device)
+        line["variants"] = variants(zc, args, dg, sources, device, phase="zerocopy")
+    dg.close()
     if rank == 0 and not args.no_configs and world == 1:
-        dg.close()
         line["configs"] = other_configs(zc, args, device)
+    if rank == 0 and not args.no_variants and world == 1:
+        line["variants"].update(variants(zc, args, None, sources, device, phase="placements"))
+        finish_variants(line["variants"])
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -488,16 +493,18 @@ def other_configs(zc, args, device) -> dict:
     return out
 
 
-def variants(zc, args, dg, sources, device) -> dict:
-    """configs[1]'s comparison: naive vs merged vs merged+aligned (zero-copy),
-    UVM (cold, merged+aligned) and the in-HBM control."""
+def variants(zc, args, dg, sources, device, phase: str) -> dict:
+    """configs[1]'s comparison: naive vs merged vs merged+aligned vs packed
+    (zero-copy), then the in-HBM control and UVM (cold; and at the reference's
+    25% capacity)."""
     out = {}
-    for s in ("naive", "merged", "merged-aligned", "packed"):
-        # naive walks each hub list with one thread (seconds per BFS): one rep
-        out[f"zerocopy/{s}"] = _gteps(zc, dg, sources, s, reps=1 if s == "naive" else 2)
-    dg.close()
+    if phase == "zerocopy":
+        for s in ("naive", "merged", "merged-aligned", "packed"):
+            # naive walks each hub list with one thread (seconds per BFS): one rep
+            out[f"zerocopy/{s}"] = _gteps(zc, dg, sources, s, reps=1 if s == "naive" else 2)
+        return out
     import torch
-    for placement in ("uvm", "hbm"):
+    for placement in ("hbm", "uvm"):
         h = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, device=device,
                              placement=placement)
         out[f"{placement}/merged-aligned"] = _gteps(zc, h, sources, "merged-aligned", reps=2,
@@ -515,12 +522,15 @@ def variants(zc, args, dg, sources, device) -> dict:
             del ballast
             torch.cuda.empty_cache()
         h.close()
-    zc_ = out["zerocopy/merged-aligned"]["gteps"]
-    out["speedup_vs_uvm"] = zc_ / out["uvm/merged-aligned"]["gteps"]
-    out["speedup_vs_uvm_cap25"] = zc_ / out["uvm_cap25/merged-aligned"]["gteps"]
-    out["packed_speedup_vs_uvm_cap25"] = (out["zerocopy/packed"]["gteps"]
-                                          / out["uvm_cap25/merged-aligned"]["gteps"])
     return out
+
+
+def finish_variants(v: dict) -> None:
+    ma = v["zerocopy/merged-aligned"]["gteps"]
+    v["speedup_vs_uvm"] = ma / v["uvm/merged-aligned"]["gteps"]
+    v["speedup_vs_uvm_cap25"] = ma / v["uvm_cap25/merged-aligned"]["gteps"]
+    v["packed_speedup_vs_uvm_cap25"] = (v["zerocopy/packed"]["gteps"]
+                                        / v["uvm_cap25/merged-aligned"]["gteps"])
 
 
 if __name__ == "__main__":

@@ -229,6 +229,20 @@ int zc_part_expand(zc_graph *g, void *exchange /* device pointer */);
 int zc_part_apply(zc_graph *g, const void *mine /* device pointer, stride slots */,
                   uint64_t *n_next, uint64_t *traversed_next);
 int zc_part_result(zc_graph *g, int64_t *out_local /* range size */, zc_stats *stats);
+/* Fused exchange (no reduce-scatter): the expand kernel writes each candidate
+ * straight into its owner's buffer -- peer memory over NVLink (CUDA IPC) --
+ * BFS: byte stores, deduplicated per iteration; SSSP / CC: atomicMin
+ * reductions.  Per iteration: every rank zc_part_fused_reset; barrier;
+ * zc_part_fused_expand; barrier; zc_part_apply(g, local, ...).
+ * init allocates this rank's buffer (stride slots) and exports its IPC
+ * handle (64 bytes, may be NULL); connect opens the other ranks' handles
+ * (nparts * 64 bytes, own slot ignored) or, for parts sharing one device and
+ * process, takes raw device pointers (ptrs, nparts entries). */
+int zc_part_fused_init(zc_graph *g, int algo, void *ipc_handle_out, void **local_buffer);
+int zc_part_fused_connect(zc_graph *g, const void *ipc_handles, void *const *ptrs);
+int zc_part_fused_reset(zc_graph *g);
+int zc_part_fused_expand(zc_graph *g);
+
 /* Part `part` of the directed graph zc_generate_rmat builds with the same
  * parameters (same arcs, same list order), edge-balanced across nparts;
  * bounds (nparts+1) receives the vertex ranges of all parts. */

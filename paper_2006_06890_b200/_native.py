@@ -29,6 +29,7 @@ EXPORTED = (
     "zc_run_profile", "zc_graph_evict", "zc_read_probe", "zc_part_create",
     "zc_part_exchange_elem_bytes", "zc_part_begin", "zc_part_expand", "zc_part_apply",
     "zc_part_result", "zc_generate_rmat_part", "zc_pagerank", "zc_graph_multigraph",
+    "zc_part_fused_init", "zc_part_fused_connect", "zc_part_fused_reset", "zc_part_fused_expand",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -102,6 +103,10 @@ def _declare(lib: C.CDLL) -> None:
         "zc_part_expand": (C.c_int, [P, P]),
         "zc_part_apply": (C.c_int, [P, P, C.POINTER(u64), C.POINTER(u64)]),
         "zc_part_result": (C.c_int, [P, P, C.POINTER(Stats)]),
+        "zc_part_fused_init": (C.c_int, [P, C.c_int, P, C.POINTER(P)]),
+        "zc_part_fused_connect": (C.c_int, [P, P, P]),
+        "zc_part_fused_reset": (C.c_int, [P]),
+        "zc_part_fused_expand": (C.c_int, [P]),
         "zc_generate_rmat_part": (C.c_int, [u32, u32, dbl, dbl, dbl, u64, i64, i64, u32, u32, i32,
                                             i32, P, C.POINTER(P)]),
     }

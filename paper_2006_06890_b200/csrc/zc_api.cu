@@ -136,6 +136,10 @@ void zc::free_graph(zc_graph* g) {
   cudaFree(g->d_big_prefix);
   cudaFree(g->d_ctr);
   cudaFree(g->d_part_lo);
+  for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
+  cudaFree(g->d_mine);
+  cudaFree(g->d_peers);
+  cudaFree(g->d_sent);
   cudaFree(g->d_wcnt);
   cudaFree(g->d_wpre);
   cudaFree(g->d_scan_tmp);
@@ -732,15 +736,22 @@ int zc_part_begin(zc_graph* g, int algo, uint64_t src, int strategy, uint64_t* n
   return ZC_OK;
 }
 
-int zc_part_expand(zc_graph* g, void* exch) {
+static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
   if (!g || !g->nparts || g->p_algo < 0) {
     set_error("zc_part_begin first");
+    return ZC_ESTATE;
+  }
+  if (fused && (!g->d_peers || g->fused_algo != g->p_algo)) {
+    set_error("fused exchange not initialised for this algorithm (zc_part_fused_init/connect)");
     return ZC_ESTATE;
   }
   DeviceGuard dg(g->device);
   cudaStream_t st = g->stream;
   const int algo = g->p_algo;
-  ZC_CUDA_TRY(launch_fill_exchange(algo, exch, g->nparts * g->stride, st, &g->p_launches));
+  if (!fused)
+    ZC_CUDA_TRY(launch_fill_exchange(algo, exch, g->nparts * g->stride, st, &g->p_launches));
+  else if (algo == kBfs)
+    ZC_CUDA_TRY(cudaMemsetAsync(g->d_sent, 0, (g->global_nv + 31) / 32 * 4, st));
   ++g->p_iter;
   g->log_front.push_back(g->p_n);
   while (g->iter_ev.size() < 2 * g->p_iter) {
@@ -770,6 +781,8 @@ int zc_part_expand(zc_graph* g, void* exch) {
   a.part_lo = g->d_part_lo;
   a.nparts = g->nparts;
   a.stride = g->stride;
+  a.peers = fused ? g->d_peers : nullptr;
+  a.sent = fused && algo == kBfs ? g->d_sent : nullptr;
   a.wcnt = g->d_wcnt;
   a.wpre = g->d_wpre;
   a.scan_tmp = g->d_scan_tmp;
@@ -785,6 +798,75 @@ int zc_part_expand(zc_graph* g, void* exch) {
   g->log_expand_ms.push_back(ms);
   return ZC_OK;
 }
+
+int zc_part_expand(zc_graph* g, void* exch) { return part_expand_impl(g, exch, false); }
+
+int zc_part_fused_init(zc_graph* g, int algo, void* ipc_handle, void** local) {
+  if (!g || !g->nparts) {
+    set_error("not a partition handle");
+    return ZC_ESTATE;
+  }
+  if (algo < kBfs || algo > kCc) {
+    set_error("unknown algorithm");
+    return ZC_EINVAL;
+  }
+  DeviceGuard dg(g->device);
+  if (!g->d_mine) {
+    ZC_CUDA_TRY(cudaMalloc(&g->d_mine, std::max<uint64_t>(g->stride, 1) * sizeof(uint64_t)));
+    ZC_CUDA_TRY(cudaMalloc(&g->d_peers, g->nparts * sizeof(void*)));
+    ZC_CUDA_TRY(cudaMalloc(&g->d_sent, (g->global_nv + 31) / 32 * 4 + 4));
+  }
+  g->fused_algo = algo;
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    ZC_CUDA_TRY(cudaIpcGetMemHandle(&h, g->d_mine));
+    memcpy(ipc_handle, &h, sizeof(h));
+  }
+  if (local) *local = g->d_mine;
+  return ZC_OK;
+}
+
+int zc_part_fused_connect(zc_graph* g, const void* handles, void* const* ptrs) {
+  if (!g || !g->d_mine) {
+    set_error("zc_part_fused_init first");
+    return ZC_ESTATE;
+  }
+  DeviceGuard dg(g->device);
+  for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
+  g->ipc_opened.clear();
+  std::vector<void*> peers(g->nparts);
+  for (uint32_t k = 0; k < g->nparts; ++k) {
+    if (k == g->part) {
+      peers[k] = g->d_mine;
+    } else if (ptrs) {
+      peers[k] = ptrs[k];  // same-process device pointers (one-GPU validation)
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, static_cast<const char*>(handles) + k * sizeof(h), sizeof(h));
+      void* p = nullptr;
+      ZC_CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      g->ipc_opened.push_back(p);
+      peers[k] = p;
+    }
+  }
+  ZC_CUDA_TRY(cudaMemcpy(g->d_peers, peers.data(), g->nparts * sizeof(void*),
+                         cudaMemcpyHostToDevice));
+  return ZC_OK;
+}
+
+int zc_part_fused_reset(zc_graph* g) {
+  if (!g || !g->d_mine || g->fused_algo < 0) {
+    set_error("zc_part_fused_init first");
+    return ZC_ESTATE;
+  }
+  DeviceGuard dg(g->device);
+  ZC_CUDA_TRY(launch_fill_exchange(g->fused_algo, g->d_mine, g->stride, g->stream,
+                                   &g->p_launches));
+  ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  return ZC_OK;
+}
+
+int zc_part_fused_expand(zc_graph* g) { return part_expand_impl(g, nullptr, true); }
 
 int zc_part_apply(zc_graph* g, const void* mine, uint64_t* n_next, uint64_t* trav_next) {
   if (!g || !g->nparts || g->p_algo < 0 || g->p_iter == 0) {

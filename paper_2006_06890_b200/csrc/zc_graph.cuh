@@ -64,6 +64,13 @@ struct zc_graph {
   uint32_t nparts = 0, part = 0;
   uint64_t global_nv = 0, lo = 0, stride = 0;
   uint64_t* d_part_lo = nullptr;  // nparts + 1
+  // fused exchange: own candidate buffer (stride slots of <= 8 bytes), the
+  // owners' buffers (device array of nparts pointers), IPC-opened peers
+  void* d_mine = nullptr;
+  void** d_peers = nullptr;
+  uint32_t* d_sent = nullptr;  // BFS: discoveries already sent this iteration
+  std::vector<void*> ipc_opened;
+  int fused_algo = -1;
   // stepped run state (zc_part_begin / expand / apply)
   int p_algo = -1, p_strategy = 0, p_cur = 0;
   uint64_t p_iter = 0, p_n = 0, p_launches = 0;

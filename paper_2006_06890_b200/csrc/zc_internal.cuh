@@ -98,6 +98,10 @@ struct ExpandArgs {
   const uint64_t* part_lo;  // nparts + 1 range starts (device)
   uint32_t nparts;
   uint64_t stride;
+  // fused mode: owners' buffers reached directly (NVLink peer pointers);
+  // `sent` dedups BFS discoveries per iteration (global V bits)
+  void* const* peers;
+  uint32_t* sent;
   // CTA-sweep scheduling: per-slot window counts, their exclusive prefix
   uint32_t* wcnt;
   uint64_t* wpre;  // n + 1

@@ -114,21 +114,35 @@ struct Visit<kPr> {
   }
 };
 
-// Slot of global vertex w in the exchange buffer (partitioned mode).
-__device__ __forceinline__ uint64_t part_slot(const ExpandArgs& a, uint64_t w) {
+// Owner part of global vertex w.
+__device__ __forceinline__ uint32_t part_of(const ExpandArgs& a, uint64_t w) {
   uint32_t lo = 0, hi = a.nparts;  // part_lo[lo] <= w < part_lo[hi]
   while (hi - lo > 1) {
     const uint32_t mid = (lo + hi) >> 1;
     if (a.part_lo[mid] <= w) lo = mid; else hi = mid;
   }
-  return lo * a.stride + (w - a.part_lo[lo]);
+  return lo;
+}
+
+// Candidate slot of w: in the local exchange buffer (reduce-scatter mode) or,
+// fused mode, directly in the owner's buffer (peer pointer over NVLink).
+template <typename T>
+__device__ __forceinline__ T* cand_slot(const ExpandArgs& a, uint64_t w) {
+  const uint32_t k = part_of(a, w);
+  if (a.peers) return static_cast<T*>(a.peers[k]) + (w - a.part_lo[k]);
+  return static_cast<T*>(a.exch) + (k * a.stride + (w - a.part_lo[k]));
 }
 
 template <>
 struct Visit<kBfs + kPartAlgo> {
   static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
                                                uint64_t) {
-    static_cast<uint8_t*>(a.exch)[part_slot(a, w)] = 1;
+    if (a.sent) {  // send each discovery once per iteration
+      uint32_t* word = a.sent + (w >> 5);
+      const uint32_t bit = 1u << (w & 31);
+      if ((*word & bit) || (atomicOr(word, bit) & bit)) return;
+    }
+    *cand_slot<uint8_t>(a, w) = 1;
   }
 };
 
@@ -136,9 +150,10 @@ template <>
 struct Visit<kSssp + kPartAlgo> {
   static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t wt,
                                                uint64_t val) {
-    unsigned long long* x = static_cast<unsigned long long*>(a.exch) + part_slot(a, w);
+    unsigned long long* x = cand_slot<unsigned long long>(a, w);
     const unsigned long long cand = val + wt;
-    if (cand < *x) atomicMin(x, cand);
+    if (a.peers) atomicMin(x, cand);  // remote: reduction, no read-back
+    else if (cand < *x) atomicMin(x, cand);
   }
 };
 
@@ -146,9 +161,10 @@ template <>
 struct Visit<kCc + kPartAlgo> {
   static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
                                                uint64_t val) {
-    unsigned* x = static_cast<unsigned*>(a.exch) + part_slot(a, w);
+    unsigned* x = cand_slot<unsigned>(a, w);
     const unsigned cand = static_cast<unsigned>(val);
-    if (cand < *x) atomicMin(x, cand);
+    if (a.peers) atomicMin(x, cand);
+    else if (cand < *x) atomicMin(x, cand);
   }
 };
 

@@ -165,6 +165,33 @@ class CudaPartition:
         return CsrGraph(dg.num_vertices, dg.num_edges, off, edges, weights, dg.edge_elem_bytes,
                         dg.weight_elem_bytes, dg.directed)
 
+    # -- fused exchange (candidates written straight into the owners' buffers)
+    def fused_init(self, algo: str) -> tuple[bytes, int]:
+        handle = (C.c_char * 64)()
+        local = C.c_void_p()
+        N.check(N.lib().zc_part_fused_init(self._h, ALGO_IDS[algo], handle, C.byref(local)))
+        return bytes(handle), local.value
+
+    def fused_connect(self, handles: Optional[Sequence[bytes]] = None,
+                      ptrs: Optional[Sequence[int]] = None) -> None:
+        if ptrs is not None:
+            arr = (C.c_void_p * len(ptrs))(*ptrs)
+            N.check(N.lib().zc_part_fused_connect(self._h, None, arr))
+        else:
+            blob = b"".join(handles)
+            N.check(N.lib().zc_part_fused_connect(self._h, blob, None))
+
+    def fused_reset(self) -> None:
+        N.check(N.lib().zc_part_fused_reset(self._h))
+
+    def fused_expand(self) -> None:
+        N.check(N.lib().zc_part_fused_expand(self._h))
+
+    def apply_ptr(self, ptr: int) -> tuple[int, int]:
+        n, t = C.c_uint64(), C.c_uint64()
+        N.check(N.lib().zc_part_apply(self._h, ptr, C.byref(n), C.byref(t)))
+        return n.value, t.value
+
     def result(self) -> np.ndarray:
         from .device import pinned_empty
         out = pinned_empty(self.num_local, np.int64)
@@ -210,7 +237,7 @@ def _torch_dtype(algo: str):
 
 def run_partition(engine: Engine, algo: str, source: int, strategy, *, group=None,
                   tensor_device=None, stage_host: bool = False, fetch: bool = True,
-                  buffers=None) -> PartResult:
+                  buffers=None, fused: bool = False) -> PartResult:
     """SPMD driver: call on every rank of `group` with that rank's engine.
 
     stage_host: run the collectives on host copies of the exchange buffers
@@ -223,6 +250,8 @@ def run_partition(engine: Engine, algo: str, source: int, strategy, *, group=Non
 
     if algo not in ALGO_IDS:
         raise ValueError(f"unknown algorithm {algo!r}")
+    if fused:
+        return _run_partition_fused(engine, algo, source, strategy, group, fetch)
     nparts = dist.get_world_size(group)
     stride = engine.stride
     dev = tensor_device if tensor_device is not None else torch.device("cuda", engine.device)
@@ -260,6 +289,45 @@ def run_partition(engine: Engine, algo: str, source: int, strategy, *, group=Non
     return PartResult(algo, engine.lo, values, iters, trav, front)
 
 
+def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartResult:
+    """Fused exchange: the expand kernel stores / atomicMin's each candidate
+    directly into its owner's buffer over NVLink (CUDA IPC peer pointers);
+    two barriers per level replace the reduce-scatter."""
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", engine.device)
+    handle, local = engine.fused_init(algo)
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, handle, group=group)
+    engine.fused_connect(handles=handles)
+    counts = torch.zeros(2, dtype=torch.int64, device=dev)
+
+    def sync_all():
+        counts.zero_()
+        dist.all_reduce(counts, group=group)  # doubles as a device-ordered barrier
+        torch.cuda.current_stream(dev).synchronize()
+
+    def global_counts(n: int, t: int) -> tuple[int, int]:
+        counts[0], counts[1] = n, t
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+        return int(counts[0]), int(counts[1])
+
+    n, t = global_counts(*engine.begin(algo, source, strategy))
+    iters, trav, front = 0, [], []
+    while n > 0:
+        iters += 1
+        trav.append(t)
+        front.append(n)
+        engine.fused_reset()
+        sync_all()              # every owner buffer reset before anyone writes
+        engine.fused_expand()   # kernel done (its peer stores performed) on return
+        sync_all()              # every rank's candidates delivered
+        n, t = global_counts(*engine.apply_ptr(local))
+    values = engine.result() if fetch else None
+    return PartResult(algo, engine.lo, values, iters, trav, front)
+
+
 def exchange_buffers(algo: str, nparts: int, stride: int, device):
     """(exchange, owned-slice) tensors for run_partition."""
     import torch
@@ -268,12 +336,32 @@ def exchange_buffers(algo: str, nparts: int, stride: int, device):
             torch.empty(stride, dtype=dt, device=device))
 
 
-def run_partitions_local(engines: Sequence[Engine], algo: str, source: int, strategy
-                         ) -> tuple[np.ndarray, int, list]:
+def run_partitions_local(engines: Sequence[Engine], algo: str, source: int, strategy,
+                         fused: bool = False) -> tuple[np.ndarray, int, list]:
     """All partitions in one process (one device): the reduce-scatter becomes a
-    host-driven reduction over the stacked exchange buffers.  Used to validate
-    the partitioned kernels on a single GPU."""
+    host-driven reduction over the stacked exchange buffers (or, fused, the
+    expand kernels write into each other's buffers by device pointer).  Used to
+    validate the partitioned kernels on a single GPU."""
     import torch
+
+    if fused:
+        locals_ = [e.fused_init(algo)[1] for e in engines]
+        for e in engines:
+            e.fused_connect(ptrs=locals_)
+        nt = [e.begin(algo, source, strategy) for e in engines]
+        n, t = sum(x[0] for x in nt), sum(x[1] for x in nt)
+        iters, trav = 0, []
+        while n > 0:
+            iters += 1
+            trav.append(t)
+            for e in engines:
+                e.fused_reset()
+            for e in engines:
+                e.fused_expand()
+            nt = [e.apply_ptr(p) for e, p in zip(engines, locals_)]
+            n, t = sum(x[0] for x in nt), sum(x[1] for x in nt)
+        values = np.concatenate([e.result() for e in engines])
+        return values, iters, trav
 
     p = len(engines)
     stride = engines[0].stride

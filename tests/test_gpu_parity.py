@@ -214,6 +214,25 @@ def test_cuda_partitions_match_reference(nparts):
     assert not bad, bad[:8]
 
 
+@pytest.mark.parametrize("nparts", [2, 3])
+def test_cuda_partitions_fused_exchange(nparts):
+    """Fused exchange (expand writes into the owners' buffers by pointer) on
+    one GPU: identical values / iterations / traversed edges."""
+    bad = []
+    for c in [c for c in CASES if c.tag.startswith(("c8_", "pl_")) or c.index < 11]:
+        b = edge_balanced_bounds(c.graph.offsets, nparts)
+        engines = [CudaPartition(local_part(c.graph, b, k), b, k) for k in range(nparts)]
+        for s in ("merged-aligned", "packed"):
+            vals, iters, trav = run_partitions_local(engines, c.algo, max(c.source, 0), s,
+                                                     fused=True)
+            if not (np.array_equal(vals, c.values) and iters == c.iterations
+                    and trav == c.traversed):
+                bad.append((c.tag, c.index, s))
+        for e in engines:
+            e.close()
+    assert not bad, bad[:8]
+
+
 def test_rmat_partition_generator_matches_whole_graph():
     whole = zc.generate_rmat(16, 16, seed=11, weights=(8, 72)).as_csr()
     parts = [generate_rmat_part(16, 4, k, seed=11, weights=(8, 72)) for k in range(4)]
