@@ -60,6 +60,8 @@ def parse():
     p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     p.add_argument("--device-override", type=int, default=-1)
     p.add_argument("--force-partitioned", action="store_true")
+    p.add_argument("--no-fused", action="store_true",
+                   help="N>1: skip the fused (NVLink peer-store) exchange variant")
     return p.parse_args()
 
 
@@ -383,6 +385,7 @@ def main_partitioned(args, rank, world, device, config):
         one(i, False)
     barrier(world, device)
     trav = 0
+    launches = 0
     expand_ms = 0.0
     with ClockSampler(device) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -391,6 +394,7 @@ def main_partitioned(args, rank, world, device, config):
         for i in range(args.steps):
             r = one(args.warmup + i, False)
             trav += r.total_traversed_edges
+            launches += part.launches()
         ev1.record()
         torch.cuda.synchronize(device)
     barrier(world, device)
@@ -407,6 +411,30 @@ def main_partitioned(args, rank, world, device, config):
     barrier(world, device)
     wall = max_over_ranks(time.perf_counter() - t1, world, device)
     e2e_value = trav / wall / 1e9
+    fused = None
+    if not args.no_fused:
+        # variant: fused exchange -- the expand kernel writes candidates straight
+        # into the owners' buffers (CUDA IPC peer pointers over NVLink)
+        try:
+            for i in range(args.warmup):
+                run_partition(part, "bfs", int(sources[i % 64]), strat, fetch=False, fused=True)
+            barrier(world, device)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ftrav = 0
+            for i in range(args.steps):
+                r = run_partition(part, "bfs", int(sources[(args.warmup + i) % 64]), strat,
+                                  fetch=False, fused=True)
+                ftrav += r.total_traversed_edges
+            e1.record()
+            torch.cuda.synchronize(device)
+            barrier(world, device)
+            fms = max_over_ranks(e0.elapsed_time(e1), world, device)
+            fused = {"gteps": ftrav / (fms * 1e-3) / 1e9, "ms_per_step": fms / args.steps,
+                     "same_traversed": ftrav == trav}
+        except Exception as exc:  # report, keep the headline
+            fused = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     cfg = dict(config)
     cfg.update({"workload": f"BFS, Kronecker (R-MAT a=.57 b=.19 c=.19) scale {scale}, edge factor "
                             f"{args.edge_factor}, {args.edge_factor << scale} directed arcs, "
@@ -423,7 +451,8 @@ def main_partitioned(args, rank, world, device, config):
             "e2e": {"value": e2e_value, "unit": "GTEPS", "h2d_bytes_per_step": 8,
                     "d2h_bytes_per_step": int(sum_over_ranks(d2h, world, device)) // args.steps,
                     "ms_per_step": wall / args.steps * 1e3},
-            "gpu_launches": None,
+            "gpu_launches": int(sum_over_ranks(launches, world, device)),
+            "variants": {"fused_exchange": fused},
             "clocks": clk.summary(),
             "graph": {"vertices": 1 << scale, "arcs": args.edge_factor << scale,
                       "local_arcs_rank0": part.graph_view().num_edges, "gen_s": gen_s,

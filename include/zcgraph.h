@@ -228,7 +228,8 @@ int zc_part_begin(zc_graph *g, int algo, uint64_t source, int strategy, uint64_t
 int zc_part_expand(zc_graph *g, void *exchange /* device pointer */);
 int zc_part_apply(zc_graph *g, const void *mine /* device pointer, stride slots */,
                   uint64_t *n_next, uint64_t *traversed_next);
-int zc_part_result(zc_graph *g, int64_t *out_local /* range size */, zc_stats *stats);
+int zc_part_result(zc_graph *g, int64_t *out_local /* range size, or NULL: stats only */,
+                   zc_stats *stats);
 /* Fused exchange (no reduce-scatter): the expand kernel writes each candidate
  * straight into its owner's buffer -- peer memory over NVLink (CUDA IPC) --
  * BFS: byte stores, deduplicated per iteration; SSSP / CC: atomicMin

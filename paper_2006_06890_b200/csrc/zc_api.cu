@@ -908,11 +908,14 @@ int zc_part_result(zc_graph* g, int64_t* out, zc_stats* stats) {
   }
   DeviceGuard dg(g->device);
   cudaStream_t st = g->stream;
-  int64_t* d_out = reinterpret_cast<int64_t*>(g->d_fval[g->p_cur ^ 1]);
-  ZC_CUDA_TRY(launch_widen(g->p_algo, g->d_state, g->nv, d_out, st, &g->p_launches));
-  if (g->nv)
-    ZC_CUDA_TRY(cudaMemcpyAsync(out, d_out, g->nv * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  if (out) {  // NULL: statistics only
+    int64_t* d_out = reinterpret_cast<int64_t*>(g->d_fval[g->p_cur ^ 1]);
+    ZC_CUDA_TRY(launch_widen(g->p_algo, g->d_state, g->nv, d_out, st, &g->p_launches));
+    if (g->nv)
+      ZC_CUDA_TRY(cudaMemcpyAsync(out, d_out, g->nv * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                  st));
+    ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  }
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     stats->iterations = g->p_iter;
@@ -920,7 +923,7 @@ int zc_part_result(zc_graph* g, int64_t* out, zc_stats* stats) {
     double ex = 0;
     for (double x : g->log_expand_ms) ex += x;
     stats->expand_ms = ex;
-    stats->d2h_bytes = g->nv * sizeof(int64_t);
+    stats->d2h_bytes = out ? g->nv * sizeof(int64_t) : 0;
   }
   return ZC_OK;
 }

@@ -192,6 +192,11 @@ class CudaPartition:
         N.check(N.lib().zc_part_apply(self._h, ptr, C.byref(n), C.byref(t)))
         return n.value, t.value
 
+    def launches(self) -> int:
+        """Kernels launched since the last begin (this rank)."""
+        N.check(N.lib().zc_part_result(self._h, None, C.byref(self.stats)))
+        return int(self.stats.launches)
+
     def result(self) -> np.ndarray:
         from .device import pinned_empty
         out = pinned_empty(self.num_local, np.int64)
@@ -301,12 +306,14 @@ def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartRe
     handles = [None] * dist.get_world_size(group)
     dist.all_gather_object(handles, handle, group=group)
     engine.fused_connect(handles=handles)
-    counts = torch.zeros(2, dtype=torch.int64, device=dev)
+    cdev = torch.device("cpu") if dist.get_backend(group) == "gloo" else dev
+    counts = torch.zeros(2, dtype=torch.int64, device=cdev)
 
     def sync_all():
         counts.zero_()
-        dist.all_reduce(counts, group=group)  # doubles as a device-ordered barrier
-        torch.cuda.current_stream(dev).synchronize()
+        dist.all_reduce(counts, group=group)  # doubles as a barrier
+        if cdev.type == "cuda":
+            torch.cuda.current_stream(dev).synchronize()
 
     def global_counts(n: int, t: int) -> tuple[int, int]:
         counts[0], counts[1] = n, t

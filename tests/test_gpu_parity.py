@@ -284,3 +284,18 @@ def test_pagerank_traffic_and_validation():
         zc.pagerank(g, max_iters=0)
     with pytest.raises(ValueError):
         zc.pagerank(g, tol=-1.0)
+
+
+def test_report_rows_join_reference_checksums(tmp_path):
+    """Rows carry the reference's columns; levels_checksum and the modelled
+    histogram equal the reference's for the same run (config-1 style graph)."""
+    from paper_2006_06890_b200.report import COLUMNS, measure, write_rows_csv
+    g = zc.generate_uniform(2 ** 16, 16, 16, seed=3)
+    gold = goldens()["uniform_2p16_d16"]
+    rows = measure(g, "bfs", ("merged-aligned", "packed"), sources=[gold["src"]], label="u16")
+    assert {r["levels_checksum"] for r in rows} == {gold["bfs"]["crc"]}
+    assert rows[0]["requests_total"] > 0 and rows[1]["requests_total"] == ""
+    p = tmp_path / "results.csv"
+    write_rows_csv(rows, str(p))
+    lines = p.read_text().splitlines()
+    assert lines[0].startswith("# emogi-b200") and lines[1].split(",") == COLUMNS
