@@ -124,6 +124,15 @@ int zc_device_count(int *count);
 /* Graph handle lifecycle. */
 int zc_graph_create(const zc_graph_desc *desc, zc_graph **out);
 void zc_graph_destroy(zc_graph *g);
+/* Open an EMGI v1 file (csr.py:17-23, 180-245: 28-byte header, u64 offsets,
+ * 128-byte aligned edge / weight payloads) straight into a handle: the
+ * payloads are read in parallel directly into their pinned (zero-copy),
+ * managed (UVM) or staging (HBM) buffers.  Same errors as load_csr_binary
+ * (ZC_EINVAL: truncated / bad magic / version).  flags: ZC_F_DIRECTED (the
+ * reference's directed argument), ZC_F_UVM_PREFETCH, ZC_F_NO_VALIDATE. */
+int zc_graph_open_emgi(const char *path, int32_t placement, int32_t device, uint32_t flags,
+                       zc_graph **out);
+
 /* Host pointers of the handle's edge / weight lists (pinned, managed or a
  * host shadow for HBM placement) -- used by checkers and generators. */
 int zc_graph_host_lists(zc_graph *g, void **edges, void **weights, const int64_t **offsets);

@@ -13,7 +13,7 @@ from .csr import (CsrGraph, DegreeCdf, degree_cdf, generate_powerlaw, generate_u
                   load_csr_binary, pick_sources, store_csr_binary, symmetrized, validate,
                   with_uniform_weights)
 from .device import (DeviceGraph, device_graph, evict, generate_rmat, generate_uniform_device,
-                     link_probe, pinned_empty, release)
+                     link_probe, open_emgi, pinned_empty, release)
 from .traffic import TrafficStats
 from .traversal import (UNREACHED_DIST, UNREACHED_LEVEL, TraversalResult, bfs, cc, pagerank,
                         sssp)
@@ -24,7 +24,7 @@ __all__ = [
     "AccessStrategy", "CsrGraph", "DegreeCdf", "DeviceGraph", "LINE_BYTES", "SECTOR_BYTES",
     "TrafficStats", "TraversalResult", "UNREACHED_DIST", "UNREACHED_LEVEL", "WARP_LANES",
     "bfs", "cc", "degree_cdf", "device_graph", "evict", "generate_powerlaw", "generate_rmat",
-    "generate_uniform", "generate_uniform_device", "link_probe", "load_csr_binary",
+    "generate_uniform", "generate_uniform_device", "link_probe", "load_csr_binary", "open_emgi",
     "pagerank", "pick_sources", "pinned_empty", "release", "sssp", "store_csr_binary", "symmetrized",
     "validate", "with_uniform_weights",
 ]

@@ -30,6 +30,7 @@ EXPORTED = (
     "zc_part_exchange_elem_bytes", "zc_part_begin", "zc_part_expand", "zc_part_apply",
     "zc_part_result", "zc_generate_rmat_part", "zc_pagerank", "zc_graph_multigraph",
     "zc_part_fused_init", "zc_part_fused_connect", "zc_part_fused_reset", "zc_part_fused_expand",
+    "zc_graph_open_emgi",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -75,6 +76,7 @@ def _declare(lib: C.CDLL) -> None:
         "zc_device_count": (C.c_int, [C.POINTER(C.c_int)]),
         "zc_graph_create": (C.c_int, [C.POINTER(GraphDesc), C.POINTER(P)]),
         "zc_graph_destroy": (None, [P]),
+        "zc_graph_open_emgi": (C.c_int, [C.c_char_p, i32, i32, u32, C.POINTER(P)]),
         "zc_graph_host_lists": (C.c_int, [P, C.POINTER(P), C.POINTER(P), C.POINTER(P)]),
         "zc_graph_info": (C.c_int, [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(u32),
                                     C.POINTER(u32), C.POINTER(i32), C.POINTER(u32)]),

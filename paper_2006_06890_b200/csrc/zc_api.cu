@@ -14,6 +14,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -633,6 +637,179 @@ static int create_impl(const zc_graph_desc* d, zc_graph** out, uint64_t dest_lim
 }
 
 int zc_graph_create(const zc_graph_desc* d, zc_graph** out) { return create_impl(d, out, 0); }
+
+// ------------------------------------------------------------ EMGI loader
+// Reads an EMGI v1 file (csr.py:17-23, 180-245) straight into the handle's
+// list buffers (pinned / managed / pinned staging for HBM) with parallel
+// preads: no intermediate copy of the payload.
+namespace {
+int pread_all(int fd, void* dst, uint64_t bytes, uint64_t off) {
+  std::atomic<int> bad{0};
+  const uint64_t chunk = 64ull << 20;
+  const uint64_t nchunks = (bytes + chunk - 1) / chunk;
+  parallel_for(nchunks, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t c = lo; c < hi && !bad; ++c) {
+      uint64_t done = c * chunk;
+      const uint64_t end = std::min(bytes, done + chunk);
+      while (done < end) {
+        const ssize_t r = pread(fd, static_cast<char*>(dst) + done, end - done, off + done);
+        if (r <= 0) {
+          bad = 1;
+          break;
+        }
+        done += static_cast<uint64_t>(r);
+      }
+    }
+  });
+  return bad ? ZC_EINVAL : ZC_OK;
+}
+
+uint64_t round_up(uint64_t n, uint64_t a) { return (n + a - 1) / a * a; }
+}  // namespace
+
+int zc_graph_open_emgi(const char* path, int32_t placement, int32_t device, uint32_t flags,
+                       zc_graph** out) {
+  if (!path || !out) {
+    set_error("null argument");
+    return ZC_ESTATE;
+  }
+  *out = nullptr;
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) {
+    set_error(std::string("cannot open ") + path);
+    return ZC_EINVAL;
+  }
+  struct FdGuard {
+    int fd;
+    ~FdGuard() { close(fd); }
+  } guard{fd};
+  struct stat stt;
+  fstat(fd, &stt);
+  const uint64_t size = static_cast<uint64_t>(stt.st_size);
+  unsigned char hdr[28];
+  if (size < sizeof(hdr) || pread(fd, hdr, sizeof(hdr), 0) != (ssize_t)sizeof(hdr)) {
+    set_error("truncated file: " + std::to_string(size) + " bytes, header needs 28");
+    return ZC_EINVAL;
+  }
+  if (memcmp(hdr, "EMGI", 4) != 0) {
+    set_error("bad magic");
+    return ZC_EINVAL;
+  }
+  uint32_t version, fl;
+  uint64_t nv, ne;
+  memcpy(&version, hdr + 4, 4);
+  memcpy(&fl, hdr + 8, 4);
+  memcpy(&nv, hdr + 12, 8);
+  memcpy(&ne, hdr + 20, 8);
+  if (version != 1) {
+    set_error("unsupported format version " + std::to_string(version));
+    return ZC_EINVAL;
+  }
+  const uint32_t eb = (fl & 2) ? 8 : 4, wb = (fl & 4) ? 8 : 4;
+  const bool has_w = fl & 1;
+  const uint64_t off_pos = 28, off_end = off_pos + (nv + 1) * 8;
+  if (size < off_end) {
+    set_error("truncated file: offsets array incomplete");
+    return ZC_EINVAL;
+  }
+  const uint64_t e_pos = round_up(off_end, 128), e_end = e_pos + ne * eb;
+  if (size < e_end) {
+    set_error("truncated file: edge array incomplete");
+    return ZC_EINVAL;
+  }
+  const uint64_t w_pos = round_up(e_end, 128), w_end = w_pos + ne * wb;
+  if (has_w && size < w_end) {
+    set_error("truncated file: weight array incomplete");
+    return ZC_EINVAL;
+  }
+  if (placement < ZC_PLACE_ZEROCOPY || placement > ZC_PLACE_HBM) {
+    set_error("unknown placement");
+    return ZC_EINVAL;
+  }
+  if (nv >= 0xffffffffull) {
+    set_error("device path supports fewer than 2^32-1 vertices");
+    return ZC_EINVAL;
+  }
+  int ndev = 0;
+  ZC_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) {
+    set_error("device not present");
+    return ZC_EINVAL;
+  }
+  DeviceGuard dg(device);
+  zc_graph* g = new zc_graph();
+  g->nv = nv;
+  g->ne = ne;
+  g->eb = eb;
+  g->wb = wb;
+  g->placement = placement;
+  g->device = device;
+  g->flags = flags & (ZC_F_DIRECTED | ZC_F_UVM_PREFETCH | ZC_F_NO_VALIDATE);
+  g->has_weights = has_w;
+  auto fail = [&](int code) {
+    free_graph(g);
+    return code;
+  };
+  if (cudaHostAlloc(&g->h_off, (nv + 1) * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess) {
+    set_error("cannot allocate pinned offsets");
+    return fail(ZC_ENOMEM);
+  }
+  if (pread_all(fd, g->h_off, (nv + 1) * 8, off_pos)) {
+    set_error("read error (offsets)");
+    return fail(ZC_EINVAL);
+  }
+  // lists: read straight into their final host-side buffer
+  auto load = [&](uint64_t pos, uint32_t w, void** h, const void** dptr, void** hbm) -> int {
+    const size_t bytes = std::max<size_t>(ne * w, kLineBytes);
+    void* p = nullptr;
+    if (placement == ZC_PLACE_UVM) {
+      ZC_CUDA_TRY(cudaMallocManaged(&p, bytes, cudaMemAttachGlobal));
+    } else {
+      ZC_CUDA_TRY(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    }
+    *h = p;
+    if (ne && pread_all(fd, p, ne * w, pos)) {
+      set_error("read error (lists)");
+      return ZC_EINVAL;
+    }
+    if (placement == ZC_PLACE_UVM) {
+      ZC_CUDA_TRY(cudaMemAdvise(p, bytes, cudaMemAdviseSetReadMostly, device));
+      *dptr = p;
+    } else if (placement == ZC_PLACE_HBM) {
+      ZC_CUDA_TRY(cudaMalloc(hbm, bytes));
+      ZC_CUDA_TRY(cudaMemcpy(*hbm, p, ne * w, cudaMemcpyHostToDevice));
+      *dptr = *hbm;
+    } else {
+      void* d = nullptr;
+      ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, p, 0));
+      *dptr = d;
+    }
+    return ZC_OK;
+  };
+  int rc = load(e_pos, eb, &g->h_edges, &g->d_edges, &g->hbm_edges);
+  if (rc) return fail(rc);
+  if (has_w && (rc = load(w_pos, wb, &g->h_weights, &g->d_weights, &g->hbm_weights)))
+    return fail(rc);
+  // invariants (csr.py:80-105) on the loaded buffers
+  zc_graph_desc d{};
+  d.num_vertices = nv;
+  d.num_edges = ne;
+  d.offsets = g->h_off;
+  d.edges = g->h_edges;
+  d.weights = has_w ? g->h_weights : nullptr;
+  d.src_edge_bytes = d.edge_elem_bytes = eb;
+  d.src_weight_bytes = d.weight_elem_bytes = wb;
+  d.placement = placement;
+  d.device = device;
+  d.flags = g->flags;
+  bool neg = false;
+  if ((rc = validate_desc(&d, &neg))) return fail(rc);
+  g->negative_weight = neg;
+  if ((rc = alloc_state(g))) return fail(rc);
+  if ((rc = finish_create(g))) return fail(rc);
+  *out = g;
+  return ZC_OK;
+}
 
 void zc_graph_destroy(zc_graph* g) { free_graph(g); }
 

@@ -323,6 +323,20 @@ def generate_uniform_device(num_vertices: int, min_degree: int, max_degree: int,
     return DeviceGraph(placement=placement, device=device, _handle=h.value)
 
 
+def open_emgi(path: str, directed: bool = True, placement: str = "zerocopy",
+              device: int = 0, validate: bool = True) -> DeviceGraph:
+    """EMGI file -> DeviceGraph, the payloads read straight into the handle's
+    pinned / managed / staging buffers (reference load_csr_binary semantics,
+    csr.py:204-245, without the int64 widening or a second copy)."""
+    if placement not in N.PLACEMENTS:
+        raise ValueError(f"placement must be one of {sorted(N.PLACEMENTS)}")
+    flags = (N.ZC_F_DIRECTED if directed else 0) | (0 if validate else N.ZC_F_NO_VALIDATE)
+    h = C.c_void_p()
+    N.check(N.lib().zc_graph_open_emgi(str(path).encode(), N.PLACEMENTS[placement], device,
+                                       flags, C.byref(h)))
+    return DeviceGraph(placement=placement, device=device, _handle=h.value)
+
+
 def evict(dg: DeviceGraph) -> None:
     dg.evict()
 

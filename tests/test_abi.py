@@ -87,3 +87,25 @@ def test_no_cpu_fallback_without_device():
     g = zc.generate_uniform(64, 1, 3, seed=1)
     with pytest.raises(RuntimeError):
         zc.bfs(g, 0)
+
+
+def test_open_emgi_header_errors_match_reference(tmp_path):
+    """zc_graph_open_emgi rejects bad files before touching a device, with the
+    reference load_csr_binary's ValueErrors (csr.py:204-245)."""
+    bad = tmp_path / "bad.emgi"
+    bad.write_bytes(b"XXXX" + bytes(40))
+    with pytest.raises(ValueError, match="magic"):
+        zc.open_emgi(str(bad))
+    bad.write_bytes(b"EMGI")
+    with pytest.raises(ValueError, match="truncated"):
+        zc.open_emgi(str(bad))
+    g = zc.with_uniform_weights(zc.generate_uniform(100, 1, 3, seed=1))
+    p = tmp_path / "g.emgi"
+    zc.store_csr_binary(g, str(p))
+    raw = p.read_bytes()
+    p.write_bytes(raw[:-5])
+    with pytest.raises(ValueError, match="weight array incomplete"):
+        zc.open_emgi(str(p))
+    p.write_bytes(raw[:4] + (2).to_bytes(4, "little") + raw[8:])
+    with pytest.raises(ValueError, match="version"):
+        zc.open_emgi(str(p))

@@ -299,3 +299,17 @@ def test_report_rows_join_reference_checksums(tmp_path):
     write_rows_csv(rows, str(p))
     lines = p.read_text().splitlines()
     assert lines[0].startswith("# emogi-b200") and lines[1].split(",") == COLUMNS
+
+
+@pytest.mark.parametrize("placement", ["zerocopy", "uvm", "hbm"])
+def test_open_emgi_roundtrip(tmp_path, placement):
+    g = zc.with_uniform_weights(zc.generate_uniform(2 ** 16, 16, 16, seed=3))
+    gold = goldens()["uniform_2p16_d16"]
+    p = tmp_path / "u16.emgi"
+    zc.store_csr_binary(g, str(p))
+    dg = zc.open_emgi(str(p), placement=placement)
+    h = dg.as_csr()
+    assert crc(h.edges, "<u4") == gold["graph"]["edges_crc_u4"]
+    assert crc(zc.bfs(dg, gold["src"], collect_traffic=False).values) == gold["bfs"]["crc"]
+    assert crc(zc.sssp(dg, gold["src"], collect_traffic=False).values) == gold["sssp"]["crc"]
+    dg.close()
