@@ -493,6 +493,15 @@ def other_configs(zc, args, device) -> dict:
             "kernel_ms": r.kernel_ms, "iterations": r.iterations,
             "link_gbs": r.total_traversed_edges * 8 / (r.expand_ms * 1e-3) / 1e9,
             "work_edges": r.total_traversed_edges}
+    u.build_sssp_pairs()  # B200 layout option: one interleaved (dst, weight) stream
+    for s in ("merged-aligned", "packed"):
+        zc.sssp(u, src, s, collect_traffic=False)
+        r = zc.sssp(u, src, s, collect_traffic=False)
+        out[f"sssp_uniform{args.scale}/{s}+pairs"] = {
+            "work_gteps": r.total_traversed_edges / (r.kernel_ms * 1e-3) / 1e9,
+            "kernel_ms": r.kernel_ms, "iterations": r.iterations,
+            "link_gbs": r.total_traversed_edges * 8 / (r.expand_ms * 1e-3) / 1e9,
+            "work_edges": r.total_traversed_edges}
     t0 = time.perf_counter()
     ref = oracle.sssp(u.as_csr(), src, threads=os.cpu_count())
     out[f"sssp_uniform{args.scale}/cpu_port_work_gteps"] = (

@@ -151,6 +151,13 @@ int zc_cc(zc_graph *g, int strategy, int64_t *out, zc_stats *stats);
  * caller buffer of V doubles.  Same ValueError conditions (ZC_EINVAL). */
 int zc_pagerank(zc_graph *g, int strategy, double damping, uint64_t max_iters, double tol,
                 double *out, zc_stats *stats);
+/* Build (once) an interleaved copy of the lists as 8-byte (dst, weight) u32
+ * pairs in the handle's placement; SSSP then reads one stream instead of two,
+ * so a list of n edges costs ceil(8n/128) line requests instead of two
+ * half-used ones.  A B200 layout option; results are identical.  The request
+ * model (ZC_OPT_TRAFFIC_MODEL) keeps describing the reference's separate
+ * arrays, so modelled runs read those. */
+int zc_graph_build_pairs(zc_graph *g);
 /* 1 if some list repeats a destination (traversal.py:182-188), cached. */
 int zc_graph_multigraph(zc_graph *g, int *out);
 

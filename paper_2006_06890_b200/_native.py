@@ -30,7 +30,7 @@ EXPORTED = (
     "zc_part_exchange_elem_bytes", "zc_part_begin", "zc_part_expand", "zc_part_apply",
     "zc_part_result", "zc_generate_rmat_part", "zc_pagerank", "zc_graph_multigraph",
     "zc_part_fused_init", "zc_part_fused_connect", "zc_part_fused_reset", "zc_part_fused_expand",
-    "zc_graph_open_emgi",
+    "zc_graph_open_emgi", "zc_graph_build_pairs",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -85,6 +85,7 @@ def _declare(lib: C.CDLL) -> None:
         "zc_cc": (C.c_int, [P, C.c_int, P, C.POINTER(Stats)]),
         "zc_pagerank": (C.c_int, [P, C.c_int, dbl, u64, dbl, P, C.POINTER(Stats)]),
         "zc_graph_multigraph": (C.c_int, [P, C.POINTER(C.c_int)]),
+        "zc_graph_build_pairs": (C.c_int, [P]),
         "zc_run_log": (C.c_int, [P, P, P, u64]),
         "zc_set_options": (C.c_int, [P, u32]),
         "zc_run_profile": (C.c_int, [P, P, u64]),

@@ -122,6 +122,7 @@ void zc::free_graph(zc_graph* g) {
   };
   free_list(g->h_edges, g->edges_registered, g->hbm_edges);
   free_list(g->h_weights, g->weights_registered, g->hbm_weights);
+  free_list(g->h_pairs, false, g->hbm_pairs);
   if (g->h_off) cudaFreeHost(g->h_off);
   cudaFree(g->d_off);
   cudaFree(g->d_state);
@@ -493,6 +494,11 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     a.state = g->d_state;
     a.flags = g->d_flags;
     a.visited = g->d_visited;
+    if (algo == kSssp && g->d_pairs && !model) {  // interleaved (dst, weight) stream
+      a.edges = g->d_pairs;
+      a.weights = nullptr;
+      a.pairs = 1;
+    }
     a.iter = static_cast<uint32_t>(iters);
     a.big_s = g->d_big_s;
     a.big_e = g->d_big_e;
@@ -510,7 +516,8 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
       g->iter_ev.push_back(e);
     }
     ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (iters - 1)], st));
-    ZC_CUDA_TRY(launch_expand(strategy, algo, g->eb, g->wb, a, g->num_sms, st, &launches));
+    ZC_CUDA_TRY(launch_expand(strategy, algo, a.pairs ? 8 : g->eb, g->wb, a, g->num_sms, st,
+                              &launches));
     ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (iters - 1) + 1], st));
     CompactArgs c;
     c.flags = g->d_flags;
@@ -1283,6 +1290,45 @@ int zc_pagerank(zc_graph* g, int strategy, double damping, uint64_t max_iters, d
     stats->launches = launches;
     stats->expand_ms = expand_ms;
     stats->total_ms = now_ms() - t0;
+  }
+  return ZC_OK;
+}
+
+int zc_graph_build_pairs(zc_graph* g) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (!g->has_weights || g->eb != 4 || g->wb != 4) {
+    set_error("pairs need 4-byte edges and 4-byte weights");
+    return ZC_EINVAL;
+  }
+  if (g->h_pairs) return ZC_OK;
+  DeviceGuard dg(g->device);
+  ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  const uint64_t ne = g->ne;
+  const size_t bytes = std::max<size_t>(ne * 8, kLineBytes);
+  void* p = nullptr;
+  if (g->placement == ZC_PLACE_UVM) ZC_CUDA_TRY(cudaMallocManaged(&p, bytes, cudaMemAttachGlobal));
+  else ZC_CUDA_TRY(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  g->h_pairs = p;
+  const uint32_t* e = static_cast<const uint32_t*>(g->h_edges);
+  const uint32_t* w = static_cast<const uint32_t*>(g->h_weights);
+  uint64_t* out = static_cast<uint64_t*>(p);
+  parallel_for(ne, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo; i < hi; ++i) out[i] = uint64_t(e[i]) | (uint64_t(w[i]) << 32);
+  });
+  if (g->placement == ZC_PLACE_UVM) {
+    ZC_CUDA_TRY(cudaMemAdvise(p, bytes, cudaMemAdviseSetReadMostly, g->device));
+    g->d_pairs = p;
+  } else if (g->placement == ZC_PLACE_HBM) {
+    ZC_CUDA_TRY(cudaMalloc(&g->hbm_pairs, bytes));
+    ZC_CUDA_TRY(cudaMemcpy(g->hbm_pairs, p, ne * 8, cudaMemcpyHostToDevice));
+    g->d_pairs = g->hbm_pairs;
+  } else {
+    void* d = nullptr;
+    ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, p, 0));
+    g->d_pairs = d;
   }
   return ZC_OK;
 }

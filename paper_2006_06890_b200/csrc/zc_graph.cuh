@@ -29,6 +29,10 @@ struct zc_graph {
   const void* d_weights = nullptr;
   void* hbm_edges = nullptr;
   void* hbm_weights = nullptr;
+  // optional interleaved (dst, weight) u32 pairs for SSSP (zc_graph_build_pairs)
+  void* h_pairs = nullptr;
+  const void* d_pairs = nullptr;
+  void* hbm_pairs = nullptr;
   // HBM state
   uint64_t* d_off = nullptr;
   void* d_state = nullptr;

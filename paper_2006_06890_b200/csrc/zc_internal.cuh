@@ -111,6 +111,7 @@ struct ExpandArgs {
   int unroll;
   int ctas_per_sm;
   int chunk_sched;  // 1: the per-warp chunk + big-list scheduler instead of the sweep
+  int pairs;        // SSSP: `edges` is the interleaved (dst, weight) u32-pair list
 };
 
 // ZC_TUNE="unroll=8,ctas=6,sched=chunk": expansion tuning knobs for experiments.

@@ -53,6 +53,18 @@ __device__ __forceinline__ uint64_t ld_list(const uint64_t* p) {
   return v;
 }
 
+// Interleaved (destination, weight) u32 pairs in one 8-byte element stream
+// (zc_graph_build_pairs): the weight rides in the high half, no second load.
+struct PairW {};
+template <typename WT>
+struct IsPair {
+  static constexpr bool value = false;
+};
+template <>
+struct IsPair<PairW> {
+  static constexpr bool value = true;
+};
+
 // ---------------------------------------------------------------- visitors
 // Apply one traversed edge (v -> w, weight wt) whose source carries the
 // start-of-iteration value `val`.
@@ -195,10 +207,15 @@ template <int ALGO, typename ET, typename WT, int U>
 __device__ __forceinline__ void visit_batch(const ExpandArgs& a,
                                             const Batch<ALGO, ET, WT, U>& b) {
 #pragma unroll
-  for (int u = 0; u < U; ++u)
-    if (b.ok[u])
+  for (int u = 0; u < U; ++u) {
+    if (!b.ok[u]) continue;
+    if constexpr (IsPair<WT>::value)
+      Visit<ALGO>::apply(a, uint64_t(b.dst[u]) & 0xffffffffull, uint64_t(b.dst[u]) >> 32,
+                         b.sval[u]);
+    else
       Visit<ALGO>::apply(a, b.dst[u], AlgoTraits<ALGO>::weighted ? uint64_t(b.wt[u]) : 0,
                          b.sval[u]);
+  }
 }
 
 // Per-lane metadata of one 32-slot chunk of the frontier.
@@ -283,7 +300,8 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_warp(ExpandArgs a) {
           b.ok[u] = idx >= sk && idx < ek;
           if (b.ok[u]) {
             b.dst[u] = ld_list(E + idx);
-            if (AlgoTraits<ALGO>::weighted) b.wt[u] = ld_list(W + idx);
+            if constexpr (AlgoTraits<ALGO>::weighted && !IsPair<WT>::value)
+              b.wt[u] = ld_list(W + idx);
           }
         }
       }
@@ -351,7 +369,8 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_big(ExpandArgs a) {
         bt.ok[u] = idx >= s && idx < e;
         if (bt.ok[u]) {
           bt.dst[u] = ld_list(E + idx);
-          if (AlgoTraits<ALGO>::weighted) bt.wt[u] = ld_list(W + idx);
+          if constexpr (AlgoTraits<ALGO>::weighted && !IsPair<WT>::value)
+            bt.wt[u] = ld_list(W + idx);
         }
       }
     }
@@ -498,7 +517,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
           }
           if (bt.ok[u]) {
             bt.dst[u] = ld_list(E + idx);
-            if (AlgoTraits<ALGO>::weighted) bt.wt[u] = ld_list(Wt + idx);
+            if constexpr (AlgoTraits<ALGO>::weighted && !IsPair<WT>::value)
+              bt.wt[u] = ld_list(Wt + idx);
           }
         }
       }
@@ -576,8 +596,12 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_naive(ExpandArgs a) {
     const uint64_t val = AlgoTraits<ALGO>::has_val ? a.fval[j] : 0;
     for (uint64_t k = s; k < e; ++k) {
       const ET w = ld_list(E + k);
-      const uint64_t wt = AlgoTraits<ALGO>::weighted ? uint64_t(ld_list(W + k)) : 0;
-      Visit<ALGO>::apply(a, w, wt, val);
+      if constexpr (IsPair<WT>::value) {
+        Visit<ALGO>::apply(a, uint64_t(w) & 0xffffffffull, uint64_t(w) >> 32, val);
+      } else {
+        const uint64_t wt = AlgoTraits<ALGO>::weighted ? uint64_t(ld_list(W + k)) : 0;
+        Visit<ALGO>::apply(a, w, wt, val);
+      }
     }
   }
 }
@@ -1182,6 +1206,9 @@ template <int STRAT, int ALGO>
 cudaError_t expand_w(int eb, int wb, const ExpandArgs& a, int num_sms, cudaStream_t st,
                      uint64_t* l) {
   constexpr bool W = AlgoTraits<ALGO>::weighted;
+  if constexpr (W) {
+    if (a.pairs) return expand_t<STRAT, ALGO, uint64_t, PairW>(a, num_sms, st, l);
+  }
   if (eb == 4) {
     if (W && wb == 8) return expand_t<STRAT, ALGO, uint32_t, uint64_t>(a, num_sms, st, l);
     return expand_t<STRAT, ALGO, uint32_t, uint32_t>(a, num_sms, st, l);

@@ -192,6 +192,11 @@ class DeviceGraph:
         """UVM: move the lists back to host memory so the next run is cold."""
         N.check(N.lib().zc_graph_evict(self.handle))
 
+    def build_sssp_pairs(self) -> None:
+        """Interleave (dst, weight) into one 8-byte stream for SSSP (extra
+        8 B/edge of host memory); results are identical."""
+        N.check(N.lib().zc_graph_build_pairs(self.handle))
+
     def expand_profile(self, iterations: int) -> np.ndarray:
         """Per-iteration device time (ms) of the expansion kernels of the last run."""
         out = np.zeros(iterations, np.float64)

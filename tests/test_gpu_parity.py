@@ -313,3 +313,24 @@ def test_open_emgi_roundtrip(tmp_path, placement):
     assert crc(zc.bfs(dg, gold["src"], collect_traffic=False).values) == gold["bfs"]["crc"]
     assert crc(zc.sssp(dg, gold["src"], collect_traffic=False).values) == gold["sssp"]["crc"]
     dg.close()
+
+
+def test_sssp_pairs_layout_identical():
+    """Interleaved (dst, weight) stream: same SSSP results, all strategies."""
+    bad = []
+    for c in [c for c in CASES if c.algo == "sssp" and c.graph.edge_elem_bytes == 4]:
+        dg = zc.DeviceGraph(c.graph)
+        dg.build_sssp_pairs()
+        for s in ALL:
+            r = zc.sssp(dg, c.source, s, collect_traffic=False)
+            if not (np.array_equal(r.values, c.values) and r.iterations == c.iterations
+                    and r.traversed_edges == c.traversed):
+                bad.append((c.tag, c.index, getattr(s, "value", s)))
+        dg.close()
+    assert not bad, bad[:8]
+    u = zc.generate_uniform_device(1 << 16, 16, 16, seed=9, weights=(8, 72))
+    ref = zc.sssp(u, 5, "packed", collect_traffic=False)
+    u.build_sssp_pairs()
+    for s in ALL:
+        r = zc.sssp(u, 5, s, collect_traffic=False)
+        assert np.array_equal(r.values, ref.values) and r.iterations == ref.iterations
