@@ -173,23 +173,29 @@ def load_ncu_summary() -> dict:
     return {}
 
 
-def cpu_baseline(g, sources, threads: int, budget_s: float = 25.0) -> dict:
+def cpu_baseline(g, sources, threads: int, budget_s: float = 25.0, check=None) -> dict:
     """The oracle port (oracle/zc_oracle.c, OpenMP) on the same graph: BFS from
-    the bench sources until ~budget_s of CPU work."""
+    the bench sources until ~budget_s of CPU work.  check(source, oracle
+    result) -> bool compares the GPU's result for the same source (parity at
+    the full bench size)."""
     import oracle
     done, edges, t_total = 0, 0, 0.0
+    parity = []
     for s in sources:
         t0 = time.perf_counter()
         r = oracle.bfs(g, int(s), threads=threads)
         t_total += time.perf_counter() - t0
         edges += sum(r.traversed_edges)
         done += 1
+        if check is not None and len(parity) < 3:
+            parity.append(bool(check(int(s), r)))
         if t_total > budget_s:
             break
     return {"value": edges / t_total / 1e9, "unit": "GTEPS", "cores": threads, "kind": "port",
             "sample": f"{done} full BFS run(s) of the oracle port (OpenMP C restatement of "
                       f"traversal.py:98-120) on the same in-memory graph, {threads} threads",
-            "seconds": t_total}
+            "seconds": t_total,
+            "gpu_bit_exact_vs_oracle": parity}
 
 
 def main():
@@ -292,7 +298,11 @@ def main():
 
     if rank == 0 and not args.no_cpu_baseline:
         threads = args.cpu_threads or os.cpu_count()
-        line["cpu_baseline"] = cpu_baseline(g, sources, threads)
+        def check(src, ref):
+            r = zc.bfs(dg, src, strat, collect_traffic=False)
+            return (np.array_equal(r.values, ref.values) and r.iterations == ref.iterations
+                    and r.traversed_edges == ref.traversed_edges)
+        line["cpu_baseline"] = cpu_baseline(g, sources, threads, check=check)
 
     # configs before the UVM variants: managed-memory runs leave the process
     # slower on later zero-copy work (measured), so UVM goes last

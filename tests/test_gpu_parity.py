@@ -2,6 +2,8 @@
 the CPU oracle.  Bit-exact: values (int64), iteration counts and per-iteration
 traversed-edge counts; modelled traffic histograms too.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -333,4 +335,24 @@ def test_sssp_pairs_layout_identical():
     u.build_sssp_pairs()
     for s in ALL:
         r = zc.sssp(u, 5, s, collect_traffic=False)
+        assert np.array_equal(r.values, ref.values) and r.iterations == ref.iterations
+
+
+def test_scale_parity_k24():
+    """2^28-arc Kronecker graphs (2^29 symmetrized): GPU vs the oracle on the
+    same in-memory graph, every strategy but naive (hubs make it slow)."""
+    dg = zc.generate_rmat(24, 16, seed=31, weights=(8, 72))
+    g = dg.as_csr()
+    src = int(zc.pick_sources(g, 1, seed=7)[0])
+    for algo in ("bfs", "sssp"):
+        ref = oracle.run(algo, g, src, threads=os.cpu_count())
+        for s in ("merged", "merged-aligned", "packed"):
+            r = getattr(zc, algo)(dg, src, s, collect_traffic=False)
+            assert np.array_equal(r.values, ref.values), (algo, s)
+            assert r.iterations == ref.iterations and r.traversed_edges == ref.traversed_edges
+    dg.close()
+    sg = zc.generate_rmat(23, 16, seed=31, symmetrize=True)
+    ref = oracle.cc(sg.as_csr(), threads=os.cpu_count())
+    for s in ("merged-aligned", "packed"):
+        r = zc.cc(sg, s, collect_traffic=False)
         assert np.array_equal(r.values, ref.values) and r.iterations == ref.iterations

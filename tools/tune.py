@@ -9,6 +9,7 @@ ap.add_argument("--algo", default="bfs")
 ap.add_argument("--configs", default="sched=chunk;;unroll=2;unroll=8;ctas=4;ctas=6")
 ap.add_argument("--strategy", default="merged-aligned")
 ap.add_argument("--strategies", default="")
+ap.add_argument("--pairs", action="store_true")
 a = ap.parse_args()
 t = time.time()
 if a.algo == "sssp":
@@ -16,6 +17,8 @@ if a.algo == "sssp":
 else:
     dg = zc.generate_rmat(a.scale, 16, seed=27, symmetrize=a.algo == "cc")
 print(f"gen {time.time()-t:.1f}s V={dg.num_vertices} E={dg.num_edges}", flush=True)
+if a.pairs:
+    dg.build_sssp_pairs()
 src = int(zc.pick_sources(dg.as_csr(), 64, seed=7)[0])
 eb = 8 if a.algo == "sssp" else 4
 ref = None
