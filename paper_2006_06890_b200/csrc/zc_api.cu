@@ -14,9 +14,15 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <dirent.h>
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
+#include <sys/syscall.h>
 #include <unistd.h>
+
+#include <mutex>
+#include <unordered_map>
 
 #include <algorithm>
 #include <atomic>
@@ -83,6 +89,82 @@ void tune_params(ExpandArgs* a) {
   a->chunk_sched = sched;
 }
 
+// ---------------------------------------------------------- pinned lists
+// Zero-copy lists are read by the GPU across PCIe: on a multi-socket host
+// they belong on the GPU's own NUMA node.  Allocate an
+// anonymous mapping bound to that node (mbind), advise transparent huge
+// pages, and cudaHostRegister it; fall back to cudaHostAlloc when the node is
+// unknown (single-node hosts, as the pool's), mbind is refused, or ZC_NUMA=0.
+static std::mutex g_map_mu;
+static std::unordered_map<void*, size_t> g_mapped;  // our mbind'ed registrations
+
+static int gpu_numa_node(int device) {
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) return -1;
+  for (char* c = bus; *c; ++c) *c = static_cast<char>(tolower(*c));
+  std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+  FILE* f = fopen(path.c_str(), "r");
+  if (!f) return -1;
+  int node = -1;
+  if (fscanf(f, "%d", &node) != 1) node = -1;
+  fclose(f);
+  int nodes = 0;
+  if (DIR* d = opendir("/sys/devices/system/node")) {
+    while (dirent* e = readdir(d))
+      if (!strncmp(e->d_name, "node", 4) && isdigit(static_cast<unsigned char>(e->d_name[4])))
+        ++nodes;
+    closedir(d);
+  }
+  return nodes > 1 ? node : -1;
+}
+
+void* pinned_list_alloc(int device, size_t bytes) {
+  const char* env = getenv("ZC_NUMA");
+  const int node = (env && env[0] == '0') ? -1 : gpu_numa_node(device);
+  if (node >= 0 && node < 64) {
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p != MAP_FAILED) {
+      unsigned long mask = 1ul << node;
+      const long rc = syscall(SYS_mbind, p, bytes, 2 /* MPOL_BIND */, &mask, 64, 0);
+      madvise(p, bytes, MADV_HUGEPAGE);
+      if (rc == 0 &&
+          cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) ==
+              cudaSuccess) {
+        std::lock_guard<std::mutex> lk(g_map_mu);
+        g_mapped[p] = bytes;
+        return p;
+      }
+      cudaGetLastError();
+      munmap(p, bytes);
+    }
+  }
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void pinned_list_free(void* p) {
+  if (!p) return;
+  size_t bytes = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_mapped.find(p);
+    if (it != g_mapped.end()) {
+      bytes = it->second;
+      g_mapped.erase(it);
+    }
+  }
+  if (bytes) {
+    cudaHostUnregister(p);
+    munmap(p, bytes);
+  } else {
+    cudaFreeHost(p);
+  }
+}
+
 static double now_ms() {
   using namespace std::chrono;
   return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
@@ -114,7 +196,7 @@ void zc::free_graph(zc_graph* g) {
     if (h) {
       if (registered) cudaHostUnregister(h);
       else if (g->placement == ZC_PLACE_UVM) cudaFree(h);
-      else cudaFreeHost(h);
+      else pinned_list_free(h);
     }
     h = nullptr;
     if (hbm) cudaFree(hbm);
@@ -283,7 +365,11 @@ int place_list(zc_graph* g, const void* src, uint32_t sw, uint32_t dw, uint64_t 
   }
   // pinned mapped host buffer (zero-copy list, or the host shadow of HBM)
   void* p = nullptr;
-  ZC_CUDA_TRY(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  p = pinned_list_alloc(g->device, bytes);
+  if (!p) {
+    set_error("cannot allocate pinned host memory for a list");
+    return ZC_ENOMEM;
+  }
   *h = p;
   if (src && n) convert_copy(p, dw, src, sw, n);
   if (g->placement == ZC_PLACE_HBM) {
@@ -378,7 +464,11 @@ int zc::adopt_device_list(zc_graph* g, void* d_src, uint32_t w, uint64_t n, void
     return ZC_OK;
   }
   void* p = nullptr;
-  ZC_CUDA_TRY(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  p = pinned_list_alloc(g->device, bytes);
+  if (!p) {
+    set_error("cannot allocate pinned host memory for a list");
+    return ZC_ENOMEM;
+  }
   *h = p;
   ZC_CUDA_TRY(cudaMemcpy(p, d_src, n * w, cudaMemcpyDeviceToHost));
   if (g->placement == ZC_PLACE_HBM) {
@@ -772,7 +862,11 @@ int zc_graph_open_emgi(const char* path, int32_t placement, int32_t device, uint
     if (placement == ZC_PLACE_UVM) {
       ZC_CUDA_TRY(cudaMallocManaged(&p, bytes, cudaMemAttachGlobal));
     } else {
-      ZC_CUDA_TRY(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+      p = pinned_list_alloc(g->device, bytes);
+  if (!p) {
+    set_error("cannot allocate pinned host memory for a list");
+    return ZC_ENOMEM;
+  }
     }
     *h = p;
     if (ne && pread_all(fd, p, ne * w, pos)) {
@@ -1310,7 +1404,10 @@ int zc_graph_build_pairs(zc_graph* g) {
   const size_t bytes = std::max<size_t>(ne * 8, kLineBytes);
   void* p = nullptr;
   if (g->placement == ZC_PLACE_UVM) ZC_CUDA_TRY(cudaMallocManaged(&p, bytes, cudaMemAttachGlobal));
-  else ZC_CUDA_TRY(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  else if (!(p = pinned_list_alloc(g->device, bytes))) {
+    set_error("cannot allocate pinned host memory for a list");
+    return ZC_ENOMEM;
+  }
   g->h_pairs = p;
   const uint32_t* e = static_cast<const uint32_t*>(g->h_edges);
   const uint32_t* w = static_cast<const uint32_t*>(g->h_weights);

@@ -87,6 +87,9 @@ void free_graph(zc_graph* g);
 int alloc_state(zc_graph* g);
 int finish_create(zc_graph* g);  // prefetch (UVM) + sync
 int init_partition(zc_graph* g, const zc_part_info* info);
+// pinned mapped list buffers, NUMA-local to the GPU when the host has several nodes
+void* pinned_list_alloc(int device, size_t bytes);
+void pinned_list_free(void* p);
 // Adopt a list generated in HBM (d_src, n elements of width w) into the
 // handle's placement; frees d_src unless it becomes the HBM copy.
 int adopt_device_list(zc_graph* g, void* d_src, uint32_t w, uint64_t n, void** h,
