@@ -1,26 +1,23 @@
-"""Quick timing of config 1 (uniform 2^20 deg 16) on the GPU: each strategy x
-placement, plus the link probe.  Development tool, not the bench."""
+"""Config 1 (uniform 2^20 deg 16, the reference's own CPU case): per-call
+latency of every strategy -- where per-level host round trips matter."""
 import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 import paper_2006_06890_b200 as zc
 
-print("probe", zc.link_probe(nbytes=1 << 30, iters=5), flush=True)
-t = time.time()
 g = zc.generate_uniform(2 ** 20, 16, 16, seed=3)
-print("gen", time.time() - t, flush=True)
 gw = zc.with_uniform_weights(g)
-for placement in ("zerocopy", "hbm", "uvm"):
-    for s in zc.AccessStrategy:
-        for algo, graph in (("bfs", g), ("sssp", gw)):
-            fn = getattr(zc, algo)
-            best = 1e9
+gu = zc.symmetrized(g)
+for placement in ("zerocopy", "hbm"):
+    for s in ("merged-aligned", "packed"):
+        for algo, graph in (("bfs", g), ("sssp", gw), ("cc", gu)):
+            best = None
             for _ in range(5):
-                r = fn(graph, 0, s, collect_traffic=False, placement=placement)
-                best = min(best, r.kernel_ms)
-            te = r.total_traversed_edges
-            eb = 8 if algo == "sssp" else 4
-            print(f"{placement:8s} {algo:4s} {s.value:15s} iters={r.iterations:3d} "
-                  f"kernel={best:8.3f} ms total={r.total_ms:8.3f} ms GTEPS={te/best/1e6:7.3f} "
-                  f"linkGB/s={te*eb/best/1e6:7.2f} launches={r.launches}", flush=True)
-        zc.release(graph)
+                r = zc.cc(graph, s, collect_traffic=False, placement=placement) if algo == "cc" \
+                    else getattr(zc, algo)(graph, 0, s, collect_traffic=False, placement=placement)
+                if best is None or r.kernel_ms < best.kernel_ms:
+                    best = r
+            te = best.total_traversed_edges
+            print(f"{placement:8s} {algo:4s} {s:15s} iters={best.iterations:3d} kernel={best.kernel_ms:7.3f} ms "
+                  f"expand={best.expand_ms:7.3f} ms call={best.total_ms:7.3f} ms "
+                  f"GTEPS={te/best.kernel_ms/1e6:7.2f} launches={best.launches}", flush=True)
+        zc.release(g); zc.release(gw); zc.release(gu)
