@@ -179,6 +179,9 @@ int zc_graph_evict(zc_graph *g);
 /* Per-handle run options. */
 #define ZC_OPT_TRAFFIC_MODEL 1u /* also evaluate the reference's request model
                                    (coalesce.py:165-207) on every frontier */
+#define ZC_OPT_HOST_LOOP 2u     /* drive the levels from the host instead of the
+                                   device-driven CUDA-graph loop (default for the
+                                   merged / merged-aligned / packed strategies) */
 int zc_set_options(zc_graph *g, uint32_t options);
 
 /* Modelled request histogram of the most recent run (needs

@@ -223,6 +223,9 @@ void zc::free_graph(zc_graph* g) {
   cudaFree(g->d_big_prefix);
   cudaFree(g->d_ctr);
   cudaFree(g->d_part_lo);
+  if (g->loop.exec) cudaGraphExecDestroy(g->loop.exec);
+  if (g->loop.graph) cudaGraphDestroy(g->loop.graph);
+  cudaFree(g->d_log);
   for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
   cudaFree(g->d_mine);
   cudaFree(g->d_peers);
@@ -410,6 +413,7 @@ int zc::alloc_state(zc_graph* g) {
   ZC_CUDA_TRY(cudaMalloc(&g->d_big_val, n1 * sizeof(uint64_t)));
   ZC_CUDA_TRY(cudaMalloc(&g->d_big_prefix, (n1 + 1) * sizeof(uint64_t)));
   ZC_CUDA_TRY(cudaMalloc(&g->d_ctr, kCtrCount * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMalloc(&g->d_log, 4 * kLogCap * sizeof(uint64_t)));
   ZC_CUDA_TRY(cudaMalloc(&g->d_wcnt, n1 * sizeof(uint32_t)));
   ZC_CUDA_TRY(cudaMalloc(&g->d_wpre, (n1 + 1) * sizeof(uint64_t)));
   g->scan_tmp_bytes = scan_tmp_bytes(n1);
@@ -484,6 +488,67 @@ int zc::adopt_device_list(zc_graph* g, void* d_src, uint32_t w, uint64_t n, void
 }
 
 namespace {
+
+bool tune_host_loop() {
+  const char* t = getenv("ZC_TUNE");
+  return t && strstr(t, "loop=host");
+}
+
+// Build (or reuse) the device-driven level loop of (algo, strategy): a CUDA
+// graph whose conditional WHILE node repeats
+//   stamp -> window counts -> scan -> sweep expansion -> stamp ->
+//   compaction -> level end (log + cudaGraphSetConditional)
+// with the frontier size / level read from device memory.
+int build_loop_graph(zc_graph* g, int algo, int strategy, int ebytes, const ExpandArgs& base,
+                     const CompactArgs& c) {
+  LoopGraph& L = g->loop;
+  if (L.exec && L.algo == algo && L.strategy == strategy && L.ebytes == ebytes &&
+      L.unroll == base.unroll && L.ctas == base.ctas_per_sm)
+    return ZC_OK;
+  if (L.exec) cudaGraphExecDestroy(L.exec);
+  if (L.graph) cudaGraphDestroy(L.graph);
+  L = LoopGraph{};
+  cudaStream_t st = g->stream;
+  ZC_CUDA_TRY(cudaGraphCreate(&L.graph, 0));
+  cudaGraphConditionalHandle loop;
+  ZC_CUDA_TRY(cudaGraphConditionalHandleCreate(&loop, L.graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = loop;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  ZC_CUDA_TRY(cudaGraphAddNode(&node, L.graph, nullptr, 0, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  ZC_CUDA_TRY(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeRelaxed));
+  ExpandArgs a = base;
+  a.n = g->nv;  // sizes grids; the kernels read the live size from n_dev
+  a.n_dev = g->d_ctr + kCtrCur;
+  a.iter_dev = g->d_ctr + kCtrIter;
+  uint64_t launches = 0;
+  cudaError_t e = launch_stamp(g->d_ctr, g->d_log + 2 * kLogCap, st);
+  if (e == cudaSuccess) e = launch_expand(strategy, algo, ebytes, g->wb, a, g->num_sms, st, &launches);
+  if (e == cudaSuccess) e = launch_stamp(g->d_ctr, g->d_log + 3 * kLogCap, st);
+  if (e == cudaSuccess) e = launch_compact(algo, c, st, &launches);
+  if (e == cudaSuccess)
+    e = launch_level_end(g->d_ctr, g->d_log, g->d_log + kLogCap, kLogCap, loop, st);
+  cudaGraph_t captured = nullptr;
+  const cudaError_t e2 = cudaStreamEndCapture(st, &captured);
+  if (e != cudaSuccess || e2 != cudaSuccess) {
+    set_error(std::string("level-loop capture: ") +
+              cudaGetErrorString(e != cudaSuccess ? e : e2));
+    return ZC_ECUDA;
+  }
+  ZC_CUDA_TRY(cudaGraphInstantiate(&L.exec, L.graph, 0));
+  L.algo = algo;
+  L.strategy = strategy;
+  L.ebytes = ebytes;
+  L.unroll = base.unroll;
+  L.ctas = base.ctas_per_sm;
+  L.launches_per_iter = launches + 3;
+  return ZC_OK;
+}
 
 // One traversal (traversal.py:98-179) on the handle.
 int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stats* stats) {
@@ -560,36 +625,25 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     n = 1;
     trav = g->h_off[src + 1] - g->h_off[src];
   }
-  ZC_CUDA_TRY(cudaEventRecord(g->ev[0], st));
-  int cur = 0;
-  uint64_t iters = 0, total_trav = 0, max_front = 0;
-  while (n > 0) {
-    ++iters;
-    g->log_trav.push_back(trav);
-    g->log_front.push_back(n);
-    total_trav += trav;
-    max_front = std::max(max_front, n);
-    if (model)
-      ZC_CUDA_TRY(launch_traffic_model(strategy, g->eb, g->wb, algo == kSssp, g->d_front[cur], n,
-                                       g->d_off, g->d_ctr, g->num_sms, st, &launches));
+  // Frontier buffers [0] are both read by the expansion and rewritten by the
+  // compaction (which only reads the marks), so the level loop has fixed
+  // pointers -- the device-driven loop below is one instantiated CUDA graph.
+  const bool pairs = algo == kSssp && g->d_pairs && !model;
+  auto expand_args = [&](uint64_t nn, uint32_t iter) {
     ExpandArgs a{};
-    a.front = g->d_front[cur];
-    a.fs = g->d_fs[cur];
-    a.fd = g->d_fd[cur];
-    a.fval = g->d_fval[cur];
-    a.n = n;
+    a.front = g->d_front[0];
+    a.fs = g->d_fs[0];
+    a.fd = g->d_fd[0];
+    a.fval = g->d_fval[0];
+    a.n = nn;
     a.off = g->d_off;
-    a.edges = g->d_edges;
-    a.weights = g->d_weights;
+    a.edges = pairs ? g->d_pairs : g->d_edges;  // interleaved (dst, weight) stream
+    a.weights = pairs ? nullptr : g->d_weights;
+    a.pairs = pairs ? 1 : 0;
     a.state = g->d_state;
     a.flags = g->d_flags;
     a.visited = g->d_visited;
-    if (algo == kSssp && g->d_pairs && !model) {  // interleaved (dst, weight) stream
-      a.edges = g->d_pairs;
-      a.weights = nullptr;
-      a.pairs = 1;
-    }
-    a.iter = static_cast<uint32_t>(iters);
+    a.iter = iter;
     a.big_s = g->d_big_s;
     a.big_e = g->d_big_e;
     a.big_val = g->d_big_val;
@@ -600,28 +654,88 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     a.scan_tmp = g->d_scan_tmp;
     a.scan_tmp_bytes = g->scan_tmp_bytes;
     tune_params(&a);
-    while (g->iter_ev.size() < 2 * iters) {
-      cudaEvent_t e;
-      ZC_CUDA_TRY(cudaEventCreate(&e));
-      g->iter_ev.push_back(e);
-    }
-    ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (iters - 1)], st));
-    ZC_CUDA_TRY(launch_expand(strategy, algo, a.pairs ? 8 : g->eb, g->wb, a, g->num_sms, st,
-                              &launches));
-    ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (iters - 1) + 1], st));
+    return a;
+  };
+  auto compact_args = [&]() {
     CompactArgs c;
     c.flags = g->d_flags;
     c.nv = g->nv;
     c.ntiles = g->ntiles;
     c.tiles = g->d_tiles;
-    c.front_out = g->d_front[cur ^ 1];
-    c.fs_out = g->d_fs[cur ^ 1];
-    c.fd_out = g->d_fd[cur ^ 1];
-    c.fval_out = g->d_fval[cur ^ 1];
+    c.front_out = g->d_front[0];
+    c.fs_out = g->d_fs[0];
+    c.fd_out = g->d_fd[0];
+    c.fval_out = g->d_fval[0];
     c.off = g->d_off;
     c.state = g->d_state;
     c.ctr = g->d_ctr;
-    ZC_CUDA_TRY(launch_compact(algo, c, st, &launches));
+    return c;
+  };
+  const int ebytes = pairs ? 8 : static_cast<int>(g->eb);
+  ZC_CUDA_TRY(cudaEventRecord(g->ev[0], st));
+  uint64_t iters = 0, total_trav = 0, max_front = 0;
+
+  // ---- device-driven loop: the whole traversal is one graph launch
+  const ExpandArgs probe = expand_args(g->nv, 0);
+  const bool device_loop = n > 0 && strategy != kNaive && !model && !probe.chunk_sched &&
+                           !(g->options & ZC_OPT_HOST_LOOP) && !tune_host_loop();
+  if (device_loop) {
+    int rc = build_loop_graph(g, algo, strategy, ebytes, expand_args(g->nv, 0), compact_args());
+    if (rc) return rc;
+    uint64_t* h = g->h_ctr;
+    h[kCtrCur] = n;
+    h[kCtrIter] = 0;
+    h[20] = trav;
+    h[21] = n;
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->d_ctr + kCtrCur, h + kCtrCur, 2 * sizeof(uint64_t),
+                                cudaMemcpyHostToDevice, st));
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->d_log, h + 20, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->d_log + kLogCap, h + 21, sizeof(uint64_t),
+                                cudaMemcpyHostToDevice, st));
+    ZC_CUDA_TRY(cudaGraphLaunch(g->loop.exec, st));
+    ZC_CUDA_TRY(cudaMemcpyAsync(h, g->d_ctr, kCtrCount * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                st));
+    ZC_CUDA_TRY(cudaStreamSynchronize(st));
+    iters = h[kCtrIter];
+    const uint64_t logged = std::min<uint64_t>(iters, kLogCap);
+    std::vector<uint64_t> lg(4 * kLogCap);
+    ZC_CUDA_TRY(cudaMemcpy(lg.data(), g->d_log, 4 * kLogCap * sizeof(uint64_t),
+                           cudaMemcpyDeviceToHost));
+    for (uint64_t k = 0; k < logged; ++k) {
+      g->log_trav.push_back(lg[k]);
+      g->log_front.push_back(lg[kLogCap + k]);
+      g->log_expand_ms.push_back((lg[3 * kLogCap + k] - lg[2 * kLogCap + k]) * 1e-6);
+      total_trav += lg[k];
+      max_front = std::max(max_front, lg[kLogCap + k]);
+    }
+    launches += iters * g->loop.launches_per_iter;
+    n = h[kCtrCur];  // non-zero only if the log capacity ran out: finish on the host
+    trav = h[kCtrTrav];
+  }
+
+  // ---- host-driven loop (naive, request model, tuning, or the tail past the log)
+  std::vector<uint64_t> host_iters;
+  while (n > 0) {
+    ++iters;
+    g->log_trav.push_back(trav);
+    g->log_front.push_back(n);
+    total_trav += trav;
+    max_front = std::max(max_front, n);
+    if (model)
+      ZC_CUDA_TRY(launch_traffic_model(strategy, g->eb, g->wb, algo == kSssp, g->d_front[0], n,
+                                       g->d_off, g->d_ctr, g->num_sms, st, &launches));
+    const ExpandArgs a = expand_args(n, static_cast<uint32_t>(iters));
+    while (g->iter_ev.size() < 2 * (host_iters.size() + 1)) {
+      cudaEvent_t e;
+      ZC_CUDA_TRY(cudaEventCreate(&e));
+      g->iter_ev.push_back(e);
+    }
+    const size_t ev = 2 * host_iters.size();
+    host_iters.push_back(iters);
+    ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[ev], st));
+    ZC_CUDA_TRY(launch_expand(strategy, algo, ebytes, g->wb, a, g->num_sms, st, &launches));
+    ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[ev + 1], st));
+    ZC_CUDA_TRY(launch_compact(algo, compact_args(), st, &launches));
     const size_t nctr = model ? kCtrCount : 2;
     ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, nctr * sizeof(uint64_t),
                                 cudaMemcpyDeviceToHost, st));
@@ -631,7 +745,6 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     n = g->h_ctr[kCtrNext];
     trav = g->h_ctr[kCtrTrav];
     if (model) g->log_hist.insert(g->log_hist.end(), g->h_ctr + kCtrHist, g->h_ctr + kCtrHist + 8);
-    cur ^= 1;
   }
   ZC_CUDA_TRY(cudaEventRecord(g->ev[1], st));
   // widen into an int64 staging buffer (free fval slot) and download
@@ -641,13 +754,13 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     ZC_CUDA_TRY(cudaMemcpyAsync(out, d_out, g->nv * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
   ZC_CUDA_TRY(cudaStreamSynchronize(st));
-  double expand_ms = 0;
-  for (uint64_t k = 0; k < iters; ++k) {
+  for (size_t k = 0; k < host_iters.size(); ++k) {
     float e = 0;
     cudaEventElapsedTime(&e, g->iter_ev[2 * k], g->iter_ev[2 * k + 1]);
     g->log_expand_ms.push_back(e);
-    expand_ms += e;
   }
+  double expand_ms = 0;
+  for (double x : g->log_expand_ms) expand_ms += x;
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     stats->iterations = iters;
@@ -659,7 +772,9 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     cudaEventElapsedTime(&ms, g->ev[1], g->ev[2]);
     stats->d2h_ms = ms;
     stats->h2d_bytes = h2d;
-    stats->d2h_bytes = g->nv * sizeof(int64_t) + iters * (model ? kCtrCount : 2) * sizeof(uint64_t);
+    stats->d2h_bytes = g->nv * sizeof(int64_t) +
+                       (device_loop ? (kCtrCount + 4 * kLogCap) : iters * (model ? kCtrCount : 2)) *
+                           sizeof(uint64_t);
     stats->launches = launches;
     stats->expand_ms = expand_ms;
     stats->total_ms = now_ms() - t0;
@@ -1499,7 +1614,7 @@ int zc_set_options(zc_graph* g, uint32_t options) {
     set_error("null graph handle");
     return ZC_ESTATE;
   }
-  if (options & ~ZC_OPT_TRAFFIC_MODEL) {
+  if (options & ~(ZC_OPT_TRAFFIC_MODEL | ZC_OPT_HOST_LOOP)) {
     set_error("unknown option bits");
     return ZC_EINVAL;
   }

@@ -10,6 +10,16 @@
 #include "../../include/zcgraph.h"
 #include "zc_internal.cuh"
 
+// Instantiated device-driven level loop (zc_api.cu build_loop_graph).
+struct LoopGraph {
+  int algo = -1, strategy = -1, ebytes = 0, unroll = 0, ctas = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t launches_per_iter = 0;
+};
+// log entries per array of the device loop (trav, front, t0, t1)
+constexpr uint64_t kLogCap = 4096;
+
 struct zc_graph {
   uint64_t nv = 0, ne = 0;
   uint32_t eb = 4, wb = 4;
@@ -64,6 +74,8 @@ struct zc_graph {
   std::vector<cudaEvent_t> iter_ev;  // 2 per iteration, grown on demand
   uint32_t options = 0;
   int multigraph = -1;  // cached duplicate-arc check (-1 unknown)
+  LoopGraph loop;
+  uint64_t* d_log = nullptr;  // 4 * kLogCap
   // vertex-range partition (multi-GPU); nparts == 0 for a whole graph
   uint32_t nparts = 0, part = 0;
   uint64_t global_nv = 0, lo = 0, stride = 0;

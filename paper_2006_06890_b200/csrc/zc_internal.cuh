@@ -71,7 +71,9 @@ enum Ctr : int {
   kCtrPrDelta = 5,     //   L1 change of the iteration
   kCtrPrSum = 6,       //   sum of ranks
   kCtrHist = 8,      // 8..11 modelled edge requests of 1..4 sectors, 12..15 weights
-  kCtrCount = 16
+  kCtrCur = 16,      // device level loop: size of the current frontier
+  kCtrIter = 17,     //   completed iterations
+  kCtrCount = 24
 };
 
 struct ExpandArgs {
@@ -112,6 +114,10 @@ struct ExpandArgs {
   int ctas_per_sm;
   int chunk_sched;  // 1: the per-warp chunk + big-list scheduler instead of the sweep
   int pairs;        // SSSP: `edges` is the interleaved (dst, weight) u32-pair list
+  // device-driven level loop: frontier size / completed iterations in device
+  // memory (then `n` is only the maximum, used to size grids)
+  const uint64_t* n_dev;
+  const uint64_t* iter_dev;
 };
 
 // ZC_TUNE="unroll=8,ctas=6,sched=chunk": expansion tuning knobs for experiments.
@@ -173,7 +179,11 @@ int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, const 
 
 // Exclusive scan of u32 counts into u64 offsets (n+1 outputs), device-wide.
 cudaError_t scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp,
-                            size_t tmp_bytes, cudaStream_t st);
+                            size_t tmp_bytes, cudaStream_t st, const uint64_t* n_dev = nullptr);
+// device level loop (CUDA graph with a conditional while node)
+cudaError_t launch_level_end(uint64_t* ctr, uint64_t* log_trav, uint64_t* log_front, uint64_t cap,
+                             cudaGraphConditionalHandle loop, cudaStream_t st);
+cudaError_t launch_stamp(const uint64_t* ctr, uint64_t* log_t, cudaStream_t st);
 size_t scan_tmp_bytes(uint64_t n);
 
 // error plumbing (zc_api.cu)

@@ -29,6 +29,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "zc_internal.cuh"
 
 namespace zc {
@@ -404,8 +406,9 @@ constexpr int kStage = 256;  // frontier slots staged in shared memory at a time
 // touches it -- so every block is fetched once per group and the lists that
 // share it are always staged together.
 template <int STRAT, typename ET>
-__global__ void k_window_counts(const uint64_t* fs, const uint32_t* fd, uint64_t n,
-                                uint32_t* wcnt) {
+__global__ void k_window_counts(const uint64_t* fs, const uint32_t* fd, uint64_t n0,
+                                const uint64_t* n_dev, uint32_t* wcnt) {
+  const uint64_t n = n_dev ? *n_dev : n0;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t s = fs[j], d = fd[j];
@@ -430,6 +433,10 @@ __global__ void k_window_counts(const uint64_t* fs, const uint32_t* fd, uint64_t
 
 template <int STRAT, int ALGO, typename ET, typename WT, int U>
 __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
+  if (a.n_dev) {  // device-driven level loop: size and level live in device memory
+    a.n = *a.n_dev;
+    a.iter = static_cast<uint32_t>(*a.iter_dev) + 1;
+  }
   __shared__ uint64_t sh_s[kStage], sh_e[kStage], sh_v[kStage];
   __shared__ uint64_t sh_w[kStage + 1];
   __shared__ uint64_t sh_j;
@@ -857,6 +864,31 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
   }
 }
 
+// ------------------------------------------------------- device level loop
+// One body of the CUDA-graph while loop ends here: log the next frontier,
+// make it current, and keep looping while it is non-empty (and the log has
+// room).  Single thread.
+__global__ void k_level_end(uint64_t* ctr, uint64_t* log_trav, uint64_t* log_front, uint64_t cap,
+                            cudaGraphConditionalHandle loop) {
+  const uint64_t it = ctr[kCtrIter] + 1;  // completed iterations
+  const uint64_t n = ctr[kCtrNext], t = ctr[kCtrTrav];
+  ctr[kCtrIter] = it;
+  ctr[kCtrCur] = n;
+  const bool more = n > 0 && it < cap;
+  if (more) {
+    log_trav[it] = t;
+    log_front[it] = n;
+  }
+  cudaGraphSetConditional(loop, more ? 1u : 0u);
+}
+
+// %globaltimer stamp of the current iteration (per-level expansion time).
+__global__ void k_stamp(const uint64_t* ctr, uint64_t* log_t) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  log_t[ctr[kCtrIter]] = t;
+}
+
 // ---------------------------------------------------------------- helpers
 __global__ void k_init_cc(uint32_t* label, uint64_t nv, uint32_t* front, uint64_t* fval,
                           const uint64_t* off, uint64_t* fs, uint32_t* fd, uint64_t base) {
@@ -1053,28 +1085,40 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr uint64_t kScanChunk = kScanThreads * kScanItems;
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* in, uint64_t n,
+// The size may live in device memory (n_dev, device-driven level loop): the
+// kernels then loop over chunks with a fixed grid.
+__device__ __forceinline__ uint64_t scan_n(uint64_t n, const uint64_t* n_dev) {
+  return n_dev ? *n_dev : n;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* in, uint64_t n0,
+                                                              const uint64_t* n_dev,
                                                               uint64_t* part) {
   __shared__ unsigned long long sh[kScanThreads / 32];
-  const uint64_t b = blockIdx.x;
-  const uint64_t base = b * kScanChunk + threadIdx.x * (uint64_t)kScanItems;
-  unsigned long long sum = 0;
+  const uint64_t n = scan_n(n0, n_dev), nb = (n + kScanChunk - 1) / kScanChunk;
+  for (uint64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const uint64_t base = b * kScanChunk + threadIdx.x * (uint64_t)kScanItems;
+    unsigned long long sum = 0;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i)
-    if (base + i < n) sum += in[base + i];
+    for (int i = 0; i < kScanItems; ++i)
+      if (base + i < n) sum += in[base + i];
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) sum += __shfl_down_sync(kFull, sum, d);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = sum;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int w = 0; w < kScanThreads / 32; ++w) t += sh[w];
-    part[b] = t;
+    for (int d = 16; d > 0; d >>= 1) sum += __shfl_down_sync(kFull, sum, d);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+      for (int w = 0; w < kScanThreads / 32; ++w) t += sh[w];
+      part[b] = t;
+    }
+    __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(1024) k_scan_partials(uint64_t* part, uint64_t nb) {
+__global__ void __launch_bounds__(1024) k_scan_partials(uint64_t* part, uint64_t nb0,
+                                                        const uint64_t* n_dev) {
   __shared__ uint64_t warp_sums[32];
+  const uint64_t nb = n_dev ? (*n_dev + kScanChunk - 1) / kScanChunk : nb0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t chunk = (nb + blockDim.x - 1) / blockDim.x;
   const uint64_t lo = min(nb, tid * chunk), hi = min(nb, lo + chunk);
@@ -1106,37 +1150,43 @@ __global__ void __launch_bounds__(1024) k_scan_partials(uint64_t* part, uint64_t
     run += c;
   }
   if (hi == nb && lo < hi) part[nb] = run;
+  if (nb == 0 && tid == 0) part[0] = 0;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* in, uint64_t n,
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* in, uint64_t n0,
+                                                            const uint64_t* n_dev,
                                                             const uint64_t* part, uint64_t* out) {
   __shared__ unsigned long long warp_tot[kScanThreads / 32];
-  const uint64_t b = blockIdx.x;
+  const uint64_t n = scan_n(n0, n_dev), nb = (n + kScanChunk - 1) / kScanChunk;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint64_t base = b * kScanChunk + threadIdx.x * (uint64_t)kScanItems;
-  uint32_t vals[kScanItems];
-  unsigned long long sum = 0;
+  if (nb == 0 && blockIdx.x == 0 && threadIdx.x == 0) out[0] = 0;
+  for (uint64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const uint64_t base = b * kScanChunk + threadIdx.x * (uint64_t)kScanItems;
+    uint32_t vals[kScanItems];
+    unsigned long long sum = 0;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    vals[i] = base + i < n ? in[base + i] : 0;
-    sum += vals[i];
-  }
-  unsigned long long incl = sum;
+    for (int i = 0; i < kScanItems; ++i) {
+      vals[i] = base + i < n ? in[base + i] : 0;
+      sum += vals[i];
+    }
+    unsigned long long incl = sum;
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const unsigned long long t = __shfl_up_sync(kFull, incl, d);
-    if (lane >= d) incl += t;
-  }
-  if (lane == 31) warp_tot[wid] = incl;
-  __syncthreads();
-  unsigned long long run = part[b] + incl - sum;
-  for (int w = 0; w < wid; ++w) run += warp_tot[w];
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long t = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += t;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    unsigned long long run = part[b] + incl - sum;
+    for (int w = 0; w < wid; ++w) run += warp_tot[w];
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    if (base + i < n) out[base + i] = run;
-    run += vals[i];
+    for (int i = 0; i < kScanItems; ++i) {
+      if (base + i < n) out[base + i] = run;
+      run += vals[i];
+    }
+    if (b == nb - 1 && threadIdx.x == kScanThreads - 1) out[n] = part[nb];
+    __syncthreads();
   }
-  if (b == gridDim.x - 1 && threadIdx.x == kScanThreads - 1) out[n] = part[gridDim.x];
 }
 
 int grid_for(uint64_t work, int threads, int num_sms, int per_sm) {
@@ -1159,8 +1209,9 @@ cudaError_t expand_sweep(const ExpandArgs& a, int num_sms, cudaStream_t st,
                          uint64_t* launches) {
   // window counts -> global exclusive prefix (wpre[n] = total windows)
   const int g1 = grid_for(a.n, 256, num_sms, 16);
-  k_window_counts<STRAT, ET><<<g1, 256, 0, st>>>(a.fs, a.fd, a.n, a.wcnt);
-  cudaError_t e = scan_u32_to_u64(a.wcnt, a.wpre, a.n, a.scan_tmp, a.scan_tmp_bytes, st);
+  k_window_counts<STRAT, ET><<<g1, 256, 0, st>>>(a.fs, a.fd, a.n, a.n_dev, a.wcnt);
+  cudaError_t e =
+      scan_u32_to_u64(a.wcnt, a.wpre, a.n, a.scan_tmp, a.scan_tmp_bytes, st, a.n_dev);
   if (e != cudaSuccess) return e;
   static int grid = 0;  // per instantiation: all CTAs resident at once
   if (!grid) grid = resident_ctas(k_expand_sweep<STRAT, ALGO, ET, WT, U>, kSweepThreads, num_sms);
@@ -1318,6 +1369,17 @@ cudaError_t launch_part_apply(int algo, const void* mine, uint64_t nlocal, void*
   return cudaGetLastError();
 }
 
+cudaError_t launch_level_end(uint64_t* ctr, uint64_t* log_trav, uint64_t* log_front, uint64_t cap,
+                             cudaGraphConditionalHandle loop, cudaStream_t st) {
+  k_level_end<<<1, 1, 0, st>>>(ctr, log_trav, log_front, cap, loop);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stamp(const uint64_t* ctr, uint64_t* log_t, cudaStream_t st) {
+  k_stamp<<<1, 1, 0, st>>>(ctr, log_t);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pr_init(uint64_t nv, const uint64_t* off, uint32_t* front, uint64_t* fs,
                            uint32_t* fd, double* rank, cudaStream_t st, uint64_t* launches) {
   if (nv == 0) return cudaSuccess;
@@ -1394,14 +1456,16 @@ size_t scan_tmp_bytes(uint64_t n) {
 }
 
 cudaError_t scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp,
-                            size_t tmp_bytes, cudaStream_t st) {
-  if (n == 0) return cudaMemsetAsync(out, 0, sizeof(uint64_t), st);
+                            size_t tmp_bytes, cudaStream_t st, const uint64_t* n_dev) {
+  // n: the size, or with n_dev the maximum size (the grid is sized for it)
+  if (n == 0 && !n_dev) return cudaMemsetAsync(out, 0, sizeof(uint64_t), st);
   const uint64_t nb = (n + kScanChunk - 1) / kScanChunk;
   if (tmp_bytes < (nb + 1) * sizeof(uint64_t)) return cudaErrorInvalidValue;
   uint64_t* part = static_cast<uint64_t*>(tmp);
-  k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, st>>>(in, n, part);
-  k_scan_partials<<<1, 1024, 0, st>>>(part, nb);
-  k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, st>>>(in, n, part, out);
+  const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(nb, 148 * 8)));
+  k_scan_reduce<<<grid, kScanThreads, 0, st>>>(in, n, n_dev, part);
+  k_scan_partials<<<1, 1024, 0, st>>>(part, nb, n_dev);
+  k_scan_down<<<grid, kScanThreads, 0, st>>>(in, n, n_dev, part, out);
   return cudaGetLastError();
 }
 

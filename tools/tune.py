@@ -6,7 +6,7 @@ import paper_2006_06890_b200 as zc
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=27)
 ap.add_argument("--algo", default="bfs")
-ap.add_argument("--configs", default="sched=chunk;;unroll=2;unroll=8;ctas=4;ctas=6")
+ap.add_argument("--configs", default="loop=host;;sched=chunk;unroll=8")
 ap.add_argument("--strategy", default="merged-aligned")
 ap.add_argument("--strategies", default="")
 ap.add_argument("--pairs", action="store_true")
