@@ -356,3 +356,19 @@ def test_scale_parity_k24():
     for s in ("merged-aligned", "packed"):
         r = zc.cc(sg, s, collect_traffic=False)
         assert np.array_equal(r.values, ref.values) and r.iterations == ref.iterations
+
+
+def test_device_loop_hands_off_past_log_capacity():
+    """A 6000-level chain outgrows the device loop's 4096-entry level log;
+    the host loop finishes the traversal with identical results and logs."""
+    n = 6000
+    chain = zc.CsrGraph(n, n - 1, np.concatenate([np.arange(n), [n - 1]]).astype(np.int64),
+                        np.arange(1, n, dtype=np.int64), weights=np.ones(n - 1, np.int64))
+    for algo in ("bfs", "sssp"):
+        ref = oracle.run(algo, chain, 0)
+        for s in ("merged-aligned", "packed"):
+            r = getattr(zc, algo)(chain, 0, s, collect_traffic=False)
+            assert r.iterations == ref.iterations == n
+            assert np.array_equal(r.values, ref.values)
+            assert r.traversed_edges == ref.traversed_edges
+            assert len(r.frontier_sizes) == n
