@@ -279,6 +279,11 @@ int zc_generate_rmat_part(uint32_t scale, uint32_t edge_factor, double a, double
 int zc_read_probe(int32_t device, uint64_t bytes, int pattern, uint32_t chunk_bytes, int alloc,
                   int iters, double *gbs);
 
+/* TMA bulk-copy (cp.async.bulk) streaming read of pinned host memory:
+ * `chunk`-byte copies into a 4-stage shared-memory ring per CTA. */
+int zc_bulk_probe(int32_t device, uint64_t bytes, uint32_t chunk, int ctas_per_sm, int iters,
+                  double *gbs);
+
 #ifdef __cplusplus
 }
 #endif

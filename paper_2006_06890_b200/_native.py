@@ -30,7 +30,7 @@ EXPORTED = (
     "zc_part_exchange_elem_bytes", "zc_part_begin", "zc_part_expand", "zc_part_apply",
     "zc_part_result", "zc_generate_rmat_part", "zc_pagerank", "zc_graph_multigraph",
     "zc_part_fused_init", "zc_part_fused_connect", "zc_part_fused_reset", "zc_part_fused_expand",
-    "zc_graph_open_emgi", "zc_graph_build_pairs",
+    "zc_graph_open_emgi", "zc_graph_build_pairs", "zc_bulk_probe",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -100,6 +100,7 @@ def _declare(lib: C.CDLL) -> None:
         "zc_link_probe": (C.c_int, [i32, u64, C.c_int, C.POINTER(dbl), C.POINTER(dbl),
                                     C.POINTER(dbl)]),
         "zc_read_probe": (C.c_int, [i32, u64, C.c_int, u32, C.c_int, C.c_int, C.POINTER(dbl)]),
+        "zc_bulk_probe": (C.c_int, [i32, u64, u32, C.c_int, C.c_int, C.POINTER(dbl)]),
         "zc_part_create": (C.c_int, [C.POINTER(GraphDesc), C.POINTER(PartInfo), C.POINTER(P)]),
         "zc_part_exchange_elem_bytes": (C.c_size_t, [C.c_int]),
         "zc_part_begin": (C.c_int, [P, C.c_int, u64, C.c_int, C.POINTER(u64), C.POINTER(u64)]),

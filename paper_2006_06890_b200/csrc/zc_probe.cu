@@ -96,8 +96,122 @@ __global__ void __launch_bounds__(256) k_chunk_read(const uint32_t* __restrict__
   if (acc == 0x12345678u) atomicAdd(sink, 1ull);
 }
 
+// Bulk-copy (TMA engine, cp.async.bulk) streaming read: every CTA streams
+// its own contiguous region chunk by chunk into a ring of shared-memory
+// stages; one elected thread issues the copies, an mbarrier per stage
+// tracks the transaction bytes.
+constexpr int kBulkStages = 4;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(bytes));
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, "
+      "p; }"
+      : "=r"(ok)
+      : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))), "r"(phase));
+  return ok;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(128) k_bulk_read(const char* __restrict__ src, uint64_t bytes,
+                                                   uint32_t chunk,
+                                                   unsigned long long* sink) {
+  extern __shared__ __align__(128) char stage[];
+  __shared__ __align__(8) uint64_t bar[kBulkStages];
+  const uint64_t nchunks = bytes / chunk;
+  const uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+  const uint64_t c0 = blockIdx.x * per, c1 = min(nchunks, c0 + per);
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kBulkStages; ++s) mbar_init(&bar[s], 1);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  uint32_t acc = 0;
+  if (threadIdx.x == 0) {
+    uint64_t issued = c0;
+    for (int s = 0; s < kBulkStages && issued < c1; ++s, ++issued) {
+      mbar_expect_tx(&bar[s], chunk);
+      bulk_g2s(stage + s * chunk, src + issued * chunk, chunk, &bar[s]);
+    }
+    uint32_t phase[kBulkStages] = {0, 0, 0, 0};
+    for (uint64_t c = c0; c < c1; ++c) {
+      const int s = static_cast<int>((c - c0) % kBulkStages);
+      while (!mbar_try_wait(&bar[s], phase[s])) {
+      }
+      phase[s] ^= 1;
+      acc ^= *reinterpret_cast<const uint32_t*>(stage + s * chunk);
+      if (issued < c1) {
+        mbar_expect_tx(&bar[s], chunk);
+        bulk_g2s(stage + s * chunk, src + issued * chunk, chunk, &bar[s]);
+        ++issued;
+      }
+    }
+  }
+  if (acc == 0x12345678u) atomicAdd(sink, 1ull);
+}
+
 }  // namespace
 }  // namespace zc
+
+// TMA bulk-copy streaming read of `bytes` of pinned host memory in `chunk`-
+// byte copies (multiple of 16, <= 48 KB), `ctas_per_sm` CTAs per SM.
+extern "C" int zc_bulk_probe(int32_t device, uint64_t bytes, uint32_t chunk, int ctas_per_sm,
+                             int iters, double* gbs) {
+  using namespace zc;
+  cudaSetDevice(device);
+  if (chunk < 16 || chunk % 16 || chunk * kBulkStages > 200 * 1024) {
+    set_error("chunk must be a multiple of 16 with 4 stages fitting in shared memory");
+    return ZC_EINVAL;
+  }
+  bytes = std::max<uint64_t>(bytes / chunk * chunk, chunk);
+  void* h = nullptr;
+  ZC_CUDA_TRY(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(h, 1, bytes);
+  void* d = nullptr;
+  ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, h, 0));
+  unsigned long long* sink = nullptr;
+  ZC_CUDA_TRY(cudaMalloc(&sink, sizeof(unsigned long long)));
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  const size_t smem = static_cast<size_t>(chunk) * kBulkStages;
+  ZC_CUDA_TRY(cudaFuncSetAttribute(k_bulk_read, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  const int grid = nsm * std::max(1, ctas_per_sm);
+  k_bulk_read<<<grid, 128, smem>>>(static_cast<const char*>(d), bytes, chunk, sink);
+  ZC_CUDA_TRY(cudaGetLastError());
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  for (int k = 0; k < std::max(iters, 1); ++k)
+    k_bulk_read<<<grid, 128, smem>>>(static_cast<const char*>(d), bytes, chunk, sink);
+  cudaEventRecord(b);
+  ZC_CUDA_TRY(cudaEventSynchronize(b));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  *gbs = static_cast<double>(bytes) * std::max(iters, 1) / (ms * 1e6);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  cudaFreeHost(h);
+  return ZC_OK;
+}
 
 // alloc: 0 = cudaHostAlloc(Mapped), 1 = THP (madvise) + cudaHostRegister,
 // 2 = device memory.  Returns GB/s of useful bytes in *gbs.
