@@ -290,6 +290,9 @@ def main():
                      "peak_kind": "PCIe Gen5 x16 theoretical per direction",
                      "measured_peaks_gbs": probe,
                      "frac_of_measured_memcpy": achieved / probe["memcpy_h2d_gbs"],
+                     # SM-side sysmem reads (ld or TMA cp.async.bulk) cap at the
+                     # zero-copy streaming peak (profiles/r01_tma_bulk_probe.txt)
+                     "frac_of_measured_zerocopy_ceiling": achieved / probe["zerocopy_read_gbs"],
                      "sysmem_bytes_per_launch": ncu.get("sysmem_bytes_per_launch")},
         "clocks": clk.summary(),
         "graph": {"vertices": dg.num_vertices, "arcs": dg.num_edges, "gen_s": gen_s,
