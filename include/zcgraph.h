@@ -63,6 +63,9 @@ extern "C" {
 #define ZC_PACKED 3         /* B200 extension (not in the reference): windows are
                                aligned 32-element blocks of the union of the
                                frontier's lists, each fetched once           */
+#define ZC_COMPRESSED 4     /* B200 host-store option: lists sorted and stored
+                               delta-encoded (zc_graph_build_compressed); BFS,
+                               CC, PageRank (order-independent) only          */
 
 /* where the edge / weight lists live */
 #define ZC_PLACE_ZEROCOPY 0 /* cudaHostAlloc(Mapped|Portable) or cudaHostRegister */
@@ -151,6 +154,11 @@ int zc_cc(zc_graph *g, int strategy, int64_t *out, zc_stats *stats);
  * caller buffer of V doubles.  Same ValueError conditions (ZC_EINVAL). */
 int zc_pagerank(zc_graph *g, int strategy, double damping, uint64_t max_iters, double tol,
                 double *out, zc_stats *stats);
+/* Build (once) the delta-compressed copy of the lists (sorted, 128-element
+ * blocks: u32 base + deltas at the list's bit width) in the handle's
+ * placement; *compressed_bytes (may be NULL) receives its size.  Built
+ * automatically by the first ZC_COMPRESSED run. */
+int zc_graph_build_compressed(zc_graph *g, uint64_t *compressed_bytes);
 /* Build (once) an interleaved copy of the lists as 8-byte (dst, weight) u32
  * pairs in the handle's placement; SSSP then reads one stream instead of two,
  * so a list of n edges costs ceil(8n/128) line requests instead of two

@@ -15,7 +15,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_NAME = "libzcgraph_b200.so"
 LIB_PATH = os.path.join(PKG, LIB_NAME)
 
-SOURCES = ["zc_api.cu", "zc_kernels.cu", "zc_gen.cu", "zc_probe.cu"]
+SOURCES = ["zc_api.cu", "zc_kernels.cu", "zc_gen.cu", "zc_probe.cu", "zc_compress.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
               "-Xptxas", "-v", "--expt-relaxed-constexpr"]

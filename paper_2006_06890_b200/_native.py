@@ -13,7 +13,7 @@ import threading
 from ._build import LIB_PATH
 
 ZC_OK, ZC_EINVAL, ZC_ECUDA, ZC_ENOMEM, ZC_ESTATE = 0, -1, -2, -3, -4
-ZC_NAIVE, ZC_MERGED, ZC_MERGED_ALIGNED, ZC_PACKED = 0, 1, 2, 3
+ZC_NAIVE, ZC_MERGED, ZC_MERGED_ALIGNED, ZC_PACKED, ZC_COMPRESSED = 0, 1, 2, 3, 4
 ZC_PLACE_ZEROCOPY, ZC_PLACE_UVM, ZC_PLACE_HBM = 0, 1, 2
 ZC_F_DIRECTED, ZC_F_REGISTER, ZC_F_UVM_PREFETCH, ZC_F_NO_VALIDATE = 1, 2, 4, 8
 ABI_VERSION = 1
@@ -30,7 +30,7 @@ EXPORTED = (
     "zc_part_exchange_elem_bytes", "zc_part_begin", "zc_part_expand", "zc_part_apply",
     "zc_part_result", "zc_generate_rmat_part", "zc_pagerank", "zc_graph_multigraph",
     "zc_part_fused_init", "zc_part_fused_connect", "zc_part_fused_reset", "zc_part_fused_expand",
-    "zc_graph_open_emgi", "zc_graph_build_pairs", "zc_bulk_probe",
+    "zc_graph_open_emgi", "zc_graph_build_pairs", "zc_bulk_probe", "zc_graph_build_compressed",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -86,6 +86,7 @@ def _declare(lib: C.CDLL) -> None:
         "zc_pagerank": (C.c_int, [P, C.c_int, dbl, u64, dbl, P, C.POINTER(Stats)]),
         "zc_graph_multigraph": (C.c_int, [P, C.POINTER(C.c_int)]),
         "zc_graph_build_pairs": (C.c_int, [P]),
+        "zc_graph_build_compressed": (C.c_int, [P, C.POINTER(u64)]),
         "zc_run_log": (C.c_int, [P, P, P, u64]),
         "zc_set_options": (C.c_int, [P, u32]),
         "zc_run_profile": (C.c_int, [P, P, u64]),

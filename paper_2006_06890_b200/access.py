@@ -21,7 +21,9 @@ class AccessStrategy(Enum):
 # "packed" is a B200 extension beyond the reference's three (include/zcgraph.h
 # ZC_PACKED): windows are the aligned 32-element blocks of the union of the
 # frontier's lists, fetched once each.  Results are identical.
-_IDS = {"naive": 0, "merged": 1, "merged-aligned": 2, "packed": 3}
+# "compressed" (ZC_COMPRESSED) streams the lists delta-encoded (sorted, so only
+# for the order-independent BFS / CC / PageRank).
+_IDS = {"naive": 0, "merged": 1, "merged-aligned": 2, "packed": 3, "compressed": 4}
 
 
 def strategy_id(strategy) -> int:

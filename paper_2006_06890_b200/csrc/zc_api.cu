@@ -205,6 +205,9 @@ void zc::free_graph(zc_graph* g) {
   free_list(g->h_edges, g->edges_registered, g->hbm_edges);
   free_list(g->h_weights, g->weights_registered, g->hbm_weights);
   free_list(g->h_pairs, false, g->hbm_pairs);
+  free_list(g->h_cmp, false, g->hbm_cmp);
+  cudaFree(g->d_coff);
+  cudaFree(g->d_cw);
   if (g->h_off) cudaFreeHost(g->h_off);
   cudaFree(g->d_off);
   cudaFree(g->d_state);
@@ -557,13 +560,21 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     set_error("null graph handle");
     return ZC_ESTATE;
   }
-  if (strategy < kNaive || strategy > kPacked) {
+  if (strategy < kNaive || strategy > kCompressed) {
     set_error("unknown access strategy " + std::to_string(strategy));
     return ZC_EINVAL;
   }
-  if (strategy == kPacked && (g->options & ZC_OPT_TRAFFIC_MODEL)) {
+  if (strategy >= kPacked && (g->options & ZC_OPT_TRAFFIC_MODEL)) {
     set_error("the request model is defined for the reference's three strategies "
-              "(naive, merged, merged-aligned), not for packed");
+              "(naive, merged, merged-aligned), not for packed / compressed");
+    return ZC_EINVAL;
+  }
+  if (strategy == kCompressed && algo == kSssp) {
+    set_error("compressed lists carry no weights: use packed (or the pairs layout) for sssp");
+    return ZC_EINVAL;
+  }
+  if (strategy == kCompressed && g->eb != 4) {
+    set_error("compressed lists need 4-byte edges");
     return ZC_EINVAL;
   }
   if (algo != kCc && src >= g->nv) {  // traversal.py:93-95
@@ -591,6 +602,10 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     return ZC_EINVAL;
   }
   DeviceGuard dg(g->device);
+  if (strategy == kCompressed && !g->d_cmp) {  // built once per handle
+    const int rc = zc_graph_build_compressed(g, nullptr);
+    if (rc) return rc;
+  }
   cudaStream_t st = g->stream;
   uint64_t launches = 0;
   g->log_trav.clear();
@@ -653,6 +668,9 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     a.wpre = g->d_wpre;
     a.scan_tmp = g->d_scan_tmp;
     a.scan_tmp_bytes = g->scan_tmp_bytes;
+    a.cmp = static_cast<const uint32_t*>(g->d_cmp);
+    a.coff = g->d_coff;
+    a.cw = g->d_cw;
     tune_params(&a);
     return a;
   };
@@ -1392,12 +1410,16 @@ int zc_pagerank(zc_graph* g, int strategy, double damping, uint64_t max_iters, d
     set_error("pagerank needs at least one vertex");
     return ZC_EINVAL;
   }
-  if (strategy < kNaive || strategy > kPacked) {
+  if (strategy < kNaive || strategy > kCompressed) {
     set_error("unknown access strategy " + std::to_string(strategy));
     return ZC_EINVAL;
   }
   const bool model = (g->options & ZC_OPT_TRAFFIC_MODEL) != 0;
-  if (strategy == kPacked && model) {
+  if (strategy == kCompressed && !g->d_cmp) {
+    const int rc = zc_graph_build_compressed(g, nullptr);
+    if (rc) return rc;
+  }
+  if (strategy >= kPacked && model) {
     set_error("the request model is defined for the reference's three strategies "
               "(naive, merged, merged-aligned), not for packed");
     return ZC_EINVAL;
@@ -1451,6 +1473,9 @@ int zc_pagerank(zc_graph* g, int strategy, double damping, uint64_t max_iters, d
     a.big_prefix = g->d_big_prefix;
     a.ctr = g->d_ctr;
     a.exch = pushed;
+    a.cmp = static_cast<const uint32_t*>(g->d_cmp);
+    a.coff = g->d_coff;
+    a.cw = g->d_cw;
     a.wcnt = g->d_wcnt;
     a.wpre = g->d_wpre;
     a.scan_tmp = g->d_scan_tmp;

@@ -39,6 +39,13 @@ struct zc_graph {
   const void* d_weights = nullptr;
   void* hbm_edges = nullptr;
   void* hbm_weights = nullptr;
+  // optional delta-compressed lists (zc_graph_build_compressed)
+  void* h_cmp = nullptr;
+  const void* d_cmp = nullptr;
+  void* hbm_cmp = nullptr;
+  uint64_t* d_coff = nullptr;
+  uint8_t* d_cw = nullptr;
+  uint64_t cmp_bytes = 0;
   // optional interleaved (dst, weight) u32 pairs for SSSP (zc_graph_build_pairs)
   void* h_pairs = nullptr;
   const void* d_pairs = nullptr;

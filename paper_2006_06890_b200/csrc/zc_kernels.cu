@@ -416,6 +416,10 @@ __global__ void k_window_counts(const uint64_t* fs, const uint32_t* fd, uint64_t
       wcnt[j] = 0;
       continue;
     }
+    if (STRAT == kCompressed) {
+      wcnt[j] = static_cast<uint32_t>((d + kCmpBlock - 1) / kCmpBlock);
+      continue;
+    }
     uint64_t w = (s + d - window_base<STRAT, ET>(s) + kWarp - 1) / kWarp;
     if (STRAT == kPacked) {
       const uint64_t group0 = j - j % kStage;
@@ -541,6 +545,120 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
         visit_batch<ALGO, ET, WT, U>(a, cur);
         cur = nxt;
       }
+    }
+    __syncthreads();
+    W = Wend;
+    j += kStage;
+  }
+}
+
+// Compressed lists (kCompressed): the sweep schedule with one window = one
+// 128-element block.  A warp loads the block's words (coalesced, <= 512 B),
+// stages them in shared memory, decodes 4 elements per lane (bit extraction +
+// a warp prefix sum over base and deltas) and visits them.
+template <int ALGO>
+__global__ void __launch_bounds__(kSweepThreads) k_expand_sweep_cmp(ExpandArgs a) {
+  if (a.n_dev) {
+    a.n = *a.n_dev;
+    a.iter = static_cast<uint32_t>(*a.iter_dev) + 1;
+  }
+  __shared__ uint64_t sh_c[kStage], sh_v[kStage];
+  __shared__ uint64_t sh_w[kStage + 1];
+  __shared__ uint32_t sh_d[kStage];
+  __shared__ uint8_t sh_bits[kStage];
+  __shared__ uint32_t sh_blk[kSweepWarps][4 * kWarp + 2];
+  __shared__ uint64_t sh_j;
+  const uint64_t n = a.n;
+  const uint64_t T = a.wpre[n];
+  const uint64_t G = gridDim.x, b = blockIdx.x;
+  const uint64_t Wb = T / G * b + min(b, T % G);
+  const uint64_t We = Wb + T / G + (b < T % G ? 1 : 0);
+  if (Wb >= We) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    uint64_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+      const uint64_t step = (hi - lo + 31) / 32;
+      const uint64_t probe = lo + step * (lane + 1);
+      const bool le = probe < hi && a.wpre[probe] <= Wb;
+      const unsigned m = __ballot_sync(kFull, le);
+      const int k = m ? 31 - __clz(m) : -1;
+      const uint64_t nlo = k >= 0 ? lo + step * (k + 1) : lo;
+      hi = min(hi, nlo + step);
+      lo = nlo;
+    }
+    if (lane == 0) sh_j = lo - lo % kStage;
+  }
+  __syncthreads();
+  uint64_t j = sh_j;
+  uint64_t W = Wb;
+  uint32_t* blk = sh_blk[warp];
+  while (W < We) {
+    for (int i = threadIdx.x; i <= kStage; i += kSweepThreads) {
+      const uint64_t jj = j + i;
+      sh_w[i] = jj <= n ? a.wpre[jj] : T;
+      if (i < kStage && jj < n) {
+        const uint32_t v = a.front[jj];
+        sh_c[i] = a.coff[v];
+        sh_bits[i] = a.cw[v];
+        sh_d[i] = a.fd[jj];
+        if (AlgoTraits<ALGO>::has_val) sh_v[i] = a.fval[jj];
+      }
+    }
+    __syncthreads();
+    const uint64_t Wend = min(We, sh_w[kStage]);
+    for (uint64_t q = W + warp; q < Wend; q += kSweepWarps) {
+      int lo = 0, hi = kStage;  // sh_w[lo] <= q < sh_w[hi]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (sh_w[mid] <= q) lo = mid; else hi = mid;
+      }
+      const uint64_t t = q - sh_w[lo];
+      const uint32_t w = sh_bits[lo];
+      const uint64_t rem = sh_d[lo] - t * kCmpBlock;
+      const uint64_t cnt = rem < kCmpBlock ? rem : kCmpBlock;
+      const uint32_t words = static_cast<uint32_t>(cmp_block_bytes(w, cnt) / 4);
+      const uint32_t* src = a.cmp + (sh_c[lo] + t * cmp_full_bytes(w)) / 4;
+      uint32_t x[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t qi = r * kWarp + lane;
+        x[r] = qi < words ? ld_list(src + qi) : 0u;
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) blk[r * kWarp + lane] = x[r];
+      if (lane < 2) blk[4 * kWarp + lane] = 0;
+      __syncwarp();
+      // element e = 4 * lane + i: e == 0 -> base, else delta e-1 at bit 32 + (e-1) w
+      const uint64_t mask = w >= 32 ? 0xffffffffull : ((1ull << w) - 1);
+      uint64_t val[4];
+      uint64_t run = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t e = 4 * lane + i;
+        uint64_t xval = 0;
+        if (e == 0) {
+          xval = blk[0];
+        } else if (e < cnt) {
+          const uint32_t bit = 32 + (e - 1) * w;
+          const uint64_t pair = (static_cast<uint64_t>(blk[(bit >> 5) + 1]) << 32) | blk[bit >> 5];
+          xval = (pair >> (bit & 31)) & mask;
+        }
+        run += xval;
+        val[i] = run;
+      }
+      uint64_t incl = run;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t o = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += o;
+      }
+      const uint64_t before = incl - run;
+      __syncwarp();
+      const uint64_t sval = AlgoTraits<ALGO>::has_val ? sh_v[lo] : 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (4 * lane + i < cnt) Visit<ALGO>::apply(a, before + val[i], 0, sval);
     }
     __syncthreads();
     W = Wend;
@@ -1284,9 +1402,34 @@ cudaError_t expand_a(int algo, int eb, int wb, const ExpandArgs& a, int num_sms,
 
 }  // namespace
 
+template <int ALGO>
+cudaError_t expand_cmp(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t* launches) {
+  const int g1 = grid_for(a.n, 256, num_sms, 16);
+  k_window_counts<kCompressed, uint32_t><<<g1, 256, 0, st>>>(a.fs, a.fd, a.n, a.n_dev, a.wcnt);
+  cudaError_t e =
+      scan_u32_to_u64(a.wcnt, a.wpre, a.n, a.scan_tmp, a.scan_tmp_bytes, st, a.n_dev);
+  if (e != cudaSuccess) return e;
+  static int grid = 0;
+  if (!grid) grid = resident_ctas(k_expand_sweep_cmp<ALGO>, kSweepThreads, num_sms);
+  const int g = a.ctas_per_sm > 0 ? num_sms * a.ctas_per_sm : grid;
+  k_expand_sweep_cmp<ALGO><<<g, kSweepThreads, 0, st>>>(a);
+  *launches += 5;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_expand(int strategy, int algo, int edge_bytes, int weight_bytes,
                           const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t* launches) {
   if (a.n == 0) return cudaSuccess;
+  if (strategy == kCompressed) {
+    switch (algo) {
+      case kBfs: return expand_cmp<kBfs>(a, num_sms, st, launches);
+      case kCc: return expand_cmp<kCc>(a, num_sms, st, launches);
+      case kPr: return expand_cmp<kPr>(a, num_sms, st, launches);
+      case kBfs + kPartAlgo: return expand_cmp<kBfs + kPartAlgo>(a, num_sms, st, launches);
+      case kCc + kPartAlgo: return expand_cmp<kCc + kPartAlgo>(a, num_sms, st, launches);
+      default: return cudaErrorInvalidValue;  // sssp: no weights in the compressed stream
+    }
+  }
   switch (strategy) {
     case kNaive: return expand_a<kNaive>(algo, edge_bytes, weight_bytes, a, num_sms, st, launches);
     case kMerged: return expand_a<kMerged>(algo, edge_bytes, weight_bytes, a, num_sms, st, launches);

@@ -197,6 +197,13 @@ class DeviceGraph:
         8 B/edge of host memory); results are identical."""
         N.check(N.lib().zc_graph_build_pairs(self.handle))
 
+    def build_compressed(self) -> int:
+        """Build the delta-compressed list stream (strategy "compressed");
+        returns its size in bytes."""
+        nbytes = C.c_uint64()
+        N.check(N.lib().zc_graph_build_compressed(self.handle, C.byref(nbytes)))
+        return nbytes.value
+
     def expand_profile(self, iterations: int) -> np.ndarray:
         """Per-iteration device time (ms) of the expansion kernels of the last run."""
         out = np.zeros(iterations, np.float64)

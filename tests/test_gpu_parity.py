@@ -372,3 +372,40 @@ def test_device_loop_hands_off_past_log_capacity():
             assert np.array_equal(r.values, ref.values)
             assert r.traversed_edges == ref.traversed_edges
             assert len(r.frontier_sizes) == n
+
+
+def test_compressed_lists_match_reference():
+    """Delta-compressed list stream: BFS / CC identical on every fixture graph
+    (values, iterations, traversed edges); SSSP is rejected."""
+    bad = []
+    for c in CASES:
+        if c.algo == "sssp" or c.graph.edge_elem_bytes != 4:
+            continue
+        r = zc.cc(c.graph, "compressed", collect_traffic=False) if c.algo == "cc" else \
+            zc.bfs(c.graph, c.source, "compressed", collect_traffic=False)
+        if not (np.array_equal(r.values, c.values) and r.iterations == c.iterations
+                and r.traversed_edges == c.traversed):
+            bad.append((c.index, c.tag))
+    assert not bad, bad[:8]
+    g = zc.with_uniform_weights(zc.generate_uniform(500, 1, 9, seed=2))
+    with pytest.raises(ValueError, match="compressed"):
+        zc.sssp(g, 0, "compressed", collect_traffic=False)
+
+
+def test_compressed_rmat_and_pagerank():
+    dg = zc.generate_rmat(18, 16, seed=21)
+    nbytes = dg.build_compressed()
+    assert 0 < nbytes < dg.num_edges * 4
+    g = dg.as_csr()
+    src = int(zc.pick_sources(g, 1, seed=7)[0])
+    ref = oracle.bfs(g, src, threads=8)
+    r = zc.bfs(dg, src, "compressed", collect_traffic=False)
+    assert np.array_equal(r.values, ref.values) and r.traversed_edges == ref.traversed_edges
+    sg = zc.generate_rmat(16, 8, seed=5, symmetrize=True)
+    ref = oracle.cc(sg.as_csr(), threads=8)
+    r = zc.cc(sg, "compressed", collect_traffic=False)
+    assert np.array_equal(r.values, ref.values) and r.iterations == ref.iterations
+    gu = zc.symmetrized(zc.generate_uniform(3000, 1, 12, seed=8))
+    a = zc.pagerank(gu, "compressed", collect_traffic=False)
+    b = oracle.pagerank(gu)
+    assert np.abs(a.values - b.values).max() < 1e-8

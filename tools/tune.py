@@ -19,6 +19,10 @@ else:
 print(f"gen {time.time()-t:.1f}s V={dg.num_vertices} E={dg.num_edges}", flush=True)
 if a.pairs:
     dg.build_sssp_pairs()
+if "compressed" in a.strategies:
+    t = time.time()
+    nb = dg.build_compressed()
+    print(f"compressed {nb/1e9:.2f} GB = {nb/dg.num_edges:.2f} B/edge in {time.time()-t:.1f}s", flush=True)
 src = int(zc.pick_sources(dg.as_csr(), 64, seed=7)[0])
 eb = 8 if a.algo == "sssp" else 4
 ref = None
