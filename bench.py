@@ -553,6 +553,14 @@ def variants(zc, args, dg, sources, device, phase: str) -> dict:
         for s in ("naive", "merged", "merged-aligned", "packed"):
             # naive walks each hub list with one thread (seconds per BFS): one rep
             out[f"zerocopy/{s}"] = _gteps(zc, dg, sources, s, reps=1 if s == "naive" else 2)
+        # B200 host-store option: the same lists sorted and delta-encoded
+        t0 = time.time()
+        nbytes = dg.build_compressed()
+        r = _gteps(zc, dg, sources, "compressed", reps=2)
+        bpe = nbytes / dg.num_edges
+        r.update({"bytes_per_edge": bpe, "build_s": time.time() - t0,
+                  "approx_link_gbs": r["expand_gbs"] * bpe / 4.0})
+        out["zerocopy/compressed"] = r
         return out
     import torch
     for placement in ("hbm", "uvm"):
