@@ -99,64 +99,78 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
   cudaSetDevice(g->device);
   ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
   const uint64_t nv = g->nv, ne = g->ne;
-  uint32_t* sorted = nullptr;
-  uint32_t* sizes = nullptr;
-  void* tmp = nullptr;
-  ZC_CUDA_TRY(cudaMalloc(&sorted, std::max<uint64_t>(ne, 1) * 4));
-  ZC_CUDA_TRY(cudaMemcpy(sorted, g->h_edges, ne * 4, cudaMemcpyDefault));
-  int rc = sort_lists_device(4, nv, g->d_off, g->h_off, sorted);
-  if (rc) {
-    cudaFree(sorted);
-    return rc;
-  }
-  ZC_CUDA_TRY(cudaMalloc(&g->d_cw, std::max<uint64_t>(nv, 1)));
-  ZC_CUDA_TRY(cudaMalloc(&g->d_coff, (nv + 1) * sizeof(uint64_t)));
-  ZC_CUDA_TRY(cudaMalloc(&sizes, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
-  k_cmp_sizes<<<kCmpGrid, 256>>>(nv, g->d_off, sorted, g->d_cw, sizes);
-  const size_t tb = scan_tmp_bytes(nv);
-  ZC_CUDA_TRY(cudaMalloc(&tmp, tb));
-  ZC_CUDA_TRY(scan_u32_to_u64(sizes, g->d_coff, nv, tmp, tb, 0));
-  uint64_t total = 0;
-  ZC_CUDA_TRY(cudaMemcpy(&total, g->d_coff + nv, sizeof(total), cudaMemcpyDeviceToHost));
-  uint32_t* enc = nullptr;
-  ZC_CUDA_TRY(cudaMalloc(&enc, std::max<uint64_t>(total, 4) + 16));
-  ZC_CUDA_TRY(cudaMemset(enc, 0, std::max<uint64_t>(total, 4) + 16));
-  k_cmp_encode<<<kCmpGrid, 256>>>(nv, g->d_off, sorted, g->d_cw, g->d_coff, enc);
-  ZC_CUDA_TRY(cudaDeviceSynchronize());
-  cudaFree(sorted);
-  cudaFree(sizes);
-  cudaFree(tmp);
-  // place the stream like the lists (+16 bytes of slack for the decoder)
-  const size_t bytes = std::max<uint64_t>(total, 4) + 16;
-  if (g->placement == ZC_PLACE_HBM) {
-    g->h_cmp = pinned_list_alloc(g->device, bytes);  // host shadow
-    if (!g->h_cmp) {
-      set_error("cannot allocate pinned memory for the compressed lists");
-      return ZC_ENOMEM;
-    }
-    ZC_CUDA_TRY(cudaMemcpy(g->h_cmp, enc, bytes, cudaMemcpyDeviceToHost));
-    g->hbm_cmp = enc;
-    g->d_cmp = enc;
-  } else if (g->placement == ZC_PLACE_UVM) {
+  // device temporaries are released on every path; the handle is only
+  // updated once the whole stream is built
+  struct DevBuf {
     void* p = nullptr;
-    ZC_CUDA_TRY(cudaMallocManaged(&p, bytes, cudaMemAttachGlobal));
-    ZC_CUDA_TRY(cudaMemcpy(p, enc, bytes, cudaMemcpyDefault));
-    cudaFree(enc);
-    ZC_CUDA_TRY(cudaMemAdvise(p, bytes, cudaMemAdviseSetReadMostly, g->device));
-    g->h_cmp = p;
-    g->d_cmp = p;
+    ~DevBuf() { cudaFree(p); }
+    void* release() {
+      void* q = p;
+      p = nullptr;
+      return q;
+    }
+  } sorted, sizes, tmp, enc, cw, coff;
+  ZC_CUDA_TRY(cudaMalloc(&sorted.p, std::max<uint64_t>(ne, 1) * 4));
+  ZC_CUDA_TRY(cudaMemcpy(sorted.p, g->h_edges, ne * 4, cudaMemcpyDefault));
+  const int rc = sort_lists_device(4, nv, g->d_off, g->h_off, sorted.p);
+  if (rc) return rc;
+  ZC_CUDA_TRY(cudaMalloc(&cw.p, std::max<uint64_t>(nv, 1)));
+  ZC_CUDA_TRY(cudaMalloc(&coff.p, (nv + 1) * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMalloc(&sizes.p, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
+  k_cmp_sizes<<<kCmpGrid, 256>>>(nv, g->d_off, static_cast<uint32_t*>(sorted.p),
+                                 static_cast<uint8_t*>(cw.p), static_cast<uint32_t*>(sizes.p));
+  const size_t tb = scan_tmp_bytes(nv);
+  ZC_CUDA_TRY(cudaMalloc(&tmp.p, tb));
+  ZC_CUDA_TRY(scan_u32_to_u64(static_cast<uint32_t*>(sizes.p), static_cast<uint64_t*>(coff.p), nv,
+                              tmp.p, tb, 0));
+  uint64_t total = 0;
+  ZC_CUDA_TRY(cudaMemcpy(&total, static_cast<uint64_t*>(coff.p) + nv, sizeof(total),
+                         cudaMemcpyDeviceToHost));
+  const size_t bytes = std::max<uint64_t>(total, 4) + 16;  // + slack for the decoder
+  ZC_CUDA_TRY(cudaMalloc(&enc.p, bytes));
+  ZC_CUDA_TRY(cudaMemset(enc.p, 0, bytes));
+  k_cmp_encode<<<kCmpGrid, 256>>>(nv, g->d_off, static_cast<uint32_t*>(sorted.p),
+                                  static_cast<uint8_t*>(cw.p), static_cast<uint64_t*>(coff.p),
+                                  static_cast<uint32_t*>(enc.p));
+  ZC_CUDA_TRY(cudaDeviceSynchronize());
+  // place the stream like the lists
+  void* host = nullptr;
+  const void* dev = nullptr;
+  void* hbm = nullptr;
+  if (g->placement == ZC_PLACE_UVM) {
+    ZC_CUDA_TRY(cudaMallocManaged(&host, bytes, cudaMemAttachGlobal));
+    if (cudaMemcpy(host, enc.p, bytes, cudaMemcpyDefault) != cudaSuccess ||
+        cudaMemAdvise(host, bytes, cudaMemAdviseSetReadMostly, g->device) != cudaSuccess) {
+      cudaFree(host);
+      set_error(std::string("compressed lists (uvm): ") + cudaGetErrorString(cudaGetLastError()));
+      return ZC_ECUDA;
+    }
+    dev = host;
   } else {
-    g->h_cmp = pinned_list_alloc(g->device, bytes);
-    if (!g->h_cmp) {
+    host = pinned_list_alloc(g->device, bytes);  // the stream, or the HBM run's host shadow
+    if (!host) {
       set_error("cannot allocate pinned memory for the compressed lists");
       return ZC_ENOMEM;
     }
-    ZC_CUDA_TRY(cudaMemcpy(g->h_cmp, enc, bytes, cudaMemcpyDeviceToHost));
-    cudaFree(enc);
     void* d = nullptr;
-    ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, g->h_cmp, 0));
-    g->d_cmp = d;
+    if (cudaMemcpy(host, enc.p, bytes, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        (g->placement != ZC_PLACE_HBM && cudaHostGetDevicePointer(&d, host, 0) != cudaSuccess)) {
+      pinned_list_free(host);
+      set_error(std::string("compressed lists: ") + cudaGetErrorString(cudaGetLastError()));
+      return ZC_ECUDA;
+    }
+    if (g->placement == ZC_PLACE_HBM) {
+      hbm = enc.release();
+      dev = hbm;
+    } else {
+      dev = d;
+    }
   }
+  g->h_cmp = host;
+  g->d_cmp = dev;
+  g->hbm_cmp = hbm;
+  g->d_cw = static_cast<uint8_t*>(cw.release());
+  g->d_coff = static_cast<uint64_t*>(coff.release());
   g->cmp_bytes = total;
   if (compressed_bytes) *compressed_bytes = total;
   return ZC_OK;

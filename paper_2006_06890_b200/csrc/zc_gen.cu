@@ -290,15 +290,54 @@ __global__ void k_weights(uint64_t ne, uint64_t seed, int64_t lo, int64_t hi, ui
 
 constexpr int kGenGrid = 148 * 16;
 
+// Frees a half-built handle on every early return (ZC_CUDA_TRY included).
+struct GraphGuard {
+  zc_graph* g;
+  ~GraphGuard() {
+    if (g) free_graph(g);
+  }
+  zc_graph* release() {
+    zc_graph* r = g;
+    g = nullptr;
+    return r;
+  }
+};
+
+// Device temporaries of one generator call: freed on every exit path (error
+// returns included) unless handed over to the handle.
+struct Temps {
+  std::vector<void*> ps;
+  template <typename T>
+  void add(T* p) {
+    ps.push_back(p);
+  }
+  void forget(const void* p) {
+    for (auto& q : ps)
+      if (q == p) q = nullptr;
+  }
+  void release(const void* p) {
+    for (auto& q : ps)
+      if (q == p) {
+        cudaFree(q);
+        q = nullptr;
+      }
+  }
+  ~Temps() {
+    for (void* p : ps) cudaFree(p);
+  }
+};
+
 // deg (u32, device) -> offsets into g->h_off (pinned) and g's device offsets.
 int offsets_from_degrees(zc_graph* g, uint32_t* d_deg, uint64_t nv, uint64_t** d_off_out) {
+  Temps t;
   uint64_t* d_off = nullptr;
   ZC_CUDA_TRY(cudaMalloc(&d_off, (nv + 1) * sizeof(uint64_t)));
+  t.add(d_off);
   const size_t tb = scan_tmp_bytes(nv);
   void* tmp = nullptr;
   ZC_CUDA_TRY(cudaMalloc(&tmp, tb));
+  t.add(tmp);
   ZC_CUDA_TRY(scan_u32_to_u64(d_deg, d_off, nv, tmp, tb, 0));
-  ZC_CUDA_TRY(cudaFree(tmp));
   if (!g->h_off) {
     if (cudaHostAlloc(&g->h_off, (nv + 1) * sizeof(int64_t), cudaHostAllocDefault) !=
         cudaSuccess) {
@@ -307,6 +346,7 @@ int offsets_from_degrees(zc_graph* g, uint32_t* d_deg, uint64_t nv, uint64_t** d
     }
   }
   ZC_CUDA_TRY(cudaMemcpy(g->h_off, d_off, (nv + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  t.forget(d_off);  // handed to the caller
   *d_off_out = d_off;
   return ZC_OK;
 }
@@ -377,10 +417,13 @@ zc_graph* new_handle(int32_t placement, int32_t device, uint32_t flags) {
 int attach_weights_range(zc_graph* g, uint64_t seed, int64_t wlow, int64_t whigh,
                          uint64_t ebase) {
   if (wlow > whigh) return ZC_OK;
+  Temps t;
   uint32_t* d_w = nullptr;
   ZC_CUDA_TRY(cudaMalloc(&d_w, std::max<uint64_t>(g->ne, 32) * sizeof(uint32_t)));
+  t.add(d_w);
   if (g->ne) k_weights<<<kGenGrid, 256>>>(g->ne, seed, wlow, whigh, d_w, ebase);
   ZC_CUDA_TRY(cudaGetLastError());
+  t.forget(d_w);  // adopt_device_list frees or keeps it
   g->has_weights = true;
   return adopt_device_list(g, d_w, 4, g->ne, &g->h_weights, &g->d_weights, &g->hbm_weights);
 }
@@ -438,6 +481,7 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
   const uint64_t nv = 1ull << scale;
   const uint64_t narcs = static_cast<uint64_t>(ef) << scale;
   const RmatParams p = rmat_params(scale, a, b, c, seed);
+  Temps t;
   // global degrees -> global offsets (identical on every rank)
   uint32_t* d_deg = nullptr;
   uint64_t* d_goff = nullptr;
@@ -445,17 +489,21 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
     set_error("out of device memory");
     return ZC_ENOMEM;
   }
+  t.add(d_deg);
   cudaMemset(d_deg, 0, nv * sizeof(uint32_t));
   k_rmat_count<<<kGenGrid, 256>>>(p, narcs, d_deg);
   ZC_CUDA_TRY(cudaMalloc(&d_goff, (nv + 1) * sizeof(uint64_t)));
+  t.add(d_goff);
   {
     const size_t tb = scan_tmp_bytes(nv);
     void* tmp = nullptr;
     ZC_CUDA_TRY(cudaMalloc(&tmp, tb));
+    t.add(tmp);
     ZC_CUDA_TRY(scan_u32_to_u64(d_deg, d_goff, nv, tmp, tb, 0));
-    ZC_CUDA_TRY(cudaFree(tmp));
+    ZC_CUDA_TRY(cudaDeviceSynchronize());
+    t.release(tmp);
   }
-  ZC_CUDA_TRY(cudaFree(d_deg));
+  t.release(d_deg);
   // edge-balanced bounds: first vertex whose offset reaches E*k/nparts
   std::vector<uint64_t> cut(nparts + 1);
   cut[0] = 0;
@@ -478,11 +526,8 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
   ZC_CUDA_TRY(cudaMemcpy(&e1, d_goff + hi, sizeof(e1), cudaMemcpyDeviceToHost));
 
   zc_graph* g = new_handle(placement, device, ZC_F_DIRECTED);
-  auto fail = [&](int code) {
-    cudaFree(d_goff);
-    free_graph(g);
-    return code;
-  };
+  GraphGuard guard{g};
+  auto fail = [](int code) { return code; };
   g->nv = nl;
   g->ne = e1 - e0;
   if (cudaHostAlloc(&g->h_off, (nl + 1) * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess) {
@@ -494,20 +539,25 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
   for (uint64_t v = 0; v <= nl; ++v) g->h_off[v] -= static_cast<int64_t>(e0);
   uint64_t* d_loff = nullptr;
   uint32_t* d_edges = nullptr;
-  if (cudaMalloc(&d_loff, (nl + 1) * sizeof(uint64_t)) != cudaSuccess ||
-      cudaMalloc(&d_edges, std::max<uint64_t>(g->ne, 32) * sizeof(uint32_t)) != cudaSuccess) {
+  if (cudaMalloc(&d_loff, (nl + 1) * sizeof(uint64_t)) != cudaSuccess) {
     set_error("out of device memory");
     return fail(ZC_ENOMEM);
   }
+  t.add(d_loff);
+  if (cudaMalloc(&d_edges, std::max<uint64_t>(g->ne, 32) * sizeof(uint32_t)) != cudaSuccess) {
+    set_error("out of device memory");
+    return fail(ZC_ENOMEM);
+  }
+  t.add(d_edges);
   ZC_CUDA_TRY(cudaMemcpy(d_loff, g->h_off, (nl + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice));
-  cudaFree(d_goff);
-  d_goff = nullptr;
+  t.release(d_goff);
   k_rmat_fill<uint32_t><<<kGenGrid, 256>>>(p, nl, d_loff, d_edges, lo);
   if (cudaDeviceSynchronize() != cudaSuccess) {
     set_error(std::string("rmat fill: ") + cudaGetErrorString(cudaGetLastError()));
     return fail(ZC_ECUDA);
   }
-  cudaFree(d_loff);
+  t.release(d_loff);
+  t.forget(d_edges);  // adopt_device_list frees or keeps it
   if ((rc = adopt_device_list(g, d_edges, 4, g->ne, &g->h_edges, &g->d_edges, &g->hbm_edges)))
     return fail(rc);
   if ((rc = attach_weights_range(g, seed ^ 0x77ull, wlow, whigh, e0))) return fail(rc);
@@ -522,7 +572,7 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
   info.stride = stride;
   if ((rc = init_partition(g, &info))) return fail(rc);
   if ((rc = finish_create(g))) return fail(rc);
-  *out = g;
+  *out = guard.release();
   return ZC_OK;
 }
 
@@ -547,8 +597,10 @@ int generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uin
   const RmatParams p = rmat_params(scale, a, b, c, seed);
 
   zc_graph* g = new_handle(placement, device, symmetrize ? 0u : ZC_F_DIRECTED);
-  auto fail = [&](int code) {
-    free_graph(g);
+  GraphGuard guard{g};
+  Temps t;
+  auto fail = [](int code) {
+    if (code == ZC_ENOMEM) set_error("out of device memory");
     return code;
   };
   g->nv = nv;
@@ -556,11 +608,14 @@ int generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uin
   uint64_t* d_off = nullptr;
   uint32_t* d_edges = nullptr;
   if (cudaMalloc(&d_deg, nv * sizeof(uint32_t)) != cudaSuccess) return fail(ZC_ENOMEM);
+  t.add(d_deg);
   cudaMemset(d_deg, 0, nv * sizeof(uint32_t));
   k_rmat_count<<<kGenGrid, 256>>>(p, narcs, d_deg);
   if ((rc = offsets_from_degrees(g, d_deg, nv, &d_off))) return fail(rc);
+  t.add(d_off);
   if (cudaMalloc(&d_edges, std::max<uint64_t>(narcs, 32) * sizeof(uint32_t)) != cudaSuccess)
     return fail(ZC_ENOMEM);
+  t.add(d_edges);
   k_rmat_fill<uint32_t><<<kGenGrid, 256>>>(p, nv, d_off, d_edges);
   if (cudaDeviceSynchronize() != cudaSuccess) {
     set_error(std::string("rmat fill: ") + cudaGetErrorString(cudaGetLastError()));
@@ -573,13 +628,16 @@ int generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uin
     uint32_t* d_sedges = nullptr;
     uint64_t* d_soff = nullptr;
     if (cudaMalloc(&d_cursor, nv * sizeof(uint32_t)) != cudaSuccess) return fail(ZC_ENOMEM);
+    t.add(d_cursor);
     k_deg_from_off<<<kGenGrid, 256>>>(nv, d_off, d_deg);
     k_count_in<uint32_t><<<kGenGrid, 256>>>(narcs, d_edges, d_deg);
     if ((rc = offsets_from_degrees(g, d_deg, nv, &d_soff))) return fail(rc);
+    t.add(d_soff);
     k_deg_from_off<<<kGenGrid, 256>>>(nv, d_off, d_cursor);
     if (cudaMalloc(&d_sedges, std::max<uint64_t>(2 * narcs, 32) * sizeof(uint32_t)) !=
         cudaSuccess)
       return fail(ZC_ENOMEM);
+    t.add(d_sedges);
     k_sym_copy_out<uint32_t><<<kGenGrid, 256>>>(nv, d_off, d_edges, d_soff, d_sedges);
     k_sym_scatter_in<uint32_t><<<kGenGrid, 256>>>(nv, d_off, d_edges, d_soff, d_cursor, d_sedges);
     if ((rc = sort_lists<uint32_t>(nv, d_soff, g->h_off, d_sedges))) return fail(rc);
@@ -587,22 +645,23 @@ int generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uin
       set_error(std::string("symmetrize: ") + cudaGetErrorString(cudaGetLastError()));
       return fail(ZC_ECUDA);
     }
-    cudaFree(d_cursor);
-    cudaFree(d_edges);
-    cudaFree(d_off);
+    t.release(d_cursor);
+    t.release(d_edges);
+    t.release(d_off);
     d_edges = d_sedges;
     d_off = d_soff;
     g->ne = 2 * narcs;
   }
-  cudaFree(d_deg);
+  t.release(d_deg);
   g->eb = 4;
+  t.forget(d_edges);  // adopt_device_list frees or keeps it
   if ((rc = adopt_device_list(g, d_edges, 4, g->ne, &g->h_edges, &g->d_edges, &g->hbm_edges)))
     return fail(rc);
-  cudaFree(d_off);
+  t.release(d_off);
   if ((rc = attach_weights(g, seed ^ 0x77ull, wlow, whigh))) return fail(rc);
   if ((rc = alloc_state(g))) return fail(rc);
   if ((rc = finish_create(g))) return fail(rc);
-  *out = g;
+  *out = guard.release();
   return ZC_OK;
 }
 
@@ -618,8 +677,10 @@ int generate_uniform(uint64_t nv, uint32_t dmin, uint32_t dmax, uint64_t seed, i
   }
   cudaSetDevice(device);
   zc_graph* g = new_handle(placement, device, ZC_F_DIRECTED);
-  auto fail = [&](int code) {
-    free_graph(g);
+  GraphGuard guard{g};
+  Temps t;
+  auto fail = [](int code) {
+    if (code == ZC_ENOMEM) set_error("out of device memory");
     return code;
   };
   g->nv = nv;
@@ -628,24 +689,28 @@ int generate_uniform(uint64_t nv, uint32_t dmin, uint32_t dmax, uint64_t seed, i
   uint32_t* d_edges = nullptr;
   if (cudaMalloc(&d_deg, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)) != cudaSuccess)
     return fail(ZC_ENOMEM);
+  t.add(d_deg);
   k_uniform_deg<<<kGenGrid, 256>>>(nv, seed, dmin, dmax, d_deg);
   if ((rc = offsets_from_degrees(g, d_deg, nv, &d_off))) return fail(rc);
+  t.add(d_off);
   g->ne = static_cast<uint64_t>(g->h_off[nv]);
   if (cudaMalloc(&d_edges, std::max<uint64_t>(g->ne, 32) * sizeof(uint32_t)) != cudaSuccess)
     return fail(ZC_ENOMEM);
+  t.add(d_edges);
   k_uniform_fill<uint32_t><<<kGenGrid, 128>>>(nv, seed, d_off, d_edges);
   if (cudaDeviceSynchronize() != cudaSuccess) {
     set_error(std::string("uniform fill: ") + cudaGetErrorString(cudaGetLastError()));
     return fail(ZC_ECUDA);
   }
-  cudaFree(d_deg);
-  cudaFree(d_off);
+  t.release(d_deg);
+  t.release(d_off);
+  t.forget(d_edges);  // adopt_device_list frees or keeps it
   if ((rc = adopt_device_list(g, d_edges, 4, g->ne, &g->h_edges, &g->d_edges, &g->hbm_edges)))
     return fail(rc);
   if ((rc = attach_weights(g, seed ^ 0x77ull, wlow, whigh))) return fail(rc);
   if ((rc = alloc_state(g))) return fail(rc);
   if ((rc = finish_create(g))) return fail(rc);
-  *out = g;
+  *out = guard.release();
   return ZC_OK;
 }
 
