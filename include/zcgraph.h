@@ -16,6 +16,9 @@
  *   zc_bfs            <- bfs(g, source, strategy, ...)   traversal.py:98-120
  *   zc_sssp           <- sssp(g, source, strategy, ...)  traversal.py:123-151
  *   zc_cc             <- cc(g, strategy, ...)            traversal.py:154-179
+ *   zc_bfs_async / zc_sssp_async / zc_sync
+ *                     <- the per-source loop of run_experiment
+ *                        (report.py:168-170: one bfs/sssp per picked source)
  *   zc_pagerank       <- pagerank(g, strategy, ...)      traversal.py:191-249
  *   zc_graph_multigraph <- _is_multigraph(g)             traversal.py:182-188
  *   zc_run_log        <- TraversalResult.traversed_edges traversal.py:26-45,63-65
@@ -147,6 +150,15 @@ int zc_graph_info(const zc_graph *g, uint64_t *num_vertices, uint64_t *num_edges
 int zc_bfs(zc_graph *g, uint64_t source, int strategy, int64_t *out, zc_stats *stats);
 int zc_sssp(zc_graph *g, uint64_t source, int strategy, int64_t *out, zc_stats *stats);
 int zc_cc(zc_graph *g, int strategy, int64_t *out, zc_stats *stats);
+/* Pipelined variants for a batch of sources on one handle: return as soon as
+ * the traversal has finished (stats and zc_run_log are final), while the
+ * int64 result is still being downloaded to `out` on a second stream -- so
+ * the D2H of source k overlaps the edge-list reads of source k+1.  `out`
+ * must stay valid and untouched until zc_sync(g) returns; stats->d2h_ms is 0.
+ * Up to two downloads are in flight; a third call waits for the oldest. */
+int zc_bfs_async(zc_graph *g, uint64_t source, int strategy, int64_t *out, zc_stats *stats);
+int zc_sssp_async(zc_graph *g, uint64_t source, int strategy, int64_t *out, zc_stats *stats);
+int zc_sync(zc_graph *g);
 
 /* PageRank (traversal.py:191-249): synchronous push over the whole edge list
  * every iteration, float64, dangling mass redistributed uniformly, stop when

@@ -31,6 +31,7 @@ EXPORTED = (
     "zc_part_result", "zc_generate_rmat_part", "zc_pagerank", "zc_graph_multigraph",
     "zc_part_fused_init", "zc_part_fused_connect", "zc_part_fused_reset", "zc_part_fused_expand",
     "zc_graph_open_emgi", "zc_graph_build_pairs", "zc_bulk_probe", "zc_graph_build_compressed",
+    "zc_bfs_async", "zc_sssp_async", "zc_sync",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -83,6 +84,9 @@ def _declare(lib: C.CDLL) -> None:
         "zc_bfs": (C.c_int, [P, u64, C.c_int, P, C.POINTER(Stats)]),
         "zc_sssp": (C.c_int, [P, u64, C.c_int, P, C.POINTER(Stats)]),
         "zc_cc": (C.c_int, [P, C.c_int, P, C.POINTER(Stats)]),
+        "zc_bfs_async": (C.c_int, [P, u64, C.c_int, P, C.POINTER(Stats)]),
+        "zc_sssp_async": (C.c_int, [P, u64, C.c_int, P, C.POINTER(Stats)]),
+        "zc_sync": (C.c_int, [P]),
         "zc_pagerank": (C.c_int, [P, C.c_int, dbl, u64, dbl, P, C.POINTER(Stats)]),
         "zc_graph_multigraph": (C.c_int, [P, C.POINTER(C.c_int)]),
         "zc_graph_build_pairs": (C.c_int, [P]),

@@ -192,6 +192,7 @@ void zc::free_graph(zc_graph* g) {
   if (!g) return;
   cudaSetDevice(g->device);
   if (g->stream) cudaStreamSynchronize(g->stream);
+  if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);
   auto free_list = [&](void*& h, bool registered, void*& hbm) {
     if (h) {
       if (registered) cudaHostUnregister(h);
@@ -241,6 +242,12 @@ void zc::free_graph(zc_graph* g) {
   for (auto& e : g->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : g->iter_ev) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(g->d_outbuf[i]);
+    if (g->out_ready[i]) cudaEventDestroy(g->out_ready[i]);
+    if (g->out_done[i]) cudaEventDestroy(g->out_done[i]);
+  }
+  if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
 }
@@ -554,7 +561,26 @@ int build_loop_graph(zc_graph* g, int algo, int strategy, int ebytes, const Expa
 }
 
 // One traversal (traversal.py:98-179) on the handle.
-int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stats* stats) {
+// Lazily created resources of the pipelined result path.
+int ensure_async(zc_graph* g) {
+  if (g->copy_stream) return ZC_OK;
+  for (int i = 0; i < 2; ++i) {
+    if (!g->d_outbuf[i] &&
+        cudaMalloc(&g->d_outbuf[i], std::max<uint64_t>(g->nv, 1) * sizeof(int64_t)) !=
+            cudaSuccess) {
+      cudaGetLastError();
+      set_error("out of device memory for the pipelined result slots");
+      return ZC_ENOMEM;
+    }
+    if (!g->out_ready[i]) ZC_CUDA_TRY(cudaEventCreateWithFlags(&g->out_ready[i], cudaEventDisableTiming));
+    if (!g->out_done[i]) ZC_CUDA_TRY(cudaEventCreateWithFlags(&g->out_done[i], cudaEventDisableTiming));
+  }
+  ZC_CUDA_TRY(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking));
+  return ZC_OK;
+}
+
+int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stats* stats,
+        bool async = false) {
   const double t0 = now_ms();
   if (!g) {
     set_error("null graph handle");
@@ -604,6 +630,10 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
   DeviceGuard dg(g->device);
   if (strategy == kCompressed && !g->d_cmp) {  // built once per handle
     const int rc = zc_graph_build_compressed(g, nullptr);
+    if (rc) return rc;
+  }
+  if (async) {
+    const int rc = ensure_async(g);
     if (rc) return rc;
   }
   cudaStream_t st = g->stream;
@@ -765,13 +795,31 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     if (model) g->log_hist.insert(g->log_hist.end(), g->h_ctr + kCtrHist, g->h_ctr + kCtrHist + 8);
   }
   ZC_CUDA_TRY(cudaEventRecord(g->ev[1], st));
-  // widen into an int64 staging buffer (free fval slot) and download
-  int64_t* d_out = reinterpret_cast<int64_t*>(g->d_fval[0]);
-  ZC_CUDA_TRY(launch_widen(algo, g->d_state, g->nv, d_out, st, &launches));
-  if (g->nv)
-    ZC_CUDA_TRY(cudaMemcpyAsync(out, d_out, g->nv * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
-  ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  if (async) {
+    // widen into the slot the download two calls ago has finished with, then
+    // download it on copy_stream: the D2H direction of the link is idle while
+    // the next traversal streams the edge list H2D
+    const uint32_t b = g->out_next;
+    g->out_next ^= 1;
+    ZC_CUDA_TRY(cudaStreamWaitEvent(st, g->out_done[b], 0));
+    ZC_CUDA_TRY(launch_widen(algo, g->d_state, g->nv, g->d_outbuf[b], st, &launches));
+    ZC_CUDA_TRY(cudaEventRecord(g->out_ready[b], st));
+    ZC_CUDA_TRY(cudaStreamWaitEvent(g->copy_stream, g->out_ready[b], 0));
+    if (g->nv)
+      ZC_CUDA_TRY(cudaMemcpyAsync(out, g->d_outbuf[b], g->nv * sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, g->copy_stream));
+    ZC_CUDA_TRY(cudaEventRecord(g->out_done[b], g->copy_stream));
+    ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
+    ZC_CUDA_TRY(cudaEventSynchronize(g->ev[1]));
+  } else {
+    // widen into an int64 staging buffer (free fval slot) and download
+    int64_t* d_out = reinterpret_cast<int64_t*>(g->d_fval[0]);
+    ZC_CUDA_TRY(launch_widen(algo, g->d_state, g->nv, d_out, st, &launches));
+    if (g->nv)
+      ZC_CUDA_TRY(cudaMemcpyAsync(out, d_out, g->nv * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
+    ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  }
   for (size_t k = 0; k < host_iters.size(); ++k) {
     float e = 0;
     cudaEventElapsedTime(&e, g->iter_ev[2 * k], g->iter_ev[2 * k + 1]);
@@ -787,8 +835,10 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     float ms = 0;
     cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]);
     stats->kernel_ms = ms;
-    cudaEventElapsedTime(&ms, g->ev[1], g->ev[2]);
-    stats->d2h_ms = ms;
+    if (!async) {  // the pipelined download has not finished yet
+      cudaEventElapsedTime(&ms, g->ev[1], g->ev[2]);
+      stats->d2h_ms = ms;
+    }
     stats->h2d_bytes = h2d;
     stats->d2h_bytes = g->nv * sizeof(int64_t) +
                        (device_loop ? (kCtrCount + 4 * kLogCap) : iters * (model ? kCtrCount : 2)) *
@@ -1370,6 +1420,22 @@ int zc_bfs(zc_graph* g, uint64_t source, int strategy, int64_t* out, zc_stats* s
 }
 int zc_sssp(zc_graph* g, uint64_t source, int strategy, int64_t* out, zc_stats* stats) {
   return run(g, kSssp, source, strategy, out, stats);
+}
+int zc_bfs_async(zc_graph* g, uint64_t source, int strategy, int64_t* out, zc_stats* stats) {
+  return run(g, kBfs, source, strategy, out, stats, true);
+}
+int zc_sssp_async(zc_graph* g, uint64_t source, int strategy, int64_t* out, zc_stats* stats) {
+  return run(g, kSssp, source, strategy, out, stats, true);
+}
+int zc_sync(zc_graph* g) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (!g->copy_stream) return ZC_OK;
+  DeviceGuard dg(g->device);
+  ZC_CUDA_TRY(cudaStreamSynchronize(g->copy_stream));
+  return ZC_OK;
 }
 int zc_cc(zc_graph* g, int strategy, int64_t* out, zc_stats* stats) {
   return run(g, kCc, 0, strategy, out, stats);

@@ -94,6 +94,13 @@ struct zc_graph {
   uint32_t* d_sent = nullptr;  // BFS: discoveries already sent this iteration
   std::vector<void*> ipc_opened;
   int fused_algo = -1;
+  // pipelined results (zc_bfs_async / zc_sssp_async / zc_sync): two int64
+  // staging slots widened on the run stream, downloaded on copy_stream while
+  // the next traversal streams the edge list
+  cudaStream_t copy_stream = nullptr;
+  int64_t* d_outbuf[2] = {nullptr, nullptr};
+  cudaEvent_t out_ready[2] = {nullptr, nullptr}, out_done[2] = {nullptr, nullptr};
+  uint32_t out_next = 0;
   // stepped run state (zc_part_begin / expand / apply)
   int p_algo = -1, p_strategy = 0, p_cur = 0;
   uint64_t p_iter = 0, p_n = 0, p_launches = 0;

@@ -607,58 +607,90 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep_cmp(ExpandArgs a
     }
     __syncthreads();
     const uint64_t Wend = min(We, sh_w[kStage]);
-    for (uint64_t q = W + warp; q < Wend; q += kSweepWarps) {
+    // block q of the staged slots: owner slot, width, element count, words
+    struct Blk {
+      int slot;
+      uint32_t w, cnt, words;
+      const uint32_t* src;
+    };
+    auto locate = [&](uint64_t q) {
       int lo = 0, hi = kStage;  // sh_w[lo] <= q < sh_w[hi]
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (sh_w[mid] <= q) lo = mid; else hi = mid;
       }
+      Blk k;
+      k.slot = lo;
       const uint64_t t = q - sh_w[lo];
-      const uint32_t w = sh_bits[lo];
+      k.w = sh_bits[lo];
       const uint64_t rem = sh_d[lo] - t * kCmpBlock;
-      const uint64_t cnt = rem < kCmpBlock ? rem : kCmpBlock;
-      const uint32_t words = static_cast<uint32_t>(cmp_block_bytes(w, cnt) / 4);
-      const uint32_t* src = a.cmp + (sh_c[lo] + t * cmp_full_bytes(w)) / 4;
-      uint32_t x[4];
+      k.cnt = static_cast<uint32_t>(rem < kCmpBlock ? rem : kCmpBlock);
+      k.words = static_cast<uint32_t>(cmp_block_bytes(k.w, k.cnt) / 4);
+      k.src = a.cmp + (sh_c[lo] + t * cmp_full_bytes(k.w)) / 4;
+      return k;
+    };
+    auto load = [&](const Blk& k, uint32_t (&x)[4]) {
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const uint32_t qi = r * kWarp + lane;
-        x[r] = qi < words ? ld_list(src + qi) : 0u;
+        x[r] = qi < k.words ? ld_list(k.src + qi) : 0u;
       }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) blk[r * kWarp + lane] = x[r];
-      if (lane < 2) blk[4 * kWarp + lane] = 0;
-      __syncwarp();
-      // element e = 4 * lane + i: e == 0 -> base, else delta e-1 at bit 32 + (e-1) w
-      const uint64_t mask = w >= 32 ? 0xffffffffull : ((1ull << w) - 1);
-      uint64_t val[4];
-      uint64_t run = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t e = 4 * lane + i;
-        uint64_t xval = 0;
-        if (e == 0) {
-          xval = blk[0];
-        } else if (e < cnt) {
-          const uint32_t bit = 32 + (e - 1) * w;
-          const uint64_t pair = (static_cast<uint64_t>(blk[(bit >> 5) + 1]) << 32) | blk[bit >> 5];
-          xval = (pair >> (bit & 31)) & mask;
+    };
+    // software pipeline: the next block's words are in flight while this
+    // block is decoded and visited
+    uint64_t q = W + warp;
+    if (q < Wend) {
+      Blk kc = locate(q);
+      uint32_t xc[4];
+      load(kc, xc);
+      for (; q < Wend; q += kSweepWarps) {
+        const uint64_t qn = q + kSweepWarps;
+        Blk kn = kc;
+        uint32_t xn[4] = {0u, 0u, 0u, 0u};
+        if (qn < Wend) {
+          kn = locate(qn);
+          load(kn, xn);
         }
-        run += xval;
-        val[i] = run;
-      }
-      uint64_t incl = run;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t o = __shfl_up_sync(kFull, incl, d);
-        if (lane >= d) incl += o;
-      }
-      const uint64_t before = incl - run;
-      __syncwarp();
-      const uint64_t sval = AlgoTraits<ALGO>::has_val ? sh_v[lo] : 0;
+        for (int r = 0; r < 4; ++r) blk[r * kWarp + lane] = xc[r];
+        if (lane < 2) blk[4 * kWarp + lane] = 0;
+        __syncwarp();
+        // element e = 4 * lane + i: e == 0 -> base, else delta e-1 at bit 32 + (e-1) w
+        const uint32_t w = kc.w, cnt = kc.cnt;
+        const uint64_t mask = w >= 32 ? 0xffffffffull : ((1ull << w) - 1);
+        uint64_t val[4];
+        uint64_t run = 0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (4 * lane + i < cnt) Visit<ALGO>::apply(a, before + val[i], 0, sval);
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t e = 4 * lane + i;
+          uint64_t xval = 0;
+          if (e == 0) {
+            xval = blk[0];
+          } else if (e < cnt) {
+            const uint32_t bit = 32 + (e - 1) * w;
+            const uint64_t pair =
+                (static_cast<uint64_t>(blk[(bit >> 5) + 1]) << 32) | blk[bit >> 5];
+            xval = (pair >> (bit & 31)) & mask;
+          }
+          run += xval;
+          val[i] = run;
+        }
+        uint64_t incl = run;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint64_t o = __shfl_up_sync(kFull, incl, d);
+          if (lane >= d) incl += o;
+        }
+        const uint64_t before = incl - run;
+        __syncwarp();
+        const uint64_t sval = AlgoTraits<ALGO>::has_val ? sh_v[kc.slot] : 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (4 * lane + i < cnt) Visit<ALGO>::apply(a, before + val[i], 0, sval);
+        kc = kn;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) xc[r] = xn[r];
+      }
     }
     __syncthreads();
     W = Wend;

@@ -245,6 +245,34 @@ class DeviceGraph:
         return out, st, trav, front, hist
 
 
+    def run_many(self, algo: str, sources, strategy_id: int):
+        """Traverse from each source with the result downloads pipelined behind
+        the next traversal (zc_bfs_async / zc_sssp_async + zc_sync); returns a
+        list of (values, Stats, traversed, frontier)."""
+        lib = N.lib()
+        fn = {"bfs": lib.zc_bfs_async, "sssp": lib.zc_sssp_async}.get(algo)
+        if fn is None:
+            raise ValueError(f"no pipelined runner for {algo!r}")
+        done = []
+        with self._lock:
+            self.set_traffic_model(False)
+            try:
+                for s in sources:
+                    out = pinned_empty(self.num_vertices, np.int64)
+                    st = N.Stats()
+                    N.check(fn(self.handle, int(s), strategy_id, out.ctypes.data, C.byref(st)))
+                    # `out` is still being written: keep it referenced until zc_sync
+                    done.append((out, st))
+                    it = st.iterations
+                    trav = np.zeros(it, np.uint64)
+                    front = np.zeros(it, np.uint64)
+                    N.check(lib.zc_run_log(self.handle, trav.ctypes.data, front.ctypes.data, it))
+                    done[-1] = (out, st, trav, front)
+            finally:
+                N.check(lib.zc_sync(self.handle))
+        return done
+
+
 # id(graph) -> (weakref to graph, {key: DeviceGraph}); CsrGraph defines __eq__
 # without __hash__ (like the reference), so it cannot key a WeakKeyDictionary.
 def _pagerank_run(dg: "DeviceGraph", sid: int, damping: float, max_iters: int, tol: float,

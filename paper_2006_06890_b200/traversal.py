@@ -126,6 +126,46 @@ def cc(g, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traffic: bool = Tru
     return _run("cc", g, 0, strategy, collect_traffic, want_pages, placement, device)
 
 
+def _run_many(algo: str, g, sources, strategy, collect_traffic: bool, placement: str,
+              device: int) -> list:
+    srcs = [int(s) for s in sources]
+    for s in srcs:
+        _check_source(g, s)
+    if collect_traffic:  # the request model runs per level on the host loop
+        return [_run(algo, g, s, strategy, True, False, placement, device) for s in srcs]
+    dg = device_graph(g, placement, device)
+    return [
+        TraversalResult(
+            algo=algo, values=out, iterations=int(st.iterations),
+            per_iteration_traffic=[TrafficStats.zero() for _ in range(st.iterations)],
+            traversed_edges=[int(x) for x in trav], frontier_sizes=[int(x) for x in front],
+            kernel_ms=st.kernel_ms, total_ms=st.total_ms, d2h_ms=st.d2h_ms,
+            expand_ms=st.expand_ms, launches=int(st.launches), h2d_bytes=int(st.h2d_bytes),
+            d2h_bytes=int(st.d2h_bytes))
+        for out, st, trav, front in dg.run_many(algo, srcs, strategy_id(strategy))]
+
+
+def bfs_many(g, sources, strategy=AccessStrategy.MERGED_ALIGNED, *,
+             collect_traffic: bool = False, placement: str = "zerocopy",
+             device: int = 0) -> list:
+    """bfs() from each source, in order -- the per-source loop of the
+    reference's run_experiment (report.py:168-170) as one pipelined call: the
+    int64 levels of source k download while source k+1 streams the edge list.
+    Same results as calling bfs() per source."""
+    return _run_many("bfs", g, sources, strategy, collect_traffic, placement, device)
+
+
+def sssp_many(g, sources, strategy=AccessStrategy.MERGED_ALIGNED, *,
+              collect_traffic: bool = False, placement: str = "zerocopy",
+              device: int = 0) -> list:
+    """sssp() from each source, pipelined like bfs_many."""
+    if not _has_weights(g):
+        raise ValueError("sssp requires edge weights")
+    if not isinstance(g, DeviceGraph) and g.num_edges and int(np.min(g.weights)) < 0:
+        raise ValueError("sssp requires non-negative weights")
+    return _run_many("sssp", g, sources, strategy, collect_traffic, placement, device)
+
+
 def pagerank(g, strategy=AccessStrategy.MERGED_ALIGNED, damping: float = 0.85,
              max_iters: int = 100, tol: float = 1e-6, *, collect_traffic: bool = True,
              want_pages: bool = False, page_bytes: int = 4096, placement: str = "zerocopy",
