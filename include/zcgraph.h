@@ -10,8 +10,10 @@
  *   zc_graph_create   <- CsrGraph (csr.py:34-77) + validate (csr.py:80-105):
  *                        the caller's CSR arrays become a handle whose edge /
  *                        weight lists live in pinned mapped host memory
- *                        (ZC_PLACE_ZEROCOPY), managed memory (ZC_PLACE_UVM) or
- *                        HBM (ZC_PLACE_HBM); offsets and all per-vertex state
+ *                        (ZC_PLACE_ZEROCOPY), host-resident managed memory
+ *                        (ZC_PLACE_ZEROCOPY_MANAGED), migrating managed
+ *                        memory (ZC_PLACE_UVM) or HBM (ZC_PLACE_HBM);
+ *                        offsets and all per-vertex state
  *                        live in HBM.
  *   zc_bfs            <- bfs(g, source, strategy, ...)   traversal.py:98-120
  *   zc_sssp           <- sssp(g, source, strategy, ...)  traversal.py:123-151
@@ -74,6 +76,12 @@ extern "C" {
 #define ZC_PLACE_ZEROCOPY 0 /* cudaHostAlloc(Mapped|Portable) or cudaHostRegister */
 #define ZC_PLACE_UVM 1      /* cudaMallocManaged + cudaMemAdviseSetReadMostly     */
 #define ZC_PLACE_HBM 2      /* cudaMalloc: in-HBM control run                     */
+#define ZC_PLACE_ZEROCOPY_MANAGED 3 /* B200 host mapping (not in the reference):
+                               host-resident cudaMallocManaged lists
+                               (PreferredLocation = CPU, AccessedBy = the GPU),
+                               never migrated; the GPU reads them over PCIe with
+                               the same zero-copy loads, through the UVM
+                               driver's large-page GPU mappings             */
 
 /* zc_graph_desc.flags */
 #define ZC_F_DIRECTED 1u        /* CsrGraph.directed (csr.py:45)                     */
@@ -295,9 +303,17 @@ int zc_generate_rmat_part(uint32_t scale, uint32_t edge_factor, double a, double
  * warps read chunk_bytes contiguous bytes per request at consecutive
  * (pattern 0) or random (pattern 1) chunk-aligned offsets of a `bytes`
  * buffer allocated by cudaHostAlloc (alloc 0), transparent-huge-page
- * mmap + cudaHostRegister (alloc 1) or cudaMalloc (alloc 2). */
+ * mmap + cudaHostRegister (alloc 1), cudaMalloc (alloc 2), a host-NUMA
+ * VMM allocation (cuMemCreate, alloc 3), hugetlbfs 2 MB pages +
+ * cudaHostRegister (alloc 4) or cudaMallocManaged preferred on the CPU and
+ * accessed-by the device (alloc 5). */
 int zc_read_probe(int32_t device, uint64_t bytes, int pattern, uint32_t chunk_bytes, int alloc,
                   int iters, double *gbs);
+
+/* Host-NUMA VMM allocation check: allocates `bytes` with cuMemCreate
+ * (CU_MEM_LOCATION_TYPE_HOST_NUMA, node 0), maps it for the device and the
+ * CPU, frees it; *granularity = the recommended allocation granularity. */
+int zc_vmm_host_probe(int32_t device, uint64_t bytes, uint64_t *granularity);
 
 /* TMA bulk-copy (cp.async.bulk) streaming read of pinned host memory:
  * `chunk`-byte copies into a 4-stage shared-memory ring per CTA. */

@@ -14,11 +14,12 @@ from ._build import LIB_PATH
 
 ZC_OK, ZC_EINVAL, ZC_ECUDA, ZC_ENOMEM, ZC_ESTATE = 0, -1, -2, -3, -4
 ZC_NAIVE, ZC_MERGED, ZC_MERGED_ALIGNED, ZC_PACKED, ZC_COMPRESSED = 0, 1, 2, 3, 4
-ZC_PLACE_ZEROCOPY, ZC_PLACE_UVM, ZC_PLACE_HBM = 0, 1, 2
+ZC_PLACE_ZEROCOPY, ZC_PLACE_UVM, ZC_PLACE_HBM, ZC_PLACE_ZEROCOPY_MANAGED = 0, 1, 2, 3
 ZC_F_DIRECTED, ZC_F_REGISTER, ZC_F_UVM_PREFETCH, ZC_F_NO_VALIDATE = 1, 2, 4, 8
 ABI_VERSION = 1
 
-PLACEMENTS = {"zerocopy": ZC_PLACE_ZEROCOPY, "uvm": ZC_PLACE_UVM, "hbm": ZC_PLACE_HBM}
+PLACEMENTS = {"zerocopy": ZC_PLACE_ZEROCOPY, "uvm": ZC_PLACE_UVM, "hbm": ZC_PLACE_HBM,
+              "zerocopy-managed": ZC_PLACE_ZEROCOPY_MANAGED}
 
 # every symbol include/zcgraph.h declares
 EXPORTED = (
@@ -31,7 +32,7 @@ EXPORTED = (
     "zc_part_result", "zc_generate_rmat_part", "zc_pagerank", "zc_graph_multigraph",
     "zc_part_fused_init", "zc_part_fused_connect", "zc_part_fused_reset", "zc_part_fused_expand",
     "zc_graph_open_emgi", "zc_graph_build_pairs", "zc_bulk_probe", "zc_graph_build_compressed",
-    "zc_bfs_async", "zc_sssp_async", "zc_sync",
+    "zc_bfs_async", "zc_sssp_async", "zc_sync", "zc_vmm_host_probe",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -106,6 +107,7 @@ def _declare(lib: C.CDLL) -> None:
                                     C.POINTER(dbl)]),
         "zc_read_probe": (C.c_int, [i32, u64, C.c_int, u32, C.c_int, C.c_int, C.POINTER(dbl)]),
         "zc_bulk_probe": (C.c_int, [i32, u64, u32, C.c_int, C.c_int, C.POINTER(dbl)]),
+        "zc_vmm_host_probe": (C.c_int, [i32, u64, C.POINTER(u64)]),
         "zc_part_create": (C.c_int, [C.POINTER(GraphDesc), C.POINTER(PartInfo), C.POINTER(P)]),
         "zc_part_exchange_elem_bytes": (C.c_size_t, [C.c_int]),
         "zc_part_begin": (C.c_int, [P, C.c_int, u64, C.c_int, C.POINTER(u64), C.POINTER(u64)]),

@@ -146,11 +146,64 @@ void* pinned_list_alloc(int device, size_t bytes) {
   return p;
 }
 
+// Host-resident managed lists (ZC_PLACE_ZEROCOPY_MANAGED).  The pages stay
+// in host memory (PreferredLocation = CPU) and are mapped in the GPU's page
+// tables up front (AccessedBy), so the GPU reads them over PCIe exactly like
+// pinned memory -- but through the UVM driver's mappings, whose large GPU
+// pages keep the scattered line reads of sparse frontiers out of the
+// translation misses that cap pinned memory at ~70 M random lines/s
+// (profiles/r01_alloc_probe.txt: random 128 B reads over 8 GiB, 9.0 GB/s
+// pinned vs 34.0 GB/s managed-on-host).  No ReadMostly: no GPU copies.
+static std::unordered_map<void*, size_t> g_managed;
+
+static void* managed_host_alloc(int device, size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocManaged(&p, bytes, cudaMemAttachGlobal) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (cudaMemAdvise(p, bytes, cudaMemAdviseSetPreferredLocation, cudaCpuDeviceId) !=
+          cudaSuccess ||
+      cudaMemAdvise(p, bytes, cudaMemAdviseSetAccessedBy, device) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(p);
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  g_managed[p] = bytes;
+  return p;
+}
+
+void* host_list_alloc(const zc_graph* g, size_t bytes) {
+  if (g->placement == ZC_PLACE_ZEROCOPY_MANAGED) return managed_host_alloc(g->device, bytes);
+  return pinned_list_alloc(g->device, bytes);
+}
+
+int host_list_device_ptr(void* p, const void** d) {
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    if (g_managed.count(p)) {
+      *d = p;
+      return ZC_OK;
+    }
+  }
+  void* dp = nullptr;
+  ZC_CUDA_TRY(cudaHostGetDevicePointer(&dp, p, 0));
+  *d = dp;
+  return ZC_OK;
+}
+
 void pinned_list_free(void* p) {
   if (!p) return;
   size_t bytes = 0;
   {
     std::lock_guard<std::mutex> lk(g_map_mu);
+    auto m = g_managed.find(p);
+    if (m != g_managed.end()) {
+      g_managed.erase(m);
+      cudaFree(p);
+      return;
+    }
     auto it = g_mapped.find(p);
     if (it != g_mapped.end()) {
       bytes = it->second;
@@ -281,7 +334,7 @@ int validate_desc(const zc_graph_desc* d, bool* negative_weight, uint64_t dest_l
     set_error("offsets / edges must not be NULL");
     return ZC_EINVAL;
   }
-  if (d->placement < ZC_PLACE_ZEROCOPY || d->placement > ZC_PLACE_HBM) {
+  if (!placement_valid(d->placement)) {
     set_error("unknown placement");
     return ZC_EINVAL;
   }
@@ -376,11 +429,10 @@ int place_list(zc_graph* g, const void* src, uint32_t sw, uint32_t dw, uint64_t 
     *dptr = p;
     return ZC_OK;
   }
-  // pinned mapped host buffer (zero-copy list, or the host shadow of HBM)
-  void* p = nullptr;
-  p = pinned_list_alloc(g->device, bytes);
+  // host buffer read in place (zero-copy list), or the host shadow of HBM
+  void* p = host_list_alloc(g, bytes);
   if (!p) {
-    set_error("cannot allocate pinned host memory for a list");
+    set_error("cannot allocate host memory for a list");
     return ZC_ENOMEM;
   }
   *h = p;
@@ -389,12 +441,9 @@ int place_list(zc_graph* g, const void* src, uint32_t sw, uint32_t dw, uint64_t 
     ZC_CUDA_TRY(cudaMalloc(hbm, bytes));
     ZC_CUDA_TRY(cudaMemcpy(*hbm, p, n * dw, cudaMemcpyHostToDevice));
     *dptr = *hbm;
-  } else {
-    void* d = nullptr;
-    ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, p, 0));
-    *dptr = d;
+    return ZC_OK;
   }
-  return ZC_OK;
+  return host_list_device_ptr(p, dptr);
 }
 
 }  // namespace
@@ -477,24 +526,20 @@ int zc::adopt_device_list(zc_graph* g, void* d_src, uint32_t w, uint64_t n, void
     *dptr = p;
     return ZC_OK;
   }
-  void* p = nullptr;
-  p = pinned_list_alloc(g->device, bytes);
+  void* p = host_list_alloc(g, bytes);
   if (!p) {
-    set_error("cannot allocate pinned host memory for a list");
+    set_error("cannot allocate host memory for a list");
     return ZC_ENOMEM;
   }
   *h = p;
-  ZC_CUDA_TRY(cudaMemcpy(p, d_src, n * w, cudaMemcpyDeviceToHost));
+  ZC_CUDA_TRY(cudaMemcpy(p, d_src, n * w, cudaMemcpyDefault));
   if (g->placement == ZC_PLACE_HBM) {
     *hbm = d_src;
     *dptr = d_src;
-  } else {
-    ZC_CUDA_TRY(cudaFree(d_src));
-    void* d = nullptr;
-    ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, p, 0));
-    *dptr = d;
+    return ZC_OK;
   }
-  return ZC_OK;
+  ZC_CUDA_TRY(cudaFree(d_src));
+  return host_list_device_ptr(p, dptr);
 }
 
 namespace {
@@ -1002,7 +1047,7 @@ int zc_graph_open_emgi(const char* path, int32_t placement, int32_t device, uint
     set_error("truncated file: weight array incomplete");
     return ZC_EINVAL;
   }
-  if (placement < ZC_PLACE_ZEROCOPY || placement > ZC_PLACE_HBM) {
+  if (!placement_valid(placement)) {
     set_error("unknown placement");
     return ZC_EINVAL;
   }
@@ -1044,12 +1089,9 @@ int zc_graph_open_emgi(const char* path, int32_t placement, int32_t device, uint
     void* p = nullptr;
     if (placement == ZC_PLACE_UVM) {
       ZC_CUDA_TRY(cudaMallocManaged(&p, bytes, cudaMemAttachGlobal));
-    } else {
-      p = pinned_list_alloc(g->device, bytes);
-  if (!p) {
-    set_error("cannot allocate pinned host memory for a list");
-    return ZC_ENOMEM;
-  }
+    } else if (!(p = host_list_alloc(g, bytes))) {
+      set_error("cannot allocate host memory for a list");
+      return ZC_ENOMEM;
     }
     *h = p;
     if (ne && pread_all(fd, p, ne * w, pos)) {
@@ -1064,9 +1106,7 @@ int zc_graph_open_emgi(const char* path, int32_t placement, int32_t device, uint
       ZC_CUDA_TRY(cudaMemcpy(*hbm, p, ne * w, cudaMemcpyHostToDevice));
       *dptr = *hbm;
     } else {
-      void* d = nullptr;
-      ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, p, 0));
-      *dptr = d;
+      return host_list_device_ptr(p, dptr);
     }
     return ZC_OK;
   };
@@ -1610,8 +1650,8 @@ int zc_graph_build_pairs(zc_graph* g) {
   const size_t bytes = std::max<size_t>(ne * 8, kLineBytes);
   void* p = nullptr;
   if (g->placement == ZC_PLACE_UVM) ZC_CUDA_TRY(cudaMallocManaged(&p, bytes, cudaMemAttachGlobal));
-  else if (!(p = pinned_list_alloc(g->device, bytes))) {
-    set_error("cannot allocate pinned host memory for a list");
+  else if (!(p = host_list_alloc(g, bytes))) {
+    set_error("cannot allocate host memory for a list");
     return ZC_ENOMEM;
   }
   g->h_pairs = p;
@@ -1629,9 +1669,7 @@ int zc_graph_build_pairs(zc_graph* g) {
     ZC_CUDA_TRY(cudaMemcpy(g->hbm_pairs, p, ne * 8, cudaMemcpyHostToDevice));
     g->d_pairs = g->hbm_pairs;
   } else {
-    void* d = nullptr;
-    ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, p, 0));
-    g->d_pairs = d;
+    return host_list_device_ptr(p, &g->d_pairs);
   }
   return ZC_OK;
 }

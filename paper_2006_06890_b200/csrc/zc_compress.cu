@@ -147,14 +147,14 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
     }
     dev = host;
   } else {
-    host = pinned_list_alloc(g->device, bytes);  // the stream, or the HBM run's host shadow
+    host = host_list_alloc(g, bytes);  // the stream, or the HBM run's host shadow
     if (!host) {
-      set_error("cannot allocate pinned memory for the compressed lists");
+      set_error("cannot allocate host memory for the compressed lists");
       return ZC_ENOMEM;
     }
-    void* d = nullptr;
-    if (cudaMemcpy(host, enc.p, bytes, cudaMemcpyDeviceToHost) != cudaSuccess ||
-        (g->placement != ZC_PLACE_HBM && cudaHostGetDevicePointer(&d, host, 0) != cudaSuccess)) {
+    const void* d = nullptr;
+    if (cudaMemcpy(host, enc.p, bytes, cudaMemcpyDefault) != cudaSuccess ||
+        (g->placement != ZC_PLACE_HBM && host_list_device_ptr(host, &d) != ZC_OK)) {
       pinned_list_free(host);
       set_error(std::string("compressed lists: ") + cudaGetErrorString(cudaGetLastError()));
       return ZC_ECUDA;

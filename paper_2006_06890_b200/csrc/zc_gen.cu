@@ -439,7 +439,7 @@ int check_common(int32_t placement, int32_t device, int64_t wlow, int64_t whigh)
     set_error("device not present");
     return ZC_EINVAL;
   }
-  if (placement < ZC_PLACE_ZEROCOPY || placement > ZC_PLACE_HBM) {
+  if (!placement_valid(placement)) {
     set_error("unknown placement");
     return ZC_EINVAL;
   }

@@ -116,6 +116,12 @@ int init_partition(zc_graph* g, const zc_part_info* info);
 // pinned mapped list buffers, NUMA-local to the GPU when the host has several nodes
 void* pinned_list_alloc(int device, size_t bytes);
 void pinned_list_free(void* p);
+// Host-side list buffer of a handle: pinned (ZEROCOPY, and the HBM run's
+// shadow) or host-resident managed memory (ZEROCOPY_MANAGED).  Freed with
+// pinned_list_free; host_list_device_ptr gives the address kernels use.
+void* host_list_alloc(const zc_graph* g, size_t bytes);
+int host_list_device_ptr(void* p, const void** d);
+inline bool placement_valid(int32_t p) { return p >= ZC_PLACE_ZEROCOPY && p <= ZC_PLACE_ZEROCOPY_MANAGED; }
 // Adopt a list generated in HBM (d_src, n elements of width w) into the
 // handle's placement; frees d_src unless it becomes the HBM copy.
 int adopt_device_list(zc_graph* g, void* d_src, uint32_t w, uint64_t n, void** h,

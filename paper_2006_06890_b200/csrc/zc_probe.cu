@@ -1,6 +1,7 @@
 // Host-link and HBM probes: the measured denominators for the roofline
 // (pinned cudaMemcpy H2D peak, zero-copy streaming-read peak,
 // next to the 63.0 GB/s PCIe Gen5 x16 theoretical figure).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -213,8 +214,130 @@ extern "C" int zc_bulk_probe(int32_t device, uint64_t bytes, uint32_t chunk, int
   return ZC_OK;
 }
 
+namespace zc {
+namespace {
+// Driver VMM entry points, fetched through the runtime (no -lcuda link).
+struct Vmm {
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemAddressFree) addr_free = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemSetAccess) set_access = nullptr;
+  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+  bool ok = false;
+};
+
+template <class F>
+bool entry(const char* name, F* fn) {
+  cudaDriverEntryPointQueryResult q;
+  void* p = nullptr;
+  if (cudaGetDriverEntryPointByVersion(name, &p, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !p)
+    return false;
+  *fn = reinterpret_cast<F>(p);
+  return true;
+}
+
+const Vmm& vmm() {
+  static Vmm v = [] {
+    Vmm x;
+    x.ok = entry("cuMemCreate", &x.create) && entry("cuMemRelease", &x.release) &&
+           entry("cuMemAddressReserve", &x.reserve) && entry("cuMemAddressFree", &x.addr_free) &&
+           entry("cuMemMap", &x.map) && entry("cuMemUnmap", &x.unmap) &&
+           entry("cuMemSetAccess", &x.set_access) &&
+           entry("cuMemGetAllocationGranularity", &x.granularity);
+    return x;
+  }();
+  return v;
+}
+
+// Host-NUMA-located VMM allocation mapped for the device and the CPU at one
+// address (cuMemCreate with CU_MEM_LOCATION_TYPE_HOST_NUMA).
+struct VmmHost {
+  CUdeviceptr va = 0;
+  size_t size = 0;
+  CUmemGenericAllocationHandle h = 0;
+};
+
+int vmm_host_alloc(int device, int numa, size_t bytes, VmmHost* out, size_t* gran_out) {
+  const Vmm& v = vmm();
+  if (!v.ok) {
+    set_error("driver VMM entry points unavailable");
+    return ZC_ECUDA;
+  }
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_HOST_NUMA;
+  prop.location.id = numa;
+  size_t gran = 0;
+  if (v.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS ||
+      !gran) {
+    set_error("cuMemGetAllocationGranularity(HOST_NUMA) failed");
+    return ZC_ECUDA;
+  }
+  if (gran_out) *gran_out = gran;
+  bytes = (bytes + gran - 1) / gran * gran;
+  CUresult r = v.create(&out->h, bytes, &prop, 0);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuMemCreate(HOST_NUMA) failed: " + std::to_string(static_cast<int>(r)));
+    return ZC_ENOMEM;
+  }
+  r = v.reserve(&out->va, bytes, std::max<size_t>(gran, 2u << 20), 0, 0);
+  if (r == CUDA_SUCCESS) r = v.map(out->va, bytes, 0, out->h, 0);
+  if (r == CUDA_SUCCESS) {
+    CUmemAccessDesc acc[2] = {};
+    acc[0].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc[0].location.id = device;
+    acc[0].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    acc[1].location.type = CU_MEM_LOCATION_TYPE_HOST_NUMA;
+    acc[1].location.id = numa;
+    acc[1].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    r = v.set_access(out->va, bytes, acc, 2);
+  }
+  if (r != CUDA_SUCCESS) {
+    set_error("cuMemMap/SetAccess(HOST_NUMA) failed: " + std::to_string(static_cast<int>(r)));
+    if (out->va) v.addr_free(out->va, bytes);
+    v.release(out->h);
+    return ZC_ECUDA;
+  }
+  out->size = bytes;
+  return ZC_OK;
+}
+
+void vmm_host_free(VmmHost* a) {
+  const Vmm& v = vmm();
+  if (!a->va) return;
+  v.unmap(a->va, a->size);
+  v.addr_free(a->va, a->size);
+  v.release(a->h);
+  a->va = 0;
+}
+}  // namespace
+}  // namespace zc
+
+// Granularity (bytes) of host-NUMA VMM allocations, 0 when unsupported.
+extern "C" int zc_vmm_host_probe(int32_t device, uint64_t bytes, uint64_t* granularity) {
+  using namespace zc;
+  cudaSetDevice(device);
+  cudaFree(nullptr);
+  VmmHost a;
+  size_t g = 0;
+  const int rc = vmm_host_alloc(device, 0, bytes, &a, &g);
+  if (granularity) *granularity = g;
+  if (rc == ZC_OK) {
+    memset(reinterpret_cast<void*>(a.va), 0, 4096);
+    vmm_host_free(&a);
+  }
+  return rc;
+}
+
 // alloc: 0 = cudaHostAlloc(Mapped), 1 = THP (madvise) + cudaHostRegister,
-// 2 = device memory.  Returns GB/s of useful bytes in *gbs.
+// 2 = device memory, 3 = host-NUMA VMM allocation (cuMemCreate),
+// 4 = hugetlbfs 2 MB pages (MAP_HUGETLB) + cudaHostRegister,
+// 5 = cudaMallocManaged preferred on the CPU, accessed-by the device.
+// Returns GB/s of useful bytes in *gbs.
 extern "C" int zc_read_probe(int32_t device, uint64_t bytes, int pattern, uint32_t chunk_bytes,
                              int alloc, int iters, double* gbs) {
   using namespace zc;
@@ -227,6 +350,8 @@ extern "C" int zc_read_probe(int32_t device, uint64_t bytes, int pattern, uint32
   void* h = nullptr;
   const void* dp = nullptr;
   bool registered = false;
+  VmmHost vh;
+  void* managed = nullptr;
   if (alloc == 0) {
     ZC_CUDA_TRY(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
     memset(h, 1, bytes);
@@ -249,6 +374,40 @@ extern "C" int zc_read_probe(int32_t device, uint64_t bytes, int pattern, uint32
     void* d = nullptr;
     ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, h, 0));
     dp = d;
+  } else if (alloc == 3) {
+    const int rc = vmm_host_alloc(device, 0, bytes, &vh, nullptr);
+    if (rc != ZC_OK) return rc;
+    memset(reinterpret_cast<void*>(vh.va), 1, bytes);
+    dp = reinterpret_cast<const void*>(vh.va);
+  } else if (alloc == 4) {
+    const size_t huge = 2u << 20;
+    bytes = (bytes + huge - 1) / huge * huge;
+    void* m = mmap(nullptr, bytes, PROT_READ | PROT_WRITE,
+                   MAP_PRIVATE | MAP_ANONYMOUS | MAP_HUGETLB, -1, 0);
+    if (m == MAP_FAILED) {
+      set_error("mmap(MAP_HUGETLB) failed (no reserved hugepages?)");
+      return ZC_ENOMEM;
+    }
+    memset(m, 1, bytes);
+    h = m;
+    ZC_CUDA_TRY(cudaHostRegister(h, bytes, cudaHostRegisterMapped));
+    registered = true;
+    void* d = nullptr;
+    ZC_CUDA_TRY(cudaHostGetDevicePointer(&d, h, 0));
+    dp = d;
+  } else if (alloc == 5) {
+    void* m = nullptr;
+    ZC_CUDA_TRY(cudaMallocManaged(&m, bytes));
+    cudaMemLocation cpu = {};
+    cpu.type = cudaMemLocationTypeHost;
+    cudaMemLocation gpu = {};
+    gpu.type = cudaMemLocationTypeDevice;
+    gpu.id = device;
+    ZC_CUDA_TRY(cudaMemAdvise(m, bytes, cudaMemAdviseSetPreferredLocation, cpu));
+    ZC_CUDA_TRY(cudaMemAdvise(m, bytes, cudaMemAdviseSetAccessedBy, gpu));
+    memset(m, 1, bytes);
+    managed = m;
+    dp = m;
   } else {
     void* d = nullptr;
     ZC_CUDA_TRY(cudaMalloc(&d, bytes));
@@ -280,10 +439,12 @@ extern "C" int zc_read_probe(int32_t device, uint64_t bytes, int pattern, uint32
   cudaEventDestroy(b);
   cudaFree(sink);
   if (alloc == 0) cudaFreeHost(h);
-  else if (alloc == 1) {
+  else if (alloc == 1 || alloc == 4) {
     if (registered) cudaHostUnregister(h);
     munmap(h, bytes);
-  } else cudaFree(const_cast<void*>(dp));
+  } else if (alloc == 3) vmm_host_free(&vh);
+  else if (alloc == 5) cudaFree(managed);
+  else cudaFree(const_cast<void*>(dp));
   return ZC_OK;
 }
 

@@ -2,6 +2,8 @@
 
 ``DeviceGraph`` owns one ``zc_graph`` handle of the C ABI: the edge / weight
 lists live in pinned mapped host memory (``placement="zerocopy"``, EMOGI),
+in host-resident managed memory read in place (``"zerocopy-managed"``, the
+same zero-copy loads through the UVM driver's large-page GPU mappings),
 in managed memory with read-mostly advice (``"uvm"``, the paper's baseline,
 PAPER.md:593) or in HBM (``"hbm"``, control run); offsets and all per-vertex
 state live in HBM.  Building a handle pins and copies the lists once;
@@ -384,7 +386,7 @@ def evict(dg: DeviceGraph) -> None:
 def read_probe(nbytes: int, chunk_bytes: int, random, alloc: str = "pinned",
                device: int = 0, iters: int = 3) -> float:
     """GB/s of warps reading chunk_bytes per request (zero-copy toy kernel)."""
-    a = {"pinned": 0, "thp": 1, "hbm": 2}[alloc]
+    a = {"pinned": 0, "thp": 1, "hbm": 2, "vmm": 3, "hugetlb": 4, "managed_host": 5}[alloc]
     out = C.c_double()
     N.check(N.lib().zc_read_probe(device, nbytes, int(random), chunk_bytes, a, iters,
                                   C.byref(out)))

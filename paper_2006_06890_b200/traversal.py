@@ -6,7 +6,8 @@ messages), same ``TraversalResult`` (int64 values with -1 / INT64_MAX for
 unreached, iteration count, per-iteration traversed edges, per-iteration
 modelled traffic).  The work runs in the CUDA library through the C ABI;
 there is no CPU path.  Extra keyword-only arguments select the placement of
-the edge list (``placement="zerocopy" | "uvm" | "hbm"``) and the GPU.
+the edge list (``placement="zerocopy" | "zerocopy-managed" | "uvm" | "hbm"``)
+and the GPU.
 """
 from __future__ import annotations
 

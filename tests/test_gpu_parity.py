@@ -42,7 +42,7 @@ def test_small_graphs_match_reference(strategy):
     assert not bad, f"{len(bad)} mismatches, first {bad[:8]}"
 
 
-@pytest.mark.parametrize("placement", ["uvm", "hbm"])
+@pytest.mark.parametrize("placement", ["uvm", "hbm", "zerocopy-managed"])
 def test_small_graphs_other_placements(placement):
     bad = []
     for c in CASES[::3]:
@@ -303,7 +303,7 @@ def test_report_rows_join_reference_checksums(tmp_path):
     assert lines[0].startswith("# emogi-b200") and lines[1].split(",") == COLUMNS
 
 
-@pytest.mark.parametrize("placement", ["zerocopy", "uvm", "hbm"])
+@pytest.mark.parametrize("placement", ["zerocopy", "uvm", "hbm", "zerocopy-managed"])
 def test_open_emgi_roundtrip(tmp_path, placement):
     g = zc.with_uniform_weights(zc.generate_uniform(2 ** 16, 16, 16, seed=3))
     gold = goldens()["uniform_2p16_d16"]
