@@ -261,7 +261,6 @@ void zc::free_graph(zc_graph* g) {
   free_list(g->h_pairs, false, g->hbm_pairs);
   free_list(g->h_cmp, false, g->hbm_cmp);
   cudaFree(g->d_coff);
-  cudaFree(g->d_cw);
   if (g->h_off) cudaFreeHost(g->h_off);
   cudaFree(g->d_off);
   cudaFree(g->d_state);
@@ -745,7 +744,6 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     a.scan_tmp_bytes = g->scan_tmp_bytes;
     a.cmp = static_cast<const uint32_t*>(g->d_cmp);
     a.coff = g->d_coff;
-    a.cw = g->d_cw;
     tune_params(&a);
     return a;
   };
@@ -1581,7 +1579,6 @@ int zc_pagerank(zc_graph* g, int strategy, double damping, uint64_t max_iters, d
     a.exch = pushed;
     a.cmp = static_cast<const uint32_t*>(g->d_cmp);
     a.coff = g->d_coff;
-    a.cw = g->d_cw;
     a.wcnt = g->d_wcnt;
     a.wpre = g->d_wpre;
     a.scan_tmp = g->d_scan_tmp;

@@ -1,17 +1,18 @@
-// Delta-compressed lists: an optional B200-native host-store format.
+// Line-compressed lists: an optional B200-native host-store format.
 //
-// Zero-copy traversal is bound by the host link (51.5 GB/s for SM-side
-// reads, profiles/r01_tma_bulk_probe.txt); BFS / CC / PageRank results do not
-// depend on the order inside a list, so the lists can be sorted and stored
-// delta-encoded to move fewer bytes over PCIe.  Format (per list of degree d,
-// sorted ascending):
-//   blocks of kCmpBlock = 128 elements; block = u32 base (first element)
-//   followed by the block's 127 (or count-1) deltas at the list's width w
-//   bits, packed little-endian from bit 32, padded to a 4-byte word;
-//   full blocks are cmp_full_bytes(w) long, the last block exactly as long
-//   as its count needs.
-// Per-vertex byte offset (u64[V+1]) and width (u8[V]) live in HBM next to the
-// CSR offsets; the stream itself lives in the handle's placement.
+// Zero-copy traversal is bound by the host link: ~437 M fully-used 128-byte
+// line reads/s (55.9 GB/s of PCIe read bytes, profiles/ncu_summary.json), and
+// about as much by the request count as by the bytes.  BFS / CC / PageRank
+// results do not depend on the order inside a list, so a list can be sorted
+// and stored delta-encoded in self-describing 128-byte lines (format in
+// zc_internal.cuh): one aligned line read then carries ~50-100 edges of a hub
+// list instead of 32.  A list is compressed only when that needs fewer lines
+// than its raw form touches; short lists stay raw (packed windows share their
+// lines).  Lines are filled greedily: as many deltas as fit 1024 - 48 bits at
+// the width of the widest one, at most 255.
+//
+// Per-vertex first-line index coff (u64[V+1]) lives in HBM next to the CSR
+// offsets; the line stream lives in the handle's placement.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -24,54 +25,102 @@
 namespace zc {
 namespace {
 
-__global__ void k_cmp_sizes(uint64_t nv, const uint64_t* off, const uint32_t* e, uint8_t* width,
-                            uint32_t* bytes) {
+constexpr unsigned kFullMask = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t bits_of(uint32_t x) { return x ? 32 - __clz(x) : 0; }
+
+// Greedy fill of one line starting at element p of the sorted list e[0, d):
+// the largest K <= min(255, d-1-p) with 48 + K * max(bits(delta 1..K)) <=
+// 1024.  Warp-cooperative; returns count = K + 1 and the width.
+__device__ __forceinline__ void line_fill(const uint32_t* e, uint64_t d, uint64_t p, int lane,
+                                          uint32_t* count, uint32_t* width) {
+  const uint64_t rest = d - 1 - p;
+  const uint32_t kmax = static_cast<uint32_t>(rest < kCmpMaxCount - 1 ? rest : kCmpMaxCount - 1);
+  uint32_t K = 0, m = 0;
+  for (uint32_t c = 0; c < kmax; c += 32) {
+    const uint32_t k = c + lane + 1;
+    uint32_t pm = m;
+    if (k <= kmax) pm = max(pm, bits_of(e[p + k] - e[p + k - 1]));
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFullMask, pm, o);
+      if (lane >= o) pm = max(pm, t);
+    }
+    // 48 + k * pm is non-decreasing in the lane: the fitting lanes are a prefix
+    const bool ok = k <= kmax && kCmpHdrBits + k * pm <= kLineWords * 32;
+    const int nok = __popc(__ballot_sync(kFullMask, ok));
+    if (nok) m = __shfl_sync(kFullMask, pm, nok - 1);
+    K = c + nok;
+    if (nok < 32) break;
+  }
+  *count = K + 1;
+  *width = m;
+}
+
+// Lines the list of v needs compressed, or 0 when raw is no worse.  Host
+// memory is read in 32-byte sectors: a raw list costs the sectors it touches
+// (and shares its partial lines with neighbouring lists under packed
+// windows), a compressed one full lines -- so compress only when that reads
+// strictly fewer sectors (in practice lists of more than ~28 elements).
+__global__ void k_cmp_lines(uint64_t nv, const uint64_t* off, const uint32_t* e,
+                            uint32_t* lines) {
+  constexpr uint64_t kSectorElems = 8, kLineSectors = 4;
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t v = gw; v < nv; v += nw) {
     const uint64_t s = off[v], d = off[v + 1] - s;
-    uint32_t mx = 0;
-    for (uint64_t k = 1 + lane; k < d; k += 32) mx = max(mx, e[s + k] - e[s + k - 1]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) {
-      const uint32_t w = mx ? 32 - __clz(mx) : 0;
-      width[v] = static_cast<uint8_t>(w);
-      bytes[v] = static_cast<uint32_t>(cmp_list_bytes(w, d));
+    const uint64_t raw = d ? (s + d - 1) / kSectorElems - s / kSectorElems + 1 : 0;
+    uint32_t n = 0;
+    if (raw > kLineSectors) {
+      for (uint64_t p = 0; p < d && n * kLineSectors < raw; ++n) {
+        uint32_t cnt, w;
+        line_fill(e + s, d, p, lane, &cnt, &w);
+        p += cnt;
+      }
+      if (n * kLineSectors >= raw) n = 0;
     }
+    if (lane == 0) lines[v] = n;
   }
 }
 
-// Warp per list, lane per block: base word, then the deltas bit-packed.
-__global__ void k_cmp_encode(uint64_t nv, const uint64_t* off, const uint32_t* e,
-                             const uint8_t* width, const uint64_t* coff, uint32_t* out) {
+// Encode: warp per compressed list, one shared-memory line buffer per warp.
+__global__ void __launch_bounds__(256) k_cmp_encode(uint64_t nv, const uint64_t* off,
+                                                    const uint32_t* e, const uint64_t* coff,
+                                                    uint32_t* out) {
+  __shared__ uint32_t buf[8][kLineWords + 2];
   const int lane = threadIdx.x & 31;
+  uint32_t* L = buf[threadIdx.x >> 5];
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t v = gw; v < nv; v += nw) {
+    const uint64_t l0 = coff[v], nl = coff[v + 1] - l0;
+    if (!nl) continue;
     const uint64_t s = off[v], d = off[v + 1] - s;
-    if (!d) continue;
-    const uint32_t w = width[v];
-    const uint64_t nb = (d + kCmpBlock - 1) / kCmpBlock;
-    for (uint64_t b = lane; b < nb; b += 32) {
-      uint32_t* dst = out + (coff[v] + b * cmp_full_bytes(w)) / 4;
-      const uint64_t e0 = s + b * kCmpBlock;
-      const uint64_t rem = d - b * kCmpBlock;
-      const uint64_t cnt = rem < kCmpBlock ? rem : kCmpBlock;
-      dst[0] = e[e0];
-      uint64_t acc = 0;
-      uint32_t nbits = 0, word = 1;
-      for (uint64_t i = 1; i < cnt; ++i) {
-        acc |= static_cast<uint64_t>(e[e0 + i] - e[e0 + i - 1]) << nbits;
-        nbits += w;
-        if (nbits >= 32) {
-          dst[word++] = static_cast<uint32_t>(acc);
-          acc >>= 32;
-          nbits -= 32;
+    const uint32_t* x = e + s;
+    uint64_t p = 0;
+    for (uint64_t t = 0; t < nl; ++t) {
+      uint32_t cnt, w;
+      line_fill(x, d, p, lane, &cnt, &w);
+      L[lane] = 0;
+      if (lane < 2) L[kLineWords + lane] = 0;
+      __syncwarp();
+      if (w)
+        for (uint32_t k = lane + 1; k < cnt; k += 32) {
+          const uint32_t dl = x[p + k] - x[p + k - 1];
+          const uint32_t bit = kCmpHdrBits + (k - 1) * w;
+          atomicOr(&L[bit >> 5], dl << (bit & 31));
+          if ((bit & 31) + w > 32) atomicOr(&L[(bit >> 5) + 1], dl >> (32 - (bit & 31)));
         }
+      __syncwarp();
+      if (lane == 0) {
+        L[0] = x[p];
+        L[1] |= w | ((cnt - 1) << 6);
       }
-      if (nbits) dst[word] = static_cast<uint32_t>(acc);
+      __syncwarp();
+      out[(l0 + t) * kLineWords + lane] = L[lane];
+      __syncwarp();
+      p += cnt;
     }
   }
 }
@@ -109,29 +158,28 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
       p = nullptr;
       return q;
     }
-  } sorted, sizes, tmp, enc, cw, coff;
+  } sorted, lines, tmp, enc, coff;
   ZC_CUDA_TRY(cudaMalloc(&sorted.p, std::max<uint64_t>(ne, 1) * 4));
   ZC_CUDA_TRY(cudaMemcpy(sorted.p, g->h_edges, ne * 4, cudaMemcpyDefault));
   const int rc = sort_lists_device(4, nv, g->d_off, g->h_off, sorted.p);
   if (rc) return rc;
-  ZC_CUDA_TRY(cudaMalloc(&cw.p, std::max<uint64_t>(nv, 1)));
   ZC_CUDA_TRY(cudaMalloc(&coff.p, (nv + 1) * sizeof(uint64_t)));
-  ZC_CUDA_TRY(cudaMalloc(&sizes.p, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
-  k_cmp_sizes<<<kCmpGrid, 256>>>(nv, g->d_off, static_cast<uint32_t*>(sorted.p),
-                                 static_cast<uint8_t*>(cw.p), static_cast<uint32_t*>(sizes.p));
+  ZC_CUDA_TRY(cudaMalloc(&lines.p, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
+  k_cmp_lines<<<kCmpGrid, 256>>>(nv, g->d_off, static_cast<uint32_t*>(sorted.p),
+                                 static_cast<uint32_t*>(lines.p));
+  ZC_CUDA_TRY(cudaGetLastError());
   const size_t tb = scan_tmp_bytes(nv);
   ZC_CUDA_TRY(cudaMalloc(&tmp.p, tb));
-  ZC_CUDA_TRY(scan_u32_to_u64(static_cast<uint32_t*>(sizes.p), static_cast<uint64_t*>(coff.p), nv,
+  ZC_CUDA_TRY(scan_u32_to_u64(static_cast<uint32_t*>(lines.p), static_cast<uint64_t*>(coff.p), nv,
                               tmp.p, tb, 0));
   uint64_t total = 0;
   ZC_CUDA_TRY(cudaMemcpy(&total, static_cast<uint64_t*>(coff.p) + nv, sizeof(total),
                          cudaMemcpyDeviceToHost));
-  const size_t bytes = std::max<uint64_t>(total, 4) + 16;  // + slack for the decoder
+  const size_t bytes = std::max<uint64_t>(total, 1) * kLineBytes;
   ZC_CUDA_TRY(cudaMalloc(&enc.p, bytes));
   ZC_CUDA_TRY(cudaMemset(enc.p, 0, bytes));
   k_cmp_encode<<<kCmpGrid, 256>>>(nv, g->d_off, static_cast<uint32_t*>(sorted.p),
-                                  static_cast<uint8_t*>(cw.p), static_cast<uint64_t*>(coff.p),
-                                  static_cast<uint32_t*>(enc.p));
+                                  static_cast<uint64_t*>(coff.p), static_cast<uint32_t*>(enc.p));
   ZC_CUDA_TRY(cudaDeviceSynchronize());
   // place the stream like the lists
   void* host = nullptr;
@@ -169,9 +217,8 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
   g->h_cmp = host;
   g->d_cmp = dev;
   g->hbm_cmp = hbm;
-  g->d_cw = static_cast<uint8_t*>(cw.release());
   g->d_coff = static_cast<uint64_t*>(coff.release());
-  g->cmp_bytes = total;
-  if (compressed_bytes) *compressed_bytes = total;
+  g->cmp_bytes = total * kLineBytes;
+  if (compressed_bytes) *compressed_bytes = g->cmp_bytes;
   return ZC_OK;
 }

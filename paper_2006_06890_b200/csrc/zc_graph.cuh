@@ -44,7 +44,6 @@ struct zc_graph {
   const void* d_cmp = nullptr;
   void* hbm_cmp = nullptr;
   uint64_t* d_coff = nullptr;
-  uint8_t* d_cw = nullptr;
   uint64_t cmp_bytes = 0;
   // optional interleaved (dst, weight) u32 pairs for SSSP (zc_graph_build_pairs)
   void* h_pairs = nullptr;

@@ -46,20 +46,17 @@ constexpr uint32_t kExchNone32 = 0x7fffffffu;
 constexpr uint32_t kBigSteps = 16;
 
 enum Strategy : int { kNaive = 0, kMerged = 1, kMergedAligned = 2, kPacked = 3, kCompressed = 4 };
-// kCompressed (B200 host-store option): the lists as sorted, delta-encoded
-// 128-element blocks (zc_compress.cu); window = one block.
-constexpr uint32_t kCmpBlock = 128;
-__host__ __device__ __forceinline__ uint64_t cmp_block_bytes(uint32_t w, uint64_t count) {
-  return 4 + ((count - 1) * w + 31) / 32 * 4;  // base word + packed deltas
-}
-__host__ __device__ __forceinline__ uint64_t cmp_full_bytes(uint32_t w) {
-  return cmp_block_bytes(w, kCmpBlock);
-}
-__host__ __device__ __forceinline__ uint64_t cmp_list_bytes(uint32_t w, uint64_t d) {
-  if (!d) return 0;
-  const uint64_t nb = (d + kCmpBlock - 1) / kCmpBlock;
-  return (nb - 1) * cmp_full_bytes(w) + cmp_block_bytes(w, d - (nb - 1) * kCmpBlock);
-}
+// kCompressed (B200 host-store option, zc_compress.cu): every list whose
+// compressed form needs fewer 128-byte lines than its raw form touches is
+// stored as self-describing compressed lines; the other lists are read raw
+// with packed windows.  A compressed line (32 u32 words, 128-byte aligned):
+//   word 0        base = first element
+//   word 1 [0,6)  w = delta width in bits (0..32); [6,14) count - 1 (<= 255)
+//   bit 48 + (k-1) w, k = 1..count-1: delta k = elem[k] - elem[k-1] (sorted)
+// Window = one line: one fully-used, aligned PCIe read per warp request.
+constexpr uint32_t kCmpHdrBits = 48;
+constexpr uint32_t kCmpMaxCount = 256;
+constexpr uint32_t kLineWords = 32;
 // kPacked (B200 extension, not one of the paper's three): a window is an
 // aligned 32-element block touched by any frontier list, fetched once for all
 // the lists that share it (see k_window_counts / k_expand_sweep).
@@ -132,10 +129,10 @@ struct ExpandArgs {
   // memory (then `n` is only the maximum, used to size grids)
   const uint64_t* n_dev;
   const uint64_t* iter_dev;
-  // compressed lists (kCompressed)
+  // compressed lists (kCompressed): the line stream and each vertex's first
+  // line (coff[v+1] - coff[v] lines; 0 = the list is read raw)
   const uint32_t* cmp;
   const uint64_t* coff;
-  const uint8_t* cw;
 };
 
 // ZC_TUNE="unroll=8,ctas=6,sched=chunk": expansion tuning knobs for experiments.

@@ -190,7 +190,7 @@ struct LineElems {
 template <int STRAT, typename ET>
 __device__ __forceinline__ uint64_t window_base(uint64_t s) {
   if (STRAT == kMergedAligned) return s & ~(LineElems<ET>::value - 1);
-  if (STRAT == kPacked) return s & ~static_cast<uint64_t>(kWarp - 1);
+  if (STRAT == kPacked || STRAT == kCompressed) return s & ~static_cast<uint64_t>(kWarp - 1);
   return s;
 }
 
@@ -203,6 +203,7 @@ struct Batch {
   WT wt[U];
   uint64_t sval[U];
   bool ok[U];
+  bool line[U];  // kCompressed: window u is a compressed line (warp-uniform)
 };
 
 template <int ALGO, typename ET, typename WT, int U>
@@ -404,35 +405,87 @@ constexpr int kStage = 256;  // frontier slots staged in shared memory at a time
 // first block when the nearest earlier non-empty slot of the same aligned
 // group of kStage slots (one shared-memory stage of the sweep) already
 // touches it -- so every block is fetched once per group and the lists that
-// share it are always staged together.
+// share it are always staged together.  Compressed: a compressed list's
+// windows are its lines; the other lists count as packed, sharing only with
+// raw lists.
+__device__ __forceinline__ uint64_t cmp_lines(const ExpandArgs& a, uint64_t j) {
+  const uint32_t v = a.front[j];
+  return a.coff[v + 1] - a.coff[v];
+}
+
 template <int STRAT, typename ET>
-__global__ void k_window_counts(const uint64_t* fs, const uint32_t* fd, uint64_t n0,
-                                const uint64_t* n_dev, uint32_t* wcnt) {
-  const uint64_t n = n_dev ? *n_dev : n0;
+__global__ void k_window_counts(ExpandArgs a) {
+  const uint64_t n = a.n_dev ? *a.n_dev : a.n;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t s = fs[j], d = fd[j];
+    const uint64_t s = a.fs[j], d = a.fd[j];
     if (!d) {
-      wcnt[j] = 0;
+      a.wcnt[j] = 0;
       continue;
     }
     if (STRAT == kCompressed) {
-      wcnt[j] = static_cast<uint32_t>((d + kCmpBlock - 1) / kCmpBlock);
-      continue;
-    }
-    uint64_t w = (s + d - window_base<STRAT, ET>(s) + kWarp - 1) / kWarp;
-    if (STRAT == kPacked) {
-      const uint64_t group0 = j - j % kStage;
-      for (uint64_t i = j; i > group0; --i) {
-        const uint32_t di = fd[i - 1];
-        if (di) {
-          w -= ((fs[i - 1] + di - 1) / kWarp) == (s / kWarp);
-          break;
-        }
+      const uint64_t nl = cmp_lines(a, j);
+      if (nl) {
+        a.wcnt[j] = static_cast<uint32_t>(nl);
+        continue;
       }
     }
-    wcnt[j] = static_cast<uint32_t>(w);
+    uint64_t w = (s + d - window_base<STRAT, ET>(s) + kWarp - 1) / kWarp;
+    if (STRAT == kPacked || STRAT == kCompressed) {
+      const uint64_t group0 = j - j % kStage;
+      for (uint64_t i = j; i > group0; --i) {
+        const uint32_t di = a.fd[i - 1];
+        if (!di || (STRAT == kCompressed && cmp_lines(a, i - 1))) continue;
+        w -= ((a.fs[i - 1] + di - 1) / kWarp) == (s / kWarp);
+        break;
+      }
+    }
+    a.wcnt[j] = static_cast<uint32_t>(w);
   }
+}
+
+// Decode one compressed line (this lane's word in x) and visit its elements:
+// lane l takes elements [l m, l m + m), m = ceil(count / 32); values are the
+// base plus a warp prefix sum of the deltas (u32 exact: ids < 2^32).
+template <int ALGO>
+__device__ __forceinline__ void visit_line(const ExpandArgs& a, uint32_t x, uint64_t sval,
+                                           uint32_t* L, int lane) {
+  L[lane] = x;
+  if (lane < 2) L[kLineWords + lane] = 0;
+  __syncwarp();
+  const uint32_t hdr = L[1];
+  const uint32_t w = hdr & 63, cnt = ((hdr >> 6) & 255) + 1;
+  const uint32_t m = (cnt + 31) >> 5;
+  const uint32_t e0 = lane * m, e1 = min(cnt, e0 + m);
+  const uint64_t mask = w >= 32 ? 0xffffffffull : ((1ull << w) - 1);
+  uint32_t run = 0;
+  for (uint32_t e = e0; e < e1; ++e) {
+    if (e == 0) {
+      run += L[0];
+    } else {
+      const uint32_t bit = kCmpHdrBits + (e - 1) * w;
+      const uint64_t pair = (static_cast<uint64_t>(L[(bit >> 5) + 1]) << 32) | L[bit >> 5];
+      run += static_cast<uint32_t>((pair >> (bit & 31)) & mask);
+    }
+  }
+  uint32_t incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
+  }
+  uint32_t val = incl - run;
+  for (uint32_t e = e0; e < e1; ++e) {
+    if (e == 0) {
+      val += L[0];
+    } else {
+      const uint32_t bit = kCmpHdrBits + (e - 1) * w;
+      const uint64_t pair = (static_cast<uint64_t>(L[(bit >> 5) + 1]) << 32) | L[bit >> 5];
+      val += static_cast<uint32_t>((pair >> (bit & 31)) & mask);
+    }
+    Visit<ALGO>::apply(a, val, 0, sval);
+  }
+  __syncwarp();
 }
 
 template <int STRAT, int ALGO, typename ET, typename WT, int U>
@@ -441,8 +494,11 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
     a.n = *a.n_dev;
     a.iter = static_cast<uint32_t>(*a.iter_dev) + 1;
   }
+  constexpr bool kCmp = STRAT == kCompressed;
   __shared__ uint64_t sh_s[kStage], sh_e[kStage], sh_v[kStage];
   __shared__ uint64_t sh_w[kStage + 1];
+  __shared__ uint64_t sh_c[kCmp ? kStage : 1];                // first line, or ~0 (raw)
+  __shared__ uint32_t sh_line[kCmp ? kSweepWarps : 1][kLineWords + 2];  // decode buffer
   __shared__ uint64_t sh_j;
   const uint64_t n = a.n;
   const uint64_t T = a.wpre[n];
@@ -482,6 +538,15 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
         sh_s[i] = s0;
         sh_e[i] = s0 + a.fd[jj];
         if (AlgoTraits<ALGO>::has_val) sh_v[i] = a.fval[jj];
+        if constexpr (kCmp) {
+          // a compressed list keeps an empty raw range (the owner search
+          // over sh_s stays monotone and never matches it)
+          const uint32_t v = a.front[jj];
+          const uint64_t c0 = a.coff[v];
+          const bool c = a.coff[v + 1] != c0;
+          sh_c[i] = c ? c0 : ~0ull;
+          if (c) sh_e[i] = s0;
+        }
       }
     }
     __syncthreads();
@@ -495,6 +560,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
         const uint64_t q = q0 + u;
         bt.ok[u] = false;
         bt.sval[u] = 0;
+        if constexpr (kCmp) bt.line[u] = false;
         if (q < Wend) {  // warp-uniform
           if (u == 0) {  // binary search for the batch head, then walk
             int lo = 0, hi = kStage;  // sh_w[lo] <= q < sh_w[hi]
@@ -508,7 +574,15 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
           }
           const uint64_t s0 = sh_s[k], e0 = sh_e[k];
           uint64_t idx;
-          if (STRAT == kPacked) {
+          if constexpr (kCmp) {
+            bt.line[u] = sh_c[k] != ~0ull;
+            if (bt.line[u]) {  // one aligned compressed line, a word per lane
+              if (AlgoTraits<ALGO>::has_val) bt.sval[u] = sh_v[k];
+              bt.dst[u] = ld_list(a.cmp + (sh_c[k] + (q - sh_w[k])) * kLineWords + lane);
+              continue;
+            }
+          }
+          if (STRAT == kPacked || kCmp) {
             // block t of slot k's new blocks; the lane's element may belong to
             // any staged list that shares the block: search its owner
             const uint64_t fb = s0 / kWarp;
@@ -542,154 +616,19 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
       for (; q0 < Wend; q0 += kSweepWarps * U) {
         const uint64_t qn = q0 + kSweepWarps * U;
         if (qn < Wend) issue(nxt, qn);
-        visit_batch<ALGO, ET, WT, U>(a, cur);
-        cur = nxt;
-      }
-    }
-    __syncthreads();
-    W = Wend;
-    j += kStage;
-  }
-}
-
-// Compressed lists (kCompressed): the sweep schedule with one window = one
-// 128-element block.  A warp loads the block's words (coalesced, <= 512 B),
-// stages them in shared memory, decodes 4 elements per lane (bit extraction +
-// a warp prefix sum over base and deltas) and visits them.
-template <int ALGO>
-__global__ void __launch_bounds__(kSweepThreads) k_expand_sweep_cmp(ExpandArgs a) {
-  if (a.n_dev) {
-    a.n = *a.n_dev;
-    a.iter = static_cast<uint32_t>(*a.iter_dev) + 1;
-  }
-  __shared__ uint64_t sh_c[kStage], sh_v[kStage];
-  __shared__ uint64_t sh_w[kStage + 1];
-  __shared__ uint32_t sh_d[kStage];
-  __shared__ uint8_t sh_bits[kStage];
-  __shared__ uint32_t sh_blk[kSweepWarps][4 * kWarp + 2];
-  __shared__ uint64_t sh_j;
-  const uint64_t n = a.n;
-  const uint64_t T = a.wpre[n];
-  const uint64_t G = gridDim.x, b = blockIdx.x;
-  const uint64_t Wb = T / G * b + min(b, T % G);
-  const uint64_t We = Wb + T / G + (b < T % G ? 1 : 0);
-  if (Wb >= We) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp == 0) {
-    uint64_t lo = 0, hi = n;
-    while (hi - lo > 1) {
-      const uint64_t step = (hi - lo + 31) / 32;
-      const uint64_t probe = lo + step * (lane + 1);
-      const bool le = probe < hi && a.wpre[probe] <= Wb;
-      const unsigned m = __ballot_sync(kFull, le);
-      const int k = m ? 31 - __clz(m) : -1;
-      const uint64_t nlo = k >= 0 ? lo + step * (k + 1) : lo;
-      hi = min(hi, nlo + step);
-      lo = nlo;
-    }
-    if (lane == 0) sh_j = lo - lo % kStage;
-  }
-  __syncthreads();
-  uint64_t j = sh_j;
-  uint64_t W = Wb;
-  uint32_t* blk = sh_blk[warp];
-  while (W < We) {
-    for (int i = threadIdx.x; i <= kStage; i += kSweepThreads) {
-      const uint64_t jj = j + i;
-      sh_w[i] = jj <= n ? a.wpre[jj] : T;
-      if (i < kStage && jj < n) {
-        const uint32_t v = a.front[jj];
-        sh_c[i] = a.coff[v];
-        sh_bits[i] = a.cw[v];
-        sh_d[i] = a.fd[jj];
-        if (AlgoTraits<ALGO>::has_val) sh_v[i] = a.fval[jj];
-      }
-    }
-    __syncthreads();
-    const uint64_t Wend = min(We, sh_w[kStage]);
-    // block q of the staged slots: owner slot, width, element count, words
-    struct Blk {
-      int slot;
-      uint32_t w, cnt, words;
-      const uint32_t* src;
-    };
-    auto locate = [&](uint64_t q) {
-      int lo = 0, hi = kStage;  // sh_w[lo] <= q < sh_w[hi]
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (sh_w[mid] <= q) lo = mid; else hi = mid;
-      }
-      Blk k;
-      k.slot = lo;
-      const uint64_t t = q - sh_w[lo];
-      k.w = sh_bits[lo];
-      const uint64_t rem = sh_d[lo] - t * kCmpBlock;
-      k.cnt = static_cast<uint32_t>(rem < kCmpBlock ? rem : kCmpBlock);
-      k.words = static_cast<uint32_t>(cmp_block_bytes(k.w, k.cnt) / 4);
-      k.src = a.cmp + (sh_c[lo] + t * cmp_full_bytes(k.w)) / 4;
-      return k;
-    };
-    auto load = [&](const Blk& k, uint32_t (&x)[4]) {
+        if constexpr (kCmp) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint32_t qi = r * kWarp + lane;
-        x[r] = qi < k.words ? ld_list(k.src + qi) : 0u;
-      }
-    };
-    // software pipeline: the next block's words are in flight while this
-    // block is decoded and visited
-    uint64_t q = W + warp;
-    if (q < Wend) {
-      Blk kc = locate(q);
-      uint32_t xc[4];
-      load(kc, xc);
-      for (; q < Wend; q += kSweepWarps) {
-        const uint64_t qn = q + kSweepWarps;
-        Blk kn = kc;
-        uint32_t xn[4] = {0u, 0u, 0u, 0u};
-        if (qn < Wend) {
-          kn = locate(qn);
-          load(kn, xn);
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r) blk[r * kWarp + lane] = xc[r];
-        if (lane < 2) blk[4 * kWarp + lane] = 0;
-        __syncwarp();
-        // element e = 4 * lane + i: e == 0 -> base, else delta e-1 at bit 32 + (e-1) w
-        const uint32_t w = kc.w, cnt = kc.cnt;
-        const uint64_t mask = w >= 32 ? 0xffffffffull : ((1ull << w) - 1);
-        uint64_t val[4];
-        uint64_t run = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t e = 4 * lane + i;
-          uint64_t xval = 0;
-          if (e == 0) {
-            xval = blk[0];
-          } else if (e < cnt) {
-            const uint32_t bit = 32 + (e - 1) * w;
-            const uint64_t pair =
-                (static_cast<uint64_t>(blk[(bit >> 5) + 1]) << 32) | blk[bit >> 5];
-            xval = (pair >> (bit & 31)) & mask;
+          for (int u = 0; u < U; ++u) {
+            if (cur.line[u])  // warp-uniform
+              visit_line<ALGO>(a, static_cast<uint32_t>(cur.dst[u]), cur.sval[u], sh_line[warp],
+                               lane);
+            else if (cur.ok[u])
+              Visit<ALGO>::apply(a, cur.dst[u], 0, cur.sval[u]);
           }
-          run += xval;
-          val[i] = run;
+        } else {
+          visit_batch<ALGO, ET, WT, U>(a, cur);
         }
-        uint64_t incl = run;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint64_t o = __shfl_up_sync(kFull, incl, d);
-          if (lane >= d) incl += o;
-        }
-        const uint64_t before = incl - run;
-        __syncwarp();
-        const uint64_t sval = AlgoTraits<ALGO>::has_val ? sh_v[kc.slot] : 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (4 * lane + i < cnt) Visit<ALGO>::apply(a, before + val[i], 0, sval);
-        kc = kn;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) xc[r] = xn[r];
+        cur = nxt;
       }
     }
     __syncthreads();
@@ -1359,7 +1298,7 @@ cudaError_t expand_sweep(const ExpandArgs& a, int num_sms, cudaStream_t st,
                          uint64_t* launches) {
   // window counts -> global exclusive prefix (wpre[n] = total windows)
   const int g1 = grid_for(a.n, 256, num_sms, 16);
-  k_window_counts<STRAT, ET><<<g1, 256, 0, st>>>(a.fs, a.fd, a.n, a.n_dev, a.wcnt);
+  k_window_counts<STRAT, ET><<<g1, 256, 0, st>>>(a);
   cudaError_t e =
       scan_u32_to_u64(a.wcnt, a.wpre, a.n, a.scan_tmp, a.scan_tmp_bytes, st, a.n_dev);
   if (e != cudaSuccess) return e;
@@ -1436,17 +1375,7 @@ cudaError_t expand_a(int algo, int eb, int wb, const ExpandArgs& a, int num_sms,
 
 template <int ALGO>
 cudaError_t expand_cmp(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t* launches) {
-  const int g1 = grid_for(a.n, 256, num_sms, 16);
-  k_window_counts<kCompressed, uint32_t><<<g1, 256, 0, st>>>(a.fs, a.fd, a.n, a.n_dev, a.wcnt);
-  cudaError_t e =
-      scan_u32_to_u64(a.wcnt, a.wpre, a.n, a.scan_tmp, a.scan_tmp_bytes, st, a.n_dev);
-  if (e != cudaSuccess) return e;
-  static int grid = 0;
-  if (!grid) grid = resident_ctas(k_expand_sweep_cmp<ALGO>, kSweepThreads, num_sms);
-  const int g = a.ctas_per_sm > 0 ? num_sms * a.ctas_per_sm : grid;
-  k_expand_sweep_cmp<ALGO><<<g, kSweepThreads, 0, st>>>(a);
-  *launches += 5;
-  return cudaGetLastError();
+  return expand_sweep<kCompressed, ALGO, uint32_t, uint32_t, kUnroll>(a, num_sms, st, launches);
 }
 
 cudaError_t launch_expand(int strategy, int algo, int edge_bytes, int weight_bytes,
