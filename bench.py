@@ -49,9 +49,12 @@ def parse():
     p.add_argument("--scale", type=int, default=27)
     p.add_argument("--edge-factor", type=int, default=16)
     p.add_argument("--seed", type=int, default=27)
-    # packed: merged-aligned line windows merged across adjacent frontier lists
-    # (B200 extension, bit-identical results); variants report all four
-    p.add_argument("--strategy", default="packed")
+    # compressed: lists that read fewer sectors that way are stored as
+    # self-describing 128-byte delta lines, the rest read raw with packed
+    # windows (merged-aligned line windows shared across adjacent frontier
+    # lists) -- B200 host-store extension, bit-identical results; variants
+    # report naive / merged / merged-aligned / packed beside it
+    p.add_argument("--strategy", default="compressed")
     p.add_argument("--no-variants", action="store_true",
                    help="skip the naive / merged / UVM / HBM comparison runs")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -218,6 +221,9 @@ def main():
                           "pinned host memory (zero-copy)",
               "graph": f"kron{args.scale}", "scale": args.scale, "edge_factor": args.edge_factor,
               "seed": args.seed + rank, "strategy": args.strategy, "placement": "zerocopy",
+              "list_store": ("raw u32 lists; lists that read fewer 32 B sectors compressed are "
+                             "also stored as 128 B delta lines (B200 host-store extension)"
+                             if args.strategy == "compressed" else "raw u32 lists"),
               "sources": "pick_sources(g, 64, seed=7)",
               "l2": "inputs larger than L2 (8 GiB edge list in host memory, 512 MiB level "
                     "array)",
@@ -236,6 +242,12 @@ def main():
 
     strat = args.strategy
     probe = zc.link_probe(device=device, nbytes=1 << 30, iters=5)
+    cmp_info = None
+    if strat == "compressed":  # host-store build, like pinning: outside the timed region
+        t0 = time.time()
+        nbytes = dg.build_compressed()
+        cmp_info = {"build_s": time.time() - t0, "line_stream_bytes": nbytes}
+    link = LinkBytes(dg, strat)
 
     # warm-up (untimed)
     for i in range(args.warmup):
@@ -244,7 +256,7 @@ def main():
     # timed region 1: device time of the traversal loop (value)
     barrier(world, device)
     kernel_ms = expand_ms = 0.0
-    trav = launches = 0
+    trav = launches = link_bytes = 0
     with ClockSampler(device) as clk:
         for i in range(args.steps):
             r = zc.bfs(dg, int(sources[(args.warmup + i) % 64]), strat, collect_traffic=False)
@@ -252,6 +264,7 @@ def main():
             expand_ms += r.expand_ms
             trav += r.total_traversed_edges
             launches += r.launches
+            link_bytes += link(r.values >= 0)  # BFS expands every reached vertex once
     barrier(world, device)
     kernel_ms_max = max_over_ranks(kernel_ms, world, device)
     trav_all = sum_over_ranks(trav, world, device)
@@ -290,7 +303,8 @@ def main():
     wall_1 = max_over_ranks(time.perf_counter() - t2, world, device)
     e2e_per_call = sum_over_ranks(e2e_trav, world, device) / wall_1 / 1e9
 
-    achieved = trav * 4 / (expand_ms * 1e-3) / 1e9  # GB/s of the expansion kernels
+    # GB/s of list data the expansion kernels must read over the link
+    achieved = link_bytes / (expand_ms * 1e-3) / 1e9
     ncu = load_ncu_summary().get("bfs_expand", {})
     line = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
@@ -310,7 +324,9 @@ def main():
                      "frac": achieved / PCIE_GEN5_X16_GBS,
                      "traffic": ncu.get("dram_bytes_per_launch"),
                      "kernel": "k_expand_sweep (zero-copy edge stream)",
-                     "algorithmic_bytes": "traversed edges x 4 B (u32 edge list)",
+                     "algorithmic_bytes": link.describe,
+                     "algorithmic_bytes_per_step": link_bytes / args.steps,
+                     "u32_equivalent_gbs": trav * 4 / (expand_ms * 1e-3) / 1e9,
                      "peak_kind": "PCIe Gen5 x16 theoretical per direction",
                      "measured_peaks_gbs": probe,
                      "frac_of_measured_memcpy": achieved / probe["memcpy_h2d_gbs"],
@@ -322,6 +338,8 @@ def main():
         "graph": {"vertices": dg.num_vertices, "arcs": dg.num_edges, "gen_s": gen_s,
                   "traversed_edges_per_step": trav / args.steps},
     }
+    if cmp_info:
+        line["graph"]["compressed"] = cmp_info
 
     if rank == 0 and not args.no_cpu_baseline:
         threads = args.cpu_threads or os.cpu_count()
@@ -499,6 +517,27 @@ def main_partitioned(args, rank, world, device, config):
     part.close()
 
 
+class LinkBytes:
+    """Algorithmic link bytes of a BFS step: the list data of every expanded
+    vertex in its stored form -- 4 B per edge of a raw u32 list, 128 B per
+    line of a compressed list (strategy "compressed")."""
+
+    def __init__(self, dg, strategy: str):
+        import numpy as np
+        self.deg = np.diff(dg.as_csr().offsets).astype(np.int64)
+        self.cost = self.deg * dg.edge_elem_bytes
+        self.describe = f"expanded vertices' list bytes ({dg.edge_elem_bytes} B per edge, u32 list)"
+        if strategy == "compressed":
+            idx = dg.compressed_index().astype(np.int64)
+            lines = idx[1:] - idx[:-1]
+            self.cost = np.where(lines > 0, lines * 128, self.cost)
+            self.describe = ("expanded vertices' list bytes as stored: 128 B per compressed "
+                             "line, 4 B per edge of a raw (short) u32 list")
+
+    def __call__(self, mask) -> int:
+        return int(self.cost[mask].sum())
+
+
 def _gteps(zc, dg, sources, strategy, reps=1, evict=False):
     best = None
     for i in range(reps):
@@ -550,7 +589,7 @@ def other_configs(zc, args, device) -> dict:
     k = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, symmetrize=True,
                          device=device)
     gen_s = time.time() - t0
-    for s in ("merged-aligned", "packed"):
+    for s in ("merged-aligned", "packed", "compressed"):
         zc.cc(k, s, collect_traffic=False)
         r = zc.cc(k, s, collect_traffic=False)
         out[f"cc_kron{args.scale}_sym/{s}"] = {
@@ -574,17 +613,9 @@ def variants(zc, args, dg, sources, device, phase: str) -> dict:
     25% capacity)."""
     out = {}
     if phase == "zerocopy":
-        for s in ("naive", "merged", "merged-aligned", "packed"):
+        for s in ("naive", "merged", "merged-aligned", "packed", "compressed"):
             # naive walks each hub list with one thread (seconds per BFS): one rep
             out[f"zerocopy/{s}"] = _gteps(zc, dg, sources, s, reps=1 if s == "naive" else 2)
-        # B200 host-store option: the same lists sorted and delta-encoded
-        t0 = time.time()
-        nbytes = dg.build_compressed()
-        r = _gteps(zc, dg, sources, "compressed", reps=2)
-        bpe = nbytes / dg.num_edges
-        r.update({"bytes_per_edge": bpe, "build_s": time.time() - t0,
-                  "approx_link_gbs": r["expand_gbs"] * bpe / 4.0})
-        out["zerocopy/compressed"] = r
         return out
     import torch
     for placement in ("hbm", "uvm"):
@@ -612,8 +643,9 @@ def finish_variants(v: dict) -> None:
     ma = v["zerocopy/merged-aligned"]["gteps"]
     v["speedup_vs_uvm"] = ma / v["uvm/merged-aligned"]["gteps"]
     v["speedup_vs_uvm_cap25"] = ma / v["uvm_cap25/merged-aligned"]["gteps"]
-    v["packed_speedup_vs_uvm_cap25"] = (v["zerocopy/packed"]["gteps"]
-                                        / v["uvm_cap25/merged-aligned"]["gteps"])
+    for s in ("packed", "compressed"):
+        v[f"{s}_speedup_vs_uvm_cap25"] = (v[f"zerocopy/{s}"]["gteps"]
+                                          / v["uvm_cap25/merged-aligned"]["gteps"])
 
 
 if __name__ == "__main__":

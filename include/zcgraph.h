@@ -174,11 +174,17 @@ int zc_sync(zc_graph *g);
  * caller buffer of V doubles.  Same ValueError conditions (ZC_EINVAL). */
 int zc_pagerank(zc_graph *g, int strategy, double damping, uint64_t max_iters, double tol,
                 double *out, zc_stats *stats);
-/* Build (once) the delta-compressed copy of the lists (sorted, 128-element
- * blocks: u32 base + deltas at the list's bit width) in the handle's
- * placement; *compressed_bytes (may be NULL) receives its size.  Built
+/* Build (once) the line-compressed copy of the lists in the handle's
+ * placement: every list that reads fewer 32-byte sectors that way is sorted
+ * and stored as self-describing 128-byte lines (u32 base, 6-bit delta width,
+ * 8-bit count, deltas); the other lists stay in the raw edge list.
+ * *compressed_bytes (may be NULL) receives the line stream's size.  Built
  * automatically by the first ZC_COMPRESSED run. */
 int zc_graph_build_compressed(zc_graph *g, uint64_t *compressed_bytes);
+/* Copy the compressed-line index to the caller's V+1 u64 buffer: vertex v's
+ * list is lines [first_line[v], first_line[v+1]) of the stream (none: read
+ * raw).  ZC_ESTATE before zc_graph_build_compressed. */
+int zc_graph_compressed_index(const zc_graph *g, uint64_t *first_line);
 /* Build (once) an interleaved copy of the lists as 8-byte (dst, weight) u32
  * pairs in the handle's placement; SSSP then reads one stream instead of two,
  * so a list of n edges costs ceil(8n/128) line requests instead of two

@@ -1174,9 +1174,17 @@ int zc_part_begin(zc_graph* g, int algo, uint64_t src, int strategy, uint64_t* n
     set_error("not a partition handle");
     return ZC_ESTATE;
   }
-  if (algo < kBfs || algo > kCc || strategy < kNaive || strategy > kPacked) {
+  if (algo < kBfs || algo > kCc || strategy < kNaive || strategy > kCompressed) {
     set_error("unknown algorithm or strategy");
     return ZC_EINVAL;
+  }
+  if (strategy == kCompressed && (algo == kSssp || g->eb != 4)) {
+    set_error("compressed lists carry no weights and need 4-byte edges (bfs / cc only)");
+    return ZC_EINVAL;
+  }
+  if (strategy == kCompressed && !g->d_cmp) {  // built once per handle
+    const int rc = zc_graph_build_compressed(g, nullptr);
+    if (rc) return rc;
   }
   if (algo != kCc && src >= g->global_nv) {
     set_error("source " + std::to_string(src) + " out of range for " +
@@ -1286,6 +1294,8 @@ static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
   a.wpre = g->d_wpre;
   a.scan_tmp = g->d_scan_tmp;
   a.scan_tmp_bytes = g->scan_tmp_bytes;
+  a.cmp = static_cast<const uint32_t*>(g->d_cmp);
+  a.coff = g->d_coff;
   tune_params(&a);
   ZC_CUDA_TRY(launch_expand(g->p_strategy, algo + kPartAlgo, g->eb, g->wb, a, g->num_sms, st,
                             &g->p_launches));

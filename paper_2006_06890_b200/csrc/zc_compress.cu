@@ -222,3 +222,18 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
   if (compressed_bytes) *compressed_bytes = g->cmp_bytes;
   return ZC_OK;
 }
+
+extern "C" int zc_graph_compressed_index(const zc_graph* g, uint64_t* first_line) {
+  if (!g || !g->d_coff) {
+    set_error(g ? "compressed lists not built" : "null graph handle");
+    return ZC_ESTATE;
+  }
+  if (!first_line) {
+    set_error("null output buffer");
+    return ZC_EINVAL;
+  }
+  cudaSetDevice(g->device);
+  ZC_CUDA_TRY(cudaMemcpy(first_line, g->d_coff, (g->nv + 1) * sizeof(uint64_t),
+                         cudaMemcpyDeviceToHost));
+  return ZC_OK;
+}

@@ -200,11 +200,31 @@ class DeviceGraph:
         N.check(N.lib().zc_graph_build_pairs(self.handle))
 
     def build_compressed(self) -> int:
-        """Build the delta-compressed list stream (strategy "compressed");
+        """Build the line-compressed list stream (strategy "compressed");
         returns its size in bytes."""
         nbytes = C.c_uint64()
         N.check(N.lib().zc_graph_build_compressed(self.handle, C.byref(nbytes)))
         return nbytes.value
+
+    def compressed_index(self) -> np.ndarray:
+        """First compressed line of every vertex (V+1 u64): vertex v's list is
+        lines [idx[v], idx[v+1]) of the stream, none = read raw."""
+        out = np.empty(self.num_vertices + 1, np.uint64)
+        N.check(N.lib().zc_graph_compressed_index(self.handle, out.ctypes.data))
+        return out
+
+    def link_bytes(self, expanded: np.ndarray, strategy: str = "compressed") -> int:
+        """Bytes of list data the expansion of the vertex set `expanded` (bool
+        mask or ids) must read over the link: 4 B (edge width) per raw-list
+        edge, 128 B per compressed line (strategy "compressed")."""
+        g = self.as_csr()
+        deg = np.diff(g.offsets)[expanded]
+        if strategy != "compressed":
+            return int(deg.sum()) * self.edge_elem_bytes
+        idx = self.compressed_index()
+        lines = (idx[1:] - idx[:-1])[expanded]
+        raw = lines == 0
+        return int(deg[raw].sum()) * self.edge_elem_bytes + int(lines.sum()) * 128
 
     def expand_profile(self, iterations: int) -> np.ndarray:
         """Per-iteration device time (ms) of the expansion kernels of the last run."""

@@ -433,3 +433,80 @@ def test_pipelined_many_sources_match_single_calls(placement):
     with pytest.raises(ValueError):
         zc.bfs_many(g, [0, g.num_vertices])
     assert zc.bfs_many(g, []) == []
+
+
+def _crafted_long_lists(seed=3):
+    """Lists that exercise the compressed-line encoder: all-duplicate lists
+    (width 0, split at the 256-element line cap), dense and sparse hubs,
+    lists just either side of the ~28-element compression threshold, empty
+    and single-element lists, self loops."""
+    rng = np.random.default_rng(seed)
+    nv = 1 << 20
+    lists = []
+    for v in range(4096):
+        kind = v % 8
+        if kind == 0:
+            d = int(rng.integers(0, 3))
+            lst = rng.integers(0, nv, d)
+        elif kind == 1:
+            lst = np.full(int(rng.integers(250, 700)), int(rng.integers(0, nv)))
+        elif kind == 2:
+            lst = rng.integers(0, nv, int(rng.integers(24, 36)))
+        elif kind == 3:
+            lo = int(rng.integers(0, nv - 5000))
+            lst = rng.integers(lo, lo + 4000, int(rng.integers(300, 3000)))
+        elif kind == 4:
+            lst = rng.integers(0, nv, int(rng.integers(40, 2000)))
+        elif kind == 5:
+            lst = np.concatenate([[v], rng.integers(0, 4096, int(rng.integers(1, 60)))])
+        else:
+            lst = rng.integers(0, 4096, int(rng.integers(0, 20)))
+        lists.append(np.sort(lst).astype(np.int64) if v % 3 else lst.astype(np.int64))
+    lists += [np.array([], np.int64)] * (nv - len(lists))
+    deg = np.array([len(x) for x in lists], np.int64)
+    off = np.concatenate([[0], np.cumsum(deg)])
+    edges = np.concatenate(lists)
+    return zc.CsrGraph(nv, len(edges), off, edges, None, 4, 4, True)
+
+
+def test_compressed_lines_crafted_lists():
+    """Compressed lines (widths 0..~20, the 256-element cap, lists either side
+    of the threshold, unsorted input lists): BFS from several sources and
+    PageRank equal the oracle; the index marks only long lists compressed."""
+    g = _crafted_long_lists()
+    dg = zc.DeviceGraph(g)
+    nbytes = dg.build_compressed()
+    idx = dg.compressed_index().astype(np.int64)
+    lines = idx[1:] - idx[:-1]
+    deg = np.diff(g.offsets)
+    assert nbytes == int(lines.sum()) * 128 and lines.sum() > 0
+    assert (deg[lines > 0] > 24).all() and (lines[deg <= 24] == 0).all()
+    assert (lines[deg > 0] <= (deg[deg > 0] + 31) // 32 + 1).all()
+    for src in (0, 1, 9, 12, 33, 4095):
+        r = zc.bfs(dg, src, "compressed", collect_traffic=False)
+        ref = oracle.bfs(g, src)
+        assert np.array_equal(r.values, ref.values) and r.traversed_edges == ref.traversed_edges
+    gu = zc.symmetrized(g)
+    r = zc.cc(gu, "compressed", collect_traffic=False)
+    assert np.array_equal(r.values, oracle.cc(gu).values)
+    dg.close()
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_cuda_partitions_compressed(fused):
+    """Compressed lines inside partitions (local lists, global destinations),
+    both exchanges: identical to the whole-graph reference."""
+    g = zc.generate_powerlaw(1 << 15, 24, seed=4)
+    gu = zc.symmetrized(g)
+    for algo, graph in (("bfs", g), ("cc", gu)):
+        src = int(zc.pick_sources(graph, 1, seed=7)[0])
+        ref = oracle.run(algo, graph, src) if algo == "bfs" else oracle.cc(graph)
+        for nparts in (2, 3):
+            b = edge_balanced_bounds(graph.offsets, nparts)
+            engines = [CudaPartition(local_part(graph, b, k), b, k) for k in range(nparts)]
+            vals, iters, trav = run_partitions_local(engines, algo, src, "compressed",
+                                                     fused=fused)
+            assert np.array_equal(vals, ref.values), (algo, nparts)
+            assert iters == ref.iterations and trav == ref.traversed_edges
+            for e in engines:
+                e.close()
