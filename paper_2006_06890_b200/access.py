@@ -21,8 +21,9 @@ class AccessStrategy(Enum):
 # "packed" is a B200 extension beyond the reference's three (include/zcgraph.h
 # ZC_PACKED): windows are the aligned 32-element blocks of the union of the
 # frontier's lists, fetched once each.  Results are identical.
-# "compressed" (ZC_COMPRESSED) streams the lists delta-encoded (sorted, so only
-# for the order-independent BFS / CC / PageRank).
+# "compressed" (ZC_COMPRESSED) streams the lists sorted and delta-encoded in
+# 128-byte lines (hub lists in whole lines, short lists sharing lines, SSSP
+# weights alongside); every result is independent of the order inside a list.
 _IDS = {"naive": 0, "merged": 1, "merged-aligned": 2, "packed": 3, "compressed": 4}
 
 

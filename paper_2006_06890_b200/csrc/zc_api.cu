@@ -260,7 +260,7 @@ void zc::free_graph(zc_graph* g) {
   free_list(g->h_weights, g->weights_registered, g->hbm_weights);
   free_list(g->h_pairs, false, g->hbm_pairs);
   free_list(g->h_cmp, false, g->hbm_cmp);
-  cudaFree(g->d_coff);
+  cudaFree(g->d_cpos);
   if (g->h_off) cudaFreeHost(g->h_off);
   cudaFree(g->d_off);
   cudaFree(g->d_state);
@@ -639,8 +639,8 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
               "(naive, merged, merged-aligned), not for packed / compressed");
     return ZC_EINVAL;
   }
-  if (strategy == kCompressed && algo == kSssp) {
-    set_error("compressed lists carry no weights: use packed (or the pairs layout) for sssp");
+  if (strategy == kCompressed && algo == kSssp && g->has_weights && g->wb != 4) {
+    set_error("compressed lists carry 4-byte weights only: use packed for 8-byte weights");
     return ZC_EINVAL;
   }
   if (strategy == kCompressed && g->eb != 4) {
@@ -743,7 +743,9 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     a.scan_tmp = g->d_scan_tmp;
     a.scan_tmp_bytes = g->scan_tmp_bytes;
     a.cmp = static_cast<const uint32_t*>(g->d_cmp);
-    a.coff = g->d_coff;
+    a.cpos = g->d_cpos;
+    a.cmp_ww = g->cmp_ww;
+    a.cmp_wmin = g->cmp_wmin;
     tune_params(&a);
     return a;
   };
@@ -1178,8 +1180,8 @@ int zc_part_begin(zc_graph* g, int algo, uint64_t src, int strategy, uint64_t* n
     set_error("unknown algorithm or strategy");
     return ZC_EINVAL;
   }
-  if (strategy == kCompressed && (algo == kSssp || g->eb != 4)) {
-    set_error("compressed lists carry no weights and need 4-byte edges (bfs / cc only)");
+  if (strategy == kCompressed && (g->eb != 4 || (algo == kSssp && g->has_weights && g->wb != 4))) {
+    set_error("compressed lists need 4-byte edges (and 4-byte weights for sssp)");
     return ZC_EINVAL;
   }
   if (strategy == kCompressed && !g->d_cmp) {  // built once per handle
@@ -1295,7 +1297,9 @@ static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
   a.scan_tmp = g->d_scan_tmp;
   a.scan_tmp_bytes = g->scan_tmp_bytes;
   a.cmp = static_cast<const uint32_t*>(g->d_cmp);
-  a.coff = g->d_coff;
+  a.cpos = g->d_cpos;
+  a.cmp_ww = g->cmp_ww;
+  a.cmp_wmin = g->cmp_wmin;
   tune_params(&a);
   ZC_CUDA_TRY(launch_expand(g->p_strategy, algo + kPartAlgo, g->eb, g->wb, a, g->num_sms, st,
                             &g->p_launches));
@@ -1588,7 +1592,9 @@ int zc_pagerank(zc_graph* g, int strategy, double damping, uint64_t max_iters, d
     a.ctr = g->d_ctr;
     a.exch = pushed;
     a.cmp = static_cast<const uint32_t*>(g->d_cmp);
-    a.coff = g->d_coff;
+    a.cpos = g->d_cpos;
+    a.cmp_ww = g->cmp_ww;
+    a.cmp_wmin = g->cmp_wmin;
     a.wcnt = g->d_wcnt;
     a.wpre = g->d_wpre;
     a.scan_tmp = g->d_scan_tmp;

@@ -1,23 +1,27 @@
-// Line-compressed lists: an optional B200-native host-store format.
+// Compressed line stream: an optional B200-native host-store format.
 //
 // Zero-copy traversal is bound by the host link: ~437 M fully-used 128-byte
 // line reads/s (55.9 GB/s of PCIe read bytes, profiles/ncu_summary.json), and
-// about as much by the request count as by the bytes.  BFS / CC / PageRank
-// results do not depend on the order inside a list, so a list can be sorted
-// and stored delta-encoded in self-describing 128-byte lines (format in
-// zc_internal.cuh): one aligned line read then carries ~50-100 edges of a hub
-// list instead of 32.  A list is compressed only when that needs fewer lines
-// than its raw form touches; short lists stay raw (packed windows share their
-// lines).  Lines are filled greedily: as many deltas as fit 1024 - 48 bits at
-// the width of the widest one, at most 255.
+// about as much by the request count as by the bytes.  BFS / CC / PageRank /
+// SSSP results do not depend on the order inside a list, so every list is
+// sorted and stored delta-encoded in 128-byte lines (format in
+// zc_internal.cuh): a hub list as whole self-describing lines (~50-100 edges
+// per aligned line read instead of 32), short lists packed into shared lines
+// (one line read serves every frontier list in it).  SSSP weights ride in the
+// same lines as (weight - wmin) fields of the narrowest width that holds them.
 //
-// Per-vertex first-line index coff (u64[V+1]) lives in HBM next to the CSR
-// offsets; the line stream lives in the handle's placement.
+// Build, on the GPU except the placement scan: sort each list (by destination,
+// then weight), size every list (short: its bit length; long: the lines of a
+// greedy fill -- as many deltas as fit 1024 - 48 bits at the width of the
+// widest one, at most 255), place them in vertex order on the host (a short
+// list starts a new line only when it does not fit the current one; a long
+// list always starts one), then encode.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
 #include <string>
+#include <vector>
 
 #include "zc_graph.cuh"
 #include "zc_internal.cuh"
@@ -26,28 +30,44 @@ namespace zc {
 namespace {
 
 constexpr unsigned kFullMask = 0xffffffffu;
+constexpr uint32_t kLongSize = 1u << 31;  // size word: long list, low bits = lines
 
 __device__ __forceinline__ uint32_t bits_of(uint32_t x) { return x ? 32 - __clz(x) : 0; }
 
-// Greedy fill of one line starting at element p of the sorted list e[0, d):
-// the largest K <= min(255, d-1-p) with 48 + K * max(bits(delta 1..K)) <=
-// 1024.  Warp-cooperative; returns count = K + 1 and the width.
-__device__ __forceinline__ void line_fill(const uint32_t* e, uint64_t d, uint64_t p, int lane,
-                                          uint32_t* count, uint32_t* width) {
+// Sorted list element k: destination (and weight - wmin) of a u32 list or of a
+// u64 (dst << 32 | weight) pair list.
+struct Elems {
+  const uint32_t* e32;
+  const uint64_t* e64;
+  uint32_t wmin;
+  __device__ __forceinline__ uint32_t dst(uint64_t i) const {
+    return e64 ? static_cast<uint32_t>(e64[i] >> 32) : e32[i];
+  }
+  __device__ __forceinline__ uint32_t wt(uint64_t i) const {
+    return e64 ? static_cast<uint32_t>(e64[i]) - wmin : 0u;
+  }
+};
+
+// Greedy fill of one long-list line starting at element p of the list [0, d):
+// the largest K <= min(255, d-1-p) with 48 + K * max(bits(delta 1..K)) +
+// (K + 1) * ww <= 1024.  Warp-cooperative; returns count = K + 1 and width.
+__device__ __forceinline__ void line_fill(const Elems& x, uint64_t s, uint64_t d, uint64_t p,
+                                          uint32_t ww, int lane, uint32_t* count,
+                                          uint32_t* width) {
   const uint64_t rest = d - 1 - p;
   const uint32_t kmax = static_cast<uint32_t>(rest < kCmpMaxCount - 1 ? rest : kCmpMaxCount - 1);
   uint32_t K = 0, m = 0;
   for (uint32_t c = 0; c < kmax; c += 32) {
     const uint32_t k = c + lane + 1;
     uint32_t pm = m;
-    if (k <= kmax) pm = max(pm, bits_of(e[p + k] - e[p + k - 1]));
+    if (k <= kmax) pm = max(pm, bits_of(x.dst(s + p + k) - x.dst(s + p + k - 1)));
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t t = __shfl_up_sync(kFullMask, pm, o);
       if (lane >= o) pm = max(pm, t);
     }
-    // 48 + k * pm is non-decreasing in the lane: the fitting lanes are a prefix
-    const bool ok = k <= kmax && kCmpHdrBits + k * pm <= kLineWords * 32;
+    // the bit count is non-decreasing in the lane: the fitting lanes are a prefix
+    const bool ok = k <= kmax && kCmpHdrBits + k * pm + (k + 1) * ww <= kLineBits;
     const int nok = __popc(__ballot_sync(kFullMask, ok));
     if (nok) m = __shfl_sync(kFullMask, pm, nok - 1);
     K = c + nok;
@@ -57,36 +77,62 @@ __device__ __forceinline__ void line_fill(const uint32_t* e, uint64_t d, uint64_
   *width = m;
 }
 
-// Lines the list of v needs compressed, or 0 when raw is no worse.  Host
-// memory is read in 32-byte sectors: a raw list costs the sectors it touches
-// (and shares its partial lines with neighbouring lists under packed
-// windows), a compressed one full lines -- so compress only when that reads
-// strictly fewer sectors (in practice lists of more than ~28 elements).
-__global__ void k_cmp_lines(uint64_t nv, const uint64_t* off, const uint32_t* e,
-                            uint32_t* lines) {
-  constexpr uint64_t kSectorElems = 8, kLineSectors = 4;
+// Width of the widest delta of the whole list (warp-cooperative).
+__device__ __forceinline__ uint32_t list_width(const Elems& x, uint64_t s, uint64_t d,
+                                               int lane) {
+  uint32_t mx = 0;
+  for (uint64_t k = 1 + lane; k < d; k += 32) mx = max(mx, x.dst(s + k) - x.dst(s + k - 1));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFullMask, mx, o));
+  return bits_of(mx);
+}
+
+__host__ __device__ __forceinline__ uint64_t short_bits(uint64_t d, uint32_t w, uint32_t ww) {
+  return kCmpShortHdrBits + (d - 1) * w + d * ww;
+}
+
+// Size word of every list: 0 (empty), its bit length (short), or
+// kLongSize | lines (long).
+__global__ void k_cmp_size(uint64_t nv, const uint64_t* off, Elems x, uint32_t ww,
+                           uint32_t* size) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t v = gw; v < nv; v += nw) {
     const uint64_t s = off[v], d = off[v + 1] - s;
-    const uint64_t raw = d ? (s + d - 1) / kSectorElems - s / kSectorElems + 1 : 0;
-    uint32_t n = 0;
-    if (raw > kLineSectors) {
-      for (uint64_t p = 0; p < d && n * kLineSectors < raw; ++n) {
-        uint32_t cnt, w;
-        line_fill(e + s, d, p, lane, &cnt, &w);
-        p += cnt;
+    uint32_t out = 0;
+    if (d) {
+      const uint64_t sb = short_bits(d, list_width(x, s, d, lane), ww);
+      if (sb <= kLineBits && d <= kCmpShortMaxDeg) {  // one lane decodes a short list
+        out = static_cast<uint32_t>(sb);
+      } else {
+        uint32_t n = 0;
+        for (uint64_t p = 0; p < d; ++n) {
+          uint32_t cnt, w;
+          line_fill(x, s, d, p, ww, lane, &cnt, &w);
+          p += cnt;
+        }
+        out = kLongSize | n;
       }
-      if (n * kLineSectors >= raw) n = 0;
     }
-    if (lane == 0) lines[v] = n;
+    if (lane == 0) size[v] = out;
   }
 }
 
-// Encode: warp per compressed list, one shared-memory line buffer per warp.
-__global__ void __launch_bounds__(256) k_cmp_encode(uint64_t nv, const uint64_t* off,
-                                                    const uint32_t* e, const uint64_t* coff,
+// OR `nbits` (<= 32) of `val` into the bit stream at bit position `bit`.
+__device__ __forceinline__ void put_bits(uint32_t* out, uint64_t bit, uint32_t val,
+                                         uint32_t nbits) {
+  if (!nbits) return;
+  if (nbits < 32) val &= (1u << nbits) - 1;
+  const uint32_t sh = static_cast<uint32_t>(bit & 31);
+  atomicOr(out + (bit >> 5), val << sh);
+  if (sh + nbits > 32) atomicOr(out + (bit >> 5) + 1, val >> (32 - sh));
+}
+
+// Encode: warp per list.  Short lists OR their fields into shared lines;
+// long lists build each line in a shared-memory buffer and store it whole.
+__global__ void __launch_bounds__(256) k_cmp_encode(uint64_t nv, const uint64_t* off, Elems x,
+                                                    uint32_t ww, const uint64_t* cpos,
                                                     uint32_t* out) {
   __shared__ uint32_t buf[8][kLineWords + 2];
   const int lane = threadIdx.x & 31;
@@ -94,27 +140,48 @@ __global__ void __launch_bounds__(256) k_cmp_encode(uint64_t nv, const uint64_t*
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t v = gw; v < nv; v += nw) {
-    const uint64_t l0 = coff[v], nl = coff[v + 1] - l0;
-    if (!nl) continue;
     const uint64_t s = off[v], d = off[v + 1] - s;
-    const uint32_t* x = e + s;
+    if (!d) continue;
+    const uint64_t c = cpos[v], pos = cmp_pos(c);
+    if (!(c & kCmpLong)) {
+      const uint32_t w = list_width(x, s, d, lane);
+      if (lane == 0) {
+        put_bits(out, pos, w, 6);
+        put_bits(out, pos + 6, x.dst(s), 32);
+      }
+      const uint64_t wbase = pos + kCmpShortHdrBits + (d - 1) * w;
+      for (uint64_t k = lane; k < d; k += 32) {
+        if (k) put_bits(out, pos + kCmpShortHdrBits + (k - 1) * w, x.dst(s + k) - x.dst(s + k - 1), w);
+        put_bits(out, wbase + k * ww, x.wt(s + k), ww);
+      }
+      continue;
+    }
+    const uint64_t l0 = pos / kLineBits, nl = (cmp_pos(cpos[v + 1]) - pos) / kLineBits;
     uint64_t p = 0;
     for (uint64_t t = 0; t < nl; ++t) {
       uint32_t cnt, w;
-      line_fill(x, d, p, lane, &cnt, &w);
+      line_fill(x, s, d, p, ww, lane, &cnt, &w);
       L[lane] = 0;
       if (lane < 2) L[kLineWords + lane] = 0;
       __syncwarp();
-      if (w)
-        for (uint32_t k = lane + 1; k < cnt; k += 32) {
-          const uint32_t dl = x[p + k] - x[p + k - 1];
+      const uint32_t wb = kCmpHdrBits + (cnt - 1) * w;
+      for (uint32_t k = lane; k < cnt; k += 32) {
+        if (k && w) {
+          const uint32_t dl = x.dst(s + p + k) - x.dst(s + p + k - 1);
           const uint32_t bit = kCmpHdrBits + (k - 1) * w;
           atomicOr(&L[bit >> 5], dl << (bit & 31));
           if ((bit & 31) + w > 32) atomicOr(&L[(bit >> 5) + 1], dl >> (32 - (bit & 31)));
         }
+        if (ww) {
+          const uint32_t wv = x.wt(s + p + k) & (ww < 32 ? (1u << ww) - 1 : ~0u);
+          const uint32_t bit = wb + k * ww;
+          atomicOr(&L[bit >> 5], wv << (bit & 31));
+          if ((bit & 31) + ww > 32) atomicOr(&L[(bit >> 5) + 1], wv >> (32 - (bit & 31)));
+        }
+      }
       __syncwarp();
       if (lane == 0) {
-        L[0] = x[p];
+        L[0] = x.dst(s + p);
         L[1] |= w | ((cnt - 1) << 6);
       }
       __syncwarp();
@@ -122,6 +189,27 @@ __global__ void __launch_bounds__(256) k_cmp_encode(uint64_t nv, const uint64_t*
       __syncwarp();
       p += cnt;
     }
+  }
+}
+
+// (dst << 32 | weight) pair list of u32 edges + u32 weights; weight range.
+__global__ void k_cmp_pairs(uint64_t ne, const uint32_t* e, const uint32_t* w, uint64_t* out,
+                            unsigned* wmin, unsigned* wmax) {
+  unsigned lo = 0xffffffffu, hi = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    out[i] = (static_cast<uint64_t>(e[i]) << 32) | w[i];
+    lo = min(lo, w[i]);
+    hi = max(hi, w[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(kFullMask, lo, o));
+    hi = max(hi, __shfl_xor_sync(kFullMask, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(wmin, lo);
+    atomicMax(wmax, hi);
   }
 }
 
@@ -148,6 +236,8 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
   cudaSetDevice(g->device);
   ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
   const uint64_t nv = g->nv, ne = g->ne;
+  // weights ride along when they are 4-byte (SSSP on the compressed stream)
+  const bool weighted = g->has_weights && g->wb == 4 && g->h_weights;
   // device temporaries are released on every path; the handle is only
   // updated once the whole stream is built
   struct DevBuf {
@@ -158,28 +248,69 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
       p = nullptr;
       return q;
     }
-  } sorted, lines, tmp, enc, coff;
-  ZC_CUDA_TRY(cudaMalloc(&sorted.p, std::max<uint64_t>(ne, 1) * 4));
-  ZC_CUDA_TRY(cudaMemcpy(sorted.p, g->h_edges, ne * 4, cudaMemcpyDefault));
-  const int rc = sort_lists_device(4, nv, g->d_off, g->h_off, sorted.p);
-  if (rc) return rc;
-  ZC_CUDA_TRY(cudaMalloc(&coff.p, (nv + 1) * sizeof(uint64_t)));
-  ZC_CUDA_TRY(cudaMalloc(&lines.p, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
-  k_cmp_lines<<<kCmpGrid, 256>>>(nv, g->d_off, static_cast<uint32_t*>(sorted.p),
-                                 static_cast<uint32_t*>(lines.p));
+  } sorted, wtmp, size, enc, cpos, range;
+  Elems x{nullptr, nullptr, 0};
+  uint32_t ww = 0;
+  if (weighted) {
+    ZC_CUDA_TRY(cudaMalloc(&sorted.p, std::max<uint64_t>(ne, 1) * 8));
+    ZC_CUDA_TRY(cudaMalloc(&wtmp.p, std::max<uint64_t>(ne, 1) * 8));
+    ZC_CUDA_TRY(cudaMalloc(&range.p, 2 * sizeof(unsigned)));
+    const unsigned init[2] = {0xffffffffu, 0u};
+    ZC_CUDA_TRY(cudaMemcpy(range.p, init, sizeof(init), cudaMemcpyHostToDevice));
+    uint32_t* de = static_cast<uint32_t*>(wtmp.p);
+    uint32_t* dw = de + std::max<uint64_t>(ne, 1);
+    ZC_CUDA_TRY(cudaMemcpy(de, g->h_edges, ne * 4, cudaMemcpyDefault));
+    ZC_CUDA_TRY(cudaMemcpy(dw, g->h_weights, ne * 4, cudaMemcpyDefault));
+    unsigned* r = static_cast<unsigned*>(range.p);
+    k_cmp_pairs<<<kCmpGrid, 256>>>(ne, de, dw, static_cast<uint64_t*>(sorted.p), r, r + 1);
+    ZC_CUDA_TRY(cudaGetLastError());
+    unsigned hr[2];
+    ZC_CUDA_TRY(cudaMemcpy(hr, r, sizeof(hr), cudaMemcpyDeviceToHost));
+    cudaFree(wtmp.release());
+    if (!ne) hr[0] = hr[1] = 0;
+    x.e64 = static_cast<const uint64_t*>(sorted.p);
+    x.wmin = hr[0];
+    ww = hr[1] > hr[0] ? 32 - __builtin_clz(hr[1] - hr[0]) : 0;
+    const int rc = sort_lists_device(8, nv, g->d_off, g->h_off, sorted.p);
+    if (rc) return rc;
+  } else {
+    ZC_CUDA_TRY(cudaMalloc(&sorted.p, std::max<uint64_t>(ne, 1) * 4));
+    ZC_CUDA_TRY(cudaMemcpy(sorted.p, g->h_edges, ne * 4, cudaMemcpyDefault));
+    const int rc = sort_lists_device(4, nv, g->d_off, g->h_off, sorted.p);
+    if (rc) return rc;
+    x.e32 = static_cast<const uint32_t*>(sorted.p);
+  }
+  // sizes, then the placement scan on the host (a sequential first-fit)
+  ZC_CUDA_TRY(cudaMalloc(&size.p, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
+  k_cmp_size<<<kCmpGrid, 256>>>(nv, g->d_off, x, ww, static_cast<uint32_t*>(size.p));
   ZC_CUDA_TRY(cudaGetLastError());
-  const size_t tb = scan_tmp_bytes(nv);
-  ZC_CUDA_TRY(cudaMalloc(&tmp.p, tb));
-  ZC_CUDA_TRY(scan_u32_to_u64(static_cast<uint32_t*>(lines.p), static_cast<uint64_t*>(coff.p), nv,
-                              tmp.p, tb, 0));
-  uint64_t total = 0;
-  ZC_CUDA_TRY(cudaMemcpy(&total, static_cast<uint64_t*>(coff.p) + nv, sizeof(total),
-                         cudaMemcpyDeviceToHost));
-  const size_t bytes = std::max<uint64_t>(total, 1) * kLineBytes;
+  std::vector<uint32_t> hs(nv);
+  std::vector<uint64_t> hp(nv + 1);
+  ZC_CUDA_TRY(cudaMemcpy(hs.data(), size.p, nv * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  cudaFree(size.release());
+  uint64_t pos = 0;
+  auto round_line = [](uint64_t b) { return (b + kLineBits - 1) / kLineBits * kLineBits; };
+  for (uint64_t v = 0; v < nv; ++v) {
+    const uint32_t sz = hs[v];
+    if (sz & kLongSize) {
+      pos = round_line(pos);
+      hp[v] = pos | kCmpLong;
+      pos += static_cast<uint64_t>(sz & ~kLongSize) * kLineBits;
+    } else {
+      if (sz && (pos % kLineBits) + sz > kLineBits) pos = round_line(pos);
+      hp[v] = pos;
+      pos += sz;
+    }
+  }
+  hp[nv] = round_line(pos);
+  const uint64_t lines = hp[nv] / kLineBits;
+  ZC_CUDA_TRY(cudaMalloc(&cpos.p, (nv + 1) * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMemcpy(cpos.p, hp.data(), (nv + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  const size_t bytes = std::max<uint64_t>(lines, 1) * kLineBytes;
   ZC_CUDA_TRY(cudaMalloc(&enc.p, bytes));
   ZC_CUDA_TRY(cudaMemset(enc.p, 0, bytes));
-  k_cmp_encode<<<kCmpGrid, 256>>>(nv, g->d_off, static_cast<uint32_t*>(sorted.p),
-                                  static_cast<uint64_t*>(coff.p), static_cast<uint32_t*>(enc.p));
+  k_cmp_encode<<<kCmpGrid, 256>>>(nv, g->d_off, x, ww, static_cast<uint64_t*>(cpos.p),
+                                  static_cast<uint32_t*>(enc.p));
   ZC_CUDA_TRY(cudaDeviceSynchronize());
   // place the stream like the lists
   void* host = nullptr;
@@ -217,23 +348,26 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
   g->h_cmp = host;
   g->d_cmp = dev;
   g->hbm_cmp = hbm;
-  g->d_coff = static_cast<uint64_t*>(coff.release());
-  g->cmp_bytes = total * kLineBytes;
+  g->d_cpos = static_cast<uint64_t*>(cpos.release());
+  g->cmp_bytes = bytes;
+  g->cmp_weighted = weighted;
+  g->cmp_ww = ww;
+  g->cmp_wmin = x.wmin;
   if (compressed_bytes) *compressed_bytes = g->cmp_bytes;
   return ZC_OK;
 }
 
-extern "C" int zc_graph_compressed_index(const zc_graph* g, uint64_t* first_line) {
-  if (!g || !g->d_coff) {
+extern "C" int zc_graph_compressed_index(const zc_graph* g, uint64_t* cpos) {
+  if (!g || !g->d_cpos) {
     set_error(g ? "compressed lists not built" : "null graph handle");
     return ZC_ESTATE;
   }
-  if (!first_line) {
+  if (!cpos) {
     set_error("null output buffer");
     return ZC_EINVAL;
   }
   cudaSetDevice(g->device);
-  ZC_CUDA_TRY(cudaMemcpy(first_line, g->d_coff, (g->nv + 1) * sizeof(uint64_t),
+  ZC_CUDA_TRY(cudaMemcpy(cpos, g->d_cpos, (g->nv + 1) * sizeof(uint64_t),
                          cudaMemcpyDeviceToHost));
   return ZC_OK;
 }

@@ -39,12 +39,14 @@ struct zc_graph {
   const void* d_weights = nullptr;
   void* hbm_edges = nullptr;
   void* hbm_weights = nullptr;
-  // optional delta-compressed lists (zc_graph_build_compressed)
+  // optional compressed line stream (zc_graph_build_compressed)
   void* h_cmp = nullptr;
   const void* d_cmp = nullptr;
   void* hbm_cmp = nullptr;
-  uint64_t* d_coff = nullptr;
+  uint64_t* d_cpos = nullptr;  // per-vertex bit position (| kCmpLong), V+1
   uint64_t cmp_bytes = 0;
+  uint32_t cmp_ww = 0, cmp_wmin = 0;  // weight field width / offset (0: unweighted)
+  bool cmp_weighted = false;
   // optional interleaved (dst, weight) u32 pairs for SSSP (zc_graph_build_pairs)
   void* h_pairs = nullptr;
   const void* d_pairs = nullptr;

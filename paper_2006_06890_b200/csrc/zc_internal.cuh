@@ -46,17 +46,28 @@ constexpr uint32_t kExchNone32 = 0x7fffffffu;
 constexpr uint32_t kBigSteps = 16;
 
 enum Strategy : int { kNaive = 0, kMerged = 1, kMergedAligned = 2, kPacked = 3, kCompressed = 4 };
-// kCompressed (B200 host-store option, zc_compress.cu): every list whose
-// compressed form needs fewer 128-byte lines than its raw form touches is
-// stored as self-describing compressed lines; the other lists are read raw
-// with packed windows.  A compressed line (32 u32 words, 128-byte aligned):
-//   word 0        base = first element
-//   word 1 [0,6)  w = delta width in bits (0..32); [6,14) count - 1 (<= 255)
-//   bit 48 + (k-1) w, k = 1..count-1: delta k = elem[k] - elem[k-1] (sorted)
-// Window = one line: one fully-used, aligned PCIe read per warp request.
+// kCompressed (B200 host-store option, zc_compress.cu): every list is stored
+// sorted and delta-encoded in a stream of 128-byte lines, in vertex order.
+//   short list (encoding <= 1024 bits, <= 64 elements): packed with its
+//     neighbours into a
+//     shared line, never straddling one -- 6-bit delta width w, 32-bit first
+//     element, d-1 deltas of w bits, then (weighted) d weights of ww bits
+//     (weight - wmin);
+//   long list: whole self-describing lines -- word 0 base, word 1 [0,6) w,
+//     [6,14) count - 1 (<= 255); from bit 48: count-1 deltas of w bits, then
+//     (weighted) count weights of ww bits.
+// Per-vertex cpos (u64[V+1], HBM): bit position of the list in the stream,
+// kCmpLong set for long lists (their lines end where the next list starts).
+// A window is one line: a long list's lines, or a shared line of short lists
+// fetched once for all its frontier lists.
 constexpr uint32_t kCmpHdrBits = 48;
+constexpr uint32_t kCmpShortHdrBits = 38;
 constexpr uint32_t kCmpMaxCount = 256;
 constexpr uint32_t kLineWords = 32;
+constexpr uint32_t kLineBits = 1024;
+constexpr uint32_t kCmpShortMaxDeg = 64;
+constexpr uint64_t kCmpLong = 1ull << 63;
+__host__ __device__ __forceinline__ uint64_t cmp_pos(uint64_t c) { return c & ~kCmpLong; }
 // kPacked (B200 extension, not one of the paper's three): a window is an
 // aligned 32-element block touched by any frontier list, fetched once for all
 // the lists that share it (see k_window_counts / k_expand_sweep).
@@ -129,10 +140,12 @@ struct ExpandArgs {
   // memory (then `n` is only the maximum, used to size grids)
   const uint64_t* n_dev;
   const uint64_t* iter_dev;
-  // compressed lists (kCompressed): the line stream and each vertex's first
-  // line (coff[v+1] - coff[v] lines; 0 = the list is read raw)
+  // compressed lists (kCompressed): the line stream, each vertex's bit
+  // position (kCmpLong: whole lines), the weight field width and offset
   const uint32_t* cmp;
-  const uint64_t* coff;
+  const uint64_t* cpos;
+  uint32_t cmp_ww;
+  uint32_t cmp_wmin;
 };
 
 // ZC_TUNE="unroll=8,ctas=6,sched=chunk": expansion tuning knobs for experiments.

@@ -190,7 +190,7 @@ struct LineElems {
 template <int STRAT, typename ET>
 __device__ __forceinline__ uint64_t window_base(uint64_t s) {
   if (STRAT == kMergedAligned) return s & ~(LineElems<ET>::value - 1);
-  if (STRAT == kPacked || STRAT == kCompressed) return s & ~static_cast<uint64_t>(kWarp - 1);
+  if (STRAT == kPacked) return s & ~static_cast<uint64_t>(kWarp - 1);
   return s;
 }
 
@@ -203,7 +203,10 @@ struct Batch {
   WT wt[U];
   uint64_t sval[U];
   bool ok[U];
-  bool line[U];  // kCompressed: window u is a compressed line (warp-uniform)
+  // kCompressed (warp-uniform): window u is 1 = a long-list line, 2 = a shared
+  // line of the staged short lists [k0, k1)
+  uint8_t line[U];
+  int16_t k0[U], k1[U];
 };
 
 template <int ALGO, typename ET, typename WT, int U>
@@ -405,14 +408,9 @@ constexpr int kStage = 256;  // frontier slots staged in shared memory at a time
 // first block when the nearest earlier non-empty slot of the same aligned
 // group of kStage slots (one shared-memory stage of the sweep) already
 // touches it -- so every block is fetched once per group and the lists that
-// share it are always staged together.  Compressed: a compressed list's
-// windows are its lines; the other lists count as packed, sharing only with
-// raw lists.
-__device__ __forceinline__ uint64_t cmp_lines(const ExpandArgs& a, uint64_t j) {
-  const uint32_t v = a.front[j];
-  return a.coff[v + 1] - a.coff[v];
-}
-
+// share it are always staged together.  Compressed: a long list's windows
+// are its lines; a short list's line is one window unless the nearest earlier
+// non-empty slot of the group has its list in the same line.
 template <int STRAT, typename ET>
 __global__ void k_window_counts(ExpandArgs a) {
   const uint64_t n = a.n_dev ? *a.n_dev : a.n;
@@ -423,19 +421,29 @@ __global__ void k_window_counts(ExpandArgs a) {
       a.wcnt[j] = 0;
       continue;
     }
+    const uint64_t group0 = j - j % kStage;
     if (STRAT == kCompressed) {
-      const uint64_t nl = cmp_lines(a, j);
-      if (nl) {
-        a.wcnt[j] = static_cast<uint32_t>(nl);
+      const uint32_t v = a.front[j];
+      const uint64_t c = a.cpos[v];
+      if (c & kCmpLong) {
+        a.wcnt[j] = static_cast<uint32_t>((cmp_pos(a.cpos[v + 1]) - cmp_pos(c)) / kLineBits);
         continue;
       }
+      uint32_t w = 1;
+      for (uint64_t i = j; i > group0; --i) {
+        if (!a.fd[i - 1]) continue;
+        const uint64_t ci = a.cpos[a.front[i - 1]];
+        w = (ci & kCmpLong) || cmp_pos(ci) / kLineBits != cmp_pos(c) / kLineBits;
+        break;
+      }
+      a.wcnt[j] = w;
+      continue;
     }
     uint64_t w = (s + d - window_base<STRAT, ET>(s) + kWarp - 1) / kWarp;
-    if (STRAT == kPacked || STRAT == kCompressed) {
-      const uint64_t group0 = j - j % kStage;
+    if (STRAT == kPacked) {
       for (uint64_t i = j; i > group0; --i) {
         const uint32_t di = a.fd[i - 1];
-        if (!di || (STRAT == kCompressed && cmp_lines(a, i - 1))) continue;
+        if (!di) continue;
         w -= ((a.fs[i - 1] + di - 1) / kWarp) == (s / kWarp);
         break;
       }
@@ -444,7 +452,14 @@ __global__ void k_window_counts(ExpandArgs a) {
   }
 }
 
-// Decode one compressed line (this lane's word in x) and visit its elements:
+// `nbits` (<= 32) of the staged line L at bit position `bit` (< 1024).
+__device__ __forceinline__ uint32_t line_bits(const uint32_t* L, uint32_t bit, uint32_t nbits) {
+  const uint64_t pair = (static_cast<uint64_t>(L[(bit >> 5) + 1]) << 32) | L[bit >> 5];
+  return static_cast<uint32_t>((pair >> (bit & 31)) & (nbits >= 32 ? 0xffffffffull
+                                                                    : ((1ull << nbits) - 1)));
+}
+
+// Decode one long-list line (this lane's word in x) and visit its elements:
 // lane l takes elements [l m, l m + m), m = ceil(count / 32); values are the
 // base plus a warp prefix sum of the deltas (u32 exact: ids < 2^32).
 template <int ALGO>
@@ -457,17 +472,9 @@ __device__ __forceinline__ void visit_line(const ExpandArgs& a, uint32_t x, uint
   const uint32_t w = hdr & 63, cnt = ((hdr >> 6) & 255) + 1;
   const uint32_t m = (cnt + 31) >> 5;
   const uint32_t e0 = lane * m, e1 = min(cnt, e0 + m);
-  const uint64_t mask = w >= 32 ? 0xffffffffull : ((1ull << w) - 1);
   uint32_t run = 0;
-  for (uint32_t e = e0; e < e1; ++e) {
-    if (e == 0) {
-      run += L[0];
-    } else {
-      const uint32_t bit = kCmpHdrBits + (e - 1) * w;
-      const uint64_t pair = (static_cast<uint64_t>(L[(bit >> 5) + 1]) << 32) | L[bit >> 5];
-      run += static_cast<uint32_t>((pair >> (bit & 31)) & mask);
-    }
-  }
+  for (uint32_t e = e0; e < e1; ++e)
+    run += e == 0 ? L[0] : line_bits(L, kCmpHdrBits + (e - 1) * w, w);
   uint32_t incl = run;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -475,15 +482,42 @@ __device__ __forceinline__ void visit_line(const ExpandArgs& a, uint32_t x, uint
     if (lane >= o) incl += t;
   }
   uint32_t val = incl - run;
+  const uint32_t wb = kCmpHdrBits + (cnt - 1) * w;
   for (uint32_t e = e0; e < e1; ++e) {
-    if (e == 0) {
-      val += L[0];
-    } else {
-      const uint32_t bit = kCmpHdrBits + (e - 1) * w;
-      const uint64_t pair = (static_cast<uint64_t>(L[(bit >> 5) + 1]) << 32) | L[bit >> 5];
-      val += static_cast<uint32_t>((pair >> (bit & 31)) & mask);
+    val += e == 0 ? L[0] : line_bits(L, kCmpHdrBits + (e - 1) * w, w);
+    uint64_t wt = 0;
+    if constexpr (AlgoTraits<ALGO>::weighted) wt = a.cmp_wmin + line_bits(L, wb + e * a.cmp_ww, a.cmp_ww);
+    Visit<ALGO>::apply(a, val, wt, sval);
+  }
+  __syncwarp();
+}
+
+// Decode the short lists of staged slots [k0, k1) from their shared line
+// (this lane's word in x): a lane per list, elements in order.  Every slot
+// in [k0, k1) is in the frontier; empty lists take no bits, so there can be
+// more than 32 of them.
+template <int ALGO>
+__device__ __forceinline__ void visit_short(const ExpandArgs& a, uint32_t x, int k0, int k1,
+                                            const uint64_t* sh_c, const uint64_t* sh_s,
+                                            const uint64_t* sh_e, const uint64_t* sh_v,
+                                            uint32_t* L, int lane) {
+  L[lane] = x;
+  if (lane < 2) L[kLineWords + lane] = 0;
+  __syncwarp();
+  // more than 32 staged slots can share a line when empty lists sit between
+  for (int i = k0 + lane; i < k1; i += 32) {
+    const uint32_t d = static_cast<uint32_t>(sh_e[i] - sh_s[i]);
+    const uint32_t p = static_cast<uint32_t>(cmp_pos(sh_c[i]) % kLineBits);
+    const uint64_t sval = AlgoTraits<ALGO>::has_val ? sh_v[i] : 0;
+    const uint32_t w = d ? line_bits(L, p, 6) : 0;
+    uint32_t val = d ? line_bits(L, p + 6, 32) : 0;
+    const uint32_t wb = p + kCmpShortHdrBits + (d - 1) * w;
+    for (uint32_t e = 0; e < d; ++e) {
+      if (e) val += line_bits(L, p + kCmpShortHdrBits + (e - 1) * w, w);
+      uint64_t wt = 0;
+      if constexpr (AlgoTraits<ALGO>::weighted) wt = a.cmp_wmin + line_bits(L, wb + e * a.cmp_ww, a.cmp_ww);
+      Visit<ALGO>::apply(a, val, wt, sval);
     }
-    Visit<ALGO>::apply(a, val, 0, sval);
   }
   __syncwarp();
 }
@@ -497,7 +531,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
   constexpr bool kCmp = STRAT == kCompressed;
   __shared__ uint64_t sh_s[kStage], sh_e[kStage], sh_v[kStage];
   __shared__ uint64_t sh_w[kStage + 1];
-  __shared__ uint64_t sh_c[kCmp ? kStage : 1];                // first line, or ~0 (raw)
+  __shared__ uint64_t sh_c[kCmp ? kStage : 1];  // list position (| kCmpLong)
+  __shared__ uint64_t sh_n[kCmp ? kStage : 1];  // next vertex's position (list end bound)
   __shared__ uint32_t sh_line[kCmp ? kSweepWarps : 1][kLineWords + 2];  // decode buffer
   __shared__ uint64_t sh_j;
   const uint64_t n = a.n;
@@ -539,13 +574,9 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
         sh_e[i] = s0 + a.fd[jj];
         if (AlgoTraits<ALGO>::has_val) sh_v[i] = a.fval[jj];
         if constexpr (kCmp) {
-          // a compressed list keeps an empty raw range (the owner search
-          // over sh_s stays monotone and never matches it)
           const uint32_t v = a.front[jj];
-          const uint64_t c0 = a.coff[v];
-          const bool c = a.coff[v + 1] != c0;
-          sh_c[i] = c ? c0 : ~0ull;
-          if (c) sh_e[i] = s0;
+          sh_c[i] = a.cpos[v];
+          sh_n[i] = cmp_pos(a.cpos[v + 1]);
         }
       }
     }
@@ -560,7 +591,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
         const uint64_t q = q0 + u;
         bt.ok[u] = false;
         bt.sval[u] = 0;
-        if constexpr (kCmp) bt.line[u] = false;
+        if constexpr (kCmp) bt.line[u] = 0;
         if (q < Wend) {  // warp-uniform
           if (u == 0) {  // binary search for the batch head, then walk
             int lo = 0, hi = kStage;  // sh_w[lo] <= q < sh_w[hi]
@@ -575,14 +606,27 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
           const uint64_t s0 = sh_s[k], e0 = sh_e[k];
           uint64_t idx;
           if constexpr (kCmp) {
-            bt.line[u] = sh_c[k] != ~0ull;
-            if (bt.line[u]) {  // one aligned compressed line, a word per lane
+            const uint64_t c = sh_c[k];
+            if (c & kCmpLong) {  // line t of a long list: a word per lane
+              bt.line[u] = 1;
               if (AlgoTraits<ALGO>::has_val) bt.sval[u] = sh_v[k];
-              bt.dst[u] = ld_list(a.cmp + (sh_c[k] + (q - sh_w[k])) * kLineWords + lane);
-              continue;
+              const uint64_t line = cmp_pos(c) / kLineBits + (q - sh_w[k]);
+              bt.dst[u] = ld_list(a.cmp + line * kLineWords + lane);
+            } else {  // a shared line: the words of its staged frontier lists
+              bt.line[u] = 2;
+              const uint64_t L = cmp_pos(c) / kLineBits;
+              int m = k + 1;
+              while (m < stage_n && !(sh_c[m] & kCmpLong) && cmp_pos(sh_c[m]) / kLineBits == L) ++m;
+              const uint32_t w0 = static_cast<uint32_t>(cmp_pos(c) % kLineBits) / 32;
+              const uint64_t endb = min(sh_n[m - 1], (L + 1) * kLineBits);
+              const uint32_t w1 = static_cast<uint32_t>(endb - 1 - L * kLineBits) / 32;
+              bt.k0[u] = static_cast<int16_t>(k);
+              bt.k1[u] = static_cast<int16_t>(m);
+              bt.dst[u] = lane >= w0 && lane <= w1 ? ld_list(a.cmp + L * kLineWords + lane) : 0u;
             }
+            continue;
           }
-          if (STRAT == kPacked || kCmp) {
+          if (STRAT == kPacked) {
             // block t of slot k's new blocks; the lane's element may belong to
             // any staged list that shares the block: search its owner
             const uint64_t fb = s0 / kWarp;
@@ -618,12 +662,13 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
         if (qn < Wend) issue(nxt, qn);
         if constexpr (kCmp) {
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (cur.line[u])  // warp-uniform
+          for (int u = 0; u < U; ++u) {  // line kinds are warp-uniform
+            if (cur.line[u] == 1)
               visit_line<ALGO>(a, static_cast<uint32_t>(cur.dst[u]), cur.sval[u], sh_line[warp],
                                lane);
-            else if (cur.ok[u])
-              Visit<ALGO>::apply(a, cur.dst[u], 0, cur.sval[u]);
+            else if (cur.line[u] == 2)
+              visit_short<ALGO>(a, static_cast<uint32_t>(cur.dst[u]), cur.k0[u], cur.k1[u], sh_c,
+                                sh_s, sh_e, sh_v, sh_line[warp], lane);
           }
         } else {
           visit_batch<ALGO, ET, WT, U>(a, cur);
@@ -1384,11 +1429,13 @@ cudaError_t launch_expand(int strategy, int algo, int edge_bytes, int weight_byt
   if (strategy == kCompressed) {
     switch (algo) {
       case kBfs: return expand_cmp<kBfs>(a, num_sms, st, launches);
+      case kSssp: return expand_cmp<kSssp>(a, num_sms, st, launches);
       case kCc: return expand_cmp<kCc>(a, num_sms, st, launches);
       case kPr: return expand_cmp<kPr>(a, num_sms, st, launches);
       case kBfs + kPartAlgo: return expand_cmp<kBfs + kPartAlgo>(a, num_sms, st, launches);
+      case kSssp + kPartAlgo: return expand_cmp<kSssp + kPartAlgo>(a, num_sms, st, launches);
       case kCc + kPartAlgo: return expand_cmp<kCc + kPartAlgo>(a, num_sms, st, launches);
-      default: return cudaErrorInvalidValue;  // sssp: no weights in the compressed stream
+      default: return cudaErrorInvalidValue;
     }
   }
   switch (strategy) {

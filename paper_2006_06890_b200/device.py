@@ -207,24 +207,21 @@ class DeviceGraph:
         return nbytes.value
 
     def compressed_index(self) -> np.ndarray:
-        """First compressed line of every vertex (V+1 u64): vertex v's list is
-        lines [idx[v], idx[v+1]) of the stream, none = read raw."""
+        """Bit position of every vertex's list in the compressed line stream
+        (V+1 u64; bit 63 set: a long list stored as whole lines)."""
         out = np.empty(self.num_vertices + 1, np.uint64)
         N.check(N.lib().zc_graph_compressed_index(self.handle, out.ctypes.data))
         return out
 
-    def link_bytes(self, expanded: np.ndarray, strategy: str = "compressed") -> int:
-        """Bytes of list data the expansion of the vertex set `expanded` (bool
-        mask or ids) must read over the link: 4 B (edge width) per raw-list
-        edge, 128 B per compressed line (strategy "compressed")."""
-        g = self.as_csr()
-        deg = np.diff(g.offsets)[expanded]
+    def stored_list_bytes(self, strategy: str = "compressed") -> np.ndarray:
+        """Bytes each vertex's list occupies in the stream a strategy reads:
+        edge width x degree for the raw lists (+ weight width x degree when
+        `weights`), the list's span of the compressed line stream (its lines,
+        or its share of a shared line including padding) for "compressed"."""
         if strategy != "compressed":
-            return int(deg.sum()) * self.edge_elem_bytes
-        idx = self.compressed_index()
-        lines = (idx[1:] - idx[:-1])[expanded]
-        raw = lines == 0
-        return int(deg[raw].sum()) * self.edge_elem_bytes + int(lines.sum()) * 128
+            return np.diff(self.as_csr().offsets).astype(np.int64) * self.edge_elem_bytes
+        pos = (self.compressed_index() & np.uint64((1 << 63) - 1)).astype(np.int64)
+        return np.diff(pos) // 8
 
     def expand_profile(self, iterations: int) -> np.ndarray:
         """Per-iteration device time (ms) of the expansion kernels of the last run."""

@@ -375,21 +375,22 @@ def test_device_loop_hands_off_past_log_capacity():
 
 
 def test_compressed_lists_match_reference():
-    """Delta-compressed list stream: BFS / CC identical on every fixture graph
-    (values, iterations, traversed edges); SSSP is rejected."""
+    """Compressed line stream: BFS / SSSP / CC identical on every fixture graph
+    with 4-byte elements (values, iterations, traversed edges); 8-byte
+    elements are rejected."""
     bad = []
     for c in CASES:
-        if c.algo == "sssp" or c.graph.edge_elem_bytes != 4:
+        if c.graph.edge_elem_bytes != 4 or (c.algo == "sssp" and c.graph.weight_elem_bytes != 4):
             continue
-        r = zc.cc(c.graph, "compressed", collect_traffic=False) if c.algo == "cc" else \
-            zc.bfs(c.graph, c.source, "compressed", collect_traffic=False)
+        r = _run(c, "compressed")
         if not (np.array_equal(r.values, c.values) and r.iterations == c.iterations
                 and r.traversed_edges == c.traversed):
             bad.append((c.index, c.tag))
     assert not bad, bad[:8]
-    g = zc.with_uniform_weights(zc.generate_uniform(500, 1, 9, seed=2))
-    with pytest.raises(ValueError, match="compressed"):
-        zc.sssp(g, 0, "compressed", collect_traffic=False)
+    e8 = [c for c in CASES if c.graph.edge_elem_bytes == 8]
+    if e8:
+        with pytest.raises(ValueError, match="compressed"):
+            _run(e8[0], "compressed")
 
 
 def test_compressed_rmat_and_pagerank():
@@ -470,22 +471,35 @@ def _crafted_long_lists(seed=3):
 
 
 def test_compressed_lines_crafted_lists():
-    """Compressed lines (widths 0..~20, the 256-element cap, lists either side
-    of the threshold, unsorted input lists): BFS from several sources and
-    PageRank equal the oracle; the index marks only long lists compressed."""
+    """Compressed lines (widths 0..~20, the 256-element line cap, short lists
+    sharing lines, long lists, unsorted input lists): BFS, SSSP and CC equal
+    the oracle; the index keeps long lists on whole lines and short lists
+    inside one line."""
     g = _crafted_long_lists()
     dg = zc.DeviceGraph(g)
     nbytes = dg.build_compressed()
-    idx = dg.compressed_index().astype(np.int64)
-    lines = idx[1:] - idx[:-1]
+    idx = dg.compressed_index()
+    long_ = (idx[:-1] >> np.uint64(63)).astype(bool)
+    pos = (idx & np.uint64((1 << 63) - 1)).astype(np.int64)
+    span = np.diff(pos)
     deg = np.diff(g.offsets)
-    assert nbytes == int(lines.sum()) * 128 and lines.sum() > 0
-    assert (deg[lines > 0] > 24).all() and (lines[deg <= 24] == 0).all()
-    assert (lines[deg > 0] <= (deg[deg > 0] + 31) // 32 + 1).all()
+    assert nbytes == pos[-1] // 8 and pos[-1] % 1024 == 0 and (span >= 0).all()
+    assert long_.any() and (~long_ & (deg > 0)).any()
+    assert (pos[:-1][long_] % 1024 == 0).all() and (span[long_] % 1024 == 0).all()
+    assert (deg[long_] > 1).all() and (span[deg == 0] <= 1024).all()
+    short = ~long_ & (deg > 0)
+    # a short list never straddles a line
+    assert ((pos[:-1][short] % 1024) + 38 <= 1024).all()
+    assert (span[long_] // 1024 <= (deg[long_] + 31) // 32 + 1).all()
     for src in (0, 1, 9, 12, 33, 4095):
         r = zc.bfs(dg, src, "compressed", collect_traffic=False)
         ref = oracle.bfs(g, src)
         assert np.array_equal(r.values, ref.values) and r.traversed_edges == ref.traversed_edges
+    gw = zc.with_uniform_weights(g)
+    for src in (1, 33):
+        r = zc.sssp(gw, src, "compressed", collect_traffic=False)
+        ref = oracle.sssp(gw, src)
+        assert np.array_equal(r.values, ref.values) and r.iterations == ref.iterations
     gu = zc.symmetrized(g)
     r = zc.cc(gu, "compressed", collect_traffic=False)
     assert np.array_equal(r.values, oracle.cc(gu).values)
@@ -496,11 +510,11 @@ def test_compressed_lines_crafted_lists():
 def test_cuda_partitions_compressed(fused):
     """Compressed lines inside partitions (local lists, global destinations),
     both exchanges: identical to the whole-graph reference."""
-    g = zc.generate_powerlaw(1 << 15, 24, seed=4)
+    g = zc.with_uniform_weights(zc.generate_powerlaw(1 << 15, 24, seed=4))
     gu = zc.symmetrized(g)
-    for algo, graph in (("bfs", g), ("cc", gu)):
+    for algo, graph in (("bfs", g), ("sssp", g), ("cc", gu)):
         src = int(zc.pick_sources(graph, 1, seed=7)[0])
-        ref = oracle.run(algo, graph, src) if algo == "bfs" else oracle.cc(graph)
+        ref = oracle.run(algo, graph, src) if algo != "cc" else oracle.cc(graph)
         for nparts in (2, 3):
             b = edge_balanced_bounds(graph.offsets, nparts)
             engines = [CudaPartition(local_part(graph, b, k), b, k) for k in range(nparts)]
@@ -510,3 +524,27 @@ def test_cuda_partitions_compressed(fused):
             assert iters == ref.iterations and trav == ref.traversed_edges
             for e in engines:
                 e.close()
+
+
+def test_compressed_shared_lines_with_many_empty_lists():
+    """Short lists separated by runs of empty lists: a shared line then holds
+    far more than 32 frontier slots (CC puts every vertex in the frontier)."""
+    nv = 20000
+    src = np.arange(0, nv - 1, 37)
+    dst = src + 1
+    g = zc.with_uniform_weights(zc.symmetrized(_from_edges(nv, src, dst)))
+    for algo in ("bfs", "sssp", "cc"):
+        s0 = int(src[3])
+        r = zc.cc(g, "compressed", collect_traffic=False) if algo == "cc" else \
+            getattr(zc, algo)(g, s0, "compressed", collect_traffic=False)
+        ref = oracle.cc(g) if algo == "cc" else oracle.run(algo, g, s0)
+        assert np.array_equal(r.values, ref.values), algo
+        assert r.iterations == ref.iterations and r.traversed_edges == ref.traversed_edges
+
+
+def _from_edges(nv, src, dst):
+    order = np.lexsort((dst, src))
+    src, dst = src[order], dst[order]
+    off = np.zeros(nv + 1, np.int64)
+    np.add.at(off, src + 1, 1)
+    return zc.CsrGraph(nv, len(dst), np.cumsum(off), dst.astype(np.int64), None, 4, 4, True)
