@@ -221,9 +221,11 @@ def main():
                           "pinned host memory (zero-copy)",
               "graph": f"kron{args.scale}", "scale": args.scale, "edge_factor": args.edge_factor,
               "seed": args.seed + rank, "strategy": args.strategy, "placement": "zerocopy",
-              "list_store": ("raw u32 lists; lists that read fewer 32 B sectors compressed are "
-                             "also stored as 128 B delta lines (B200 host-store extension)"
-                             if args.strategy == "compressed" else "raw u32 lists"),
+              "list_store": ("compressed line stream in pinned host memory (B200 host-store "
+                             "extension): every list sorted and delta-encoded in 128 B lines, "
+                             "hub lists on whole lines, short lists sharing lines; the raw u32 "
+                             "lists stay beside it" if args.strategy == "compressed"
+                             else "raw u32 lists"),
               "sources": "pick_sources(g, 64, seed=7)",
               "l2": "inputs larger than L2 (8 GiB edge list in host memory, 512 MiB level "
                     "array)",
