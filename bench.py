@@ -205,11 +205,16 @@ def cpu_baseline(g, sources, threads: int, budget_s: float = 25.0, check=None) -
 
 def main():
     args = parse()
-    rank, world, local = dist_setup(args)
+    if args.impl == "reference":
+        # the CPU reference arm runs on rank 0 only, without a process group
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        rank, world = 0, int(os.environ.get("WORLD_SIZE", "1"))
+        local = max(args.device_override, 0)
+    else:
+        rank, world, local = dist_setup(args)
     import numpy as np
 
-    if args.impl == "reference" and world > 1 and rank != 0:
-        return  # the CPU reference arm runs on rank 0 only
     import paper_2006_06890_b200 as zc
     import torch
 
