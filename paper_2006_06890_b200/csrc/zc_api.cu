@@ -15,7 +15,10 @@
 #include <string.h>
 
 #include <dirent.h>
+#include <dlfcn.h>
+#include <execinfo.h>
 #include <fcntl.h>
+#include <signal.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
 #include <sys/syscall.h>
@@ -216,6 +219,32 @@ void pinned_list_free(void* p) {
   } else {
     cudaFreeHost(p);
   }
+}
+
+// Debug aid (ZC_SEGV_TRACE=1): on SIGSEGV print the native frames with their
+// offsets inside the shared objects, for addr2line.
+static void segv_trace(int sig) {
+  void* fr[64];
+  const int n = backtrace(fr, 64);
+  for (int i = 0; i < n; ++i) {
+    Dl_info info;
+    char line[512];
+    int len;
+    if (dladdr(fr[i], &info) && info.dli_fname)
+      len = snprintf(line, sizeof(line), "zc-segv #%d %s+0x%lx\n", i, info.dli_fname,
+                     static_cast<unsigned long>(static_cast<char*>(fr[i]) -
+                                                static_cast<char*>(info.dli_fbase)));
+    else
+      len = snprintf(line, sizeof(line), "zc-segv #%d %p\n", i, fr[i]);
+    if (len > 0) (void)!write(2, line, static_cast<size_t>(len));
+  }
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+
+__attribute__((constructor)) static void install_segv_trace() {
+  const char* e = getenv("ZC_SEGV_TRACE");
+  if (e && e[0] == '1') signal(SIGSEGV, segv_trace);
 }
 
 static double now_ms() {

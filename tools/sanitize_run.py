@@ -9,8 +9,8 @@ from paper_2006_06890_b200.multi import (CudaPartition, edge_balanced_bounds, lo
 g = zc.with_uniform_weights(zc.generate_powerlaw(3000, 12.0, 2.0, seed=2))
 gu = zc.symmetrized(g)
 src = int(zc.pick_sources(g, 1)[0])
-for s in ["naive", "merged", "merged-aligned", "packed"]:
-    zc.bfs(g, src, s, collect_traffic=s != "packed")
+for s in ["naive", "merged", "merged-aligned", "packed", "compressed"]:
+    zc.bfs(g, src, s, collect_traffic=s not in ("packed", "compressed"))
     zc.sssp(g, src, s, collect_traffic=False)
     zc.cc(gu, s, collect_traffic=False)
     zc.pagerank(gu, s, collect_traffic=False, max_iters=5)
@@ -21,6 +21,12 @@ b = edge_balanced_bounds(g.offsets, 2)
 parts = [CudaPartition(local_part(g, b, k), b, k) for k in range(2)]
 run_partitions_local(parts, "bfs", src, "packed")
 run_partitions_local(parts, "sssp", src, "merged-aligned", fused=True)
+run_partitions_local(parts, "cc" if not g.directed else "bfs", src, "compressed", fused=True)
+run_partitions_local(parts, "sssp", src, "compressed")
+# compressed lines: long lists (whole lines) and short lists sharing lines
+h = zc.generate_powerlaw(20000, 40.0, 1.8, seed=5)
+zc.bfs(h, int(zc.pick_sources(h, 1)[0]), "compressed", collect_traffic=False)
 r = zc.generate_rmat(12, 8, seed=1, symmetrize=True)
 zc.cc(r, "packed", collect_traffic=False)
+zc.cc(r, "compressed", collect_traffic=False)
 print("sanitize run ok")
