@@ -54,7 +54,10 @@ def parse():
     # windows (merged-aligned line windows shared across adjacent frontier
     # lists) -- B200 host-store extension, bit-identical results; variants
     # report naive / merged / merged-aligned / packed beside it
-    p.add_argument("--strategy", default="compressed")
+    # direction-optimizing: compressed top-down steps, bottom-up steps over the
+    # compressed in-lists once the frontier is large (B200 extension; levels,
+    # iterations and traversed_edges identical to the reference)
+    p.add_argument("--strategy", default="direction-optimizing")
     p.add_argument("--no-variants", action="store_true",
                    help="skip the naive / merged / UVM / HBM comparison runs")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -226,11 +229,18 @@ def main():
                           "pinned host memory (zero-copy)",
               "graph": f"kron{args.scale}", "scale": args.scale, "edge_factor": args.edge_factor,
               "seed": args.seed + rank, "strategy": args.strategy, "placement": "zerocopy",
-              "list_store": ("compressed line stream in pinned host memory (B200 host-store "
+              "list_store": ("compressed line streams in pinned host memory (B200 host-store "
                              "extension): every list sorted and delta-encoded in 128 B lines, "
                              "hub lists on whole lines, short lists sharing lines; the raw u32 "
-                             "lists stay beside it" if args.strategy == "compressed"
-                             else "raw u32 lists"),
+                             "lists stay beside them"
+                             + ("; out-lists and the in-lists (transpose, built on the GPU)"
+                                if args.strategy == "direction-optimizing" else "")
+                             if args.strategy in COMPRESSED_STRATEGIES else "raw u32 lists"),
+              "direction": ("top-down steps, bottom-up steps (unvisited vertices scan their "
+                            "in-lists for a parent in the frontier) once the frontier's "
+                            "out-edges exceed twice the unvisited vertices' in-edges; levels, "
+                            "iterations and traversed_edges are the reference's"
+                            if args.strategy == "direction-optimizing" else "top-down"),
               "sources": "pick_sources(g, 64, seed=7)",
               "l2": "inputs larger than L2 (8 GiB edge list in host memory, 512 MiB level "
                     "array)",
@@ -250,10 +260,14 @@ def main():
     strat = args.strategy
     probe = zc.link_probe(device=device, nbytes=1 << 30, iters=5)
     cmp_info = None
-    if strat == "compressed":  # host-store build, like pinning: outside the timed region
+    if strat in COMPRESSED_STRATEGIES:  # host-store build, like pinning: outside the timed region
         t0 = time.time()
         nbytes = dg.build_compressed()
         cmp_info = {"build_s": time.time() - t0, "line_stream_bytes": nbytes}
+        if strat == "direction-optimizing":
+            t0 = time.time()
+            cmp_info["in_line_stream_bytes"] = dg.build_in_lists()
+            cmp_info["in_build_s"] = time.time() - t0
     link = LinkBytes(dg, strat)
 
     # warm-up (untimed)
@@ -264,6 +278,7 @@ def main():
     barrier(world, device)
     kernel_ms = expand_ms = 0.0
     trav = launches = link_bytes = 0
+    bottom_up = []
     with ClockSampler(device) as clk:
         for i in range(args.steps):
             r = zc.bfs(dg, int(sources[(args.warmup + i) % 64]), strat, collect_traffic=False)
@@ -271,7 +286,9 @@ def main():
             expand_ms += r.expand_ms
             trav += r.total_traversed_edges
             launches += r.launches
-            link_bytes += link(r.values >= 0)  # BFS expands every reached vertex once
+            link_bytes += link(r)
+            if strat == "direction-optimizing":
+                bottom_up.append([int(x) for x in np.flatnonzero(dg.directions(r.iterations))])
     barrier(world, device)
     kernel_ms_max = max_over_ranks(kernel_ms, world, device)
     trav_all = sum_over_ranks(trav, world, device)
@@ -347,6 +364,8 @@ def main():
     }
     if cmp_info:
         line["graph"]["compressed"] = cmp_info
+    if bottom_up:
+        line["bottom_up_iterations_per_step"] = bottom_up
 
     if rank == 0 and not args.no_cpu_baseline:
         threads = args.cpu_threads or os.cpu_count()
@@ -524,20 +543,29 @@ def main_partitioned(args, rank, world, device, config):
     part.close()
 
 
+COMPRESSED_STRATEGIES = ("compressed", "direction-optimizing")
+
+
 class LinkBytes:
-    """Algorithmic link bytes of a BFS step: the list data of every expanded
-    vertex in its stored form -- 4 B per edge of a raw u32 list, or its span of
-    the compressed line stream (strategy "compressed")."""
+    """Algorithmic link bytes of a BFS step: the list data the expansion
+    kernels must read -- 4 B per traversed edge of the raw u32 lists, or, for
+    the compressed strategies, the line-stream bytes the kernels requested
+    (counted on the device: whole lines of long lists, the spanned words of
+    shared lines; bottom-up steps read candidates' in-lists up to the first
+    parent)."""
 
     def __init__(self, dg, strategy: str):
-        self.cost = dg.stored_list_bytes(strategy)
-        self.describe = ("expanded vertices' list bytes as stored: their span of the compressed "
-                         "line stream (whole lines of long lists, shares of shared lines)"
-                         if strategy == "compressed" else
-                         f"expanded vertices' list bytes ({dg.edge_elem_bytes} B per edge)")
+        self.dg = dg
+        self.compressed = strategy in COMPRESSED_STRATEGIES
+        self.describe = ("line-stream bytes requested by the expansion kernels (device counter: "
+                         "128 B per long-list line, the spanned words of shared lines)"
+                         if self.compressed else
+                         f"traversed edges x {dg.edge_elem_bytes} B (raw u32 lists)")
 
-    def __call__(self, mask) -> int:
-        return int(self.cost[mask].sum())
+    def __call__(self, r) -> int:
+        if self.compressed:
+            return self.dg.link_bytes_requested()
+        return r.total_traversed_edges * self.dg.edge_elem_bytes
 
 
 def _gteps(zc, dg, sources, strategy, reps=1, evict=False):
@@ -546,9 +574,12 @@ def _gteps(zc, dg, sources, strategy, reps=1, evict=False):
         if evict:
             zc.evict(dg)
         r = zc.bfs(dg, int(sources[i % 64]), strategy, collect_traffic=False)
+        gbs = r.total_traversed_edges * 4 / (r.expand_ms * 1e-3) / 1e9
         cur = {"gteps": r.total_traversed_edges / (r.kernel_ms * 1e-3) / 1e9,
-               "kernel_ms": r.kernel_ms, "expand_gbs":
-                   r.total_traversed_edges * 4 / (r.expand_ms * 1e-3) / 1e9}
+               "kernel_ms": r.kernel_ms,
+               ("u32_equivalent_gbs" if strategy in COMPRESSED_STRATEGIES else "expand_gbs"): gbs}
+        if strategy in COMPRESSED_STRATEGIES:
+            cur["requested_link_gbs"] = dg.link_bytes_requested() / (r.expand_ms * 1e-3) / 1e9
         if best is None or cur["gteps"] > best["gteps"]:
             best = cur
     return best
@@ -624,7 +655,8 @@ def variants(zc, args, dg, sources, device, phase: str) -> dict:
     25% capacity)."""
     out = {}
     if phase == "zerocopy":
-        for s in ("naive", "merged", "merged-aligned", "packed", "compressed"):
+        for s in ("naive", "merged", "merged-aligned", "packed", "compressed",
+                  "direction-optimizing"):
             # naive walks each hub list with one thread (seconds per BFS): one rep
             out[f"zerocopy/{s}"] = _gteps(zc, dg, sources, s, reps=1 if s == "naive" else 2)
         return out
@@ -654,7 +686,7 @@ def finish_variants(v: dict) -> None:
     ma = v["zerocopy/merged-aligned"]["gteps"]
     v["speedup_vs_uvm"] = ma / v["uvm/merged-aligned"]["gteps"]
     v["speedup_vs_uvm_cap25"] = ma / v["uvm_cap25/merged-aligned"]["gteps"]
-    for s in ("packed", "compressed"):
+    for s in ("packed", "compressed", "direction-optimizing"):
         v[f"{s}_speedup_vs_uvm_cap25"] = (v[f"zerocopy/{s}"]["gteps"]
                                           / v["uvm_cap25/merged-aligned"]["gteps"])
 

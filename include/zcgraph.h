@@ -69,8 +69,15 @@ extern "C" {
                                aligned 32-element blocks of the union of the
                                frontier's lists, each fetched once           */
 #define ZC_COMPRESSED 4     /* B200 host-store option: lists sorted and stored
-                               delta-encoded (zc_graph_build_compressed); BFS,
-                               CC, PageRank (order-independent) only          */
+                               delta-encoded in 128-byte lines
+                               (zc_graph_build_compressed)                   */
+#define ZC_DIRECTION_OPT 5  /* B200 extension, BFS only: compressed top-down
+                               steps, switching to bottom-up steps (unvisited
+                               vertices scan their compressed in-lists for a
+                               parent in the frontier) when the frontier's
+                               out-edges outnumber half the unvisited
+                               vertices' in-edges.  Same levels, iterations and
+                               traversed_edges (the frontier's out-degrees)  */
 
 /* where the edge / weight lists live */
 #define ZC_PLACE_ZEROCOPY 0 /* cudaHostAlloc(Mapped|Portable) or cudaHostRegister */
@@ -181,6 +188,11 @@ int zc_pagerank(zc_graph *g, int strategy, double damping, uint64_t max_iters, d
  * *compressed_bytes (may be NULL) receives the line stream's size.  Built
  * automatically by the first ZC_COMPRESSED run. */
 int zc_graph_build_compressed(zc_graph *g, uint64_t *compressed_bytes);
+/* Build (once) the in-lists of the graph as a compressed line stream (the
+ * transpose, built on the GPU; an undirected graph reuses its out-lists) for
+ * the bottom-up steps of ZC_DIRECTION_OPT.  *compressed_bytes (may be NULL)
+ * receives its size.  Built automatically by the first ZC_DIRECTION_OPT run. */
+int zc_graph_build_in_lists(zc_graph *g, uint64_t *compressed_bytes);
 /* Copy the compressed-line index to the caller's V+1 u64 buffer: vertex v's
  * list is lines [first_line[v], first_line[v+1]) of the stream (none: read
  * raw).  ZC_ESTATE before zc_graph_build_compressed. */
@@ -202,6 +214,13 @@ int zc_graph_multigraph(zc_graph *g, int *out);
 int zc_run_log(const zc_graph *g, uint64_t *traversed_edges, uint64_t *frontier_sizes,
                uint64_t capacity);
 
+/* Bytes of the compressed line streams (out- and in-lists) the expansion
+ * kernels of the last ZC_COMPRESSED / ZC_DIRECTION_OPT run requested over the
+ * link (4 bytes per loaded word; 0 for the other strategies). */
+int zc_run_link_bytes(const zc_graph *g, uint64_t *bytes);
+/* Direction of each iteration of the last ZC_DIRECTION_OPT run: 1 = bottom-up
+ * step, 0 = top-down; at most `cap` entries (the run's iterations). */
+int zc_run_directions(const zc_graph *g, uint8_t *bottom_up, uint64_t cap);
 /* Device time (ms, CUDA events on the handle's stream) of each iteration's
  * expansion kernels in the most recent run. */
 int zc_run_profile(const zc_graph *g, double *expand_ms, uint64_t capacity);

@@ -33,6 +33,7 @@ EXPORTED = (
     "zc_part_fused_init", "zc_part_fused_connect", "zc_part_fused_reset", "zc_part_fused_expand",
     "zc_graph_open_emgi", "zc_graph_build_pairs", "zc_bulk_probe", "zc_graph_build_compressed",
     "zc_bfs_async", "zc_sssp_async", "zc_sync", "zc_vmm_host_probe", "zc_graph_compressed_index",
+    "zc_graph_build_in_lists", "zc_run_directions", "zc_run_link_bytes",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -93,6 +94,9 @@ def _declare(lib: C.CDLL) -> None:
         "zc_graph_build_pairs": (C.c_int, [P]),
         "zc_graph_build_compressed": (C.c_int, [P, C.POINTER(u64)]),
         "zc_graph_compressed_index": (C.c_int, [P, C.c_void_p]),
+        "zc_graph_build_in_lists": (C.c_int, [P, C.POINTER(u64)]),
+        "zc_run_directions": (C.c_int, [P, C.c_void_p, u64]),
+        "zc_run_link_bytes": (C.c_int, [P, C.POINTER(u64)]),
         "zc_run_log": (C.c_int, [P, P, P, u64]),
         "zc_set_options": (C.c_int, [P, u32]),
         "zc_run_profile": (C.c_int, [P, P, u64]),

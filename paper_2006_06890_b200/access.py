@@ -24,7 +24,12 @@ class AccessStrategy(Enum):
 # "compressed" (ZC_COMPRESSED) streams the lists sorted and delta-encoded in
 # 128-byte lines (hub lists in whole lines, short lists sharing lines, SSSP
 # weights alongside); every result is independent of the order inside a list.
-_IDS = {"naive": 0, "merged": 1, "merged-aligned": 2, "packed": 3, "compressed": 4}
+# "direction-optimizing" (ZC_DIRECTION_OPT, BFS only) runs compressed top-down
+# steps and switches to bottom-up steps over the compressed in-lists when the
+# frontier is large (Beamer et al.); levels, iterations and traversed_edges
+# (the frontier's out-degrees) are the reference's.
+_IDS = {"naive": 0, "merged": 1, "merged-aligned": 2, "packed": 3, "compressed": 4,
+        "direction-optimizing": 5}
 
 
 def strategy_id(strategy) -> int:

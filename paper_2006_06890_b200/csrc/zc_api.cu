@@ -289,6 +289,13 @@ void zc::free_graph(zc_graph* g) {
   free_list(g->h_weights, g->weights_registered, g->hbm_weights);
   free_list(g->h_pairs, false, g->hbm_pairs);
   free_list(g->h_cmp, false, g->hbm_cmp);
+  if (!g->in_alias) {
+    free_list(g->h_cmp_in, false, g->hbm_cmp_in);
+    cudaFree(g->d_cpos_in);
+    cudaFree(g->d_in_off);
+  }
+  cudaFree(g->d_cand);
+  cudaFree(g->d_fbits);
   cudaFree(g->d_cpos);
   if (g->h_off) cudaFreeHost(g->h_off);
   cudaFree(g->d_off);
@@ -577,6 +584,16 @@ bool tune_host_loop() {
   return t && strstr(t, "loop=host");
 }
 
+// Direction-optimizing switch factor (ZC_TUNE=do_alpha=X, default 0.5:
+// bottom-up once the frontier's out-edges exceed twice the unvisited
+// vertices' in-edges; measured best over 16 K27 sources, tools/do_alpha.py).
+double tune_do_alpha() {
+  const char* t = getenv("ZC_TUNE");
+  const char* p = t ? strstr(t, "do_alpha=") : nullptr;
+  const double v = p ? atof(p + 9) : 0.0;
+  return v > 0 ? v : 0.5;
+}
+
 // Build (or reuse) the device-driven level loop of (algo, strategy): a CUDA
 // graph whose conditional WHILE node repeats
 //   stamp -> window counts -> scan -> sweep expansion -> stamp ->
@@ -659,20 +676,25 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     set_error("null graph handle");
     return ZC_ESTATE;
   }
-  if (strategy < kNaive || strategy > kCompressed) {
+  if (strategy < kNaive || strategy > kDirOpt) {
     set_error("unknown access strategy " + std::to_string(strategy));
     return ZC_EINVAL;
   }
   if (strategy >= kPacked && (g->options & ZC_OPT_TRAFFIC_MODEL)) {
     set_error("the request model is defined for the reference's three strategies "
-              "(naive, merged, merged-aligned), not for packed / compressed");
+              "(naive, merged, merged-aligned), not for packed / compressed / "
+              "direction-optimizing");
+    return ZC_EINVAL;
+  }
+  if (strategy == kDirOpt && algo != kBfs) {
+    set_error("direction-optimizing is a bfs strategy");
     return ZC_EINVAL;
   }
   if (strategy == kCompressed && algo == kSssp && g->has_weights && g->wb != 4) {
     set_error("compressed lists carry 4-byte weights only: use packed for 8-byte weights");
     return ZC_EINVAL;
   }
-  if (strategy == kCompressed && g->eb != 4) {
+  if ((strategy == kCompressed || strategy == kDirOpt) && g->eb != 4) {
     set_error("compressed lists need 4-byte edges");
     return ZC_EINVAL;
   }
@@ -705,6 +727,13 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     const int rc = zc_graph_build_compressed(g, nullptr);
     if (rc) return rc;
   }
+  if (strategy == kDirOpt && !g->d_cpos_in) {  // + the in-lists
+    const int rc = zc_graph_build_in_lists(g, nullptr);
+    if (rc) return rc;
+  }
+  // top-down steps of the direction-optimizing strategy are compressed steps
+  const bool dobfs = strategy == kDirOpt;
+  const int td_strategy = dobfs ? static_cast<int>(kCompressed) : strategy;
   if (async) {
     const int rc = ensure_async(g);
     if (rc) return rc;
@@ -715,6 +744,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
   g->log_front.clear();
   g->log_hist.clear();
   g->log_expand_ms.clear();
+  g->log_pull.clear();
   const bool model = (g->options & ZC_OPT_TRAFFIC_MODEL) != 0;
 
   ZC_CUDA_TRY(cudaMemsetAsync(g->d_flags, 0, g->vpad, st));
@@ -779,7 +809,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     return a;
   };
   auto compact_args = [&]() {
-    CompactArgs c;
+    CompactArgs c{};
     c.flags = g->d_flags;
     c.nv = g->nv;
     c.ntiles = g->ntiles;
@@ -791,6 +821,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     c.off = g->d_off;
     c.state = g->d_state;
     c.ctr = g->d_ctr;
+    c.in_off = dobfs ? g->d_in_off : nullptr;  // unvisited in-edge bookkeeping
     return c;
   };
   const int ebytes = pairs ? 8 : static_cast<int>(g->eb);
@@ -799,8 +830,19 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
 
   // ---- device-driven loop: the whole traversal is one graph launch
   const ExpandArgs probe = expand_args(g->nv, 0);
-  const bool device_loop = n > 0 && strategy != kNaive && !model && !probe.chunk_sched &&
-                           !(g->options & ZC_OPT_HOST_LOOP) && !tune_host_loop();
+  const bool device_loop = n > 0 && strategy != kNaive && !dobfs && !model &&
+                           !probe.chunk_sched && !(g->options & ZC_OPT_HOST_LOOP) &&
+                           !tune_host_loop();
+  // direction-optimizing: in-edges of the unvisited vertices (Beamer's m_u)
+  uint64_t unvisited_in = 0;
+  if (dobfs && n) {
+    uint64_t io[2];
+    ZC_CUDA_TRY(cudaMemcpy(io, g->d_in_off + src, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    uint64_t e_in = 0;
+    ZC_CUDA_TRY(cudaMemcpy(&e_in, g->d_in_off + g->nv, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    unvisited_in = e_in - (io[1] - io[0]);
+  }
+  const double do_alpha = tune_do_alpha();
   if (device_loop) {
     int rc = build_loop_graph(g, algo, strategy, ebytes, expand_args(g->nv, 0), compact_args());
     if (rc) return rc;
@@ -854,11 +896,50 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     }
     const size_t ev = 2 * host_iters.size();
     host_iters.push_back(iters);
-    ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[ev], st));
-    ZC_CUDA_TRY(launch_expand(strategy, algo, ebytes, g->wb, a, g->num_sms, st, &launches));
+    // bottom-up when the frontier's out-edges outnumber the unvisited
+    // vertices' in-edges / alpha (the step then reads the candidates' in-list
+    // lines, stopping at the first parent, instead of the frontier's lists)
+    const bool pull = dobfs && iters > 1 && static_cast<double>(trav) * do_alpha >
+                                                static_cast<double>(unvisited_in);
+    if (!pull) ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[ev], st));
+    if (pull) {
+      ZC_CUDA_TRY(launch_pull_prepare(g->d_front[0], n, g->d_fbits, g->nv, g->d_visited,
+                                      g->d_in_off, g->d_cand, g->num_sms, st, &launches));
+      CompactArgs cc{};
+      cc.flags = g->d_cand;
+      cc.nv = g->nv;
+      cc.ntiles = g->ntiles;
+      cc.tiles = g->d_tiles;
+      cc.front_out = g->d_front[1];
+      cc.fs_out = g->d_fs[1];
+      cc.fd_out = g->d_fd[1];
+      cc.fval_out = g->d_fval[1];
+      cc.off = g->d_in_off;
+      cc.state = g->d_state;
+      cc.ctr = g->d_ctr;
+      ZC_CUDA_TRY(launch_compact(kBfs, cc, st, &launches));
+      ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+      ZC_CUDA_TRY(cudaStreamSynchronize(st));
+      const uint64_t ncand = g->h_ctr[kCtrNext];
+      // the expansion-time events bracket the sweep only (candidate set-up is
+      // compaction work, like the top-down steps' next-frontier compaction)
+      ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[ev], st));
+      ExpandArgs b = a;
+      b.front = g->d_front[1];
+      b.fs = g->d_fs[1];
+      b.fd = g->d_fd[1];
+      b.fval = g->d_fval[1];
+      b.n = ncand;
+      b.cmp = static_cast<const uint32_t*>(g->d_cmp_in);
+      b.cpos = g->d_cpos_in;
+      b.fbits = g->d_fbits;
+      ZC_CUDA_TRY(launch_expand(kCompressed, kBfsPull, 4, g->wb, b, g->num_sms, st, &launches));
+    } else {
+      ZC_CUDA_TRY(launch_expand(td_strategy, algo, ebytes, g->wb, a, g->num_sms, st, &launches));
+    }
     ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[ev + 1], st));
     ZC_CUDA_TRY(launch_compact(algo, compact_args(), st, &launches));
-    const size_t nctr = model ? kCtrCount : 2;
+    const size_t nctr = model ? kCtrCount : dobfs ? kCtrTravIn + 1 : 2;
     ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, nctr * sizeof(uint64_t),
                                 cudaMemcpyDeviceToHost, st));
     if (model)
@@ -866,8 +947,15 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     ZC_CUDA_TRY(cudaStreamSynchronize(st));
     n = g->h_ctr[kCtrNext];
     trav = g->h_ctr[kCtrTrav];
+    if (dobfs) {
+      unvisited_in -= std::min(unvisited_in, g->h_ctr[kCtrTravIn]);
+      g->log_pull.push_back(pull ? 1 : 0);
+    }
     if (model) g->log_hist.insert(g->log_hist.end(), g->h_ctr + kCtrHist, g->h_ctr + kCtrHist + 8);
   }
+  // compressed sweeps: the line-stream bytes they requested over the whole run
+  ZC_CUDA_TRY(cudaMemcpyAsync(&g->h_small[3], g->d_ctr + kCtrLoaded, sizeof(uint64_t),
+                              cudaMemcpyDeviceToHost, st));
   ZC_CUDA_TRY(cudaEventRecord(g->ev[1], st));
   if (async) {
     // widen into the slot the download two calls ago has finished with, then
@@ -1420,7 +1508,7 @@ int zc_part_apply(zc_graph* g, const void* mine, uint64_t* n_next, uint64_t* tra
   const int algo = g->p_algo;
   ZC_CUDA_TRY(launch_part_apply(algo, mine, g->nv, g->d_state, g->d_flags,
                                 static_cast<uint32_t>(g->p_iter), st, &g->p_launches));
-  CompactArgs c;
+  CompactArgs c{};
   c.flags = g->d_flags;
   c.nv = g->nv;
   c.ntiles = g->ntiles;
@@ -1745,6 +1833,25 @@ int zc_graph_multigraph(zc_graph* g, int* out) {
     }
   }
   *out = g->multigraph;
+  return ZC_OK;
+}
+
+int zc_run_link_bytes(const zc_graph* g, uint64_t* bytes) {
+  if (!g || !bytes) {
+    set_error("null argument");
+    return ZC_ESTATE;
+  }
+  *bytes = g->h_small ? g->h_small[3] : 0;
+  return ZC_OK;
+}
+
+int zc_run_directions(const zc_graph* g, uint8_t* bottom_up, uint64_t cap) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  const uint64_t n = std::min<uint64_t>(cap, g->log_pull.size());
+  if (bottom_up) std::copy(g->log_pull.begin(), g->log_pull.begin() + n, bottom_up);
   return ZC_OK;
 }
 

@@ -215,6 +215,119 @@ __global__ void k_cmp_pairs(uint64_t ne, const uint32_t* e, const uint32_t* w, u
 
 constexpr int kCmpGrid = 148 * 16;
 
+// Transpose: in-degree count, then a scatter of every arc (v -> d) into d's
+// in-list (slot from a per-vertex cursor; the lists are sorted afterwards).
+__global__ void k_in_count(uint64_t ne, const uint32_t* e, uint32_t* deg) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(deg + e[i], 1u);
+}
+
+__global__ void k_in_scatter(uint64_t nv, const uint64_t* off, const uint32_t* e,
+                             const uint64_t* in_off, uint32_t* cursor, uint32_t* in_e) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t v = gw; v < nv; v += nw)
+    for (uint64_t k = off[v] + lane; k < off[v + 1]; k += 32) {
+      const uint32_t d = e[k];
+      in_e[in_off[d] + atomicAdd(cursor + d, 1u)] = static_cast<uint32_t>(v);
+    }
+}
+
+// device temporaries are released on every path
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { cudaFree(p); }
+  void* release() {
+    void* q = p;
+    p = nullptr;
+    return q;
+  }
+};
+
+// Sorted lists (x) over offsets d_off -> the line stream in device memory
+// (enc) and the per-vertex bit positions (cpos).
+int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t ww, DevBuf* cpos,
+                  DevBuf* enc, size_t* bytes) {
+  DevBuf size;
+  // sizes, then the placement scan on the host (a sequential first-fit)
+  ZC_CUDA_TRY(cudaMalloc(&size.p, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
+  k_cmp_size<<<kCmpGrid, 256>>>(nv, d_off, x, ww, static_cast<uint32_t*>(size.p));
+  ZC_CUDA_TRY(cudaGetLastError());
+  std::vector<uint32_t> hs(nv);
+  std::vector<uint64_t> hp(nv + 1);
+  ZC_CUDA_TRY(cudaMemcpy(hs.data(), size.p, nv * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  cudaFree(size.release());
+  uint64_t pos = 0;
+  auto round_line = [](uint64_t b) { return (b + kLineBits - 1) / kLineBits * kLineBits; };
+  for (uint64_t v = 0; v < nv; ++v) {
+    const uint32_t sz = hs[v];
+    if (sz & kLongSize) {
+      pos = round_line(pos);
+      hp[v] = pos | kCmpLong;
+      pos += static_cast<uint64_t>(sz & ~kLongSize) * kLineBits;
+    } else {
+      if (sz && (pos % kLineBits) + sz > kLineBits) pos = round_line(pos);
+      hp[v] = pos;
+      pos += sz;
+    }
+  }
+  hp[nv] = round_line(pos);
+  const uint64_t lines = hp[nv] / kLineBits;
+  ZC_CUDA_TRY(cudaMalloc(&cpos->p, (nv + 1) * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMemcpy(cpos->p, hp.data(), (nv + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  *bytes = std::max<uint64_t>(lines, 1) * kLineBytes;
+  ZC_CUDA_TRY(cudaMalloc(&enc->p, *bytes));
+  ZC_CUDA_TRY(cudaMemset(enc->p, 0, *bytes));
+  k_cmp_encode<<<kCmpGrid, 256>>>(nv, d_off, x, ww, static_cast<uint64_t*>(cpos->p),
+                                  static_cast<uint32_t*>(enc->p));
+  ZC_CUDA_TRY(cudaDeviceSynchronize());
+  return ZC_OK;
+}
+
+// Place an encoded stream like the handle's lists: host (pinned / managed,
+// read zero-copy), managed (UVM) or HBM (with a host shadow).
+int place_stream(zc_graph* g, DevBuf* enc, size_t bytes, void** host_out, const void** dev_out,
+                 void** hbm_out) {
+  void* host = nullptr;
+  const void* dev = nullptr;
+  void* hbm = nullptr;
+  if (g->placement == ZC_PLACE_UVM) {
+    ZC_CUDA_TRY(cudaMallocManaged(&host, bytes, cudaMemAttachGlobal));
+    if (cudaMemcpy(host, enc->p, bytes, cudaMemcpyDefault) != cudaSuccess ||
+        cudaMemAdvise(host, bytes, cudaMemAdviseSetReadMostly, g->device) != cudaSuccess) {
+      cudaFree(host);
+      set_error(std::string("compressed lists (uvm): ") + cudaGetErrorString(cudaGetLastError()));
+      return ZC_ECUDA;
+    }
+    dev = host;
+  } else {
+    host = host_list_alloc(g, bytes);  // the stream, or the HBM run's host shadow
+    if (!host) {
+      set_error("cannot allocate host memory for the compressed lists");
+      return ZC_ENOMEM;
+    }
+    const void* d = nullptr;
+    if (cudaMemcpy(host, enc->p, bytes, cudaMemcpyDefault) != cudaSuccess ||
+        (g->placement != ZC_PLACE_HBM && host_list_device_ptr(host, &d) != ZC_OK)) {
+      pinned_list_free(host);
+      set_error(std::string("compressed lists: ") + cudaGetErrorString(cudaGetLastError()));
+      return ZC_ECUDA;
+    }
+    if (g->placement == ZC_PLACE_HBM) {
+      hbm = enc->release();
+      dev = hbm;
+    } else {
+      dev = d;
+    }
+  }
+  *host_out = host;
+  *dev_out = dev;
+  *hbm_out = hbm;
+  return ZC_OK;
+}
+
 }  // namespace
 }  // namespace zc
 
@@ -238,17 +351,7 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
   const uint64_t nv = g->nv, ne = g->ne;
   // weights ride along when they are 4-byte (SSSP on the compressed stream)
   const bool weighted = g->has_weights && g->wb == 4 && g->h_weights;
-  // device temporaries are released on every path; the handle is only
-  // updated once the whole stream is built
-  struct DevBuf {
-    void* p = nullptr;
-    ~DevBuf() { cudaFree(p); }
-    void* release() {
-      void* q = p;
-      p = nullptr;
-      return q;
-    }
-  } sorted, wtmp, size, enc, cpos, range;
+  DevBuf sorted, wtmp, enc, cpos, range;
   Elems x{nullptr, nullptr, 0};
   uint32_t ww = 0;
   if (weighted) {
@@ -280,71 +383,14 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
     if (rc) return rc;
     x.e32 = static_cast<const uint32_t*>(sorted.p);
   }
-  // sizes, then the placement scan on the host (a sequential first-fit)
-  ZC_CUDA_TRY(cudaMalloc(&size.p, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
-  k_cmp_size<<<kCmpGrid, 256>>>(nv, g->d_off, x, ww, static_cast<uint32_t*>(size.p));
-  ZC_CUDA_TRY(cudaGetLastError());
-  std::vector<uint32_t> hs(nv);
-  std::vector<uint64_t> hp(nv + 1);
-  ZC_CUDA_TRY(cudaMemcpy(hs.data(), size.p, nv * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-  cudaFree(size.release());
-  uint64_t pos = 0;
-  auto round_line = [](uint64_t b) { return (b + kLineBits - 1) / kLineBits * kLineBits; };
-  for (uint64_t v = 0; v < nv; ++v) {
-    const uint32_t sz = hs[v];
-    if (sz & kLongSize) {
-      pos = round_line(pos);
-      hp[v] = pos | kCmpLong;
-      pos += static_cast<uint64_t>(sz & ~kLongSize) * kLineBits;
-    } else {
-      if (sz && (pos % kLineBits) + sz > kLineBits) pos = round_line(pos);
-      hp[v] = pos;
-      pos += sz;
-    }
-  }
-  hp[nv] = round_line(pos);
-  const uint64_t lines = hp[nv] / kLineBits;
-  ZC_CUDA_TRY(cudaMalloc(&cpos.p, (nv + 1) * sizeof(uint64_t)));
-  ZC_CUDA_TRY(cudaMemcpy(cpos.p, hp.data(), (nv + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice));
-  const size_t bytes = std::max<uint64_t>(lines, 1) * kLineBytes;
-  ZC_CUDA_TRY(cudaMalloc(&enc.p, bytes));
-  ZC_CUDA_TRY(cudaMemset(enc.p, 0, bytes));
-  k_cmp_encode<<<kCmpGrid, 256>>>(nv, g->d_off, x, ww, static_cast<uint64_t*>(cpos.p),
-                                  static_cast<uint32_t*>(enc.p));
-  ZC_CUDA_TRY(cudaDeviceSynchronize());
-  // place the stream like the lists
+  size_t bytes = 0;
+  int rc = encode_stream(nv, g->d_off, x, ww, &cpos, &enc, &bytes);
+  if (rc) return rc;
+  cudaFree(sorted.release());
   void* host = nullptr;
   const void* dev = nullptr;
   void* hbm = nullptr;
-  if (g->placement == ZC_PLACE_UVM) {
-    ZC_CUDA_TRY(cudaMallocManaged(&host, bytes, cudaMemAttachGlobal));
-    if (cudaMemcpy(host, enc.p, bytes, cudaMemcpyDefault) != cudaSuccess ||
-        cudaMemAdvise(host, bytes, cudaMemAdviseSetReadMostly, g->device) != cudaSuccess) {
-      cudaFree(host);
-      set_error(std::string("compressed lists (uvm): ") + cudaGetErrorString(cudaGetLastError()));
-      return ZC_ECUDA;
-    }
-    dev = host;
-  } else {
-    host = host_list_alloc(g, bytes);  // the stream, or the HBM run's host shadow
-    if (!host) {
-      set_error("cannot allocate host memory for the compressed lists");
-      return ZC_ENOMEM;
-    }
-    const void* d = nullptr;
-    if (cudaMemcpy(host, enc.p, bytes, cudaMemcpyDefault) != cudaSuccess ||
-        (g->placement != ZC_PLACE_HBM && host_list_device_ptr(host, &d) != ZC_OK)) {
-      pinned_list_free(host);
-      set_error(std::string("compressed lists: ") + cudaGetErrorString(cudaGetLastError()));
-      return ZC_ECUDA;
-    }
-    if (g->placement == ZC_PLACE_HBM) {
-      hbm = enc.release();
-      dev = hbm;
-    } else {
-      dev = d;
-    }
-  }
+  if ((rc = place_stream(g, &enc, bytes, &host, &dev, &hbm))) return rc;
   g->h_cmp = host;
   g->d_cmp = dev;
   g->hbm_cmp = hbm;
@@ -354,6 +400,78 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
   g->cmp_ww = ww;
   g->cmp_wmin = x.wmin;
   if (compressed_bytes) *compressed_bytes = g->cmp_bytes;
+  return ZC_OK;
+}
+
+extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (g->d_cpos_in) {
+    if (compressed_bytes) *compressed_bytes = g->cmp_in_bytes;
+    return ZC_OK;
+  }
+  int rc = zc_graph_build_compressed(g, nullptr);
+  if (rc) return rc;
+  cudaSetDevice(g->device);
+  const uint64_t nv = g->nv, ne = g->ne;
+  if (!(g->flags & ZC_F_DIRECTED)) {  // in-lists are the out-lists
+    g->d_in_off = g->d_off;
+    g->d_cpos_in = g->d_cpos;
+    g->d_cmp_in = g->d_cmp;
+    g->cmp_in_bytes = g->cmp_bytes;
+    g->in_alias = true;
+  } else {
+    DevBuf out_e, in_e, deg, cursor, in_off, tmp, enc, cpos;
+    ZC_CUDA_TRY(cudaMalloc(&out_e.p, std::max<uint64_t>(ne, 1) * 4));
+    ZC_CUDA_TRY(cudaMemcpy(out_e.p, g->h_edges, ne * 4, cudaMemcpyDefault));
+    ZC_CUDA_TRY(cudaMalloc(&deg.p, std::max<uint64_t>(nv, 1) * 4));
+    ZC_CUDA_TRY(cudaMemset(deg.p, 0, std::max<uint64_t>(nv, 1) * 4));
+    k_in_count<<<kCmpGrid, 256>>>(ne, static_cast<uint32_t*>(out_e.p),
+                                  static_cast<uint32_t*>(deg.p));
+    ZC_CUDA_TRY(cudaGetLastError());
+    ZC_CUDA_TRY(cudaMalloc(&in_off.p, (nv + 1) * sizeof(uint64_t)));
+    const size_t tb = scan_tmp_bytes(nv);
+    ZC_CUDA_TRY(cudaMalloc(&tmp.p, tb));
+    ZC_CUDA_TRY(scan_u32_to_u64(static_cast<uint32_t*>(deg.p), static_cast<uint64_t*>(in_off.p),
+                                nv, tmp.p, tb, 0));
+    cudaFree(tmp.release());
+    ZC_CUDA_TRY(cudaMemset(deg.p, 0, std::max<uint64_t>(nv, 1) * 4));  // now the cursors
+    ZC_CUDA_TRY(cudaMalloc(&in_e.p, std::max<uint64_t>(ne, 1) * 4));
+    k_in_scatter<<<kCmpGrid, 256>>>(nv, g->d_off, static_cast<uint32_t*>(out_e.p),
+                                    static_cast<uint64_t*>(in_off.p),
+                                    static_cast<uint32_t*>(deg.p), static_cast<uint32_t*>(in_e.p));
+    ZC_CUDA_TRY(cudaGetLastError());
+    cudaFree(out_e.release());
+    cudaFree(deg.release());
+    std::vector<int64_t> h_in_off(nv + 1);
+    ZC_CUDA_TRY(cudaMemcpy(h_in_off.data(), in_off.p, (nv + 1) * sizeof(uint64_t),
+                           cudaMemcpyDeviceToHost));
+    rc = sort_lists_device(4, nv, static_cast<uint64_t*>(in_off.p), h_in_off.data(), in_e.p);
+    if (rc) return rc;
+    Elems x{static_cast<const uint32_t*>(in_e.p), nullptr, 0};
+    size_t bytes = 0;
+    if ((rc = encode_stream(nv, static_cast<uint64_t*>(in_off.p), x, 0, &cpos, &enc, &bytes)))
+      return rc;
+    cudaFree(in_e.release());
+    void* host = nullptr;
+    const void* dev = nullptr;
+    void* hbm = nullptr;
+    if ((rc = place_stream(g, &enc, bytes, &host, &dev, &hbm))) return rc;
+    g->h_cmp_in = host;
+    g->d_cmp_in = dev;
+    g->hbm_cmp_in = hbm;
+    g->d_cpos_in = static_cast<uint64_t*>(cpos.release());
+    g->d_in_off = static_cast<uint64_t*>(in_off.release());
+    g->cmp_in_bytes = bytes;
+  }
+  if (!g->d_cand) {
+    ZC_CUDA_TRY(cudaMalloc(&g->d_cand, g->vpad));
+    ZC_CUDA_TRY(cudaMemset(g->d_cand, 0, g->vpad));
+    ZC_CUDA_TRY(cudaMalloc(&g->d_fbits, ((nv + 31) / 32 + 1) * sizeof(uint32_t)));
+  }
+  if (compressed_bytes) *compressed_bytes = g->cmp_in_bytes;
   return ZC_OK;
 }
 

@@ -47,6 +47,18 @@ struct zc_graph {
   uint64_t cmp_bytes = 0;
   uint32_t cmp_ww = 0, cmp_wmin = 0;  // weight field width / offset (0: unweighted)
   bool cmp_weighted = false;
+  // direction-optimizing BFS: in-list offsets and the compressed in-list
+  // stream (undirected graphs alias the out-lists), candidate marks and the
+  // frontier bitmap of the bottom-up steps
+  uint64_t* d_in_off = nullptr;
+  void* h_cmp_in = nullptr;
+  const void* d_cmp_in = nullptr;
+  void* hbm_cmp_in = nullptr;
+  uint64_t* d_cpos_in = nullptr;
+  uint64_t cmp_in_bytes = 0;
+  bool in_alias = false;
+  uint8_t* d_cand = nullptr;
+  uint32_t* d_fbits = nullptr;
   // optional interleaved (dst, weight) u32 pairs for SSSP (zc_graph_build_pairs)
   void* h_pairs = nullptr;
   const void* d_pairs = nullptr;
@@ -77,6 +89,7 @@ struct zc_graph {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // last run's per-iteration log
   std::vector<uint64_t> log_trav, log_front;
+  std::vector<uint8_t> log_pull;  // direction-optimizing: 1 = bottom-up step
   std::vector<uint64_t> log_hist;  // 8 per iteration (ZC_OPT_TRAFFIC_MODEL)
   std::vector<double> log_expand_ms;
   std::vector<cudaEvent_t> iter_ev;  // 2 per iteration, grown on demand

@@ -45,7 +45,14 @@ constexpr uint32_t kExchNone32 = 0x7fffffffu;
 // expanded by its chunk warp but queued and split across all warps.
 constexpr uint32_t kBigSteps = 16;
 
-enum Strategy : int { kNaive = 0, kMerged = 1, kMergedAligned = 2, kPacked = 3, kCompressed = 4 };
+enum Strategy : int {
+  kNaive = 0,
+  kMerged = 1,
+  kMergedAligned = 2,
+  kPacked = 3,
+  kCompressed = 4,
+  kDirOpt = 5  // BFS: compressed top-down + bottom-up steps over the compressed in-lists
+};
 // kCompressed (B200 host-store option, zc_compress.cu): every list is stored
 // sorted and delta-encoded in a stream of 128-byte lines, in vertex order.
 //   short list (encoding <= 1024 bits, <= 64 elements): packed with its
@@ -75,11 +82,16 @@ enum Algo : int { kBfs = 0, kSssp = 1, kCc = 2, kPr = 3 };
 // Partitioned (multi-GPU) variants: the visit writes candidates for any
 // global vertex into the exchange buffer instead of updating local state.
 constexpr int kPartAlgo = 4;  // algo + kPartAlgo
+// Bottom-up BFS step (direction-optimizing strategy): the slots are the
+// unvisited candidates, their in-lists are scanned for a parent in the
+// current frontier (frontier bitmap), the slot's vertex is the value.
+constexpr int kBfsPull = 8;
 template <int A>
 struct AlgoTraits {
-  static constexpr int base = A % kPartAlgo;
-  static constexpr bool part = A >= kPartAlgo;
-  static constexpr bool has_val = base != kBfs;  // frontier carries a value
+  static constexpr bool pull = A == kBfsPull;
+  static constexpr int base = pull ? kBfs : A % kPartAlgo;
+  static constexpr bool part = A >= kPartAlgo && !pull;
+  static constexpr bool has_val = base != kBfs || pull;  // slot carries a value
   static constexpr bool weighted = base == kSssp;
 };
 
@@ -92,9 +104,11 @@ enum Ctr : int {
   kCtrPrDangling = 4,  // PageRank: dangling mass (double bits)
   kCtrPrDelta = 5,     //   L1 change of the iteration
   kCtrPrSum = 6,       //   sum of ranks
+  kCtrTravIn = 7,    // sum of in-degrees of the next frontier (compaction with in_off)
   kCtrHist = 8,      // 8..11 modelled edge requests of 1..4 sectors, 12..15 weights
   kCtrCur = 16,      // device level loop: size of the current frontier
   kCtrIter = 17,     //   completed iterations
+  kCtrLoaded = 18,   // compressed sweeps: bytes requested from the line streams
   kCtrCount = 24
 };
 
@@ -146,6 +160,8 @@ struct ExpandArgs {
   const uint64_t* cpos;
   uint32_t cmp_ww;
   uint32_t cmp_wmin;
+  // bottom-up step (kBfsPull): bitmap of the current frontier
+  const uint32_t* fbits;
 };
 
 // ZC_TUNE="unroll=8,ctas=6,sched=chunk": expansion tuning knobs for experiments.
@@ -163,6 +179,7 @@ struct CompactArgs {
   const uint64_t* off;
   const void* state;
   uint64_t* ctr;
+  const uint64_t* in_off;  // optional: also sum the in-degrees into ctr[kCtrTravIn]
 };
 
 // Launchers (zc_kernels.cu).  All launch on `st`; return cudaError_t.
@@ -174,6 +191,11 @@ cudaError_t launch_traffic_model(int strategy, int edge_bytes, int weight_bytes,
                                  const uint32_t* front, uint64_t n, const uint64_t* off,
                                  uint64_t* ctr, int num_sms, cudaStream_t st, uint64_t* launches);
 cudaError_t launch_compact(int algo, const CompactArgs& c, cudaStream_t st, uint64_t* launches);
+// Bottom-up step inputs: zero + set the frontier bitmap from front[0, n), and
+// mark (u8 per vertex, padded to 16) every unvisited vertex with in-edges.
+cudaError_t launch_pull_prepare(const uint32_t* front, uint64_t n, uint32_t* fbits, uint64_t nv,
+                                const uint32_t* visited, const uint64_t* in_off, uint8_t* cand,
+                                int num_sms, cudaStream_t st, uint64_t* launches);
 cudaError_t launch_init(int algo, void* state, uint64_t nv, uint64_t src, const uint64_t* off,
                         uint32_t* front, uint64_t* fval, uint64_t* fs, uint32_t* fd,
                         cudaStream_t st, uint64_t* launches, uint64_t label_base = 0,

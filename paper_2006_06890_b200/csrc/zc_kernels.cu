@@ -90,6 +90,27 @@ struct Visit<kBfs> {
 };
 
 template <>
+struct Visit<kBfsPull> {
+  // Bottom-up: w is an in-neighbour of the candidate u; u joins the next
+  // level when w is in the current frontier (the same level traversal.py
+  // :116-118 gives it top-down).  The visited bitmap elects one writer.
+  static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
+                                               uint64_t u) {
+    if (!(a.fbits[w >> 5] & (1u << (w & 31)))) return;
+    uint32_t* word = a.visited + (u >> 5);
+    const uint32_t bit = 1u << (u & 31);
+    if (!(*word & bit) && !(atomicOr(word, bit) & bit)) {
+      static_cast<uint32_t*>(a.state)[u] = a.iter;
+      a.flags[u] = 1;
+    }
+  }
+};
+
+__device__ __forceinline__ bool is_visited(const ExpandArgs& a, uint64_t u) {
+  return (a.visited[u >> 5] >> (u & 31)) & 1u;
+}
+
+template <>
 struct Visit<kSssp> {
   // traversal.py:146-150: cand = dist_old[v] + w; dist = min(dist, cand);
   // improved vertices form the next frontier.
@@ -513,6 +534,8 @@ __device__ __forceinline__ void visit_short(const ExpandArgs& a, uint32_t x, int
     uint32_t val = d ? line_bits(L, p + 6, 32) : 0;
     const uint32_t wb = p + kCmpShortHdrBits + (d - 1) * w;
     for (uint32_t e = 0; e < d; ++e) {
+      // bottom-up: stop at the first parent (or a candidate found elsewhere)
+      if (AlgoTraits<ALGO>::pull && is_visited(a, sval)) break;
       if (e) val += line_bits(L, p + kCmpShortHdrBits + (e - 1) * w, w);
       uint64_t wt = 0;
       if constexpr (AlgoTraits<ALGO>::weighted) wt = a.cmp_wmin + line_bits(L, wb + e * a.cmp_ww, a.cmp_ww);
@@ -563,6 +586,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
   __syncthreads();
   uint64_t j = sh_j;
   uint64_t W = Wb;
+  uint64_t words = 0;  // compressed: 4-byte words this warp requested (warp-uniform)
   while (W < We) {
     // stage slots [j, j + kStage)
     for (int i = threadIdx.x; i <= kStage; i += kSweepThreads) {
@@ -572,7 +596,8 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
         const uint64_t s0 = a.fs[jj];
         sh_s[i] = s0;
         sh_e[i] = s0 + a.fd[jj];
-        if (AlgoTraits<ALGO>::has_val) sh_v[i] = a.fval[jj];
+        if (AlgoTraits<ALGO>::has_val)
+          sh_v[i] = AlgoTraits<ALGO>::pull ? a.front[jj] : a.fval[jj];
         if constexpr (kCmp) {
           const uint32_t v = a.front[jj];
           sh_c[i] = a.cpos[v];
@@ -608,21 +633,30 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
           if constexpr (kCmp) {
             const uint64_t c = sh_c[k];
             if (c & kCmpLong) {  // line t of a long list: a word per lane
+              // bottom-up: a candidate found earlier in this level needs no more lines
+              if (AlgoTraits<ALGO>::pull && is_visited(a, sh_v[k])) continue;
               bt.line[u] = 1;
               if (AlgoTraits<ALGO>::has_val) bt.sval[u] = sh_v[k];
               const uint64_t line = cmp_pos(c) / kLineBits + (q - sh_w[k]);
               bt.dst[u] = ld_list(a.cmp + line * kLineWords + lane);
+              words += kLineWords;
             } else {  // a shared line: the words of its staged frontier lists
               bt.line[u] = 2;
               const uint64_t L = cmp_pos(c) / kLineBits;
               int m = k + 1;
               while (m < stage_n && !(sh_c[m] & kCmpLong) && cmp_pos(sh_c[m]) / kLineBits == L) ++m;
+              if constexpr (AlgoTraits<ALGO>::pull) {  // all candidates of the line found?
+                bool open = false;
+                for (int i = k + lane; i < m && !open; i += 32) open = !is_visited(a, sh_v[i]);
+                if (!__any_sync(kFull, open)) continue;
+              }
               const uint32_t w0 = static_cast<uint32_t>(cmp_pos(c) % kLineBits) / 32;
               const uint64_t endb = min(sh_n[m - 1], (L + 1) * kLineBits);
               const uint32_t w1 = static_cast<uint32_t>(endb - 1 - L * kLineBits) / 32;
               bt.k0[u] = static_cast<int16_t>(k);
               bt.k1[u] = static_cast<int16_t>(m);
               bt.dst[u] = lane >= w0 && lane <= w1 ? ld_list(a.cmp + L * kLineWords + lane) : 0u;
+              words += w1 - w0 + 1;
             }
             continue;
           }
@@ -679,6 +713,15 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
     __syncthreads();
     W = Wend;
     j += kStage;
+  }
+  if constexpr (kCmp) {  // link bytes requested: one atomic per CTA
+    __shared__ unsigned long long sh_words;
+    if (threadIdx.x == 0) sh_words = 0;
+    __syncthreads();
+    if (lane == 0 && words) atomicAdd(&sh_words, static_cast<unsigned long long>(words));
+    __syncthreads();
+    if (threadIdx.x == 0 && sh_words)
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.ctr + kCtrLoaded), sh_words * 4ull);
   }
 }
 
@@ -933,6 +976,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(CompactArgs c) {
     if (lane == 31) {
       c.ctr[kCtrNext] = wi;  // grand total
       c.ctr[kCtrTrav] = 0;
+      c.ctr[kCtrTravIn] = 0;
       c.ctr[kCtrBig] = 0;
     }
   }
@@ -948,7 +992,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(CompactArgs c) {
 template <int ALGO>
 __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
   __shared__ uint32_t warp_tot[kTileThreads / 32];
-  __shared__ unsigned long long deg_sh[kTileThreads / 32];
+  __shared__ unsigned long long deg_sh[kTileThreads / 32], indeg_sh[kTileThreads / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (uint64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
     uint4* fp = reinterpret_cast<uint4*>(c.flags) + t * kTileThreads + threadIdx.x;
@@ -966,7 +1010,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
     uint32_t before = 0;
     for (int w = 0; w < wid; ++w) before += warp_tot[w];
     uint64_t pos = static_cast<uint64_t>(c.tiles[t]) + before + incl - cnt;
-    unsigned long long deg = 0;
+    unsigned long long deg = 0, indeg = 0;
     if (cnt) {
       const uint64_t v0 = t * kTileVerts + static_cast<uint64_t>(threadIdx.x) * 16;
 #pragma unroll
@@ -980,19 +1024,30 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
           if (ALGO == kSssp) c.fval_out[pos] = static_cast<const uint64_t*>(c.state)[v];
           if (ALGO == kCc) c.fval_out[pos] = static_cast<const uint32_t*>(c.state)[v];
           deg += d0;
+          if (c.in_off) indeg += c.in_off[v + 1] - c.in_off[v];
           ++pos;
         }
       }
       *fp = make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) deg += __shfl_down_sync(kFull, deg, d);
-    if (lane == 0) deg_sh[wid] = deg;
+    for (int d = 16; d > 0; d >>= 1) {
+      deg += __shfl_down_sync(kFull, deg, d);
+      indeg += __shfl_down_sync(kFull, indeg, d);
+    }
+    if (lane == 0) {
+      deg_sh[wid] = deg;
+      indeg_sh[wid] = indeg;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      unsigned long long tot = 0;
-      for (int w = 0; w < kTileThreads / 32; ++w) tot += deg_sh[w];
+      unsigned long long tot = 0, tin = 0;
+      for (int w = 0; w < kTileThreads / 32; ++w) {
+        tot += deg_sh[w];
+        tin += indeg_sh[w];
+      }
       if (tot) atomicAdd(reinterpret_cast<unsigned long long*>(c.ctr + kCtrTrav), tot);
+      if (tin) atomicAdd(reinterpret_cast<unsigned long long*>(c.ctr + kCtrTravIn), tin);
     }
     __syncthreads();
   }
@@ -1435,6 +1490,7 @@ cudaError_t launch_expand(int strategy, int algo, int edge_bytes, int weight_byt
       case kBfs + kPartAlgo: return expand_cmp<kBfs + kPartAlgo>(a, num_sms, st, launches);
       case kSssp + kPartAlgo: return expand_cmp<kSssp + kPartAlgo>(a, num_sms, st, launches);
       case kCc + kPartAlgo: return expand_cmp<kCc + kPartAlgo>(a, num_sms, st, launches);
+      case kBfsPull: return expand_cmp<kBfsPull>(a, num_sms, st, launches);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -1461,6 +1517,53 @@ cudaError_t launch_traffic_model(int strategy, int edge_bytes, int weight_bytes,
     k_model_merged<kMergedAligned><<<g, 256, 0, st>>>(front, n, off, edge_bytes, weight_bytes,
                                                       weights, ctr);
   *launches += 1;
+  return cudaGetLastError();
+}
+
+namespace {
+// Bottom-up step inputs: the current frontier as a bitmap, and the candidate
+// marks (unvisited vertices with in-edges), 16 vertices per thread.
+__global__ void k_fbits_set(const uint32_t* front, uint64_t n, uint32_t* fbits) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = front[j];
+    atomicOr(fbits + (v >> 5), 1u << (v & 31));
+  }
+}
+
+__global__ void k_cand_marks(uint64_t nv, const uint32_t* visited, const uint64_t* in_off,
+                             uint8_t* cand) {
+  const uint64_t ngroups = (nv + 15) / 16;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ngroups;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v0 = t * 16;
+    const uint32_t vis = (visited[v0 >> 5] >> (v0 & 31)) & 0xffffu;
+    uint32_t m[4] = {0, 0, 0, 0};
+    if (vis != 0xffffu) {
+      uint64_t prev = in_off[v0];
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        const uint64_t v = v0 + b;
+        if (v >= nv) break;
+        const uint64_t nxt = in_off[v + 1];
+        if (!((vis >> b) & 1u) && nxt > prev) m[b >> 2] |= 1u << ((b & 3) * 8);
+        prev = nxt;
+      }
+    }
+    reinterpret_cast<uint4*>(cand)[t] = make_uint4(m[0], m[1], m[2], m[3]);
+  }
+}
+}  // namespace
+
+cudaError_t launch_pull_prepare(const uint32_t* front, uint64_t n, uint32_t* fbits,
+                                uint64_t nv, const uint32_t* visited, const uint64_t* in_off,
+                                uint8_t* cand, int num_sms, cudaStream_t st, uint64_t* launches) {
+  cudaError_t e = cudaMemsetAsync(fbits, 0, ((nv + 31) / 32 + 1) * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  if (n) k_fbits_set<<<grid_for(n, 256, num_sms, 16), 256, 0, st>>>(front, n, fbits);
+  k_cand_marks<<<grid_for((nv + 15) / 16, 256, num_sms, 16), 256, 0, st>>>(nv, visited, in_off,
+                                                                            cand);
+  *launches += 2;
   return cudaGetLastError();
 }
 

@@ -223,6 +223,28 @@ class DeviceGraph:
         pos = (self.compressed_index() & np.uint64((1 << 63) - 1)).astype(np.int64)
         return np.diff(pos) // 8
 
+    def build_in_lists(self) -> int:
+        """Build the compressed in-list stream (the transpose; an undirected
+        graph reuses its out-lists) used by "direction-optimizing"; returns
+        its size in bytes."""
+        nbytes = C.c_uint64()
+        N.check(N.lib().zc_graph_build_in_lists(self.handle, C.byref(nbytes)))
+        return nbytes.value
+
+    def link_bytes_requested(self) -> int:
+        """Line-stream bytes the last compressed / direction-optimizing run's
+        expansion kernels requested over the link (0 for other strategies)."""
+        out = C.c_uint64()
+        N.check(N.lib().zc_run_link_bytes(self.handle, C.byref(out)))
+        return out.value
+
+    def directions(self, iterations: int) -> np.ndarray:
+        """Per-iteration direction of the last "direction-optimizing" run
+        (True = bottom-up step)."""
+        out = np.zeros(iterations, np.uint8)
+        N.check(N.lib().zc_run_directions(self.handle, out.ctypes.data, iterations))
+        return out.astype(bool)
+
     def expand_profile(self, iterations: int) -> np.ndarray:
         """Per-iteration device time (ms) of the expansion kernels of the last run."""
         out = np.zeros(iterations, np.float64)

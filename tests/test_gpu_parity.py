@@ -548,3 +548,48 @@ def _from_edges(nv, src, dst):
     off = np.zeros(nv + 1, np.int64)
     np.add.at(off, src + 1, 1)
     return zc.CsrGraph(nv, len(dst), np.cumsum(off), dst.astype(np.int64), None, 4, 4, True)
+
+
+def test_direction_optimizing_matches_reference():
+    """Direction-optimizing BFS (compressed top-down + bottom-up steps over
+    the compressed in-lists): values, iterations and traversed edges equal the
+    reference on every BFS fixture (directed and undirected)."""
+    bad = []
+    for c in CASES:
+        if c.algo != "bfs" or c.graph.edge_elem_bytes != 4:
+            continue
+        r = _run(c, "direction-optimizing")
+        if not (np.array_equal(r.values, c.values) and r.iterations == c.iterations
+                and r.traversed_edges == c.traversed):
+            bad.append((c.index, c.tag))
+    assert not bad, bad[:8]
+
+
+@pytest.mark.parametrize("symmetrize", [False, True])
+def test_direction_optimizing_rmat(symmetrize):
+    """Bottom-up steps really run (directions log), and the levels equal the
+    oracle's on R-MAT graphs from several sources; bfs_many agrees."""
+    dg = zc.generate_rmat(18, 16, seed=9, symmetrize=symmetrize)
+    g = dg.as_csr()
+    srcs = [int(s) for s in zc.pick_sources(g, 3, seed=7)]
+    pulled = False
+    for s in srcs:
+        r = zc.bfs(dg, s, "direction-optimizing", collect_traffic=False)
+        ref = oracle.bfs(g, s, threads=8)
+        assert np.array_equal(r.values, ref.values)
+        assert r.iterations == ref.iterations and r.traversed_edges == ref.traversed_edges
+        pulled |= bool(dg.directions(r.iterations).any())
+    assert pulled
+    for s, r in zip(srcs, zc.bfs_many(dg, srcs, "direction-optimizing")):
+        assert np.array_equal(r.values, oracle.bfs(g, s, threads=8).values)
+    dg.close()
+
+
+def test_direction_optimizing_rejects_other_algorithms():
+    g = zc.with_uniform_weights(zc.generate_uniform(500, 1, 9, seed=2))
+    with pytest.raises(ValueError, match="bfs strategy"):
+        zc.sssp(g, 0, "direction-optimizing", collect_traffic=False)
+    with pytest.raises(ValueError, match="bfs strategy"):
+        zc.cc(zc.symmetrized(g), "direction-optimizing", collect_traffic=False)
+    with pytest.raises(ValueError, match="request model"):
+        zc.bfs(g, 0, "direction-optimizing", collect_traffic=True)
