@@ -247,6 +247,14 @@ __attribute__((constructor)) static void install_segv_trace() {
   if (e && e[0] == '1') signal(SIGSEGV, segv_trace);
 }
 
+// int64 BFS levels from the narrowed download (0xff = unreached -> -1,
+// traversal.py:22), on the host cores.
+static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n) {
+  parallel_for(n, [&](uint64_t lo, uint64_t hi) {
+    for (uint64_t i = lo; i < hi; ++i) out[i] = src[i] == 0xffu ? -1ll : static_cast<int64_t>(src[i]);
+  });
+}
+
 static double now_ms() {
   using namespace std::chrono;
   return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
@@ -273,6 +281,10 @@ struct DeviceGuard {
 void zc::free_graph(zc_graph* g) {
   if (!g) return;
   cudaSetDevice(g->device);
+  for (auto& t : g->widen_th)
+    if (t.joinable()) t.join();
+  for (auto* p : g->h_stage)
+    if (p) cudaFreeHost(p);
   if (g->stream) cudaStreamSynchronize(g->stream);
   if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);
   auto free_list = [&](void*& h, bool registered, void*& hbm) {
@@ -957,12 +969,53 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
   ZC_CUDA_TRY(cudaMemcpyAsync(&g->h_small[3], g->d_ctr + kCtrLoaded, sizeof(uint64_t),
                               cudaMemcpyDeviceToHost, st));
   ZC_CUDA_TRY(cudaEventRecord(g->ev[1], st));
-  if (async) {
+  // BFS levels below 255 travel as one byte each and are widened to int64 on
+  // the host: the download is V bytes instead of 8 V (which, at the link's
+  // speed, costs as much as a bottom-up traversal and competes with its reads)
+  const bool narrow = algo == kBfs && g->nv && iters <= 255;
+  if (async && narrow) {
+    const uint32_t b = g->out_next;
+    g->out_next ^= 1;
+    if (g->widen_th[b].joinable()) g->widen_th[b].join();  // slot b's host staging is free
+    ZC_CUDA_TRY(cudaStreamWaitEvent(st, g->out_done[b], 0));
+    uint8_t* d_u8 = reinterpret_cast<uint8_t*>(g->d_outbuf[b]);
+    ZC_CUDA_TRY(launch_narrow_levels(g->d_state, g->nv, d_u8, st, &launches));
+    ZC_CUDA_TRY(cudaEventRecord(g->out_ready[b], st));
+    ZC_CUDA_TRY(cudaStreamWaitEvent(g->copy_stream, g->out_ready[b], 0));
+    if (!g->h_stage[b]) ZC_CUDA_TRY(cudaHostAlloc(&g->h_stage[b], g->nv, cudaHostAllocDefault));
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->h_stage[b], d_u8, g->nv, cudaMemcpyDeviceToHost,
+                                g->copy_stream));
+    ZC_CUDA_TRY(cudaEventRecord(g->out_done[b], g->copy_stream));
+    ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
+    const cudaEvent_t done = g->out_done[b];
+    const uint8_t* src8 = g->h_stage[b];
+    const uint64_t nv = g->nv;
+    const int dev = g->device;
+    int* err = &g->widen_err;
+    g->widen_th[b] = std::thread([=] {  // widens while the caller starts the next traversal
+      cudaSetDevice(dev);
+      if (cudaEventSynchronize(done) != cudaSuccess) {
+        *err = ZC_ECUDA;
+        return;
+      }
+      widen_levels(src8, out, nv);
+    });
+    ZC_CUDA_TRY(cudaEventSynchronize(g->ev[1]));
+  } else if (narrow) {
+    uint8_t* d_u8 = reinterpret_cast<uint8_t*>(g->d_fval[0]);
+    ZC_CUDA_TRY(launch_narrow_levels(g->d_state, g->nv, d_u8, st, &launches));
+    if (!g->h_stage[2]) ZC_CUDA_TRY(cudaHostAlloc(&g->h_stage[2], g->nv, cudaHostAllocDefault));
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->h_stage[2], d_u8, g->nv, cudaMemcpyDeviceToHost, st));
+    ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
+    ZC_CUDA_TRY(cudaStreamSynchronize(st));
+    widen_levels(g->h_stage[2], out, g->nv);
+  } else if (async) {
     // widen into the slot the download two calls ago has finished with, then
     // download it on copy_stream: the D2H direction of the link is idle while
     // the next traversal streams the edge list H2D
     const uint32_t b = g->out_next;
     g->out_next ^= 1;
+    if (g->widen_th[b].joinable()) g->widen_th[b].join();
     ZC_CUDA_TRY(cudaStreamWaitEvent(st, g->out_done[b], 0));
     ZC_CUDA_TRY(launch_widen(algo, g->d_state, g->nv, g->d_outbuf[b], st, &launches));
     ZC_CUDA_TRY(cudaEventRecord(g->out_ready[b], st));
@@ -1002,7 +1055,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
       stats->d2h_ms = ms;
     }
     stats->h2d_bytes = h2d;
-    stats->d2h_bytes = g->nv * sizeof(int64_t) +
+    stats->d2h_bytes = g->nv * (narrow ? 1 : sizeof(int64_t)) +
                        (device_loop ? (kCtrCount + 4 * kLogCap) : iters * (model ? kCtrCount : 2)) *
                            sizeof(uint64_t);
     stats->launches = launches;
@@ -1604,6 +1657,13 @@ int zc_sync(zc_graph* g) {
   if (!g->copy_stream) return ZC_OK;
   DeviceGuard dg(g->device);
   ZC_CUDA_TRY(cudaStreamSynchronize(g->copy_stream));
+  for (auto& t : g->widen_th)
+    if (t.joinable()) t.join();
+  if (g->widen_err) {
+    g->widen_err = 0;
+    set_error("pipelined result download failed");
+    return ZC_ECUDA;
+  }
   return ZC_OK;
 }
 int zc_cc(zc_graph* g, int strategy, int64_t* out, zc_stats* stats) {

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <thread>
 #include <vector>
 
 #include "../../include/zcgraph.h"
@@ -115,6 +116,11 @@ struct zc_graph {
   int64_t* d_outbuf[2] = {nullptr, nullptr};
   cudaEvent_t out_ready[2] = {nullptr, nullptr}, out_done[2] = {nullptr, nullptr};
   uint32_t out_next = 0;
+  // narrowed BFS results: pinned u8 staging per slot, widened to int64 on the
+  // host by a worker thread while the next traversal runs
+  uint8_t* h_stage[3] = {nullptr, nullptr, nullptr};  // [2]: the blocking path
+  std::thread widen_th[2];
+  int widen_err = 0;
   // stepped run state (zc_part_begin / expand / apply)
   int p_algo = -1, p_strategy = 0, p_cur = 0;
   uint64_t p_iter = 0, p_n = 0, p_launches = 0;

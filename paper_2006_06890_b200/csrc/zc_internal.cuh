@@ -207,6 +207,9 @@ cudaError_t launch_fill_exchange(int algo, void* x, uint64_t n, cudaStream_t st,
                                  uint64_t* launches);
 cudaError_t launch_part_apply(int algo, const void* mine, uint64_t nlocal, void* state,
                               uint8_t* flags, uint32_t iter, cudaStream_t st, uint64_t* launches);
+// BFS levels (all below 255) as u8, 0xff = unreached.
+cudaError_t launch_narrow_levels(const void* state, uint64_t nv, uint8_t* out, cudaStream_t st,
+                                 uint64_t* launches);
 cudaError_t launch_widen(int algo, const void* state, uint64_t nv, int64_t* out, cudaStream_t st,
                          uint64_t* launches);
 cudaError_t launch_check_edges(const void* edges, int edge_bytes, uint64_t ne, uint64_t nv,

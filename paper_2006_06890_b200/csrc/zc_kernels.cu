@@ -1691,6 +1691,27 @@ cudaError_t launch_widen(int algo, const void* state, uint64_t nv, int64_t* out,
   return cudaGetLastError();
 }
 
+namespace {
+// BFS levels below 255 as one byte each (0xff = unreached): the download is
+// V bytes instead of 8 V; the host widens to the reference's int64.
+__global__ void k_narrow_levels(const uint32_t* level, uint64_t nv, uint8_t* out) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = level[v];
+    out[v] = x == kUnreached32 ? 0xffu : static_cast<uint8_t>(x);
+  }
+}
+}  // namespace
+
+cudaError_t launch_narrow_levels(const void* state, uint64_t nv, uint8_t* out, cudaStream_t st,
+                                 uint64_t* launches) {
+  if (nv == 0) return cudaSuccess;
+  k_narrow_levels<<<grid_for(nv, 256, 148, 16), 256, 0, st>>>(static_cast<const uint32_t*>(state),
+                                                             nv, out);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_check_edges(const void* edges, int edge_bytes, uint64_t ne, uint64_t nv,
                                uint64_t* bad, cudaStream_t st) {
   if (ne == 0) return cudaSuccess;
