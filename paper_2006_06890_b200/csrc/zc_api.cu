@@ -596,14 +596,14 @@ bool tune_host_loop() {
   return t && strstr(t, "loop=host");
 }
 
-// Direction-optimizing switch factor (ZC_TUNE=do_alpha=X, default 0.5:
-// bottom-up once the frontier's out-edges exceed twice the unvisited
+// Direction-optimizing switch factor (ZC_TUNE=do_alpha=X, default 2:
+// bottom-up once the frontier's out-edges exceed half the unvisited
 // vertices' in-edges; measured best over 16 K27 sources, tools/do_alpha.py).
 double tune_do_alpha() {
   const char* t = getenv("ZC_TUNE");
   const char* p = t ? strstr(t, "do_alpha=") : nullptr;
   const double v = p ? atof(p + 9) : 0.0;
-  return v > 0 ? v : 0.5;
+  return v > 0 ? v : 2.0;
 }
 
 // Build (or reuse) the device-driven level loop of (algo, strategy): a CUDA
@@ -891,6 +891,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
 
   // ---- host-driven loop (naive, request model, tuning, or the tail past the log)
   std::vector<uint64_t> host_iters;
+  uint64_t dbg_ncand = 0;
   while (n > 0) {
     ++iters;
     g->log_trav.push_back(trav);
@@ -933,6 +934,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
       ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
       ZC_CUDA_TRY(cudaStreamSynchronize(st));
       const uint64_t ncand = g->h_ctr[kCtrNext];
+      dbg_ncand = ncand;
       // the expansion-time events bracket the sweep only (candidate set-up is
       // compaction work, like the top-down steps' next-frontier compaction)
       ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[ev], st));
@@ -945,13 +947,18 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
       b.cmp = static_cast<const uint32_t*>(g->d_cmp_in);
       b.cpos = g->d_cpos_in;
       b.fbits = g->d_fbits;
+      // pass 1: first lines (most candidates find their parent there); pass 2:
+      // the remaining lines of long in-lists still without one
+      b.pull_pass = 1;
+      ZC_CUDA_TRY(launch_expand(kCompressed, kBfsPull, 4, g->wb, b, g->num_sms, st, &launches));
+      b.pull_pass = 2;
       ZC_CUDA_TRY(launch_expand(kCompressed, kBfsPull, 4, g->wb, b, g->num_sms, st, &launches));
     } else {
       ZC_CUDA_TRY(launch_expand(td_strategy, algo, ebytes, g->wb, a, g->num_sms, st, &launches));
     }
     ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[ev + 1], st));
     ZC_CUDA_TRY(launch_compact(algo, compact_args(), st, &launches));
-    const size_t nctr = model ? kCtrCount : dobfs ? kCtrTravIn + 1 : 2;
+    const size_t nctr = model ? kCtrCount : dobfs ? kCtrLoaded + 1 : 2;
     ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, nctr * sizeof(uint64_t),
                                 cudaMemcpyDeviceToHost, st));
     if (model)
@@ -960,6 +967,15 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     n = g->h_ctr[kCtrNext];
     trav = g->h_ctr[kCtrTrav];
     if (dobfs) {
+      if (getenv("ZC_DEBUG_DO")) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, g->iter_ev[ev], g->iter_ev[ev + 1]);
+        fprintf(stderr, "zc-do it=%lu pull=%d front=%lu trav=%lu unvisited_in=%lu ncand=%lu "
+                "loaded=%lu sweep_ms=%.2f\n", (unsigned long)iters, pull ? 1 : 0,
+                (unsigned long)g->log_front.back(), (unsigned long)g->log_trav.back(),
+                (unsigned long)unvisited_in, (unsigned long)(pull ? dbg_ncand : 0),
+                (unsigned long)g->h_ctr[kCtrLoaded], ms);
+      }
       unvisited_in -= std::min(unvisited_in, g->h_ctr[kCtrTravIn]);
       g->log_pull.push_back(pull ? 1 : 0);
     }

@@ -160,8 +160,11 @@ struct ExpandArgs {
   const uint64_t* cpos;
   uint32_t cmp_ww;
   uint32_t cmp_wmin;
-  // bottom-up step (kBfsPull): bitmap of the current frontier
+  // bottom-up step (kBfsPull): bitmap of the current frontier; pass 1 reads
+  // every candidate's first line (short lists whole), pass 2 the remaining
+  // lines of the long in-lists still without a parent (0: one pass, all)
   const uint32_t* fbits;
+  uint32_t pull_pass;
 };
 
 // ZC_TUNE="unroll=8,ctas=6,sched=chunk": expansion tuning knobs for experiments.

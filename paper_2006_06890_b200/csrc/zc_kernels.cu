@@ -446,8 +446,16 @@ __global__ void k_window_counts(ExpandArgs a) {
     if (STRAT == kCompressed) {
       const uint32_t v = a.front[j];
       const uint64_t c = a.cpos[v];
+      if (a.pull_pass == 2) {  // the rest of the long in-lists still without a parent
+        a.wcnt[j] = (c & kCmpLong) && !((a.visited[v >> 5] >> (v & 31)) & 1u)
+                        ? static_cast<uint32_t>((cmp_pos(a.cpos[v + 1]) - cmp_pos(c)) / kLineBits - 1)
+                        : 0u;
+        continue;
+      }
       if (c & kCmpLong) {
-        a.wcnt[j] = static_cast<uint32_t>((cmp_pos(a.cpos[v + 1]) - cmp_pos(c)) / kLineBits);
+        a.wcnt[j] = a.pull_pass == 1 ? 1u
+                                     : static_cast<uint32_t>((cmp_pos(a.cpos[v + 1]) - cmp_pos(c)) /
+                                                             kLineBits);
         continue;
       }
       uint32_t w = 1;
@@ -637,7 +645,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
               if (AlgoTraits<ALGO>::pull && is_visited(a, sh_v[k])) continue;
               bt.line[u] = 1;
               if (AlgoTraits<ALGO>::has_val) bt.sval[u] = sh_v[k];
-              const uint64_t line = cmp_pos(c) / kLineBits + (q - sh_w[k]);
+              const uint64_t line = cmp_pos(c) / kLineBits + (q - sh_w[k]) + (a.pull_pass == 2);
               bt.dst[u] = ld_list(a.cmp + line * kLineWords + lane);
               words += kLineWords;
             } else {  // a shared line: the words of its staged frontier lists
