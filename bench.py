@@ -523,7 +523,12 @@ def main_partitioned(args, rank, world, device, config):
                             "rank's u32 edge slice zero-copy in pinned host memory",
                 "graph": f"kron{scale}", "scale": scale, "seed": args.seed,
                 "parallelism": f"vertex-partition{world}",
-                "exchange": "per level: reduce-scatter of u8 flags (MAX), all-reduce of counts",
+                "exchange": ("per level: reduce-scatter of u8 flags (MAX) for top-down steps; "
+                             "bottom-up steps all-reduce (SUM of disjoint bits = OR) the "
+                             "owned-frontier bitmaps and scan the owned vertices' in-lists "
+                             "(generated per rank, no edge exchange); all-reduce of counts"
+                             if strat == "direction-optimizing" else
+                             "per level: reduce-scatter of u8 flags (MAX), all-reduce of counts"),
                 "backend": args.backend})
     line = {"metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": loop_ms / args.steps,

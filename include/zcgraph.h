@@ -300,6 +300,27 @@ int zc_part_begin(zc_graph *g, int algo, uint64_t source, int strategy, uint64_t
 int zc_part_expand(zc_graph *g, void *exchange /* device pointer */);
 int zc_part_apply(zc_graph *g, const void *mine /* device pointer, stride slots */,
                   uint64_t *n_next, uint64_t *traversed_next);
+/* Direction-optimizing partitions (strategy ZC_DIRECTION_OPT, bfs):
+ *   zc_part_build_in_lists  the owned vertices' in-lists as a compressed line
+ *                           stream: an undirected partition reuses its
+ *                           out-lists; a directed one must come from
+ *                           zc_generate_rmat_part (every rank enumerates the
+ *                           counter-based arcs into its range; no exchange).
+ *                           Built by zc_part_begin when needed.
+ *   zc_part_unvisited_in    in-edges of the owned, still unvisited vertices
+ *                           (sum over ranks = the switch test's denominator).
+ *   zc_part_frontier_bits   zero the caller's device bitmap of
+ *                           (global_vertices + 31) / 32 + 1 words and set the
+ *                           owned frontier's bits (global ids).  Ranks own
+ *                           disjoint bits, so a SUM all-reduce of the words
+ *                           is their OR.
+ *   zc_part_pull            a bottom-up step with the all-reduced bitmap in
+ *                           place of zc_part_expand + zc_part_apply: the
+ *                           owned unvisited vertices scan their in-lists. */
+int zc_part_build_in_lists(zc_graph *g, uint64_t *compressed_bytes);
+int zc_part_unvisited_in(const zc_graph *g, uint64_t *in_edges);
+int zc_part_frontier_bits(zc_graph *g, uint32_t *bits);
+int zc_part_pull(zc_graph *g, const uint32_t *bits, uint64_t *n_next, uint64_t *trav_next);
 int zc_part_result(zc_graph *g, int64_t *out_local /* range size, or NULL: stats only */,
                    zc_stats *stats);
 /* Fused exchange (no reduce-scatter): the expand kernel writes each candidate

@@ -34,6 +34,7 @@ EXPORTED = (
     "zc_graph_open_emgi", "zc_graph_build_pairs", "zc_bulk_probe", "zc_graph_build_compressed",
     "zc_bfs_async", "zc_sssp_async", "zc_sync", "zc_vmm_host_probe", "zc_graph_compressed_index",
     "zc_graph_build_in_lists", "zc_run_directions", "zc_run_link_bytes",
+    "zc_part_build_in_lists", "zc_part_unvisited_in", "zc_part_frontier_bits", "zc_part_pull",
 )
 ZC_OPT_TRAFFIC_MODEL = 1
 
@@ -97,6 +98,10 @@ def _declare(lib: C.CDLL) -> None:
         "zc_graph_build_in_lists": (C.c_int, [P, C.POINTER(u64)]),
         "zc_run_directions": (C.c_int, [P, C.c_void_p, u64]),
         "zc_run_link_bytes": (C.c_int, [P, C.POINTER(u64)]),
+        "zc_part_build_in_lists": (C.c_int, [P, C.POINTER(u64)]),
+        "zc_part_unvisited_in": (C.c_int, [P, C.POINTER(u64)]),
+        "zc_part_frontier_bits": (C.c_int, [P, C.c_void_p]),
+        "zc_part_pull": (C.c_int, [P, C.c_void_p, C.POINTER(u64), C.POINTER(u64)]),
         "zc_run_log": (C.c_int, [P, P, P, u64]),
         "zc_set_options": (C.c_int, [P, u32]),
         "zc_run_profile": (C.c_int, [P, P, u64]),

@@ -1362,16 +1362,25 @@ int zc_part_begin(zc_graph* g, int algo, uint64_t src, int strategy, uint64_t* n
     set_error("not a partition handle");
     return ZC_ESTATE;
   }
-  if (algo < kBfs || algo > kCc || strategy < kNaive || strategy > kCompressed) {
+  if (algo < kBfs || algo > kCc || strategy < kNaive || strategy > kDirOpt) {
     set_error("unknown algorithm or strategy");
     return ZC_EINVAL;
   }
-  if (strategy == kCompressed && (g->eb != 4 || (algo == kSssp && g->has_weights && g->wb != 4))) {
+  if (strategy == kDirOpt && algo != kBfs) {
+    set_error("direction-optimizing is a bfs strategy");
+    return ZC_EINVAL;
+  }
+  if ((strategy == kCompressed || strategy == kDirOpt) &&
+      (g->eb != 4 || (algo == kSssp && g->has_weights && g->wb != 4))) {
     set_error("compressed lists need 4-byte edges (and 4-byte weights for sssp)");
     return ZC_EINVAL;
   }
-  if (strategy == kCompressed && !g->d_cmp) {  // built once per handle
+  if ((strategy == kCompressed || strategy == kDirOpt) && !g->d_cmp) {  // built once per handle
     const int rc = zc_graph_build_compressed(g, nullptr);
+    if (rc) return rc;
+  }
+  if (strategy == kDirOpt && !g->d_cpos_in) {  // + the owned vertices' in-lists
+    const int rc = zc_part_build_in_lists(g, nullptr);
     if (rc) return rc;
   }
   if (algo != kCc && src >= g->global_nv) {
@@ -1423,6 +1432,13 @@ int zc_part_begin(zc_graph* g, int algo, uint64_t src, int strategy, uint64_t* n
                                 cudaMemcpyHostToDevice, st));
     n = 1;
     trav = g->h_off[lsrc + 1] - g->h_off[lsrc];
+  }
+  if (strategy == kDirOpt) {  // owned unvisited vertices' in-edges (the source is visited)
+    uint64_t e_in = 0, io[2] = {0, 0};
+    ZC_CUDA_TRY(cudaMemcpy(&e_in, g->d_in_off + g->nv, sizeof(e_in), cudaMemcpyDeviceToHost));
+    if (owned)
+      ZC_CUDA_TRY(cudaMemcpy(io, g->d_in_off + lsrc, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    g->p_unvisited_in = e_in - (io[1] - io[0]);
   }
   ZC_CUDA_TRY(cudaStreamSynchronize(st));
   g->p_n = n;
@@ -1487,7 +1503,9 @@ static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
   a.cmp_ww = g->cmp_ww;
   a.cmp_wmin = g->cmp_wmin;
   tune_params(&a);
-  ZC_CUDA_TRY(launch_expand(g->p_strategy, algo + kPartAlgo, g->eb, g->wb, a, g->num_sms, st,
+  // top-down steps of the direction-optimizing strategy are compressed steps
+  const int td = g->p_strategy == kDirOpt ? static_cast<int>(kCompressed) : g->p_strategy;
+  ZC_CUDA_TRY(launch_expand(td, algo + kPartAlgo, g->eb, g->wb, a, g->num_sms, st,
                             &g->p_launches));
   ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (g->p_iter - 1) + 1], st));
   ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr + kCtrBig, 0, sizeof(uint64_t), st));
@@ -1589,12 +1607,124 @@ int zc_part_apply(zc_graph* g, const void* mine, uint64_t* n_next, uint64_t* tra
   c.off = g->d_off;
   c.state = g->d_state;
   c.ctr = g->d_ctr;
+  c.in_off = g->p_strategy == kDirOpt ? g->d_in_off : nullptr;
   ZC_CUDA_TRY(launch_compact(algo, c, st, &g->p_launches));
-  ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                              st));
+  ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, (kCtrTravIn + 1) * sizeof(uint64_t),
+                              cudaMemcpyDeviceToHost, st));
   ZC_CUDA_TRY(cudaStreamSynchronize(st));
   g->p_n = g->h_ctr[kCtrNext];
   g->p_cur ^= 1;
+  if (c.in_off) g->p_unvisited_in -= std::min(g->p_unvisited_in, g->h_ctr[kCtrTravIn]);
+  if (n_next) *n_next = g->h_ctr[kCtrNext];
+  if (trav_next) *trav_next = g->h_ctr[kCtrTrav];
+  return ZC_OK;
+}
+
+int zc_part_unvisited_in(const zc_graph* g, uint64_t* in_edges) {
+  if (!g || !g->nparts || !in_edges) {
+    set_error("not a partition handle");
+    return ZC_ESTATE;
+  }
+  *in_edges = g->p_unvisited_in;
+  return ZC_OK;
+}
+
+int zc_part_frontier_bits(zc_graph* g, uint32_t* bits) {
+  if (!g || !g->nparts || g->p_algo < 0 || !bits) {
+    set_error("zc_part_begin first");
+    return ZC_ESTATE;
+  }
+  DeviceGuard dg(g->device);
+  ZC_CUDA_TRY(launch_frontier_bits(g->d_front[g->p_cur], g->p_n, g->lo, bits,
+                                   (g->global_nv + 31) / 32 + 1, g->num_sms, g->stream,
+                                   &g->p_launches));
+  ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  return ZC_OK;
+}
+
+int zc_part_pull(zc_graph* g, const uint32_t* bits, uint64_t* n_next, uint64_t* trav_next) {
+  if (!g || !g->nparts || g->p_algo != kBfs || g->p_strategy != kDirOpt || !bits) {
+    set_error("zc_part_pull needs a direction-optimizing bfs (zc_part_begin) and the bitmap");
+    return ZC_ESTATE;
+  }
+  DeviceGuard dg(g->device);
+  cudaStream_t st = g->stream;
+  ++g->p_iter;
+  g->log_front.push_back(g->p_n);
+  while (g->iter_ev.size() < 2 * g->p_iter) {
+    cudaEvent_t e;
+    ZC_CUDA_TRY(cudaEventCreate(&e));
+    g->iter_ev.push_back(e);
+  }
+  const int nb = g->p_cur ^ 1;
+  // candidates: owned unvisited vertices with in-edges, sorted, over the in-offsets
+  ZC_CUDA_TRY(launch_part_pull_prepare(g->d_state, g->nv, g->d_visited, g->d_in_off, g->d_cand,
+                                       g->num_sms, st, &g->p_launches));
+  CompactArgs cc{};
+  cc.flags = g->d_cand;
+  cc.nv = g->nv;
+  cc.ntiles = g->ntiles;
+  cc.tiles = g->d_tiles;
+  cc.front_out = g->d_front[nb];
+  cc.fs_out = g->d_fs[nb];
+  cc.fd_out = g->d_fd[nb];
+  cc.fval_out = g->d_fval[nb];
+  cc.off = g->d_in_off;
+  cc.state = g->d_state;
+  cc.ctr = g->d_ctr;
+  ZC_CUDA_TRY(launch_compact(kBfs, cc, st, &g->p_launches));
+  ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  const uint64_t ncand = g->h_ctr[kCtrNext];
+  ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (g->p_iter - 1)], st));
+  ExpandArgs b{};
+  b.front = g->d_front[nb];
+  b.fs = g->d_fs[nb];
+  b.fd = g->d_fd[nb];
+  b.fval = g->d_fval[nb];
+  b.n = ncand;
+  b.off = g->d_in_off;
+  b.state = g->d_state;
+  b.flags = g->d_flags;
+  b.visited = g->d_visited;
+  b.iter = static_cast<uint32_t>(g->p_iter);
+  b.ctr = g->d_ctr;
+  b.wcnt = g->d_wcnt;
+  b.wpre = g->d_wpre;
+  b.scan_tmp = g->d_scan_tmp;
+  b.scan_tmp_bytes = g->scan_tmp_bytes;
+  b.cmp = static_cast<const uint32_t*>(g->d_cmp_in);
+  b.cpos = g->d_cpos_in;
+  b.fbits = bits;
+  tune_params(&b);
+  for (uint32_t pass = 1; pass <= 2; ++pass) {
+    b.pull_pass = pass;
+    ZC_CUDA_TRY(launch_expand(kCompressed, kBfsPull, 4, g->wb, b, g->num_sms, st, &g->p_launches));
+  }
+  ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (g->p_iter - 1) + 1], st));
+  CompactArgs c{};
+  c.flags = g->d_flags;
+  c.nv = g->nv;
+  c.ntiles = g->ntiles;
+  c.tiles = g->d_tiles;
+  c.front_out = g->d_front[nb];
+  c.fs_out = g->d_fs[nb];
+  c.fd_out = g->d_fd[nb];
+  c.fval_out = g->d_fval[nb];
+  c.off = g->d_off;
+  c.state = g->d_state;
+  c.ctr = g->d_ctr;
+  c.in_off = g->d_in_off;
+  ZC_CUDA_TRY(launch_compact(kBfs, c, st, &g->p_launches));
+  ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, (kCtrTravIn + 1) * sizeof(uint64_t),
+                              cudaMemcpyDeviceToHost, st));
+  ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, g->iter_ev[2 * (g->p_iter - 1)], g->iter_ev[2 * (g->p_iter - 1) + 1]);
+  g->log_expand_ms.push_back(ms);
+  g->p_n = g->h_ctr[kCtrNext];
+  g->p_cur = nb;
+  g->p_unvisited_in -= std::min(g->p_unvisited_in, g->h_ctr[kCtrTravIn]);
   if (n_next) *n_next = g->h_ctr[kCtrNext];
   if (trav_next) *trav_next = g->h_ctr[kCtrTrav];
   return ZC_OK;

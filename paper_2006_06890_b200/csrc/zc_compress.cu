@@ -235,6 +235,8 @@ __global__ void k_in_scatter(uint64_t nv, const uint64_t* off, const uint32_t* e
     }
 }
 
+}  // namespace
+
 // device temporaries are released on every path
 struct DevBuf {
   void* p = nullptr;
@@ -248,6 +250,7 @@ struct DevBuf {
 
 // Sorted lists (x) over offsets d_off -> the line stream in device memory
 // (enc) and the per-vertex bit positions (cpos).
+namespace {
 int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t ww, DevBuf* cpos,
                   DevBuf* enc, size_t* bytes) {
   DevBuf size;
@@ -285,6 +288,8 @@ int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t w
   ZC_CUDA_TRY(cudaDeviceSynchronize());
   return ZC_OK;
 }
+
+}  // namespace
 
 // Place an encoded stream like the handle's lists: host (pinned / managed,
 // read zero-copy), managed (UVM) or HBM (with a host shadow).
@@ -328,7 +333,33 @@ int place_stream(zc_graph* g, DevBuf* enc, size_t bytes, void** host_out, const 
   return ZC_OK;
 }
 
-}  // namespace
+int install_in_lists(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted) {
+  DevBuf enc, cpos;
+  Elems x{d_in_sorted, nullptr, 0};
+  size_t bytes = 0;
+  int rc = encode_stream(g->nv, d_in_off, x, 0, &cpos, &enc, &bytes);
+  if (rc) return rc;
+  void* host = nullptr;
+  const void* dev = nullptr;
+  void* hbm = nullptr;
+  if ((rc = place_stream(g, &enc, bytes, &host, &dev, &hbm))) return rc;
+  g->h_cmp_in = host;
+  g->d_cmp_in = dev;
+  g->hbm_cmp_in = hbm;
+  g->d_cpos_in = static_cast<uint64_t*>(cpos.release());
+  g->d_in_off = d_in_off;
+  g->cmp_in_bytes = bytes;
+  if (!g->d_cand) {
+    ZC_CUDA_TRY(cudaMalloc(&g->d_cand, g->vpad));
+    ZC_CUDA_TRY(cudaMemset(g->d_cand, 0, g->vpad));
+  }
+  if (!g->d_fbits) {
+    const uint64_t words = ((g->nparts ? g->global_nv : g->nv) + 31) / 32 + 1;
+    ZC_CUDA_TRY(cudaMalloc(&g->d_fbits, words * sizeof(uint32_t)));
+  }
+  return ZC_OK;
+}
+
 }  // namespace zc
 
 using namespace zc;
@@ -416,6 +447,10 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
   if (rc) return rc;
   cudaSetDevice(g->device);
   const uint64_t nv = g->nv, ne = g->ne;
+  if (g->nparts && (g->flags & ZC_F_DIRECTED)) {
+    set_error("a directed partition's in-lists come from zc_part_build_in_lists");
+    return ZC_EINVAL;
+  }
   if (!(g->flags & ZC_F_DIRECTED)) {  // in-lists are the out-lists
     g->d_in_off = g->d_off;
     g->d_cpos_in = g->d_cpos;
@@ -423,7 +458,7 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
     g->cmp_in_bytes = g->cmp_bytes;
     g->in_alias = true;
   } else {
-    DevBuf out_e, in_e, deg, cursor, in_off, tmp, enc, cpos;
+    DevBuf out_e, in_e, deg, in_off, tmp;
     ZC_CUDA_TRY(cudaMalloc(&out_e.p, std::max<uint64_t>(ne, 1) * 4));
     ZC_CUDA_TRY(cudaMemcpy(out_e.p, g->h_edges, ne * 4, cudaMemcpyDefault));
     ZC_CUDA_TRY(cudaMalloc(&deg.p, std::max<uint64_t>(nv, 1) * 4));
@@ -450,26 +485,18 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
                            cudaMemcpyDeviceToHost));
     rc = sort_lists_device(4, nv, static_cast<uint64_t*>(in_off.p), h_in_off.data(), in_e.p);
     if (rc) return rc;
-    Elems x{static_cast<const uint32_t*>(in_e.p), nullptr, 0};
-    size_t bytes = 0;
-    if ((rc = encode_stream(nv, static_cast<uint64_t*>(in_off.p), x, 0, &cpos, &enc, &bytes)))
+    if ((rc = install_in_lists(g, static_cast<uint64_t*>(in_off.p),
+                               static_cast<uint32_t*>(in_e.p))))
       return rc;
-    cudaFree(in_e.release());
-    void* host = nullptr;
-    const void* dev = nullptr;
-    void* hbm = nullptr;
-    if ((rc = place_stream(g, &enc, bytes, &host, &dev, &hbm))) return rc;
-    g->h_cmp_in = host;
-    g->d_cmp_in = dev;
-    g->hbm_cmp_in = hbm;
-    g->d_cpos_in = static_cast<uint64_t*>(cpos.release());
-    g->d_in_off = static_cast<uint64_t*>(in_off.release());
-    g->cmp_in_bytes = bytes;
+    in_off.release();  // owned by the handle now
   }
   if (!g->d_cand) {
     ZC_CUDA_TRY(cudaMalloc(&g->d_cand, g->vpad));
     ZC_CUDA_TRY(cudaMemset(g->d_cand, 0, g->vpad));
-    ZC_CUDA_TRY(cudaMalloc(&g->d_fbits, ((nv + 31) / 32 + 1) * sizeof(uint32_t)));
+  }
+  if (!g->d_fbits) {
+    const uint64_t words = ((g->nparts ? g->global_nv : nv) + 31) / 32 + 1;
+    ZC_CUDA_TRY(cudaMalloc(&g->d_fbits, words * sizeof(uint32_t)));
   }
   if (compressed_bytes) *compressed_bytes = g->cmp_in_bytes;
   return ZC_OK;

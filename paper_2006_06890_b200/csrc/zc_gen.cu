@@ -113,6 +113,29 @@ __device__ __forceinline__ uint64_t rmat_dst(const RmatParams& p, uint64_t src_o
   return d;
 }
 
+// Arcs of every global source whose destination lies in [lo, lo + nl): count
+// them per local destination (FILL = false), or write the source into the
+// destination's in-list (FILL = true; deg = cursors).
+template <bool FILL>
+__global__ void k_rmat_in_arcs(RmatParams p, uint64_t nv, const uint64_t* goff, uint64_t lo,
+                               uint64_t nl, uint32_t* deg, const uint64_t* in_off,
+                               uint32_t* in_e) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t v = gw; v < nv; v += nw) {
+    const uint64_t s = goff[v], e = goff[v + 1];
+    if (s == e) continue;
+    const uint64_t src_old = p.perm.inv(v);
+    for (uint64_t k = s + lane; k < e; k += 32) {
+      const uint64_t d = p.perm.fwd(rmat_dst(p, src_old, (v << 32) | (k - s)));
+      if (d < lo || d >= lo + nl) continue;
+      const uint32_t slot = atomicAdd(deg + (d - lo), 1u);
+      if (FILL) in_e[in_off[d - lo] + slot] = static_cast<uint32_t>(v);
+    }
+  }
+}
+
 __global__ void k_rmat_count(RmatParams p, uint64_t narcs, uint32_t* deg) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < narcs;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -572,7 +595,67 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
   info.stride = stride;
   if ((rc = init_partition(g, &info))) return fail(rc);
   if ((rc = finish_create(g))) return fail(rc);
+  g->gen_rmat = true;
+  g->gen_scale = scale;
+  g->gen_ef = ef;
+  g->gen_a = a;
+  g->gen_b = b;
+  g->gen_c = c;
+  g->gen_seed = seed;
   *out = guard.release();
+  return ZC_OK;
+}
+
+// In-lists of a generated R-MAT partition: every rank enumerates all arcs
+// (the generator is counter-based) and keeps those whose destination it
+// owns -- no edge exchange between ranks.
+int rmat_part_in_lists(zc_graph* g) {
+  const RmatParams p = rmat_params(g->gen_scale, g->gen_a, g->gen_b, g->gen_c, g->gen_seed);
+  const uint64_t nv = 1ull << g->gen_scale;
+  const uint64_t narcs = static_cast<uint64_t>(g->gen_ef) << g->gen_scale;
+  const uint64_t lo = g->lo, nl = g->nv;
+  Temps t;
+  uint32_t* d_deg = nullptr;
+  uint64_t* d_goff = nullptr;
+  ZC_CUDA_TRY(cudaMalloc(&d_deg, nv * sizeof(uint32_t)));
+  t.add(d_deg);
+  ZC_CUDA_TRY(cudaMemset(d_deg, 0, nv * sizeof(uint32_t)));
+  k_rmat_count<<<kGenGrid, 256>>>(p, narcs, d_deg);
+  ZC_CUDA_TRY(cudaMalloc(&d_goff, (nv + 1) * sizeof(uint64_t)));
+  t.add(d_goff);
+  const size_t tb = scan_tmp_bytes(std::max(nv, nl));
+  void* tmp = nullptr;
+  ZC_CUDA_TRY(cudaMalloc(&tmp, tb));
+  t.add(tmp);
+  ZC_CUDA_TRY(scan_u32_to_u64(d_deg, d_goff, nv, tmp, tb, 0));
+  uint32_t* d_ideg = d_deg;  // reuse: local in-degrees, then cursors
+  ZC_CUDA_TRY(cudaMemset(d_ideg, 0, std::max<uint64_t>(nl, 1) * sizeof(uint32_t)));
+  k_rmat_in_arcs<false><<<kGenGrid, 256>>>(p, nv, d_goff, lo, nl, d_ideg, nullptr, nullptr);
+  uint64_t* d_in_off = nullptr;
+  ZC_CUDA_TRY(cudaMalloc(&d_in_off, (nl + 1) * sizeof(uint64_t)));
+  t.add(d_in_off);
+  ZC_CUDA_TRY(scan_u32_to_u64(d_ideg, d_in_off, nl, tmp, tb, 0));
+  uint64_t ne_in = 0;
+  ZC_CUDA_TRY(cudaMemcpy(&ne_in, d_in_off + nl, sizeof(ne_in), cudaMemcpyDeviceToHost));
+  uint32_t* d_in = nullptr;
+  ZC_CUDA_TRY(cudaMalloc(&d_in, std::max<uint64_t>(ne_in, 32) * sizeof(uint32_t)));
+  t.add(d_in);
+  ZC_CUDA_TRY(cudaMemset(d_ideg, 0, std::max<uint64_t>(nl, 1) * sizeof(uint32_t)));
+  k_rmat_in_arcs<true><<<kGenGrid, 256>>>(p, nv, d_goff, lo, nl, d_ideg, d_in_off, d_in);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    set_error(std::string("rmat in-lists: ") + cudaGetErrorString(cudaGetLastError()));
+    return ZC_ECUDA;
+  }
+  t.release(d_goff);
+  t.release(d_deg);
+  std::vector<int64_t> h_in_off(nl + 1);
+  ZC_CUDA_TRY(cudaMemcpy(h_in_off.data(), d_in_off, (nl + 1) * sizeof(uint64_t),
+                         cudaMemcpyDeviceToHost));
+  int rc = sort_lists<uint32_t>(nl, d_in_off, h_in_off.data(), d_in);
+  if (rc) return rc;
+  ZC_CUDA_TRY(cudaDeviceSynchronize());
+  if ((rc = install_in_lists(g, d_in_off, d_in))) return rc;
+  t.forget(d_in_off);  // the handle owns it
   return ZC_OK;
 }
 
@@ -716,6 +799,8 @@ int generate_uniform(uint64_t nv, uint32_t dmin, uint32_t dmax, uint64_t seed, i
 
 }  // namespace
 
+int part_in_lists(zc_graph* g) { return rmat_part_in_lists(g); }
+
 int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, const int64_t* h_off,
                       void* edges) {
   int rc = elem_bytes == 4 ? sort_lists<uint32_t>(nv, d_off, h_off, static_cast<uint32_t*>(edges))
@@ -751,4 +836,26 @@ extern "C" int zc_generate_rmat_part(uint32_t scale, uint32_t edge_factor, doubl
   if (!out) return ZC_ESTATE;
   return zc::generate_rmat_part(scale, edge_factor, a, b, c, seed, wlow, whigh, nparts, part,
                                 placement, device, bounds, out);
+}
+
+extern "C" int zc_part_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) {
+  if (!g || !g->nparts) {
+    zc::set_error("not a partition handle");
+    return ZC_ESTATE;
+  }
+  if (g->d_cpos_in) {
+    if (compressed_bytes) *compressed_bytes = g->cmp_in_bytes;
+    return ZC_OK;
+  }
+  if (!(g->flags & ZC_F_DIRECTED)) return zc_graph_build_in_lists(g, compressed_bytes);
+  if (!g->gen_rmat) {
+    zc::set_error("in-lists of a directed partition need its generator (zc_generate_rmat_part)");
+    return ZC_EINVAL;
+  }
+  int rc = zc_graph_build_compressed(g, nullptr);
+  if (rc) return rc;
+  cudaSetDevice(g->device);
+  if ((rc = zc::part_in_lists(g))) return rc;
+  if (compressed_bytes) *compressed_bytes = g->cmp_in_bytes;
+  return ZC_OK;
 }

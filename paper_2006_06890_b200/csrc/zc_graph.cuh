@@ -60,6 +60,13 @@ struct zc_graph {
   bool in_alias = false;
   uint8_t* d_cand = nullptr;
   uint32_t* d_fbits = nullptr;
+  // R-MAT partitions remember their generator, so their in-lists (arcs from
+  // any rank into the owned range) can be generated on demand
+  bool gen_rmat = false;
+  uint32_t gen_scale = 0, gen_ef = 0;
+  double gen_a = 0, gen_b = 0, gen_c = 0;
+  uint64_t gen_seed = 0;
+  uint64_t p_unvisited_in = 0;  // partition: owned unvisited vertices' in-edges
   // optional interleaved (dst, weight) u32 pairs for SSSP (zc_graph_build_pairs)
   void* h_pairs = nullptr;
   const void* d_pairs = nullptr;
@@ -141,6 +148,12 @@ void pinned_list_free(void* p);
 // pinned_list_free; host_list_device_ptr gives the address kernels use.
 void* host_list_alloc(const zc_graph* g, size_t bytes);
 int host_list_device_ptr(void* p, const void** d);
+// Compress the handle's sorted in-lists (device offsets + u32 lists, both
+// over the handle's own vertices) into its in-list line stream; takes
+// ownership of d_in_off (zc_compress.cu).
+int install_in_lists(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted);
+// In-lists of a generated R-MAT partition (zc_gen.cu).
+int part_in_lists(zc_graph* g);
 inline bool placement_valid(int32_t p) { return p >= ZC_PLACE_ZEROCOPY && p <= ZC_PLACE_ZEROCOPY_MANAGED; }
 // Adopt a list generated in HBM (d_src, n elements of width w) into the
 // handle's placement; frees d_src unless it becomes the HBM copy.

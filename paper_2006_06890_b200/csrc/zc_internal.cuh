@@ -210,6 +210,15 @@ cudaError_t launch_fill_exchange(int algo, void* x, uint64_t n, cudaStream_t st,
                                  uint64_t* launches);
 cudaError_t launch_part_apply(int algo, const void* mine, uint64_t nlocal, void* state,
                               uint8_t* flags, uint32_t iter, cudaStream_t st, uint64_t* launches);
+// Frontier bitmap over global ids: zero `words` words, set vbase + front[j].
+cudaError_t launch_frontier_bits(const uint32_t* front, uint64_t n, uint64_t vbase,
+                                 uint32_t* bits, uint64_t words, int num_sms, cudaStream_t st,
+                                 uint64_t* launches);
+// Partition bottom-up inputs: the owned range's visited bitmap from its
+// levels, then the candidate marks.
+cudaError_t launch_part_pull_prepare(const void* level, uint64_t nv, uint32_t* visited,
+                                     const uint64_t* in_off, uint8_t* cand, int num_sms,
+                                     cudaStream_t st, uint64_t* launches);
 // BFS levels (all below 255) as u8, 0xff = unreached.
 cudaError_t launch_narrow_levels(const void* state, uint64_t nv, uint8_t* out, cudaStream_t st,
                                  uint64_t* launches);

@@ -1531,11 +1531,25 @@ cudaError_t launch_traffic_model(int strategy, int edge_bytes, int weight_bytes,
 namespace {
 // Bottom-up step inputs: the current frontier as a bitmap, and the candidate
 // marks (unvisited vertices with in-edges), 16 vertices per thread.
-__global__ void k_fbits_set(const uint32_t* front, uint64_t n, uint32_t* fbits) {
+__global__ void k_fbits_set(const uint32_t* front, uint64_t n, uint64_t vbase, uint32_t* fbits) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
        j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = front[j];
+    const uint64_t v = vbase + front[j];
     atomicOr(fbits + (v >> 5), 1u << (v & 31));
+  }
+}
+
+// Visited bitmap of a partition's owned range from its levels.
+__global__ void k_visited_from_levels(const uint32_t* level, uint64_t nv, uint32_t* visited) {
+  const uint64_t nw = (nv + 31) / 32;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+      const uint64_t v = w * 32 + b;
+      if (v < nv && level[v] != kUnreached32) bits |= 1u << b;
+    }
+    visited[w] = bits;
   }
 }
 
@@ -1568,7 +1582,30 @@ cudaError_t launch_pull_prepare(const uint32_t* front, uint64_t n, uint32_t* fbi
                                 uint8_t* cand, int num_sms, cudaStream_t st, uint64_t* launches) {
   cudaError_t e = cudaMemsetAsync(fbits, 0, ((nv + 31) / 32 + 1) * sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
-  if (n) k_fbits_set<<<grid_for(n, 256, num_sms, 16), 256, 0, st>>>(front, n, fbits);
+  if (n) k_fbits_set<<<grid_for(n, 256, num_sms, 16), 256, 0, st>>>(front, n, 0, fbits);
+  k_cand_marks<<<grid_for((nv + 15) / 16, 256, num_sms, 16), 256, 0, st>>>(nv, visited, in_off,
+                                                                            cand);
+  *launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_frontier_bits(const uint32_t* front, uint64_t n, uint64_t vbase,
+                                 uint32_t* bits, uint64_t words, int num_sms, cudaStream_t st,
+                                 uint64_t* launches) {
+  cudaError_t e = cudaMemsetAsync(bits, 0, words * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return e;
+  if (n) {
+    k_fbits_set<<<grid_for(n, 256, num_sms, 16), 256, 0, st>>>(front, n, vbase, bits);
+    *launches += 1;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_part_pull_prepare(const void* level, uint64_t nv, uint32_t* visited,
+                                     const uint64_t* in_off, uint8_t* cand, int num_sms,
+                                     cudaStream_t st, uint64_t* launches) {
+  k_visited_from_levels<<<grid_for((nv + 31) / 32, 256, num_sms, 16), 256, 0, st>>>(
+      static_cast<const uint32_t*>(level), nv, visited);
   k_cand_marks<<<grid_for((nv + 15) / 16, 256, num_sms, 16), 256, 0, st>>>(nv, visited, in_off,
                                                                             cand);
   *launches += 2;

@@ -147,6 +147,25 @@ class CudaPartition:
         N.check(N.lib().zc_part_apply(self._h, mine.data_ptr(), C.byref(n), C.byref(t)))
         return n.value, t.value
 
+    # -- direction-optimizing bfs: bottom-up steps against the global frontier bitmap
+    @property
+    def bitmap_words(self) -> int:
+        return (int(self.bounds[-1]) + 31) // 32 + 1
+
+    def unvisited_in(self) -> int:
+        x = C.c_uint64()
+        N.check(N.lib().zc_part_unvisited_in(self._h, C.byref(x)))
+        return x.value
+
+    def frontier_bits(self, bits) -> None:
+        """Zero `bits` (device, bitmap_words int32) and set the owned frontier's bits."""
+        N.check(N.lib().zc_part_frontier_bits(self._h, bits.data_ptr()))
+
+    def pull(self, bits) -> tuple[int, int]:
+        n, t = C.c_uint64(), C.c_uint64()
+        N.check(N.lib().zc_part_pull(self._h, bits.data_ptr(), C.byref(n), C.byref(t)))
+        return n.value, t.value
+
     def graph_view(self):
         """DeviceGraph-style host views (offsets, edges, weights) of this part."""
         from .device import DeviceGraph
@@ -267,19 +286,38 @@ def run_partition(engine: Engine, algo: str, source: int, strategy, *, group=Non
         h_exch, h_mine = exch.cpu(), mine.cpu()
     op = dist.ReduceOp.MAX if algo == "bfs" else dist.ReduceOp.MIN
     cdev = torch.device("cpu") if stage_host else dev
-    counts = torch.zeros(2, dtype=torch.int64, device=cdev)
+    counts = torch.zeros(3, dtype=torch.int64, device=cdev)
+    dobfs = is_direction_optimizing(strategy)
 
-    def global_counts(n: int, t: int) -> tuple[int, int]:
+    def global_counts(n: int, t: int) -> tuple[int, int, int]:
         counts[0], counts[1] = n, t
+        counts[2] = engine.unvisited_in() if dobfs else 0
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
-        return int(counts[0]), int(counts[1])
+        return int(counts[0]), int(counts[1]), int(counts[2])
 
-    n, t = global_counts(*engine.begin(algo, source, strategy))
+    def pull_step():
+        # the owned frontiers' disjoint bits, OR-ed by a SUM all-reduce
+        bits = torch.empty(engine.bitmap_words, dtype=torch.int32, device=dev)
+        engine.frontier_bits(bits)
+        if stage_host:
+            hb = bits.cpu()
+            dist.all_reduce(hb, op=dist.ReduceOp.SUM, group=group)
+            bits.copy_(hb)
+        else:
+            dist.all_reduce(bits, op=dist.ReduceOp.SUM, group=group)
+        if dev.type == "cuda":
+            torch.cuda.current_stream(dev).synchronize()
+        return engine.pull(bits)
+
+    n, t, m = global_counts(*engine.begin(algo, source, strategy))
     iters, trav, front = 0, [], []
     while n > 0:
         iters += 1
         trav.append(t)
         front.append(n)
+        if dobfs and pull_now(iters, t, m):
+            n, t, m = global_counts(*pull_step())
+            continue
         engine.expand(exch)                      # device work done when this returns
         if stage_host:
             h_exch.copy_(exch)
@@ -289,9 +327,27 @@ def run_partition(engine: Engine, algo: str, source: int, strategy, *, group=Non
             dist.reduce_scatter_tensor(mine, exch, op=op, group=group)
         if dev.type == "cuda":
             torch.cuda.current_stream(dev).synchronize()
-        n, t = global_counts(*engine.apply(mine))
+        n, t, m = global_counts(*engine.apply(mine))
     values = engine.result() if fetch else None
     return PartResult(algo, engine.lo, values, iters, trav, front)
+
+
+def is_direction_optimizing(strategy) -> bool:
+    return strategy_id(strategy) == 5
+
+
+def do_alpha() -> float:
+    """The direction switch factor: ZC_TUNE=do_alpha=X, default 2 (as zc_api.cu)."""
+    import os
+    import re
+    m = re.search(r"do_alpha=([0-9.]+)", os.environ.get("ZC_TUNE", ""))
+    return float(m.group(1)) if m and float(m.group(1)) > 0 else 2.0
+
+
+def pull_now(iteration: int, frontier_out_edges: int, unvisited_in_edges: int) -> bool:
+    """Bottom-up when the frontier's out-edges exceed the unvisited vertices'
+    in-edges / alpha (never the source's own expansion) -- zc_api.cu's rule."""
+    return iteration > 1 and frontier_out_edges * do_alpha() > unvisited_in_edges
 
 
 def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartResult:
@@ -320,17 +376,36 @@ def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartRe
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
         return int(counts[0]), int(counts[1])
 
-    n, t = global_counts(*engine.begin(algo, source, strategy))
+    dobfs = is_direction_optimizing(strategy)
+    counts3 = torch.zeros(3, dtype=torch.int64, device=cdev)
+
+    def global_counts3(n: int, t: int) -> tuple[int, int, int]:
+        counts3[0], counts3[1] = n, t
+        counts3[2] = engine.unvisited_in() if dobfs else 0
+        dist.all_reduce(counts3, op=dist.ReduceOp.SUM, group=group)
+        return int(counts3[0]), int(counts3[1]), int(counts3[2])
+
+    n, t, m = global_counts3(*engine.begin(algo, source, strategy))
     iters, trav, front = 0, [], []
     while n > 0:
         iters += 1
         trav.append(t)
         front.append(n)
+        if dobfs and pull_now(iters, t, m):
+            bits = torch.empty(engine.bitmap_words, dtype=torch.int32, device=dev)
+            engine.frontier_bits(bits)
+            hb = bits.cpu() if cdev.type == "cpu" else bits
+            dist.all_reduce(hb, op=dist.ReduceOp.SUM, group=group)
+            if cdev.type == "cpu":
+                bits.copy_(hb)
+            torch.cuda.current_stream(dev).synchronize()
+            n, t, m = global_counts3(*engine.pull(bits))
+            continue
         engine.fused_reset()
         sync_all()              # every owner buffer reset before anyone writes
         engine.fused_expand()   # kernel done (its peer stores performed) on return
         sync_all()              # every rank's candidates delivered
-        n, t = global_counts(*engine.apply_ptr(local))
+        n, t, m = global_counts3(*engine.apply_ptr(local))
     values = engine.result() if fetch else None
     return PartResult(algo, engine.lo, values, iters, trav, front)
 
@@ -351,6 +426,26 @@ def run_partitions_local(engines: Sequence[Engine], algo: str, source: int, stra
     validate the partitioned kernels on a single GPU."""
     import torch
 
+    dobfs = is_direction_optimizing(strategy)
+
+    def unvisited_in() -> int:
+        return sum(e.unvisited_in() for e in engines) if dobfs else 0
+
+    def pull_all() -> tuple[int, int]:
+        """Bottom-up step of every partition against the OR of their frontiers."""
+        dev = torch.device("cuda", engines[0].device)
+        parts = []
+        for e in engines:
+            b = torch.empty(e.bitmap_words, dtype=torch.int32, device=dev)
+            e.frontier_bits(b)
+            parts.append(b)
+        bits = parts[0]
+        for b in parts[1:]:
+            bits = torch.bitwise_or(bits, b)
+        torch.cuda.synchronize(dev)
+        nt = [e.pull(bits) for e in engines]
+        return sum(x[0] for x in nt), sum(x[1] for x in nt)
+
     if fused:
         locals_ = [e.fused_init(algo)[1] for e in engines]
         for e in engines:
@@ -361,6 +456,9 @@ def run_partitions_local(engines: Sequence[Engine], algo: str, source: int, stra
         while n > 0:
             iters += 1
             trav.append(t)
+            if dobfs and pull_now(iters, t, unvisited_in()):
+                n, t = pull_all()
+                continue
             for e in engines:
                 e.fused_reset()
             for e in engines:
@@ -381,6 +479,9 @@ def run_partitions_local(engines: Sequence[Engine], algo: str, source: int, stra
     while n > 0:
         iters += 1
         trav.append(t)
+        if dobfs and pull_now(iters, t, unvisited_in()):
+            n, t = pull_all()
+            continue
         for e, b in zip(engines, bufs):
             e.expand(b)
         st = torch.stack(bufs)

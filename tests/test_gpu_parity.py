@@ -593,3 +593,33 @@ def test_direction_optimizing_rejects_other_algorithms():
         zc.cc(zc.symmetrized(g), "direction-optimizing", collect_traffic=False)
     with pytest.raises(ValueError, match="request model"):
         zc.bfs(g, 0, "direction-optimizing", collect_traffic=True)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_cuda_partitions_direction_optimizing(fused):
+    """Direction-optimizing partitions: bottom-up steps against the OR of the
+    owned frontiers' bitmaps; generated directed R-MAT partitions (in-lists
+    from the counter-based generator) and undirected local partitions (in-lists
+    = out-lists).  Identical to the oracle."""
+    whole = zc.generate_rmat(16, 16, seed=11).as_csr()
+    src = int(zc.pick_sources(whole, 1, seed=7)[0])
+    ref = oracle.bfs(whole, src, threads=8)
+    for nparts in (1, 2, 3):
+        engines = [generate_rmat_part(16, nparts, k, seed=11) for k in range(nparts)]
+        vals, iters, trav = run_partitions_local(engines, "bfs", src, "direction-optimizing",
+                                                 fused=fused)
+        assert np.array_equal(vals, ref.values), nparts
+        assert iters == ref.iterations and trav == ref.traversed_edges
+        for e in engines:
+            e.close()
+    gu = zc.symmetrized(zc.generate_powerlaw(1 << 14, 12, seed=3))
+    src = int(zc.pick_sources(gu, 1, seed=7)[0])
+    ref = oracle.bfs(gu, src)
+    for nparts in (2, 3):
+        b = edge_balanced_bounds(gu.offsets, nparts)
+        engines = [CudaPartition(local_part(gu, b, k), b, k) for k in range(nparts)]
+        vals, iters, trav = run_partitions_local(engines, "bfs", src, "direction-optimizing",
+                                                 fused=fused)
+        assert np.array_equal(vals, ref.values) and trav == ref.traversed_edges
+        for e in engines:
+            e.close()
