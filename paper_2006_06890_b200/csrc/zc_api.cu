@@ -43,10 +43,11 @@ namespace zc {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
-// Run fn(lo, hi) over [0, n) on all host cores.
+// Run fn(lo, hi) over [0, n) on all host cores but `spare`.
 template <typename F>
-static void parallel_for(uint64_t n, F fn) {
-  unsigned nt = std::max(1u, std::thread::hardware_concurrency());
+static void parallel_for(uint64_t n, F fn, unsigned spare = 0) {
+  const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+  unsigned nt = hc > spare + 1 ? hc - spare : 1;
   if (n < (1u << 16)) nt = 1;
   if (nt == 1) {
     fn(uint64_t(0), n);
@@ -248,11 +249,16 @@ __attribute__((constructor)) static void install_segv_trace() {
 }
 
 // int64 BFS levels from the narrowed download (0xff = unreached -> -1,
-// traversal.py:22), on the host cores.
+// traversal.py:22), on the host cores but two: the widen of one result runs
+// while the caller's thread drives the next traversal's level loop.
 static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n) {
-  parallel_for(n, [&](uint64_t lo, uint64_t hi) {
-    for (uint64_t i = lo; i < hi; ++i) out[i] = src[i] == 0xffu ? -1ll : static_cast<int64_t>(src[i]);
-  });
+  parallel_for(
+      n,
+      [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t i = lo; i < hi; ++i)
+          out[i] = src[i] == 0xffu ? -1ll : static_cast<int64_t>(src[i]);
+      },
+      2);
 }
 
 static double now_ms() {
