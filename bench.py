@@ -329,7 +329,8 @@ def main():
 
     # GB/s of list data the expansion kernels must read over the link
     achieved = link_bytes / (expand_ms * 1e-3) / 1e9
-    ncu = load_ncu_summary().get("bfs_expand", {})
+    summ = load_ncu_summary()
+    ncu = summ.get("bfs_expand_dobfs" if strat == "direction-optimizing" else "bfs_expand", {})
     line = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
