@@ -16,7 +16,7 @@ for r in rows[1:]:
     scale = {"ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(r[ui], 1e-6)
     tot[name] += v * scale
     cnt[name] += 1
-trav = {k: v for k, v in tot.items() if k.startswith(("k_expand", "k_window", "k_tile", "k_level",
+trav = {k: v for k, v in tot.items() if k.startswith(("k_expand", "k_window", "k_tile", "k_level", "k_cand", "k_fbits", "k_narrow",
                                                      "k_init", "k_widen", "cub::DeviceScan",
                                                      "DeviceScan", "k_scan"))}
 s = sum(trav.values())
