@@ -15,11 +15,12 @@ import paper_2006_06890_b200 as zc
 from paper_2006_06890_b200.multi import edge_balanced_bounds, exchange_stride, local_part
 
 
-def _run_world(world, graphs, algos, sources):
+def _run_world(world, graphs, algos, sources, strategy="merged-aligned"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = random.randint(20000, 40000)
-    ps = [ctx.Process(target=gloo_worker, args=(r, world, port, graphs, algos, sources, q))
+    ps = [ctx.Process(target=gloo_worker,
+                      args=(r, world, port, graphs, algos, sources, q, strategy))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -74,3 +75,29 @@ def test_edge_balanced_bounds():
         parts = [local_part(g, b, k) for k in range(p)]
         assert sum(x.num_vertices for x in parts) == g.num_vertices
         assert exchange_stride(b) == int(np.diff(b).max())
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_direction_optimizing_driver(world):
+    """Direction-optimizing SPMD protocol: top-down steps by reduce-scatter,
+    bottom-up steps against the SUM-all-reduced (= OR) owned-frontier bitmaps,
+    switch test on all-reduced unvisited in-edges -- reference levels,
+    iterations and traversed edges on directed and undirected graphs."""
+    g = zc.generate_powerlaw(4000, 12.0, 2.0, seed=6)
+    gu = zc.symmetrized(g)
+    cases = [c for c in _cases() if c.algo == "bfs"]
+    graphs = [g, gu] + [c.graph for c in cases]
+    srcs = [int(zc.pick_sources(g, 1)[0]), int(zc.pick_sources(gu, 1)[0])] + \
+           [max(c.source, 0) for c in cases]
+    got = _run_world(world, graphs, ["bfs"] * len(graphs), srcs, "direction-optimizing")
+    for gr, s, (vals, iters, trav) in zip(graphs, srcs, got):
+        ref = oracle.bfs(gr, s)
+        assert np.array_equal(vals, ref.values)
+        assert iters == ref.iterations and trav == ref.traversed_edges
+
+
+def test_pull_rule():
+    from paper_2006_06890_b200.multi import do_alpha, pull_now
+    assert do_alpha() == 2.0
+    assert not pull_now(1, 10**9, 1)          # never the source's own expansion
+    assert pull_now(2, 600, 1000) and not pull_now(2, 400, 1000)
