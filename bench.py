@@ -43,7 +43,7 @@ METRIC = "BFS GTEPS (Kronecker scale-27, edge list zero-copy in pinned host memo
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--scale", type=int, default=27)
@@ -297,10 +297,10 @@ def main():
     # timed region 2: end to end through the public API (host wall clock).
     # bfs_many = the reference's per-source loop (report.py:168-170) as one
     # call: each source's int64 levels download to pinned host memory while
-    # the next source streams the edge list.  Batches of <= 8 sources keep
+    # the next source streams the edge list.  Batches of <= 10 sources keep
     # the result buffers inside the pinned pool (warmed here, untimed).
     step_srcs = [int(sources[(args.warmup + i) % 64]) for i in range(args.steps)]
-    batch = min(8, args.steps)
+    batch = min(10, args.steps)
     r = None
     zc.bfs_many(dg, step_srcs[:batch], strat)
     barrier(world, device)

@@ -32,7 +32,7 @@ class _PinnedPool:
     """Recycles pinned host buffers of result arrays (D2H at link speed
     without paying cudaHostAlloc on every call)."""
 
-    def __init__(self, cap_bytes: int = 8 << 30):
+    def __init__(self, cap_bytes: int = 16 << 30):
         self.free: dict[int, list[int]] = {}
         self.pooled = 0
         self.cap = cap_bytes

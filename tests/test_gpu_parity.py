@@ -158,9 +158,17 @@ def test_edge_cases():
     off = np.array([0, 3] + [3 + n] * (n - 1), np.int64)
     edges = np.concatenate([[1, 2, 3], np.arange(1, n + 1) % n]).astype(np.int64)
     g = zc.CsrGraph(n, int(off[-1]), off, edges)
-    for s in ALL:
+    for s in ALL + ["compressed", "direction-optimizing"]:
         r = zc.bfs(g, 1, s, collect_traffic=False)
         assert np.array_equal(r.values, oracle.bfs(g, 1).values)
+    # compressed / direction-optimizing on the degenerate graphs
+    for s in ("compressed", "direction-optimizing"):
+        assert zc.bfs(single, 0, s, collect_traffic=False).values.tolist() == [0]
+        nolinks = zc.CsrGraph(5, 0, np.zeros(6, np.int64), np.zeros(0, np.int64))
+        r = zc.bfs(nolinks, 2, s, collect_traffic=False)
+        assert r.values.tolist() == [-1, -1, 0, -1, -1] and r.iterations == 1
+    assert zc.sssp(single, 0, "compressed", collect_traffic=False).values.tolist() == [0]
+    assert zc.cc(empty, "compressed", collect_traffic=False).values.size == 0
 
 
 def test_packed_many_empty_and_shared_blocks():

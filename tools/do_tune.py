@@ -3,7 +3,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2006_06890_b200 as zc
 
-dg = zc.generate_rmat(27, 16, seed=27)
+dg = zc.generate_rmat(27, 16, seed=27, placement=os.environ.get("PLACEMENT", "zerocopy"))
 srcs = [int(s) for s in zc.pick_sources(dg.as_csr(), 64, seed=7)[:16]]
 zc.bfs(dg, srcs[0], "direction-optimizing", collect_traffic=False)
 for tune in sys.argv[1:]:
