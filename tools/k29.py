@@ -21,9 +21,11 @@ print(f"gen {time.time()-t:.1f}s V={dg.num_vertices} E={dg.num_edges} "
       f"({dg.num_edges*4/2**30:.0f} GiB u32 lists pinned)", flush=True)
 g = dg.as_csr()
 src = int(zc.pick_sources(g, 64, seed=7)[0])
+results = {}
 for s in a.strategies.split(","):
     for rep in range(2):
         r = zc.bfs(dg, src, s, collect_traffic=False)
+    results[s] = r
     print(f"bfs {s:15s} src={src} iters={r.iterations} kernel={r.kernel_ms:.1f}ms "
           f"GTEPS={r.total_traversed_edges/r.kernel_ms/1e6:.3f} "
           f"link={r.total_traversed_edges*4/r.expand_ms/1e6:.2f}GB/s", flush=True)
@@ -31,8 +33,10 @@ if not a.no_oracle:
     import oracle
     t = time.time()
     ref = oracle.bfs(g, src, threads=os.cpu_count())
-    print(f"oracle bfs {time.time()-t:.1f}s same={np.array_equal(ref.values, r.values)} "
-          f"trav_same={ref.traversed_edges == list(r.traversed_edges)}", flush=True)
+    print(f"oracle bfs {time.time()-t:.1f}s", flush=True)
+    for s, r in results.items():
+        print(f"  {s}: same={np.array_equal(ref.values, r.values)} "
+              f"trav_same={ref.traversed_edges == list(r.traversed_edges)}", flush=True)
 if a.cc:
     r = zc.cc(dg, "packed", collect_traffic=False)
     print(f"cc packed iters={r.iterations} kernel={r.kernel_ms:.1f}ms "
