@@ -16,6 +16,7 @@
 
 #include <dirent.h>
 #include <dlfcn.h>
+#include <immintrin.h>
 #include <execinfo.h>
 #include <fcntl.h>
 #include <signal.h>
@@ -251,10 +252,40 @@ __attribute__((constructor)) static void install_segv_trace() {
 // int64 BFS levels from the narrowed download (0xff = unreached -> -1,
 // traversal.py:22), on the host cores but two: the widen of one result runs
 // while the caller's thread drives the next traversal's level loop.
+// AVX2 body: 8 levels per step, streamed (non-temporal) stores so the 8 B
+// per vertex written do not also cost a read-for-ownership of host memory
+// the GPU is streaming lists from.
+__attribute__((target("avx2"))) static void widen_levels_avx2(const uint8_t* src, int64_t* out,
+                                                              uint64_t lo, uint64_t hi) {
+  uint64_t i = lo;
+  for (; i < hi && (reinterpret_cast<uintptr_t>(out + i) & 31); ++i)
+    out[i] = src[i] == 0xffu ? -1ll : static_cast<int64_t>(src[i]);
+  const __m256i ff = _mm256_set1_epi64x(0xff);
+  for (; i + 8 <= hi; i += 8) {
+    uint64_t b8;
+    memcpy(&b8, src + i, 8);
+    const __m128i b = _mm_cvtsi64_si128(static_cast<long long>(b8));
+    __m256i lo4 = _mm256_cvtepu8_epi64(b);
+    __m256i hi4 = _mm256_cvtepu8_epi64(_mm_srli_si128(b, 4));
+    // 0xff (unreached) -> -1: OR in the all-ones mask of the equal lanes
+    lo4 = _mm256_or_si256(lo4, _mm256_cmpeq_epi64(lo4, ff));
+    hi4 = _mm256_or_si256(hi4, _mm256_cmpeq_epi64(hi4, ff));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(out + i), lo4);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(out + i + 4), hi4);
+  }
+  for (; i < hi; ++i) out[i] = src[i] == 0xffu ? -1ll : static_cast<int64_t>(src[i]);
+  _mm_sfence();
+}
+
 static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
   parallel_for(
       n,
       [&](uint64_t lo, uint64_t hi) {
+        if (avx2) {
+          widen_levels_avx2(src, out, lo, hi);
+          return;
+        }
         for (uint64_t i = lo; i < hi; ++i)
           out[i] = src[i] == 0xffu ? -1ll : static_cast<int64_t>(src[i]);
       },
@@ -957,6 +988,12 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
       // the remaining lines of long in-lists still without one
       b.pull_pass = 1;
       ZC_CUDA_TRY(launch_expand(kCompressed, kBfsPull, 4, g->wb, b, g->num_sms, st, &launches));
+      if (getenv("ZC_DEBUG_DO")) {  // bytes after pass 1
+        ZC_CUDA_TRY(cudaMemcpyAsync(&g->h_small[0], g->d_ctr + kCtrLoaded, sizeof(uint64_t),
+                                    cudaMemcpyDeviceToHost, st));
+        ZC_CUDA_TRY(cudaStreamSynchronize(st));
+        fprintf(stderr, "zc-do   pass1 loaded=%lu\n", (unsigned long)g->h_small[0]);
+      }
       b.pull_pass = 2;
       ZC_CUDA_TRY(launch_expand(kCompressed, kBfsPull, 4, g->wb, b, g->num_sms, st, &launches));
     } else {
