@@ -103,7 +103,7 @@ __global__ void k_cmp_size(uint64_t nv, const uint64_t* off, Elems x, uint32_t w
     uint32_t out = 0;
     if (d) {
       const uint64_t sb = short_bits(d, list_width(x, s, d, lane), ww);
-      if (sb <= kLineBits && d <= kCmpShortMaxDeg) {  // one lane decodes a short list
+      if (sb <= kShortSpanBits && d <= kCmpShortMaxDeg) {  // one lane decodes a short list
         out = static_cast<uint32_t>(sb);
       } else {
         uint32_t n = 0;
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256) k_cmp_encode(uint64_t nv, const uint64_t*
       }
       continue;
     }
-    const uint64_t l0 = pos / kLineBits, nl = (cmp_pos(cpos[v + 1]) - pos) / kLineBits;
+    const uint64_t l0 = pos / kLineBits, nl = cmp_lines(c);
     uint64_t p = 0;
     for (uint64_t t = 0; t < nl; ++t) {
       uint32_t cnt, w;
@@ -267,16 +267,26 @@ int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t w
   for (uint64_t v = 0; v < nv; ++v) {
     const uint32_t sz = hs[v];
     if (sz & kLongSize) {
+      const uint64_t nl = sz & ~kLongSize;
+      if (nl > kCmpMaxLines) {
+        set_error("a list needs more compressed lines than the index can record");
+        return ZC_EINVAL;
+      }
       pos = round_line(pos);
-      hp[v] = pos | kCmpLong;
-      pos += static_cast<uint64_t>(sz & ~kLongSize) * kLineBits;
+      hp[v] = pos | kCmpLong | (nl << kCmpPosBits);
+      pos += nl * kLineBits;
     } else {
-      if (sz && (pos % kLineBits) + sz > kLineBits) pos = round_line(pos);
+      if (sz && (pos % kShortSpanBits) + sz > kShortSpanBits)  // next 256-byte span
+        pos = (pos + kShortSpanBits - 1) / kShortSpanBits * kShortSpanBits;
       hp[v] = pos;
       pos += sz;
     }
   }
   hp[nv] = round_line(pos);
+  if (hp[nv] > kCmpPosMask) {
+    set_error("compressed stream exceeds the index's 2^40-bit positions");
+    return ZC_EINVAL;
+  }
   const uint64_t lines = hp[nv] / kLineBits;
   ZC_CUDA_TRY(cudaMalloc(&cpos->p, (nv + 1) * sizeof(uint64_t)));
   ZC_CUDA_TRY(cudaMemcpy(cpos->p, hp.data(), (nv + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice));

@@ -64,7 +64,7 @@ enum Strategy : int {
 //     [6,14) count - 1 (<= 255); from bit 48: count-1 deltas of w bits, then
 //     (weighted) count weights of ww bits.
 // Per-vertex cpos (u64[V+1], HBM): bit position of the list in the stream,
-// kCmpLong set for long lists (their lines end where the next list starts).
+// kCmpLong and the line count for long lists (layout below).
 // A window is one line: a long list's lines, or a shared line of short lists
 // fetched once for all its frontier lists.
 constexpr uint32_t kCmpHdrBits = 48;
@@ -73,8 +73,21 @@ constexpr uint32_t kCmpMaxCount = 256;
 constexpr uint32_t kLineWords = 32;
 constexpr uint32_t kLineBits = 1024;
 constexpr uint32_t kCmpShortMaxDeg = 64;
+// Short lists are packed into 256-byte spans (two lines) and never straddle
+// one: a U27 SSSP list (540 bits) then shares its span with two others.
+constexpr uint32_t kShortSpanBits = 2 * kLineBits;
+constexpr uint32_t kShortSpanWords = 2 * kLineWords;
+// cpos word: bit 63 = long list; bits [40, 63) = a long list's line count
+// (padding may follow it, so it is not the gap to the next list); bits
+// [0, 40) = the bit position in the stream (streams up to 128 GiB).
 constexpr uint64_t kCmpLong = 1ull << 63;
-__host__ __device__ __forceinline__ uint64_t cmp_pos(uint64_t c) { return c & ~kCmpLong; }
+constexpr int kCmpPosBits = 40;
+constexpr uint64_t kCmpPosMask = (1ull << kCmpPosBits) - 1;
+constexpr uint64_t kCmpMaxLines = (1ull << (63 - kCmpPosBits)) - 1;
+__host__ __device__ __forceinline__ uint64_t cmp_pos(uint64_t c) { return c & kCmpPosMask; }
+__host__ __device__ __forceinline__ uint64_t cmp_lines(uint64_t c) {
+  return (c & ~kCmpLong) >> kCmpPosBits;
+}
 // kPacked (B200 extension, not one of the paper's three): a window is an
 // aligned 32-element block touched by any frontier list, fetched once for all
 // the lists that share it (see k_window_counts / k_expand_sweep).

@@ -218,21 +218,23 @@ __device__ __forceinline__ uint64_t window_base(uint64_t s) {
 // ------------------------------------------------ merged / merged-aligned
 // A batch of kUnroll windows of one warp: each lane holds the element it
 // loaded from each window (ok = lane inside the list).
-template <int ALGO, typename ET, typename WT, int U>
+template <int ALGO, typename ET, typename WT, int U, bool CMP = false>
 struct Batch {
   ET dst[U];
   WT wt[U];
   uint64_t sval[U];
   bool ok[U];
-  // kCompressed (warp-uniform): window u is 1 = a long-list line, 2 = a shared
-  // line of the staged short lists [k0, k1)
-  uint8_t line[U];
-  int16_t k0[U], k1[U];
+  // kCompressed only (warp-uniform): window u is 1 = a long-list line, 2 = a
+  // shared span of the staged short lists [k0, k1), dst2 its second line
+  static constexpr int C = CMP ? U : 1;
+  uint8_t line[C];
+  int16_t k0[C], k1[C];
+  uint32_t dst2[C];
 };
 
-template <int ALGO, typename ET, typename WT, int U>
+template <int ALGO, typename ET, typename WT, int U, bool CMP = false>
 __device__ __forceinline__ void visit_batch(const ExpandArgs& a,
-                                            const Batch<ALGO, ET, WT, U>& b) {
+                                            const Batch<ALGO, ET, WT, U, CMP>& b) {
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     if (!b.ok[u]) continue;
@@ -424,6 +426,16 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_big(ExpandArgs a) {
 constexpr int kSweepThreads = 256;
 constexpr int kSweepWarps = kSweepThreads / 32;
 constexpr int kStage = 256;  // frontier slots staged in shared memory at a time
+// Resident CTAs per SM the register allocation must allow: the compressed
+// decode is latency-bound, so occupancy beats a few spilled registers.
+// Measured on K27 / U27 (compressed): SSSP 96 registers / 2 CTAs 1,305 ms,
+// 80 / 3 CTAs 976 ms; CC 80 / 3 CTAs 1,074 ms, 64 / 4 CTAs 1,006 ms.
+// The raw strategies keep the compiler's choice (the HBM control run is
+// occupancy-sensitive the other way: 117 vs 94 GTEPS).
+template <int STRAT, int ALGO>
+struct SweepMinBlocks {
+  static constexpr int value = STRAT != kCompressed ? 0 : AlgoTraits<ALGO>::weighted ? 3 : 4;
+};
 
 // Windows per frontier slot.  Packed: the slot's 32-element blocks minus its
 // first block when the nearest earlier non-empty slot of the same aligned
@@ -448,21 +460,19 @@ __global__ void k_window_counts(ExpandArgs a) {
       const uint64_t c = a.cpos[v];
       if (a.pull_pass == 2) {  // the rest of the long in-lists still without a parent
         a.wcnt[j] = (c & kCmpLong) && !((a.visited[v >> 5] >> (v & 31)) & 1u)
-                        ? static_cast<uint32_t>((cmp_pos(a.cpos[v + 1]) - cmp_pos(c)) / kLineBits - 1)
+                        ? static_cast<uint32_t>(cmp_lines(c) - 1)
                         : 0u;
         continue;
       }
       if (c & kCmpLong) {
-        a.wcnt[j] = a.pull_pass == 1 ? 1u
-                                     : static_cast<uint32_t>((cmp_pos(a.cpos[v + 1]) - cmp_pos(c)) /
-                                                             kLineBits);
+        a.wcnt[j] = a.pull_pass == 1 ? 1u : static_cast<uint32_t>(cmp_lines(c));
         continue;
       }
       uint32_t w = 1;
       for (uint64_t i = j; i > group0; --i) {
         if (!a.fd[i - 1]) continue;
         const uint64_t ci = a.cpos[a.front[i - 1]];
-        w = (ci & kCmpLong) || cmp_pos(ci) / kLineBits != cmp_pos(c) / kLineBits;
+        w = (ci & kCmpLong) || cmp_pos(ci) / kShortSpanBits != cmp_pos(c) / kShortSpanBits;
         break;
       }
       a.wcnt[j] = w;
@@ -526,17 +536,18 @@ __device__ __forceinline__ void visit_line(const ExpandArgs& a, uint32_t x, uint
 // in [k0, k1) is in the frontier; empty lists take no bits, so there can be
 // more than 32 of them.
 template <int ALGO>
-__device__ __forceinline__ void visit_short(const ExpandArgs& a, uint32_t x, int k0, int k1,
-                                            const uint64_t* sh_c, const uint64_t* sh_s,
+__device__ __forceinline__ void visit_short(const ExpandArgs& a, uint32_t x, uint32_t x2, int k0,
+                                            int k1, const uint64_t* sh_c, const uint64_t* sh_s,
                                             const uint64_t* sh_e, const uint64_t* sh_v,
                                             uint32_t* L, int lane) {
   L[lane] = x;
-  if (lane < 2) L[kLineWords + lane] = 0;
+  L[kLineWords + lane] = x2;
+  if (lane < 2) L[kShortSpanWords + lane] = 0;
   __syncwarp();
   // more than 32 staged slots can share a line when empty lists sit between
   for (int i = k0 + lane; i < k1; i += 32) {
     const uint32_t d = static_cast<uint32_t>(sh_e[i] - sh_s[i]);
-    const uint32_t p = static_cast<uint32_t>(cmp_pos(sh_c[i]) % kLineBits);
+    const uint32_t p = static_cast<uint32_t>(cmp_pos(sh_c[i]) % kShortSpanBits);
     const uint64_t sval = AlgoTraits<ALGO>::has_val ? sh_v[i] : 0;
     const uint32_t w = d ? line_bits(L, p, 6) : 0;
     uint32_t val = d ? line_bits(L, p + 6, 32) : 0;
@@ -554,7 +565,8 @@ __device__ __forceinline__ void visit_short(const ExpandArgs& a, uint32_t x, int
 }
 
 template <int STRAT, int ALGO, typename ET, typename WT, int U>
-__global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, SweepMinBlocks<STRAT, ALGO>::value)
+    k_expand_sweep(ExpandArgs a) {
   if (a.n_dev) {  // device-driven level loop: size and level live in device memory
     a.n = *a.n_dev;
     a.iter = static_cast<uint32_t>(*a.iter_dev) + 1;
@@ -564,7 +576,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
   __shared__ uint64_t sh_w[kStage + 1];
   __shared__ uint64_t sh_c[kCmp ? kStage : 1];  // list position (| kCmpLong)
   __shared__ uint64_t sh_n[kCmp ? kStage : 1];  // next vertex's position (list end bound)
-  __shared__ uint32_t sh_line[kCmp ? kSweepWarps : 1][kLineWords + 2];  // decode buffer
+  __shared__ uint32_t sh_line[kCmp ? kSweepWarps : 1][kShortSpanWords + 2];  // decode buffer
   __shared__ uint64_t sh_j;
   const uint64_t n = a.n;
   const uint64_t T = a.wpre[n];
@@ -618,7 +630,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
     const int stage_n = static_cast<int>(n - j < kStage ? n - j : kStage);  // staged slots
 
     int k = 0;  // per-warp slot cursor, monotone within this stage
-    auto issue = [&](Batch<ALGO, ET, WT, U>& bt, uint64_t q0) {
+    auto issue = [&](Batch<ALGO, ET, WT, U, kCmp>& bt, uint64_t q0) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint64_t q = q0 + u;
@@ -648,22 +660,25 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
               const uint64_t line = cmp_pos(c) / kLineBits + (q - sh_w[k]) + (a.pull_pass == 2);
               bt.dst[u] = ld_list(a.cmp + line * kLineWords + lane);
               words += kLineWords;
-            } else {  // a shared line: the words of its staged frontier lists
+            } else {  // a shared span: the words of its staged frontier lists
               bt.line[u] = 2;
-              const uint64_t L = cmp_pos(c) / kLineBits;
+              const uint64_t L = cmp_pos(c) / kShortSpanBits;
               int m = k + 1;
-              while (m < stage_n && !(sh_c[m] & kCmpLong) && cmp_pos(sh_c[m]) / kLineBits == L) ++m;
+              while (m < stage_n && !(sh_c[m] & kCmpLong) && cmp_pos(sh_c[m]) / kShortSpanBits == L)
+                ++m;
               if constexpr (AlgoTraits<ALGO>::pull) {  // all candidates of the line found?
                 bool open = false;
                 for (int i = k + lane; i < m && !open; i += 32) open = !is_visited(a, sh_v[i]);
                 if (!__any_sync(kFull, open)) continue;
               }
-              const uint32_t w0 = static_cast<uint32_t>(cmp_pos(c) % kLineBits) / 32;
-              const uint64_t endb = min(sh_n[m - 1], (L + 1) * kLineBits);
-              const uint32_t w1 = static_cast<uint32_t>(endb - 1 - L * kLineBits) / 32;
+              const uint32_t w0 = static_cast<uint32_t>(cmp_pos(c) % kShortSpanBits) / 32;
+              const uint64_t endb = min(sh_n[m - 1], (L + 1) * kShortSpanBits);
+              const uint32_t w1 = static_cast<uint32_t>(endb - 1 - L * kShortSpanBits) / 32;
               bt.k0[u] = static_cast<int16_t>(k);
               bt.k1[u] = static_cast<int16_t>(m);
-              bt.dst[u] = lane >= w0 && lane <= w1 ? ld_list(a.cmp + L * kLineWords + lane) : 0u;
+              const uint32_t* sp = a.cmp + L * kShortSpanWords;
+              bt.dst[u] = lane >= w0 && lane <= w1 ? ld_list(sp + lane) : 0u;
+              bt.dst2[u] = lane + 32 >= w0 && lane + 32 <= w1 ? ld_list(sp + 32 + lane) : 0u;
               words += w1 - w0 + 1;
             }
             continue;
@@ -697,7 +712,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
     // warps interleave batches of U windows: warp w takes [W + (i*8 + w)*U, +U)
     uint64_t q0 = W + static_cast<uint64_t>(warp) * U;
     if (q0 < Wend) {
-      Batch<ALGO, ET, WT, U> cur, nxt;
+      Batch<ALGO, ET, WT, U, kCmp> cur, nxt;
       issue(cur, q0);
       for (; q0 < Wend; q0 += kSweepWarps * U) {
         const uint64_t qn = q0 + kSweepWarps * U;
@@ -709,11 +724,11 @@ __global__ void __launch_bounds__(kSweepThreads) k_expand_sweep(ExpandArgs a) {
               visit_line<ALGO>(a, static_cast<uint32_t>(cur.dst[u]), cur.sval[u], sh_line[warp],
                                lane);
             else if (cur.line[u] == 2)
-              visit_short<ALGO>(a, static_cast<uint32_t>(cur.dst[u]), cur.k0[u], cur.k1[u], sh_c,
-                                sh_s, sh_e, sh_v, sh_line[warp], lane);
+              visit_short<ALGO>(a, static_cast<uint32_t>(cur.dst[u]), cur.dst2[u], cur.k0[u],
+                                cur.k1[u], sh_c, sh_s, sh_e, sh_v, sh_line[warp], lane);
           }
         } else {
-          visit_batch<ALGO, ET, WT, U>(a, cur);
+          visit_batch<ALGO, ET, WT, U, kCmp>(a, cur);
         }
         cur = nxt;
       }

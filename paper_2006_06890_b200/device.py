@@ -207,8 +207,9 @@ class DeviceGraph:
         return nbytes.value
 
     def compressed_index(self) -> np.ndarray:
-        """Bit position of every vertex's list in the compressed line stream
-        (V+1 u64; bit 63 set: a long list stored as whole lines)."""
+        """Every vertex's entry of the compressed line stream's index (V+1
+        u64): bits [0, 40) the list's bit position; bit 63 set: a long list
+        stored as whole lines, their count in bits [40, 63)."""
         out = np.empty(self.num_vertices + 1, np.uint64)
         N.check(N.lib().zc_graph_compressed_index(self.handle, out.ctypes.data))
         return out
@@ -220,8 +221,11 @@ class DeviceGraph:
         or its share of a shared line including padding) for "compressed"."""
         if strategy != "compressed":
             return np.diff(self.as_csr().offsets).astype(np.int64) * self.edge_elem_bytes
-        pos = (self.compressed_index() & np.uint64((1 << 63) - 1)).astype(np.int64)
-        return np.diff(pos) // 8
+        idx = self.compressed_index()
+        pos = (idx & np.uint64((1 << 40) - 1)).astype(np.int64)
+        lines = ((idx[:-1] & np.uint64((1 << 63) - 1)) >> np.uint64(40)).astype(np.int64)
+        long_ = (idx[:-1] >> np.uint64(63)).astype(bool)
+        return np.where(long_, lines * 128, np.diff(pos) // 8)
 
     def build_in_lists(self) -> int:
         """Build the compressed in-list stream (the transpose; an undirected

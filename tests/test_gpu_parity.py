@@ -488,16 +488,20 @@ def test_compressed_lines_crafted_lists():
     nbytes = dg.build_compressed()
     idx = dg.compressed_index()
     long_ = (idx[:-1] >> np.uint64(63)).astype(bool)
-    pos = (idx & np.uint64((1 << 63) - 1)).astype(np.int64)
+    pos = (idx & np.uint64((1 << 40) - 1)).astype(np.int64)
+    nlines = ((idx[:-1] & np.uint64((1 << 63) - 1)) >> np.uint64(40)).astype(np.int64)
     span = np.diff(pos)
     deg = np.diff(g.offsets)
     assert nbytes == pos[-1] // 8 and pos[-1] % 1024 == 0 and (span >= 0).all()
     assert long_.any() and (~long_ & (deg > 0)).any()
-    assert (pos[:-1][long_] % 1024 == 0).all() and (span[long_] % 1024 == 0).all()
-    assert (deg[long_] > 1).all() and (span[deg == 0] <= 1024).all()
+    assert (pos[:-1][long_] % 1024 == 0).all() and (nlines[long_] >= 1).all()
+    # a long list's lines end at or before the next list (padding may follow)
+    assert (nlines[long_] * 1024 <= span[long_]).all() and (nlines[~long_] == 0).all()
+    assert (deg[long_] > 1).all() and (span[deg == 0] <= 2048).all()
+    span = np.where(long_, nlines * 1024, span)
     short = ~long_ & (deg > 0)
-    # a short list never straddles a line
-    assert ((pos[:-1][short] % 1024) + 38 <= 1024).all()
+    # a short list never straddles a 256-byte span
+    assert ((pos[:-1][short] % 2048) + 38 <= 2048).all()
     assert (span[long_] // 1024 <= (deg[long_] + 31) // 32 + 1).all()
     for src in (0, 1, 9, 12, 33, 4095):
         r = zc.bfs(dg, src, "compressed", collect_traffic=False)
