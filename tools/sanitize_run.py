@@ -25,7 +25,16 @@ run_partitions_local(parts, "cc" if not g.directed else "bfs", src, "compressed"
 run_partitions_local(parts, "sssp", src, "compressed")
 # compressed lines: long lists (whole lines) and short lists sharing lines
 h = zc.generate_powerlaw(20000, 40.0, 1.8, seed=5)
-zc.bfs(h, int(zc.pick_sources(h, 1)[0]), "compressed", collect_traffic=False)
+hs = int(zc.pick_sources(h, 1)[0])
+zc.bfs(h, hs, "compressed", collect_traffic=False)
+# direction-optimizing: in-list transpose, bottom-up passes, narrowed download,
+# pipelined results (widen threads), partitions with bottom-up steps
+zc.bfs(h, hs, "direction-optimizing", collect_traffic=False)
+zc.bfs(zc.symmetrized(h), hs, "direction-optimizing", collect_traffic=False)
+zc.bfs_many(h, [hs, hs + 1], "direction-optimizing")
+from paper_2006_06890_b200.multi import generate_rmat_part
+rp = [generate_rmat_part(12, 2, k, seed=3) for k in range(2)]
+run_partitions_local(rp, "bfs", 1, "direction-optimizing")
 r = zc.generate_rmat(12, 8, seed=1, symmetrize=True)
 zc.cc(r, "packed", collect_traffic=False)
 zc.cc(r, "compressed", collect_traffic=False)
