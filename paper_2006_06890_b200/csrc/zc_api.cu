@@ -250,8 +250,8 @@ __attribute__((constructor)) static void install_segv_trace() {
 }
 
 // int64 BFS levels from the narrowed download (0xff = unreached -> -1,
-// traversal.py:22), on the host cores but two: the widen of one result runs
-// while the caller's thread drives the next traversal's level loop.
+// traversal.py:22); the widen of one result runs while the caller's thread
+// drives the next traversal's level loop.
 // AVX2 body: 8 levels per step, streamed (non-temporal) stores so the 8 B
 // per vertex written do not also cost a read-for-ownership of host memory
 // the GPU is streaming lists from.
@@ -279,6 +279,16 @@ __attribute__((target("avx2"))) static void widen_levels_avx2(const uint8_t* src
 
 static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n) {
   static const bool avx2 = __builtin_cpu_supports("avx2");
+  // Four threads: the widen overlaps the next traversal, whose zero-copy reads
+  // share the host's memory bandwidth with its 8 B/vertex writes -- more
+  // threads finish sooner but slow the traversal (tools/e2e_probe.py: 2 / 4 /
+  // 16 threads: e2e 39.6 / 40.9 / 40.0 GTEPS).  ZC_WIDEN_SPARE overrides the
+  // number of host cores left out.
+  static const unsigned spare = [] {
+    const char* e = getenv("ZC_WIDEN_SPARE");
+    const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+    return e ? static_cast<unsigned>(atoi(e)) : (hc > 4 ? hc - 4 : 0u);
+  }();
   parallel_for(
       n,
       [&](uint64_t lo, uint64_t hi) {
@@ -289,7 +299,7 @@ static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n) {
         for (uint64_t i = lo; i < hi; ++i)
           out[i] = src[i] == 0xffu ? -1ll : static_cast<int64_t>(src[i]);
       },
-      2);
+      spare);
 }
 
 static double now_ms() {
