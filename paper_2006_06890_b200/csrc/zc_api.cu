@@ -277,18 +277,19 @@ __attribute__((target("avx2"))) static void widen_levels_avx2(const uint8_t* src
   _mm_sfence();
 }
 
-static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n) {
+static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n, bool overlapped) {
   static const bool avx2 = __builtin_cpu_supports("avx2");
-  // Four threads: the widen overlaps the next traversal, whose zero-copy reads
-  // share the host's memory bandwidth with its 8 B/vertex writes -- more
+  // Overlapped (pipelined) widens run on four threads: they share the host's
+  // memory bandwidth with the next traversal's zero-copy reads -- more
   // threads finish sooner but slow the traversal (tools/e2e_probe.py: 2 / 4 /
-  // 16 threads: e2e 39.6 / 40.9 / 40.0 GTEPS).  ZC_WIDEN_SPARE overrides the
-  // number of host cores left out.
-  static const unsigned spare = [] {
+  // 16 threads: e2e 39.6 / 40.9 / 40.0 GTEPS).  A blocking call's widen uses
+  // all cores but two.  ZC_WIDEN_SPARE overrides the overlapped setting.
+  static const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+  static const unsigned spare_overlap = [] {
     const char* e = getenv("ZC_WIDEN_SPARE");
-    const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
     return e ? static_cast<unsigned>(atoi(e)) : (hc > 4 ? hc - 4 : 0u);
   }();
+  const unsigned spare = overlapped ? spare_overlap : 2u;
   parallel_for(
       n,
       [&](uint64_t lo, uint64_t hi) {
@@ -1067,7 +1068,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
         *err = ZC_ECUDA;
         return;
       }
-      widen_levels(src8, out, nv);
+      widen_levels(src8, out, nv, true);
     });
     ZC_CUDA_TRY(cudaEventSynchronize(g->ev[1]));
   } else if (narrow) {
@@ -1077,7 +1078,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     ZC_CUDA_TRY(cudaMemcpyAsync(g->h_stage[2], d_u8, g->nv, cudaMemcpyDeviceToHost, st));
     ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
     ZC_CUDA_TRY(cudaStreamSynchronize(st));
-    widen_levels(g->h_stage[2], out, g->nv);
+    widen_levels(g->h_stage[2], out, g->nv, false);
   } else if (async) {
     // widen into the slot the download two calls ago has finished with, then
     // download it on copy_stream: the D2H direction of the link is idle while
