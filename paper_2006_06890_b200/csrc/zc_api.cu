@@ -356,6 +356,7 @@ void zc::free_graph(zc_graph* g) {
   }
   cudaFree(g->d_cand);
   cudaFree(g->d_fbits);
+  cudaFree(g->d_hasin);
   cudaFree(g->d_cpos);
   if (g->h_off) cudaFreeHost(g->h_off);
   cudaFree(g->d_off);
@@ -965,7 +966,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     if (!pull) ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[ev], st));
     if (pull) {
       ZC_CUDA_TRY(launch_pull_prepare(g->d_front[0], n, g->d_fbits, g->nv, g->d_visited,
-                                      g->d_in_off, g->d_cand, g->num_sms, st, &launches));
+                                      g->d_hasin, g->d_cand, g->num_sms, st, &launches));
       CompactArgs cc{};
       cc.flags = g->d_cand;
       cc.nv = g->nv;
@@ -1712,7 +1713,7 @@ int zc_part_pull(zc_graph* g, const uint32_t* bits, uint64_t* n_next, uint64_t* 
   }
   const int nb = g->p_cur ^ 1;
   // candidates: owned unvisited vertices with in-edges, sorted, over the in-offsets
-  ZC_CUDA_TRY(launch_part_pull_prepare(g->d_state, g->nv, g->d_visited, g->d_in_off, g->d_cand,
+  ZC_CUDA_TRY(launch_part_pull_prepare(g->d_state, g->nv, g->d_visited, g->d_hasin, g->d_cand,
                                        g->num_sms, st, &g->p_launches));
   CompactArgs cc{};
   cc.flags = g->d_cand;

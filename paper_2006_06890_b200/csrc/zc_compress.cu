@@ -359,6 +359,10 @@ int install_in_lists(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted) {
   g->d_cpos_in = static_cast<uint64_t*>(cpos.release());
   g->d_in_off = d_in_off;
   g->cmp_in_bytes = bytes;
+  return alloc_pull_state(g);
+}
+
+int alloc_pull_state(zc_graph* g) {
   if (!g->d_cand) {
     ZC_CUDA_TRY(cudaMalloc(&g->d_cand, g->vpad));
     ZC_CUDA_TRY(cudaMemset(g->d_cand, 0, g->vpad));
@@ -366,6 +370,12 @@ int install_in_lists(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted) {
   if (!g->d_fbits) {
     const uint64_t words = ((g->nparts ? g->global_nv : g->nv) + 31) / 32 + 1;
     ZC_CUDA_TRY(cudaMalloc(&g->d_fbits, words * sizeof(uint32_t)));
+  }
+  if (!g->d_hasin) {
+    ZC_CUDA_TRY(cudaMalloc(&g->d_hasin, ((g->nv + 31) / 32 + 1) * sizeof(uint32_t)));
+    ZC_CUDA_TRY(cudaMemset(g->d_hasin, 0, ((g->nv + 31) / 32 + 1) * sizeof(uint32_t)));
+    ZC_CUDA_TRY(launch_hasin(g->nv, g->d_in_off, g->d_hasin, 0));
+    ZC_CUDA_TRY(cudaDeviceSynchronize());
   }
   return ZC_OK;
 }
@@ -500,14 +510,7 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
       return rc;
     in_off.release();  // owned by the handle now
   }
-  if (!g->d_cand) {
-    ZC_CUDA_TRY(cudaMalloc(&g->d_cand, g->vpad));
-    ZC_CUDA_TRY(cudaMemset(g->d_cand, 0, g->vpad));
-  }
-  if (!g->d_fbits) {
-    const uint64_t words = ((g->nparts ? g->global_nv : nv) + 31) / 32 + 1;
-    ZC_CUDA_TRY(cudaMalloc(&g->d_fbits, words * sizeof(uint32_t)));
-  }
+  if ((rc = alloc_pull_state(g))) return rc;
   if (compressed_bytes) *compressed_bytes = g->cmp_in_bytes;
   return ZC_OK;
 }

@@ -60,6 +60,7 @@ struct zc_graph {
   bool in_alias = false;
   uint8_t* d_cand = nullptr;
   uint32_t* d_fbits = nullptr;
+  uint32_t* d_hasin = nullptr;  // vertices with in-edges (bitmap)
   // R-MAT partitions remember their generator, so their in-lists (arcs from
   // any rank into the owned range) can be generated on demand
   bool gen_rmat = false;
@@ -152,6 +153,9 @@ int host_list_device_ptr(void* p, const void** d);
 // over the handle's own vertices) into its in-list line stream; takes
 // ownership of d_in_off (zc_compress.cu).
 int install_in_lists(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted);
+// Candidate marks, frontier bitmap and in-edge bitmap of the bottom-up steps
+// (once the in-lists exist).
+int alloc_pull_state(zc_graph* g);
 // In-lists of a generated R-MAT partition (zc_gen.cu).
 int part_in_lists(zc_graph* g);
 inline bool placement_valid(int32_t p) { return p >= ZC_PLACE_ZEROCOPY && p <= ZC_PLACE_ZEROCOPY_MANAGED; }

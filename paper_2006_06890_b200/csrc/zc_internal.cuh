@@ -210,8 +210,10 @@ cudaError_t launch_compact(int algo, const CompactArgs& c, cudaStream_t st, uint
 // Bottom-up step inputs: zero + set the frontier bitmap from front[0, n), and
 // mark (u8 per vertex, padded to 16) every unvisited vertex with in-edges.
 cudaError_t launch_pull_prepare(const uint32_t* front, uint64_t n, uint32_t* fbits, uint64_t nv,
-                                const uint32_t* visited, const uint64_t* in_off, uint8_t* cand,
+                                const uint32_t* visited, const uint32_t* hasin, uint8_t* cand,
                                 int num_sms, cudaStream_t st, uint64_t* launches);
+// Bitmap of the vertices with in-edges ((nv + 31) / 32 words).
+cudaError_t launch_hasin(uint64_t nv, const uint64_t* in_off, uint32_t* bits, cudaStream_t st);
 cudaError_t launch_init(int algo, void* state, uint64_t nv, uint64_t src, const uint64_t* off,
                         uint32_t* front, uint64_t* fval, uint64_t* fs, uint32_t* fd,
                         cudaStream_t st, uint64_t* launches, uint64_t label_base = 0,
@@ -230,7 +232,7 @@ cudaError_t launch_frontier_bits(const uint32_t* front, uint64_t n, uint64_t vba
 // Partition bottom-up inputs: the owned range's visited bitmap from its
 // levels, then the candidate marks.
 cudaError_t launch_part_pull_prepare(const void* level, uint64_t nv, uint32_t* visited,
-                                     const uint64_t* in_off, uint8_t* cand, int num_sms,
+                                     const uint32_t* hasin, uint8_t* cand, int num_sms,
                                      cudaStream_t st, uint64_t* launches);
 // BFS levels (all below 255) as u8, 0xff = unreached.
 cudaError_t launch_narrow_levels(const void* state, uint64_t nv, uint8_t* out, cudaStream_t st,

@@ -1568,39 +1568,51 @@ __global__ void k_visited_from_levels(const uint32_t* level, uint64_t nv, uint32
   }
 }
 
-__global__ void k_cand_marks(uint64_t nv, const uint32_t* visited, const uint64_t* in_off,
+__global__ void k_cand_marks(uint64_t nv, const uint32_t* visited, const uint32_t* hasin,
                              uint8_t* cand) {
   const uint64_t ngroups = (nv + 15) / 16;
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ngroups;
        t += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v0 = t * 16;
-    const uint32_t vis = (visited[v0 >> 5] >> (v0 & 31)) & 0xffffu;
+    const uint32_t sh = static_cast<uint32_t>(v0 & 31);
+    const uint32_t c = ~(visited[v0 >> 5] >> sh) & (hasin[v0 >> 5] >> sh) & 0xffffu;
     uint32_t m[4] = {0, 0, 0, 0};
-    if (vis != 0xffffu) {
-      uint64_t prev = in_off[v0];
 #pragma unroll
-      for (int b = 0; b < 16; ++b) {
-        const uint64_t v = v0 + b;
-        if (v >= nv) break;
-        const uint64_t nxt = in_off[v + 1];
-        if (!((vis >> b) & 1u) && nxt > prev) m[b >> 2] |= 1u << ((b & 3) * 8);
-        prev = nxt;
-      }
-    }
+    for (int b = 0; b < 16; ++b)
+      if ((c >> b) & 1u) m[b >> 2] |= 1u << ((b & 3) * 8);
     reinterpret_cast<uint4*>(cand)[t] = make_uint4(m[0], m[1], m[2], m[3]);
+  }
+}
+
+// Bitmap of the vertices with in-edges (bits past nv stay 0).
+__global__ void k_hasin(uint64_t nv, const uint64_t* in_off, uint32_t* bits) {
+  const uint64_t nw = (nv + 31) / 32;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t x = 0;
+    for (int b = 0; b < 32; ++b) {
+      const uint64_t v = w * 32 + b;
+      if (v < nv && in_off[v + 1] > in_off[v]) x |= 1u << b;
+    }
+    bits[w] = x;
   }
 }
 }  // namespace
 
 cudaError_t launch_pull_prepare(const uint32_t* front, uint64_t n, uint32_t* fbits,
-                                uint64_t nv, const uint32_t* visited, const uint64_t* in_off,
+                                uint64_t nv, const uint32_t* visited, const uint32_t* hasin,
                                 uint8_t* cand, int num_sms, cudaStream_t st, uint64_t* launches) {
   cudaError_t e = cudaMemsetAsync(fbits, 0, ((nv + 31) / 32 + 1) * sizeof(uint32_t), st);
   if (e != cudaSuccess) return e;
   if (n) k_fbits_set<<<grid_for(n, 256, num_sms, 16), 256, 0, st>>>(front, n, 0, fbits);
-  k_cand_marks<<<grid_for((nv + 15) / 16, 256, num_sms, 16), 256, 0, st>>>(nv, visited, in_off,
+  k_cand_marks<<<grid_for((nv + 15) / 16, 256, num_sms, 16), 256, 0, st>>>(nv, visited, hasin,
                                                                             cand);
   *launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hasin(uint64_t nv, const uint64_t* in_off, uint32_t* bits, cudaStream_t st) {
+  k_hasin<<<grid_for((nv + 31) / 32 + 1, 256, 148, 16), 256, 0, st>>>(nv, in_off, bits);
   return cudaGetLastError();
 }
 
@@ -1617,11 +1629,11 @@ cudaError_t launch_frontier_bits(const uint32_t* front, uint64_t n, uint64_t vba
 }
 
 cudaError_t launch_part_pull_prepare(const void* level, uint64_t nv, uint32_t* visited,
-                                     const uint64_t* in_off, uint8_t* cand, int num_sms,
+                                     const uint32_t* hasin, uint8_t* cand, int num_sms,
                                      cudaStream_t st, uint64_t* launches) {
   k_visited_from_levels<<<grid_for((nv + 31) / 32, 256, num_sms, 16), 256, 0, st>>>(
       static_cast<const uint32_t*>(level), nv, visited);
-  k_cand_marks<<<grid_for((nv + 15) / 16, 256, num_sms, 16), 256, 0, st>>>(nv, visited, in_off,
+  k_cand_marks<<<grid_for((nv + 15) / 16, 256, num_sms, 16), 256, 0, st>>>(nv, visited, hasin,
                                                                             cand);
   *launches += 2;
   return cudaGetLastError();
