@@ -667,6 +667,13 @@ def variants(zc, args, dg, sources, device, phase: str) -> dict:
             out[f"zerocopy/{s}"] = _gteps(zc, dg, sources, s, reps=1 if s == "naive" else 2)
         return out
     import torch
+    # host-resident managed lists read in place (zerocopy-managed): the same
+    # zero-copy loads through the UVM driver's large-page GPU mappings
+    h = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, device=device,
+                         placement="zerocopy-managed")
+    out["zerocopy-managed/direction-optimizing"] = _gteps(zc, h, sources, "direction-optimizing",
+                                                          reps=2)
+    h.close()
     for placement in ("hbm", "uvm"):
         h = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, device=device,
                              placement=placement)
