@@ -866,6 +866,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     a.cpos = g->d_cpos;
     a.cmp_ww = g->cmp_ww;
     a.cmp_wmin = g->cmp_wmin;
+    a.cmp_b0 = g->cmp_b0;
     tune_params(&a);
     return a;
   };
@@ -1557,6 +1558,7 @@ static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
   a.cpos = g->d_cpos;
   a.cmp_ww = g->cmp_ww;
   a.cmp_wmin = g->cmp_wmin;
+  a.cmp_b0 = g->cmp_b0;
   tune_params(&a);
   // top-down steps of the direction-optimizing strategy are compressed steps
   const int td = g->p_strategy == kDirOpt ? static_cast<int>(kCompressed) : g->p_strategy;
@@ -1750,6 +1752,7 @@ int zc_part_pull(zc_graph* g, const uint32_t* bits, uint64_t* n_next, uint64_t* 
   b.scan_tmp_bytes = g->scan_tmp_bytes;
   b.cmp = static_cast<const uint32_t*>(g->d_cmp_in);
   b.cpos = g->d_cpos_in;
+  b.cmp_b0 = g->cmp_b0;
   b.fbits = bits;
   tune_params(&b);
   for (uint32_t pass = 1; pass <= 2; ++pass) {
@@ -1973,6 +1976,7 @@ int zc_pagerank(zc_graph* g, int strategy, double damping, uint64_t max_iters, d
     a.cpos = g->d_cpos;
     a.cmp_ww = g->cmp_ww;
     a.cmp_wmin = g->cmp_wmin;
+    a.cmp_b0 = g->cmp_b0;
     a.wcnt = g->d_wcnt;
     a.wpre = g->d_wpre;
     a.scan_tmp = g->d_scan_tmp;

@@ -87,13 +87,14 @@ __device__ __forceinline__ uint32_t list_width(const Elems& x, uint64_t s, uint6
   return bits_of(mx);
 }
 
-__host__ __device__ __forceinline__ uint64_t short_bits(uint64_t d, uint32_t w, uint32_t ww) {
-  return kCmpShortHdrBits + (d - 1) * w + d * ww;
+__host__ __device__ __forceinline__ uint64_t short_bits(uint64_t d, uint32_t w, uint32_t ww,
+                                                        uint32_t b0) {
+  return kCmpShortWidthBits + b0 + (d - 1) * w + d * ww;
 }
 
 // Size word of every list: 0 (empty), its bit length (short), or
 // kLongSize | lines (long).
-__global__ void k_cmp_size(uint64_t nv, const uint64_t* off, Elems x, uint32_t ww,
+__global__ void k_cmp_size(uint64_t nv, const uint64_t* off, Elems x, uint32_t ww, uint32_t b0,
                            uint32_t* size) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -102,7 +103,7 @@ __global__ void k_cmp_size(uint64_t nv, const uint64_t* off, Elems x, uint32_t w
     const uint64_t s = off[v], d = off[v + 1] - s;
     uint32_t out = 0;
     if (d) {
-      const uint64_t sb = short_bits(d, list_width(x, s, d, lane), ww);
+      const uint64_t sb = short_bits(d, list_width(x, s, d, lane), ww, b0);
       if (sb <= kShortSpanBits && d <= kCmpShortMaxDeg) {  // one lane decodes a short list
         out = static_cast<uint32_t>(sb);
       } else {
@@ -132,7 +133,7 @@ __device__ __forceinline__ void put_bits(uint32_t* out, uint64_t bit, uint32_t v
 // Encode: warp per list.  Short lists OR their fields into shared lines;
 // long lists build each line in a shared-memory buffer and store it whole.
 __global__ void __launch_bounds__(256) k_cmp_encode(uint64_t nv, const uint64_t* off, Elems x,
-                                                    uint32_t ww, const uint64_t* cpos,
+                                                    uint32_t ww, uint32_t b0, const uint64_t* cpos,
                                                     uint32_t* out) {
   __shared__ uint32_t buf[8][kLineWords + 2];
   const int lane = threadIdx.x & 31;
@@ -145,13 +146,14 @@ __global__ void __launch_bounds__(256) k_cmp_encode(uint64_t nv, const uint64_t*
     const uint64_t c = cpos[v], pos = cmp_pos(c);
     if (!(c & kCmpLong)) {
       const uint32_t w = list_width(x, s, d, lane);
+      const uint64_t hdr = kCmpShortWidthBits + b0;
       if (lane == 0) {
-        put_bits(out, pos, w, 6);
-        put_bits(out, pos + 6, x.dst(s), 32);
+        put_bits(out, pos, w, kCmpShortWidthBits);
+        put_bits(out, pos + kCmpShortWidthBits, x.dst(s), b0);
       }
-      const uint64_t wbase = pos + kCmpShortHdrBits + (d - 1) * w;
+      const uint64_t wbase = pos + hdr + (d - 1) * w;
       for (uint64_t k = lane; k < d; k += 32) {
-        if (k) put_bits(out, pos + kCmpShortHdrBits + (k - 1) * w, x.dst(s + k) - x.dst(s + k - 1), w);
+        if (k) put_bits(out, pos + hdr + (k - 1) * w, x.dst(s + k) - x.dst(s + k - 1), w);
         put_bits(out, wbase + k * ww, x.wt(s + k), ww);
       }
       continue;
@@ -251,12 +253,18 @@ struct DevBuf {
 // Sorted lists (x) over offsets d_off -> the line stream in device memory
 // (enc) and the per-vertex bit positions (cpos).
 namespace {
-int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t ww, DevBuf* cpos,
-                  DevBuf* enc, size_t* bytes) {
+// Bits of the largest vertex id a list can hold (global ids for partitions).
+uint32_t first_element_bits(const zc_graph* g) {
+  const uint64_t maxid = (g->nparts ? g->global_nv : g->nv);
+  return maxid > 1 ? 64 - __builtin_clzll(maxid - 1) : 1;
+}
+
+int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t ww, uint32_t b0,
+                  DevBuf* cpos, DevBuf* enc, size_t* bytes) {
   DevBuf size;
   // sizes, then the placement scan on the host (a sequential first-fit)
   ZC_CUDA_TRY(cudaMalloc(&size.p, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
-  k_cmp_size<<<kCmpGrid, 256>>>(nv, d_off, x, ww, static_cast<uint32_t*>(size.p));
+  k_cmp_size<<<kCmpGrid, 256>>>(nv, d_off, x, ww, b0, static_cast<uint32_t*>(size.p));
   ZC_CUDA_TRY(cudaGetLastError());
   std::vector<uint32_t> hs(nv);
   std::vector<uint64_t> hp(nv + 1);
@@ -293,7 +301,7 @@ int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t w
   *bytes = std::max<uint64_t>(lines, 1) * kLineBytes;
   ZC_CUDA_TRY(cudaMalloc(&enc->p, *bytes));
   ZC_CUDA_TRY(cudaMemset(enc->p, 0, *bytes));
-  k_cmp_encode<<<kCmpGrid, 256>>>(nv, d_off, x, ww, static_cast<uint64_t*>(cpos->p),
+  k_cmp_encode<<<kCmpGrid, 256>>>(nv, d_off, x, ww, b0, static_cast<uint64_t*>(cpos->p),
                                   static_cast<uint32_t*>(enc->p));
   ZC_CUDA_TRY(cudaDeviceSynchronize());
   return ZC_OK;
@@ -347,7 +355,7 @@ int install_in_lists(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted) {
   DevBuf enc, cpos;
   Elems x{d_in_sorted, nullptr, 0};
   size_t bytes = 0;
-  int rc = encode_stream(g->nv, d_in_off, x, 0, &cpos, &enc, &bytes);
+  int rc = encode_stream(g->nv, d_in_off, x, 0, first_element_bits(g), &cpos, &enc, &bytes);
   if (rc) return rc;
   void* host = nullptr;
   const void* dev = nullptr;
@@ -435,7 +443,8 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
     x.e32 = static_cast<const uint32_t*>(sorted.p);
   }
   size_t bytes = 0;
-  int rc = encode_stream(nv, g->d_off, x, ww, &cpos, &enc, &bytes);
+  const uint32_t b0 = first_element_bits(g);
+  int rc = encode_stream(nv, g->d_off, x, ww, b0, &cpos, &enc, &bytes);
   if (rc) return rc;
   cudaFree(sorted.release());
   void* host = nullptr;
@@ -449,6 +458,7 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
   g->cmp_bytes = bytes;
   g->cmp_weighted = weighted;
   g->cmp_ww = ww;
+  g->cmp_b0 = b0;
   g->cmp_wmin = x.wmin;
   if (compressed_bytes) *compressed_bytes = g->cmp_bytes;
   return ZC_OK;

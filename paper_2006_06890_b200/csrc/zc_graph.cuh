@@ -47,6 +47,7 @@ struct zc_graph {
   uint64_t* d_cpos = nullptr;  // per-vertex bit position (| kCmpLong), V+1
   uint64_t cmp_bytes = 0;
   uint32_t cmp_ww = 0, cmp_wmin = 0;  // weight field width / offset (0: unweighted)
+  uint32_t cmp_b0 = 32;               // bits of a short list's first element
   bool cmp_weighted = false;
   // direction-optimizing BFS: in-list offsets and the compressed in-list
   // stream (undirected graphs alias the out-lists), candidate marks and the

@@ -68,7 +68,9 @@ enum Strategy : int {
 // A window is one line: a long list's lines, or a shared line of short lists
 // fetched once for all its frontier lists.
 constexpr uint32_t kCmpHdrBits = 48;
-constexpr uint32_t kCmpShortHdrBits = 38;
+// A short list's header: the 6-bit delta width, then the first element in
+// b0 = bits(largest vertex id) bits (cmp_b0; at most 32).
+constexpr uint32_t kCmpShortWidthBits = 6;
 constexpr uint32_t kCmpMaxCount = 256;
 constexpr uint32_t kLineWords = 32;
 constexpr uint32_t kLineBits = 1024;
@@ -173,6 +175,7 @@ struct ExpandArgs {
   const uint64_t* cpos;
   uint32_t cmp_ww;
   uint32_t cmp_wmin;
+  uint32_t cmp_b0;  // bits of a short list's first element
   // bottom-up step (kBfsPull): bitmap of the current frontier; pass 1 reads
   // every candidate's first line (short lists whole), pass 2 the remaining
   // lines of the long in-lists still without a parent (0: one pass, all)

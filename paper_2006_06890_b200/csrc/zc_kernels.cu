@@ -549,13 +549,14 @@ __device__ __forceinline__ void visit_short(const ExpandArgs& a, uint32_t x, uin
     const uint32_t d = static_cast<uint32_t>(sh_e[i] - sh_s[i]);
     const uint32_t p = static_cast<uint32_t>(cmp_pos(sh_c[i]) % kShortSpanBits);
     const uint64_t sval = AlgoTraits<ALGO>::has_val ? sh_v[i] : 0;
-    const uint32_t w = d ? line_bits(L, p, 6) : 0;
-    uint32_t val = d ? line_bits(L, p + 6, 32) : 0;
-    const uint32_t wb = p + kCmpShortHdrBits + (d - 1) * w;
+    const uint32_t hdr = kCmpShortWidthBits + a.cmp_b0;
+    const uint32_t w = d ? line_bits(L, p, kCmpShortWidthBits) : 0;
+    uint32_t val = d ? line_bits(L, p + kCmpShortWidthBits, a.cmp_b0) : 0;
+    const uint32_t wb = p + hdr + (d - 1) * w;
     for (uint32_t e = 0; e < d; ++e) {
       // bottom-up: stop at the first parent (or a candidate found elsewhere)
       if (AlgoTraits<ALGO>::pull && is_visited(a, sval)) break;
-      if (e) val += line_bits(L, p + kCmpShortHdrBits + (e - 1) * w, w);
+      if (e) val += line_bits(L, p + hdr + (e - 1) * w, w);
       uint64_t wt = 0;
       if constexpr (AlgoTraits<ALGO>::weighted) wt = a.cmp_wmin + line_bits(L, wb + e * a.cmp_ww, a.cmp_ww);
       Visit<ALGO>::apply(a, val, wt, sval);
