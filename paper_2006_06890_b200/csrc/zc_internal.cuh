@@ -74,7 +74,7 @@ constexpr uint32_t kCmpShortWidthBits = 6;
 constexpr uint32_t kCmpMaxCount = 256;
 constexpr uint32_t kLineWords = 32;
 constexpr uint32_t kLineBits = 1024;
-constexpr uint32_t kCmpShortMaxDeg = 64;
+constexpr uint32_t kCmpShortMaxDeg = 96;
 // Short lists are packed into 256-byte spans (two lines) and never straddle
 // one: a U27 SSSP list (540 bits) then shares its span with two others.
 constexpr uint32_t kShortSpanBits = 2 * kLineBits;
