@@ -55,11 +55,11 @@ enum Strategy : int {
 };
 // kCompressed (B200 host-store option, zc_compress.cu): every list is stored
 // sorted and delta-encoded in a stream of 128-byte lines, in vertex order.
-//   short list (encoding <= 1024 bits, <= 64 elements): packed with its
-//     neighbours into a
-//     shared line, never straddling one -- 6-bit delta width w, 32-bit first
-//     element, d-1 deltas of w bits, then (weighted) d weights of ww bits
-//     (weight - wmin);
+//   short list (encoding <= 2048 bits, <= 96 elements): packed with its
+//     neighbours into a shared 256-byte span (two lines), never straddling
+//     one -- 6-bit delta width w, the first element in cmp_b0 bits (bits of
+//     the largest vertex id), d-1 deltas of w bits, then (weighted) d weights
+//     of ww bits (weight - wmin);
 //   long list: whole self-describing lines -- word 0 base, word 1 [0,6) w,
 //     [6,14) count - 1 (<= 255); from bit 48: count-1 deltas of w bits, then
 //     (weighted) count weights of ww bits.
