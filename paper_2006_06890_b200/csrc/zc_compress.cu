@@ -6,8 +6,8 @@
 // SSSP results do not depend on the order inside a list, so every list is
 // sorted and stored delta-encoded in 128-byte lines (format in
 // zc_internal.cuh): a hub list as whole self-describing lines (~50-100 edges
-// per aligned line read instead of 32), short lists packed into shared lines
-// (one line read serves every frontier list in it).  SSSP weights ride in the
+// per aligned line read instead of 32), short lists packed into shared
+// 256-byte spans (one read serves every frontier list in it).  SSSP weights ride in the
 // same lines as (weight - wmin) fields of the narrowest width that holds them.
 //
 // Build, on the GPU except the placement scan: sort each list (by destination,

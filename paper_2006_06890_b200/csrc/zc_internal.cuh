@@ -65,8 +65,8 @@ enum Strategy : int {
 //     (weighted) count weights of ww bits.
 // Per-vertex cpos (u64[V+1], HBM): bit position of the list in the stream,
 // kCmpLong and the line count for long lists (layout below).
-// A window is one line: a long list's lines, or a shared line of short lists
-// fetched once for all its frontier lists.
+// A window is one long-list line, or one shared span of short lists fetched
+// once for all its frontier lists.
 constexpr uint32_t kCmpHdrBits = 48;
 // A short list's header: the 6-bit delta width, then the first element in
 // b0 = bits(largest vertex id) bits (cmp_b0; at most 32).
