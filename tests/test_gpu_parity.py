@@ -635,3 +635,25 @@ def test_cuda_partitions_direction_optimizing(fused):
         assert np.array_equal(vals, ref.values) and trav == ref.traversed_edges
         for e in engines:
             e.close()
+
+
+def test_compressed_byte_accounting():
+    """The bench's roofline inputs: the device counter of requested line-stream
+    bytes, and the per-vertex stored bytes of the stream."""
+    dg = zc.generate_rmat(16, 16, seed=13)
+    nbytes = dg.build_compressed()
+    stored = dg.stored_list_bytes("compressed")
+    assert stored.shape == (dg.num_vertices,) and (stored >= 0).all()
+    assert 0 < stored.sum() <= nbytes  # padding is the difference
+    raw = dg.stored_list_bytes("packed")
+    assert raw.sum() == dg.num_edges * 4
+    src = int(zc.pick_sources(dg.as_csr(), 1, seed=7)[0])
+    r = zc.bfs(dg, src, "compressed", collect_traffic=False)
+    req = dg.link_bytes_requested()
+    assert 0 < req <= nbytes * r.iterations and req % 4 == 0
+    zc.bfs(dg, src, "packed", collect_traffic=False)
+    assert dg.link_bytes_requested() == 0  # raw strategies do not count
+    r = zc.bfs(dg, src, "direction-optimizing", collect_traffic=False)
+    assert dg.link_bytes_requested() > 0
+    assert dg.directions(r.iterations).shape == (r.iterations,)
+    dg.close()
