@@ -237,6 +237,15 @@ int zc_graph_evict(zc_graph *g);
                                    merged / merged-aligned / packed strategies) */
 int zc_set_options(zc_graph *g, uint32_t options);
 
+/* Launch tuning of a handle (B200 extension, no reference counterpart):
+ * comma-separated "unroll=2|4|8", "ctas=N" (sweep CTAs per SM),
+ * "sched=chunk|sweep", "loop=host|device" (host-driven level loop, e.g. under
+ * a profiler, which cannot see kernels inside conditional graph nodes),
+ * "do_alpha=X" (direction-optimizing switch factor).  NULL or "" resets the
+ * defaults; an unknown entry is ZC_EINVAL.  Read by the run path; nothing is
+ * taken from the environment. */
+int zc_set_tuning(zc_graph *g, const char *spec);
+
 /* Modelled request histogram of the most recent run (needs
  * ZC_OPT_TRAFFIC_MODEL): for iteration k, hist[8k+i] = edge-list requests of
  * (i+1)*32 bytes and hist[8k+4+i] = weight-list requests (SSSP), i = 0..3 --
@@ -265,11 +274,6 @@ int zc_generate_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, d
 int zc_generate_uniform(uint64_t num_vertices, uint32_t min_degree, uint32_t max_degree,
                         uint64_t seed, int64_t wlow, int64_t whigh, int32_t placement,
                         int32_t device, zc_graph **out);
-
-/* Host-link probe: pinned cudaMemcpy H2D GB/s and a zero-copy streaming
- * read kernel GB/s over `bytes` of pinned memory (the denominators). */
-int zc_link_probe(int32_t device, uint64_t bytes, int iters, double *memcpy_h2d_gbs,
-                  double *zerocopy_read_gbs, double *hbm_read_gbs);
 
 /* ---------------------------------------------------------------------------
  * Vertex-range partitions (multi-GPU; no reference counterpart --
@@ -344,27 +348,6 @@ int zc_generate_rmat_part(uint32_t scale, uint32_t edge_factor, double a, double
                           uint64_t seed, int64_t wlow, int64_t whigh, uint32_t nparts,
                           uint32_t part, int32_t placement, int32_t device, uint64_t *bounds,
                           zc_graph **out);
-
-/* Read microbenchmark (the paper's zero-copy toy kernel):
- * warps read chunk_bytes contiguous bytes per request at consecutive
- * (pattern 0) or random (pattern 1) chunk-aligned offsets of a `bytes`
- * buffer allocated by cudaHostAlloc (alloc 0), transparent-huge-page
- * mmap + cudaHostRegister (alloc 1), cudaMalloc (alloc 2), a host-NUMA
- * VMM allocation (cuMemCreate, alloc 3), hugetlbfs 2 MB pages +
- * cudaHostRegister (alloc 4) or cudaMallocManaged preferred on the CPU and
- * accessed-by the device (alloc 5). */
-int zc_read_probe(int32_t device, uint64_t bytes, int pattern, uint32_t chunk_bytes, int alloc,
-                  int iters, double *gbs);
-
-/* Host-NUMA VMM allocation check: allocates `bytes` with cuMemCreate
- * (CU_MEM_LOCATION_TYPE_HOST_NUMA, node 0), maps it for the device and the
- * CPU, frees it; *granularity = the recommended allocation granularity. */
-int zc_vmm_host_probe(int32_t device, uint64_t bytes, uint64_t *granularity);
-
-/* TMA bulk-copy (cp.async.bulk) streaming read of pinned host memory:
- * `chunk`-byte copies into a 4-stage shared-memory ring per CTA. */
-int zc_bulk_probe(int32_t device, uint64_t bytes, uint32_t chunk, int ctas_per_sm, int iters,
-                  double *gbs);
 
 #ifdef __cplusplus
 }

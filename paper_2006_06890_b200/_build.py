@@ -14,8 +14,13 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_NAME = "libzcgraph_b200.so"
 LIB_PATH = os.path.join(PKG, LIB_NAME)
+# measurement probes (include/zcprobe.h): a separate tool library linked
+# against the product library, so the traversal ABI exports no probe symbols
+PROBE_LIB_NAME = "libzcprobe_b200.so"
+PROBE_LIB_PATH = os.path.join(PKG, PROBE_LIB_NAME)
 
-SOURCES = ["zc_api.cu", "zc_kernels.cu", "zc_gen.cu", "zc_probe.cu", "zc_compress.cu"]
+SOURCES = ["zc_api.cu", "zc_kernels.cu", "zc_gen.cu", "zc_compress.cu"]
+PROBE_SOURCES = ["zc_probe.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
               "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -36,12 +41,22 @@ def _stale(target: str, deps: list[str]) -> bool:
 
 
 def build_native(force: bool = False, verbose: bool = False) -> str:
-    """Compile every .cu under csrc/ into the in-tree shared library."""
-    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    """Compile every .cu under csrc/ into the in-tree shared libraries (the
+    product library and the probe tool library)."""
+    _build_lib(SOURCES, LIB_PATH, [], force, verbose)
+    _build_lib(PROBE_SOURCES, PROBE_LIB_PATH,
+               ["-L", PKG, "-l:" + LIB_NAME, "-Xlinker", "-rpath,$ORIGIN"], force, verbose,
+               extra_deps=[LIB_PATH])
+    return LIB_PATH
+
+
+def _build_lib(sources, lib_path, link_extra, force, verbose, extra_deps=()):
+    srcs = [os.path.join(CSRC, s) for s in sources]
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    deps.append(os.path.join(ROOT, "include", "zcgraph.h"))
-    if not force and not _stale(LIB_PATH, deps):
-        return LIB_PATH
+    deps += [os.path.join(ROOT, "include", f) for f in ("zcgraph.h", "zcprobe.h")]
+    deps += list(extra_deps)
+    if not force and not _stale(lib_path, deps):
+        return lib_path
     objdir = os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
     objs = []
@@ -57,13 +72,13 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
         with open(obj + ".ptxas.txt", "w") as fh:
             fh.write(res.stderr)
         objs.append(obj)
-    tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    tmp = lib_path + ".tmp"
+    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, *link_extra, "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":

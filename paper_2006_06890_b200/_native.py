@@ -10,7 +10,7 @@ import ctypes as C
 import os
 import threading
 
-from ._build import LIB_PATH
+from ._build import LIB_PATH, PROBE_LIB_PATH
 
 ZC_OK, ZC_EINVAL, ZC_ECUDA, ZC_ENOMEM, ZC_ESTATE = 0, -1, -2, -3, -4
 ZC_NAIVE, ZC_MERGED, ZC_MERGED_ALIGNED, ZC_PACKED, ZC_COMPRESSED = 0, 1, 2, 3, 4
@@ -26,17 +26,19 @@ EXPORTED = (
     "zc_last_error", "zc_abi_version", "zc_device_count", "zc_graph_create",
     "zc_graph_destroy", "zc_graph_host_lists", "zc_graph_info", "zc_bfs", "zc_sssp",
     "zc_cc", "zc_run_log", "zc_host_alloc", "zc_host_free", "zc_generate_rmat",
-    "zc_generate_uniform", "zc_link_probe", "zc_set_options", "zc_run_traffic",
-    "zc_run_profile", "zc_graph_evict", "zc_read_probe", "zc_part_create",
+    "zc_generate_uniform", "zc_set_options", "zc_set_tuning", "zc_run_traffic",
+    "zc_run_profile", "zc_graph_evict", "zc_part_create",
     "zc_part_exchange_elem_bytes", "zc_part_begin", "zc_part_expand", "zc_part_apply",
     "zc_part_result", "zc_generate_rmat_part", "zc_pagerank", "zc_graph_multigraph",
     "zc_part_fused_init", "zc_part_fused_connect", "zc_part_fused_reset", "zc_part_fused_expand",
-    "zc_graph_open_emgi", "zc_graph_build_pairs", "zc_bulk_probe", "zc_graph_build_compressed",
-    "zc_bfs_async", "zc_sssp_async", "zc_sync", "zc_vmm_host_probe", "zc_graph_compressed_index",
+    "zc_graph_open_emgi", "zc_graph_build_pairs", "zc_graph_build_compressed",
+    "zc_bfs_async", "zc_sssp_async", "zc_sync", "zc_graph_compressed_index",
     "zc_graph_build_in_lists", "zc_run_directions", "zc_run_link_bytes",
     "zc_part_build_in_lists", "zc_part_unvisited_in", "zc_part_frontier_bits", "zc_part_pull",
 )
-ZC_OPT_TRAFFIC_MODEL = 1
+# every symbol include/zcprobe.h declares (the measurement tool library)
+PROBE_EXPORTED = ("zc_link_probe", "zc_read_probe", "zc_bulk_probe", "zc_vmm_host_probe")
+ZC_OPT_TRAFFIC_MODEL, ZC_OPT_HOST_LOOP = 1, 2
 
 
 class GraphDesc(C.Structure):
@@ -104,6 +106,7 @@ def _declare(lib: C.CDLL) -> None:
         "zc_part_pull": (C.c_int, [P, C.c_void_p, C.POINTER(u64), C.POINTER(u64)]),
         "zc_run_log": (C.c_int, [P, P, P, u64]),
         "zc_set_options": (C.c_int, [P, u32]),
+        "zc_set_tuning": (C.c_int, [P, C.c_char_p]),
         "zc_run_profile": (C.c_int, [P, P, u64]),
         "zc_graph_evict": (C.c_int, [P]),
         "zc_run_traffic": (C.c_int, [P, P, u64]),
@@ -113,11 +116,6 @@ def _declare(lib: C.CDLL) -> None:
                                        i32, C.POINTER(P)]),
         "zc_generate_uniform": (C.c_int, [u64, u32, u32, u64, i64, i64, i32, i32,
                                           C.POINTER(P)]),
-        "zc_link_probe": (C.c_int, [i32, u64, C.c_int, C.POINTER(dbl), C.POINTER(dbl),
-                                    C.POINTER(dbl)]),
-        "zc_read_probe": (C.c_int, [i32, u64, C.c_int, u32, C.c_int, C.c_int, C.POINTER(dbl)]),
-        "zc_bulk_probe": (C.c_int, [i32, u64, u32, C.c_int, C.c_int, C.POINTER(dbl)]),
-        "zc_vmm_host_probe": (C.c_int, [i32, u64, C.POINTER(u64)]),
         "zc_part_create": (C.c_int, [C.POINTER(GraphDesc), C.POINTER(PartInfo), C.POINTER(P)]),
         "zc_part_exchange_elem_bytes": (C.c_size_t, [C.c_int]),
         "zc_part_begin": (C.c_int, [P, C.c_int, u64, C.c_int, C.POINTER(u64), C.POINTER(u64)]),
@@ -158,6 +156,38 @@ def lib() -> C.CDLL:
                 raise NativeLibraryError("zcgraph ABI version mismatch; rebuild the library")
             _lib = handle
     return _lib
+
+
+_probe = None
+
+
+def probe_lib() -> C.CDLL:
+    """Load (once) the probe tool library (include/zcprobe.h)."""
+    global _probe
+    if _probe is not None:
+        return _probe
+    lib()  # the probes report errors through the product library's zc_last_error
+    with _lock:
+        if _probe is None:
+            try:
+                handle = C.CDLL(PROBE_LIB_PATH)
+            except OSError as exc:
+                raise NativeLibraryError(f"cannot load {PROBE_LIB_PATH}: {exc}") from exc
+            P, u64, u32, i32, dbl = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int32, C.c_double
+            sig = {
+                "zc_link_probe": (C.c_int, [i32, u64, C.c_int, C.POINTER(dbl), C.POINTER(dbl),
+                                            C.POINTER(dbl)]),
+                "zc_read_probe": (C.c_int, [i32, u64, C.c_int, u32, C.c_int, C.c_int,
+                                            C.POINTER(dbl)]),
+                "zc_bulk_probe": (C.c_int, [i32, u64, u32, C.c_int, C.c_int, C.POINTER(dbl)]),
+                "zc_vmm_host_probe": (C.c_int, [i32, u64, C.POINTER(u64)]),
+            }
+            for name, (res, args) in sig.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _probe = handle
+    return _probe
 
 
 def last_error() -> str:

@@ -15,11 +15,8 @@
 #include <string.h>
 
 #include <dirent.h>
-#include <dlfcn.h>
 #include <immintrin.h>
-#include <execinfo.h>
 #include <fcntl.h>
-#include <signal.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
 #include <sys/syscall.h>
@@ -80,18 +77,10 @@ static void convert_copy(void* dst, uint32_t dw, const void* src, uint32_t sw, u
   });
 }
 
-void tune_params(ExpandArgs* a) {
-  int u = 4, c = 0, sched = 0;
-  if (const char* t = getenv("ZC_TUNE")) {  // read per run: experiments vary it in-process
-    const char* p = strstr(t, "unroll=");
-    if (p) u = atoi(p + 7);
-    p = strstr(t, "ctas=");
-    if (p) c = atoi(p + 5);
-    sched = strstr(t, "sched=chunk") != nullptr;
-  }
-  a->unroll = u;
-  a->ctas_per_sm = c;
-  a->chunk_sched = sched;
+void tune_params(ExpandArgs* a, const zc_graph* g) {
+  a->unroll = g->tune.unroll;
+  a->ctas_per_sm = g->tune.ctas;
+  a->chunk_sched = g->tune.sched;
 }
 
 // ---------------------------------------------------------- pinned lists
@@ -223,32 +212,6 @@ void pinned_list_free(void* p) {
   }
 }
 
-// Debug aid (ZC_SEGV_TRACE=1): on SIGSEGV print the native frames with their
-// offsets inside the shared objects, for addr2line.
-static void segv_trace(int sig) {
-  void* fr[64];
-  const int n = backtrace(fr, 64);
-  for (int i = 0; i < n; ++i) {
-    Dl_info info;
-    char line[512];
-    int len;
-    if (dladdr(fr[i], &info) && info.dli_fname)
-      len = snprintf(line, sizeof(line), "zc-segv #%d %s+0x%lx\n", i, info.dli_fname,
-                     static_cast<unsigned long>(static_cast<char*>(fr[i]) -
-                                                static_cast<char*>(info.dli_fbase)));
-    else
-      len = snprintf(line, sizeof(line), "zc-segv #%d %p\n", i, fr[i]);
-    if (len > 0) (void)!write(2, line, static_cast<size_t>(len));
-  }
-  signal(sig, SIG_DFL);
-  raise(sig);
-}
-
-__attribute__((constructor)) static void install_segv_trace() {
-  const char* e = getenv("ZC_SEGV_TRACE");
-  if (e && e[0] == '1') signal(SIGSEGV, segv_trace);
-}
-
 // int64 BFS levels from the narrowed download (0xff = unreached -> -1,
 // traversal.py:22); the widen of one result runs while the caller's thread
 // drives the next traversal's level loop.
@@ -283,12 +246,9 @@ static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n, bool over
   // memory bandwidth with the next traversal's zero-copy reads -- more
   // threads finish sooner but slow the traversal (tools/e2e_probe.py: 2 / 4 /
   // 16 threads: e2e 39.6 / 40.9 / 40.0 GTEPS).  A blocking call's widen uses
-  // all cores but two.  ZC_WIDEN_SPARE overrides the overlapped setting.
+  // all cores but two.
   static const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
-  static const unsigned spare_overlap = [] {
-    const char* e = getenv("ZC_WIDEN_SPARE");
-    return e ? static_cast<unsigned>(atoi(e)) : (hc > 4 ? hc - 4 : 0u);
-  }();
+  static const unsigned spare_overlap = hc > 4 ? hc - 4 : 0u;
   const unsigned spare = overlapped ? spare_overlap : 2u;
   parallel_for(
       n,
@@ -640,21 +600,6 @@ int zc::adopt_device_list(zc_graph* g, void* d_src, uint32_t w, uint64_t n, void
 
 namespace {
 
-bool tune_host_loop() {
-  const char* t = getenv("ZC_TUNE");
-  return t && strstr(t, "loop=host");
-}
-
-// Direction-optimizing switch factor (ZC_TUNE=do_alpha=X, default 2:
-// bottom-up once the frontier's out-edges exceed half the unvisited
-// vertices' in-edges; measured best over 16 K27 sources, tools/do_alpha.py).
-double tune_do_alpha() {
-  const char* t = getenv("ZC_TUNE");
-  const char* p = t ? strstr(t, "do_alpha=") : nullptr;
-  const double v = p ? atof(p + 9) : 0.0;
-  return v > 0 ? v : 2.0;
-}
-
 // Build (or reuse) the device-driven level loop of (algo, strategy): a CUDA
 // graph whose conditional WHILE node repeats
 //   stamp -> window counts -> scan -> sweep expansion -> stamp ->
@@ -867,7 +812,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     a.cmp_ww = g->cmp_ww;
     a.cmp_wmin = g->cmp_wmin;
     a.cmp_b0 = g->cmp_b0;
-    tune_params(&a);
+    tune_params(&a, g);
     return a;
   };
   auto compact_args = [&]() {
@@ -894,7 +839,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
   const ExpandArgs probe = expand_args(g->nv, 0);
   const bool device_loop = n > 0 && strategy != kNaive && !dobfs && !model &&
                            !probe.chunk_sched && !(g->options & ZC_OPT_HOST_LOOP) &&
-                           !tune_host_loop();
+                           !g->tune.host_loop;
   // direction-optimizing: in-edges of the unvisited vertices (Beamer's m_u)
   uint64_t unvisited_in = 0;
   if (dobfs && n) {
@@ -904,7 +849,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     ZC_CUDA_TRY(cudaMemcpy(&e_in, g->d_in_off + g->nv, sizeof(uint64_t), cudaMemcpyDeviceToHost));
     unvisited_in = e_in - (io[1] - io[0]);
   }
-  const double do_alpha = tune_do_alpha();
+  const double do_alpha = g->tune.do_alpha;
   if (device_loop) {
     int rc = build_loop_graph(g, algo, strategy, ebytes, expand_args(g->nv, 0), compact_args());
     if (rc) return rc;
@@ -941,7 +886,6 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
 
   // ---- host-driven loop (naive, request model, tuning, or the tail past the log)
   std::vector<uint64_t> host_iters;
-  uint64_t dbg_ncand = 0;
   while (n > 0) {
     ++iters;
     g->log_trav.push_back(trav);
@@ -984,7 +928,6 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
       ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
       ZC_CUDA_TRY(cudaStreamSynchronize(st));
       const uint64_t ncand = g->h_ctr[kCtrNext];
-      dbg_ncand = ncand;
       // the expansion-time events bracket the sweep only (candidate set-up is
       // compaction work, like the top-down steps' next-frontier compaction)
       ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[ev], st));
@@ -1001,12 +944,6 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
       // the remaining lines of long in-lists still without one
       b.pull_pass = 1;
       ZC_CUDA_TRY(launch_expand(kCompressed, kBfsPull, 4, g->wb, b, g->num_sms, st, &launches));
-      if (getenv("ZC_DEBUG_DO")) {  // bytes after pass 1
-        ZC_CUDA_TRY(cudaMemcpyAsync(&g->h_small[0], g->d_ctr + kCtrLoaded, sizeof(uint64_t),
-                                    cudaMemcpyDeviceToHost, st));
-        ZC_CUDA_TRY(cudaStreamSynchronize(st));
-        fprintf(stderr, "zc-do   pass1 loaded=%lu\n", (unsigned long)g->h_small[0]);
-      }
       b.pull_pass = 2;
       ZC_CUDA_TRY(launch_expand(kCompressed, kBfsPull, 4, g->wb, b, g->num_sms, st, &launches));
     } else {
@@ -1023,15 +960,6 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     n = g->h_ctr[kCtrNext];
     trav = g->h_ctr[kCtrTrav];
     if (dobfs) {
-      if (getenv("ZC_DEBUG_DO")) {
-        float ms = 0;
-        cudaEventElapsedTime(&ms, g->iter_ev[ev], g->iter_ev[ev + 1]);
-        fprintf(stderr, "zc-do it=%lu pull=%d front=%lu trav=%lu unvisited_in=%lu ncand=%lu "
-                "loaded=%lu sweep_ms=%.2f\n", (unsigned long)iters, pull ? 1 : 0,
-                (unsigned long)g->log_front.back(), (unsigned long)g->log_trav.back(),
-                (unsigned long)unvisited_in, (unsigned long)(pull ? dbg_ncand : 0),
-                (unsigned long)g->h_ctr[kCtrLoaded], ms);
-      }
       unvisited_in -= std::min(unvisited_in, g->h_ctr[kCtrTravIn]);
       g->log_pull.push_back(pull ? 1 : 0);
     }
@@ -1274,18 +1202,24 @@ int zc_graph_open_emgi(const char* path, int32_t placement, int32_t device, uint
   }
   const uint32_t eb = (fl & 2) ? 8 : 4, wb = (fl & 4) ? 8 : 4;
   const bool has_w = fl & 1;
-  const uint64_t off_pos = 28, off_end = off_pos + (nv + 1) * 8;
-  if (size < off_end) {
+  // header fields are untrusted: bound every count by the bytes that follow
+  // before multiplying, so no product can wrap past the size checks
+  const uint64_t off_pos = 28;
+  if (nv > (size - off_pos) / 8 - 1 || (size - off_pos) / 8 == 0) {
     set_error("truncated file: offsets array incomplete");
     return ZC_EINVAL;
   }
-  const uint64_t e_pos = round_up(off_end, 128), e_end = e_pos + ne * eb;
-  if (size < e_end) {
+  const uint64_t off_end = off_pos + (nv + 1) * 8;
+  const uint64_t e_pos = round_up(off_end, 128);
+  if (e_pos > size || ne > (size - e_pos) / eb) {
     set_error("truncated file: edge array incomplete");
     return ZC_EINVAL;
   }
-  const uint64_t w_pos = round_up(e_end, 128), w_end = w_pos + ne * wb;
-  if (has_w && size < w_end) {
+  const uint64_t e_end = e_pos + ne * eb;
+  const uint64_t w_pos = round_up(e_end, 128);
+  const uint64_t w_end = has_w && w_pos <= size && ne <= (size - w_pos) / wb ? w_pos + ne * wb
+                                                                              : UINT64_MAX;
+  if (has_w && w_end > size) {
     set_error("truncated file: weight array incomplete");
     return ZC_EINVAL;
   }
@@ -1559,7 +1493,7 @@ static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
   a.cmp_ww = g->cmp_ww;
   a.cmp_wmin = g->cmp_wmin;
   a.cmp_b0 = g->cmp_b0;
-  tune_params(&a);
+  tune_params(&a, g);
   // top-down steps of the direction-optimizing strategy are compressed steps
   const int td = g->p_strategy == kDirOpt ? static_cast<int>(kCompressed) : g->p_strategy;
   ZC_CUDA_TRY(launch_expand(td, algo + kPartAlgo, g->eb, g->wb, a, g->num_sms, st,
@@ -1754,7 +1688,7 @@ int zc_part_pull(zc_graph* g, const uint32_t* bits, uint64_t* n_next, uint64_t* 
   b.cpos = g->d_cpos_in;
   b.cmp_b0 = g->cmp_b0;
   b.fbits = bits;
-  tune_params(&b);
+  tune_params(&b, g);
   for (uint32_t pass = 1; pass <= 2; ++pass) {
     b.pull_pass = pass;
     ZC_CUDA_TRY(launch_expand(kCompressed, kBfsPull, 4, g->wb, b, g->num_sms, st, &g->p_launches));
@@ -1981,7 +1915,7 @@ int zc_pagerank(zc_graph* g, int strategy, double damping, uint64_t max_iters, d
     a.wpre = g->d_wpre;
     a.scan_tmp = g->d_scan_tmp;
     a.scan_tmp_bytes = g->scan_tmp_bytes;
-    tune_params(&a);
+    tune_params(&a, g);
     while (g->iter_ev.size() < 2 * iters) {
       cudaEvent_t e;
       ZC_CUDA_TRY(cudaEventCreate(&e));
@@ -1995,8 +1929,8 @@ int zc_pagerank(zc_graph* g, int strategy, double damping, uint64_t max_iters, d
     ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr + kCtrPrDelta, g->d_ctr + kCtrPrDelta, sizeof(uint64_t),
                                 cudaMemcpyDeviceToHost, st));
     ZC_CUDA_TRY(cudaStreamSynchronize(st));
-    double delta;
-    memcpy(&delta, g->h_ctr + kCtrPrDelta, sizeof(delta));
+    // the L1 change is a fixed-point sum (x 2^62, zc_kernels.cu pr_fx)
+    const double delta = static_cast<double>(g->h_ctr[kCtrPrDelta]) / 4611686018427387904.0;
     if (delta < tol) break;
   }
   ZC_CUDA_TRY(cudaEventRecord(g->ev[1], st));
@@ -2150,6 +2084,37 @@ int zc_graph_evict(zc_graph* g) {
   int rc = cold(g->h_edges, g->ne * g->eb);
   if (rc == ZC_OK && g->h_weights) rc = cold(g->h_weights, g->ne * g->wb);
   return rc;
+}
+
+int zc_set_tuning(zc_graph* g, const char* spec) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  zc_graph::Tuning t;
+  const std::string sp = spec ? spec : "";
+  size_t pos = 0;
+  while (pos < sp.size()) {
+    size_t end = sp.find(',', pos);
+    if (end == std::string::npos) end = sp.size();
+    const std::string kv = sp.substr(pos, end - pos);
+    pos = end + 1;
+    if (kv.empty()) continue;
+    const size_t eq = kv.find('=');
+    const std::string k = kv.substr(0, eq);
+    const std::string v = eq == std::string::npos ? "" : kv.substr(eq + 1);
+    if (k == "unroll" && (v == "2" || v == "4" || v == "8")) t.unroll = std::stoi(v);
+    else if (k == "ctas") t.ctas = std::max(0, atoi(v.c_str()));
+    else if (k == "sched" && (v == "chunk" || v == "sweep")) t.sched = v == "chunk";
+    else if (k == "loop" && (v == "host" || v == "device")) t.host_loop = v == "host";
+    else if (k == "do_alpha" && atof(v.c_str()) > 0) t.do_alpha = atof(v.c_str());
+    else {
+      set_error("unknown tuning entry '" + kv + "'");
+      return ZC_EINVAL;
+    }
+  }
+  g->tune = t;
+  return ZC_OK;
 }
 
 int zc_set_options(zc_graph* g, uint32_t options) {

@@ -104,6 +104,14 @@ struct zc_graph {
   std::vector<double> log_expand_ms;
   std::vector<cudaEvent_t> iter_ev;  // 2 per iteration, grown on demand
   uint32_t options = 0;
+  // launch tuning (zc_set_tuning; read by the run path, never from the environment)
+  struct Tuning {
+    int unroll = 4;   // windows per warp batch in the sweep (2 / 4 / 8)
+    int ctas = 0;     // sweep CTAs per SM (0: occupancy maximum)
+    int sched = 0;    // 1: the round-1 chunk scheduler instead of the sweep
+    int host_loop = 0;  // 1: host-driven level loop (profilers cannot see graph kernels)
+    double do_alpha = 2.0;  // direction-optimizing switch factor
+  } tune;
   int multigraph = -1;  // cached duplicate-arc check (-1 unknown)
   LoopGraph loop;
   uint64_t* d_log = nullptr;  // 4 * kLogCap

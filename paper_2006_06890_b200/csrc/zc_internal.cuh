@@ -29,6 +29,8 @@
 
 #include <string>
 
+struct zc_graph;
+
 namespace zc {
 
 constexpr int kWarp = 32;
@@ -160,7 +162,7 @@ struct ExpandArgs {
   uint64_t* wpre;  // n + 1
   void* scan_tmp;
   size_t scan_tmp_bytes;
-  // launch tuning (host side only; ZC_TUNE environment variable)
+  // launch tuning (host side only; zc_set_tuning)
   int unroll;
   int ctas_per_sm;
   int chunk_sched;  // 1: the per-warp chunk + big-list scheduler instead of the sweep
@@ -183,8 +185,8 @@ struct ExpandArgs {
   uint32_t pull_pass;
 };
 
-// ZC_TUNE="unroll=8,ctas=6,sched=chunk": expansion tuning knobs for experiments.
-void tune_params(ExpandArgs* a);
+// Expansion tuning knobs of a handle (zc_set_tuning "unroll=8,ctas=6,sched=chunk").
+void tune_params(ExpandArgs* a, const ::zc_graph* g);
 
 struct CompactArgs {
   uint8_t* flags;

@@ -139,13 +139,23 @@ struct Visit<kCc> {
   }
 };
 
+// PageRank sums are fixed point (value x 2^62 in a u64): integer atomics add
+// in any order to the same bits, so ranks, the L1 change and with it the
+// iteration count do not depend on the schedule (a float64 atomicAdd does).
+// Every PageRank sum is below 4 (ranks sum to 1); the quantum 2^-62 ~ 2e-19.
+constexpr double kPrFx = 4611686018427387904.0;  // 2^62
+__device__ __forceinline__ unsigned long long pr_fx(double x) { return __double2ull_rn(x * kPrFx); }
+__device__ __forceinline__ double pr_unfx(unsigned long long v) {
+  return __ull2double_rn(v) * (1.0 / kPrFx);
+}
+
 template <>
 struct Visit<kPr> {
   // traversal.py:229: pushed[d] += rank[s] / out[s]; the contribution rides in
-  // the frontier value slot (double bits); pushed lives in a.exch.
+  // the frontier value slot (fixed point, pr_fx); pushed (u64) lives in a.exch.
   static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
                                                uint64_t val) {
-    atomicAdd(static_cast<double*>(a.exch) + w, __longlong_as_double(static_cast<long long>(val)));
+    atomicAdd(static_cast<unsigned long long*>(a.exch) + w, static_cast<unsigned long long>(val));
   }
 };
 
@@ -1176,28 +1186,29 @@ __global__ void k_part_apply(const void* mine, uint64_t n, void* state, uint8_t*
 }
 
 // ---------------------------------------------------------------- PageRank
-__device__ __forceinline__ void atomic_add_ctr(uint64_t* ctr, int slot, double x) {
-  atomicAdd(reinterpret_cast<double*>(ctr + slot), x);
-}
-
-__device__ __forceinline__ double block_sum(double x, double* sh) {
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long x,
+                                                            unsigned long long* sh) {
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) x += __shfl_down_sync(kFull, x, d);
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = x;
   __syncthreads();
-  double t = 0;
+  unsigned long long t = 0;
   if (threadIdx.x == 0)
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sh[w];
   __syncthreads();
   return t;
 }
 
-// contrib[v] = rank[v] / out[v] into the frontier value slot, dangling mass,
-// pushed[] = 0 (traversal.py:218-230).
+__device__ __forceinline__ void add_ctr_fx(uint64_t* ctr, int slot, unsigned long long t) {
+  if (t) atomicAdd(reinterpret_cast<unsigned long long*>(ctr + slot), t);
+}
+
+// contrib[v] = rank[v] / out[v] (fixed point) into the frontier value slot,
+// dangling mass, pushed[] = 0 (traversal.py:218-230).
 __global__ void k_pr_prepare(const double* rank, const uint32_t* deg, uint64_t nv, uint64_t* fval,
-                             double* pushed, uint64_t* ctr) {
-  __shared__ double sh[32];
-  double dang = 0;
+                             unsigned long long* pushed, uint64_t* ctr) {
+  __shared__ unsigned long long sh[32];
+  unsigned long long dang = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t rounds = (nv + stride - 1) / stride;
   for (uint64_t r = 0; r < rounds; ++r) {
@@ -1205,53 +1216,53 @@ __global__ void k_pr_prepare(const double* rank, const uint32_t* deg, uint64_t n
     if (v < nv) {
       const double rv = rank[v];
       const uint32_t d = deg[v];
-      fval[v] = static_cast<uint64_t>(__double_as_longlong(d ? rv * (1.0 / d) : 0.0));
-      if (!d) dang += rv;
-      pushed[v] = 0.0;
+      fval[v] = d ? pr_fx(rv * (1.0 / d)) : 0ull;
+      if (!d) dang += pr_fx(rv);
+      pushed[v] = 0ull;
     }
   }
-  const double t = block_sum(dang, sh);
-  if (threadIdx.x == 0 && t != 0.0) atomic_add_ctr(ctr, kCtrPrDangling, t);
+  const unsigned long long t = block_sum_u64(dang, sh);
+  if (threadIdx.x == 0) add_ctr_fx(ctr, kCtrPrDangling, t);
 }
 
 // new = (1-d)/V + d (pushed + dangling/V); delta += |new - rank| (traversal.py:231-233)
-__global__ void k_pr_update(double* rank, const double* pushed, uint64_t nv, double damping,
-                            uint64_t* ctr) {
-  __shared__ double sh[32];
-  const double dang = __longlong_as_double(static_cast<long long>(ctr[kCtrPrDangling]));
+__global__ void k_pr_update(double* rank, const unsigned long long* pushed, uint64_t nv,
+                            double damping, uint64_t* ctr) {
+  __shared__ unsigned long long sh[32];
+  const double dang = pr_unfx(ctr[kCtrPrDangling]);
   const double base = (1.0 - damping) / static_cast<double>(nv);
-  double delta = 0;
+  unsigned long long delta = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t rounds = (nv + stride - 1) / stride;
   for (uint64_t r = 0; r < rounds; ++r) {
     const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + r * stride;
     if (v < nv) {
-      const double nr = base + damping * (pushed[v] + dang / static_cast<double>(nv));
-      delta += fabs(nr - rank[v]);
+      const double nr = base + damping * (pr_unfx(pushed[v]) + dang / static_cast<double>(nv));
+      delta += pr_fx(fabs(nr - rank[v]));
       rank[v] = nr;
     }
   }
-  const double t = block_sum(delta, sh);
-  if (threadIdx.x == 0 && t != 0.0) atomic_add_ctr(ctr, kCtrPrDelta, t);
+  const unsigned long long t = block_sum_u64(delta, sh);
+  if (threadIdx.x == 0) add_ctr_fx(ctr, kCtrPrDelta, t);
 }
 
 // sum of ranks (divide == false) or rank /= sum (divide == true) (traversal.py:248)
 __global__ void k_pr_normalize(double* rank, uint64_t nv, uint64_t* ctr, int divide) {
-  __shared__ double sh[32];
-  const double total = __longlong_as_double(static_cast<long long>(ctr[kCtrPrSum]));
-  double acc = 0;
+  __shared__ unsigned long long sh[32];
+  const double total = pr_unfx(ctr[kCtrPrSum]);
+  unsigned long long acc = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t rounds = (nv + stride - 1) / stride;
   for (uint64_t r = 0; r < rounds; ++r) {
     const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x + r * stride;
     if (v < nv) {
       if (divide) rank[v] = rank[v] / total;
-      else acc += rank[v];
+      else acc += pr_fx(rank[v]);
     }
   }
   if (!divide) {
-    const double t = block_sum(acc, sh);
-    if (threadIdx.x == 0) atomic_add_ctr(ctr, kCtrPrSum, t);
+    const unsigned long long t = block_sum_u64(acc, sh);
+    if (threadIdx.x == 0) add_ctr_fx(ctr, kCtrPrSum, t);
   }
 }
 
@@ -1718,8 +1729,10 @@ cudaError_t launch_pr_init(uint64_t nv, const uint64_t* off, uint32_t* front, ui
 
 cudaError_t launch_pr_prepare(const double* rank, const uint32_t* deg, uint64_t nv, uint64_t* fval,
                               double* pushed, uint64_t* ctr, cudaStream_t st, uint64_t* launches) {
+  // pushed holds fixed-point sums (pr_fx): same 8 bytes per vertex
   const int g = grid_for(nv, 256, 148, 8);
-  k_pr_prepare<<<g, 256, 0, st>>>(rank, deg, nv, fval, pushed, ctr);
+  k_pr_prepare<<<g, 256, 0, st>>>(rank, deg, nv, fval,
+                                   reinterpret_cast<unsigned long long*>(pushed), ctr);
   *launches += 1;
   return cudaGetLastError();
 }
@@ -1727,7 +1740,8 @@ cudaError_t launch_pr_prepare(const double* rank, const uint32_t* deg, uint64_t 
 cudaError_t launch_pr_update(double* rank, const double* pushed, uint64_t nv, double damping,
                              uint64_t* ctr, cudaStream_t st, uint64_t* launches) {
   const int g = grid_for(nv, 256, 148, 8);
-  k_pr_update<<<g, 256, 0, st>>>(rank, pushed, nv, damping, ctr);
+  k_pr_update<<<g, 256, 0, st>>>(rank, reinterpret_cast<const unsigned long long*>(pushed), nv,
+                                  damping, ctr);
   *launches += 1;
   return cudaGetLastError();
 }

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "../../include/zcgraph.h"
+#include "../../include/zcprobe.h"
 #include "zc_internal.cuh"
 
 namespace zc {

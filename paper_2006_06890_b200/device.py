@@ -256,6 +256,12 @@ class DeviceGraph:
         return out
 
     # -- run plumbing
+    def set_tuning(self, spec: str = "") -> None:
+        """Launch tuning of this handle (zc_set_tuning): comma-separated
+        unroll=2|4|8, ctas=N, sched=chunk|sweep, loop=host|device, do_alpha=X;
+        "" restores the defaults."""
+        N.check(N.lib().zc_set_tuning(self.handle, spec.encode()))
+
     def set_traffic_model(self, on: bool) -> None:
         opt = N.ZC_OPT_TRAFFIC_MODEL if on else 0
         if opt != self._options:
@@ -431,7 +437,7 @@ def read_probe(nbytes: int, chunk_bytes: int, random, alloc: str = "pinned",
     """GB/s of warps reading chunk_bytes per request (zero-copy toy kernel)."""
     a = {"pinned": 0, "thp": 1, "hbm": 2, "vmm": 3, "hugetlb": 4, "managed_host": 5}[alloc]
     out = C.c_double()
-    N.check(N.lib().zc_read_probe(device, nbytes, int(random), chunk_bytes, a, iters,
+    N.check(N.probe_lib().zc_read_probe(device, nbytes, int(random), chunk_bytes, a, iters,
                                   C.byref(out)))
     return out.value
 
@@ -439,5 +445,5 @@ def read_probe(nbytes: int, chunk_bytes: int, random, alloc: str = "pinned",
 def link_probe(device: int = 0, nbytes: int = 1 << 30, iters: int = 5) -> dict:
     """Measured host-link and HBM read bandwidths (GB/s)."""
     m, z, h = C.c_double(), C.c_double(), C.c_double()
-    N.check(N.lib().zc_link_probe(device, nbytes, iters, C.byref(m), C.byref(z), C.byref(h)))
+    N.check(N.probe_lib().zc_link_probe(device, nbytes, iters, C.byref(m), C.byref(z), C.byref(h)))
     return {"memcpy_h2d_gbs": m.value, "zerocopy_read_gbs": z.value, "hbm_read_gbs": h.value}

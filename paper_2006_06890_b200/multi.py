@@ -336,18 +336,14 @@ def is_direction_optimizing(strategy) -> bool:
     return strategy_id(strategy) == 5
 
 
-def do_alpha() -> float:
-    """The direction switch factor: ZC_TUNE=do_alpha=X, default 2 (as zc_api.cu)."""
-    import os
-    import re
-    m = re.search(r"do_alpha=([0-9.]+)", os.environ.get("ZC_TUNE", ""))
-    return float(m.group(1)) if m and float(m.group(1)) > 0 else 2.0
+DO_ALPHA = 2.0  # the direction switch factor, zc_graph::Tuning::do_alpha's default
 
 
-def pull_now(iteration: int, frontier_out_edges: int, unvisited_in_edges: int) -> bool:
+def pull_now(iteration: int, frontier_out_edges: int, unvisited_in_edges: int,
+             alpha: float = DO_ALPHA) -> bool:
     """Bottom-up when the frontier's out-edges exceed the unvisited vertices'
     in-edges / alpha (never the source's own expansion) -- zc_api.cu's rule."""
-    return iteration > 1 and frontier_out_edges * do_alpha() > unvisited_in_edges
+    return iteration > 1 and frontier_out_edges * alpha > unvisited_in_edges
 
 
 def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartResult:

@@ -69,9 +69,21 @@ def _has_weights(g) -> bool:
     return g.weights is not None
 
 
-def _run(algo: str, g, source: int, strategy, collect_traffic: bool, want_pages: bool,
+def _model_wanted(collect_traffic: Optional[bool], sid: int) -> bool:
+    """The reference's request model (coalesce.py:165-207) is defined for its
+    three strategies only.  ``collect_traffic=None`` (the default) means "if
+    the strategy has a model": on for naive / merged / merged-aligned (the
+    reference's default, traversal.py:99), off for the B200 extensions, which
+    then return zero TrafficStats.  An explicit True with an extension raises."""
+    if collect_traffic is None:
+        return sid <= 2
+    return bool(collect_traffic)
+
+
+def _run(algo: str, g, source: int, strategy, collect_traffic: Optional[bool], want_pages: bool,
          placement: str, device: int) -> TraversalResult:
     sid = strategy_id(strategy)
+    collect_traffic = _model_wanted(collect_traffic, sid)
     if want_pages:
         # The page streams feed the reference's LRU page-migration simulator
         # (uvm.py), which this build replaces with a real managed-memory run.
@@ -81,7 +93,7 @@ def _run(algo: str, g, source: int, strategy, collect_traffic: bool, want_pages:
     dg = device_graph(g, placement, device)
     out, st, trav, front, hist = dg.run(algo, int(source), sid, traffic=collect_traffic)
     if hist is not None:
-        per_iter = [TrafficStats.from_size_counts(h[:4] + h[4:]) for h in hist.astype(np.int64)]
+        per_iter = [TrafficStats.from_device_hist(h) for h in hist]
     else:
         per_iter = [TrafficStats.zero() for _ in range(st.iterations)]
     return TraversalResult(
@@ -91,9 +103,9 @@ def _run(algo: str, g, source: int, strategy, collect_traffic: bool, want_pages:
         launches=int(st.launches), h2d_bytes=int(st.h2d_bytes), d2h_bytes=int(st.d2h_bytes))
 
 
-def bfs(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traffic: bool = True,
-        want_pages: bool = False, page_bytes: int = 4096, placement: str = "zerocopy",
-        device: int = 0) -> TraversalResult:
+def bfs(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *,
+        collect_traffic: Optional[bool] = None, want_pages: bool = False,
+        page_bytes: int = 4096, placement: str = "zerocopy", device: int = 0) -> TraversalResult:
     """Unweighted hop distances from source; unreached vertices get -1.
 
     One iteration per level including the final empty expansion, so
@@ -103,9 +115,9 @@ def bfs(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traff
     return _run("bfs", g, source, strategy, collect_traffic, want_pages, placement, device)
 
 
-def sssp(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traffic: bool = True,
-         want_pages: bool = False, page_bytes: int = 4096, placement: str = "zerocopy",
-         device: int = 0) -> TraversalResult:
+def sssp(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *,
+         collect_traffic: Optional[bool] = None, want_pages: bool = False,
+         page_bytes: int = 4096, placement: str = "zerocopy", device: int = 0) -> TraversalResult:
     """Exact shortest distances by frontier-restricted (Jacobi) relaxation
     (reference traversal.py:123-151); unreached vertices get INT64_MAX."""
     _check_source(g, source)
@@ -116,7 +128,7 @@ def sssp(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traf
     return _run("sssp", g, source, strategy, collect_traffic, want_pages, placement, device)
 
 
-def cc(g, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traffic: bool = True,
+def cc(g, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traffic: Optional[bool] = None,
        want_pages: bool = False, page_bytes: int = 4096, placement: str = "zerocopy",
        device: int = 0) -> TraversalResult:
     """Connected-component labels (min vertex id) by minimum-label propagation,
@@ -130,6 +142,7 @@ def cc(g, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traffic: bool = Tru
 def _run_many(algo: str, g, sources, strategy, collect_traffic: bool, placement: str,
               device: int) -> list:
     srcs = [int(s) for s in sources]
+    collect_traffic = bool(collect_traffic)
     for s in srcs:
         _check_source(g, s)
     if collect_traffic:  # the request model runs per level on the host loop
@@ -168,7 +181,7 @@ def sssp_many(g, sources, strategy=AccessStrategy.MERGED_ALIGNED, *,
 
 
 def pagerank(g, strategy=AccessStrategy.MERGED_ALIGNED, damping: float = 0.85,
-             max_iters: int = 100, tol: float = 1e-6, *, collect_traffic: bool = True,
+             max_iters: int = 100, tol: float = 1e-6, *, collect_traffic: Optional[bool] = None,
              want_pages: bool = False, page_bytes: int = 4096, placement: str = "zerocopy",
              device: int = 0) -> TraversalResult:
     """Synchronous push PageRank over the full edge list each iteration
@@ -185,6 +198,7 @@ def pagerank(g, strategy=AccessStrategy.MERGED_ALIGNED, damping: float = 0.85,
     if g.num_vertices == 0:
         raise ValueError("pagerank needs at least one vertex")
     sid = strategy_id(strategy)
+    collect_traffic = _model_wanted(collect_traffic, sid)
     if want_pages:
         raise NotImplementedError(
             "page streams are a simulator artefact; run with placement='uvm' for the real "
@@ -198,7 +212,7 @@ def pagerank(g, strategy=AccessStrategy.MERGED_ALIGNED, damping: float = 0.85,
     out, st, hist = _pagerank_run(dg, sid, damping, max_iters, tol, collect_traffic)
     it = int(st.iterations)
     if hist is not None:
-        per_iter = [TrafficStats.from_size_counts(h[:4] + h[4:]) for h in hist.astype(np.int64)]
+        per_iter = [TrafficStats.from_device_hist(h) for h in hist]
     else:
         per_iter = [TrafficStats.zero() for _ in range(it)]
     return TraversalResult(

@@ -13,11 +13,18 @@ from paper_2006_06890_b200 import _native
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "zcgraph.h")
+PROBE_HEADER = os.path.join(ROOT, "include", "zcprobe.h")
 
 
-def header_functions():
-    text = open(HEADER).read()
+def header_functions(path=HEADER):
+    text = open(path).read()
     return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(zc_\w+)\s*\(", text, re.M)))
+
+
+def exported_symbols(path):
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True,
+                         text=True, check=True).stdout
+    return set(re.findall(r" T (zc_\w+)", out))
 
 
 def test_header_declares_expected_api():
@@ -30,12 +37,22 @@ def test_header_declares_expected_api():
 
 def test_library_exports_every_declared_symbol():
     lib = _native.lib()
-    out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True,
-                         text=True, check=True).stdout
-    exported = set(re.findall(r" T (zc_\w+)", out))
+    exported = exported_symbols(_native.LIB_PATH)
     missing = set(header_functions()) - exported
     assert not missing, missing
+    # the product ABI is exactly the header: no probe / debug entry points
+    assert exported == set(header_functions()), exported - set(header_functions())
     for name in header_functions():
+        assert hasattr(lib, name)
+
+
+def test_probe_library_is_separate():
+    probes = header_functions(PROBE_HEADER)
+    assert set(probes) == set(_native.PROBE_EXPORTED)
+    assert not set(probes) & set(header_functions())
+    assert set(probes) <= exported_symbols(_native.PROBE_LIB_PATH)
+    lib = _native.probe_lib()
+    for name in probes:
         assert hasattr(lib, name)
 
 
@@ -109,3 +126,15 @@ def test_open_emgi_header_errors_match_reference(tmp_path):
     p.write_bytes(raw[:4] + (2).to_bytes(4, "little") + raw[8:])
     with pytest.raises(ValueError, match="version"):
         zc.open_emgi(str(p))
+
+
+def test_open_emgi_rejects_wrapping_header_counts(tmp_path):
+    """Untrusted header counts are bounded by the file size before any
+    multiplication (a wrapped ne * 4 must not pass the truncation check)."""
+    import struct
+    for nv, ne in ((4, (1 << 62) + 1), (4, (1 << 64) - 1), ((1 << 61), 2), ((1 << 64) - 1, 0)):
+        path = tmp_path / f"bad_{nv}_{ne}.emgi"
+        body = struct.pack("<4sIIQQ", b"EMGI", 1, 0, nv, ne) + bytes(8 * 5 + 128)
+        path.write_bytes(body)
+        with pytest.raises(ValueError, match="truncated"):
+            zc.open_emgi(str(path))

@@ -264,8 +264,9 @@ def test_rmat_partition_generator_matches_whole_graph():
 
 def test_pagerank_matches_reference():
     """Reference pagerank outputs (incl. acceptance criterion 6's PR stream):
-    L-inf <= 1e-8 (test_acceptance.py:169-180), same iteration count, the
-    multigraph flag; all strategies."""
+    L-inf <= 1e-8 (test_acceptance.py:169-180), the same iteration count (the
+    push sums are fixed point, so the count does not depend on the atomic
+    order), the multigraph flag; all strategies."""
     import warnings
     from fixtures import pagerank_cases
     bad = []
@@ -275,7 +276,7 @@ def test_pagerank_matches_reference():
                 warnings.simplefilter("always")
                 r = zc.pagerank(g, s, dmp, mi, tol, collect_traffic=False)
             err = float(np.abs(r.values - ranks).max())
-            if err > 1e-8 or abs(r.iterations - iters) > 1 or ("multigraph" in r.flags) != multi:
+            if err > 1e-8 or r.iterations != iters or ("multigraph" in r.flags) != multi:
                 bad.append((k, getattr(s, "value", s), err, r.iterations, iters))
             if multi:
                 assert any("multigraph" in str(w.message) for w in caught)

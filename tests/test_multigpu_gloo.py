@@ -97,7 +97,7 @@ def test_partitioned_direction_optimizing_driver(world):
 
 
 def test_pull_rule():
-    from paper_2006_06890_b200.multi import do_alpha, pull_now
-    assert do_alpha() == 2.0
+    from paper_2006_06890_b200.multi import DO_ALPHA, pull_now
+    assert DO_ALPHA == 2.0
     assert not pull_now(1, 10**9, 1)          # never the source's own expansion
     assert pull_now(2, 600, 1000) and not pull_now(2, 400, 1000)

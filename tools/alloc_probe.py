@@ -14,7 +14,7 @@ size = int(sys.argv[1]) if len(sys.argv) > 1 else 8 << 30
 print(subprocess.run("grep -i huge /proc/meminfo; cat /sys/kernel/mm/transparent_hugepage/enabled",
                      shell=True, capture_output=True, text=True).stdout, flush=True)
 g = C.c_uint64()
-rc = N.lib().zc_vmm_host_probe(0, 1 << 30, C.byref(g))
+rc = N.probe_lib().zc_vmm_host_probe(0, 1 << 30, C.byref(g))
 print("vmm host granularity", g.value, "rc", rc, N.lib().zc_last_error().decode() if rc else "",
       flush=True)
 if os.geteuid() == 0:

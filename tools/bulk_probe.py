@@ -12,6 +12,6 @@ for ctas in (1, 2, 4, 8):
         if chunk * 4 > 200 * 1024:
             continue
         out = C.c_double()
-        rc = N.lib().zc_bulk_probe(0, size, chunk, ctas, 3, C.byref(out))
+        rc = N.probe_lib().zc_bulk_probe(0, size, chunk, ctas, 3, C.byref(out))
         row.append(f"{chunk}B:{out.value:6.2f}" if rc == 0 else f"{chunk}B:err")
     print(f"ctas/SM={ctas}: " + " ".join(row), flush=True)

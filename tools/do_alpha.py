@@ -8,7 +8,7 @@ dg = zc.generate_rmat(27, 16, seed=27)
 srcs = [int(s) for s in zc.pick_sources(dg.as_csr(), 64, seed=7)[:16]]
 zc.bfs(dg, srcs[0], "direction-optimizing", collect_traffic=False)
 for a in [float(x) for x in sys.argv[1].split(",")]:
-    os.environ["ZC_TUNE"] = f"do_alpha={a}"
+    dg.set_tuning(f"do_alpha={a}")
     e = ms = 0
     per = []
     for s in srcs:

@@ -24,7 +24,7 @@ for s in srcs[:1]:
     print(f"compressed src={s} {ref.kernel_ms:.2f} ms GTEPS={ref.total_traversed_edges/ref.kernel_ms/1e6:.2f} "
           f"levels: " + " ".join(f"{p:.2f}" for p in prof), flush=True)
 for a in alphas:
-    os.environ["ZC_TUNE"] = f"do_alpha={a}"
+    dg.set_tuning(f"do_alpha={a}")
     tot_e = tot_ms = 0
     for s in srcs:
         zc.bfs(dg, s, "direction-optimizing", collect_traffic=False)

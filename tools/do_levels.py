@@ -22,7 +22,7 @@ for s in [int(x) for x in sys.argv[1].split(",")]:
               f"ratio={r.traversed_edges[k]/max(mu,1):7.3f} td={td[k]:7.2f} ms", flush=True)
         mu -= int(indeg[lv == k + 1].sum())
     for a in (0.5, 1, 2, 4):
-        os.environ["ZC_TUNE"] = f"do_alpha={a}"
+        dg.set_tuning(f"do_alpha={a}")
         r = zc.bfs(dg, s, "direction-optimizing", collect_traffic=False)
         p = dg.expand_profile(r.iterations)
         d = dg.directions(r.iterations)

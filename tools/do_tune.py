@@ -7,7 +7,7 @@ dg = zc.generate_rmat(27, 16, seed=27, placement=os.environ.get("PLACEMENT", "ze
 srcs = [int(s) for s in zc.pick_sources(dg.as_csr(), 64, seed=7)[:16]]
 zc.bfs(dg, srcs[0], "direction-optimizing", collect_traffic=False)
 for tune in sys.argv[1:]:
-    os.environ["ZC_TUNE"] = tune
+    dg.set_tuning(tune)
     e = ms = 0
     for s in srcs:
         r = zc.bfs(dg, s, "direction-optimizing", collect_traffic=False)

@@ -11,6 +11,7 @@ ap.add_argument("--algo", default="bfs")
 ap.add_argument("--strategies", default="merged-aligned,merged")
 ap.add_argument("--placement", default="zerocopy")
 ap.add_argument("--uniform", action="store_true")
+ap.add_argument("--tuning", default="", help="zc_set_tuning spec, e.g. loop=host under ncu")
 a = ap.parse_args()
 t = time.time()
 if a.algo == "sssp" and a.uniform:
@@ -19,6 +20,7 @@ if a.algo == "sssp" and a.uniform:
 else:
     dg = zc.generate_rmat(a.scale, a.ef, seed=27, symmetrize=a.algo == "cc",
                           weights=(8, 72) if a.algo == "sssp" else None, placement=a.placement)
+dg.set_tuning(a.tuning)
 print(f"gen {time.time()-t:.1f}s V={dg.num_vertices} E={dg.num_edges}", flush=True)
 src = int(zc.pick_sources(dg.as_csr(), 64, seed=7)[0])
 eb = 8 if a.algo == "sssp" else 4

@@ -7,8 +7,7 @@ set -x
 R=${1:-r01}
 STRAT=${2:-compressed}
 mkdir -p gpurun_out
-export ZC_TUNE=loop=host
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$R.csv \
-    python bench.py --steps 2 --warmup 3 --no-variants --no-cpu-baseline --no-configs \
+    python bench.py --tuning loop=host --steps 2 --warmup 3 --no-variants --no-cpu-baseline --no-configs \
     > gpurun_out/bench_ncu_$R.log 2>&1
 bash tools/ncu_levels.sh ${R}_$STRAT $STRAT "2 3 4"

@@ -31,7 +31,7 @@ if a.strategies:
     runs = [("", s) for s in a.strategies.split(",")]
 for cfg, strategy in runs:
     a.strategy = strategy
-    os.environ["ZC_TUNE"] = cfg
+    dg.set_tuning(cfg)
     best = None
     for rep in range(3):
         r = zc.cc(dg, a.strategy, collect_traffic=False) if a.algo == "cc" else \
