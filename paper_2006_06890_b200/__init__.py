@@ -10,7 +10,7 @@ CUDA kernels behind a C ABI (include/zcgraph.h); there is no CPU fallback.
 """
 from .access import LINE_BYTES, SECTOR_BYTES, WARP_LANES, AccessStrategy
 from .csr import (CsrGraph, DegreeCdf, degree_cdf, generate_powerlaw, generate_uniform,
-                  load_csr_binary, pick_sources, store_csr_binary, symmetrized, validate,
+                  load_csr_binary, load_edge_list_text, pick_sources, store_csr_binary, symmetrized, validate,
                   with_uniform_weights)
 from .device import (DeviceGraph, device_graph, evict, generate_rmat, generate_uniform_device,
                      link_probe, open_emgi, pinned_empty, release)
@@ -24,7 +24,7 @@ __all__ = [
     "AccessStrategy", "CsrGraph", "DegreeCdf", "DeviceGraph", "LINE_BYTES", "SECTOR_BYTES",
     "TrafficStats", "TraversalResult", "UNREACHED_DIST", "UNREACHED_LEVEL", "WARP_LANES",
     "bfs", "bfs_many", "cc", "degree_cdf", "device_graph", "evict", "generate_powerlaw", "generate_rmat",
-    "generate_uniform", "generate_uniform_device", "link_probe", "load_csr_binary", "open_emgi",
+    "generate_uniform", "generate_uniform_device", "link_probe", "load_csr_binary", "load_edge_list_text", "open_emgi",
     "pagerank", "pick_sources", "pinned_empty", "release", "sssp", "sssp_many", "store_csr_binary", "symmetrized",
     "validate", "with_uniform_weights",
 ]

@@ -9,6 +9,8 @@ from fixtures import crc, goldens
 
 import paper_2006_06890_b200 as zc
 
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
 
 def _check_graph(g, rec):
     assert g.num_vertices == rec["V"] and g.num_edges == rec["E"]
@@ -99,8 +101,40 @@ def test_validate_rejects():
         zc.validate(bad)
 
 
+def _reference():
+    import oracle
+    try:
+        return oracle.reference()
+    except ImportError:
+        pytest.skip("reference package unavailable (no /root/reference, no oracle/_ref zip)")
+
+
 def test_reference_csrgraph_duck_typing():
     """Graphs built by the reference itself are accepted (duck typing)."""
-    ref = pytest.importorskip("zcgraph", reason="reference package not importable here")
+    ref = _reference()
     g = ref.generate_uniform(200, 1, 5, seed=2)
     assert zc.pick_sources(g, 2).tolist() == ref.pick_sources(g, 2).tolist()
+    zc.validate(g)
+
+
+def test_load_edge_list_text_matches_reference_fixture(tmp_path):
+    """load_edge_list_text against the reference's own outputs
+    (tests/golden/make_golden_text.py; csr.py:123-177): CSR arrays, vertex
+    count, weights, and the ValueError messages."""
+    import json
+    rows = json.loads(str(np.load(os.path.join(GOLDEN, "edge_list_text.npz"))["cases"]))
+    assert len(rows) >= 100
+    for k, row in enumerate(rows):
+        path = tmp_path / f"case{k}.txt"
+        path.write_text(row["text"])
+        if "error" in row:
+            with pytest.raises(ValueError) as exc:
+                zc.load_edge_list_text(str(path), directed=row["directed"],
+                                       num_vertices=row["num_vertices"])
+            assert str(exc.value) == row["error"], k
+            continue
+        g = zc.load_edge_list_text(str(path), directed=row["directed"],
+                                   num_vertices=row["num_vertices"])
+        assert g.num_vertices == row["nv_out"] and g.directed == row["directed"], k
+        assert g.offsets.tolist() == row["offsets"] and g.edges.tolist() == row["edges"], k
+        assert (None if g.weights is None else g.weights.tolist()) == row["weights"], k

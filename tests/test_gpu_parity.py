@@ -44,13 +44,52 @@ def test_small_graphs_match_reference(strategy):
 
 @pytest.mark.parametrize("placement", ["uvm", "hbm", "zerocopy-managed"])
 def test_small_graphs_other_placements(placement):
+    """Every fixture on the other placements: values, iterations and
+    per-iteration traversed edges."""
     bad = []
-    for c in CASES[::3]:
+    for c in CASES:
         r = _run(c, zc.AccessStrategy.MERGED_ALIGNED, placement)
-        if not (np.array_equal(r.values, c.values) and r.iterations == c.iterations):
+        if not (np.array_equal(r.values, c.values) and r.iterations == c.iterations
+                and r.traversed_edges == c.traversed):
             bad.append((c.index, c.tag))
         zc.release(c.graph)
     assert not bad, bad[:8]
+
+
+def test_host_rmat_generator_matches_device():
+    """oracle.generate_rmat (host C, the bench's reference arm input) builds
+    byte-identical CSR to the product's GPU generator."""
+    for scale, ef, seed in ((10, 16, 27), (16, 16, 5), (17, 8, 27)):
+        dg = zc.generate_rmat(scale, ef, seed=seed)
+        off, edges = oracle.generate_rmat(scale, ef, seed=seed, threads=4)
+        g = dg.as_csr()
+        assert np.array_equal(np.asarray(g.offsets, np.int64), off)
+        assert np.array_equal(np.asarray(g.edges, np.uint32), edges)
+        dg.close()
+
+
+def test_reference_built_graphs_traverse_like_the_reference():
+    """Graphs built by the unmodified reference (oracle.reference(): the
+    /root/reference tree or its oracle/_ref zip on the GPU box) traversed by
+    the CUDA path equal the reference's own bfs / sssp / cc results."""
+    try:
+        ref = oracle.reference()
+    except ImportError:
+        pytest.skip("reference package unavailable")
+    g = ref.with_uniform_weights(ref.generate_powerlaw(3000, 6.0, seed=11))
+    gu = ref.symmetrized(ref.generate_uniform(2000, 0, 5, seed=12))
+    for src in [int(x) for x in ref.pick_sources(g, 3, seed=7)]:
+        for algo in ("bfs", "sssp"):
+            want = getattr(ref, algo)(g, src, collect_traffic=False)
+            for s in ALL + ["compressed"] + (["direction-optimizing"] if algo == "bfs" else []):
+                got = getattr(zc, algo)(g, src, s, collect_traffic=False)
+                assert np.array_equal(got.values, want.values), (algo, s, src)
+                assert got.iterations == want.iterations, (algo, s, src)
+                assert got.traversed_edges == [int(x) for x in want.traversed_edges], (algo, s)
+    want = ref.cc(gu, collect_traffic=False)
+    for s in ALL + ["compressed"]:
+        got = zc.cc(gu, s, collect_traffic=False)
+        assert np.array_equal(got.values, want.values) and got.iterations == want.iterations
 
 
 def test_traffic_model_matches_reference():
