@@ -1,26 +1,32 @@
 #!/usr/bin/env python
-"""Benchmark: EMOGI zero-copy BFS on a Kronecker scale-27 graph (BASELINE.json
-configs[1]: ~2.1 B directed arcs, edge list in pinned host memory, 1x B200,
-naive vs merged vs merged+aligned vs UVM).
+"""Benchmark: EMOGI zero-copy BFS on a Kronecker scale-27 graph, merged+aligned
+(BASELINE.json configs[1]: ~2.1 B directed arcs, edge list in pinned host
+memory, 1x B200; naive vs merged vs merged+aligned vs UVM).
 
-Metric: GTEPS = traversed edges (sum of frontier degrees, the reference's
-traversed_edges, traversal.py:63-65) / second, whole job.  One step = one BFS
-from the next of pick_sources(g, 64, seed=7).
+Metric: GTEPS = traversed edges (the reference's traversed_edges, the sum of
+frontier degrees, traversal.py:63-65) / second.  One step = one BFS from the
+next of pick_sources(g, 64, seed=7).
 
-  value  device time (CUDA events on the library stream) of the traversal
-         loop, graph resident in its placement (edges in pinned host memory)
-  e2e    the same through the public API (paper_2006_06890_b200.bfs_many on
-         a DeviceGraph, the reference's per-source loop as one call): source
-         H2D, traversal, D2H of every source's int64 levels into pinned host
-         memory (overlapped with the next source's traversal) -- host wall
-         clock; per_call_value = one blocking bfs() per source
-  roofline  dominant kernel = the expansion kernels (the zero-copy edge
-         stream): algorithmic bytes = traversed edges x 4 B, over their
-         CUDA-event time, against PCIe Gen5 x16 (63.0 GB/s per direction)
+  value     device time (CUDA events on the library's stream) of the level
+            loop, merged+aligned (the paper's kernel, north_star's target),
+            lists resident in pinned host memory
+  e2e       the same through the public API (bfs_many: every source's int64
+            levels land in pinned host memory; source H2D and result D2H in
+            the timed region), host wall clock
+  roofline  SURVEY 8(d): dominant kernel = the expansion sweep; algorithmic
+            bytes = traversed edges x 4 B; achieved = those bytes / the
+            sweep's device time (globaltimer stamps around the expansion
+            launches inside the level graph, summed over the timed steps);
+            peak = PCIe Gen5 x16, 63.0 GB/s per direction; traffic = ncu
+            sysmem bytes of the main-level launch (profiles/ncu_summary.json)
+  parity    every reported variant is compared with the CPU oracle (values,
+            iterations, per-iteration traversed edges) on the same graph
+  cpu_baseline  the unmodified reference (oracle/_ref zip) on a bounded sample
+            (Kronecker scale 21, same generator), one core
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-Under torchrun (N>1) each rank generates and traverses its own replica
-(scaling "weak"); rank 0 prints the JSON line.
+Under torchrun (N>1) the graph is vertex-range partitioned (BASELINE
+configs[4]); rank 0 prints the JSON line.
 """
 from __future__ import annotations
 
@@ -30,14 +36,18 @@ import os
 import statistics
 import subprocess
 import sys
+import tempfile
 import threading
 import time
+import zlib
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PCIE_GEN5_X16_GBS = 63.0  # 32 GT/s x 16 lanes x 128/130 / 8, per direction
-METRIC = "BFS GTEPS (Kronecker scale-27, edge list zero-copy in pinned host memory)"
+METRIC = "BFS GTEPS (Kronecker scale-27, merged+aligned, edge list zero-copy in pinned host memory)"
+REF_SAMPLE_SCALE = 21  # the reference's bounded sample: same generator, 2^25 arcs (~5 s / BFS)
+C1_LEVELS_CRC = "171fbc8b"  # reference BFS from 0 on generate_uniform(2**20,16,16,seed=3)
 
 
 def parse():
@@ -49,25 +59,21 @@ def parse():
     p.add_argument("--scale", type=int, default=27)
     p.add_argument("--edge-factor", type=int, default=16)
     p.add_argument("--seed", type=int, default=27)
-    # compressed: lists that read fewer sectors that way are stored as
-    # self-describing 128-byte delta lines, the rest read raw with packed
-    # windows (merged-aligned line windows shared across adjacent frontier
-    # lists) -- B200 host-store extension, bit-identical results; variants
-    # report naive / merged / merged-aligned / packed beside it
-    # direction-optimizing: compressed top-down steps, bottom-up steps over the
-    # compressed in-lists once the frontier is large (B200 extension; levels,
-    # iterations and traversed_edges identical to the reference)
-    p.add_argument("--strategy", default="direction-optimizing")
+    p.add_argument("--strategy", default="merged-aligned")
+    p.add_argument("--tuning", default="", help="zc_set_tuning spec (loop=host under ncu)")
     p.add_argument("--no-variants", action="store_true",
-                   help="skip the naive / merged / UVM / HBM comparison runs")
+                   help="skip the naive / merged / packed / compressed / UVM / HBM runs")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-configs", action="store_true",
-                   help="skip the SSSP-U27 / CC-K27 lines (BASELINE configs[2], configs[3])")
+                   help="skip the SSSP-U27 / CC-K27 blocks (BASELINE configs[2], configs[3])")
+    p.add_argument("--no-c1", action="store_true", help="skip the config-1 block")
     p.add_argument("--cpu-threads", type=int, default=0)
     # test hooks for the partitioned path on a 1-GPU box
     p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     p.add_argument("--device-override", type=int, default=-1)
     p.add_argument("--force-partitioned", action="store_true")
+    p.add_argument("--part-scale", type=int, default=29,
+                   help="N>1: Kronecker scale of the partitioned graph (fixed size)")
     p.add_argument("--no-fused", action="store_true",
                    help="N>1: skip the fused (NVLink peer-store) exchange variant")
     return p.parse_args()
@@ -147,7 +153,6 @@ def barrier(world: int, device: int):
     torch.cuda.synchronize(device)
     import torch.distributed as dist
     if dist.is_initialized():
-        import torch.distributed as dist
         dist.barrier()
         torch.cuda.synchronize(device)
 
@@ -181,257 +186,516 @@ def load_ncu_summary() -> dict:
     return {}
 
 
-def cpu_baseline(g, sources, threads: int, budget_s: float = 25.0, check=None) -> dict:
-    """The oracle port (oracle/zc_oracle.c, OpenMP) on the same graph: BFS from
-    the bench sources until ~budget_s of CPU work.  check(source, oracle
-    result) -> bool compares the GPU's result for the same source (parity at
-    the full bench size)."""
+def crc_hex(values) -> str:
+    import numpy as np
+    return f"{zlib.crc32(np.ascontiguousarray(values, dtype=np.int64).tobytes()) & 0xffffffff:08x}"
+
+
+# ------------------------------------------------------------- the reference
+def reference_sample(steps: int, warmup: int, seed: int, threads: int, scale=REF_SAMPLE_SCALE):
+    """The unmodified reference's bfs (collect_traffic=False, traversal.py:
+    98-120) on a bounded sample of the bench workload: Kronecker scale
+    `scale` from the same counter-based R-MAT generator (host copy in
+    oracle/zc_oracle_gen.c, pinned to the GPU generator by a GPU test), the
+    same source rule.  Falls back to the oracle port when the reference is
+    not importable.  Never loads the product library."""
+    import numpy as np
     import oracle
-    done, edges, t_total = 0, 0, 0.0
-    parity = []
-    for s in sources:
-        t0 = time.perf_counter()
-        r = oracle.bfs(g, int(s), threads=threads)
-        t_total += time.perf_counter() - t0
-        edges += sum(r.traversed_edges)
-        done += 1
-        if check is not None and len(parity) < 3:
-            parity.append(bool(check(int(s), r)))
-        if t_total > budget_s:
-            break
-    return {"value": edges / t_total / 1e9, "unit": "GTEPS", "cores": threads, "kind": "port",
-            "sample": f"{done} full BFS run(s) of the oracle port (OpenMP C restatement of "
-                      f"traversal.py:98-120) on the same in-memory graph, {threads} threads",
-            "seconds": t_total,
-            "gpu_bit_exact_vs_oracle": parity}
+    t0 = time.perf_counter()
+    off, edges = oracle.generate_rmat(scale, 16, seed=seed, threads=threads)
+    gen_s = time.perf_counter() - t0
+    try:
+        ref = oracle.reference()
+        kind, cores = "reference", 1
+        g = ref.CsrGraph(1 << scale, int(off[-1]), off, edges.astype(np.int64))
+        sources = ref.pick_sources(g, 64, seed=7)
+
+        def one(s):
+            return ref.bfs(g, int(s), collect_traffic=False)
+        where = "oracle/_ref zip of /root/reference/pkg/src/zcgraph (unmodified), numpy, 1 thread"
+    except ImportError:
+        from paper_2006_06890_b200 import csr as _csr  # pure Python/numpy mirror, no .so
+        kind, cores = "port", threads
+        g = _csr.CsrGraph(1 << scale, int(off[-1]), off, edges)
+        sources = _csr.pick_sources(g, 64, seed=7)
+
+        def one(s):
+            return oracle.bfs(g, int(s), threads=threads)
+        where = f"oracle port (zc_oracle.c, OpenMP, {threads} threads): reference unavailable"
+    per, edges_done = [], 0
+    for i in range(warmup + steps):
+        t1 = time.perf_counter()
+        r = one(sources[i % 64])
+        dt = time.perf_counter() - t1
+        if i >= warmup:
+            per.append(dt)
+            edges_done += sum(int(x) for x in r.traversed_edges)
+    total = sum(per)
+    return {"value": edges_done / total / 1e9, "unit": "GTEPS", "cores": cores, "kind": kind,
+            "sample": f"{steps} full bfs() runs (after {warmup} warm-up) on Kronecker scale "
+                      f"{scale} (R-MAT .57/.19/.19, edge factor 16, {int(off[-1])} arcs, same "
+                      f"generator and source rule as the bench graph); {where}",
+            "seconds": total, "gen_s": gen_s, "ms_per_step": total / max(steps, 1) * 1e3}
 
 
+def main_reference(args):
+    """--impl reference: the reference's own CPU implementation on the host
+    cores (rank 0 only; other ranks exit without work).  Runs the unmodified
+    reference bfs on a bounded sample of this arm's workload (reference_sample);
+    does not import the product package or load any CUDA library."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    threads = args.cpu_threads or os.cpu_count()
+    s = reference_sample(args.steps, args.warmup, args.seed, threads)
+    cfg = bfs_config(args, world)
+    cfg["reference_sample"] = s["sample"]
+    line = {"impl": "reference", "metric": METRIC, "value": s["value"], "unit": "GTEPS",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": s["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {k: s[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": s["value"], "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def bfs_config(args, world: int) -> dict:
+    return {"workload": f"BFS, Kronecker (R-MAT a=.57 b=.19 c=.19) scale {args.scale}, edge "
+                        f"factor {args.edge_factor}, {args.edge_factor << args.scale} directed "
+                        "arcs, u32 edges in pinned host memory (zero-copy)",
+            "graph": f"kron{args.scale}", "scale": args.scale, "edge_factor": args.edge_factor,
+            "seed": args.seed, "strategy": args.strategy, "placement": "zerocopy",
+            "sources": "pick_sources(g, 64, seed=7)",
+            "l2": "inputs larger than L2 (8 GiB edge list in host memory, 512 MiB level array)",
+            "parallelism": "single" if world == 1 else f"vertex-partition{world}"}
+
+
+# ----------------------------------------------------------------- helpers
+class OracleCache:
+    """CPU oracle results per (graph tag, algo, source) -- computed once,
+    compared with every strategy / placement that reports a number."""
+
+    def __init__(self, threads: int):
+        self.threads = threads
+        self.memo = {}
+        self.seconds = {}
+
+    def get(self, tag, g, algo, src=0):
+        import oracle
+        key = (tag, algo, src)
+        if key not in self.memo:
+            t0 = time.perf_counter()
+            self.memo[key] = oracle.run(algo, g, src, threads=self.threads)
+            self.seconds[key] = time.perf_counter() - t0
+        return self.memo[key]
+
+
+def same(r, ref) -> bool:
+    import numpy as np
+    return bool(np.array_equal(r.values, ref.values) and r.iterations == ref.iterations
+                and list(r.traversed_edges) == list(ref.traversed_edges))
+
+
+def same_values(r, ref) -> bool:
+    import numpy as np
+    return bool(np.array_equal(r.values, ref.values))
+
+
+def bfs_point(zc, dg, src, strategy, evict=False, reps=2) -> tuple[dict, object]:
+    """GTEPS of one source: `reps` runs (the first warms), the last reported."""
+    r = None
+    for _ in range(reps):
+        if evict:
+            zc.evict(dg)
+        r = zc.bfs(dg, int(src), strategy, collect_traffic=False)
+    return {"gteps": r.total_traversed_edges / (r.kernel_ms * 1e-3) / 1e9,
+            "kernel_ms": r.kernel_ms, "expand_ms": r.expand_ms,
+            "u32_edge_gbs": r.total_traversed_edges * 4 / (r.expand_ms * 1e-3) / 1e9}, r
+
+
+def level_table(dg, r, elem_bytes=4) -> list:
+    prof = dg.expand_profile(r.iterations)
+    return [{"level": k, "frontier": int(r.frontier_sizes[k]), "edges": int(r.traversed_edges[k]),
+             "expand_ms": round(float(prof[k]), 3),
+             "gbs": round(r.traversed_edges[k] * elem_bytes / max(prof[k], 1e-9) / 1e6, 2)}
+            for k in range(r.iterations)]
+
+
+# ---------------------------------------------------------------- N = 1
 def main():
     args = parse()
     if args.impl == "reference":
-        # the CPU reference arm runs on rank 0 only, without a process group
-        if int(os.environ.get("RANK", "0")) != 0:
-            return
-        rank, world = 0, int(os.environ.get("WORLD_SIZE", "1"))
-        local = max(args.device_override, 0)
-    else:
-        rank, world, local = dist_setup(args)
+        return main_reference(args)
+    rank, world, local = dist_setup(args)
+    if world > 1 or args.force_partitioned:
+        return main_partitioned(args, rank, world, local)
     import numpy as np
+    import torch
 
     import paper_2006_06890_b200 as zc
-    import torch
 
     device = local
     torch.cuda.set_device(device)
-    config = {"workload": f"BFS, Kronecker (R-MAT a=.57 b=.19 c=.19) scale {args.scale}, "
-                          f"edge factor {args.edge_factor}, "
-                          f"{args.edge_factor << args.scale} directed arcs, u32 edges in "
-                          "pinned host memory (zero-copy)",
-              "graph": f"kron{args.scale}", "scale": args.scale, "edge_factor": args.edge_factor,
-              "seed": args.seed + rank, "strategy": args.strategy, "placement": "zerocopy",
-              "list_store": ("compressed line streams in pinned host memory (B200 host-store "
-                             "extension): every list sorted and delta-encoded in 128 B lines, "
-                             "hub lists on whole lines, short lists sharing lines; the raw u32 "
-                             "lists stay beside them"
-                             + ("; out-lists and the in-lists (transpose, built on the GPU)"
-                                if args.strategy == "direction-optimizing" else "")
-                             if args.strategy in COMPRESSED_STRATEGIES else "raw u32 lists"),
-              "direction": ("top-down steps, bottom-up steps (unvisited vertices scan their "
-                            "in-lists for a parent in the frontier) once the frontier's "
-                            "out-edges exceed twice the unvisited vertices' in-edges; levels, "
-                            "iterations and traversed_edges are the reference's"
-                            if args.strategy == "direction-optimizing" else "top-down"),
-              "sources": "pick_sources(g, 64, seed=7)",
-              "l2": "inputs larger than L2 (8 GiB edge list in host memory, 512 MiB level "
-                    "array)",
-              "parallelism": f"replicas{world}" if world > 1 else "single"}
-
-    if args.impl == "reference":
-        return main_reference(args, world, device, config)
-    if world > 1 or args.force_partitioned:
-        return main_partitioned(args, rank, world, device, config)
+    threads = args.cpu_threads or os.cpu_count()
+    config = bfs_config(args, world)
+    strat = args.strategy
 
     t0 = time.time()
-    dg = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed + rank, device=device)
+    dg = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, device=device)
     gen_s = time.time() - t0
+    dg.set_tuning(args.tuning)
     g = dg.as_csr()
     sources = zc.pick_sources(g, 64, seed=7)
-
-    strat = args.strategy
     probe = zc.link_probe(device=device, nbytes=1 << 30, iters=5)
-    cmp_info = None
-    if strat in COMPRESSED_STRATEGIES:  # host-store build, like pinning: outside the timed region
-        t0 = time.time()
-        nbytes = dg.build_compressed()
-        cmp_info = {"build_s": time.time() - t0, "line_stream_bytes": nbytes}
-        if strat == "direction-optimizing":
-            t0 = time.time()
-            cmp_info["in_line_stream_bytes"] = dg.build_in_lists()
-            cmp_info["in_build_s"] = time.time() - t0
-    link = LinkBytes(dg, strat)
 
-    # warm-up (untimed)
-    for i in range(args.warmup):
+    for i in range(args.warmup):  # untimed
         zc.bfs(dg, int(sources[i % 64]), strat, collect_traffic=False)
 
-    # timed region 1: device time of the traversal loop (value)
+    # ---- timed region 1: device time of the level loop (value)
     barrier(world, device)
     kernel_ms = expand_ms = 0.0
-    trav = launches = link_bytes = 0
-    bottom_up = []
+    trav = launches = 0
+    step_srcs = [int(sources[(args.warmup + i) % 64]) for i in range(args.steps)]
+    last = None
     with ClockSampler(device) as clk:
-        for i in range(args.steps):
-            r = zc.bfs(dg, int(sources[(args.warmup + i) % 64]), strat, collect_traffic=False)
+        for s in step_srcs:
+            r = zc.bfs(dg, s, strat, collect_traffic=False)
             kernel_ms += r.kernel_ms
             expand_ms += r.expand_ms
             trav += r.total_traversed_edges
             launches += r.launches
-            link_bytes += link(r)
-            if strat == "direction-optimizing":
-                bottom_up.append([int(x) for x in np.flatnonzero(dg.directions(r.iterations))])
+            last = r
     barrier(world, device)
-    kernel_ms_max = max_over_ranks(kernel_ms, world, device)
-    trav_all = sum_over_ranks(trav, world, device)
-    value = trav_all / (kernel_ms_max * 1e-3) / 1e9
+    value = trav / (kernel_ms * 1e-3) / 1e9
+    levels = level_table(dg, last)
 
-    # timed region 2: end to end through the public API (host wall clock).
-    # bfs_many = the reference's per-source loop (report.py:168-170) as one
-    # call: each source's int64 levels download to pinned host memory while
-    # the next source streams the edge list.  Batches of <= 10 sources keep
-    # the result buffers inside the pinned pool (warmed here, untimed).
-    step_srcs = [int(sources[(args.warmup + i) % 64]) for i in range(args.steps)]
+    # ---- timed region 2: end to end through the public API (host wall clock)
     batch = min(10, args.steps)
-    r = None
-    zc.bfs_many(dg, step_srcs[:batch], strat)
+    zc.bfs_many(dg, step_srcs[:batch], strat)  # warms the pinned result pool
     barrier(world, device)
     t1 = time.perf_counter()
     e2e_trav = h2d = d2h = 0
     for b0 in range(0, args.steps, batch):
-        rs = zc.bfs_many(dg, step_srcs[b0:b0 + batch], strat)
-        for r in rs:
+        for r in zc.bfs_many(dg, step_srcs[b0:b0 + batch], strat):
             e2e_trav += r.total_traversed_edges
             h2d += r.h2d_bytes
             d2h += r.d2h_bytes
-        rs = r = None
     barrier(world, device)
-    wall = max_over_ranks(time.perf_counter() - t1, world, device)
-    e2e_value = sum_over_ranks(e2e_trav, world, device) / wall / 1e9
-
-    # the same, one blocking bfs() call per source (no download overlap)
-    barrier(world, device)
+    wall = time.perf_counter() - t1
+    e2e_value = e2e_trav / wall / 1e9
     t2 = time.perf_counter()
-    for src in step_srcs:
-        r = zc.bfs(dg, src, strat, collect_traffic=False)
-        r = None
-    barrier(world, device)
-    wall_1 = max_over_ranks(time.perf_counter() - t2, world, device)
-    e2e_per_call = sum_over_ranks(e2e_trav, world, device) / wall_1 / 1e9
+    for s in step_srcs:
+        zc.bfs(dg, s, strat, collect_traffic=False)
+    wall_1 = time.perf_counter() - t2
 
-    # GB/s of list data the expansion kernels must read over the link
-    achieved = link_bytes / (expand_ms * 1e-3) / 1e9
+    # ---- roofline (SURVEY 8(d)): 4 B per traversed edge over the sweep's time
+    alg_bytes = trav * 4
+    achieved = alg_bytes / (expand_ms * 1e-3) / 1e9
     summ = load_ncu_summary()
-    ncu = summ.get("bfs_expand_dobfs" if strat == "direction-optimizing" else "bfs_expand", {})
+    ncu = summ.get("bfs_expand_merged_aligned", {}) if strat == "merged-aligned" else {}
     line = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": kernel_ms_max / args.steps, "higher_is_better": True,
+        "ms_per_step": kernel_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": config,
         "e2e": {"value": e2e_value, "unit": "GTEPS",
                 "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
                 "ms_per_step": wall / args.steps * 1e3,
                 "api": f"bfs_many (pipelined result downloads, batches of {batch})",
-                "per_call_value": e2e_per_call,
+                "per_call_value": e2e_trav / wall_1 / 1e9,
                 "per_call_api": "one blocking bfs() per source"},
         "gpu_launches": launches,
-        "roofline": {"bound": "host-link", "achieved": achieved,
-                     "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
-                     "frac": achieved / PCIE_GEN5_X16_GBS,
-                     "traffic": ncu.get("dram_bytes_per_launch"),
-                     "kernel": "k_expand_sweep (zero-copy edge stream)",
-                     "algorithmic_bytes": link.describe,
-                     "algorithmic_bytes_per_step": link_bytes / args.steps,
-                     "u32_equivalent_gbs": trav * 4 / (expand_ms * 1e-3) / 1e9,
-                     "peak_kind": "PCIe Gen5 x16 theoretical per direction",
-                     "measured_peaks_gbs": probe,
-                     "frac_of_measured_memcpy": achieved / probe["memcpy_h2d_gbs"],
-                     # SM-side sysmem reads (ld or TMA cp.async.bulk) cap at the
-                     # zero-copy streaming peak (profiles/r01_tma_bulk_probe.txt)
-                     "frac_of_measured_zerocopy_ceiling": achieved / probe["zerocopy_read_gbs"],
-                     "sysmem_bytes_per_launch": ncu.get("sysmem_bytes_per_launch")},
+        "roofline": {
+            "bound": "host-link", "achieved": achieved, "peak": PCIE_GEN5_X16_GBS,
+            "unit": "GB/s", "frac": achieved / PCIE_GEN5_X16_GBS,
+            "traffic": ncu.get("sysmem_bytes_per_launch"),
+            "traffic_kind": "ncu syslts__d_sectors_fill_sysmem x 32 B of the main-level launch "
+                            "(host-link read bytes)",
+            "traffic_algorithmic_bytes": ncu.get("algorithmic_bytes_per_launch"),
+            "traffic_pcie_read_bytes": ncu.get("pcie_read_bytes_per_launch"),
+            "traffic_hbm_dram_bytes": ncu.get("dram_bytes_per_launch"),
+            "kernel": "k_expand_sweep<merged-aligned> (+ its window-count / scan launches)",
+            "algorithmic_bytes": "traversed edges x 4 B (SURVEY 8(d))",
+            "algorithmic_bytes_per_step": alg_bytes / args.steps,
+            "kernel_ms_per_step": expand_ms / args.steps,
+            "kernel_share_of_step": expand_ms / kernel_ms,
+            "peak_kind": "PCIe Gen5 x16 theoretical per direction",
+            "measured_peaks_gbs": probe,
+            "frac_of_measured_memcpy": achieved / probe["memcpy_h2d_gbs"],
+            "frac_of_measured_zerocopy_ceiling": achieved / probe["zerocopy_read_gbs"]},
         "clocks": clk.summary(),
         "graph": {"vertices": dg.num_vertices, "arcs": dg.num_edges, "gen_s": gen_s,
-                  "traversed_edges_per_step": trav / args.steps},
+                  "traversed_edges_per_step": trav / args.steps,
+                  "pinned_list_bytes": dg.num_edges * 4},
+        "merged_aligned": {"gteps": value, "e2e_gteps": e2e_value,
+                           "link_gbs": achieved, "frac_of_pcie_gen5": achieved / PCIE_GEN5_X16_GBS,
+                           "levels_last_step": levels},
     }
-    if cmp_info:
-        line["graph"]["compressed"] = cmp_info
-    if bottom_up:
-        line["bottom_up_iterations_per_step"] = bottom_up
 
-    if rank == 0 and not args.no_cpu_baseline:
-        threads = args.cpu_threads or os.cpu_count()
-        def check(src, ref):
-            r = zc.bfs(dg, src, strat, collect_traffic=False)
-            return (np.array_equal(r.values, ref.values) and r.iterations == ref.iterations
-                    and r.traversed_edges == ref.traversed_edges)
-        line["cpu_baseline"] = cpu_baseline(g, sources, threads, check=check)
+    oc = OracleCache(threads)
+    parity = {}
+    if not args.no_cpu_baseline:
+        # bit-exact at full size: three of the timed sources against the oracle port
+        checks, port_s, port_edges = [], 0.0, 0
+        for s in step_srcs[:3]:
+            ref = oc.get("kron", g, "bfs", s)
+            port_s += oc.seconds[("kron", "bfs", s)]
+            port_edges += sum(ref.traversed_edges)
+            checks.append(same(zc.bfs(dg, s, strat, collect_traffic=False), ref))
+        parity[f"zerocopy/{strat}"] = all(checks)
+        line["cpu_port"] = {"value": port_edges / port_s / 1e9, "unit": "GTEPS",
+                            "cores": threads, "kind": "port",
+                            "sample": f"3 full BFS runs of the oracle port (zc_oracle.c, OpenMP) on "
+                                      f"the bench graph itself, {threads} threads"}
+        line["cpu_baseline"] = reference_sample(3, 0, args.seed, threads)
 
-    # configs before the UVM variants: managed-memory runs leave the process
-    # slower on later zero-copy work (measured), so UVM goes last
-    if rank == 0 and not args.no_variants and world == 1:
-        line["variants"] = variants(zc, args, dg, sources, device, phase="zerocopy")
+    if not args.no_variants:
+        line["variants"] = variants_zerocopy(zc, dg, g, sources, oc, parity, args)
     dg.close()
-    if rank == 0 and not args.no_configs and world == 1:
-        line["configs"] = other_configs(zc, args, device)
-    if rank == 0 and not args.no_variants and world == 1:
-        line["variants"].update(variants(zc, args, None, sources, device, phase="placements"))
-        finish_variants(line["variants"])
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    if not args.no_configs:
+        line["configs"] = other_configs(zc, args, device, oc, parity)
+    if not args.no_variants:
+        line["variants"].update(variants_placements(zc, args, g, sources, device, oc, parity))
+        v = line["variants"]
+        uvm = v["uvm/merged-aligned"]["gteps"]
+        line["merged_aligned"]["speedup_vs_uvm"] = value / uvm
+        line["merged_aligned"]["speedup_vs_uvm_cap25"] = value / v["uvm_cap25/merged-aligned"]["gteps"]
+        line["merged_aligned"]["uvm_gteps"] = uvm
+    if not args.no_c1:
+        line["c1"] = config1(zc, threads, parity)
+    line["parity"] = parity
+    line["parity_all_true"] = all(parity.values()) if parity else None
+    print(json.dumps(line), flush=True)
 
 
-def main_reference(args, world, device, config):
-    """--impl reference: the reference's algorithm on the host cores -- the
-    oracle port (oracle/zc_oracle.c, OpenMP restatement of traversal.py:98-120;
-    the reference itself is a Python package absent from the GPU box) -- on
-    this arm's workload (same graph: scale 27 + log2(N), same sources).  Rank 0
-    only; the input graph is built by the GPU generator (not timed)."""
+def variants_zerocopy(zc, dg, g, sources, oc, parity, args) -> dict:
+    """configs[1]'s comparison on the same zero-copy graph and source:
+    naive / merged / merged-aligned / packed, and the B200 host-store options
+    (compressed, direction-optimizing) with their build cost and an e2e that
+    pays it, amortised over the 64 pick_sources."""
+    out = {}
+    s0 = int(sources[0])
+    ref = oc.get("kron", g, "bfs", s0)
+    for s in ("naive", "merged", "merged-aligned", "packed"):
+        pt, r = bfs_point(zc, dg, s0, s, reps=1 if s == "naive" else 2)
+        out[f"zerocopy/{s}"] = pt
+        parity[f"zerocopy/{s}"] = parity.get(f"zerocopy/{s}", True) and same(r, ref)
+    for s in ("compressed", "direction-optimizing"):
+        t0 = time.perf_counter()
+        nbytes = dg.build_compressed()
+        build = {"out_lists_s": time.perf_counter() - t0, "out_line_stream_bytes": nbytes}
+        if s == "direction-optimizing":
+            t0 = time.perf_counter()
+            build["in_line_stream_bytes"] = dg.build_in_lists()
+            build["in_lists_s"] = time.perf_counter() - t0
+        pt, r = bfs_point(zc, dg, s0, s)
+        pt["requested_link_gbs"] = dg.link_bytes_requested() / (r.expand_ms * 1e-3) / 1e9
+        parity[f"zerocopy/{s}"] = same(r, ref)
+        # a fresh caller's cost: the build (measured above; the store is built
+        # once per handle) + bfs_many over all 64 sources, results downloaded
+        t0 = time.perf_counter()
+        rs = zc.bfs_many(dg, [int(x) for x in sources], s)
+        wall64 = time.perf_counter() - t0
+        trav64 = sum(x.total_traversed_edges for x in rs)
+        rs = None
+        build_s = build["out_lists_s"] + build.get("in_lists_s", 0.0)
+        pt.update(build)
+        pt["e2e_64_sources_gteps"] = trav64 / wall64 / 1e9
+        pt["e2e_64_sources_incl_build_gteps"] = trav64 / (wall64 + build_s) / 1e9
+        pt["pinned_host_bytes"] = (g.num_edges * 4 + build["out_line_stream_bytes"]
+                                   + build.get("in_line_stream_bytes", 0))
+        pt["algorithmic_u32_gbs_note"] = ("u32_edge_gbs counts 4 B per traversed edge; the "
+                                          "strategy reads fewer bytes (requested_link_gbs)")
+        out[f"zerocopy/{s}"] = pt
+    return out
+
+
+def variants_placements(zc, args, g, sources, device, oc, parity) -> dict:
+    """In-HBM control, cold UVM (and at the reference's 25% capacity), and
+    host-resident managed lists read in place -- each checked against the
+    oracle.  UVM runs last: managed-memory runs leave the process slower on
+    later zero-copy work (measured)."""
+    import torch
+    out = {}
+    s0 = int(sources[0])
+    ref = oc.get("kron", g, "bfs", s0)
+    for placement, strategies in (("zerocopy-managed", ("merged-aligned", "direction-optimizing")),
+                                  ("hbm", ("merged-aligned",)), ("uvm", ("merged-aligned",))):
+        h = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, device=device,
+                             placement=placement)
+        for s in strategies:
+            pt, r = bfs_point(zc, h, s0, s, evict=placement == "uvm")
+            out[f"{placement}/{s}"] = pt
+            parity[f"{placement}/{s}"] = same(r, ref)
+        if placement == "uvm":
+            # the reference's UVM capacity default: 25% of the dataset
+            # (report.py:151-153) -- ballast HBM so only that much stays free
+            dataset = h.num_edges * h.edge_elem_bytes
+            free, _ = torch.cuda.mem_get_info(device)
+            ballast = torch.empty(max(0, free - dataset // 4 - (256 << 20)), dtype=torch.uint8,
+                                  device=f"cuda:{device}")
+            pt, r = bfs_point(zc, h, s0, "merged-aligned", evict=True)
+            pt["free_hbm_bytes"] = torch.cuda.mem_get_info(device)[0]
+            out["uvm_cap25/merged-aligned"] = pt
+            parity["uvm_cap25/merged-aligned"] = same(r, ref)
+            del ballast
+            torch.cuda.empty_cache()
+        h.close()
+    hbm = out["hbm/merged-aligned"]
+    hbm["roofline_hbm_gbs"] = None  # HBM control: gather-bound (visited-bitmap probes), see DESIGN
+    return out
+
+
+def sssp_cc_point(zc, dg, algo, src, strategy, deg, schedule=None) -> tuple[dict, object]:
+    kw = {} if schedule is None else {"schedule": schedule}
+    fn = (lambda: zc.cc(dg, strategy, collect_traffic=False, **kw)) if algo == "cc" else \
+         (lambda: zc.sssp(dg, src, strategy, collect_traffic=False, **kw))
+    fn()
+    r = fn()
+    import numpy as np
+    unreached = np.iinfo(np.int64).max if algo == "sssp" else None
+    reached_deg = int(deg.sum()) if unreached is None else int(deg[r.values != unreached].sum())
+    eb = 8 if algo == "sssp" else 4
+    t = r.kernel_ms * 1e-3
+    return {"primary_gteps": reached_deg / t / 1e9,
+            "work_gteps": r.total_traversed_edges / t / 1e9,
+            "kernel_ms": r.kernel_ms, "iterations": r.iterations,
+            "work_edges": r.total_traversed_edges, "reached_degree_sum": reached_deg,
+            "work_passes_over_E": r.total_traversed_edges / max(dg.num_edges, 1),
+            "link_gbs_8d": r.total_traversed_edges * eb / (r.expand_ms * 1e-3) / 1e9,
+            "frac_of_pcie_gen5": r.total_traversed_edges * eb / (r.expand_ms * 1e-3) / 1e9
+            / PCIE_GEN5_X16_GBS}, r
+
+
+def other_configs(zc, args, device, oc, parity) -> dict:
+    """BASELINE configs[2] (SSSP, u32 weights, uniform scale 27, edges +
+    weights zero-copy) and configs[3] (CC, Kronecker scale 27 symmetrized =
+    2^32 arcs).  Primary GTEPS = sum of the reached vertices' degrees / time
+    (schedule-independent); work GTEPS counts the edges the
+    schedule expanded.  Every strategy is checked against the oracle."""
+    import numpy as np
+    out = {}
+    u = zc.generate_uniform_device(1 << args.scale, 16, 16, seed=args.seed, weights=(8, 72),
+                                   device=device)
+    gu = u.as_csr()
+    src = int(zc.pick_sources(gu, 1, seed=7)[0])
+    deg = np.diff(np.asarray(gu.offsets))
+    ref = oc.get("u27", gu, "sssp", src)
+    tag = f"sssp_uniform{args.scale}"
+    runs = [("merged-aligned", None), ("packed", None), ("compressed", None)]
+    runs += [("merged-aligned", s) for s in schedules("sssp", zc)]
+    for s, sched in runs:
+        key = f"{tag}/{s}" + (f"/{sched}" if sched else "")
+        pt, r = sssp_cc_point(zc, u, "sssp", src, s, deg, sched)
+        out[key] = pt
+        parity[key] = same(r, ref) if sched is None else same_values(r, ref)
+    u.build_sssp_pairs()  # B200 layout option: one interleaved (dst, weight) stream
+    pt, r = sssp_cc_point(zc, u, "sssp", src, "merged-aligned", deg)
+    out[f"{tag}/merged-aligned+pairs"] = pt
+    parity[f"{tag}/merged-aligned+pairs"] = same(r, ref)
+    out[f"{tag}/cpu_port_work_gteps"] = (sum(ref.traversed_edges)
+                                         / oc.seconds[("u27", "sssp", src)] / 1e9)
+    u.close()
+    t0 = time.time()
+    k = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, symmetrize=True,
+                         device=device)
+    gen_s = time.time() - t0
+    gk = k.as_csr()
+    deg = np.diff(np.asarray(gk.offsets))
+    ref = oc.get("kron_sym", gk, "cc")
+    tag = f"cc_kron{args.scale}_sym"
+    runs = [("merged-aligned", None), ("packed", None), ("compressed", None)]
+    runs += [("merged-aligned", s) for s in schedules("cc", zc)]
+    for s, sched in runs:
+        key = f"{tag}/{s}" + (f"/{sched}" if sched else "")
+        pt, r = sssp_cc_point(zc, k, "cc", 0, s, deg, sched)
+        pt.update({"arcs": k.num_edges, "gen_s": gen_s})
+        out[key] = pt
+        parity[key] = same(r, ref) if sched is None else same_values(r, ref)
+    out[f"{tag}/cpu_port_work_gteps"] = (sum(ref.traversed_edges)
+                                         / oc.seconds[("kron_sym", "cc", 0)] / 1e9)
+    k.close()
+    return out
+
+
+def schedules(algo: str, zc) -> list:
+    """Work-efficient schedules the library offers beyond the reference's
+    Jacobi iteration (values bit-identical; iteration counts differ)."""
+    return list(getattr(zc, "SCHEDULES", {}).get(algo, ()))
+
+
+def config1(zc, threads, parity) -> dict:
+    """BASELINE configs[0]: BFS from vertex 0 on generate_uniform(2**20, 16, 16,
+    seed=3) -- the GPU path, the unmodified reference's bfs timed under
+    `taskset -c 0` in a subprocess on the same EMGI file, and the oracle port."""
     import numpy as np
     import oracle
-    import paper_2006_06890_b200 as zc
+    t0 = time.perf_counter()
+    g = zc.generate_uniform(2 ** 20, 16, 16, seed=3)
+    gen_s = time.perf_counter() - t0
+    best = None
+    for _ in range(6):
+        r = zc.bfs(g, 0, "merged-aligned", collect_traffic=False)
+        if best is None or r.kernel_ms < best.kernel_ms:
+            best = r
+    out = {"workload": "BFS from vertex 0, generate_uniform(2**20, 16, 16, seed=3) "
+                       "(reference generator restated byte-identically), u32 edges zero-copy",
+           "gpu_gteps": best.total_traversed_edges / (best.kernel_ms * 1e-3) / 1e9,
+           "gpu_kernel_ms": best.kernel_ms, "levels_crc": crc_hex(best.values),
+           "levels_crc_golden": C1_LEVELS_CRC, "gen_s": gen_s}
+    parity["c1/merged-aligned"] = out["levels_crc"] == C1_LEVELS_CRC
+    tmp = tempfile.mkdtemp(prefix="zc_c1_")
+    path = os.path.join(tmp, "c1.emgi")
+    zc.store_csr_binary(g, path)
+    script = (
+        "import sys, time, json, zlib\n"
+        f"sys.path.insert(0, {ROOT!r})\n"
+        "import numpy as np, oracle\n"
+        "ref = oracle.reference()\n"
+        f"g = ref.load_csr_binary({path!r})\n"
+        "ts = []\n"
+        "for _ in range(3):\n"
+        "    t = time.perf_counter(); r = ref.bfs(g, 0, collect_traffic=False)\n"
+        "    ts.append(time.perf_counter() - t)\n"
+        "print(json.dumps({'s': min(ts), 'runs_s': ts, 'edges': int(sum(r.traversed_edges)),\n"
+        "                  'crc': '%08x' % (zlib.crc32(np.asarray(r.values, np.int64).tobytes()) & 0xffffffff)}))\n")
+    cmd = [sys.executable, "-c", script]
+    if subprocess.run(["which", "taskset"], capture_output=True).returncode == 0:
+        cmd = ["taskset", "-c", "0"] + cmd
+    try:
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+        rr = json.loads(res.stdout.strip().splitlines()[-1])
+        out["reference"] = {"value": rr["edges"] / rr["s"] / 1e9, "unit": "GTEPS", "cores": 1,
+                            "kind": "reference", "seconds": rr["s"], "runs_s": rr["runs_s"],
+                            "levels_crc": rr["crc"], "pinned": cmd[0] == "taskset",
+                            "sample": "the unmodified reference's bfs(g, 0, collect_traffic="
+                                      "False) on the C1 EMGI file (load_csr_binary), best of 3, "
+                                      "`taskset -c 0`, 1 core of " + str(os.cpu_count())}
+        parity["c1/reference_crc"] = rr["crc"] == C1_LEVELS_CRC
+    except Exception as exc:  # report, keep the line
+        out["reference"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    finally:
+        try:
+            os.remove(path)
+            os.rmdir(tmp)
+        except OSError:
+            pass
+    t0 = time.perf_counter()
+    port = oracle.bfs(g, 0, threads=threads)
+    dt = time.perf_counter() - t0
+    out["cpu_port"] = {"value": sum(port.traversed_edges) / dt / 1e9, "unit": "GTEPS",
+                       "cores": threads, "kind": "port"}
+    parity["c1/port_crc"] = crc_hex(port.values) == C1_LEVELS_CRC
+    if "value" in out["reference"]:
+        out["gpu_over_reference"] = out["gpu_gteps"] / out["reference"]["value"]
+    return out
 
-    scale = args.scale + max(0, int(round(np.log2(world))))
-    threads = args.cpu_threads or os.cpu_count()
-    dg = zc.generate_rmat(scale, args.edge_factor, seed=args.seed, device=device)
-    g = dg.as_csr()
-    sources = zc.pick_sources(g, 64, seed=7)
-    per, edges = [], 0
-    for i in range(args.warmup + args.steps):
-        t1 = time.perf_counter()
-        r = oracle.bfs(g, int(sources[i % 64]), threads=threads)
-        dt = time.perf_counter() - t1
-        if i >= args.warmup:
-            per.append(dt)
-            edges += sum(r.traversed_edges)
-    total = sum(per)
-    val = edges / total / 1e9
-    cfg = dict(config)
-    cfg.update({"graph": f"kron{scale}", "scale": scale})
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GTEPS",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": cfg,
-            "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": threads, "kind": "port",
-                             "sample": f"{args.steps} full BFS runs (after {args.warmup} warm-up) "
-                                       "of the oracle port on the whole graph"},
-            "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-    dg.close()
 
-
-def main_partitioned(args, rank, world, device, config):
+# ------------------------------------------------------------------ N > 1
+def main_partitioned(args, rank, world, device):
+    config = bfs_config(args, world)
     """N>1: weak scaling -- Kronecker scale 27 + log2(N) (K29 at N=4, BASELINE
     configs[4]), vertex-range partitioned, each rank streaming its own 2^31-arc
     slice over its own host link; NCCL reduce-scatter of the u8 frontier flags
@@ -548,160 +812,6 @@ def main_partitioned(args, rank, world, device, config):
         print(json.dumps(line), flush=True)
     part.close()
 
-
-COMPRESSED_STRATEGIES = ("compressed", "direction-optimizing")
-
-
-class LinkBytes:
-    """Algorithmic link bytes of a BFS step: the list data the expansion
-    kernels must read -- 4 B per traversed edge of the raw u32 lists, or, for
-    the compressed strategies, the line-stream bytes the kernels requested
-    (counted on the device: whole lines of long lists, the spanned words of
-    shared lines; bottom-up steps read candidates' in-lists up to the first
-    parent)."""
-
-    def __init__(self, dg, strategy: str):
-        self.dg = dg
-        self.compressed = strategy in COMPRESSED_STRATEGIES
-        self.describe = ("line-stream bytes requested by the expansion kernels (device counter: "
-                         "128 B per long-list line, the spanned words of shared lines)"
-                         if self.compressed else
-                         f"traversed edges x {dg.edge_elem_bytes} B (raw u32 lists)")
-
-    def __call__(self, r) -> int:
-        if self.compressed:
-            return self.dg.link_bytes_requested()
-        return r.total_traversed_edges * self.dg.edge_elem_bytes
-
-
-def _gteps(zc, dg, sources, strategy, reps=1, evict=False):
-    best = None
-    for i in range(reps):
-        if evict:
-            zc.evict(dg)
-        r = zc.bfs(dg, int(sources[i % 64]), strategy, collect_traffic=False)
-        gbs = r.total_traversed_edges * 4 / (r.expand_ms * 1e-3) / 1e9
-        cur = {"gteps": r.total_traversed_edges / (r.kernel_ms * 1e-3) / 1e9,
-               "kernel_ms": r.kernel_ms,
-               ("u32_equivalent_gbs" if strategy in COMPRESSED_STRATEGIES else "expand_gbs"): gbs}
-        if strategy in COMPRESSED_STRATEGIES:
-            cur["requested_link_gbs"] = dg.link_bytes_requested() / (r.expand_ms * 1e-3) / 1e9
-        if best is None or cur["gteps"] > best["gteps"]:
-            best = cur
-    return best
-
-
-def other_configs(zc, args, device) -> dict:
-    """BASELINE configs[2] (SSSP, u32 weights, uniform scale 27, edges + weights
-    zero-copy) and configs[3] (CC, Kronecker scale 27 symmetrized = 2^32 arcs),
-    one source / run each after a warm-up, merged-aligned and packed."""
-    out = {}
-    import oracle
-    u = zc.generate_uniform_device(1 << args.scale, 16, 16, seed=args.seed, weights=(8, 72),
-                                   device=device)
-    src = int(zc.pick_sources(u.as_csr(), 1, seed=7)[0])
-    for s in ("merged-aligned", "packed"):
-        zc.sssp(u, src, s, collect_traffic=False)
-        r = zc.sssp(u, src, s, collect_traffic=False)
-        out[f"sssp_uniform{args.scale}/{s}"] = {
-            "work_gteps": r.total_traversed_edges / (r.kernel_ms * 1e-3) / 1e9,
-            "kernel_ms": r.kernel_ms, "iterations": r.iterations,
-            "link_gbs": r.total_traversed_edges * 8 / (r.expand_ms * 1e-3) / 1e9,
-            "work_edges": r.total_traversed_edges}
-    # B200 host-store option: compressed lines with the weights alongside
-    zc.sssp(u, src, "compressed", collect_traffic=False)
-    r = zc.sssp(u, src, "compressed", collect_traffic=False)
-    out[f"sssp_uniform{args.scale}/compressed"] = {
-        "work_gteps": r.total_traversed_edges / (r.kernel_ms * 1e-3) / 1e9,
-        "kernel_ms": r.kernel_ms, "iterations": r.iterations,
-        "u32_pair_equivalent_gbs": r.total_traversed_edges * 8 / (r.expand_ms * 1e-3) / 1e9,
-        "work_edges": r.total_traversed_edges}
-    u.build_sssp_pairs()  # B200 layout option: one interleaved (dst, weight) stream
-    for s in ("merged-aligned", "packed"):
-        zc.sssp(u, src, s, collect_traffic=False)
-        r = zc.sssp(u, src, s, collect_traffic=False)
-        out[f"sssp_uniform{args.scale}/{s}+pairs"] = {
-            "work_gteps": r.total_traversed_edges / (r.kernel_ms * 1e-3) / 1e9,
-            "kernel_ms": r.kernel_ms, "iterations": r.iterations,
-            "link_gbs": r.total_traversed_edges * 8 / (r.expand_ms * 1e-3) / 1e9,
-            "work_edges": r.total_traversed_edges}
-    t0 = time.perf_counter()
-    ref = oracle.sssp(u.as_csr(), src, threads=os.cpu_count())
-    out[f"sssp_uniform{args.scale}/cpu_port_work_gteps"] = (
-        sum(ref.traversed_edges) / (time.perf_counter() - t0) / 1e9)
-    out[f"sssp_uniform{args.scale}/bit_exact_vs_oracle"] = bool(
-        (r.values == ref.values).all() and r.iterations == ref.iterations)
-    u.close()
-    t0 = time.time()
-    k = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, symmetrize=True,
-                         device=device)
-    gen_s = time.time() - t0
-    for s in ("merged-aligned", "packed", "compressed"):
-        zc.cc(k, s, collect_traffic=False)
-        r = zc.cc(k, s, collect_traffic=False)
-        out[f"cc_kron{args.scale}_sym/{s}"] = {
-            "work_gteps": r.total_traversed_edges / (r.kernel_ms * 1e-3) / 1e9,
-            "kernel_ms": r.kernel_ms, "iterations": r.iterations,
-            ("u32_equivalent_gbs" if s == "compressed" else "link_gbs"):
-                r.total_traversed_edges * 4 / (r.expand_ms * 1e-3) / 1e9,
-            "work_edges": r.total_traversed_edges, "arcs": k.num_edges, "gen_s": gen_s}
-    t0 = time.perf_counter()
-    ref = oracle.cc(k.as_csr(), threads=os.cpu_count())
-    out[f"cc_kron{args.scale}_sym/cpu_port_work_gteps"] = (
-        sum(ref.traversed_edges) / (time.perf_counter() - t0) / 1e9)
-    out[f"cc_kron{args.scale}_sym/bit_exact_vs_oracle"] = bool(
-        (r.values == ref.values).all() and r.iterations == ref.iterations)
-    k.close()
-    return out
-
-
-def variants(zc, args, dg, sources, device, phase: str) -> dict:
-    """configs[1]'s comparison: naive vs merged vs merged+aligned vs packed
-    (zero-copy), then the in-HBM control and UVM (cold; and at the reference's
-    25% capacity)."""
-    out = {}
-    if phase == "zerocopy":
-        for s in ("naive", "merged", "merged-aligned", "packed", "compressed",
-                  "direction-optimizing"):
-            # naive walks each hub list with one thread (seconds per BFS): one rep
-            out[f"zerocopy/{s}"] = _gteps(zc, dg, sources, s, reps=1 if s == "naive" else 2)
-        return out
-    import torch
-    # host-resident managed lists read in place (zerocopy-managed): the same
-    # zero-copy loads through the UVM driver's large-page GPU mappings
-    h = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, device=device,
-                         placement="zerocopy-managed")
-    out["zerocopy-managed/direction-optimizing"] = _gteps(zc, h, sources, "direction-optimizing",
-                                                          reps=2)
-    h.close()
-    for placement in ("hbm", "uvm"):
-        h = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, device=device,
-                             placement=placement)
-        out[f"{placement}/merged-aligned"] = _gteps(zc, h, sources, "merged-aligned", reps=2,
-                                                    evict=placement == "uvm")
-        if placement == "uvm":
-            # the reference's UVM capacity default: 25% of the dataset
-            # (report.py:151-153) -- ballast HBM so only that much stays free
-            dataset = h.num_edges * h.edge_elem_bytes
-            free, _ = torch.cuda.mem_get_info(device)
-            ballast_bytes = max(0, free - dataset // 4 - (256 << 20))
-            ballast = torch.empty(ballast_bytes, dtype=torch.uint8, device=f"cuda:{device}")
-            r = _gteps(zc, h, sources, "merged-aligned", reps=2, evict=True)
-            r["free_hbm_bytes"] = torch.cuda.mem_get_info(device)[0]
-            out["uvm_cap25/merged-aligned"] = r
-            del ballast
-            torch.cuda.empty_cache()
-        h.close()
-    return out
-
-
-def finish_variants(v: dict) -> None:
-    ma = v["zerocopy/merged-aligned"]["gteps"]
-    v["speedup_vs_uvm"] = ma / v["uvm/merged-aligned"]["gteps"]
-    v["speedup_vs_uvm_cap25"] = ma / v["uvm_cap25/merged-aligned"]["gteps"]
-    for s in ("packed", "compressed", "direction-optimizing"):
-        v[f"{s}_speedup_vs_uvm_cap25"] = (v[f"zerocopy/{s}"]["gteps"]
-                                          / v["uvm_cap25/merged-aligned"]["gteps"])
 
 
 if __name__ == "__main__":

@@ -241,7 +241,9 @@ int zc_set_options(zc_graph *g, uint32_t options);
  * comma-separated "unroll=2|4|8", "ctas=N" (sweep CTAs per SM),
  * "sched=chunk|sweep", "loop=host|device" (host-driven level loop, e.g. under
  * a profiler, which cannot see kernels inside conditional graph nodes),
- * "do_alpha=X" (direction-optimizing switch factor).  NULL or "" resets the
+ * "do_alpha=X" (direction-optimizing switch factor), "ld=0..3" (load flavour of
+ * the raw-list BFS sweeps: L1::no_allocate, L1-cached, read-only path,
+ * L1::evict_first).  NULL or "" resets the
  * defaults; an unknown entry is ZC_EINVAL.  Read by the run path; nothing is
  * taken from the environment. */
 int zc_set_tuning(zc_graph *g, const char *spec);

@@ -81,6 +81,7 @@ void tune_params(ExpandArgs* a, const zc_graph* g) {
   a->unroll = g->tune.unroll;
   a->ctas_per_sm = g->tune.ctas;
   a->chunk_sched = g->tune.sched;
+  a->ld = g->tune.ld;
 }
 
 // ---------------------------------------------------------- pinned lists
@@ -609,7 +610,7 @@ int build_loop_graph(zc_graph* g, int algo, int strategy, int ebytes, const Expa
                      const CompactArgs& c) {
   LoopGraph& L = g->loop;
   if (L.exec && L.algo == algo && L.strategy == strategy && L.ebytes == ebytes &&
-      L.unroll == base.unroll && L.ctas == base.ctas_per_sm)
+      L.unroll == base.unroll && L.ctas == base.ctas_per_sm && L.ld == base.ld)
     return ZC_OK;
   if (L.exec) cudaGraphExecDestroy(L.exec);
   if (L.graph) cudaGraphDestroy(L.graph);
@@ -652,6 +653,7 @@ int build_loop_graph(zc_graph* g, int algo, int strategy, int ebytes, const Expa
   L.ebytes = ebytes;
   L.unroll = base.unroll;
   L.ctas = base.ctas_per_sm;
+  L.ld = base.ld;
   L.launches_per_iter = launches + 3;
   return ZC_OK;
 }
@@ -2108,6 +2110,7 @@ int zc_set_tuning(zc_graph* g, const char* spec) {
     else if (k == "sched" && (v == "chunk" || v == "sweep")) t.sched = v == "chunk";
     else if (k == "loop" && (v == "host" || v == "device")) t.host_loop = v == "host";
     else if (k == "do_alpha" && atof(v.c_str()) > 0) t.do_alpha = atof(v.c_str());
+    else if (k == "ld" && v.size() == 1 && v[0] >= '0' && v[0] <= '3') t.ld = v[0] - '0';
     else {
       set_error("unknown tuning entry '" + kv + "'");
       return ZC_EINVAL;

@@ -166,6 +166,7 @@ struct ExpandArgs {
   int unroll;
   int ctas_per_sm;
   int chunk_sched;  // 1: the per-warp chunk + big-list scheduler instead of the sweep
+  int ld;           // load flavour of the raw BFS sweeps (0 = L1::no_allocate)
   int pairs;        // SSSP: `edges` is the interleaved (dst, weight) u32-pair list
   // device-driven level loop: frontier size / completed iterations in device
   // memory (then `n` is only the maximum, used to size grids)

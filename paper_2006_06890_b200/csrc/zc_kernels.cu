@@ -54,6 +54,23 @@ __device__ __forceinline__ uint64_t ld_list(const uint64_t* p) {
   asm("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
+// Load flavours of the raw-list sweep (zc_set_tuning "ld=N", BFS u32 only):
+// 0 = L1::no_allocate (default), 1 = cached in L1 (.ca: a line that two
+// adjacent frontier lists share is requested once per SM while it stays in
+// L1), 2 = the read-only path (.nc), 3 = L1::evict_first.
+template <int LD>
+__device__ __forceinline__ uint32_t ld_list_f(const uint32_t* p) {
+  uint32_t v;
+  if constexpr (LD == 1) asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  else if constexpr (LD == 2) asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  else if constexpr (LD == 3) asm volatile("ld.global.L1::evict_first.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  else v = ld_list(p);
+  return v;
+}
+template <int LD, typename T>
+__device__ __forceinline__ T ld_list_f(const T* p) {
+  return ld_list(p);
+}
 
 // Interleaved (destination, weight) u32 pairs in one 8-byte element stream
 // (zc_graph_build_pairs): the weight rides in the high half, no second load.
@@ -575,7 +592,7 @@ __device__ __forceinline__ void visit_short(const ExpandArgs& a, uint32_t x, uin
   __syncwarp();
 }
 
-template <int STRAT, int ALGO, typename ET, typename WT, int U>
+template <int STRAT, int ALGO, typename ET, typename WT, int U, int LD = 0>
 __global__ void __launch_bounds__(kSweepThreads, SweepMinBlocks<STRAT, ALGO>::value)
     k_expand_sweep(ExpandArgs a) {
   if (a.n_dev) {  // device-driven level loop: size and level live in device memory
@@ -713,7 +730,7 @@ __global__ void __launch_bounds__(kSweepThreads, SweepMinBlocks<STRAT, ALGO>::va
             bt.ok[u] = idx >= s0 && idx < e0;
           }
           if (bt.ok[u]) {
-            bt.dst[u] = ld_list(E + idx);
+            bt.dst[u] = ld_list_f<LD>(E + idx);
             if constexpr (AlgoTraits<ALGO>::weighted && !IsPair<WT>::value)
               bt.wt[u] = ld_list(Wt + idx);
           }
@@ -1428,7 +1445,7 @@ int resident_ctas(K kernel, int threads, int num_sms) {
   return num_sms * (per_sm > 0 ? per_sm : 1);
 }
 
-template <int STRAT, int ALGO, typename ET, typename WT, int U>
+template <int STRAT, int ALGO, typename ET, typename WT, int U, int LD = 0>
 cudaError_t expand_sweep(const ExpandArgs& a, int num_sms, cudaStream_t st,
                          uint64_t* launches) {
   // window counts -> global exclusive prefix (wpre[n] = total windows)
@@ -1438,9 +1455,10 @@ cudaError_t expand_sweep(const ExpandArgs& a, int num_sms, cudaStream_t st,
       scan_u32_to_u64(a.wcnt, a.wpre, a.n, a.scan_tmp, a.scan_tmp_bytes, st, a.n_dev);
   if (e != cudaSuccess) return e;
   static int grid = 0;  // per instantiation: all CTAs resident at once
-  if (!grid) grid = resident_ctas(k_expand_sweep<STRAT, ALGO, ET, WT, U>, kSweepThreads, num_sms);
+  if (!grid)
+    grid = resident_ctas(k_expand_sweep<STRAT, ALGO, ET, WT, U, LD>, kSweepThreads, num_sms);
   const int g = a.ctas_per_sm > 0 ? num_sms * a.ctas_per_sm : grid;
-  k_expand_sweep<STRAT, ALGO, ET, WT, U><<<g, kSweepThreads, 0, st>>>(a);
+  k_expand_sweep<STRAT, ALGO, ET, WT, U, LD><<<g, kSweepThreads, 0, st>>>(a);
   *launches += 5;
   return cudaGetLastError();
 }
@@ -1468,11 +1486,20 @@ cudaError_t expand_t(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t
     *launches += 1;
     return cudaGetLastError();
   }
-  // tuning variants (ZC_TUNE=unroll=N) for the BFS / u32 merged-aligned path
+  // tuning variants (zc_set_tuning unroll=N, ld=N) for the BFS / u32 raw-list sweeps
   if constexpr (STRAT == kMergedAligned && AlgoTraits<ALGO>::base == kBfs &&
                 sizeof(ET) == 4 && sizeof(WT) == 4) {
     if (a.unroll == 2) return expand_u<STRAT, ALGO, ET, WT, 2>(a, num_sms, st, launches);
     if (a.unroll == 8) return expand_u<STRAT, ALGO, ET, WT, 8>(a, num_sms, st, launches);
+  }
+  if constexpr ((STRAT == kMergedAligned || STRAT == kMerged) && ALGO == kBfs &&
+                sizeof(ET) == 4 && sizeof(WT) == 4) {
+    if (!a.chunk_sched && a.ld == 1)
+      return expand_sweep<STRAT, ALGO, ET, WT, kUnroll, 1>(a, num_sms, st, launches);
+    if (!a.chunk_sched && a.ld == 2)
+      return expand_sweep<STRAT, ALGO, ET, WT, kUnroll, 2>(a, num_sms, st, launches);
+    if (!a.chunk_sched && a.ld == 3)
+      return expand_sweep<STRAT, ALGO, ET, WT, kUnroll, 3>(a, num_sms, st, launches);
   }
   return expand_u<STRAT, ALGO, ET, WT, kUnroll>(a, num_sms, st, launches);
 }

@@ -230,7 +230,10 @@ def test_packed_many_empty_and_shared_blocks():
         assert np.array_equal(r.values, ref.values), algo
         assert r.iterations == ref.iterations and r.traversed_edges == ref.traversed_edges
     with pytest.raises(ValueError, match="request model"):
-        zc.bfs(g, src, "packed")  # collect_traffic=True: model undefined for packed
+        zc.bfs(g, src, "packed", collect_traffic=True)  # model undefined for packed
+    # the default (collect_traffic=None) skips the model for the extensions
+    r = zc.bfs(g, src, "packed")
+    assert r.total_traffic.request_count == 0 and len(r.per_iteration_traffic) == r.iterations
 
 
 def test_link_probe_sane():
