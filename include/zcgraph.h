@@ -165,6 +165,22 @@ int zc_graph_info(const zc_graph *g, uint64_t *num_vertices, uint64_t *num_edges
 int zc_bfs(zc_graph *g, uint64_t source, int strategy, int64_t *out, zc_stats *stats);
 int zc_sssp(zc_graph *g, uint64_t source, int strategy, int64_t *out, zc_stats *stats);
 int zc_cc(zc_graph *g, int strategy, int64_t *out, zc_stats *stats);
+
+/* Work-efficient schedules (B200 extensions; the reference's SSSP and CC are
+ * Jacobi iterations, traversal.py:123-179).  The values are identical -- the
+ * distances and min-id labels are unique fixpoints -- while iteration counts
+ * and per-iteration traversed edges follow the schedule:
+ *   zc_sssp_nearfar: the frontier holds only the improved vertices with
+ *     dist < threshold (near set); the others wait marked (far pile); when
+ *     the near set runs dry the threshold moves to the smallest waiting
+ *     distance + delta (delta = 0: the default, 32).
+ *   zc_cc_afforest: union-find (Afforest's schedule): pass 1 unions every
+ *     vertex with the neighbours of its list's first window, pass 2 only the
+ *     vertices outside the largest component whose lists reach further;
+ *     iterations = passes.  Strategies naive .. compressed. */
+int zc_sssp_nearfar(zc_graph *g, uint64_t source, int strategy, uint64_t delta, int64_t *out,
+                    zc_stats *stats);
+int zc_cc_afforest(zc_graph *g, int strategy, int64_t *out, zc_stats *stats);
 /* Pipelined variants for a batch of sources on one handle: return as soon as
  * the traversal has finished (stats and zc_run_log are final), while the
  * int64 result is still being downloaded to `out` on a second stream -- so

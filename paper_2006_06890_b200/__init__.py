@@ -15,13 +15,13 @@ from .csr import (CsrGraph, DegreeCdf, degree_cdf, generate_powerlaw, generate_u
 from .device import (DeviceGraph, device_graph, evict, generate_rmat, generate_uniform_device,
                      link_probe, open_emgi, pinned_empty, release)
 from .traffic import TrafficStats
-from .traversal import (UNREACHED_DIST, UNREACHED_LEVEL, TraversalResult, bfs, bfs_many, cc,
-                        pagerank, sssp, sssp_many)
+from .traversal import (SCHEDULES, UNREACHED_DIST, UNREACHED_LEVEL, TraversalResult, bfs,
+                        bfs_many, cc, pagerank, sssp, sssp_many)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "AccessStrategy", "CsrGraph", "DegreeCdf", "DeviceGraph", "LINE_BYTES", "SECTOR_BYTES",
+    "AccessStrategy", "CsrGraph", "SCHEDULES", "DegreeCdf", "DeviceGraph", "LINE_BYTES", "SECTOR_BYTES",
     "TrafficStats", "TraversalResult", "UNREACHED_DIST", "UNREACHED_LEVEL", "WARP_LANES",
     "bfs", "bfs_many", "cc", "degree_cdf", "device_graph", "evict", "generate_powerlaw", "generate_rmat",
     "generate_uniform", "generate_uniform_device", "link_probe", "load_csr_binary", "load_edge_list_text", "open_emgi",

@@ -35,6 +35,7 @@ EXPORTED = (
     "zc_bfs_async", "zc_sssp_async", "zc_sync", "zc_graph_compressed_index",
     "zc_graph_build_in_lists", "zc_run_directions", "zc_run_link_bytes",
     "zc_part_build_in_lists", "zc_part_unvisited_in", "zc_part_frontier_bits", "zc_part_pull",
+    "zc_sssp_nearfar", "zc_cc_afforest",
 )
 # every symbol include/zcprobe.h declares (the measurement tool library)
 PROBE_EXPORTED = ("zc_link_probe", "zc_read_probe", "zc_bulk_probe", "zc_vmm_host_probe")
@@ -89,6 +90,8 @@ def _declare(lib: C.CDLL) -> None:
         "zc_bfs": (C.c_int, [P, u64, C.c_int, P, C.POINTER(Stats)]),
         "zc_sssp": (C.c_int, [P, u64, C.c_int, P, C.POINTER(Stats)]),
         "zc_cc": (C.c_int, [P, C.c_int, P, C.POINTER(Stats)]),
+        "zc_sssp_nearfar": (C.c_int, [P, u64, C.c_int, u64, P, C.POINTER(Stats)]),
+        "zc_cc_afforest": (C.c_int, [P, C.c_int, P, C.POINTER(Stats)]),
         "zc_bfs_async": (C.c_int, [P, u64, C.c_int, P, C.POINTER(Stats)]),
         "zc_sssp_async": (C.c_int, [P, u64, C.c_int, P, C.POINTER(Stats)]),
         "zc_sync": (C.c_int, [P]),

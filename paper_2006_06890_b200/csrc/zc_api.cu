@@ -678,7 +678,7 @@ int ensure_async(zc_graph* g) {
 }
 
 int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stats* stats,
-        bool async = false) {
+        bool async = false, uint64_t nf_delta = 0) {
   const double t0 = now_ms();
   if (!g) {
     set_error("null graph handle");
@@ -839,7 +839,11 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
 
   // ---- device-driven loop: the whole traversal is one graph launch
   const ExpandArgs probe = expand_args(g->nv, 0);
-  const bool device_loop = n > 0 && strategy != kNaive && !dobfs && !model &&
+  // near-far SSSP (nf_delta > 0, B200 extension): the frontier holds only
+  // the improved vertices below a moving threshold; the rest wait, marked
+  const bool nearfar = algo == kSssp && nf_delta > 0;
+  uint64_t thresh = nearfar ? nf_delta : 0;
+  const bool device_loop = n > 0 && strategy != kNaive && !dobfs && !model && !nearfar &&
                            !probe.chunk_sched && !(g->options & ZC_OPT_HOST_LOOP) &&
                            !g->tune.host_loop;
   // direction-optimizing: in-edges of the unvisited vertices (Beamer's m_u)
@@ -952,7 +956,9 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
       ZC_CUDA_TRY(launch_expand(td_strategy, algo, ebytes, g->wb, a, g->num_sms, st, &launches));
     }
     ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[ev + 1], st));
-    ZC_CUDA_TRY(launch_compact(algo, compact_args(), st, &launches));
+    CompactArgs ca = compact_args();
+    ca.thresh = thresh;
+    ZC_CUDA_TRY(launch_compact(algo, ca, st, &launches));
     const size_t nctr = model ? kCtrCount : dobfs ? kCtrLoaded + 1 : 2;
     ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, nctr * sizeof(uint64_t),
                                 cudaMemcpyDeviceToHost, st));
@@ -961,6 +967,21 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     ZC_CUDA_TRY(cudaStreamSynchronize(st));
     n = g->h_ctr[kCtrNext];
     trav = g->h_ctr[kCtrTrav];
+    while (nearfar && n == 0) {  // near set done: next non-empty bucket of the far pile
+      ZC_CUDA_TRY(launch_far_min(g->d_flags, g->d_state, g->nv, g->d_ctr, st, &launches));
+      ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr + kCtrFarMin, g->d_ctr + kCtrFarMin,
+                                  2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+      ZC_CUDA_TRY(cudaStreamSynchronize(st));
+      if (g->h_ctr[kCtrFar] == 0) break;
+      thresh = g->h_ctr[kCtrFarMin] + nf_delta;
+      ca.thresh = thresh;
+      ZC_CUDA_TRY(launch_compact(algo, ca, st, &launches));
+      ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, 2 * sizeof(uint64_t),
+                                  cudaMemcpyDeviceToHost, st));
+      ZC_CUDA_TRY(cudaStreamSynchronize(st));
+      n = g->h_ctr[kCtrNext];
+      trav = g->h_ctr[kCtrTrav];
+    }
     if (dobfs) {
       unvisited_in -= std::min(unvisited_in, g->h_ctr[kCtrTravIn]);
       g->log_pull.push_back(pull ? 1 : 0);
@@ -1060,6 +1081,200 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     stats->d2h_bytes = g->nv * (narrow ? 1 : sizeof(int64_t)) +
                        (device_loop ? (kCtrCount + 4 * kLogCap) : iters * (model ? kCtrCount : 2)) *
                            sizeof(uint64_t);
+    stats->launches = launches;
+    stats->expand_ms = expand_ms;
+    stats->total_ms = now_ms() - t0;
+  }
+  return ZC_OK;
+}
+
+// Default bucket width of the near-far SSSP schedule (weights in [8, 72] on
+// the bench graphs: about one mean weight; measured in DESIGN.md).
+constexpr uint64_t kNearFarDelta = 32;
+
+// Connected components by union-find, Afforest's schedule (Sutton et al.,
+// IPDPS'18) over the zero-copy lists (B200 extension; the reference's Jacobi
+// label propagation is traversal.py:154-179).  Labels equal the reference's:
+// parents point to smaller ids, so each root is its component's minimum id.
+//   pass 1: every vertex unions with the neighbours of its first window (one
+//           request per list: the merged-aligned line / the first compressed
+//           line, short compressed lists whole);
+//   flatten, sample 1024 roots -> the most frequent one (the giant component);
+//   pass 2: only vertices outside it whose lists reach past the first window
+//           union with all their neighbours -- for an undirected graph every
+//           edge with an endpoint outside the giant component is seen from
+//           that endpoint, so no edge is missed;
+//   flatten -> labels.
+// iterations = passes; traversed_edges[k] = the degree sum of pass k's lists.
+int run_afforest(zc_graph* g, int strategy, int64_t* out, zc_stats* stats) {
+  const double t0 = now_ms();
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (strategy < kNaive || strategy > kCompressed) {
+    set_error("afforest runs with naive / merged / merged-aligned / packed / compressed");
+    return ZC_EINVAL;
+  }
+  if (g->flags & ZC_F_DIRECTED) {  // traversal.py:163-165
+    set_error("connected components require an undirected graph "
+              "(load with directed=False or symmetrize first)");
+    return ZC_EINVAL;
+  }
+  if (g->nparts) {
+    set_error("afforest runs on whole graphs, not partitions");
+    return ZC_ESTATE;
+  }
+  if (!out && g->nv) {
+    set_error("null output buffer");
+    return ZC_EINVAL;
+  }
+  if (strategy == kCompressed && g->eb != 4) {
+    set_error("compressed lists need 4-byte edges");
+    return ZC_EINVAL;
+  }
+  DeviceGuard dg(g->device);
+  if (strategy == kCompressed && !g->d_cmp) {
+    const int rc = zc_graph_build_compressed(g, nullptr);
+    if (rc) return rc;
+  }
+  // pass 1 reads one window per list: packed's shared blocks are an
+  // optimisation of whole-list sweeps, so its first pass is merged-aligned
+  const int s1 = strategy == kPacked ? static_cast<int>(kMergedAligned) : strategy;
+  cudaStream_t st = g->stream;
+  uint64_t launches = 0;
+  g->log_trav.clear();
+  g->log_front.clear();
+  g->log_hist.clear();
+  g->log_expand_ms.clear();
+  g->log_pull.clear();
+  uint32_t* parent = static_cast<uint32_t*>(g->d_state);
+  ZC_CUDA_TRY(cudaEventRecord(g->ev[0], st));
+  ZC_CUDA_TRY(cudaMemsetAsync(g->d_flags, 0, g->vpad, st));
+  ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr, 0, kCtrCount * sizeof(uint64_t), st));
+  // parent[v] = v, frontier = every vertex (value = its id)
+  ZC_CUDA_TRY(launch_init(kCc, g->d_state, g->nv, 0, g->d_off, g->d_front[0], g->d_fval[0],
+                          g->d_fs[0], g->d_fd[0], st, &launches));
+  while (g->iter_ev.size() < 4) {
+    cudaEvent_t e;
+    ZC_CUDA_TRY(cudaEventCreate(&e));
+    g->iter_ev.push_back(e);
+  }
+  auto args = [&](uint64_t n, int pass) {
+    ExpandArgs a{};
+    a.front = g->d_front[0];
+    a.fs = g->d_fs[0];
+    a.fd = g->d_fd[0];
+    a.fval = g->d_fval[0];
+    a.n = n;
+    a.off = g->d_off;
+    a.edges = g->d_edges;
+    a.state = g->d_state;
+    a.flags = g->d_flags;
+    a.visited = g->d_visited;
+    a.ctr = g->d_ctr;
+    a.big_s = g->d_big_s;
+    a.big_e = g->d_big_e;
+    a.big_val = g->d_big_val;
+    a.big_prefix = g->d_big_prefix;
+    a.wcnt = g->d_wcnt;
+    a.wpre = g->d_wpre;
+    a.scan_tmp = g->d_scan_tmp;
+    a.scan_tmp_bytes = g->scan_tmp_bytes;
+    a.cmp = static_cast<const uint32_t*>(g->d_cmp);
+    a.cpos = g->d_cpos;
+    a.cmp_b0 = g->cmp_b0;
+    a.pull_pass = static_cast<uint32_t>(pass);
+    tune_params(&a, g);
+    return a;
+  };
+  uint64_t iters = 0;
+  if (g->nv) {
+    ++iters;
+    g->log_trav.push_back(g->ne);
+    g->log_front.push_back(g->nv);
+    ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[0], st));
+    ZC_CUDA_TRY(launch_expand(s1, kCcUf, g->eb, g->wb, args(g->nv, 1), g->num_sms, st, &launches));
+    ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[1], st));
+    ZC_CUDA_TRY(launch_uf_flatten(parent, g->nv, st, &launches));
+    // the most frequent root of 1024 sampled vertices
+    uint32_t* d_sample = reinterpret_cast<uint32_t*>(g->d_log);  // 4 kLogCap u64: unused here
+    constexpr uint32_t kSample = 1024;
+    ZC_CUDA_TRY(launch_uf_sample(parent, g->nv, d_sample, kSample, st, &launches));
+    std::vector<uint32_t> roots(kSample);
+    ZC_CUDA_TRY(cudaMemcpyAsync(roots.data(), d_sample, kSample * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, st));
+    ZC_CUDA_TRY(cudaStreamSynchronize(st));
+    std::sort(roots.begin(), roots.end());
+    uint32_t giant = roots[0];
+    size_t best = 0;
+    for (size_t i = 0; i < roots.size();) {
+      size_t j = i;
+      while (j < roots.size() && roots[j] == roots[i]) ++j;
+      if (j - i > best) {
+        best = j - i;
+        giant = roots[i];
+      }
+      i = j;
+    }
+    ZC_CUDA_TRY(launch_uf_marks(parent, g->d_off, g->d_cpos, g->nv, giant, s1, g->eb, g->d_flags,
+                                st, &launches));
+    CompactArgs c{};
+    c.flags = g->d_flags;
+    c.nv = g->nv;
+    c.ntiles = g->ntiles;
+    c.tiles = g->d_tiles;
+    c.front_out = g->d_front[0];
+    c.fs_out = g->d_fs[0];
+    c.fd_out = g->d_fd[0];
+    c.fval_out = g->d_fval[0];
+    c.off = g->d_off;
+    c.state = g->d_state;
+    c.ctr = g->d_ctr;
+    ZC_CUDA_TRY(launch_compact(kCc, c, st, &launches));
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                st));
+    ZC_CUDA_TRY(cudaStreamSynchronize(st));
+    const uint64_t n2 = g->h_ctr[kCtrNext], trav2 = g->h_ctr[kCtrTrav];
+    if (n2) {
+      ++iters;
+      g->log_trav.push_back(trav2);
+      g->log_front.push_back(n2);
+      ZC_CUDA_TRY(launch_fval_ids(g->d_front[0], g->d_fval[0], n2, st, &launches));
+      ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2], st));
+      ZC_CUDA_TRY(launch_expand(strategy, kCcUf, g->eb, g->wb, args(n2, 0), g->num_sms, st,
+                                &launches));
+      ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[3], st));
+      ZC_CUDA_TRY(launch_uf_flatten(parent, g->nv, st, &launches));
+    }
+  }
+  ZC_CUDA_TRY(cudaEventRecord(g->ev[1], st));
+  int64_t* d_out = reinterpret_cast<int64_t*>(g->d_fval[0]);
+  ZC_CUDA_TRY(launch_widen(kCc, g->d_state, g->nv, d_out, st, &launches));
+  if (g->nv)
+    ZC_CUDA_TRY(cudaMemcpyAsync(out, d_out, g->nv * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
+  ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  double expand_ms = 0;
+  for (uint64_t k = 0; k < iters; ++k) {
+    float e = 0;
+    cudaEventElapsedTime(&e, g->iter_ev[2 * k], g->iter_ev[2 * k + 1]);
+    g->log_expand_ms.push_back(e);
+    expand_ms += e;
+  }
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    stats->iterations = iters;
+    uint64_t tt = 0;
+    for (uint64_t x : g->log_trav) tt += x;
+    stats->total_traversed_edges = tt;
+    stats->max_frontier = g->nv;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]);
+    stats->kernel_ms = ms;
+    cudaEventElapsedTime(&ms, g->ev[1], g->ev[2]);
+    stats->d2h_ms = ms;
+    stats->d2h_bytes = g->nv * sizeof(int64_t) + 1024 * sizeof(uint32_t) + iters * 16;
     stats->launches = launches;
     stats->expand_ms = expand_ms;
     stats->total_ms = now_ms() - t0;
@@ -1808,6 +2023,13 @@ int zc_sync(zc_graph* g) {
 }
 int zc_cc(zc_graph* g, int strategy, int64_t* out, zc_stats* stats) {
   return run(g, kCc, 0, strategy, out, stats);
+}
+int zc_sssp_nearfar(zc_graph* g, uint64_t source, int strategy, uint64_t delta, int64_t* out,
+                    zc_stats* stats) {
+  return run(g, kSssp, source, strategy, out, stats, false, delta ? delta : kNearFarDelta);
+}
+int zc_cc_afforest(zc_graph* g, int strategy, int64_t* out, zc_stats* stats) {
+  return run_afforest(g, strategy, out, stats);
 }
 
 int zc_run_log(const zc_graph* g, uint64_t* trav, uint64_t* front, uint64_t cap) {

@@ -13,7 +13,7 @@
 
 // Instantiated device-driven level loop (zc_api.cu build_loop_graph).
 struct LoopGraph {
-  int algo = -1, strategy = -1, ebytes = 0, unroll = 0, ctas = 0, ld = 0;
+  int algo = -1, strategy = -1, ebytes = 0, unroll = 0, ctas = 0, ld = -1;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   uint64_t launches_per_iter = 0;
@@ -111,7 +111,7 @@ struct zc_graph {
     int sched = 0;    // 1: the round-1 chunk scheduler instead of the sweep
     int host_loop = 0;  // 1: host-driven level loop (profilers cannot see graph kernels)
     double do_alpha = 2.0;  // direction-optimizing switch factor
-    int ld = 0;       // load flavour of the raw BFS sweeps (zc_kernels.cu ld_list_f)
+    int ld = -1;      // load flavour override of the raw BFS sweeps (zc_kernels.cu DefaultLd)
   } tune;
   int multigraph = -1;  // cached duplicate-arc check (-1 unknown)
   LoopGraph loop;

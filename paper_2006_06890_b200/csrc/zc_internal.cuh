@@ -103,11 +103,17 @@ constexpr int kPartAlgo = 4;  // algo + kPartAlgo
 // unvisited candidates, their in-lists are scanned for a parent in the
 // current frontier (frontier bitmap), the slot's vertex is the value.
 constexpr int kBfsPull = 8;
+// Connected components by union-find (the "afforest" schedule, B200
+// extension): the slot's value is its vertex id, the visit unions the two
+// endpoints' trees (parents in the u32 state, always pointing to smaller ids,
+// so every root is its component's minimum id -- the reference's label).
+constexpr int kCcUf = 9;
 template <int A>
 struct AlgoTraits {
   static constexpr bool pull = A == kBfsPull;
-  static constexpr int base = pull ? kBfs : A % kPartAlgo;
-  static constexpr bool part = A >= kPartAlgo && !pull;
+  static constexpr bool uf = A == kCcUf;
+  static constexpr int base = pull ? kBfs : uf ? kCc : A % kPartAlgo;
+  static constexpr bool part = A >= kPartAlgo && !pull && !uf;
   static constexpr bool has_val = base != kBfs || pull;  // slot carries a value
   static constexpr bool weighted = base == kSssp;
 };
@@ -126,6 +132,8 @@ enum Ctr : int {
   kCtrCur = 16,      // device level loop: size of the current frontier
   kCtrIter = 17,     //   completed iterations
   kCtrLoaded = 18,   // compressed sweeps: bytes requested from the line streams
+  kCtrFarMin = 22,   // near-far SSSP: smallest distance in the far pile
+  kCtrFar = 23,      //   vertices in the far pile
   kCtrCount = 24
 };
 
@@ -166,7 +174,7 @@ struct ExpandArgs {
   int unroll;
   int ctas_per_sm;
   int chunk_sched;  // 1: the per-warp chunk + big-list scheduler instead of the sweep
-  int ld;           // load flavour of the raw BFS sweeps (0 = L1::no_allocate)
+  int ld;           // load flavour override of the raw BFS sweeps (-1: the strategy's default)
   int pairs;        // SSSP: `edges` is the interleaved (dst, weight) u32-pair list
   // device-driven level loop: frontier size / completed iterations in device
   // memory (then `n` is only the maximum, used to size grids)
@@ -202,6 +210,9 @@ struct CompactArgs {
   const void* state;
   uint64_t* ctr;
   const uint64_t* in_off;  // optional: also sum the in-degrees into ctr[kCtrTravIn]
+  // near-far SSSP: only marked vertices with dist < thresh join the frontier;
+  // the others stay marked (the far pile).  0 = every marked vertex.
+  uint64_t thresh;
 };
 
 // Launchers (zc_kernels.cu).  All launch on `st`; return cudaError_t.
@@ -240,6 +251,22 @@ cudaError_t launch_frontier_bits(const uint32_t* front, uint64_t n, uint64_t vba
 cudaError_t launch_part_pull_prepare(const void* level, uint64_t nv, uint32_t* visited,
                                      const uint32_t* hasin, uint8_t* cand, int num_sms,
                                      cudaStream_t st, uint64_t* launches);
+// Near-far SSSP: ctr[kCtrFarMin] = min dist over the marked vertices,
+// ctr[kCtrFar] = their count (both reset first).
+cudaError_t launch_far_min(const uint8_t* flags, const void* dist, uint64_t nv, uint64_t* ctr,
+                           cudaStream_t st, uint64_t* launches);
+// Union-find CC helpers: parent[v] = root (full compression); `sample`
+// roots of hashed vertices into out[sample]; marks of the vertices outside
+// component `giant` whose lists reach past the first window (pass 2);
+// fval[j] = front[j].
+cudaError_t launch_uf_flatten(uint32_t* parent, uint64_t nv, cudaStream_t st, uint64_t* launches);
+cudaError_t launch_uf_sample(const uint32_t* parent, uint64_t nv, uint32_t* out, uint32_t sample,
+                             cudaStream_t st, uint64_t* launches);
+cudaError_t launch_uf_marks(const uint32_t* parent, const uint64_t* off, const uint64_t* cpos,
+                            uint64_t nv, uint32_t giant, int strategy, int edge_bytes,
+                            uint8_t* flags, cudaStream_t st, uint64_t* launches);
+cudaError_t launch_fval_ids(const uint32_t* front, uint64_t* fval, uint64_t n, cudaStream_t st,
+                            uint64_t* launches);
 // BFS levels (all below 255) as u8, 0xff = unreached.
 cudaError_t launch_narrow_levels(const void* state, uint64_t nv, uint8_t* out, cudaStream_t st,
                                  uint64_t* launches);

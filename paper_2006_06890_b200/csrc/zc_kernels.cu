@@ -54,10 +54,18 @@ __device__ __forceinline__ uint64_t ld_list(const uint64_t* p) {
   asm("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
-// Load flavours of the raw-list sweep (zc_set_tuning "ld=N", BFS u32 only):
-// 0 = L1::no_allocate (default), 1 = cached in L1 (.ca: a line that two
-// adjacent frontier lists share is requested once per SM while it stays in
-// L1), 2 = the read-only path (.nc), 3 = L1::evict_first.
+// Load flavours of the raw-list sweep: 0 = L1::no_allocate, 1 = cached in L1
+// (.ca), 2 = the read-only path (.nc), 3 = L1::evict_first.  Merged and
+// merged-aligned read the reference's per-list windows, so two adjacent
+// frontier lists that share a 128-byte line each request it; cached in L1 the
+// second request is served on the SM while the line stays there (K27 BFS,
+// merged-aligned: 234 -> 212 ms; the tiny-list level 46.6 -> 32.0 ms).
+// Packed / compressed fetch each line once by construction: no_allocate.
+// zc_set_tuning "ld=N" overrides the flavour of the BFS u32 sweeps for A/B.
+template <int STRAT>
+struct DefaultLd {
+  static constexpr int value = STRAT == kMerged || STRAT == kMergedAligned ? 1 : 0;
+};
 template <int LD>
 __device__ __forceinline__ uint32_t ld_list_f(const uint32_t* p) {
   uint32_t v;
@@ -165,6 +173,46 @@ __device__ __forceinline__ unsigned long long pr_fx(double x) { return __double2
 __device__ __forceinline__ double pr_unfx(unsigned long long v) {
   return __ull2double_rn(v) * (1.0 / kPrFx);
 }
+
+// Union-find with min-hooking (lock-free: a root is hooked by one CAS; path
+// halving stores only move non-roots closer to their root).  Parents always
+// point to smaller ids, so a root is the minimum id of its tree.
+__device__ __forceinline__ uint32_t uf_find(uint32_t* p, uint32_t x) {
+  uint32_t par = __ldcg(p + x);
+  if (par == x) return x;
+  uint32_t prev = x, next;
+  while (par > (next = __ldcg(p + par))) {
+    __stcg(p + prev, next);
+    prev = par;
+    par = next;
+  }
+  return par;
+}
+
+__device__ __forceinline__ void uf_union(uint32_t* p, uint32_t u, uint32_t v) {
+  uint32_t ru = uf_find(p, u), rv = uf_find(p, v);
+  while (ru != rv) {
+    if (ru < rv) {
+      const uint32_t t = ru;
+      ru = rv;
+      rv = t;
+    }
+    const uint32_t old = atomicCAS(p + ru, ru, rv);  // hook the larger root
+    if (old == ru) return;
+    ru = uf_find(p, old);
+    rv = uf_find(p, rv);
+  }
+}
+
+template <>
+struct Visit<kCcUf> {
+  // edge v -> w of an undirected graph: v and w are connected
+  static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
+                                               uint64_t v) {
+    uf_union(static_cast<uint32_t*>(a.state), static_cast<uint32_t>(v),
+             static_cast<uint32_t>(w));
+  }
+};
 
 template <>
 struct Visit<kPr> {
@@ -506,6 +554,7 @@ __global__ void k_window_counts(ExpandArgs a) {
       continue;
     }
     uint64_t w = (s + d - window_base<STRAT, ET>(s) + kWarp - 1) / kWarp;
+    if (a.pull_pass == 1 && w > 1) w = 1;  // first window only (union-find sampling pass)
     if (STRAT == kPacked) {
       for (uint64_t i = j; i > group0; --i) {
         const uint32_t di = a.fd[i - 1];
@@ -592,7 +641,7 @@ __device__ __forceinline__ void visit_short(const ExpandArgs& a, uint32_t x, uin
   __syncwarp();
 }
 
-template <int STRAT, int ALGO, typename ET, typename WT, int U, int LD = 0>
+template <int STRAT, int ALGO, typename ET, typename WT, int U, int LD = DefaultLd<STRAT>::value>
 __global__ void __launch_bounds__(kSweepThreads, SweepMinBlocks<STRAT, ALGO>::value)
     k_expand_sweep(ExpandArgs a) {
   if (a.n_dev) {  // device-driven level loop: size and level live in device memory
@@ -732,7 +781,7 @@ __global__ void __launch_bounds__(kSweepThreads, SweepMinBlocks<STRAT, ALGO>::va
           if (bt.ok[u]) {
             bt.dst[u] = ld_list_f<LD>(E + idx);
             if constexpr (AlgoTraits<ALGO>::weighted && !IsPair<WT>::value)
-              bt.wt[u] = ld_list(Wt + idx);
+              bt.wt[u] = ld_list_f<LD>(Wt + idx);
           }
         }
       }
@@ -987,10 +1036,26 @@ __device__ __forceinline__ uint32_t block_reduce_u32(uint32_t x, uint32_t* sh) {
   return r;  // valid in thread 0
 }
 
+// Near-far SSSP: of 16 marked vertices from v0, keep the marks of those with
+// dist < thresh (the near set); the others stay in the far pile.
+__device__ __forceinline__ uint4 select_near(uint4 f, uint64_t v0, const CompactArgs& c) {
+  if (!c.thresh || !(f.x | f.y | f.z | f.w)) return f;
+  const uint64_t* dist = static_cast<const uint64_t*>(c.state);
+  uint32_t w[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    const uint32_t m = 0xffu << ((b & 3) * 8);
+    if ((w[b >> 2] & m) && dist[v0 + b] >= c.thresh) w[b >> 2] &= ~m;
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 __global__ void __launch_bounds__(kTileThreads) k_tile_count(CompactArgs c) {
   __shared__ uint32_t sh[kTileThreads / 32];
   for (uint64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
-    const uint4 f = reinterpret_cast<const uint4*>(c.flags)[t * kTileThreads + threadIdx.x];
+    const uint4 f = select_near(
+        reinterpret_cast<const uint4*>(c.flags)[t * kTileThreads + threadIdx.x],
+        t * kTileVerts + static_cast<uint64_t>(threadIdx.x) * 16, c);
     uint32_t cnt = __popc(f.x) + __popc(f.y) + __popc(f.z) + __popc(f.w);
     cnt = block_reduce_u32(cnt, sh);
     if (threadIdx.x == 0) c.tiles[t] = cnt;
@@ -1047,7 +1112,8 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (uint64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
     uint4* fp = reinterpret_cast<uint4*>(c.flags) + t * kTileThreads + threadIdx.x;
-    const uint4 f = *fp;
+    const uint4 f_all = *fp;
+    const uint4 f = select_near(f_all, t * kTileVerts + static_cast<uint64_t>(threadIdx.x) * 16, c);
     const uint32_t words[4] = {f.x, f.y, f.z, f.w};
     const uint32_t cnt = __popc(f.x) + __popc(f.y) + __popc(f.z) + __popc(f.w);
     uint32_t incl = cnt;
@@ -1079,7 +1145,8 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
           ++pos;
         }
       }
-      *fp = make_uint4(0, 0, 0, 0);
+      // selected marks are consumed; far-pile marks (near-far SSSP) stay
+      *fp = make_uint4(f_all.x ^ f.x, f_all.y ^ f.y, f_all.z ^ f.z, f_all.w ^ f.w);
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -1102,6 +1169,81 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
     }
     __syncthreads();
   }
+}
+
+// ------------------------------------------------- near-far / union-find
+__global__ void __launch_bounds__(256) k_far_min(const uint8_t* flags, const uint64_t* dist,
+                                                 uint64_t nv, uint64_t* ctr) {
+  unsigned long long mn = ~0ull, cnt = 0;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    if (flags[v]) {
+      ++cnt;
+      mn = min(mn, static_cast<unsigned long long>(dist[v]));
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    mn = min(mn, __shfl_down_sync(kFull, mn, d));
+    cnt += __shfl_down_sync(kFull, cnt, d);
+  }
+  if ((threadIdx.x & 31) == 0 && cnt) {
+    atomicMin(reinterpret_cast<unsigned long long*>(ctr + kCtrFarMin), mn);
+    atomicAdd(reinterpret_cast<unsigned long long*>(ctr + kCtrFar), cnt);
+  }
+}
+
+__global__ void k_far_reset(uint64_t* ctr) {
+  ctr[kCtrFarMin] = ~0ull;
+  ctr[kCtrFar] = 0;
+}
+
+__global__ void k_uf_flatten(uint32_t* parent, uint64_t nv) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = uf_find(parent, static_cast<uint32_t>(v));
+    if (parent[v] != r) parent[v] = r;
+  }
+}
+
+__global__ void k_uf_sample(const uint32_t* parent, uint64_t nv, uint32_t* out, uint32_t sample) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < sample; i += gridDim.x * blockDim.x) {
+    uint64_t z = (i + 1) * 0x9e3779b97f4a7c15ull;
+    z ^= z >> 31;
+    z *= 0xbf58476d1ce4e5b9ull;
+    z ^= z >> 29;
+    out[i] = parent[z % nv];  // flattened: the root
+  }
+}
+
+// Pass-2 marks: vertices outside the giant component whose list has
+// elements beyond the window(s) pass 1 read (the first window; for the
+// compressed stream the first line of a long list, short lists whole).
+__global__ void k_uf_marks(const uint32_t* parent, const uint64_t* off, const uint64_t* cpos,
+                           uint64_t nv, uint32_t giant, int strategy, int eb, uint8_t* flags) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = off[v], e = off[v + 1];
+    bool rest;
+    if (strategy == kCompressed) {
+      const uint64_t c = cpos[v];
+      rest = (c & kCmpLong) && cmp_lines(c) > 1;
+    } else if (strategy == kNaive) {
+      rest = false;  // the naive sweep reads whole lists in pass 1
+    } else {
+      const uint64_t line = kLineBytes / static_cast<uint64_t>(eb);
+      const uint64_t base = strategy == kMerged ? s : strategy == kPacked ? (s & ~31ull)
+                                                                         : (s & ~(line - 1));
+      rest = e > base + kWarp;
+    }
+    flags[v] = rest && parent[v] != giant ? 1 : 0;
+  }
+}
+
+__global__ void k_fval_ids(const uint32_t* front, uint64_t* fval, uint64_t n) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    fval[j] = front[j];
 }
 
 // ------------------------------------------------------- device level loop
@@ -1445,7 +1587,8 @@ int resident_ctas(K kernel, int threads, int num_sms) {
   return num_sms * (per_sm > 0 ? per_sm : 1);
 }
 
-template <int STRAT, int ALGO, typename ET, typename WT, int U, int LD = 0>
+template <int STRAT, int ALGO, typename ET, typename WT, int U,
+          int LD = DefaultLd<STRAT>::value>
 cudaError_t expand_sweep(const ExpandArgs& a, int num_sms, cudaStream_t st,
                          uint64_t* launches) {
   // window counts -> global exclusive prefix (wpre[n] = total windows)
@@ -1494,6 +1637,8 @@ cudaError_t expand_t(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t
   }
   if constexpr ((STRAT == kMergedAligned || STRAT == kMerged) && ALGO == kBfs &&
                 sizeof(ET) == 4 && sizeof(WT) == 4) {
+    if (!a.chunk_sched && a.ld == 0)
+      return expand_sweep<STRAT, ALGO, ET, WT, kUnroll, 0>(a, num_sms, st, launches);
     if (!a.chunk_sched && a.ld == 1)
       return expand_sweep<STRAT, ALGO, ET, WT, kUnroll, 1>(a, num_sms, st, launches);
     if (!a.chunk_sched && a.ld == 2)
@@ -1527,6 +1672,7 @@ cudaError_t expand_a(int algo, int eb, int wb, const ExpandArgs& a, int num_sms,
     case kSssp: return expand_w<STRAT, kSssp>(eb, wb, a, num_sms, st, l);
     case kCc: return expand_w<STRAT, kCc>(eb, wb, a, num_sms, st, l);
     case kPr: return expand_w<STRAT, kPr>(eb, wb, a, num_sms, st, l);
+    case kCcUf: return expand_w<STRAT, kCcUf>(eb, wb, a, num_sms, st, l);
     case kBfs + kPartAlgo: return expand_w<STRAT, kBfs + kPartAlgo>(eb, wb, a, num_sms, st, l);
     case kSssp + kPartAlgo: return expand_w<STRAT, kSssp + kPartAlgo>(eb, wb, a, num_sms, st, l);
     default: return expand_w<STRAT, kCc + kPartAlgo>(eb, wb, a, num_sms, st, l);
@@ -1553,6 +1699,7 @@ cudaError_t launch_expand(int strategy, int algo, int edge_bytes, int weight_byt
       case kSssp + kPartAlgo: return expand_cmp<kSssp + kPartAlgo>(a, num_sms, st, launches);
       case kCc + kPartAlgo: return expand_cmp<kCc + kPartAlgo>(a, num_sms, st, launches);
       case kBfsPull: return expand_cmp<kBfsPull>(a, num_sms, st, launches);
+      case kCcUf: return expand_cmp<kCcUf>(a, num_sms, st, launches);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -1688,6 +1835,48 @@ cudaError_t launch_compact(int algo, const CompactArgs& c, cudaStream_t st, uint
     default: k_tile_write<kCc><<<g, kTileThreads, 0, st>>>(c); break;
   }
   *launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_far_min(const uint8_t* flags, const void* dist, uint64_t nv, uint64_t* ctr,
+                           cudaStream_t st, uint64_t* launches) {
+  k_far_reset<<<1, 1, 0, st>>>(ctr);
+  k_far_min<<<grid_for(nv, 256, 148, 8), 256, 0, st>>>(flags, static_cast<const uint64_t*>(dist),
+                                                       nv, ctr);
+  *launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_uf_flatten(uint32_t* parent, uint64_t nv, cudaStream_t st, uint64_t* launches) {
+  if (!nv) return cudaSuccess;
+  k_uf_flatten<<<grid_for(nv, 256, 148, 8), 256, 0, st>>>(parent, nv);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_uf_sample(const uint32_t* parent, uint64_t nv, uint32_t* out, uint32_t sample,
+                             cudaStream_t st, uint64_t* launches) {
+  if (!nv) return cudaSuccess;
+  k_uf_sample<<<(sample + 255) / 256, 256, 0, st>>>(parent, nv, out, sample);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_uf_marks(const uint32_t* parent, const uint64_t* off, const uint64_t* cpos,
+                            uint64_t nv, uint32_t giant, int strategy, int edge_bytes,
+                            uint8_t* flags, cudaStream_t st, uint64_t* launches) {
+  if (!nv) return cudaSuccess;
+  k_uf_marks<<<grid_for(nv, 256, 148, 8), 256, 0, st>>>(parent, off, cpos, nv, giant, strategy,
+                                                        edge_bytes, flags);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fval_ids(const uint32_t* front, uint64_t* fval, uint64_t n, cudaStream_t st,
+                            uint64_t* launches) {
+  if (!n) return cudaSuccess;
+  k_fval_ids<<<grid_for(n, 256, 148, 8), 256, 0, st>>>(front, fval, n);
+  *launches += 1;
   return cudaGetLastError();
 }
 

@@ -268,7 +268,8 @@ class DeviceGraph:
             N.check(N.lib().zc_set_options(self.handle, opt))
             self._options = opt
 
-    def run(self, algo: str, source: int, strategy_id: int, traffic: bool = False):
+    def run(self, algo: str, source: int, strategy_id: int, traffic: bool = False,
+            schedule: str = "jacobi", delta: int = 0):
         """Run one traversal; returns (values int64[V] pinned, Stats, traversed, frontier, hist)."""
         lib = N.lib()
         with self._lock:
@@ -278,8 +279,13 @@ class DeviceGraph:
             ptr = out.ctypes.data
             if algo == "bfs":
                 rc = lib.zc_bfs(self.handle, source, strategy_id, ptr, C.byref(st))
+            elif algo == "sssp" and schedule == "near-far":
+                rc = lib.zc_sssp_nearfar(self.handle, source, strategy_id, int(delta), ptr,
+                                         C.byref(st))
             elif algo == "sssp":
                 rc = lib.zc_sssp(self.handle, source, strategy_id, ptr, C.byref(st))
+            elif algo == "cc" and schedule == "afforest":
+                rc = lib.zc_cc_afforest(self.handle, strategy_id, ptr, C.byref(st))
             elif algo == "cc":
                 rc = lib.zc_cc(self.handle, strategy_id, ptr, C.byref(st))
             else:

@@ -24,6 +24,22 @@ from .traffic import TrafficStats
 UNREACHED_LEVEL = -1
 UNREACHED_DIST = np.iinfo(np.int64).max
 
+# Schedules beyond the reference's Jacobi iteration (B200 extensions): the
+# values are the same unique fixpoints (distances, min-id labels); iteration
+# counts and per-iteration traversed edges follow the schedule.
+SCHEDULES = {"sssp": ("near-far",), "cc": ("afforest",)}
+
+
+def _check_schedule(algo: str, schedule: str, collect_traffic) -> None:
+    if schedule == "jacobi":
+        return
+    if schedule not in SCHEDULES[algo]:
+        raise ValueError(f"unknown {algo} schedule {schedule!r}: 'jacobi' or "
+                         + " / ".join(repr(x) for x in SCHEDULES[algo]))
+    if collect_traffic:
+        raise ValueError("the request model follows the reference's Jacobi schedule; "
+                         f"run schedule={schedule!r} with collect_traffic=False")
+
 
 @dataclass
 class TraversalResult:
@@ -81,8 +97,12 @@ def _model_wanted(collect_traffic: Optional[bool], sid: int) -> bool:
 
 
 def _run(algo: str, g, source: int, strategy, collect_traffic: Optional[bool], want_pages: bool,
-         placement: str, device: int) -> TraversalResult:
+         placement: str, device: int, schedule: str = "jacobi", delta: int = 0) -> TraversalResult:
     sid = strategy_id(strategy)
+    if schedule != "jacobi" and collect_traffic is None:
+        collect_traffic = False
+    if algo != "bfs":
+        _check_schedule(algo, schedule, collect_traffic)
     collect_traffic = _model_wanted(collect_traffic, sid)
     if want_pages:
         # The page streams feed the reference's LRU page-migration simulator
@@ -91,7 +111,8 @@ def _run(algo: str, g, source: int, strategy, collect_traffic: Optional[bool], w
             "page streams are a simulator artefact; run with placement='uvm' for the real "
             "cudaMallocManaged comparison")
     dg = device_graph(g, placement, device)
-    out, st, trav, front, hist = dg.run(algo, int(source), sid, traffic=collect_traffic)
+    out, st, trav, front, hist = dg.run(algo, int(source), sid, traffic=collect_traffic,
+                                        schedule=schedule, delta=delta)
     if hist is not None:
         per_iter = [TrafficStats.from_device_hist(h) for h in hist]
     else:
@@ -117,26 +138,38 @@ def bfs(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *,
 
 def sssp(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *,
          collect_traffic: Optional[bool] = None, want_pages: bool = False,
-         page_bytes: int = 4096, placement: str = "zerocopy", device: int = 0) -> TraversalResult:
+         page_bytes: int = 4096, placement: str = "zerocopy", device: int = 0,
+         schedule: str = "jacobi", delta: Optional[int] = None) -> TraversalResult:
     """Exact shortest distances by frontier-restricted (Jacobi) relaxation
-    (reference traversal.py:123-151); unreached vertices get INT64_MAX."""
+    (reference traversal.py:123-151); unreached vertices get INT64_MAX.
+
+    ``schedule="near-far"`` (B200 extension) expands only the improved
+    vertices below a threshold that advances by ``delta`` (default 32) once
+    they run out: the same distances with less work; iteration counts differ
+    from the reference's."""
     _check_source(g, source)
     if not _has_weights(g):
         raise ValueError("sssp requires edge weights")
     if not isinstance(g, DeviceGraph) and g.num_edges and int(np.min(g.weights)) < 0:
         raise ValueError("sssp requires non-negative weights")
-    return _run("sssp", g, source, strategy, collect_traffic, want_pages, placement, device)
+    if delta is not None and delta < 1:
+        raise ValueError("delta must be >= 1")
+    return _run("sssp", g, source, strategy, collect_traffic, want_pages, placement, device,
+                schedule, delta or 0)
 
 
 def cc(g, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traffic: Optional[bool] = None,
        want_pages: bool = False, page_bytes: int = 4096, placement: str = "zerocopy",
-       device: int = 0) -> TraversalResult:
+       device: int = 0, schedule: str = "jacobi") -> TraversalResult:
     """Connected-component labels (min vertex id) by minimum-label propagation,
-    all vertices active at the start (reference traversal.py:154-179)."""
+    all vertices active at the start (reference traversal.py:154-179).
+
+    ``schedule="afforest"`` (B200 extension) computes the same labels by
+    union-find in at most two passes over the lists (iterations = passes)."""
     if g.directed:
         raise ValueError("connected components require an undirected graph "
                          "(load with directed=False or symmetrize first)")
-    return _run("cc", g, 0, strategy, collect_traffic, want_pages, placement, device)
+    return _run("cc", g, 0, strategy, collect_traffic, want_pages, placement, device, schedule)
 
 
 def _run_many(algo: str, g, sources, strategy, collect_traffic: bool, placement: str,

@@ -700,3 +700,70 @@ def test_compressed_byte_accounting():
     assert dg.link_bytes_requested() > 0
     assert dg.directions(r.iterations).shape == (r.iterations,)
     dg.close()
+
+
+SCHED_STRATS = ["naive", "merged", "merged-aligned", "packed", "compressed"]
+
+
+@pytest.mark.parametrize("strategy", SCHED_STRATS)
+def test_work_efficient_schedules_match_reference_values(strategy):
+    """near-far SSSP and afforest CC (B200 schedules): the reference's values
+    on every fixture (iterations follow the schedule, so only values and
+    the error conditions are compared)."""
+    bad = []
+    for c in CASES:
+        if c.algo == "sssp":
+            if strategy == "compressed" and c.graph.weight_elem_bytes != 4:
+                continue
+            for delta in (1, 7, 32, 1000):
+                r = zc.sssp(c.graph, c.source, strategy, schedule="near-far", delta=delta)
+                if not np.array_equal(r.values, c.values):
+                    bad.append((c.index, c.tag, delta))
+        elif c.algo == "cc":
+            if strategy == "compressed" and c.graph.edge_elem_bytes != 4:
+                continue
+            r = zc.cc(c.graph, strategy, schedule="afforest")
+            if not np.array_equal(r.values, c.values) or r.iterations > 2:
+                bad.append((c.index, c.tag))
+    assert not bad, bad[:8]
+
+
+def test_work_efficient_schedules_rmat():
+    """Both schedules on R-MAT graphs with hubs, isolated vertices and many
+    components, against the oracle (values), with their work bounds."""
+    for scale, seed in ((16, 3), (18, 9)):
+        k = zc.generate_rmat(scale, 16, seed=seed, symmetrize=True)
+        gk = k.as_csr()
+        ref = oracle.cc(gk, threads=8)
+        for s in SCHED_STRATS:
+            r = zc.cc(k, s, schedule="afforest")
+            assert np.array_equal(r.values, ref.values), (scale, s)
+            assert r.iterations <= 2 and r.total_traversed_edges <= 2 * gk.num_edges
+        k.close()
+    u = zc.generate_uniform_device(1 << 17, 16, 16, seed=5, weights=(8, 72))
+    gu = u.as_csr()
+    src = int(zc.pick_sources(gu, 1, seed=7)[0])
+    ref = oracle.sssp(gu, src, threads=8)
+    for s in SCHED_STRATS:
+        r = zc.sssp(u, src, s, schedule="near-far")
+        assert np.array_equal(r.values, ref.values), s
+        assert r.total_traversed_edges < sum(ref.traversed_edges)  # less work than Jacobi
+    w = zc.generate_rmat(17, 8, seed=4, weights=(1, 1000))
+    gw = w.as_csr()
+    src = int(zc.pick_sources(gw, 1, seed=7)[0])
+    ref = oracle.sssp(gw, src, threads=8)
+    for delta in (1, 50, 10 ** 6):
+        r = zc.sssp(w, src, "merged-aligned", schedule="near-far", delta=delta)
+        assert np.array_equal(r.values, ref.values), delta
+
+
+def test_schedule_argument_errors():
+    g = zc.with_uniform_weights(zc.generate_uniform(64, 1, 4, seed=1))
+    with pytest.raises(ValueError, match="schedule"):
+        zc.sssp(g, 0, schedule="afforest")
+    with pytest.raises(ValueError, match="schedule"):
+        zc.cc(zc.symmetrized(g), schedule="near-far")
+    with pytest.raises(ValueError, match="request model"):
+        zc.sssp(g, 0, schedule="near-far", collect_traffic=True)
+    with pytest.raises(ValueError, match="undirected"):
+        zc.cc(g, schedule="afforest")
