@@ -74,8 +74,12 @@ def parse():
     p.add_argument("--force-partitioned", action="store_true")
     p.add_argument("--part-scale", type=int, default=29,
                    help="N>1: Kronecker scale of the partitioned graph (fixed size)")
-    p.add_argument("--no-fused", action="store_true",
-                   help="N>1: skip the fused (NVLink peer-store) exchange variant")
+    p.add_argument("--exchange", default="fused", choices=["fused", "reduce-scatter"],
+                   help="N>1: exchange of the headline run (the other is timed beside it)")
+    p.add_argument("--no-configs4", action="store_true",
+                   help="N>1: skip the fixed-size Kronecker-29 symmetrized BFS / CC block")
+    p.add_argument("--no-parity", action="store_true",
+                   help="N>1: skip the small-scale oracle parity runs")
     return p.parse_args()
 
 
@@ -694,124 +698,279 @@ def config1(zc, threads, parity) -> dict:
 
 
 # ------------------------------------------------------------------ N > 1
+def _part_series(part, algo, sources, strat, steps, warmup, world, device, *, exchange, bufs,
+                 stage, fetch=False):
+    """`steps` traversals of a partitioned graph after `warmup`: the loop's
+    device time (CUDA events on this rank, max over ranks), the whole job's
+    traversed edges, this rank's expansion time / streamed edges / exchange
+    bytes, summed or maxed over ranks."""
+    import torch
+    from paper_2006_06890_b200.multi import run_partition
+
+    def one(i):
+        return run_partition(part, algo, int(sources[i % len(sources)]), strat, stage_host=stage,
+                             fetch=fetch, buffers=None if exchange == "fused" else bufs,
+                             fused=exchange == "fused")
+
+    for i in range(warmup):
+        one(i)
+    barrier(world, device)
+    trav = launches = local_trav = xbytes = bu = 0
+    expand_ms = 0.0
+    results = []
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    ev0.record()
+    for i in range(steps):
+        r = one(warmup + i)
+        trav += r.total_traversed_edges
+        local_trav += r.local_traversed
+        expand_ms += r.expand_ms
+        xbytes += r.exchange_bytes
+        bu += r.bottom_up_steps
+        launches += part.launches()
+        results.append(r)
+    ev1.record()
+    torch.cuda.synchronize(device)
+    wall = time.perf_counter() - t0
+    barrier(world, device)
+    loop_ms = max_over_ranks(ev0.elapsed_time(ev1), world, device)
+    # per-rank link rate (its streamed edges x 4 B over its expansion time), summed
+    link = local_trav * 4 / max(expand_ms * 1e-3, 1e-12) / 1e9
+    return {"gteps": trav / (loop_ms * 1e-3) / 1e9, "ms_per_step": loop_ms / steps,
+            "traversed_edges_per_step": trav / steps,
+            "iterations": results[-1].iterations if results else 0,
+            "aggregate_link_gbs": sum_over_ranks(link, world, device),
+            "max_rank_expand_ms_per_step": max_over_ranks(expand_ms, world, device) / steps,
+            "sum_rank_expand_ms_per_step": sum_over_ranks(expand_ms, world, device) / steps,
+            "exchange_bytes_per_step": sum_over_ranks(xbytes, world, device) / steps,
+            "bottom_up_steps_per_step": bu / steps,
+            "gpu_launches": int(sum_over_ranks(launches, world, device)),
+            "wall_s": max_over_ranks(wall, world, device), "_results": results,
+            "_trav": trav}
+
+
+def _gather_values_crc(r, world, device) -> str:
+    """crc32 of the concatenated owned slices (rank order = range order)."""
+    import torch.distributed as dist
+    parts = [None] * world
+    dist.all_gather_object(parts, r.values.astype("<i8").tobytes() if r.values is not None else b"")
+    crc = 0
+    for b in parts:
+        crc = zlib.crc32(b, crc)
+    return f"{crc & 0xffffffff:08x}"
+
+
+def _strip(d: dict) -> dict:
+    return {k: v for k, v in d.items() if not k.startswith("_")}
+
+
+def _part_parity_small(args, rank, world, device, stage) -> dict:
+    """Partitioned BFS / CC at a small scale, every exchange, against the
+    CPU oracle on rank 0 (values, iterations, traversed edges)."""
+    import numpy as np
+    import torch.distributed as dist
+    import paper_2006_06890_b200 as zc
+    from paper_2006_06890_b200.multi import generate_rmat_part, run_partition, exchange_buffers
+    out = {}
+    scale = 18
+    for sym, algo in ((False, "bfs"), (True, "cc"), (True, "bfs")):
+        part = generate_rmat_part(scale, world, rank, args.edge_factor, seed=args.seed,
+                                  symmetrize=sym, device=device)
+        ref = None
+        if rank == 0:
+            import oracle
+            whole = zc.generate_rmat(scale, args.edge_factor, seed=args.seed, symmetrize=sym,
+                                     device=device)
+            g = whole.as_csr()
+            src = int(zc.pick_sources(g, 1, seed=7)[0])
+            ref = oracle.run(algo, g, src, threads=args.cpu_threads or os.cpu_count())
+            whole.close()
+        else:
+            src = 0
+        box = [src]
+        dist.broadcast_object_list(box, 0)
+        src = box[0]
+        bufs = exchange_buffers(algo, world, part.stride,
+                                __import__("torch").device("cuda", device))
+        for exch in ("reduce-scatter", "fused"):
+            r = run_partition(part, algo, src, "merged-aligned", stage_host=stage, fetch=True,
+                              buffers=None if exch == "fused" else bufs, fused=exch == "fused")
+            parts = [None] * world
+            dist.all_gather_object(parts, r.values)
+            if rank == 0:
+                vals = np.concatenate(parts)
+                out[f"{'sym_' if sym else ''}{algo}/{exch}"] = bool(
+                    np.array_equal(vals, ref.values) and r.iterations == ref.iterations
+                    and list(r.traversed_edges) == list(ref.traversed_edges))
+        part.close()
+    return out
+
+
 def main_partitioned(args, rank, world, device):
-    config = bfs_config(args, world)
-    """N>1: weak scaling -- Kronecker scale 27 + log2(N) (K29 at N=4, BASELINE
-    configs[4]), vertex-range partitioned, each rank streaming its own 2^31-arc
-    slice over its own host link; NCCL reduce-scatter of the u8 frontier flags
-    (MAX) over NVLink every level."""
+    """N>1 (BASELINE configs[4]).  One process per GPU, vertex-range
+    partitions (edge-balanced), each rank streaming its own edge slice over its
+    own host link.
+
+    headline  weak scaling: directed Kronecker scale 27 + log2(N) (2^31 arcs
+              per rank, as the N=1 line; K29 at N=4), BFS merged+aligned, the
+              fused exchange (discoveries stored straight into the owner's
+              buffer over NVLink, deduplicated per rank and level); the NCCL
+              reduce-scatter exchange timed beside it
+    configs4  fixed size: Kronecker 29 symmetrized (2^34 arcs) BFS and CC
+    parity    small-scale BFS / CC against the oracle for both exchanges;
+              full size: both exchanges give the same levels (crc), iterations
+              and traversed edges"""
     import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2006_06890_b200 as zc
-    from paper_2006_06890_b200.multi import (exchange_buffers, generate_rmat_part,
-                                             run_partition)
+    from paper_2006_06890_b200.multi import exchange_buffers, generate_rmat_part
 
-    scale = args.scale + max(0, int(round(np.log2(world))))
     stage = args.backend == "gloo"
-    t0 = time.time()
-    part = generate_rmat_part(scale, world, rank, args.edge_factor, seed=args.seed,
-                              device=device)
-    gen_s = time.time() - t0
-    # sources: pick_sources semantics on rank 0's range, broadcast
-    src = torch.zeros(64, dtype=torch.int64)
-    if rank == 0:
-        src = torch.from_numpy(zc.pick_sources(part.graph_view(), 64, seed=7).astype(np.int64))
-    src = src.to(torch.device("cpu") if stage else torch.device("cuda", device))
-    dist.broadcast(src, 0)
-    sources = src.cpu().numpy()
-    bufs = exchange_buffers("bfs", world, part.stride, torch.device("cuda", device))
+    dev = torch.device("cuda", device)
     strat = args.strategy
+    scale = args.scale + max(0, int(round(np.log2(world))))
+    parity = {}
+    if not args.no_parity:
+        parity.update(_part_parity_small(args, rank, world, device, stage))
 
-    def one(i, fetch):
-        return run_partition(part, "bfs", int(sources[i % 64]), strat, stage_host=stage,
-                             fetch=fetch, buffers=bufs)
-
-    for i in range(args.warmup):
-        one(i, False)
-    barrier(world, device)
-    trav = 0
-    launches = 0
-    expand_ms = 0.0
+    t0 = time.time()
+    part = generate_rmat_part(scale, world, rank, args.edge_factor, seed=args.seed, device=device)
+    gen_s = max_over_ranks(time.time() - t0, world, device)
+    # sources: pick_sources semantics on rank 0's range, broadcast
+    src = [None]
+    if rank == 0:
+        src = [zc.pick_sources(part.graph_view(), 64, seed=7).astype(np.int64)
+               + int(part.bounds[0])]
+    dist.broadcast_object_list(src, 0)
+    sources = src[0]
+    bufs = exchange_buffers("bfs", world, part.stride, dev)
     with ClockSampler(device) as clk:
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        for i in range(args.steps):
-            r = one(args.warmup + i, False)
-            trav += r.total_traversed_edges
-            launches += part.launches()
-        ev1.record()
-        torch.cuda.synchronize(device)
-    barrier(world, device)
-    loop_ms = max_over_ranks(ev0.elapsed_time(ev1), world, device)
-    value = trav / (loop_ms * 1e-3) / 1e9  # traversed edges are global (summed over ranks)
+        head = _part_series(part, "bfs", sources, strat, args.steps, args.warmup, world, device,
+                            exchange=args.exchange, bufs=bufs, stage=stage)
+    other = "reduce-scatter" if args.exchange == "fused" else "fused"
+    alt = _part_series(part, "bfs", sources, strat, min(args.steps, 5), 1, world, device,
+                       exchange=other, bufs=bufs, stage=stage)
+    # e2e: the public partitioned API with every rank's int64 levels downloaded
+    e2e = _part_series(part, "bfs", sources, strat, args.steps, 0, world, device,
+                       exchange=args.exchange, bufs=bufs, stage=stage, fetch=True)
+    d2h = sum_over_ranks(sum(r.values.nbytes for r in e2e["_results"]), world, device)
+    crc_a = _gather_values_crc(e2e["_results"][0], world, device)
+    r_alt = _part_series(part, "bfs", sources[:1], strat, 1, 0, world, device, exchange=other,
+                         bufs=bufs, stage=stage, fetch=True)  # e2e's first run: sources[0]
+    crc_b = _gather_values_crc(r_alt["_results"][0], world, device)
+    ra, rb = e2e["_results"][0], r_alt["_results"][0]
+    parity[f"kron{scale}/fused_vs_reduce_scatter"] = bool(
+        crc_a == crc_b and ra.iterations == rb.iterations
+        and list(ra.traversed_edges) == list(rb.traversed_edges))
+    e2e_value = e2e["_trav"] / e2e["wall_s"] / 1e9
+    part_arcs = part.graph_view().num_edges
+    part.close()
+    del bufs
+    torch.cuda.empty_cache()
 
+    peak = world * PCIE_GEN5_X16_GBS
+    line = {
+        "metric": METRIC, "value": head["gteps"], "unit": "GTEPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": dict(bfs_config(args, world), **{
+            "workload": f"BFS, Kronecker (R-MAT a=.57 b=.19 c=.19) scale {scale}, edge factor "
+                        f"{args.edge_factor}, {args.edge_factor << scale} directed arcs, "
+                        f"vertex-range partitioned over {world} ranks (edge-balanced), each "
+                        "rank's u32 edge slice zero-copy in pinned host memory",
+            "graph": f"kron{scale}", "scale": scale, "parallelism": f"vertex-partition{world}",
+            "exchange": ("fused: the expansion kernel stores each discovery (deduplicated per "
+                         "rank and level) straight into its owner's candidate buffer through "
+                         "CUDA-IPC peer pointers over NVLink; all-reduce of the counts"
+                         if args.exchange == "fused" else
+                         "per level: NCCL reduce-scatter of u8 flags (MAX); all-reduce of counts"),
+            "backend": args.backend}),
+        "e2e": {"value": e2e_value, "unit": "GTEPS", "h2d_bytes_per_step": 8,
+                "d2h_bytes_per_step": int(d2h) // max(args.steps, 1),
+                "ms_per_step": e2e["wall_s"] / max(args.steps, 1) * 1e3,
+                "api": "run_partition(fetch=True) on every rank: owned int64 levels in host memory"},
+        "gpu_launches": head["gpu_launches"],
+        "roofline": {
+            "bound": "host-link", "achieved": head["aggregate_link_gbs"], "peak": peak,
+            "unit": "GB/s", "frac": head["aggregate_link_gbs"] / peak, "traffic": None,
+            "kernel": "k_expand_sweep<merged-aligned, partitioned bfs> on every rank",
+            "algorithmic_bytes": "each rank's traversed edges x 4 B over its expansion time, "
+                                 "summed over ranks (SURVEY 8e aggregate host-link GB/s)",
+            "peak_kind": f"{world} x PCIe Gen5 x16 theoretical per direction",
+            "kernel_share_of_step": head["max_rank_expand_ms_per_step"] / head["ms_per_step"]},
+        "clocks": clk.summary(),
+        "exchange": {"bytes_per_step": head["exchange_bytes_per_step"],
+                     "bytes_per_level": head["exchange_bytes_per_step"] / max(head["iterations"], 1),
+                     "kind": args.exchange,
+                     other.replace("-", "_") + "_bytes_per_step": alt["exchange_bytes_per_step"]},
+        "variants": {other: _strip(alt)},
+        "headline": _strip(head),
+        "graph": {"vertices": 1 << scale, "arcs": args.edge_factor << scale,
+                  "local_arcs_rank0": part_arcs, "gen_s": gen_s},
+    }
+    if not args.no_configs4:
+        line["configs4"] = configs4(args, rank, world, device, stage, parity)
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = reference_sample(3, 0, args.seed, args.cpu_threads or os.cpu_count())
     barrier(world, device)
-    t1 = time.perf_counter()
-    d2h = 0
-    for i in range(args.steps):
-        r = one(args.warmup + i, True)
-        d2h += r.values.nbytes
-        del r
-    barrier(world, device)
-    wall = max_over_ranks(time.perf_counter() - t1, world, device)
-    e2e_value = trav / wall / 1e9
-    fused = None
-    if not args.no_fused:
-        # variant: fused exchange -- the expand kernel writes candidates straight
-        # into the owners' buffers (CUDA IPC peer pointers over NVLink)
-        try:
-            for i in range(args.warmup):
-                run_partition(part, "bfs", int(sources[i % 64]), strat, fetch=False, fused=True)
-            barrier(world, device)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            ftrav = 0
-            for i in range(args.steps):
-                r = run_partition(part, "bfs", int(sources[(args.warmup + i) % 64]), strat,
-                                  fetch=False, fused=True)
-                ftrav += r.total_traversed_edges
-            e1.record()
-            torch.cuda.synchronize(device)
-            barrier(world, device)
-            fms = max_over_ranks(e0.elapsed_time(e1), world, device)
-            fused = {"gteps": ftrav / (fms * 1e-3) / 1e9, "ms_per_step": fms / args.steps,
-                     "same_traversed": ftrav == trav}
-        except Exception as exc:  # report, keep the headline
-            fused = {"error": f"{type(exc).__name__}: {exc}"[:300]}
-    cfg = dict(config)
-    cfg.update({"workload": f"BFS, Kronecker (R-MAT a=.57 b=.19 c=.19) scale {scale}, edge factor "
-                            f"{args.edge_factor}, {args.edge_factor << scale} directed arcs, "
-                            f"vertex-range partitioned over {world} ranks (edge-balanced), each "
-                            "rank's u32 edge slice zero-copy in pinned host memory",
-                "graph": f"kron{scale}", "scale": scale, "seed": args.seed,
-                "parallelism": f"vertex-partition{world}",
-                "exchange": ("per level: reduce-scatter of u8 flags (MAX) for top-down steps; "
-                             "bottom-up steps all-reduce (SUM of disjoint bits = OR) the "
-                             "owned-frontier bitmaps and scan the owned vertices' in-lists "
-                             "(generated per rank, no edge exchange); all-reduce of counts"
-                             if strat == "direction-optimizing" else
-                             "per level: reduce-scatter of u8 flags (MAX), all-reduce of counts"),
-                "backend": args.backend})
-    line = {"metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": loop_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic", "config": cfg,
-            "e2e": {"value": e2e_value, "unit": "GTEPS", "h2d_bytes_per_step": 8,
-                    "d2h_bytes_per_step": int(sum_over_ranks(d2h, world, device)) // args.steps,
-                    "ms_per_step": wall / args.steps * 1e3},
-            "gpu_launches": int(sum_over_ranks(launches, world, device)),
-            "variants": {"fused_exchange": fused},
-            "clocks": clk.summary(),
-            "graph": {"vertices": 1 << scale, "arcs": args.edge_factor << scale,
-                      "local_arcs_rank0": part.graph_view().num_edges, "gen_s": gen_s,
-                      "traversed_edges_per_step": trav / args.steps}}
+    line["parity"] = parity
+    line["parity_all_true"] = all(parity.values()) if parity else None
     if rank == 0:
         print(json.dumps(line), flush=True)
-    part.close()
 
+
+def configs4(args, rank, world, device, stage, parity) -> dict:
+    """BASELINE configs[4] at fixed size: Kronecker `part_scale` symmetrized
+    (2^34 arcs at 29), BFS and CC (Jacobi label propagation), vertex-range
+    partitioned over the N ranks (strong scaling)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2006_06890_b200 as zc
+    from paper_2006_06890_b200.multi import exchange_buffers, generate_rmat_part
+    scale = args.part_scale
+    dev = torch.device("cuda", device)
+    t0 = time.time()
+    part = generate_rmat_part(scale, world, rank, args.edge_factor, seed=args.seed,
+                              symmetrize=True, device=device)
+    gen_s = max_over_ranks(time.time() - t0, world, device)
+    src = [None]
+    if rank == 0:
+        src = [zc.pick_sources(part.graph_view(), 8, seed=7).astype(np.int64)
+               + int(part.bounds[0])]
+    dist.broadcast_object_list(src, 0)
+    sources = src[0]
+    arcs = 2 * (args.edge_factor << scale)
+    out = {"workload": f"Kronecker (R-MAT a=.57 b=.19 c=.19) scale {scale} symmetrized "
+                       f"({arcs} arcs, {arcs * 4 >> 30} GiB u32), vertex-range partitioned over "
+                       f"{world} ranks, each slice zero-copy in its rank's pinned host memory",
+           "scaling": "strong", "gen_s": gen_s, "arcs": arcs}
+    peak = world * PCIE_GEN5_X16_GBS
+    for algo, exch, steps in (("bfs", "fused", 2), ("bfs", "reduce-scatter", 2),
+                              ("cc", "reduce-scatter", 1), ("cc", "fused", 1)):
+        bufs = exchange_buffers(algo, world, part.stride, dev) if exch != "fused" else None
+        r = _part_series(part, algo, sources, "merged-aligned", steps, 1, world, device,
+                         exchange=exch, bufs=bufs, stage=stage)
+        key = f"{algo}/{exch}"
+        res = _strip(r)
+        res["aggregate_link_frac"] = r["aggregate_link_gbs"] / peak
+        if algo == "cc":  # primary GTEPS: every vertex reached, Sigma deg = arcs
+            res["primary_gteps"] = arcs / (r["ms_per_step"] * 1e-3) / 1e9
+            res["work_gteps"] = r["gteps"]
+        out[key] = res
+        del bufs
+        torch.cuda.empty_cache()
+    for algo in ("bfs", "cc"):  # both exchanges: identical iterations and work
+        a, b = out[f"{algo}/fused"], out[f"{algo}/reduce-scatter"]
+        parity[f"k{scale}sym_{algo}/fused_vs_reduce_scatter_work"] = (
+            a["iterations"] == b["iterations"]
+            and a["traversed_edges_per_step"] == b["traversed_edges_per_step"])
+    part.close()
+    return out
 
 
 if __name__ == "__main__":

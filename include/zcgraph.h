@@ -135,7 +135,10 @@ typedef struct zc_stats {
   uint64_t launches;               /* kernels launched by the call          */
   double expand_ms;                /* device time of the expansion kernels
                                       (the zero-copy edge stream) alone     */
-  uint64_t reserved[6];
+  uint64_t exchange_bytes;         /* partitions: bytes this rank sent to the
+                                      others since zc_part_begin (reduce-
+                                      scatter share, or fused remote sends) */
+  uint64_t reserved[5];
 } zc_stats;
 
 const char *zc_last_error(void);
@@ -359,13 +362,16 @@ int zc_part_fused_connect(zc_graph *g, const void *ipc_handles, void *const *ptr
 int zc_part_fused_reset(zc_graph *g);
 int zc_part_fused_expand(zc_graph *g);
 
-/* Part `part` of the directed graph zc_generate_rmat builds with the same
- * parameters (same arcs, same list order), edge-balanced across nparts;
- * bounds (nparts+1) receives the vertex ranges of all parts. */
+/* Part `part` of the graph zc_generate_rmat builds with the same parameters
+ * (same arcs, same lists), edge-balanced across nparts; bounds (nparts+1)
+ * receives the vertex ranges of all parts.  symmetrize != 0: the part of the
+ * symmetrized graph (reverse arcs added, csr.py:350-359 semantics, lists
+ * sorted; no weights), cut at 2E*k/nparts of its arcs -- every rank
+ * enumerates the counter-based arcs into its range, no edge exchange. */
 int zc_generate_rmat_part(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
-                          uint64_t seed, int64_t wlow, int64_t whigh, uint32_t nparts,
-                          uint32_t part, int32_t placement, int32_t device, uint64_t *bounds,
-                          zc_graph **out);
+                          uint64_t seed, int symmetrize, int64_t wlow, int64_t whigh,
+                          uint32_t nparts, uint32_t part, int32_t placement, int32_t device,
+                          uint64_t *bounds, zc_graph **out);
 
 #ifdef __cplusplus
 }

@@ -59,19 +59,26 @@ def _build_lib(sources, lib_path, link_extra, force, verbose, extra_deps=()):
         return lib_path
     objdir = os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
+    headers = [d for d in deps if d.endswith((".cuh", ".h"))]
+    jobs = []
     objs = []
-    for src in srcs:
+    for src in srcs:  # compile the translation units in parallel, stale ones only
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if not force and not _stale(obj, [src] + headers):
+            continue
         cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src,
                "-o", obj]
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
+        jobs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                                stderr=subprocess.PIPE, text=True)))
+    for src, obj, proc in jobs:
+        _, err = proc.communicate()
+        if proc.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{err}")
         if verbose:
-            print(res.stderr)
+            print(err)
         with open(obj + ".ptxas.txt", "w") as fh:
-            fh.write(res.stderr)
-        objs.append(obj)
+            fh.write(err)
     tmp = lib_path + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, *link_extra, "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)

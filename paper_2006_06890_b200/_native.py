@@ -58,7 +58,8 @@ class Stats(C.Structure):
         ("iterations", C.c_uint64), ("total_traversed_edges", C.c_uint64),
         ("max_frontier", C.c_uint64), ("kernel_ms", C.c_double), ("total_ms", C.c_double),
         ("d2h_ms", C.c_double), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
-        ("launches", C.c_uint64), ("expand_ms", C.c_double), ("reserved", C.c_uint64 * 6),
+        ("launches", C.c_uint64), ("expand_ms", C.c_double), ("exchange_bytes", C.c_uint64),
+        ("reserved", C.c_uint64 * 5),
     ]
 
 
@@ -129,8 +130,8 @@ def _declare(lib: C.CDLL) -> None:
         "zc_part_fused_connect": (C.c_int, [P, P, P]),
         "zc_part_fused_reset": (C.c_int, [P]),
         "zc_part_fused_expand": (C.c_int, [P]),
-        "zc_generate_rmat_part": (C.c_int, [u32, u32, dbl, dbl, dbl, u64, i64, i64, u32, u32, i32,
-                                            i32, P, C.POINTER(P)]),
+        "zc_generate_rmat_part": (C.c_int, [u32, u32, dbl, dbl, dbl, u64, C.c_int, i64, i64, u32, u32,
+                                            i32, i32, P, C.POINTER(P)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

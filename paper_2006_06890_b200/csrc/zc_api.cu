@@ -344,6 +344,7 @@ void zc::free_graph(zc_graph* g) {
   cudaFree(g->d_mine);
   cudaFree(g->d_peers);
   cudaFree(g->d_sent);
+  cudaFree(g->d_lbest);
   cudaFree(g->d_wcnt);
   cudaFree(g->d_wpre);
   cudaFree(g->d_scan_tmp);
@@ -1105,7 +1106,8 @@ constexpr uint64_t kNearFarDelta = 32;
 //           edge with an endpoint outside the giant component is seen from
 //           that endpoint, so no edge is missed;
 //   flatten -> labels.
-// iterations = passes; traversed_edges[k] = the degree sum of pass k's lists.
+// iterations = passes; traversed_edges[k] = the list elements pass k read (pass 1:
+// the first windows, counted on the device; pass 2: the degree sum of its lists).
 int run_afforest(zc_graph* g, int strategy, int64_t* out, zc_stats* stats) {
   const double t0 = now_ms();
   if (!g) {
@@ -1191,7 +1193,7 @@ int run_afforest(zc_graph* g, int strategy, int64_t* out, zc_stats* stats) {
   uint64_t iters = 0;
   if (g->nv) {
     ++iters;
-    g->log_trav.push_back(g->ne);
+    g->log_trav.push_back(g->ne);  // naive reads whole lists; else replaced by kCtrVisited below
     g->log_front.push_back(g->nv);
     ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[0], st));
     ZC_CUDA_TRY(launch_expand(s1, kCcUf, g->eb, g->wb, args(g->nv, 1), g->num_sms, st, &launches));
@@ -1232,10 +1234,13 @@ int run_afforest(zc_graph* g, int strategy, int64_t* out, zc_stats* stats) {
     c.state = g->d_state;
     c.ctr = g->d_ctr;
     ZC_CUDA_TRY(launch_compact(kCc, c, st, &launches));
-    ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                                st));
+    ZC_CUDA_TRY(cudaMemcpyAsync(g->h_ctr, g->d_ctr, (kCtrVisited + 1) * sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, st));
     ZC_CUDA_TRY(cudaStreamSynchronize(st));
     const uint64_t n2 = g->h_ctr[kCtrNext], trav2 = g->h_ctr[kCtrTrav];
+    // the sampling pass reads the first window (line) of every list: log the
+    // elements it actually read, so work and link bytes are what crossed the link
+    if (s1 != kNaive) g->log_trav[0] = g->h_ctr[kCtrVisited];
     if (n2) {
       ++iters;
       g->log_trav.push_back(trav2);
@@ -1619,6 +1624,7 @@ int zc_part_begin(zc_graph* g, int algo, uint64_t src, int strategy, uint64_t* n
   g->p_iter = 0;
   g->p_cur = 0;
   g->p_launches = 0;
+  g->p_xbytes = 0;
   g->log_trav.clear();
   g->log_front.clear();
   g->log_expand_ms.clear();
@@ -1666,10 +1672,15 @@ static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
   DeviceGuard dg(g->device);
   cudaStream_t st = g->stream;
   const int algo = g->p_algo;
-  if (!fused)
+  const size_t xb = zc_part_exchange_elem_bytes(algo);
+  if (!fused) {
     ZC_CUDA_TRY(launch_fill_exchange(algo, exch, g->nparts * g->stride, st, &g->p_launches));
-  else if (algo == kBfs)
+    g->p_xbytes += (g->nparts - 1) * g->stride * xb;  // this rank's reduce-scatter send
+  } else if (algo == kBfs) {
     ZC_CUDA_TRY(cudaMemsetAsync(g->d_sent, 0, (g->global_nv + 31) / 32 * 4, st));
+  } else {
+    ZC_CUDA_TRY(cudaMemsetAsync(g->d_lbest, 0xff, g->global_nv * xb, st));
+  }
   ++g->p_iter;
   g->log_front.push_back(g->p_n);
   while (g->iter_ev.size() < 2 * g->p_iter) {
@@ -1701,6 +1712,7 @@ static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
   a.stride = g->stride;
   a.peers = fused ? g->d_peers : nullptr;
   a.sent = fused && algo == kBfs ? g->d_sent : nullptr;
+  a.lbest = fused && algo != kBfs ? g->d_lbest : nullptr;
   a.wcnt = g->d_wcnt;
   a.wpre = g->d_wpre;
   a.scan_tmp = g->d_scan_tmp;
@@ -1717,7 +1729,17 @@ static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
                             &g->p_launches));
   ZC_CUDA_TRY(cudaEventRecord(g->iter_ev[2 * (g->p_iter - 1) + 1], st));
   ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr + kCtrBig, 0, sizeof(uint64_t), st));
+  if (fused) {  // remote destinations this rank sent to (BFS: exact stores)
+    ZC_CUDA_TRY(cudaMemsetAsync(g->d_ctr + kCtrRemote, 0, sizeof(uint64_t), st));
+    ZC_CUDA_TRY(launch_count_remote(algo == kBfs ? static_cast<const void*>(g->d_sent) : g->d_lbest,
+                                    algo == kBfs ? 0 : static_cast<int>(xb), g->global_nv, g->lo,
+                                    g->lo + g->nv, g->d_ctr + kCtrRemote, g->num_sms, st,
+                                    &g->p_launches));
+    ZC_CUDA_TRY(cudaMemcpyAsync(&g->h_small[2], g->d_ctr + kCtrRemote, sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, st));
+  }
   ZC_CUDA_TRY(cudaStreamSynchronize(st));
+  if (fused) g->p_xbytes += g->h_small[2] * xb;
   float ms = 0;
   cudaEventElapsedTime(&ms, g->iter_ev[2 * (g->p_iter - 1)], g->iter_ev[2 * (g->p_iter - 1) + 1]);
   g->log_expand_ms.push_back(ms);
@@ -1741,6 +1763,8 @@ int zc_part_fused_init(zc_graph* g, int algo, void* ipc_handle, void** local) {
     ZC_CUDA_TRY(cudaMalloc(&g->d_peers, g->nparts * sizeof(void*)));
     ZC_CUDA_TRY(cudaMalloc(&g->d_sent, (g->global_nv + 31) / 32 * 4 + 4));
   }
+  if (algo != kBfs && !g->d_lbest)  // the local pre-filter (u64: SSSP or CC)
+    ZC_CUDA_TRY(cudaMalloc(&g->d_lbest, std::max<uint64_t>(g->global_nv, 1) * sizeof(uint64_t)));
   g->fused_algo = algo;
   if (ipc_handle) {
     cudaIpcMemHandle_t h;
@@ -1962,6 +1986,7 @@ int zc_part_result(zc_graph* g, int64_t* out, zc_stats* stats) {
     for (double x : g->log_expand_ms) ex += x;
     stats->expand_ms = ex;
     stats->d2h_bytes = out ? g->nv * sizeof(int64_t) : 0;
+    stats->exchange_bytes = g->p_xbytes;
   }
   return ZC_OK;
 }

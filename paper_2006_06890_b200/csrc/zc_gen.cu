@@ -146,9 +146,11 @@ __global__ void k_rmat_count(RmatParams p, uint64_t narcs, uint32_t* deg) {
 
 // Warp per (permuted) vertex: its list in CSR order, lanes strided over k.
 // vbase: global id of local vertex 0 (partition generation fills one range).
+// woff (optional): write list lv at woff[lv] instead of off[lv] (the out-arcs
+// of a symmetric partition's lists, whose in-arcs follow them).
 template <typename ET>
 __global__ void k_rmat_fill(RmatParams p, uint64_t nv, const uint64_t* off, ET* edges,
-                            uint64_t vbase = 0) {
+                            uint64_t vbase = 0, const uint64_t* woff = nullptr) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -157,11 +159,18 @@ __global__ void k_rmat_fill(RmatParams p, uint64_t nv, const uint64_t* off, ET* 
     if (s == e) continue;
     const uint64_t v = vbase + lv;
     const uint64_t src_old = p.perm.inv(v);
+    const uint64_t w0 = woff ? woff[lv] : s;
     for (uint64_t k = s + lane; k < e; k += 32) {
       const uint64_t d_old = rmat_dst(p, src_old, (v << 32) | (k - s));
-      edges[k] = static_cast<ET>(p.perm.fwd(d_old));
+      edges[w0 + (k - s)] = static_cast<ET>(p.perm.fwd(d_old));
     }
   }
+}
+
+__global__ void k_add_u32(uint64_t n, uint32_t* a, const uint32_t* b) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] += b[i];
 }
 
 // Symmetrize: sym list of x = out-list of x followed by the sources of its
@@ -489,14 +498,19 @@ RmatParams rmat_params(uint32_t scale, double a, double b, double c, uint64_t se
 
 // One edge-balanced vertex range of the directed R-MAT graph generate_rmat
 // would build with the same parameters (the same arcs, lists and order).
+// symmetrize: the part of the symmetrized graph (out-arcs + reverse arcs,
+// csr.py:350-359 semantics, lists sorted) -- every rank enumerates all arcs
+// for the global symmetric degrees (edge-balanced cuts) and for the reverse
+// arcs into its range; no edge exchange between ranks.
 int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c, uint64_t seed,
-                       int64_t wlow, int64_t whigh, uint32_t nparts, uint32_t part,
-                       int32_t placement, int32_t device, uint64_t* bounds, zc_graph** out) {
+                       int symmetrize, int64_t wlow, int64_t whigh, uint32_t nparts,
+                       uint32_t part, int32_t placement, int32_t device, uint64_t* bounds,
+                       zc_graph** out) {
   *out = nullptr;
   int rc = check_common(placement, device, wlow, whigh);
   if (rc) return rc;
   if (scale < 1 || scale > 31 || ef < 1 || a <= 0 || b < 0 || c < 0 || 1.0 - a - b - c < 0 ||
-      nparts < 1 || part >= nparts || !bounds) {
+      nparts < 1 || part >= nparts || !bounds || (symmetrize && wlow <= whigh)) {
     set_error("invalid rmat partition parameters");
     return ZC_EINVAL;
   }
@@ -526,18 +540,41 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
     ZC_CUDA_TRY(cudaDeviceSynchronize());
     t.release(tmp);
   }
+  // symmetric: degrees = out + in (every arc enumerated once more), offsets d_soff
+  uint64_t* d_soff = nullptr;
+  if (symmetrize) {
+    uint32_t* d_ideg = nullptr;
+    ZC_CUDA_TRY(cudaMalloc(&d_ideg, nv * sizeof(uint32_t)));
+    t.add(d_ideg);
+    ZC_CUDA_TRY(cudaMemset(d_ideg, 0, nv * sizeof(uint32_t)));
+    k_rmat_in_arcs<false><<<kGenGrid, 256>>>(p, nv, d_goff, 0, nv, d_ideg, nullptr, nullptr);
+    k_add_u32<<<kGenGrid, 256>>>(nv, d_deg, d_ideg);
+    ZC_CUDA_TRY(cudaGetLastError());
+    t.release(d_ideg);
+    ZC_CUDA_TRY(cudaMalloc(&d_soff, (nv + 1) * sizeof(uint64_t)));
+    t.add(d_soff);
+    const size_t tb = scan_tmp_bytes(nv);
+    void* tmp = nullptr;
+    ZC_CUDA_TRY(cudaMalloc(&tmp, tb));
+    t.add(tmp);
+    ZC_CUDA_TRY(scan_u32_to_u64(d_deg, d_soff, nv, tmp, tb, 0));
+    ZC_CUDA_TRY(cudaDeviceSynchronize());
+    t.release(tmp);
+  }
   t.release(d_deg);
+  const uint64_t* d_coff = symmetrize ? d_soff : d_goff;  // the partitioned graph's offsets
+  const uint64_t ctotal = symmetrize ? 2 * narcs : narcs;
   // edge-balanced bounds: first vertex whose offset reaches E*k/nparts
   std::vector<uint64_t> cut(nparts + 1);
   cut[0] = 0;
   cut[nparts] = nv;
   for (uint32_t k = 1; k < nparts; ++k) {
-    const uint64_t target = static_cast<uint64_t>(static_cast<double>(narcs) * k / nparts);
-    uint64_t lo = 0, hi = nv;  // smallest v with goff[v] >= target
+    const uint64_t target = static_cast<uint64_t>(static_cast<double>(ctotal) * k / nparts);
+    uint64_t lo = 0, hi = nv;  // smallest v with coff[v] >= target
     while (lo < hi) {
       const uint64_t mid = (lo + hi) / 2;
       uint64_t val = 0;
-      ZC_CUDA_TRY(cudaMemcpy(&val, d_goff + mid, sizeof(val), cudaMemcpyDeviceToHost));
+      ZC_CUDA_TRY(cudaMemcpy(&val, d_coff + mid, sizeof(val), cudaMemcpyDeviceToHost));
       if (val >= target) hi = mid; else lo = mid + 1;
     }
     cut[k] = std::max(lo, cut[k - 1]);
@@ -545,10 +582,10 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
   for (uint32_t k = 0; k <= nparts; ++k) bounds[k] = cut[k];
   const uint64_t lo = cut[part], hi = cut[part + 1], nl = hi - lo;
   uint64_t e0 = 0, e1 = 0;
-  ZC_CUDA_TRY(cudaMemcpy(&e0, d_goff + lo, sizeof(e0), cudaMemcpyDeviceToHost));
-  ZC_CUDA_TRY(cudaMemcpy(&e1, d_goff + hi, sizeof(e1), cudaMemcpyDeviceToHost));
+  ZC_CUDA_TRY(cudaMemcpy(&e0, d_coff + lo, sizeof(e0), cudaMemcpyDeviceToHost));
+  ZC_CUDA_TRY(cudaMemcpy(&e1, d_coff + hi, sizeof(e1), cudaMemcpyDeviceToHost));
 
-  zc_graph* g = new_handle(placement, device, ZC_F_DIRECTED);
+  zc_graph* g = new_handle(placement, device, symmetrize ? 0u : ZC_F_DIRECTED);
   GraphGuard guard{g};
   auto fail = [](int code) { return code; };
   g->nv = nl;
@@ -557,7 +594,7 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
     set_error("cannot allocate pinned offsets");
     return fail(ZC_ENOMEM);
   }
-  ZC_CUDA_TRY(cudaMemcpy(g->h_off, d_goff + lo, (nl + 1) * sizeof(uint64_t),
+  ZC_CUDA_TRY(cudaMemcpy(g->h_off, d_coff + lo, (nl + 1) * sizeof(uint64_t),
                          cudaMemcpyDeviceToHost));
   for (uint64_t v = 0; v <= nl; ++v) g->h_off[v] -= static_cast<int64_t>(e0);
   uint64_t* d_loff = nullptr;
@@ -573,8 +610,27 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
   }
   t.add(d_edges);
   ZC_CUDA_TRY(cudaMemcpy(d_loff, g->h_off, (nl + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice));
-  t.release(d_goff);
-  k_rmat_fill<uint32_t><<<kGenGrid, 256>>>(p, nl, d_loff, d_edges, lo);
+  if (symmetrize) {
+    // list x = its out-arcs (generator order), then the sources of its in-arcs
+    // (cursor from the out-degree), then sorted like generate_rmat's
+    uint32_t* d_cursor = nullptr;
+    ZC_CUDA_TRY(cudaMalloc(&d_cursor, std::max<uint64_t>(nl, 1) * sizeof(uint32_t)));
+    t.add(d_cursor);
+    k_rmat_fill<uint32_t><<<kGenGrid, 256>>>(p, nl, d_goff + lo, d_edges, lo, d_loff);
+    k_deg_from_off<<<kGenGrid, 256>>>(nl, d_goff + lo, d_cursor);
+    k_rmat_in_arcs<true><<<kGenGrid, 256>>>(p, nv, d_goff, lo, nl, d_cursor, d_loff, d_edges);
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+      set_error(std::string("rmat symmetric part: ") + cudaGetErrorString(cudaGetLastError()));
+      return fail(ZC_ECUDA);
+    }
+    t.release(d_cursor);
+    t.release(d_soff);
+    t.release(d_goff);
+    if ((rc = sort_lists<uint32_t>(nl, d_loff, g->h_off, d_edges))) return fail(rc);
+  } else {
+    t.release(d_goff);
+    k_rmat_fill<uint32_t><<<kGenGrid, 256>>>(p, nl, d_loff, d_edges, lo);
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) {
     set_error(std::string("rmat fill: ") + cudaGetErrorString(cudaGetLastError()));
     return fail(ZC_ECUDA);
@@ -830,12 +886,13 @@ extern "C" int zc_generate_uniform(uint64_t num_vertices, uint32_t min_degree, u
 }
 
 extern "C" int zc_generate_rmat_part(uint32_t scale, uint32_t edge_factor, double a, double b,
-                                     double c, uint64_t seed, int64_t wlow, int64_t whigh,
-                                     uint32_t nparts, uint32_t part, int32_t placement,
-                                     int32_t device, uint64_t* bounds, zc_graph** out) {
+                                     double c, uint64_t seed, int symmetrize, int64_t wlow,
+                                     int64_t whigh, uint32_t nparts, uint32_t part,
+                                     int32_t placement, int32_t device, uint64_t* bounds,
+                                     zc_graph** out) {
   if (!out) return ZC_ESTATE;
-  return zc::generate_rmat_part(scale, edge_factor, a, b, c, seed, wlow, whigh, nparts, part,
-                                placement, device, bounds, out);
+  return zc::generate_rmat_part(scale, edge_factor, a, b, c, seed, symmetrize, wlow, whigh, nparts,
+                                part, placement, device, bounds, out);
 }
 
 extern "C" int zc_part_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) {

@@ -125,6 +125,7 @@ struct zc_graph {
   void* d_mine = nullptr;
   void** d_peers = nullptr;
   uint32_t* d_sent = nullptr;  // BFS: discoveries already sent this iteration
+  void* d_lbest = nullptr;     // SSSP / CC: best candidate sent per global vertex this iteration
   std::vector<void*> ipc_opened;
   int fused_algo = -1;
   // pipelined results (zc_bfs_async / zc_sssp_async / zc_sync): two int64
@@ -142,6 +143,7 @@ struct zc_graph {
   // stepped run state (zc_part_begin / expand / apply)
   int p_algo = -1, p_strategy = 0, p_cur = 0;
   uint64_t p_iter = 0, p_n = 0, p_launches = 0;
+  uint64_t p_xbytes = 0;  // exchange bytes this rank sent since zc_part_begin
 };
 
 

@@ -132,6 +132,8 @@ enum Ctr : int {
   kCtrCur = 16,      // device level loop: size of the current frontier
   kCtrIter = 17,     //   completed iterations
   kCtrLoaded = 18,   // compressed sweeps: bytes requested from the line streams
+  kCtrVisited = 19,  // union-find sweeps: list elements actually read (afforest pass 1)
+  kCtrRemote = 20,   // fused partitions: remote destinations sent to (launch_count_remote)
   kCtrFarMin = 22,   // near-far SSSP: smallest distance in the far pile
   kCtrFar = 23,      //   vertices in the far pile
   kCtrCount = 24
@@ -165,6 +167,9 @@ struct ExpandArgs {
   // `sent` dedups BFS discoveries per iteration (global V bits)
   void* const* peers;
   uint32_t* sent;
+  // fused SSSP / CC: this rank's best candidate per global vertex this
+  // iteration (u64 / u32, all ones = none); only improvements go to the owner
+  void* lbest;
   // CTA-sweep scheduling: per-slot window counts, their exclusive prefix
   uint32_t* wcnt;
   uint64_t* wpre;  // n + 1
@@ -242,6 +247,13 @@ cudaError_t launch_fill_exchange(int algo, void* x, uint64_t n, cudaStream_t st,
                                  uint64_t* launches);
 cudaError_t launch_part_apply(int algo, const void* mine, uint64_t nlocal, void* state,
                               uint8_t* flags, uint32_t iter, cudaStream_t st, uint64_t* launches);
+// Fused exchange accounting: how many global vertices outside [lo, hi) this
+// rank sent a candidate to this iteration -- set bits of the BFS `sent`
+// bitmap (elem_bytes 0) or entries of `lbest` other than all-ones (4 / 8) --
+// added to *out (device).
+cudaError_t launch_count_remote(const void* x, int elem_bytes, uint64_t global_nv, uint64_t lo,
+                                uint64_t hi, uint64_t* out, int num_sms, cudaStream_t st,
+                                uint64_t* launches);
 // Frontier bitmap over global ids: zero `words` words, set vbase + front[j].
 cudaError_t launch_frontier_bits(const uint32_t* front, uint64_t n, uint64_t vbase,
                                  uint32_t* bits, uint64_t words, int num_sms, cudaStream_t st,

@@ -256,14 +256,30 @@ struct Visit<kBfs + kPartAlgo> {
   }
 };
 
+// Fused mode sends a candidate to its owner only when it improves this rank's
+// best for w this iteration (local pre-filter in HBM): the owner still gets
+// every rank's minimum, with one remote reduction per improvement instead of
+// one per edge.
+template <typename T>
+__device__ __forceinline__ bool improves_local(const ExpandArgs& a, uint64_t w, T cand) {
+  if (!a.lbest) return true;
+  T* lb = static_cast<T*>(a.lbest) + w;
+  if (cand >= *lb) return false;
+  return cand < atomicMin(lb, cand);
+}
+
 template <>
 struct Visit<kSssp + kPartAlgo> {
   static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t wt,
                                                uint64_t val) {
-    unsigned long long* x = cand_slot<unsigned long long>(a, w);
     const unsigned long long cand = val + wt;
-    if (a.peers) atomicMin(x, cand);  // remote: reduction, no read-back
-    else if (cand < *x) atomicMin(x, cand);
+    if (a.peers) {  // remote: reduction, no read-back
+      if (improves_local<unsigned long long>(a, w, cand))
+        atomicMin(cand_slot<unsigned long long>(a, w), cand);
+      return;
+    }
+    unsigned long long* x = cand_slot<unsigned long long>(a, w);
+    if (cand < *x) atomicMin(x, cand);
   }
 };
 
@@ -271,10 +287,13 @@ template <>
 struct Visit<kCc + kPartAlgo> {
   static __device__ __forceinline__ void apply(const ExpandArgs& a, uint64_t w, uint64_t,
                                                uint64_t val) {
-    unsigned* x = cand_slot<unsigned>(a, w);
     const unsigned cand = static_cast<unsigned>(val);
-    if (a.peers) atomicMin(x, cand);
-    else if (cand < *x) atomicMin(x, cand);
+    if (a.peers) {
+      if (improves_local<unsigned>(a, w, cand)) atomicMin(cand_slot<unsigned>(a, w), cand);
+      return;
+    }
+    unsigned* x = cand_slot<unsigned>(a, w);
+    if (cand < *x) atomicMin(x, cand);
   }
 };
 
@@ -578,8 +597,8 @@ __device__ __forceinline__ uint32_t line_bits(const uint32_t* L, uint32_t bit, u
 // lane l takes elements [l m, l m + m), m = ceil(count / 32); values are the
 // base plus a warp prefix sum of the deltas (u32 exact: ids < 2^32).
 template <int ALGO>
-__device__ __forceinline__ void visit_line(const ExpandArgs& a, uint32_t x, uint64_t sval,
-                                           uint32_t* L, int lane) {
+__device__ __forceinline__ uint32_t visit_line(const ExpandArgs& a, uint32_t x, uint64_t sval,
+                                               uint32_t* L, int lane) {
   L[lane] = x;
   if (lane < 2) L[kLineWords + lane] = 0;
   __syncwarp();
@@ -605,6 +624,7 @@ __device__ __forceinline__ void visit_line(const ExpandArgs& a, uint32_t x, uint
     Visit<ALGO>::apply(a, val, wt, sval);
   }
   __syncwarp();
+  return e1 > e0 ? e1 - e0 : 0u;  // elements this lane visited
 }
 
 // Decode the short lists of staged slots [k0, k1) from their shared line
@@ -612,7 +632,7 @@ __device__ __forceinline__ void visit_line(const ExpandArgs& a, uint32_t x, uint
 // in [k0, k1) is in the frontier; empty lists take no bits, so there can be
 // more than 32 of them.
 template <int ALGO>
-__device__ __forceinline__ void visit_short(const ExpandArgs& a, uint32_t x, uint32_t x2, int k0,
+__device__ __forceinline__ uint32_t visit_short(const ExpandArgs& a, uint32_t x, uint32_t x2, int k0,
                                             int k1, const uint64_t* sh_c, const uint64_t* sh_s,
                                             const uint64_t* sh_e, const uint64_t* sh_v,
                                             uint32_t* L, int lane) {
@@ -620,6 +640,7 @@ __device__ __forceinline__ void visit_short(const ExpandArgs& a, uint32_t x, uin
   L[kLineWords + lane] = x2;
   if (lane < 2) L[kShortSpanWords + lane] = 0;
   __syncwarp();
+  uint32_t seen = 0;  // elements this lane visited
   // more than 32 staged slots can share a line when empty lists sit between
   for (int i = k0 + lane; i < k1; i += 32) {
     const uint32_t d = static_cast<uint32_t>(sh_e[i] - sh_s[i]);
@@ -636,9 +657,11 @@ __device__ __forceinline__ void visit_short(const ExpandArgs& a, uint32_t x, uin
       uint64_t wt = 0;
       if constexpr (AlgoTraits<ALGO>::weighted) wt = a.cmp_wmin + line_bits(L, wb + e * a.cmp_ww, a.cmp_ww);
       Visit<ALGO>::apply(a, val, wt, sval);
+      ++seen;
     }
   }
   __syncwarp();
+  return seen;
 }
 
 template <int STRAT, int ALGO, typename ET, typename WT, int U, int LD = DefaultLd<STRAT>::value>
@@ -684,6 +707,7 @@ __global__ void __launch_bounds__(kSweepThreads, SweepMinBlocks<STRAT, ALGO>::va
   uint64_t j = sh_j;
   uint64_t W = Wb;
   uint64_t words = 0;  // compressed: 4-byte words this warp requested (warp-uniform)
+  uint64_t seen = 0;   // union-find: list elements this thread visited
   while (W < We) {
     // stage slots [j, j + kStage)
     for (int i = threadIdx.x; i <= kStage; i += kSweepThreads) {
@@ -778,6 +802,7 @@ __global__ void __launch_bounds__(kSweepThreads, SweepMinBlocks<STRAT, ALGO>::va
             idx = window_base<STRAT, ET>(s0) + (q - sh_w[k]) * kWarp + lane;
             bt.ok[u] = idx >= s0 && idx < e0;
           }
+          if constexpr (ALGO == kCcUf) seen += bt.ok[u];
           if (bt.ok[u]) {
             bt.dst[u] = ld_list_f<LD>(E + idx);
             if constexpr (AlgoTraits<ALGO>::weighted && !IsPair<WT>::value)
@@ -798,11 +823,12 @@ __global__ void __launch_bounds__(kSweepThreads, SweepMinBlocks<STRAT, ALGO>::va
 #pragma unroll
           for (int u = 0; u < U; ++u) {  // line kinds are warp-uniform
             if (cur.line[u] == 1)
-              visit_line<ALGO>(a, static_cast<uint32_t>(cur.dst[u]), cur.sval[u], sh_line[warp],
-                               lane);
+              seen += visit_line<ALGO>(a, static_cast<uint32_t>(cur.dst[u]), cur.sval[u],
+                                       sh_line[warp], lane);
             else if (cur.line[u] == 2)
-              visit_short<ALGO>(a, static_cast<uint32_t>(cur.dst[u]), cur.dst2[u], cur.k0[u],
-                                cur.k1[u], sh_c, sh_s, sh_e, sh_v, sh_line[warp], lane);
+              seen += visit_short<ALGO>(a, static_cast<uint32_t>(cur.dst[u]), cur.dst2[u],
+                                        cur.k0[u], cur.k1[u], sh_c, sh_s, sh_e, sh_v,
+                                        sh_line[warp], lane);
           }
         } else {
           visit_batch<ALGO, ET, WT, U, kCmp>(a, cur);
@@ -813,6 +839,16 @@ __global__ void __launch_bounds__(kSweepThreads, SweepMinBlocks<STRAT, ALGO>::va
     __syncthreads();
     W = Wend;
     j += kStage;
+  }
+  if constexpr (ALGO == kCcUf) {  // elements read (the sampling pass reads part of each list)
+    __shared__ unsigned long long sh_seen;
+    if (threadIdx.x == 0) sh_seen = 0;
+    __syncthreads();
+    for (int o = 16; o; o >>= 1) seen += __shfl_xor_sync(kFull, seen, o);
+    if (lane == 0 && seen) atomicAdd(&sh_seen, static_cast<unsigned long long>(seen));
+    __syncthreads();
+    if (threadIdx.x == 0 && sh_seen)
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.ctr + kCtrVisited), sh_seen);
   }
   if constexpr (kCmp) {  // link bytes requested: one atomic per CTA
     __shared__ unsigned long long sh_words;
@@ -1896,6 +1932,46 @@ cudaError_t launch_init(int algo, void* state, uint64_t nv, uint64_t src, const 
   cudaError_t e = cudaMemsetAsync(state, 0xff, bytes, st);
   if (e != cudaSuccess || !with_source) return e;
   k_init_source<<<1, 1, 0, st>>>(src, off, front, fval, fs, fd);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+// elem_bytes 0: x is a bitmap of global ids (count set bits); 4 / 8: an
+// array (count entries other than all-ones); only ids outside [lo, hi).
+__global__ void k_count_remote(const void* x, int eb, uint64_t n, uint64_t lo, uint64_t hi,
+                               unsigned long long* out) {
+  unsigned long long c = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  if (eb == 0) {
+    const uint32_t* b = static_cast<const uint32_t*>(x);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (n + 31) / 32;
+         i += stride) {
+      uint32_t m = b[i];
+      const uint64_t v0 = i * 32;
+      if (v0 + 32 > lo && v0 < hi) {  // clear the owned ids of this word
+        const uint64_t a0 = max(lo, v0) - v0, a1 = min(hi, v0 + 32) - v0;
+        const uint32_t own = (a1 - a0 == 32) ? 0xffffffffu : (((1u << (a1 - a0)) - 1u) << a0);
+        m &= ~own;
+      }
+      c += __popc(m);
+    }
+  } else {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+      if (i >= lo && i < hi) continue;
+      c += eb == 4 ? static_cast<const uint32_t*>(x)[i] != 0xffffffffu
+                   : static_cast<const unsigned long long*>(x)[i] != ~0ull;
+    }
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+cudaError_t launch_count_remote(const void* x, int elem_bytes, uint64_t global_nv, uint64_t lo,
+                                uint64_t hi, uint64_t* out, int num_sms, cudaStream_t st,
+                                uint64_t* launches) {
+  if (global_nv == 0) return cudaSuccess;
+  k_count_remote<<<num_sms * 8, 256, 0, st>>>(x, elem_bytes, global_nv, lo, hi,
+                                               reinterpret_cast<unsigned long long*>(out));
   *launches += 1;
   return cudaGetLastError();
 }

@@ -213,8 +213,15 @@ class CudaPartition:
 
     def launches(self) -> int:
         """Kernels launched since the last begin (this rank)."""
+        return self.run_stats()["launches"]
+
+    def run_stats(self) -> dict:
+        """This rank's counters since the last begin: kernel launches, the
+        expansion kernels' device time, and the exchange bytes it sent
+        (reduce-scatter share, or fused remote sends)."""
         N.check(N.lib().zc_part_result(self._h, None, C.byref(self.stats)))
-        return int(self.stats.launches)
+        return {"launches": int(self.stats.launches), "expand_ms": float(self.stats.expand_ms),
+                "exchange_bytes": int(self.stats.exchange_bytes)}
 
     def result(self) -> np.ndarray:
         from .device import pinned_empty
@@ -225,16 +232,20 @@ class CudaPartition:
 
 def generate_rmat_part(scale: int, nparts: int, part: int, edge_factor: int = 16,
                        a: float = 0.57, b: float = 0.19, c: float = 0.19, seed: int = 27, *,
-                       weights=None, placement: str = "zerocopy", device: int = 0
-                       ) -> CudaPartition:
-    """This rank's edge-balanced part of generate_rmat(scale, ...) (same arcs),
-    generated on the GPU straight into a partition handle."""
+                       symmetrize: bool = False, weights=None, placement: str = "zerocopy",
+                       device: int = 0) -> CudaPartition:
+    """This rank's edge-balanced part of generate_rmat(scale, ..., symmetrize)
+    (same arcs, same sorted lists when symmetrized), generated on the GPU
+    straight into a partition handle: every rank enumerates the counter-based
+    arcs itself, so no edges move between ranks."""
+    if symmetrize and weights is not None:
+        raise ValueError("symmetrized partitions carry no weights")
     lo, hi = weights if weights is not None else (1, 0)
     bounds = np.zeros(nparts + 1, np.uint64)
     h = C.c_void_p()
-    N.check(N.lib().zc_generate_rmat_part(scale, edge_factor, a, b, c, seed, lo, hi, nparts, part,
-                                          N.PLACEMENTS[placement], device, bounds.ctypes.data,
-                                          C.byref(h)))
+    N.check(N.lib().zc_generate_rmat_part(scale, edge_factor, a, b, c, seed, int(bool(symmetrize)),
+                                          lo, hi, nparts, part, N.PLACEMENTS[placement], device,
+                                          bounds.ctypes.data, C.byref(h)))
     return CudaPartition(None, bounds, part, placement, device, _handle=h.value)
 
 
@@ -248,6 +259,10 @@ class PartResult:
     iterations: int             # global (same on every rank)
     traversed_edges: list       # global, summed over ranks
     frontier_sizes: list = field(default_factory=list)  # global
+    local_traversed: int = 0    # edges this rank streamed over its own host link
+    expand_ms: float = 0.0      # this rank's expansion kernels (device time)
+    exchange_bytes: int = 0     # bytes this rank sent: candidates + frontier bitmaps
+    bottom_up_steps: int = 0
 
     @property
     def total_traversed_edges(self) -> int:
@@ -289,7 +304,10 @@ def run_partition(engine: Engine, algo: str, source: int, strategy, *, group=Non
     counts = torch.zeros(3, dtype=torch.int64, device=cdev)
     dobfs = is_direction_optimizing(strategy)
 
+    local = [0, 0, 0]  # edges streamed by this rank, bitmap all-reduce bytes, bottom-up steps
+
     def global_counts(n: int, t: int) -> tuple[int, int, int]:
+        local[0] += t
         counts[0], counts[1] = n, t
         counts[2] = engine.unvisited_in() if dobfs else 0
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
@@ -297,6 +315,8 @@ def run_partition(engine: Engine, algo: str, source: int, strategy, *, group=Non
 
     def pull_step():
         # the owned frontiers' disjoint bits, OR-ed by a SUM all-reduce
+        local[1] += allreduce_send_bytes(engine.bitmap_words * 4, nparts)
+        local[2] += 1
         bits = torch.empty(engine.bitmap_words, dtype=torch.int32, device=dev)
         engine.frontier_bits(bits)
         if stage_host:
@@ -329,7 +349,23 @@ def run_partition(engine: Engine, algo: str, source: int, strategy, *, group=Non
             torch.cuda.current_stream(dev).synchronize()
         n, t, m = global_counts(*engine.apply(mine))
     values = engine.result() if fetch else None
-    return PartResult(algo, engine.lo, values, iters, trav, front)
+    return _finish(PartResult(algo, engine.lo, values, iters, trav, front), engine, local)
+
+
+def allreduce_send_bytes(nbytes: int, nparts: int) -> int:
+    """Bytes one rank sends in a ring all-reduce of nbytes."""
+    return 2 * (nparts - 1) * nbytes // max(nparts, 1)
+
+
+def _finish(res: PartResult, engine, local) -> PartResult:
+    """Attach this rank's counters: traversed edges of the frontiers it owned
+    (the reference's work units), expansion time, exchange bytes sent."""
+    res.local_traversed = local[0]
+    stats = engine.run_stats() if hasattr(engine, "run_stats") else {}
+    res.expand_ms = stats.get("expand_ms", 0.0)
+    res.exchange_bytes = stats.get("exchange_bytes", 0) + local[1]
+    res.bottom_up_steps = local[2]
+    return res
 
 
 def is_direction_optimizing(strategy) -> bool:
@@ -354,10 +390,14 @@ def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartRe
     import torch.distributed as dist
 
     dev = torch.device("cuda", engine.device)
-    handle, local = engine.fused_init(algo)
-    handles = [None] * dist.get_world_size(group)
-    dist.all_gather_object(handles, handle, group=group)
-    engine.fused_connect(handles=handles)
+    if getattr(engine, "_fused_for", None) == algo:  # peers opened by an earlier run
+        mine = engine._fused_mine
+    else:  # once per (engine, algorithm): export, exchange and open the IPC handles
+        handle, mine = engine.fused_init(algo)
+        handles = [None] * dist.get_world_size(group)
+        dist.all_gather_object(handles, handle, group=group)
+        engine.fused_connect(handles=handles)
+        engine._fused_for, engine._fused_mine = algo, mine
     cdev = torch.device("cpu") if dist.get_backend(group) == "gloo" else dev
     counts = torch.zeros(2, dtype=torch.int64, device=cdev)
 
@@ -367,15 +407,13 @@ def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartRe
         if cdev.type == "cuda":
             torch.cuda.current_stream(dev).synchronize()
 
-    def global_counts(n: int, t: int) -> tuple[int, int]:
-        counts[0], counts[1] = n, t
-        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
-        return int(counts[0]), int(counts[1])
-
     dobfs = is_direction_optimizing(strategy)
     counts3 = torch.zeros(3, dtype=torch.int64, device=cdev)
+    nparts = dist.get_world_size(group)
+    local = [0, 0, 0]
 
     def global_counts3(n: int, t: int) -> tuple[int, int, int]:
+        local[0] += t
         counts3[0], counts3[1] = n, t
         counts3[2] = engine.unvisited_in() if dobfs else 0
         dist.all_reduce(counts3, op=dist.ReduceOp.SUM, group=group)
@@ -388,6 +426,8 @@ def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartRe
         trav.append(t)
         front.append(n)
         if dobfs and pull_now(iters, t, m):
+            local[1] += allreduce_send_bytes(engine.bitmap_words * 4, nparts)
+            local[2] += 1
             bits = torch.empty(engine.bitmap_words, dtype=torch.int32, device=dev)
             engine.frontier_bits(bits)
             hb = bits.cpu() if cdev.type == "cpu" else bits
@@ -401,9 +441,9 @@ def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartRe
         sync_all()              # every owner buffer reset before anyone writes
         engine.fused_expand()   # kernel done (its peer stores performed) on return
         sync_all()              # every rank's candidates delivered
-        n, t, m = global_counts3(*engine.apply_ptr(local))
+        n, t, m = global_counts3(*engine.apply_ptr(mine))
     values = engine.result() if fetch else None
-    return PartResult(algo, engine.lo, values, iters, trav, front)
+    return _finish(PartResult(algo, engine.lo, values, iters, trav, front), engine, local)
 
 
 def exchange_buffers(algo: str, nparts: int, stride: int, device):

@@ -304,6 +304,38 @@ def test_rmat_partition_generator_matches_whole_graph():
         assert trav == ref.traversed_edges
 
 
+def test_symmetric_rmat_partition_generator_matches_whole_graph():
+    """Partitions of the symmetrized R-MAT graph (every rank enumerates the
+    reverse arcs into its range): the whole graph's slices, edge-balanced over
+    its 2E arcs; BFS and CC over them (both exchanges) equal the oracle."""
+    whole = zc.generate_rmat(15, 16, seed=5, symmetrize=True)
+    g = whole.as_csr()  # views of the handle's pinned lists: closed at the end
+    src = int(zc.pick_sources(g, 1, seed=7)[0])
+    for nparts in (1, 2, 3):
+        parts = [generate_rmat_part(15, nparts, k, seed=5, symmetrize=True)
+                 for k in range(nparts)]
+        b = parts[0].bounds
+        assert np.array_equal(b, edge_balanced_bounds(g.offsets, nparts))
+        for k, p in enumerate(parts):
+            ref = local_part(g, b, k)
+            got = p.graph_view()
+            assert not got.directed
+            assert np.array_equal(got.offsets, ref.offsets)
+            assert np.array_equal(np.asarray(got.edges), np.asarray(ref.edges))
+        for algo in ("bfs", "cc"):
+            ref = oracle.run(algo, g, src, threads=8)
+            for fused in (False, True):
+                vals, iters, trav = run_partitions_local(parts, algo, src, "merged-aligned",
+                                                         fused=fused)
+                assert np.array_equal(vals, ref.values), (nparts, algo, fused)
+                assert iters == ref.iterations and trav == ref.traversed_edges
+        for p in parts:
+            p.close()
+    with pytest.raises(ValueError):
+        generate_rmat_part(10, 2, 0, symmetrize=True, weights=(1, 5))
+    whole.close()
+
+
 def test_pagerank_matches_reference():
     """Reference pagerank outputs (incl. acceptance criterion 6's PR stream):
     L-inf <= 1e-8 (test_acceptance.py:169-180), the same iteration count (the
@@ -713,7 +745,8 @@ def test_work_efficient_schedules_match_reference_values(strategy):
     bad = []
     for c in CASES:
         if c.algo == "sssp":
-            if strategy == "compressed" and c.graph.weight_elem_bytes != 4:
+            if strategy == "compressed" and (c.graph.edge_elem_bytes != 4
+                                             or c.graph.weight_elem_bytes != 4):
                 continue
             for delta in (1, 7, 32, 1000):
                 r = zc.sssp(c.graph, c.source, strategy, schedule="near-far", delta=delta)
@@ -735,10 +768,21 @@ def test_work_efficient_schedules_rmat():
         k = zc.generate_rmat(scale, 16, seed=seed, symmetrize=True)
         gk = k.as_csr()
         ref = oracle.cc(gk, threads=8)
+        off = np.asarray(gk.offsets, dtype=np.int64)
+        st, en = off[:-1], off[1:]
+        first = {"merged": np.minimum(en - st, 32).sum(),  # the sampling pass's first windows
+                 "merged-aligned": (np.minimum(en, (st & ~31) + 32) - st).clip(0).sum()}
+        first["packed"] = first["merged-aligned"]
         for s in SCHED_STRATS:
             r = zc.cc(k, s, schedule="afforest")
             assert np.array_equal(r.values, ref.values), (scale, s)
             assert r.iterations <= 2 and r.total_traversed_edges <= 2 * gk.num_edges
+            if s in first:  # elements actually read, counted on the device
+                assert r.traversed_edges[0] == first[s], (scale, s)
+            elif s == "naive":
+                assert r.traversed_edges[0] == gk.num_edges
+            else:
+                assert r.traversed_edges[0] < gk.num_edges
         k.close()
     u = zc.generate_uniform_device(1 << 17, 16, 16, seed=5, weights=(8, 72))
     gu = u.as_csr()
