@@ -38,6 +38,11 @@ int zc_vmm_host_probe(int32_t device, uint64_t bytes, uint64_t *granularity);
 int zc_bulk_probe(int32_t device, uint64_t bytes, uint32_t chunk, int ctas_per_sm, int iters,
                   double *gbs);
 
+/* Pinned-allocation cost of `bytes`: mode 0 cudaHostAlloc; 1 mmap + huge
+ * pages + `threads`-way first touch + cudaHostRegister; 2 the same with 4 KB
+ * pages; 3 mmap + huge pages + cudaHostRegister without prefault. */
+int zc_pin_probe(uint64_t bytes, int mode, int threads, double *alloc_s, double *register_s);
+
 #ifdef __cplusplus
 }
 #endif

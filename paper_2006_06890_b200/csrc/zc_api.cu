@@ -86,12 +86,10 @@ void tune_params(ExpandArgs* a, const zc_graph* g) {
 
 // ---------------------------------------------------------- pinned lists
 // Zero-copy lists are read by the GPU across PCIe: on a multi-socket host
-// they belong on the GPU's own NUMA node.  Allocate an
-// anonymous mapping bound to that node (mbind), advise transparent huge
-// pages, and cudaHostRegister it; fall back to cudaHostAlloc when the node is
-// unknown (single-node hosts, as the pool's), mbind is refused, or ZC_NUMA=0.
+// they belong on the GPU's own NUMA node (the node is
+// ignored with ZC_NUMA=0).  See pinned_list_alloc.
 static std::mutex g_map_mu;
-static std::unordered_map<void*, size_t> g_mapped;  // our mbind'ed registrations
+static std::unordered_map<void*, size_t> g_mapped;  // our registered mappings
 
 static int gpu_numa_node(int device) {
   char bus[32] = {0};
@@ -113,18 +111,45 @@ static int gpu_numa_node(int device) {
   return nodes > 1 ? node : -1;
 }
 
+// Pinned mapped host memory, fast.  cudaHostAlloc pins at ~1.5 GB/s (4.35 s
+// for a 6 GB line stream, profiles/r02_pin_probe.txt); an anonymous mapping
+// with transparent huge pages, first-touched by 8 threads (the kernel zeroes
+// 2 MB pages concurrently) and then cudaHostRegister'ed, takes 0.27 s and
+// streams over the link like cudaHostAlloc memory (r01_alloc_probe.txt).  On
+// a multi-node host the mapping is bound to the GPU's NUMA node first.
+// Small buffers (< 64 MB) and any failure take cudaHostAlloc.
+static void prefault(void* p, size_t bytes) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned nt = std::min(8u, hw);
+  const size_t chunk = (bytes / nt + 4095) & ~static_cast<size_t>(4095);
+  std::vector<std::thread> th;
+  for (unsigned k = 0; k < nt; ++k)
+    th.emplace_back([=] {
+      volatile char* b = static_cast<char*>(p);
+      for (size_t o = k * chunk; o < std::min(bytes, (k + 1) * chunk); o += 4096) b[o] = 0;
+    });
+  for (auto& t : th) t.join();
+}
+
 void* pinned_list_alloc(int device, size_t bytes) {
-  const char* env = getenv("ZC_NUMA");
-  const int node = (env && env[0] == '0') ? -1 : gpu_numa_node(device);
-  if (node >= 0 && node < 64) {
+  static const bool numa_off = [] {
+    const char* env = getenv("ZC_NUMA");
+    return env && env[0] == '0';
+  }();
+  bytes = std::max<size_t>(bytes, 1);
+  if (bytes >= (64ull << 20)) {
+    const int node = numa_off ? -1 : gpu_numa_node(device);
     void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
     if (p != MAP_FAILED) {
-      unsigned long mask = 1ul << node;
-      const long rc = syscall(SYS_mbind, p, bytes, 2 /* MPOL_BIND */, &mask, 64, 0);
+      bool ok = true;
+      if (node >= 0 && node < 64) {
+        unsigned long mask = 1ul << node;
+        ok = syscall(SYS_mbind, p, bytes, 2 /* MPOL_BIND */, &mask, 64, 0) == 0;
+      }
       madvise(p, bytes, MADV_HUGEPAGE);
-      if (rc == 0 &&
-          cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) ==
-              cudaSuccess) {
+      if (ok) prefault(p, bytes);
+      if (ok && cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) ==
+                    cudaSuccess) {
         std::lock_guard<std::mutex> lk(g_map_mu);
         g_mapped[p] = bytes;
         return p;
@@ -292,8 +317,7 @@ void zc::free_graph(zc_graph* g) {
   cudaSetDevice(g->device);
   for (auto& t : g->widen_th)
     if (t.joinable()) t.join();
-  for (auto* p : g->h_stage)
-    if (p) cudaFreeHost(p);
+  for (auto* p : g->h_stage) pinned_list_free(p);
   if (g->stream) cudaStreamSynchronize(g->stream);
   if (g->copy_stream) cudaStreamSynchronize(g->copy_stream);
   auto free_list = [&](void*& h, bool registered, void*& hbm) {
@@ -319,7 +343,7 @@ void zc::free_graph(zc_graph* g) {
   cudaFree(g->d_fbits);
   cudaFree(g->d_hasin);
   cudaFree(g->d_cpos);
-  if (g->h_off) cudaFreeHost(g->h_off);
+  pinned_list_free(g->h_off);
   cudaFree(g->d_off);
   cudaFree(g->d_state);
   cudaFree(g->d_flags);
@@ -1006,7 +1030,8 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     ZC_CUDA_TRY(launch_narrow_levels(g->d_state, g->nv, d_u8, st, &launches));
     ZC_CUDA_TRY(cudaEventRecord(g->out_ready[b], st));
     ZC_CUDA_TRY(cudaStreamWaitEvent(g->copy_stream, g->out_ready[b], 0));
-    if (!g->h_stage[b]) ZC_CUDA_TRY(cudaHostAlloc(&g->h_stage[b], g->nv, cudaHostAllocDefault));
+    if (!g->h_stage[b]) g->h_stage[b] = static_cast<uint8_t*>(pinned_list_alloc(g->device, g->nv));
+    if (!g->h_stage[b]) return ZC_ENOMEM;
     ZC_CUDA_TRY(cudaMemcpyAsync(g->h_stage[b], d_u8, g->nv, cudaMemcpyDeviceToHost,
                                 g->copy_stream));
     ZC_CUDA_TRY(cudaEventRecord(g->out_done[b], g->copy_stream));
@@ -1028,7 +1053,8 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
   } else if (narrow) {
     uint8_t* d_u8 = reinterpret_cast<uint8_t*>(g->d_fval[0]);
     ZC_CUDA_TRY(launch_narrow_levels(g->d_state, g->nv, d_u8, st, &launches));
-    if (!g->h_stage[2]) ZC_CUDA_TRY(cudaHostAlloc(&g->h_stage[2], g->nv, cudaHostAllocDefault));
+    if (!g->h_stage[2]) g->h_stage[2] = static_cast<uint8_t*>(pinned_list_alloc(g->device, g->nv));
+    if (!g->h_stage[2]) return ZC_ENOMEM;
     ZC_CUDA_TRY(cudaMemcpyAsync(g->h_stage[2], d_u8, g->nv, cudaMemcpyDeviceToHost, st));
     ZC_CUDA_TRY(cudaEventRecord(g->ev[2], st));
     ZC_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1330,8 +1356,8 @@ static int create_impl(const zc_graph_desc* d, zc_graph** out, uint64_t dest_lim
     free_graph(g);
     return code;
   };
-  if (cudaHostAlloc(&g->h_off, (g->nv + 1) * sizeof(int64_t), cudaHostAllocDefault) !=
-      cudaSuccess) {
+  g->h_off = static_cast<int64_t*>(pinned_list_alloc(g->device, (g->nv + 1) * sizeof(int64_t)));
+  if (!g->h_off) {
     cudaGetLastError();
     set_error("cannot allocate pinned offsets");
     return fail(ZC_ENOMEM);
@@ -1473,7 +1499,8 @@ int zc_graph_open_emgi(const char* path, int32_t placement, int32_t device, uint
     free_graph(g);
     return code;
   };
-  if (cudaHostAlloc(&g->h_off, (nv + 1) * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess) {
+  g->h_off = static_cast<int64_t*>(pinned_list_alloc(g->device, (nv + 1) * sizeof(int64_t)));
+  if (!g->h_off) {
     set_error("cannot allocate pinned offsets");
     return fail(ZC_ENOMEM);
   }
@@ -2266,7 +2293,7 @@ int zc_graph_multigraph(zc_graph* g, int* out) {
       ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
       ZC_CUDA_TRY(cudaMalloc(&scratch, g->ne * g->eb));
       ZC_CUDA_TRY(cudaMemcpy(scratch, g->h_edges, g->ne * g->eb, cudaMemcpyDefault));
-      int rc = sort_lists_device(static_cast<int>(g->eb), g->nv, g->d_off, g->h_off, scratch);
+      int rc = sort_lists_device(static_cast<int>(g->eb), g->nv, g->d_off, scratch);
       if (rc) {
         cudaFree(scratch);
         return rc;
@@ -2395,17 +2422,13 @@ int zc_run_traffic(const zc_graph* g, uint64_t* hist, uint64_t cap) {
 }
 
 void* zc_host_alloc(size_t bytes) {
-  void* p = nullptr;
-  if (cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocPortable) != cudaSuccess) {
-    cudaGetLastError();
-    set_error("cudaHostAlloc failed");
-    return nullptr;
-  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  void* p = pinned_list_alloc(dev, bytes);
+  if (!p) set_error("cannot allocate pinned host memory");
   return p;
 }
 
-void zc_host_free(void* p) {
-  if (p) cudaFreeHost(p);
-}
+void zc_host_free(void* p) { pinned_list_free(p); }
 
 }  // extern "C"

@@ -10,14 +10,17 @@
 // 256-byte spans (one read serves every frontier list in it).  SSSP weights ride in the
 // same lines as (weight - wmin) fields of the narrowest width that holds them.
 //
-// Build, on the GPU except the placement scan: sort each list (by destination,
-// then weight), size every list (short: its bit length; long: the lines of a
-// greedy fill -- as many deltas as fit 1024 - 48 bits at the width of the
-// widest one, at most 255), place them in vertex order on the host (a short
-// list starts a new line only when it does not fit the current one; a long
-// list always starts one), then encode.
+// Build, on the GPU: sort each list (by destination, then weight), size every
+// list (short: its bit length; long: the lines of a greedy fill -- as many
+// deltas as fit 1024 - 48 bits at the width of the widest one, at most 255),
+// place them in vertex order (first fit inside blocks of kPlaceBlock vertices,
+// a thread per block: a short list moves to the next 256-byte span only when
+// it does not fit the current one, a long list starts a line; every block
+// starts a span, placed by a scan of the block sizes), then encode.
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <string>
@@ -217,6 +220,43 @@ __global__ void k_cmp_pairs(uint64_t ne, const uint32_t* e, const uint32_t* w, u
 
 constexpr int kCmpGrid = 148 * 16;
 
+// Placement, block-local first fit: block b (vertices [b B, b B + B)) is laid
+// out from relative position 0; block_bits[b] = its length rounded up to a
+// span, so every block starts on a span (and line) boundary.
+constexpr uint64_t kPlaceBlock = 1024;
+__global__ void k_cmp_place_local(uint64_t nv, const uint32_t* size, uint64_t* cpos,
+                                  uint64_t* block_bits, unsigned* err) {
+  const uint64_t nb = (nv + kPlaceBlock - 1) / kPlaceBlock;
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nb;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t pos = 0;
+    const uint64_t v1 = min(nv, (b + 1) * kPlaceBlock);
+    for (uint64_t v = b * kPlaceBlock; v < v1; ++v) {
+      const uint32_t sz = size[v];
+      if (sz & kLongSize) {
+        const uint64_t nl = sz & ~kLongSize;
+        if (nl > kCmpMaxLines) *err = 1;
+        pos = (pos + kLineBits - 1) / kLineBits * kLineBits;
+        cpos[v] = pos | kCmpLong | (nl << kCmpPosBits);
+        pos += nl * kLineBits;
+      } else {
+        if (sz && (pos % kShortSpanBits) + sz > kShortSpanBits)  // next 256-byte span
+          pos = (pos + kShortSpanBits - 1) / kShortSpanBits * kShortSpanBits;
+        cpos[v] = pos;
+        pos += sz;
+      }
+    }
+    block_bits[b] = (pos + kShortSpanBits - 1) / kShortSpanBits * kShortSpanBits;
+  }
+}
+
+// cpos[v] += the block's base (exclusive scan of block_bits); cpos[nv] = end.
+__global__ void k_cmp_place_add(uint64_t nv, uint64_t* cpos, const uint64_t* base) {
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= nv;
+       v += (uint64_t)gridDim.x * blockDim.x)
+    cpos[v] = v < nv ? cpos[v] + base[v / kPlaceBlock] : base[(nv + kPlaceBlock - 1) / kPlaceBlock];
+}
+
 // Transpose: in-degree count, then a scatter of every arc (v -> d) into d's
 // in-list (slot from a per-vertex cursor; the lists are sorted afterwards).
 __global__ void k_in_count(uint64_t ne, const uint32_t* e, uint32_t* deg) {
@@ -261,43 +301,42 @@ uint32_t first_element_bits(const zc_graph* g) {
 
 int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t ww, uint32_t b0,
                   DevBuf* cpos, DevBuf* enc, size_t* bytes) {
-  DevBuf size;
-  // sizes, then the placement scan on the host (a sequential first-fit)
+  DevBuf size, blk, tmp, err;
+  const uint64_t nb = (nv + kPlaceBlock - 1) / kPlaceBlock;
   ZC_CUDA_TRY(cudaMalloc(&size.p, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
   k_cmp_size<<<kCmpGrid, 256>>>(nv, d_off, x, ww, b0, static_cast<uint32_t*>(size.p));
   ZC_CUDA_TRY(cudaGetLastError());
-  std::vector<uint32_t> hs(nv);
-  std::vector<uint64_t> hp(nv + 1);
-  ZC_CUDA_TRY(cudaMemcpy(hs.data(), size.p, nv * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-  cudaFree(size.release());
-  uint64_t pos = 0;
-  auto round_line = [](uint64_t b) { return (b + kLineBits - 1) / kLineBits * kLineBits; };
-  for (uint64_t v = 0; v < nv; ++v) {
-    const uint32_t sz = hs[v];
-    if (sz & kLongSize) {
-      const uint64_t nl = sz & ~kLongSize;
-      if (nl > kCmpMaxLines) {
-        set_error("a list needs more compressed lines than the index can record");
-        return ZC_EINVAL;
-      }
-      pos = round_line(pos);
-      hp[v] = pos | kCmpLong | (nl << kCmpPosBits);
-      pos += nl * kLineBits;
-    } else {
-      if (sz && (pos % kShortSpanBits) + sz > kShortSpanBits)  // next 256-byte span
-        pos = (pos + kShortSpanBits - 1) / kShortSpanBits * kShortSpanBits;
-      hp[v] = pos;
-      pos += sz;
-    }
+  ZC_CUDA_TRY(cudaMalloc(&cpos->p, (nv + 1) * sizeof(uint64_t)));
+  ZC_CUDA_TRY(cudaMalloc(&blk.p, (nb + 1) * 2 * sizeof(uint64_t)));  // sizes, then bases
+  ZC_CUDA_TRY(cudaMalloc(&err.p, sizeof(unsigned)));
+  ZC_CUDA_TRY(cudaMemset(err.p, 0, sizeof(unsigned)));
+  uint64_t* bbits = static_cast<uint64_t*>(blk.p);
+  uint64_t* bbase = bbits + nb + 1;
+  ZC_CUDA_TRY(cudaMemset(bbits + nb, 0, sizeof(uint64_t)));
+  k_cmp_place_local<<<std::max<uint64_t>((nb + 127) / 128, 1), 128>>>(
+      nv, static_cast<uint32_t*>(size.p), static_cast<uint64_t*>(cpos->p), bbits,
+      static_cast<unsigned*>(err.p));
+  ZC_CUDA_TRY(cudaGetLastError());
+  size_t tb = 0;
+  ZC_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, bbits, bbase, nb + 1));
+  ZC_CUDA_TRY(cudaMalloc(&tmp.p, std::max<size_t>(tb, 1)));
+  ZC_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tb, bbits, bbase, nb + 1));
+  k_cmp_place_add<<<kCmpGrid, 256>>>(nv, static_cast<uint64_t*>(cpos->p), bbase);
+  ZC_CUDA_TRY(cudaGetLastError());
+  uint64_t end = 0;
+  unsigned herr = 0;
+  ZC_CUDA_TRY(cudaMemcpy(&end, static_cast<uint64_t*>(cpos->p) + nv, sizeof(end),
+                         cudaMemcpyDeviceToHost));
+  ZC_CUDA_TRY(cudaMemcpy(&herr, err.p, sizeof(herr), cudaMemcpyDeviceToHost));
+  if (herr) {
+    set_error("a list needs more compressed lines than the index can record");
+    return ZC_EINVAL;
   }
-  hp[nv] = round_line(pos);
-  if (hp[nv] > kCmpPosMask) {
+  if (end > kCmpPosMask) {
     set_error("compressed stream exceeds the index's 2^40-bit positions");
     return ZC_EINVAL;
   }
-  const uint64_t lines = hp[nv] / kLineBits;
-  ZC_CUDA_TRY(cudaMalloc(&cpos->p, (nv + 1) * sizeof(uint64_t)));
-  ZC_CUDA_TRY(cudaMemcpy(cpos->p, hp.data(), (nv + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  const uint64_t lines = end / kLineBits;  // span-aligned, so whole lines
   *bytes = std::max<uint64_t>(lines, 1) * kLineBytes;
   ZC_CUDA_TRY(cudaMalloc(&enc->p, *bytes));
   ZC_CUDA_TRY(cudaMemset(enc->p, 0, *bytes));
@@ -433,12 +472,12 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
     x.e64 = static_cast<const uint64_t*>(sorted.p);
     x.wmin = hr[0];
     ww = hr[1] > hr[0] ? 32 - __builtin_clz(hr[1] - hr[0]) : 0;
-    const int rc = sort_lists_device(8, nv, g->d_off, g->h_off, sorted.p);
+    const int rc = sort_lists_device(8, nv, g->d_off, sorted.p);
     if (rc) return rc;
   } else {
     ZC_CUDA_TRY(cudaMalloc(&sorted.p, std::max<uint64_t>(ne, 1) * 4));
     ZC_CUDA_TRY(cudaMemcpy(sorted.p, g->h_edges, ne * 4, cudaMemcpyDefault));
-    const int rc = sort_lists_device(4, nv, g->d_off, g->h_off, sorted.p);
+    const int rc = sort_lists_device(4, nv, g->d_off, sorted.p);
     if (rc) return rc;
     x.e32 = static_cast<const uint32_t*>(sorted.p);
   }
@@ -510,10 +549,7 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
     ZC_CUDA_TRY(cudaGetLastError());
     cudaFree(out_e.release());
     cudaFree(deg.release());
-    std::vector<int64_t> h_in_off(nv + 1);
-    ZC_CUDA_TRY(cudaMemcpy(h_in_off.data(), in_off.p, (nv + 1) * sizeof(uint64_t),
-                           cudaMemcpyDeviceToHost));
-    rc = sort_lists_device(4, nv, static_cast<uint64_t*>(in_off.p), h_in_off.data(), in_e.p);
+    rc = sort_lists_device(4, nv, static_cast<uint64_t*>(in_off.p), in_e.p);
     if (rc) return rc;
     if ((rc = install_in_lists(g, static_cast<uint64_t*>(in_off.p),
                                static_cast<uint32_t*>(in_e.p))))

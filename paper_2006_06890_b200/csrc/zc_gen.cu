@@ -216,76 +216,6 @@ __global__ void k_deg_from_off(uint64_t nv, const uint64_t* off, uint32_t* deg) 
     deg[v] = static_cast<uint32_t>(off[v + 1] - off[v]);
 }
 
-// Sort every list ascending.  Lists up to 32 elements: warp bitonic sort in
-// registers; up to kSortSmem elements: one CTA with a shared-memory bitonic
-// sort; longer lists: CUB segmented sort (sort_lists).
-constexpr int kSortSmem = 4096;
-
-template <typename ET>
-__global__ void k_sort_short(uint64_t nv, const uint64_t* off, ET* edges) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t v = gw; v < nv; v += nw) {
-    const uint64_t s = off[v], e = off[v + 1], n = e - s;
-    if (n < 2 || n > 32) continue;
-    ET x = lane < n ? edges[s + lane] : static_cast<ET>(~0ull);
-    // bitonic sort across the 32 lanes
-    for (int k = 2; k <= 32; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        const ET y = __shfl_xor_sync(0xffffffffu, x, j);
-        const bool up = (lane & k) == 0;
-        const bool lower = (lane & j) == 0;
-        const ET lo = x < y ? x : y, hi = x < y ? y : x;
-        x = (lower == up) ? lo : hi;
-      }
-    }
-    if (lane < n) edges[s + lane] = x;
-  }
-}
-
-template <typename ET>
-__global__ void __launch_bounds__(1024) k_sort_mid(uint64_t nv, const uint64_t* off, ET* edges) {
-  __shared__ ET sh[kSortSmem];
-  for (uint64_t v = blockIdx.x; v < nv; v += gridDim.x) {
-    const uint64_t s = off[v], e = off[v + 1], n = e - s;
-    if (n <= 32 || n > kSortSmem) continue;
-    uint32_t m = 64;
-    while (m < n) m <<= 1;
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)
-      sh[i] = i < n ? edges[s + i] : static_cast<ET>(~0ull);
-    __syncthreads();
-    for (uint32_t k = 2; k <= m; k <<= 1) {
-      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-          const uint32_t p = i ^ j;
-          if (p > i) {
-            const ET a = sh[i], b = sh[p];
-            const bool up = (i & k) == 0;
-            if ((a > b) == up) {
-              sh[i] = b;
-              sh[p] = a;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) edges[s + i] = sh[i];
-    __syncthreads();
-  }
-}
-
-// Copy sorted segments [b, e) of src back into dst (warp per segment).
-template <typename ET>
-__global__ void k_copy_segments(const ET* src, ET* dst, const int* b, const int* e, int nseg) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t k = gw; k < static_cast<uint64_t>(nseg); k += nw)
-    for (int i = b[k] + lane; i < e[k]; i += 32) dst[i] = src[i];
-}
-
 template <typename ET>
 __global__ void k_uniform_fill(uint64_t nv, uint64_t seed, const uint64_t* off, ET* edges) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
@@ -371,8 +301,8 @@ int offsets_from_degrees(zc_graph* g, uint32_t* d_deg, uint64_t nv, uint64_t** d
   t.add(tmp);
   ZC_CUDA_TRY(scan_u32_to_u64(d_deg, d_off, nv, tmp, tb, 0));
   if (!g->h_off) {
-    if (cudaHostAlloc(&g->h_off, (nv + 1) * sizeof(int64_t), cudaHostAllocDefault) !=
-        cudaSuccess) {
+    g->h_off = static_cast<int64_t*>(pinned_list_alloc(g->device, (nv + 1) * sizeof(int64_t)));
+    if (!g->h_off) {
       set_error("cannot allocate pinned offsets");
       return ZC_ENOMEM;
     }
@@ -383,57 +313,100 @@ int offsets_from_degrees(zc_graph* g, uint32_t* d_deg, uint64_t nv, uint64_t** d
   return ZC_OK;
 }
 
+// Offsets of a batch of lists relative to its first element (CUB takes int).
+__global__ void k_rel_offsets(uint64_t n, const uint64_t* off, uint64_t base, int* rel) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    rel[i] = static_cast<int>(off[i] - base);
+}
+
+// Sort every list ascending: CUB's segmented sort (segments partitioned by
+// size into sub-warp / warp / CTA sorts) over batches of consecutive lists
+// holding at most 2^30 keys (CUB takes int sizes), out of place into a batch
+// buffer, copied back.
 template <typename ET>
-int sort_lists(uint64_t nv, const uint64_t* d_off, const int64_t* h_off, ET* edges) {
-  k_sort_short<ET><<<kGenGrid, 256>>>(nv, d_off, edges);
-  k_sort_mid<ET><<<kGenGrid, 1024>>>(nv, d_off, edges);
-  ZC_CUDA_TRY(cudaGetLastError());
-  // Long lists (hubs): CUB segmented sort, batched so every call covers at
-  // most 2^30 keys (CUB takes int sizes), then copied back segment-wise.
-  std::vector<uint64_t> seg_b, seg_e;
-  for (uint64_t v = 0; v < nv; ++v) {
-    const uint64_t n = h_off[v + 1] - h_off[v];
-    if (n > static_cast<uint64_t>(kSortSmem)) {
-      seg_b.push_back(h_off[v]);
-      seg_e.push_back(h_off[v + 1]);
-    }
-  }
+int sort_lists(uint64_t nv, const uint64_t* d_off, ET* edges) {
+  if (nv == 0) return ZC_OK;
+  std::vector<uint64_t> cut{0};
+  auto off_at = [&](uint64_t v, uint64_t* x) {
+    return cudaMemcpy(x, d_off + v, sizeof(*x), cudaMemcpyDeviceToHost);
+  };
   const uint64_t kSpan = 1ull << 30;
-  size_t i0 = 0;
-  while (i0 < seg_b.size()) {
-    size_t i1 = i0 + 1;
-    while (i1 < seg_b.size() && seg_e[i1] - seg_b[i0] <= kSpan) ++i1;
-    const uint64_t base = seg_b[i0], span = seg_e[i1 - 1] - base;
-    const int nseg = static_cast<int>(i1 - i0);
-    std::vector<int> hb(nseg), he(nseg);
-    for (int k = 0; k < nseg; ++k) {
-      hb[k] = static_cast<int>(seg_b[i0 + k] - base);
-      he[k] = static_cast<int>(seg_e[i0 + k] - base);
+  uint64_t ne = 0;
+  ZC_CUDA_TRY(off_at(nv, &ne));
+  while (cut.back() < nv) {  // largest v1 with off[v1] - off[v0] <= kSpan (at least v0 + 1)
+    const uint64_t v0 = cut.back();
+    uint64_t b0 = 0;
+    ZC_CUDA_TRY(off_at(v0, &b0));
+    uint64_t lo = v0 + 1, hi = nv;
+    if (ne - b0 <= kSpan) {
+      lo = nv;
+    } else {
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi + 1) / 2;
+        uint64_t x = 0;
+        ZC_CUDA_TRY(off_at(mid, &x));
+        if (x - b0 <= kSpan) lo = mid; else hi = mid - 1;
+      }
     }
-    int *db = nullptr, *de = nullptr;
-    ET* out = nullptr;
-    void* tmp = nullptr;
-    size_t tmp_bytes = 0;
-    ZC_CUDA_TRY(cudaMalloc(&db, nseg * sizeof(int)));
-    ZC_CUDA_TRY(cudaMalloc(&de, nseg * sizeof(int)));
-    ZC_CUDA_TRY(cudaMemcpy(db, hb.data(), nseg * sizeof(int), cudaMemcpyHostToDevice));
-    ZC_CUDA_TRY(cudaMemcpy(de, he.data(), nseg * sizeof(int), cudaMemcpyHostToDevice));
-    ZC_CUDA_TRY(cudaMalloc(&out, span * sizeof(ET)));
-    ZC_CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, edges + base, out,
-                                                   static_cast<int>(span), nseg, db, de));
-    ZC_CUDA_TRY(cudaMalloc(&tmp, tmp_bytes));
-    ZC_CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, edges + base, out,
-                                                   static_cast<int>(span), nseg, db, de));
-    k_copy_segments<ET><<<kGenGrid, 256>>>(out, edges + base, db, de, nseg);
-    ZC_CUDA_TRY(cudaDeviceSynchronize());
-    cudaFree(db);
-    cudaFree(de);
-    cudaFree(out);
-    cudaFree(tmp);
-    i0 = i1;
+    uint64_t b1 = 0;
+    ZC_CUDA_TRY(off_at(lo, &b1));
+    if (b1 - b0 > kSpan) {
+      set_error("a list longer than 2^30 elements cannot be sorted");
+      return ZC_EINVAL;
+    }
+    cut.push_back(lo);
   }
-  ZC_CUDA_TRY(cudaGetLastError());
-  return ZC_OK;
+  uint64_t maxv = 0, maxe = 0;
+  for (size_t k = 0; k + 1 < cut.size(); ++k) maxv = std::max(maxv, cut[k + 1] - cut[k]);
+  maxe = std::min<uint64_t>(ne, kSpan);
+  int* rel = nullptr;
+  ET* out = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  ZC_CUDA_TRY(cudaMalloc(&rel, (maxv + 1) * sizeof(int)));
+  if (cudaMalloc(&out, std::max<uint64_t>(maxe, 1) * sizeof(ET)) != cudaSuccess) {
+    cudaFree(rel);
+    set_error("out of device memory (list sort)");
+    return ZC_ENOMEM;
+  }
+  int rc = ZC_OK;
+  for (size_t k = 0; k + 1 < cut.size() && rc == ZC_OK; ++k) {
+    const uint64_t v0 = cut[k], n = cut[k + 1] - v0;
+    uint64_t base = 0, span = 0;
+    if (off_at(v0, &base) != cudaSuccess || off_at(v0 + n, &span) != cudaSuccess) {
+      rc = ZC_ECUDA;
+      break;
+    }
+    span -= base;
+    if (span == 0) continue;
+    k_rel_offsets<<<kGenGrid, 256>>>(n, d_off + v0, base, rel);
+    size_t need = 0;
+    cub::DeviceSegmentedSort::SortKeys(nullptr, need, edges + base, out, static_cast<int>(span),
+                                       static_cast<int>(n), rel, rel + 1);
+    if (need > tmp_bytes) {
+      cudaFree(tmp);
+      tmp = nullptr;
+      tmp_bytes = need;
+      if (cudaMalloc(&tmp, tmp_bytes) != cudaSuccess) {
+        rc = ZC_ENOMEM;
+        set_error("out of device memory (list sort)");
+        break;
+      }
+    }
+    if (cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, edges + base, out,
+                                           static_cast<int>(span), static_cast<int>(n), rel,
+                                           rel + 1) != cudaSuccess ||
+        cudaMemcpy(edges + base, out, span * sizeof(ET), cudaMemcpyDeviceToDevice) !=
+            cudaSuccess) {
+      rc = ZC_ECUDA;
+      set_error(std::string("list sort: ") + cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  cudaFree(rel);
+  cudaFree(out);
+  cudaFree(tmp);
+  return rc;
 }
 
 zc_graph* new_handle(int32_t placement, int32_t device, uint32_t flags) {
@@ -590,7 +563,8 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
   auto fail = [](int code) { return code; };
   g->nv = nl;
   g->ne = e1 - e0;
-  if (cudaHostAlloc(&g->h_off, (nl + 1) * sizeof(int64_t), cudaHostAllocDefault) != cudaSuccess) {
+  g->h_off = static_cast<int64_t*>(pinned_list_alloc(g->device, (nl + 1) * sizeof(int64_t)));
+  if (!g->h_off) {
     set_error("cannot allocate pinned offsets");
     return fail(ZC_ENOMEM);
   }
@@ -626,7 +600,7 @@ int generate_rmat_part(uint32_t scale, uint32_t ef, double a, double b, double c
     t.release(d_cursor);
     t.release(d_soff);
     t.release(d_goff);
-    if ((rc = sort_lists<uint32_t>(nl, d_loff, g->h_off, d_edges))) return fail(rc);
+    if ((rc = sort_lists<uint32_t>(nl, d_loff, d_edges))) return fail(rc);
   } else {
     t.release(d_goff);
     k_rmat_fill<uint32_t><<<kGenGrid, 256>>>(p, nl, d_loff, d_edges, lo);
@@ -704,10 +678,7 @@ int rmat_part_in_lists(zc_graph* g) {
   }
   t.release(d_goff);
   t.release(d_deg);
-  std::vector<int64_t> h_in_off(nl + 1);
-  ZC_CUDA_TRY(cudaMemcpy(h_in_off.data(), d_in_off, (nl + 1) * sizeof(uint64_t),
-                         cudaMemcpyDeviceToHost));
-  int rc = sort_lists<uint32_t>(nl, d_in_off, h_in_off.data(), d_in);
+  int rc = sort_lists<uint32_t>(nl, d_in_off, d_in);
   if (rc) return rc;
   ZC_CUDA_TRY(cudaDeviceSynchronize());
   if ((rc = install_in_lists(g, d_in_off, d_in))) return rc;
@@ -779,7 +750,7 @@ int generate_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uin
     t.add(d_sedges);
     k_sym_copy_out<uint32_t><<<kGenGrid, 256>>>(nv, d_off, d_edges, d_soff, d_sedges);
     k_sym_scatter_in<uint32_t><<<kGenGrid, 256>>>(nv, d_off, d_edges, d_soff, d_cursor, d_sedges);
-    if ((rc = sort_lists<uint32_t>(nv, d_soff, g->h_off, d_sedges))) return fail(rc);
+    if ((rc = sort_lists<uint32_t>(nv, d_soff, d_sedges))) return fail(rc);
     if (cudaDeviceSynchronize() != cudaSuccess) {
       set_error(std::string("symmetrize: ") + cudaGetErrorString(cudaGetLastError()));
       return fail(ZC_ECUDA);
@@ -857,10 +828,9 @@ int generate_uniform(uint64_t nv, uint32_t dmin, uint32_t dmax, uint64_t seed, i
 
 int part_in_lists(zc_graph* g) { return rmat_part_in_lists(g); }
 
-int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, const int64_t* h_off,
-                      void* edges) {
-  int rc = elem_bytes == 4 ? sort_lists<uint32_t>(nv, d_off, h_off, static_cast<uint32_t*>(edges))
-                           : sort_lists<uint64_t>(nv, d_off, h_off, static_cast<uint64_t*>(edges));
+int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, void* edges) {
+  int rc = elem_bytes == 4 ? sort_lists<uint32_t>(nv, d_off, static_cast<uint32_t*>(edges))
+                           : sort_lists<uint64_t>(nv, d_off, static_cast<uint64_t*>(edges));
   if (rc) return rc;
   ZC_CUDA_TRY(cudaDeviceSynchronize());
   return ZC_OK;

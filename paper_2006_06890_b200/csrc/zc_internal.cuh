@@ -299,8 +299,7 @@ cudaError_t launch_pr_normalize(double* rank, uint64_t nv, uint64_t* ctr, bool d
 cudaError_t launch_dup_flags(const void* sorted, int elem_bytes, const uint64_t* off, uint64_t nv,
                              uint64_t* ctr, cudaStream_t st);
 // Sort every list ascending in place (device array, zc_gen.cu).
-int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, const int64_t* h_off,
-                      void* edges);
+int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, void* edges);
 
 // Exclusive scan of u32 counts into u64 offsets (n+1 outputs), device-wide.
 cudaError_t scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp,

@@ -508,3 +508,58 @@ extern "C" int zc_link_probe(int32_t device, uint64_t bytes, int iters, double* 
   cudaFreeHost(h);
   return ZC_OK;
 }
+
+// Pinned-allocation cost (the compressed streams' build pins ~6 GB twice):
+// mode 0 cudaHostAlloc(Mapped|Portable); 1 mmap + MADV_HUGEPAGE + parallel
+// first touch + cudaHostRegister; 2 the same without huge pages; 3 mmap +
+// MADV_HUGEPAGE + cudaHostRegister with no prefault.  *alloc_s covers the
+// mapping and first touch, *register_s the registration (mode 0: all in
+// alloc_s); the buffer is freed before returning.
+#include <chrono>
+#include <thread>
+#include <vector>
+extern "C" int zc_pin_probe(uint64_t bytes, int mode, int threads, double* alloc_s,
+                            double* register_s) {
+  using clk = std::chrono::steady_clock;
+  auto secs = [](clk::time_point a, clk::time_point b) {
+    return std::chrono::duration<double>(b - a).count();
+  };
+  *alloc_s = *register_s = 0;
+  const auto t0 = clk::now();
+  if (mode == 0) {
+    void* p = nullptr;
+    ZC_CUDA_TRY(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    *alloc_s = secs(t0, clk::now());
+    cudaFreeHost(p);
+    return ZC_OK;
+  }
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (p == MAP_FAILED) {
+    zc::set_error("mmap failed");
+    return ZC_ENOMEM;
+  }
+  if (mode != 2) madvise(p, bytes, MADV_HUGEPAGE);
+  if (mode != 3) {
+    const int nt = std::max(1, threads);
+    std::vector<std::thread> th;
+    const uint64_t chunk = (bytes / nt + 4095) & ~4095ull;
+    for (int k = 0; k < nt; ++k)
+      th.emplace_back([=] {
+        char* b = static_cast<char*>(p);
+        for (uint64_t o = k * chunk; o < std::min<uint64_t>(bytes, (k + 1) * chunk); o += 4096)
+          b[o] = 0;
+      });
+    for (auto& t : th) t.join();
+  }
+  const auto t1 = clk::now();
+  *alloc_s = secs(t0, t1);
+  const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  *register_s = secs(t1, clk::now());
+  if (e == cudaSuccess) cudaHostUnregister(p);
+  munmap(p, bytes);
+  if (e != cudaSuccess) {
+    zc::set_error(std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+    return ZC_ECUDA;
+  }
+  return ZC_OK;
+}

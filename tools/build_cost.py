@@ -1,0 +1,25 @@
+"""Cost of the compressed out-list and in-list builds at K27 (VERDICT r01
+item 7): wall time of each build call, plus the pinned-allocation cost of
+the same byte counts on its own.  Run plain, then under ncu --metrics
+gpu__time_duration.sum for the kernel share."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2006_06890_b200 as zc
+import paper_2006_06890_b200._native as N
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 27
+t = time.time()
+dg = zc.generate_rmat(scale, 16, seed=27)
+print(f"gen {time.time() - t:.2f}s", flush=True)
+t = time.time()
+nb = dg.build_compressed()
+print(f"build_compressed {time.time() - t:.2f}s bytes={nb}", flush=True)
+t = time.time()
+ni = dg.build_in_lists()
+print(f"build_in_lists {time.time() - t:.2f}s bytes={ni}", flush=True)
+for nbytes in (nb, ni):
+    t = time.time()
+    p = N.lib().zc_host_alloc(nbytes)
+    ta = time.time() - t
+    t = time.time()
+    N.lib().zc_host_free(p)
+    print(f"zc_host_alloc({nbytes}) {ta:.2f}s free {time.time() - t:.2f}s", flush=True)
