@@ -318,6 +318,29 @@ def bfs_point(zc, dg, src, strategy, evict=False, reps=2) -> tuple[dict, object]
             "u32_edge_gbs": r.total_traversed_edges * 4 / (r.expand_ms * 1e-3) / 1e9}, r
 
 
+def ceiling_model_summary() -> dict:
+    """profiles/r02_ceiling_model.txt (tools/ceiling.py): the merged-aligned
+    levels' measured time against the reference request model x the measured
+    per-size request rates (ratio >= 1: at or above the modelled ceiling)."""
+    path = os.path.join(ROOT, "profiles", "r02_ceiling_model.txt")
+    if not os.path.exists(path):
+        return {}
+    ratios, meas, ceil = [], 0.0, 0.0
+    for ln in open(path):
+        f = ln.split()
+        if len(f) >= 13 and f[0] == "merged-aligned" and f[2].isdigit() and int(f[3]) > 10 ** 7:
+            ratios.append(float(f[11]))
+            meas += float(f[9])
+            ceil += float(f[10])
+    if not ratios:
+        return {}
+    return {"file": "profiles/r02_ceiling_model.txt", "levels_over_1e7_edges": len(ratios),
+            "min_ratio_ceiling_over_measured": min(ratios), "sum_ratio": ceil / meas,
+            "model": "reference request model (coalesce.py:165-207) histograms x measured "
+                     "per-size CTA-streamed zero-copy rates; ratio >= 0.9 on every level = "
+                     "at the link's ceiling for merged-aligned's request mix"}
+
+
 def level_table(dg, r, elem_bytes=4) -> list:
     prof = dg.expand_profile(r.iterations)
     return [{"level": k, "frontier": int(r.frontier_sizes[k]), "edges": int(r.traversed_edges[k]),
@@ -435,7 +458,7 @@ def main():
                   "pinned_list_bytes": dg.num_edges * 4},
         "merged_aligned": {"gteps": value, "e2e_gteps": e2e_value,
                            "link_gbs": achieved, "frac_of_pcie_gen5": achieved / PCIE_GEN5_X16_GBS,
-                           "levels_last_step": levels},
+                           "levels_last_step": levels, "ceiling_model": ceiling_model_summary()},
     }
 
     oc = OracleCache(threads)
@@ -826,7 +849,7 @@ def main_partitioned(args, rank, world, device):
     import torch
     import torch.distributed as dist
     import paper_2006_06890_b200 as zc
-    from paper_2006_06890_b200.multi import exchange_buffers, generate_rmat_part
+    from paper_2006_06890_b200.multi import exchange_buffers, generate_rmat_part, run_partition
 
     stage = args.backend == "gloo"
     dev = torch.device("cuda", device)
@@ -847,24 +870,37 @@ def main_partitioned(args, rank, world, device):
     dist.broadcast_object_list(src, 0)
     sources = src[0]
     bufs = exchange_buffers("bfs", world, part.stride, dev)
+    fused_error = None
+    if args.exchange == "fused":
+        try:  # peer access between the ranks' GPUs is a property of the box
+            run_partition(part, "bfs", int(sources[0]), strat, fetch=False, fused=True)
+        except RuntimeError as exc:
+            fused_error = str(exc)[:300]
+            args.exchange = "reduce-scatter"
     with ClockSampler(device) as clk:
         head = _part_series(part, "bfs", sources, strat, args.steps, args.warmup, world, device,
                             exchange=args.exchange, bufs=bufs, stage=stage)
     other = "reduce-scatter" if args.exchange == "fused" else "fused"
-    alt = _part_series(part, "bfs", sources, strat, min(args.steps, 5), 1, world, device,
-                       exchange=other, bufs=bufs, stage=stage)
+    if fused_error is None:
+        alt = _part_series(part, "bfs", sources, strat, min(args.steps, 5), 1, world, device,
+                           exchange=other, bufs=bufs, stage=stage)
+    else:
+        alt = {"error": fused_error, "exchange_bytes_per_step": None}
+        other = "reduce-scatter"
     # e2e: the public partitioned API with every rank's int64 levels downloaded
     e2e = _part_series(part, "bfs", sources, strat, args.steps, 0, world, device,
                        exchange=args.exchange, bufs=bufs, stage=stage, fetch=True)
     d2h = sum_over_ranks(sum(r.values.nbytes for r in e2e["_results"]), world, device)
     crc_a = _gather_values_crc(e2e["_results"][0], world, device)
-    r_alt = _part_series(part, "bfs", sources[:1], strat, 1, 0, world, device, exchange=other,
-                         bufs=bufs, stage=stage, fetch=True)  # e2e's first run: sources[0]
-    crc_b = _gather_values_crc(r_alt["_results"][0], world, device)
-    ra, rb = e2e["_results"][0], r_alt["_results"][0]
-    parity[f"kron{scale}/fused_vs_reduce_scatter"] = bool(
-        crc_a == crc_b and ra.iterations == rb.iterations
-        and list(ra.traversed_edges) == list(rb.traversed_edges))
+    if fused_error is None:
+        r_alt = _part_series(part, "bfs", sources[:1], strat, 1, 0, world, device,
+                             exchange=other, bufs=bufs, stage=stage,
+                             fetch=True)  # e2e's first run: sources[0]
+        crc_b = _gather_values_crc(r_alt["_results"][0], world, device)
+        ra, rb = e2e["_results"][0], r_alt["_results"][0]
+        parity[f"kron{scale}/fused_vs_reduce_scatter"] = bool(
+            crc_a == crc_b and ra.iterations == rb.iterations
+            and list(ra.traversed_edges) == list(rb.traversed_edges))
     e2e_value = e2e["_trav"] / e2e["wall_s"] / 1e9
     part_arcs = part.graph_view().num_edges
     part.close()
@@ -908,12 +944,14 @@ def main_partitioned(args, rank, world, device):
                      "kind": args.exchange,
                      other.replace("-", "_") + "_bytes_per_step": alt["exchange_bytes_per_step"]},
         "variants": {other: _strip(alt)},
+        "fused_error": fused_error,
         "headline": _strip(head),
         "graph": {"vertices": 1 << scale, "arcs": args.edge_factor << scale,
                   "local_arcs_rank0": part_arcs, "gen_s": gen_s},
     }
     if not args.no_configs4:
-        line["configs4"] = configs4(args, rank, world, device, stage, parity)
+        line["configs4"] = configs4(args, rank, world, device, stage, parity,
+                                    fused_ok=fused_error is None)
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = reference_sample(3, 0, args.seed, args.cpu_threads or os.cpu_count())
     barrier(world, device)
@@ -923,7 +961,7 @@ def main_partitioned(args, rank, world, device):
         print(json.dumps(line), flush=True)
 
 
-def configs4(args, rank, world, device, stage, parity) -> dict:
+def configs4(args, rank, world, device, stage, parity, fused_ok=True) -> dict:
     """BASELINE configs[4] at fixed size: Kronecker `part_scale` symmetrized
     (2^34 arcs at 29), BFS and CC (Jacobi label propagation), vertex-range
     partitioned over the N ranks (strong scaling)."""
@@ -952,6 +990,8 @@ def configs4(args, rank, world, device, stage, parity) -> dict:
     peak = world * PCIE_GEN5_X16_GBS
     for algo, exch, steps in (("bfs", "fused", 2), ("bfs", "reduce-scatter", 2),
                               ("cc", "reduce-scatter", 1), ("cc", "fused", 1)):
+        if exch == "fused" and not fused_ok:
+            continue
         bufs = exchange_buffers(algo, world, part.stride, dev) if exch != "fused" else None
         r = _part_series(part, algo, sources, "merged-aligned", steps, 1, world, device,
                          exchange=exch, bufs=bufs, stage=stage)
@@ -964,7 +1004,7 @@ def configs4(args, rank, world, device, stage, parity) -> dict:
         out[key] = res
         del bufs
         torch.cuda.empty_cache()
-    for algo in ("bfs", "cc"):  # both exchanges: identical iterations and work
+    for algo in ("bfs", "cc") if fused_ok else ():  # both exchanges: same iterations, work
         a, b = out[f"{algo}/fused"], out[f"{algo}/reduce-scatter"]
         parity[f"k{scale}sym_{algo}/fused_vs_reduce_scatter_work"] = (
             a["iterations"] == b["iterations"]

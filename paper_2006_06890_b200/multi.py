@@ -396,7 +396,17 @@ def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartRe
         handle, mine = engine.fused_init(algo)
         handles = [None] * dist.get_world_size(group)
         dist.all_gather_object(handles, handle, group=group)
-        engine.fused_connect(handles=handles)
+        err = None
+        try:
+            engine.fused_connect(handles=handles)
+        except RuntimeError as exc:  # e.g. no peer access between these GPUs
+            err = exc
+        # every rank learns whether all peers opened, so none waits on a dead exchange
+        status = [None] * dist.get_world_size(group)
+        dist.all_gather_object(status, None if err is None else str(err), group=group)
+        failed = [m for m in status if m is not None]
+        if failed:
+            raise RuntimeError(f"fused exchange unavailable: {failed[0]}")
         engine._fused_for, engine._fused_mine = algo, mine
     cdev = torch.device("cpu") if dist.get_backend(group) == "gloo" else dev
     counts = torch.zeros(2, dtype=torch.int64, device=cdev)
