@@ -458,7 +458,11 @@ def main():
                   "pinned_list_bytes": dg.num_edges * 4},
         "merged_aligned": {"gteps": value, "e2e_gteps": e2e_value,
                            "link_gbs": achieved, "frac_of_pcie_gen5": achieved / PCIE_GEN5_X16_GBS,
-                           "levels_last_step": levels, "ceiling_model": ceiling_model_summary()},
+                           "levels_last_step": levels, "ceiling_model": ceiling_model_summary(),
+                           "pcie_read_gbs_whole_traversal": summ.get(
+                               "bfs_merged_aligned_whole_traversal", {}).get("pcie_read_gbs"),
+                           "pcie_read_note": "ncu pcie__read_bytes over all levels of one BFS / "
+                                             "their summed duration (profiles/ncu_summary.json)"},
     }
 
     oc = OracleCache(threads)
