@@ -219,9 +219,12 @@ int zc_graph_compressed_index(const zc_graph *g, uint64_t *first_line);
 /* Build (once) an interleaved copy of the lists as 8-byte (dst, weight) u32
  * pairs in the handle's placement; SSSP then reads one stream instead of two,
  * so a list of n edges costs ceil(8n/128) line requests instead of two
- * half-used ones.  A B200 layout option; results are identical.  The request
- * model (ZC_OPT_TRAFFIC_MODEL) keeps describing the reference's separate
- * arrays, so modelled runs read those. */
+ * half-used ones.  A B200 layout choice; results are identical.  zc_sssp /
+ * zc_sssp_nearfar build it on first use for the merged, merged-aligned and
+ * packed strategies (4-byte edges and weights; +8 bytes per edge of host
+ * memory; tuning "pairs=0" opts out).  The request model
+ * (ZC_OPT_TRAFFIC_MODEL) keeps describing the reference's separate arrays, so
+ * modelled runs read those. */
 int zc_graph_build_pairs(zc_graph *g);
 /* 1 if some list repeats a destination (traversal.py:182-188), cached. */
 int zc_graph_multigraph(zc_graph *g, int *out);
@@ -262,7 +265,8 @@ int zc_set_options(zc_graph *g, uint32_t options);
  * a profiler, which cannot see kernels inside conditional graph nodes),
  * "do_alpha=X" (direction-optimizing switch factor), "ld=0..3" (load flavour of
  * the raw-list BFS sweeps: L1::no_allocate, L1-cached, read-only path,
- * L1::evict_first).  NULL or "" resets the
+ * L1::evict_first), "pairs=0|1" (SSSP reads the separate edge and weight
+ * arrays / the interleaved pairs stream).  NULL or "" resets the
  * defaults; an unknown entry is ZC_EINVAL.  Read by the run path; nothing is
  * taken from the environment. */
 int zc_set_tuning(zc_graph *g, const char *spec);

@@ -809,7 +809,16 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
   // Frontier buffers [0] are both read by the expansion and rewritten by the
   // compaction (which only reads the marks), so the level loop has fixed
   // pointers -- the device-driven loop below is one instantiated CUDA graph.
-  const bool pairs = algo == kSssp && g->d_pairs && !model;
+  // SSSP over 4-byte edges and weights with a windowed raw strategy reads the
+  // interleaved (dst, weight) stream (built on first use): a degree-16 list is
+  // one full line instead of two half lines (U27: 0.52 -> 0.80 of the link)
+  if (algo == kSssp && !model && !g->d_pairs && g->tune.pairs && g->has_weights && g->eb == 4 &&
+      g->wb == 4 && !g->nparts &&
+      (strategy == kMerged || strategy == kMergedAligned || strategy == kPacked)) {
+    const int rc = zc_graph_build_pairs(g);
+    if (rc) return rc;
+  }
+  const bool pairs = algo == kSssp && g->d_pairs && !model && g->tune.pairs;
   auto expand_args = [&](uint64_t nn, uint32_t iter) {
     ExpandArgs a{};
     a.front = g->d_front[0];
@@ -2385,6 +2394,7 @@ int zc_set_tuning(zc_graph* g, const char* spec) {
     else if (k == "loop" && (v == "host" || v == "device")) t.host_loop = v == "host";
     else if (k == "do_alpha" && atof(v.c_str()) > 0) t.do_alpha = atof(v.c_str());
     else if (k == "ld" && v.size() == 1 && v[0] >= '0' && v[0] <= '3') t.ld = v[0] - '0';
+    else if (k == "pairs" && (v == "0" || v == "1")) t.pairs = v == "1";
     else {
       set_error("unknown tuning entry '" + kv + "'");
       return ZC_EINVAL;

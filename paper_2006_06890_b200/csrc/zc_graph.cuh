@@ -112,6 +112,7 @@ struct zc_graph {
     int host_loop = 0;  // 1: host-driven level loop (profilers cannot see graph kernels)
     double do_alpha = 2.0;  // direction-optimizing switch factor
     int ld = -1;      // load flavour override of the raw BFS sweeps (zc_kernels.cu DefaultLd)
+    int pairs = 1;    // SSSP on merged / merged-aligned / packed: build + read the pairs stream
   } tune;
   int multigraph = -1;  // cached duplicate-arc check (-1 unknown)
   LoopGraph loop;

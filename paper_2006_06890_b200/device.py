@@ -258,8 +258,8 @@ class DeviceGraph:
     # -- run plumbing
     def set_tuning(self, spec: str = "") -> None:
         """Launch tuning of this handle (zc_set_tuning): comma-separated
-        unroll=2|4|8, ctas=N, sched=chunk|sweep, loop=host|device, do_alpha=X;
-        "" restores the defaults."""
+        unroll=2|4|8, ctas=N, sched=chunk|sweep, loop=host|device, do_alpha=X,
+        ld=0..3, pairs=0|1; "" restores the defaults."""
         N.check(N.lib().zc_set_tuning(self.handle, spec.encode()))
 
     def set_traffic_model(self, on: bool) -> None:

@@ -146,7 +146,12 @@ def sssp(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *,
     ``schedule="near-far"`` (B200 extension) expands only the improved
     vertices below a threshold that advances by ``delta`` (default 32) once
     they run out: the same distances with less work; iteration counts differ
-    from the reference's."""
+    from the reference's.
+
+    With 4-byte edges and weights, the merged / merged-aligned / packed
+    strategies read an interleaved (dst, weight) copy of the lists, built on
+    first use in the graph's placement (+8 bytes per edge of host memory;
+    ``DeviceGraph.set_tuning("pairs=0")`` reads the separate arrays)."""
     _check_source(g, source)
     if not _has_weights(g):
         raise ValueError("sssp requires edge weights")

@@ -336,6 +336,25 @@ def test_symmetric_rmat_partition_generator_matches_whole_graph():
     whole.close()
 
 
+def test_sssp_pairs_stream_default_and_opt_out():
+    """SSSP with 4-byte edges and weights reads the interleaved (dst, weight)
+    stream for the windowed raw strategies (built on first use); "pairs=0"
+    reads the separate arrays.  Both equal the oracle exactly."""
+    u = zc.generate_uniform_device(1 << 15, 2, 24, seed=8, weights=(1, 90))
+    g = u.as_csr()
+    src = int(zc.pick_sources(g, 1, seed=7)[0])
+    ref = oracle.sssp(g, src, threads=8)
+    for tune in ("", "pairs=0", "pairs=1"):
+        u.set_tuning(tune)
+        for s in ALL:
+            r = zc.sssp(u, src, s, collect_traffic=False)
+            assert np.array_equal(r.values, ref.values), (tune, s)
+            assert r.iterations == ref.iterations and r.traversed_edges == ref.traversed_edges
+        r = zc.sssp(u, src, "merged-aligned", collect_traffic=False, schedule="near-far")
+        assert np.array_equal(r.values, ref.values), tune
+    u.close()
+
+
 def test_pagerank_matches_reference():
     """Reference pagerank outputs (incl. acceptance criterion 6's PR stream):
     L-inf <= 1e-8 (test_acceptance.py:169-180), the same iteration count (the
