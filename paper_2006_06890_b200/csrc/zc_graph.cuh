@@ -106,7 +106,7 @@ struct zc_graph {
   uint32_t options = 0;
   // launch tuning (zc_set_tuning; read by the run path, never from the environment)
   struct Tuning {
-    int unroll = 4;   // windows per warp batch in the sweep (2 / 4 / 8)
+    int unroll = 0;   // windows per warp batch in the sweep (2 / 4 / 8; 0: the strategy's)
     int ctas = 0;     // sweep CTAs per SM (0: occupancy maximum)
     int sched = 0;    // 1: the round-1 chunk scheduler instead of the sweep
     int host_loop = 0;  // 1: host-driven level loop (profilers cannot see graph kernels)

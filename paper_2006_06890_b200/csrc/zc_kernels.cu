@@ -1656,6 +1656,22 @@ cudaError_t expand_u(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t
   return cudaGetLastError();
 }
 
+// Unroll variants of the raw-list sweeps (u32 lists, or SSSP's interleaved
+// pairs): `value` = the default windows per warp batch.
+template <int STRAT, int ALGO, typename ET, typename WT>
+struct SweepUnroll {
+  static constexpr bool tunable =
+      (STRAT == kMergedAligned || STRAT == kMerged || STRAT == kPacked) &&
+      !AlgoTraits<ALGO>::pull && ALGO != kPr &&
+      ((sizeof(ET) == 4 && sizeof(WT) == 4) || IsPair<WT>::value);
+  static constexpr int value =
+      (STRAT == kMergedAligned || STRAT == kMerged) &&
+              (AlgoTraits<ALGO>::base == kBfs || AlgoTraits<ALGO>::base == kCc) &&
+              !AlgoTraits<ALGO>::uf
+          ? 8
+          : 4;
+};
+
 template <int STRAT, int ALGO, typename ET, typename WT>
 cudaError_t expand_t(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t* launches) {
   if (STRAT == kNaive) {
@@ -1665,22 +1681,27 @@ cudaError_t expand_t(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t
     *launches += 1;
     return cudaGetLastError();
   }
-  // tuning variants (zc_set_tuning unroll=N, ld=N) for the BFS / u32 raw-list sweeps
-  if constexpr (STRAT == kMergedAligned && AlgoTraits<ALGO>::base == kBfs &&
-                sizeof(ET) == 4 && sizeof(WT) == 4) {
-    if (a.unroll == 2) return expand_u<STRAT, ALGO, ET, WT, 2>(a, num_sms, st, launches);
-    if (a.unroll == 8) return expand_u<STRAT, ALGO, ET, WT, 8>(a, num_sms, st, launches);
-  }
-  if constexpr ((STRAT == kMergedAligned || STRAT == kMerged) && ALGO == kBfs &&
-                sizeof(ET) == 4 && sizeof(WT) == 4) {
-    if (!a.chunk_sched && a.ld == 0)
-      return expand_sweep<STRAT, ALGO, ET, WT, kUnroll, 0>(a, num_sms, st, launches);
-    if (!a.chunk_sched && a.ld == 1)
-      return expand_sweep<STRAT, ALGO, ET, WT, kUnroll, 1>(a, num_sms, st, launches);
-    if (!a.chunk_sched && a.ld == 2)
-      return expand_sweep<STRAT, ALGO, ET, WT, kUnroll, 2>(a, num_sms, st, launches);
-    if (!a.chunk_sched && a.ld == 3)
-      return expand_sweep<STRAT, ALGO, ET, WT, kUnroll, 3>(a, num_sms, st, launches);
+  // Windows per warp batch of the raw-list sweeps.  Merged / merged-aligned
+  // BFS and CC take 8 by default: twice the loads in flight per warp, and
+  // adjacent lists' windows (which share lines) issued back to back by one
+  // warp, so the L1 / L2 merge more of the reference's duplicate line requests
+  // (profiles/r02_unroll_ab.txt, K27: BFS merged-aligned 10.18 -> 10.36 GTEPS,
+  // merged 7.48 -> 8.10; CC-K27-sym merged-aligned 11.51 -> 11.77 work-GTEPS;
+  // SSSP and packed unchanged or slower at 8).  zc_set_tuning unroll=2|4|8
+  // and ld=0..3 are A/B variants.
+  if constexpr (SweepUnroll<STRAT, ALGO, ET, WT>::tunable) {
+    if (!a.chunk_sched) {
+      const int u = a.unroll ? a.unroll : SweepUnroll<STRAT, ALGO, ET, WT>::value;
+      if (u == 2) return expand_sweep<STRAT, ALGO, ET, WT, 2>(a, num_sms, st, launches);
+      if (u == 8) {
+        if constexpr (ALGO == kBfs && STRAT != kPacked) {
+          if (a.ld == 0) return expand_sweep<STRAT, ALGO, ET, WT, 8, 0>(a, num_sms, st, launches);
+          if (a.ld == 2) return expand_sweep<STRAT, ALGO, ET, WT, 8, 2>(a, num_sms, st, launches);
+          if (a.ld == 3) return expand_sweep<STRAT, ALGO, ET, WT, 8, 3>(a, num_sms, st, launches);
+        }
+        return expand_sweep<STRAT, ALGO, ET, WT, 8>(a, num_sms, st, launches);
+      }
+    }
   }
   return expand_u<STRAT, ALGO, ET, WT, kUnroll>(a, num_sms, st, launches);
 }
