@@ -1,5 +1,5 @@
 """Mean direction-optimizing GTEPS over the bench's first 16 sources for
-several switch factors (ZC_TUNE=do_alpha=X), K27."""
+several switch factors (zc_set_tuning do_alpha=X), K27."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2006_06890_b200 as zc

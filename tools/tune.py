@@ -1,4 +1,4 @@
-"""A/B the expansion schedules / knobs on one K27 graph (ZC_TUNE)."""
+"""A/B the expansion schedules / knobs on one K27 graph (zc_set_tuning specs)."""
 import argparse, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2006_06890_b200 as zc
