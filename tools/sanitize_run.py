@@ -38,4 +38,14 @@ run_partitions_local(rp, "bfs", 1, "direction-optimizing")
 r = zc.generate_rmat(12, 8, seed=1, symmetrize=True)
 zc.cc(r, "packed", collect_traffic=False)
 zc.cc(r, "compressed", collect_traffic=False)
+# round 2: work-efficient schedules, symmetric partitions with the fused
+# pre-filter and the remote-send count, the default pairs stream
+for s in ["merged", "merged-aligned", "packed", "compressed"]:
+    zc.cc(r, s, collect_traffic=False, schedule="afforest")
+    zc.sssp(g, src, s, collect_traffic=False, schedule="near-far", delta=7)
+sp = [generate_rmat_part(12, 2, k, seed=3, symmetrize=True) for k in range(2)]
+run_partitions_local(sp, "cc", 0, "merged-aligned", fused=True)
+run_partitions_local(sp, "bfs", 1, "merged-aligned", fused=True)
+wp = [generate_rmat_part(12, 2, k, seed=3, weights=(1, 9)) for k in range(2)]
+run_partitions_local(wp, "sssp", 1, "merged-aligned", fused=True)
 print("sanitize run ok")
