@@ -533,6 +533,7 @@ def variants_zerocopy(zc, dg, g, sources, oc, parity, args) -> dict:
         rs = None
         build_s = build["out_lists_s"] + build.get("in_lists_s", 0.0)
         pt.update(build)
+        pt["build_phases_ms"] = {k: round(v, 1) for k, v in dg.build_log()}
         pt["e2e_64_sources_gteps"] = trav64 / wall64 / 1e9
         pt["e2e_64_sources_incl_build_gteps"] = trav64 / (wall64 + build_s) / 1e9
         pt["pinned_host_bytes"] = (g.num_edges * 4 + build["out_line_stream_bytes"]

@@ -226,6 +226,10 @@ int zc_graph_compressed_index(const zc_graph *g, uint64_t *first_line);
  * (ZC_OPT_TRAFFIC_MODEL) keeps describing the reference's separate arrays, so
  * modelled runs read those. */
 int zc_graph_build_pairs(zc_graph *g);
+/* Wall-time log of the handle's one-time builds (compressed out / in streams):
+ * "phase milliseconds" lines in build order, NUL-terminated in buf (at most
+ * cap bytes); returns the bytes the whole log needs (>= 1). */
+int zc_graph_build_log(const zc_graph *g, char *buf, size_t cap);
 /* 1 if some list repeats a destination (traversal.py:182-188), cached. */
 int zc_graph_multigraph(zc_graph *g, int *out);
 

@@ -27,6 +27,7 @@ EXPORTED = (
     "zc_graph_destroy", "zc_graph_host_lists", "zc_graph_info", "zc_bfs", "zc_sssp",
     "zc_cc", "zc_run_log", "zc_host_alloc", "zc_host_free", "zc_generate_rmat",
     "zc_generate_uniform", "zc_set_options", "zc_set_tuning", "zc_run_traffic",
+    "zc_graph_build_log",
     "zc_run_profile", "zc_graph_evict", "zc_part_create",
     "zc_part_exchange_elem_bytes", "zc_part_begin", "zc_part_expand", "zc_part_apply",
     "zc_part_result", "zc_generate_rmat_part", "zc_pagerank", "zc_graph_multigraph",
@@ -111,6 +112,7 @@ def _declare(lib: C.CDLL) -> None:
         "zc_part_pull": (C.c_int, [P, C.c_void_p, C.POINTER(u64), C.POINTER(u64)]),
         "zc_run_log": (C.c_int, [P, P, P, u64]),
         "zc_set_options": (C.c_int, [P, u32]),
+        "zc_graph_build_log": (C.c_int, [P, C.c_char_p, C.c_size_t]),
         "zc_set_tuning": (C.c_int, [P, C.c_char_p]),
         "zc_run_profile": (C.c_int, [P, P, u64]),
         "zc_graph_evict": (C.c_int, [P]),

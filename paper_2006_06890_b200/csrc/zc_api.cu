@@ -131,14 +131,12 @@ static void prefault(void* p, size_t bytes) {
   for (auto& t : th) t.join();
 }
 
+static bool numa_disabled();
+
 void* pinned_list_alloc(int device, size_t bytes) {
-  static const bool numa_off = [] {
-    const char* env = getenv("ZC_NUMA");
-    return env && env[0] == '0';
-  }();
   bytes = std::max<size_t>(bytes, 1);
   if (bytes >= (64ull << 20)) {
-    const int node = numa_off ? -1 : gpu_numa_node(device);
+    const int node = numa_disabled() ? -1 : gpu_numa_node(device);
     void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
     if (p != MAP_FAILED) {
       bool ok = true;
@@ -164,6 +162,14 @@ void* pinned_list_alloc(int device, size_t bytes) {
     return nullptr;
   }
   return p;
+}
+
+static bool numa_disabled() {
+  static const bool off = [] {
+    const char* env = getenv("ZC_NUMA");
+    return env && env[0] == '0';
+  }();
+  return off;
 }
 
 // Host-resident managed lists (ZC_PLACE_ZEROCOPY_MANAGED).  The pages stay
@@ -292,6 +298,15 @@ static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n, bool over
 static double now_ms() {
   using namespace std::chrono;
   return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+void build_start(zc_graph* g) { g->build_t = now_ms(); }
+
+void build_mark(zc_graph* g, const char* phase) {
+  cudaDeviceSynchronize();
+  const double t = now_ms();
+  g->build_log.emplace_back(phase, t - g->build_t);
+  g->build_t = t;
 }
 
 }  // namespace zc
@@ -2432,6 +2447,21 @@ int zc_run_traffic(const zc_graph* g, uint64_t* hist, uint64_t cap) {
   const uint64_t n = std::min<uint64_t>(cap, g->log_hist.size() / 8);
   if (hist) std::copy(g->log_hist.begin(), g->log_hist.begin() + 8 * n, hist);
   return ZC_OK;
+}
+
+int zc_graph_build_log(const zc_graph* g, char* buf, size_t cap) {
+  if (!g || (!buf && cap)) {
+    set_error("null argument");
+    return ZC_ESTATE;
+  }
+  std::string out;
+  for (const auto& e : g->build_log) out += e.first + " " + std::to_string(e.second) + "\n";
+  if (cap) {
+    const size_t n = std::min(cap - 1, out.size());
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return static_cast<int>(std::min<size_t>(out.size() + 1, 0x7fffffff));
 }
 
 void* zc_host_alloc(size_t bytes) {

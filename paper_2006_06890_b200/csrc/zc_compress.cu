@@ -370,6 +370,7 @@ int place_stream(zc_graph* g, DevBuf* enc, size_t bytes, void** host_out, const 
       set_error("cannot allocate host memory for the compressed lists");
       return ZC_ENOMEM;
     }
+    build_mark(g, "pin_alloc");
     const void* d = nullptr;
     if (cudaMemcpy(host, enc->p, bytes, cudaMemcpyDefault) != cudaSuccess ||
         (g->placement != ZC_PLACE_HBM && host_list_device_ptr(host, &d) != ZC_OK)) {
@@ -384,6 +385,7 @@ int place_stream(zc_graph* g, DevBuf* enc, size_t bytes, void** host_out, const 
       dev = d;
     }
   }
+  build_mark(g, "d2h_copy");
   *host_out = host;
   *dev_out = dev;
   *hbm_out = hbm;
@@ -396,6 +398,7 @@ int install_in_lists(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted) {
   size_t bytes = 0;
   int rc = encode_stream(g->nv, d_in_off, x, 0, first_element_bits(g), &cpos, &enc, &bytes);
   if (rc) return rc;
+  build_mark(g, "in:size_place_encode");
   void* host = nullptr;
   const void* dev = nullptr;
   void* hbm = nullptr;
@@ -406,7 +409,9 @@ int install_in_lists(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted) {
   g->d_cpos_in = static_cast<uint64_t*>(cpos.release());
   g->d_in_off = d_in_off;
   g->cmp_in_bytes = bytes;
-  return alloc_pull_state(g);
+  rc = alloc_pull_state(g);
+  build_mark(g, "in:pull_state");
+  return rc;
 }
 
 int alloc_pull_state(zc_graph* g) {
@@ -431,21 +436,14 @@ int alloc_pull_state(zc_graph* g) {
 
 using namespace zc;
 
-extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes) {
-  if (!g) {
-    set_error("null graph handle");
-    return ZC_ESTATE;
-  }
-  if (g->eb != 4) {
-    set_error("compressed lists need 4-byte edges");
-    return ZC_EINVAL;
-  }
-  if (g->h_cmp) {
-    if (compressed_bytes) *compressed_bytes = g->cmp_bytes;
-    return ZC_OK;
-  }
+namespace {
+// The out-list stream.  keep_lists (unweighted graphs): hand the sorted device
+// copy of the raw lists to the caller (the in-list transpose reads it instead
+// of copying the lists from host memory again).
+int build_out_stream(zc_graph* g, DevBuf* keep_lists) {
   cudaSetDevice(g->device);
   ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
+  build_start(g);
   const uint64_t nv = g->nv, ne = g->ne;
   // weights ride along when they are 4-byte (SSSP on the compressed stream)
   const bool weighted = g->has_weights && g->wb == 4 && g->h_weights;
@@ -472,20 +470,25 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
     x.e64 = static_cast<const uint64_t*>(sorted.p);
     x.wmin = hr[0];
     ww = hr[1] > hr[0] ? 32 - __builtin_clz(hr[1] - hr[0]) : 0;
+    build_mark(g, "out:h2d_pairs");
     const int rc = sort_lists_device(8, nv, g->d_off, sorted.p);
     if (rc) return rc;
   } else {
     ZC_CUDA_TRY(cudaMalloc(&sorted.p, std::max<uint64_t>(ne, 1) * 4));
     ZC_CUDA_TRY(cudaMemcpy(sorted.p, g->h_edges, ne * 4, cudaMemcpyDefault));
+    build_mark(g, "out:h2d_copy");
     const int rc = sort_lists_device(4, nv, g->d_off, sorted.p);
     if (rc) return rc;
     x.e32 = static_cast<const uint32_t*>(sorted.p);
   }
+  build_mark(g, "out:sort");
   size_t bytes = 0;
   const uint32_t b0 = first_element_bits(g);
   int rc = encode_stream(nv, g->d_off, x, ww, b0, &cpos, &enc, &bytes);
   if (rc) return rc;
+  if (keep_lists && !weighted) keep_lists->p = sorted.release();
   cudaFree(sorted.release());
+  build_mark(g, "out:size_place_encode");
   void* host = nullptr;
   const void* dev = nullptr;
   void* hbm = nullptr;
@@ -499,6 +502,23 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
   g->cmp_ww = ww;
   g->cmp_b0 = b0;
   g->cmp_wmin = x.wmin;
+  return ZC_OK;
+}
+}  // namespace
+
+extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (g->eb != 4) {
+    set_error("compressed lists need 4-byte edges");
+    return ZC_EINVAL;
+  }
+  if (!g->h_cmp) {
+    const int rc = build_out_stream(g, nullptr);
+    if (rc) return rc;
+  }
   if (compressed_bytes) *compressed_bytes = g->cmp_bytes;
   return ZC_OK;
 }
@@ -512,14 +532,21 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
     if (compressed_bytes) *compressed_bytes = g->cmp_in_bytes;
     return ZC_OK;
   }
-  int rc = zc_graph_build_compressed(g, nullptr);
-  if (rc) return rc;
-  cudaSetDevice(g->device);
-  const uint64_t nv = g->nv, ne = g->ne;
+  if (g->eb != 4) {
+    set_error("compressed lists need 4-byte edges");
+    return ZC_EINVAL;
+  }
   if (g->nparts && (g->flags & ZC_F_DIRECTED)) {
     set_error("a directed partition's in-lists come from zc_part_build_in_lists");
     return ZC_EINVAL;
   }
+  const bool transpose = (g->flags & ZC_F_DIRECTED) != 0;
+  DevBuf out_e;  // the raw lists on the device (any order inside a list)
+  int rc = ZC_OK;
+  if (!g->h_cmp && (rc = build_out_stream(g, transpose ? &out_e : nullptr))) return rc;
+  cudaSetDevice(g->device);
+  build_start(g);
+  const uint64_t nv = g->nv, ne = g->ne;
   if (!(g->flags & ZC_F_DIRECTED)) {  // in-lists are the out-lists
     g->d_in_off = g->d_off;
     g->d_cpos_in = g->d_cpos;
@@ -527,9 +554,12 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
     g->cmp_in_bytes = g->cmp_bytes;
     g->in_alias = true;
   } else {
-    DevBuf out_e, in_e, deg, in_off, tmp;
-    ZC_CUDA_TRY(cudaMalloc(&out_e.p, std::max<uint64_t>(ne, 1) * 4));
-    ZC_CUDA_TRY(cudaMemcpy(out_e.p, g->h_edges, ne * 4, cudaMemcpyDefault));
+    DevBuf in_e, deg, in_off, tmp;
+    if (!out_e.p) {
+      ZC_CUDA_TRY(cudaMalloc(&out_e.p, std::max<uint64_t>(ne, 1) * 4));
+      ZC_CUDA_TRY(cudaMemcpy(out_e.p, g->h_edges, ne * 4, cudaMemcpyDefault));
+      build_mark(g, "in:h2d_copy");
+    }
     ZC_CUDA_TRY(cudaMalloc(&deg.p, std::max<uint64_t>(nv, 1) * 4));
     ZC_CUDA_TRY(cudaMemset(deg.p, 0, std::max<uint64_t>(nv, 1) * 4));
     k_in_count<<<kCmpGrid, 256>>>(ne, static_cast<uint32_t*>(out_e.p),
@@ -549,8 +579,10 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
     ZC_CUDA_TRY(cudaGetLastError());
     cudaFree(out_e.release());
     cudaFree(deg.release());
+    build_mark(g, "in:transpose");
     rc = sort_lists_device(4, nv, static_cast<uint64_t*>(in_off.p), in_e.p);
     if (rc) return rc;
+    build_mark(g, "in:sort");
     if ((rc = install_in_lists(g, static_cast<uint64_t*>(in_off.p),
                                static_cast<uint32_t*>(in_e.p))))
       return rc;

@@ -6,6 +6,8 @@
 #include <stdint.h>
 
 #include <thread>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/zcgraph.h"
@@ -115,6 +117,9 @@ struct zc_graph {
     int pairs = 1;    // SSSP on merged / merged-aligned / packed: build + read the pairs stream
   } tune;
   int multigraph = -1;  // cached duplicate-arc check (-1 unknown)
+  // one-time builds (compressed streams, pairs): wall ms per phase, in order
+  std::vector<std::pair<std::string, double>> build_log;
+  double build_t = 0;
   LoopGraph loop;
   uint64_t* d_log = nullptr;  // 4 * kLogCap
   // vertex-range partition (multi-GPU); nparts == 0 for a whole graph
@@ -151,6 +156,10 @@ struct zc_graph {
 namespace zc {
 // zc_api.cu
 void free_graph(zc_graph* g);
+// Build-phase timing: build_start resets the clock, build_mark(g, "x")
+// synchronizes the device and logs the wall ms since the previous mark.
+void build_start(zc_graph* g);
+void build_mark(zc_graph* g, const char* phase);
 int alloc_state(zc_graph* g);
 int finish_create(zc_graph* g);  // prefetch (UVM) + sync
 int init_partition(zc_graph* g, const zc_part_info* info);

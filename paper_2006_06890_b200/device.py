@@ -235,6 +235,17 @@ class DeviceGraph:
         N.check(N.lib().zc_graph_build_in_lists(self.handle, C.byref(nbytes)))
         return nbytes.value
 
+    def build_log(self) -> list:
+        """[(phase, wall ms)] of this handle's one-time builds (compressed out /
+        in-list streams), in order (zc_graph_build_log)."""
+        need = N.lib().zc_graph_build_log(self.handle, None, 0)
+        if need < 0:
+            N.check(need)
+        buf = C.create_string_buffer(max(need, 1))
+        N.lib().zc_graph_build_log(self.handle, buf, len(buf))
+        return [(ln.split()[0], float(ln.split()[1]))
+                for ln in buf.value.decode().splitlines() if ln.strip()]
+
     def link_bytes_requested(self) -> int:
         """Line-stream bytes the last compressed / direction-optimizing run's
         expansion kernels requested over the link (0 for other strategies)."""

@@ -16,6 +16,7 @@ print(f"build_compressed {time.time() - t:.2f}s bytes={nb}", flush=True)
 t = time.time()
 ni = dg.build_in_lists()
 print(f"build_in_lists {time.time() - t:.2f}s bytes={ni}", flush=True)
+print("phases (ms):", " ".join(f"{k}={v:.0f}" for k, v in dg.build_log()), flush=True)
 for nbytes in (nb, ni):
     t = time.time()
     p = N.lib().zc_host_alloc(nbytes)
