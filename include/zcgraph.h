@@ -176,7 +176,7 @@ int zc_cc(zc_graph *g, int strategy, int64_t *out, zc_stats *stats);
  *   zc_sssp_nearfar: the frontier holds only the improved vertices with
  *     dist < threshold (near set); the others wait marked (far pile); when
  *     the near set runs dry the threshold moves to the smallest waiting
- *     distance + delta (delta = 0: the default, 32).
+ *     distance + delta (delta = 0: the default, 16).
  *   zc_cc_afforest: union-find (Afforest's schedule): pass 1 unions every
  *     vertex with the neighbours of its list's first window, pass 2 only the
  *     vertices outside the largest component whose lists reach further;

@@ -78,7 +78,9 @@ static void convert_copy(void* dst, uint32_t dw, const void* src, uint32_t sw, u
 }
 
 void tune_params(ExpandArgs* a, const zc_graph* g) {
-  a->unroll = g->tune.unroll;
+  // the HBM control run is bound by its state gathers, not by list loads:
+  // occupancy beats loads in flight there (K27: U=4 115.7 GTEPS, U=8 102.2)
+  a->unroll = g->tune.unroll ? g->tune.unroll : g->placement == ZC_PLACE_HBM ? 4 : 0;
   a->ctas_per_sm = g->tune.ctas;
   a->chunk_sched = g->tune.sched;
   a->ld = g->tune.ld;
@@ -1142,9 +1144,11 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
   return ZC_OK;
 }
 
-// Default bucket width of the near-far SSSP schedule (weights in [8, 72] on
-// the bench graphs: about one mean weight; measured in DESIGN.md).
-constexpr uint64_t kNearFarDelta = 32;
+// Bucket width of near-far SSSP when the caller passes 0: measured over
+// 8..256 on U27 and a weighted K27 (weights 8..72, profiles/r02_delta_ab.txt),
+// 16 is within 3% of the best on every graph / strategy pair (32: up to 11%
+// slower; 8 does the least work but takes more iterations).
+constexpr uint64_t kNearFarDelta = 16;
 
 // Connected components by union-find, Afforest's schedule (Sutton et al.,
 // IPDPS'18) over the zero-copy lists (B200 extension; the reference's Jacobi

@@ -144,7 +144,7 @@ def sssp(g, source: int, strategy=AccessStrategy.MERGED_ALIGNED, *,
     (reference traversal.py:123-151); unreached vertices get INT64_MAX.
 
     ``schedule="near-far"`` (B200 extension) expands only the improved
-    vertices below a threshold that advances by ``delta`` (default 32) once
+    vertices below a threshold that advances by ``delta`` (default 16) once
     they run out: the same distances with less work; iteration counts differ
     from the reference's.
 
