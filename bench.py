@@ -785,14 +785,15 @@ def _part_series(part, algo, sources, strat, steps, warmup, world, device, *, ex
 
 
 def _gather_values_crc(r, world, device) -> str:
-    """crc32 of the concatenated owned slices (rank order = range order)."""
+    """The ranks' crc32s of their owned int64 slices, in rank (= range) order
+    (only the 8-character digests travel, not the slices)."""
+    import numpy as np
     import torch.distributed as dist
+    mine = (f"{zlib.crc32(np.ascontiguousarray(r.values, dtype='<i8')) & 0xffffffff:08x}"
+            if r.values is not None else "none")
     parts = [None] * world
-    dist.all_gather_object(parts, r.values.astype("<i8").tobytes() if r.values is not None else b"")
-    crc = 0
-    for b in parts:
-        crc = zlib.crc32(b, crc)
-    return f"{crc & 0xffffffff:08x}"
+    dist.all_gather_object(parts, mine)
+    return "-".join(parts)
 
 
 def _strip(d: dict) -> dict:

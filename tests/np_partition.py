@@ -161,7 +161,8 @@ def gloo_worker(rank, world, port, graph, algo, source, q, strategy="merged-alig
             eng = NumpyPartition(local_part(g, bounds, rank), bounds, rank,
                                  owned_in_lists(g, lo, hi))
             r = run_partition(eng, al, src, strategy, tensor_device=torch.device("cpu"))
-            results.append((r.lo, r.values, r.iterations, r.traversed_edges))
+            results.append((r.lo, r.values, r.iterations, r.traversed_edges, r.local_traversed,
+                            r.exchange_bytes, r.bottom_up_steps))
         q.put((rank, results))
     finally:
         dist.destroy_process_group()

@@ -35,6 +35,10 @@ def _run_world(world, graphs, algos, sources, strategy="merged-aligned"):
         iters = {p[2] for p in parts}
         trav = {tuple(p[3]) for p in parts}
         assert len(iters) == 1 and len(trav) == 1  # every rank agrees
+        # each rank streamed its own frontiers' lists: together the global work
+        assert sum(p[4] for p in parts) == sum(parts[0][3])
+        # bottom-up steps all-reduce the frontier bitmap: counted as sent bytes
+        assert all((p[5] > 0) == (p[6] > 0) for p in parts)
         merged.append((vals, iters.pop(), list(trav.pop())))
     return merged
 
