@@ -761,10 +761,12 @@ def _part_series(part, algo, sources, strat, steps, warmup, world, device, *, ex
     import torch
     from paper_2006_06890_b200.multi import run_partition
 
+    fused = exchange in ("fused", "fused-store")
+
     def one(i):
         return run_partition(part, algo, int(sources[i % len(sources)]), strat, stage_host=stage,
-                             fetch=fetch, buffers=None if exchange == "fused" else bufs,
-                             fused=exchange == "fused")
+                             fetch=fetch, buffers=None if fused else bufs, fused=fused,
+                             bfs_exchange="store" if exchange == "fused-store" else "bitmap")
 
     for i in range(warmup):
         one(i)
@@ -951,9 +953,10 @@ def main_partitioned(args, rank, world, device):
                         f"vertex-range partitioned over {world} ranks (edge-balanced), each "
                         "rank's u32 edge slice zero-copy in pinned host memory",
             "graph": f"kron{scale}", "scale": scale, "parallelism": f"vertex-partition{world}",
-            "exchange": ("fused: the expansion kernel stores each discovery (deduplicated per "
-                         "rank and level) straight into its owner's candidate buffer through "
-                         "CUDA-IPC peer pointers over NVLink; all-reduce of the counts"
+            "exchange": ("fused (bitmap OR over peer memory): every rank marks its "
+                         "discoveries in its own V-bit bitmap, each owner ORs the ranks' words "
+                         "over its range through CUDA-IPC peer pointers (NVLink) and applies "
+                         "them; one barrier + the counts all-reduce per level"
                          if args.exchange == "fused" else
                          "per level: NCCL reduce-scatter of u8 flags (MAX); all-reduce of counts"),
             "backend": args.backend}),
@@ -1020,11 +1023,12 @@ def configs4(args, rank, world, device, stage, parity, fused_ok=True) -> dict:
                        f"{world} ranks, each slice zero-copy in its rank's pinned host memory",
            "scaling": "strong", "gen_s": gen_s, "arcs": arcs}
     peak = world * PCIE_GEN5_X16_GBS
-    for algo, exch, steps in (("bfs", "fused", 2), ("bfs", "reduce-scatter", 2),
-                              ("cc", "reduce-scatter", 1), ("cc", "fused", 1)):
-        if exch == "fused" and not fused_ok:
+    for algo, exch, steps in (("bfs", "fused", 2), ("bfs", "fused-store", 2),
+                              ("bfs", "reduce-scatter", 2), ("cc", "reduce-scatter", 1),
+                              ("cc", "fused", 1)):
+        if exch.startswith("fused") and not fused_ok:
             continue
-        bufs = exchange_buffers(algo, world, part.stride, dev) if exch != "fused" else None
+        bufs = exchange_buffers(algo, world, part.stride, dev) if exch == "reduce-scatter" else None
         r = _part_series(part, algo, sources, "merged-aligned", steps, 1, world, device,
                          exchange=exch, bufs=bufs, stage=stage)
         key = f"{algo}/{exch}"
@@ -1036,9 +1040,9 @@ def configs4(args, rank, world, device, stage, parity, fused_ok=True) -> dict:
         out[key] = res
         del bufs
         torch.cuda.empty_cache()
-    for algo in ("bfs", "cc") if fused_ok else ():  # both exchanges: same iterations, work
-        a, b = out[f"{algo}/fused"], out[f"{algo}/reduce-scatter"]
-        parity[f"k{scale}sym_{algo}/fused_vs_reduce_scatter_work"] = (
+    for algo, ex in (("bfs", "fused"), ("bfs", "fused-store"), ("cc", "fused")) if fused_ok else ():
+        a, b = out[f"{algo}/{ex}"], out[f"{algo}/reduce-scatter"]  # same iterations and work
+        parity[f"k{scale}sym_{algo}/{ex}_vs_reduce_scatter_work"] = (
             a["iterations"] == b["iterations"]
             and a["traversed_edges_per_step"] == b["traversed_edges_per_step"])
     part.close()

@@ -369,6 +369,19 @@ int zc_part_fused_init(zc_graph *g, int algo, void *ipc_handle_out, void **local
 int zc_part_fused_connect(zc_graph *g, const void *ipc_handles, void *const *ptrs);
 int zc_part_fused_reset(zc_graph *g);
 int zc_part_fused_expand(zc_graph *g);
+/* BFS bitmap exchange (no collective, no remote stores): every rank marks its
+ * discoveries in its own global-V bitmap; each owner then ORs the ranks'
+ * words over its range, reading the peers' bitmaps through CUDA IPC (NVLink),
+ * and applies them -- V/8 bytes read per rank and level, coalesced.  Per
+ * iteration: zc_part_bitmap_expand; barrier; zc_part_bitmap_apply; barrier
+ * (the termination all-reduce).  init exports this rank's bitmap handle (64
+ * bytes, may be NULL) and its device address (may be NULL); connect opens the
+ * others' (nparts * 64 bytes, own slot ignored) or takes raw device pointers
+ * for parts in one process. */
+int zc_part_bitmap_init(zc_graph *g, void *ipc_handle_out, void **local_bitmap);
+int zc_part_bitmap_connect(zc_graph *g, const void *ipc_handles, void *const *ptrs);
+int zc_part_bitmap_expand(zc_graph *g);
+int zc_part_bitmap_apply(zc_graph *g, uint64_t *n_next, uint64_t *trav_next);
 
 /* Part `part` of the graph zc_generate_rmat builds with the same parameters
  * (same arcs, same lists), edge-balanced across nparts; bounds (nparts+1)

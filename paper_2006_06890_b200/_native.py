@@ -36,7 +36,8 @@ EXPORTED = (
     "zc_bfs_async", "zc_sssp_async", "zc_sync", "zc_graph_compressed_index",
     "zc_graph_build_in_lists", "zc_run_directions", "zc_run_link_bytes",
     "zc_part_build_in_lists", "zc_part_unvisited_in", "zc_part_frontier_bits", "zc_part_pull",
-    "zc_sssp_nearfar", "zc_cc_afforest",
+    "zc_sssp_nearfar", "zc_cc_afforest", "zc_part_bitmap_init", "zc_part_bitmap_connect",
+    "zc_part_bitmap_expand", "zc_part_bitmap_apply",
 )
 # every symbol include/zcprobe.h declares (the measurement tool library)
 PROBE_EXPORTED = ("zc_link_probe", "zc_read_probe", "zc_bulk_probe", "zc_vmm_host_probe",
@@ -133,6 +134,10 @@ def _declare(lib: C.CDLL) -> None:
         "zc_part_fused_connect": (C.c_int, [P, P, P]),
         "zc_part_fused_reset": (C.c_int, [P]),
         "zc_part_fused_expand": (C.c_int, [P]),
+        "zc_part_bitmap_init": (C.c_int, [P, P, C.POINTER(P)]),
+        "zc_part_bitmap_connect": (C.c_int, [P, P, P]),
+        "zc_part_bitmap_expand": (C.c_int, [P]),
+        "zc_part_bitmap_apply": (C.c_int, [P, C.POINTER(u64), C.POINTER(u64)]),
         "zc_generate_rmat_part": (C.c_int, [u32, u32, dbl, dbl, dbl, u64, C.c_int, i64, i64, u32, u32,
                                             i32, i32, P, C.POINTER(P)]),
     }

@@ -381,6 +381,8 @@ void zc::free_graph(zc_graph* g) {
   if (g->loop.exec) cudaGraphExecDestroy(g->loop.exec);
   if (g->loop.graph) cudaGraphDestroy(g->loop.graph);
   cudaFree(g->d_log);
+  for (void* p : g->ipc_opened_sent) cudaIpcCloseMemHandle(p);
+  cudaFree(g->d_peer_sent);
   for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
   cudaFree(g->d_mine);
   cudaFree(g->d_peers);
@@ -1718,20 +1720,29 @@ int zc_part_begin(zc_graph* g, int algo, uint64_t src, int strategy, uint64_t* n
   return ZC_OK;
 }
 
-static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
+enum PartExchange { kExchReduceScatter = 0, kExchStore = 1, kExchBitmap = 2 };
+
+static int part_expand_impl(zc_graph* g, void* exch, int mode) {
   if (!g || !g->nparts || g->p_algo < 0) {
     set_error("zc_part_begin first");
     return ZC_ESTATE;
   }
+  const bool fused = mode == kExchStore;
   if (fused && (!g->d_peers || g->fused_algo != g->p_algo)) {
     set_error("fused exchange not initialised for this algorithm (zc_part_fused_init/connect)");
+    return ZC_ESTATE;
+  }
+  if (mode == kExchBitmap && (!g->d_peer_sent || g->p_algo != kBfs)) {
+    set_error("bitmap exchange: a bfs run and zc_part_bitmap_init/connect first");
     return ZC_ESTATE;
   }
   DeviceGuard dg(g->device);
   cudaStream_t st = g->stream;
   const int algo = g->p_algo;
   const size_t xb = zc_part_exchange_elem_bytes(algo);
-  if (!fused) {
+  if (mode == kExchBitmap) {
+    ZC_CUDA_TRY(cudaMemsetAsync(g->d_sent, 0, (g->global_nv + 31) / 32 * 4, st));
+  } else if (!fused) {
     ZC_CUDA_TRY(launch_fill_exchange(algo, exch, g->nparts * g->stride, st, &g->p_launches));
     g->p_xbytes += (g->nparts - 1) * g->stride * xb;  // this rank's reduce-scatter send
   } else if (algo == kBfs) {
@@ -1769,7 +1780,8 @@ static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
   a.nparts = g->nparts;
   a.stride = g->stride;
   a.peers = fused ? g->d_peers : nullptr;
-  a.sent = fused && algo == kBfs ? g->d_sent : nullptr;
+  a.sent = (fused && algo == kBfs) || mode == kExchBitmap ? g->d_sent : nullptr;
+  a.sent_only = mode == kExchBitmap;
   a.lbest = fused && algo != kBfs ? g->d_lbest : nullptr;
   a.wcnt = g->d_wcnt;
   a.wpre = g->d_wpre;
@@ -1804,7 +1816,9 @@ static int part_expand_impl(zc_graph* g, void* exch, bool fused) {
   return ZC_OK;
 }
 
-int zc_part_expand(zc_graph* g, void* exch) { return part_expand_impl(g, exch, false); }
+int zc_part_expand(zc_graph* g, void* exch) {
+  return part_expand_impl(g, exch, kExchReduceScatter);
+}
 
 int zc_part_fused_init(zc_graph* g, int algo, void* ipc_handle, void** local) {
   if (!g || !g->nparts) {
@@ -1873,9 +1887,13 @@ int zc_part_fused_reset(zc_graph* g) {
   return ZC_OK;
 }
 
-int zc_part_fused_expand(zc_graph* g) { return part_expand_impl(g, nullptr, true); }
+int zc_part_fused_expand(zc_graph* g) { return part_expand_impl(g, nullptr, kExchStore); }
 
-int zc_part_apply(zc_graph* g, const void* mine, uint64_t* n_next, uint64_t* trav_next) {
+// Owner merge of the iteration's candidates -- a reduced slice (`mine`,
+// device) or, mine == NULL, the OR of every rank's discovery bitmap (BFS
+// bitmap exchange) -- then the next frontier's compaction.
+static int part_apply_impl(zc_graph* g, const void* mine, uint64_t* n_next,
+                           uint64_t* trav_next) {
   if (!g || !g->nparts || g->p_algo < 0 || g->p_iter == 0) {
     set_error("zc_part_expand first");
     return ZC_ESTATE;
@@ -1883,8 +1901,16 @@ int zc_part_apply(zc_graph* g, const void* mine, uint64_t* n_next, uint64_t* tra
   DeviceGuard dg(g->device);
   cudaStream_t st = g->stream;
   const int algo = g->p_algo;
-  ZC_CUDA_TRY(launch_part_apply(algo, mine, g->nv, g->d_state, g->d_flags,
-                                static_cast<uint32_t>(g->p_iter), st, &g->p_launches));
+  if (mine) {
+    ZC_CUDA_TRY(launch_part_apply(algo, mine, g->nv, g->d_state, g->d_flags,
+                                  static_cast<uint32_t>(g->p_iter), st, &g->p_launches));
+  } else {
+    ZC_CUDA_TRY(launch_part_pull_apply(g->d_peer_sent, g->nparts, g->lo, g->nv, g->d_state,
+                                       g->d_flags, static_cast<uint32_t>(g->p_iter),
+                                       g->num_sms, st, &g->p_launches));
+    // the words of this range read from every other rank
+    g->p_xbytes += (g->nparts - 1) * ((g->nv + 31) / 32 + 1) * 4;
+  }
   CompactArgs c{};
   c.flags = g->d_flags;
   c.nv = g->nv;
@@ -1908,6 +1934,71 @@ int zc_part_apply(zc_graph* g, const void* mine, uint64_t* n_next, uint64_t* tra
   if (n_next) *n_next = g->h_ctr[kCtrNext];
   if (trav_next) *trav_next = g->h_ctr[kCtrTrav];
   return ZC_OK;
+}
+
+
+int zc_part_apply(zc_graph* g, const void* mine, uint64_t* n_next, uint64_t* trav_next) {
+  if (!mine) {
+    set_error("null exchange slice");
+    return ZC_EINVAL;
+  }
+  return part_apply_impl(g, mine, n_next, trav_next);
+}
+
+int zc_part_bitmap_init(zc_graph* g, void* ipc_handle, void** local) {
+  if (!g || !g->nparts) {
+    set_error("not a partition handle");
+    return ZC_ESTATE;
+  }
+  DeviceGuard dg(g->device);
+  if (!g->d_sent) ZC_CUDA_TRY(cudaMalloc(&g->d_sent, (g->global_nv + 31) / 32 * 4 + 4));
+  if (!g->d_peer_sent)
+    ZC_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&g->d_peer_sent), g->nparts * sizeof(void*)));
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    ZC_CUDA_TRY(cudaIpcGetMemHandle(&h, g->d_sent));
+    memcpy(ipc_handle, &h, sizeof(h));
+  }
+  if (local) *local = g->d_sent;
+  return ZC_OK;
+}
+
+int zc_part_bitmap_connect(zc_graph* g, const void* handles, void* const* ptrs) {
+  if (!g || !g->d_peer_sent) {
+    set_error("zc_part_bitmap_init first");
+    return ZC_ESTATE;
+  }
+  DeviceGuard dg(g->device);
+  for (void* p : g->ipc_opened_sent) cudaIpcCloseMemHandle(p);
+  g->ipc_opened_sent.clear();
+  std::vector<const void*> peers(g->nparts);
+  for (uint32_t k = 0; k < g->nparts; ++k) {
+    if (k == g->part) {
+      peers[k] = g->d_sent;
+    } else if (ptrs) {
+      peers[k] = ptrs[k];  // same-process device pointers (one-GPU validation)
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, static_cast<const char*>(handles) + k * sizeof(h), sizeof(h));
+      void* p = nullptr;
+      ZC_CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      g->ipc_opened_sent.push_back(p);
+      peers[k] = p;
+    }
+  }
+  ZC_CUDA_TRY(cudaMemcpy(g->d_peer_sent, peers.data(), g->nparts * sizeof(void*),
+                         cudaMemcpyHostToDevice));
+  return ZC_OK;
+}
+
+int zc_part_bitmap_expand(zc_graph* g) { return part_expand_impl(g, nullptr, kExchBitmap); }
+
+int zc_part_bitmap_apply(zc_graph* g, uint64_t* n_next, uint64_t* trav_next) {
+  if (!g || !g->d_peer_sent) {
+    set_error("zc_part_bitmap_init / connect first");
+    return ZC_ESTATE;
+  }
+  return part_apply_impl(g, nullptr, n_next, trav_next);
 }
 
 int zc_part_unvisited_in(const zc_graph* g, uint64_t* in_edges) {

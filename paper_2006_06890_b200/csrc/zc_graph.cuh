@@ -131,6 +131,10 @@ struct zc_graph {
   void* d_mine = nullptr;
   void** d_peers = nullptr;
   uint32_t* d_sent = nullptr;  // BFS: discoveries already sent this iteration
+  // BFS bitmap exchange: the ranks' `sent` bitmaps (device array of nparts
+  // pointers; peers' through CUDA IPC), read by each owner for its range
+  const uint32_t** d_peer_sent = nullptr;
+  std::vector<void*> ipc_opened_sent;
   void* d_lbest = nullptr;     // SSSP / CC: best candidate sent per global vertex this iteration
   std::vector<void*> ipc_opened;
   int fused_algo = -1;

@@ -167,6 +167,7 @@ struct ExpandArgs {
   // `sent` dedups BFS discoveries per iteration (global V bits)
   void* const* peers;
   uint32_t* sent;
+  int sent_only;  // BFS bitmap exchange: discoveries only set `sent` bits
   // fused SSSP / CC: this rank's best candidate per global vertex this
   // iteration (u64 / u32, all ones = none); only improvements go to the owner
   void* lbest;
@@ -247,6 +248,12 @@ cudaError_t launch_fill_exchange(int algo, void* x, uint64_t n, cudaStream_t st,
                                  uint64_t* launches);
 cudaError_t launch_part_apply(int algo, const void* mine, uint64_t nlocal, void* state,
                               uint8_t* flags, uint32_t iter, cudaStream_t st, uint64_t* launches);
+// BFS bitmap exchange: OR the nparts ranks' discovery bitmaps over this
+// part's range [lo, lo + nlocal) (peer memory) and apply them like
+// launch_part_apply.
+cudaError_t launch_part_pull_apply(const uint32_t* const* sent, uint32_t nparts, uint64_t lo,
+                                   uint64_t nlocal, void* state, uint8_t* flags, uint32_t iter,
+                                   int num_sms, cudaStream_t st, uint64_t* launches);
 // Fused exchange accounting: how many global vertices outside [lo, hi) this
 // rank sent a candidate to this iteration -- set bits of the BFS `sent`
 // bitmap (elem_bytes 0) or entries of `lbest` other than all-ones (4 / 8) --

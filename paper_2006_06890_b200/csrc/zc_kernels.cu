@@ -251,6 +251,7 @@ struct Visit<kBfs + kPartAlgo> {
       uint32_t* word = a.sent + (w >> 5);
       const uint32_t bit = 1u << (w & 31);
       if ((*word & bit) || (atomicOr(word, bit) & bit)) return;
+      if (a.sent_only) return;  // bitmap exchange: the owner reads the bit
     }
     *cand_slot<uint8_t>(a, w) = 1;
   }
@@ -2016,6 +2017,40 @@ cudaError_t launch_part_apply(int algo, const void* mine, uint64_t nlocal, void*
     case kSssp: k_part_apply<kSssp><<<g, 256, 0, st>>>(mine, nlocal, state, flags, iter); break;
     default: k_part_apply<kCc><<<g, 256, 0, st>>>(mine, nlocal, state, flags, iter); break;
   }
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+// Thread per 32-vertex word of the owned range: OR of every rank's bit word
+// (peer loads over NVLink, coalesced across threads), applied like
+// k_part_apply<kBfs>.
+__global__ void k_part_pull_apply(const uint32_t* const* sent, uint32_t nparts, uint64_t lo,
+                                  uint64_t n, uint32_t* level, uint8_t* flags, uint32_t iter) {
+  const uint64_t w0 = lo >> 5, w1 = (lo + n + 31) >> 5;
+  for (uint64_t w = w0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < w1;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t x = 0;
+    for (uint32_t k = 0; k < nparts; ++k) x |= sent[k][w];
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      const uint64_t v = (w << 5) + b;
+      if (v < lo || v >= lo + n) continue;
+      const uint64_t lv = v - lo;
+      if (level[lv] == kUnreached32) {
+        level[lv] = iter;
+        flags[lv] = 1;
+      }
+    }
+  }
+}
+
+cudaError_t launch_part_pull_apply(const uint32_t* const* sent, uint32_t nparts, uint64_t lo,
+                                   uint64_t nlocal, void* state, uint8_t* flags, uint32_t iter,
+                                   int num_sms, cudaStream_t st, uint64_t* launches) {
+  if (nlocal == 0) return cudaSuccess;
+  k_part_pull_apply<<<num_sms * 8, 256, 0, st>>>(sent, nparts, lo, nlocal,
+                                                  static_cast<uint32_t*>(state), flags, iter);
   *launches += 1;
   return cudaGetLastError();
 }

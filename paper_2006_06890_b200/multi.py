@@ -206,6 +206,30 @@ class CudaPartition:
     def fused_expand(self) -> None:
         N.check(N.lib().zc_part_fused_expand(self._h))
 
+    # -- BFS bitmap exchange (each owner ORs the ranks' discovery bitmaps)
+    def bitmap_init(self) -> tuple[bytes, int]:
+        """(IPC handle, device address) of this part's discovery bitmap."""
+        handle = (C.c_char * 64)()
+        local = C.c_void_p()
+        N.check(N.lib().zc_part_bitmap_init(self._h, handle, C.byref(local)))
+        return bytes(handle), local.value
+
+    def bitmap_connect(self, handles: Optional[Sequence[bytes]] = None,
+                       ptrs: Optional[Sequence[int]] = None) -> None:
+        if ptrs is not None:
+            arr = (C.c_void_p * len(ptrs))(*ptrs)
+            N.check(N.lib().zc_part_bitmap_connect(self._h, None, arr))
+        else:
+            N.check(N.lib().zc_part_bitmap_connect(self._h, b"".join(handles), None))
+
+    def bitmap_expand(self) -> None:
+        N.check(N.lib().zc_part_bitmap_expand(self._h))
+
+    def bitmap_apply(self) -> tuple[int, int]:
+        n, t = C.c_uint64(), C.c_uint64()
+        N.check(N.lib().zc_part_bitmap_apply(self._h, C.byref(n), C.byref(t)))
+        return n.value, t.value
+
     def apply_ptr(self, ptr: int) -> tuple[int, int]:
         n, t = C.c_uint64(), C.c_uint64()
         N.check(N.lib().zc_part_apply(self._h, ptr, C.byref(n), C.byref(t)))
@@ -276,21 +300,29 @@ def _torch_dtype(algo: str):
 
 def run_partition(engine: Engine, algo: str, source: int, strategy, *, group=None,
                   tensor_device=None, stage_host: bool = False, fetch: bool = True,
-                  buffers=None, fused: bool = False) -> PartResult:
+                  buffers=None, fused: bool = False, bfs_exchange: str = "bitmap"
+                  ) -> PartResult:
     """SPMD driver: call on every rank of `group` with that rank's engine.
 
     stage_host: run the collectives on host copies of the exchange buffers
     (gloo; lets several ranks share one GPU in tests).  fetch=False skips the
     download of the owned values (timing of the traversal loop alone).
     buffers: reusable (exch, mine) tensors from exchange_buffers().
+    fused: no collective on the data path -- BFS: each owner ORs the ranks'
+    discovery bitmaps over its range through peer memory (bfs_exchange
+    "bitmap") or the expansion stores each discovery into its owner's buffer
+    ("store"); SSSP / CC: remote atomicMin of each locally improved candidate.
     """
     import torch
     import torch.distributed as dist
 
     if algo not in ALGO_IDS:
         raise ValueError(f"unknown algorithm {algo!r}")
+    if bfs_exchange not in ("bitmap", "store"):
+        raise ValueError("bfs_exchange must be 'bitmap' or 'store'")
     if fused:
-        return _run_partition_fused(engine, algo, source, strategy, group, fetch)
+        return _run_partition_fused(engine, algo, source, strategy, group, fetch,
+                                    algo == "bfs" and bfs_exchange == "bitmap")
     nparts = dist.get_world_size(group)
     stride = engine.stride
     dev = tensor_device if tensor_device is not None else torch.device("cuda", engine.device)
@@ -382,23 +414,28 @@ def pull_now(iteration: int, frontier_out_edges: int, unvisited_in_edges: int,
     return iteration > 1 and frontier_out_edges * alpha > unvisited_in_edges
 
 
-def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartResult:
-    """Fused exchange: the expand kernel stores / atomicMin's each candidate
-    directly into its owner's buffer over NVLink (CUDA IPC peer pointers);
-    two barriers per level replace the reduce-scatter."""
+def _run_partition_fused(engine, algo, source, strategy, group, fetch, bitmap) -> PartResult:
+    """Fused exchange over peer memory (CUDA IPC pointers; NVLink between
+    GPUs).  bitmap (BFS): every rank marks discoveries in its own global
+    bitmap, each owner ORs the ranks' words over its range -- one barrier and
+    the counts all-reduce per level.  Otherwise the expand kernel stores /
+    atomicMin's each candidate into its owner's buffer; two barriers per
+    level replace the reduce-scatter."""
     import torch
     import torch.distributed as dist
 
     dev = torch.device("cuda", engine.device)
-    if getattr(engine, "_fused_for", None) == algo:  # peers opened by an earlier run
+    key = "bitmap" if bitmap else algo
+    if getattr(engine, "_fused_for", None) == key:  # peers opened by an earlier run
         mine = engine._fused_mine
-    else:  # once per (engine, algorithm): export, exchange and open the IPC handles
-        handle, mine = engine.fused_init(algo)
+    else:  # once per (engine, mode): export, exchange and open the IPC handles
+        handle, mine = engine.bitmap_init() if bitmap else engine.fused_init(algo)
+        connect = engine.bitmap_connect if bitmap else engine.fused_connect
         handles = [None] * dist.get_world_size(group)
         dist.all_gather_object(handles, handle, group=group)
         err = None
         try:
-            engine.fused_connect(handles=handles)
+            connect(handles=handles)
         except RuntimeError as exc:  # e.g. no peer access between these GPUs
             err = exc
         # every rank learns whether all peers opened, so none waits on a dead exchange
@@ -407,7 +444,7 @@ def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartRe
         failed = [m for m in status if m is not None]
         if failed:
             raise RuntimeError(f"fused exchange unavailable: {failed[0]}")
-        engine._fused_for, engine._fused_mine = algo, mine
+        engine._fused_for, engine._fused_mine = key, mine
     cdev = torch.device("cpu") if dist.get_backend(group) == "gloo" else dev
     counts = torch.zeros(2, dtype=torch.int64, device=cdev)
 
@@ -447,6 +484,12 @@ def _run_partition_fused(engine, algo, source, strategy, group, fetch) -> PartRe
             torch.cuda.current_stream(dev).synchronize()
             n, t, m = global_counts3(*engine.pull(bits))
             continue
+        if bitmap:
+            engine.bitmap_expand()  # own bitmap zeroed, then this rank's discoveries
+            sync_all()              # every rank's bitmap complete
+            # the counts all-reduce is the barrier before the bitmaps are reused
+            n, t, m = global_counts3(*engine.bitmap_apply())
+            continue
         engine.fused_reset()
         sync_all()              # every owner buffer reset before anyone writes
         engine.fused_expand()   # kernel done (its peer stores performed) on return
@@ -465,7 +508,8 @@ def exchange_buffers(algo: str, nparts: int, stride: int, device):
 
 
 def run_partitions_local(engines: Sequence[Engine], algo: str, source: int, strategy,
-                         fused: bool = False) -> tuple[np.ndarray, int, list]:
+                         fused: bool = False, bfs_exchange: str = "bitmap"
+                         ) -> tuple[np.ndarray, int, list]:
     """All partitions in one process (one device): the reduce-scatter becomes a
     host-driven reduction over the stacked exchange buffers (or, fused, the
     expand kernels write into each other's buffers by device pointer).  Used to
@@ -492,6 +536,25 @@ def run_partitions_local(engines: Sequence[Engine], algo: str, source: int, stra
         nt = [e.pull(bits) for e in engines]
         return sum(x[0] for x in nt), sum(x[1] for x in nt)
 
+    if fused and algo == "bfs" and bfs_exchange == "bitmap":
+        ptrs = [e.bitmap_init()[1] for e in engines]
+        for e in engines:
+            e.bitmap_connect(ptrs=ptrs)
+        nt = [e.begin(algo, source, strategy) for e in engines]
+        n, t = sum(x[0] for x in nt), sum(x[1] for x in nt)
+        iters, trav = 0, []
+        while n > 0:
+            iters += 1
+            trav.append(t)
+            if dobfs and pull_now(iters, t, unvisited_in()):
+                n, t = pull_all()
+                continue
+            for e in engines:
+                e.bitmap_expand()
+            nt = [e.bitmap_apply() for e in engines]
+            n, t = sum(x[0] for x in nt), sum(x[1] for x in nt)
+        values = np.concatenate([e.result() for e in engines])
+        return values, iters, trav
     if fused:
         locals_ = [e.fused_init(algo)[1] for e in engines]
         for e in engines:

@@ -266,17 +266,19 @@ def test_cuda_partitions_match_reference(nparts):
     assert not bad, bad[:8]
 
 
-@pytest.mark.parametrize("nparts", [2, 3])
-def test_cuda_partitions_fused_exchange(nparts):
-    """Fused exchange (expand writes into the owners' buffers by pointer) on
-    one GPU: identical values / iterations / traversed edges."""
+@pytest.mark.parametrize("nparts,bfs_exchange", [(2, "bitmap"), (3, "bitmap"), (2, "store"),
+                                                 (3, "store")])
+def test_cuda_partitions_fused_exchange(nparts, bfs_exchange):
+    """Fused exchanges on one GPU (peer pointers within the device): BFS
+    bitmap OR or candidate stores, SSSP / CC remote atomicMin after the local
+    pre-filter -- identical values / iterations / traversed edges."""
     bad = []
     for c in [c for c in CASES if c.tag.startswith(("c8_", "pl_")) or c.index < 11]:
         b = edge_balanced_bounds(c.graph.offsets, nparts)
         engines = [CudaPartition(local_part(c.graph, b, k), b, k) for k in range(nparts)]
         for s in ("merged-aligned", "packed"):
             vals, iters, trav = run_partitions_local(engines, c.algo, max(c.source, 0), s,
-                                                     fused=True)
+                                                     fused=True, bfs_exchange=bfs_exchange)
             if not (np.array_equal(vals, c.values) and iters == c.iterations
                     and trav == c.traversed):
                 bad.append((c.tag, c.index, s))
@@ -324,9 +326,9 @@ def test_symmetric_rmat_partition_generator_matches_whole_graph():
             assert np.array_equal(np.asarray(got.edges), np.asarray(ref.edges))
         for algo in ("bfs", "cc"):
             ref = oracle.run(algo, g, src, threads=8)
-            for fused in (False, True):
+            for fused, bx in ((False, "bitmap"), (True, "bitmap"), (True, "store")):
                 vals, iters, trav = run_partitions_local(parts, algo, src, "merged-aligned",
-                                                         fused=fused)
+                                                         fused=fused, bfs_exchange=bx)
                 assert np.array_equal(vals, ref.values), (nparts, algo, fused)
                 assert iters == ref.iterations and trav == ref.traversed_edges
         for p in parts:

@@ -33,10 +33,12 @@ def _worker(rank, world, port, q, srcs):
                                  (False, "bfs", "direction-optimizing")):
             part = generate_rmat_part(14, world, rank, 16, seed=21, symmetrize=sym, device=0)
             bufs = exchange_buffers(algo, world, part.stride, torch.device("cuda", 0))
-            for fused in (False, True):
+            for fused, bx in ((False, "bitmap"), (True, "bitmap"), (True, "store")):
+                if bx == "store" and (algo != "bfs" or not fused):
+                    continue
                 r = run_partition(part, algo, srcs[sym], strat, stage_host=True, buffers=bufs,
-                                  fused=fused)
-                out.append((sym, algo, strat, fused, r.values, r.iterations,
+                                  fused=fused, bfs_exchange=bx)
+                out.append((sym, algo, strat, f"{fused}/{bx}", r.values, r.iterations,
                             list(r.traversed_edges), r.exchange_bytes, r.local_traversed))
             part.close()
         q.put((rank, out))
