@@ -2501,7 +2501,7 @@ int zc_set_tuning(zc_graph* g, const char* spec) {
     const size_t eq = kv.find('=');
     const std::string k = kv.substr(0, eq);
     const std::string v = eq == std::string::npos ? "" : kv.substr(eq + 1);
-    if (k == "unroll" && (v == "2" || v == "4" || v == "8")) t.unroll = std::stoi(v);
+    if (k == "unroll" && (v == "2" || v == "4" || v == "8" || v == "16")) t.unroll = std::stoi(v);
     else if (k == "ctas") t.ctas = std::max(0, atoi(v.c_str()));
     else if (k == "sched" && (v == "chunk" || v == "sweep")) t.sched = v == "chunk";
     else if (k == "loop" && (v == "host" || v == "device")) t.host_loop = v == "host";

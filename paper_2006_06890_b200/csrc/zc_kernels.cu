@@ -1665,9 +1665,10 @@ struct SweepUnroll {
       (STRAT == kMergedAligned || STRAT == kMerged || STRAT == kPacked) &&
       !AlgoTraits<ALGO>::pull && ALGO != kPr &&
       ((sizeof(ET) == 4 && sizeof(WT) == 4) || IsPair<WT>::value);
+  static constexpr bool raw_line = STRAT == kMergedAligned || STRAT == kMerged;
   static constexpr int value =
-      (STRAT == kMergedAligned || STRAT == kMerged) &&
-              (AlgoTraits<ALGO>::base == kBfs || AlgoTraits<ALGO>::base == kCc) &&
+      raw_line && ALGO == kBfs ? 16
+      : raw_line && (AlgoTraits<ALGO>::base == kBfs || AlgoTraits<ALGO>::base == kCc) &&
               !AlgoTraits<ALGO>::uf
           ? 8
           : 4;
@@ -1683,17 +1684,22 @@ cudaError_t expand_t(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t
     return cudaGetLastError();
   }
   // Windows per warp batch of the raw-list sweeps.  Merged / merged-aligned
-  // BFS and CC take 8 by default: twice the loads in flight per warp, and
-  // adjacent lists' windows (which share lines) issued back to back by one
-  // warp, so the L1 / L2 merge more of the reference's duplicate line requests
-  // (profiles/r02_unroll_ab.txt, K27: BFS merged-aligned 10.18 -> 10.36 GTEPS,
-  // merged 7.48 -> 8.10; CC-K27-sym merged-aligned 11.51 -> 11.77 work-GTEPS;
-  // SSSP and packed unchanged or slower at 8).  zc_set_tuning unroll=2|4|8
-  // and ld=0..3 are A/B variants.
+  // BFS take 16 by default, CC (and partitioned BFS) 8: more loads in flight
+  // per warp, and adjacent lists' windows (which share lines) issued back to
+  // back by one warp, so the L1 / L2 merge more of the reference's duplicate
+  // line requests (profiles/r02_unroll_ab.txt, K27 BFS merged-aligned: 4 -> 8
+  // +1.8 %, 8 -> 16 +2.1 % (108 registers, 2 CTAs / SM); merged +8 %, +7 %;
+  // CC-K27-sym merged-aligned 4 -> 8 +2.3 %, 8 -> 16 -0.9 %; SSSP and packed
+  // unchanged or slower above 4).  zc_set_tuning unroll=2|4|8|16 and ld=0..3
+  // are A/B variants.
   if constexpr (SweepUnroll<STRAT, ALGO, ET, WT>::tunable) {
     if (!a.chunk_sched) {
       const int u = a.unroll ? a.unroll : SweepUnroll<STRAT, ALGO, ET, WT>::value;
       if (u == 2) return expand_sweep<STRAT, ALGO, ET, WT, 2>(a, num_sms, st, launches);
+      if constexpr ((STRAT == kMergedAligned || STRAT == kMerged) &&
+                    (ALGO == kBfs || ALGO == kCc)) {
+        if (u == 16) return expand_sweep<STRAT, ALGO, ET, WT, 16>(a, num_sms, st, launches);
+      }
       if (u == 8) {
         if constexpr (ALGO == kBfs && STRAT != kPacked) {
           if (a.ld == 0) return expand_sweep<STRAT, ALGO, ET, WT, 8, 0>(a, num_sms, st, launches);
