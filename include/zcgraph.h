@@ -270,7 +270,9 @@ int zc_set_options(zc_graph *g, uint32_t options);
  * "do_alpha=X" (direction-optimizing switch factor), "ld=0..3" (load flavour of
  * the raw-list BFS sweeps: L1::no_allocate, L1-cached, read-only path,
  * L1::evict_first), "pairs=0|1" (SSSP reads the separate edge and weight
- * arrays / the interleaved pairs stream).  NULL or "" resets the
+ * arrays / the interleaved pairs stream), "carveout=0..100" (the sweeps'
+ * preferred shared-memory carveout; no measurable effect on K27 BFS).
+ * "unroll" also takes 16 (merged / merged-aligned BFS and CC).  NULL or "" resets the
  * defaults; an unknown entry is ZC_EINVAL.  Read by the run path; nothing is
  * taken from the environment. */
 int zc_set_tuning(zc_graph *g, const char *spec);

@@ -83,6 +83,7 @@ void tune_params(ExpandArgs* a, const zc_graph* g) {
   a->unroll = g->tune.unroll ? g->tune.unroll : g->placement == ZC_PLACE_HBM ? 4 : 0;
   a->ctas_per_sm = g->tune.ctas;
   a->chunk_sched = g->tune.sched;
+  a->carveout = g->tune.carveout;
   a->ld = g->tune.ld;
 }
 
@@ -654,7 +655,8 @@ int build_loop_graph(zc_graph* g, int algo, int strategy, int ebytes, const Expa
                      const CompactArgs& c) {
   LoopGraph& L = g->loop;
   if (L.exec && L.algo == algo && L.strategy == strategy && L.ebytes == ebytes &&
-      L.unroll == base.unroll && L.ctas == base.ctas_per_sm && L.ld == base.ld)
+      L.unroll == base.unroll && L.ctas == base.ctas_per_sm && L.ld == base.ld &&
+      L.carveout == base.carveout)
     return ZC_OK;
   if (L.exec) cudaGraphExecDestroy(L.exec);
   if (L.graph) cudaGraphDestroy(L.graph);
@@ -698,6 +700,7 @@ int build_loop_graph(zc_graph* g, int algo, int strategy, int ebytes, const Expa
   L.unroll = base.unroll;
   L.ctas = base.ctas_per_sm;
   L.ld = base.ld;
+  L.carveout = base.carveout;
   L.launches_per_iter = launches + 3;
   return ZC_OK;
 }
@@ -2508,6 +2511,8 @@ int zc_set_tuning(zc_graph* g, const char* spec) {
     else if (k == "do_alpha" && atof(v.c_str()) > 0) t.do_alpha = atof(v.c_str());
     else if (k == "ld" && v.size() == 1 && v[0] >= '0' && v[0] <= '3') t.ld = v[0] - '0';
     else if (k == "pairs" && (v == "0" || v == "1")) t.pairs = v == "1";
+    else if (k == "carveout" && !v.empty() && atoi(v.c_str()) >= 0 && atoi(v.c_str()) <= 100)
+      t.carveout = atoi(v.c_str());
     else {
       set_error("unknown tuning entry '" + kv + "'");
       return ZC_EINVAL;

@@ -15,7 +15,7 @@
 
 // Instantiated device-driven level loop (zc_api.cu build_loop_graph).
 struct LoopGraph {
-  int algo = -1, strategy = -1, ebytes = 0, unroll = 0, ctas = 0, ld = -1;
+  int algo = -1, strategy = -1, ebytes = 0, unroll = 0, ctas = 0, ld = -1, carveout = -1;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   uint64_t launches_per_iter = 0;
@@ -115,6 +115,7 @@ struct zc_graph {
     double do_alpha = 2.0;  // direction-optimizing switch factor
     int ld = -1;      // load flavour override of the raw BFS sweeps (zc_kernels.cu DefaultLd)
     int pairs = 1;    // SSSP on merged / merged-aligned / packed: build + read the pairs stream
+    int carveout = -1;  // sweep kernels' preferred shared-memory carveout (%, -1: default)
   } tune;
   int multigraph = -1;  // cached duplicate-arc check (-1 unknown)
   // one-time builds (compressed streams, pairs): wall ms per phase, in order

@@ -179,6 +179,7 @@ struct ExpandArgs {
   // launch tuning (host side only; zc_set_tuning)
   int unroll;
   int ctas_per_sm;
+  int carveout;     // sweep kernels' preferred shared-memory carveout (%, -1: driver default)
   int chunk_sched;  // 1: the per-warp chunk + big-list scheduler instead of the sweep
   int ld;           // load flavour override of the raw BFS sweeps (-1: the strategy's default)
   int pairs;        // SSSP: `edges` is the interleaved (dst, weight) u32-pair list

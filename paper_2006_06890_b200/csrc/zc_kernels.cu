@@ -1634,6 +1634,13 @@ cudaError_t expand_sweep(const ExpandArgs& a, int num_sms, cudaStream_t st,
   cudaError_t e =
       scan_u32_to_u64(a.wcnt, a.wpre, a.n, a.scan_tmp, a.scan_tmp_bytes, st, a.n_dev);
   if (e != cudaSuccess) return e;
+  static int carve = -2;  // per instantiation: the carveout last set
+  if (a.carveout != carve && a.carveout >= -1) {
+    cudaFuncSetAttribute(k_expand_sweep<STRAT, ALGO, ET, WT, U, LD>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout,
+                         a.carveout < 0 ? -1 : a.carveout);
+    carve = a.carveout;
+  }
   static int grid = 0;  // per instantiation: all CTAs resident at once
   if (!grid)
     grid = resident_ctas(k_expand_sweep<STRAT, ALGO, ET, WT, U, LD>, kSweepThreads, num_sms);
