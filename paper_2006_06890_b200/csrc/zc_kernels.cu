@@ -330,6 +330,34 @@ struct Batch {
 template <int ALGO, typename ET, typename WT, int U, bool CMP = false>
 __device__ __forceinline__ void visit_batch(const ExpandArgs& a,
                                             const Batch<ALGO, ET, WT, U, CMP>& b) {
+  if constexpr (ALGO == kBfs) {
+    // The batch's visits in three independent phases -- all bitmap probes,
+    // then the claims of the unvisited, then the winners' writes -- so the
+    // U windows' L2 round trips overlap instead of chaining probe -> atomic ->
+    // store window after window (a store to level[] may alias the next
+    // window's bitmap word, which pins the per-window order otherwise).
+    uint32_t probe[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      probe[u] = b.ok[u] ? a.visited[static_cast<uint64_t>(b.dst[u]) >> 5] : ~0u;
+    uint32_t old[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t bit = 1u << (static_cast<uint32_t>(b.dst[u]) & 31);
+      old[u] = ~0u;
+      if (!(probe[u] & bit))
+        old[u] = atomicOr(a.visited + (static_cast<uint64_t>(b.dst[u]) >> 5), bit);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t w = static_cast<uint64_t>(b.dst[u]);
+      if (!(old[u] & (1u << (w & 31)))) {
+        static_cast<uint32_t*>(a.state)[w] = a.iter;
+        a.flags[w] = 1;
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     if (!b.ok[u]) continue;
