@@ -674,6 +674,20 @@ def other_configs(zc, args, device, oc, parity) -> dict:
         parity[key] = same(r, ref) if sched is None else same_values(r, ref)
     out[f"{tag}/cpu_port_work_gteps"] = (sum(ref.traversed_edges)
                                          / oc.seconds[("kron_sym", "cc", 0)] / 1e9)
+    # PageRank streams the whole zero-copy list every
+    # iteration (5 iterations timed; parity is pinned on the reference's
+    # PageRank fixtures in the GPU tests, not at this size)
+    import warnings
+    for s in ("merged-aligned", "compressed"):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")  # the multigraph note (duplicates are kept)
+            zc.pagerank(k, s, max_iters=1, tol=1e-30, collect_traffic=False)
+            r = zc.pagerank(k, s, max_iters=5, tol=1e-30, collect_traffic=False)
+        t = r.kernel_ms * 1e-3
+        out[f"pagerank_kron{args.scale}_sym/{s}"] = {
+            "iterations": r.iterations, "kernel_ms": r.kernel_ms,
+            "edge_gteps": r.total_traversed_edges / t / 1e9,
+            "link_gbs_8d": r.total_traversed_edges * 4 / (r.expand_ms * 1e-3) / 1e9}
     k.close()
     return out
 

@@ -228,8 +228,9 @@ def pagerank(g, strategy=AccessStrategy.MERGED_ALIGNED, damping: float = 0.85,
     """Synchronous push PageRank over the full edge list each iteration
     (reference traversal.py:191-249): rank' = (1-d)/V + d (pushed + dangling/V),
     stop when the L1 change < tol or after max_iters, ranks normalised to 1.
-    float64; the push is a float64 atomicAdd, so results match the reference
-    to ~1e-15 relative (criterion: L-inf <= 1e-8, test_acceptance.py:169-180)."""
+    float64 ranks; the pushes are summed in 2^-62 fixed point (u64 atomics, so
+    the sums and the iteration count do not depend on the order), matching the
+    reference to ~1e-15 (criterion: L-inf <= 1e-8, test_acceptance.py:169-180)."""
     if not 0.0 < damping < 1.0:
         raise ValueError("damping must be in (0, 1)")
     if max_iters < 1:
