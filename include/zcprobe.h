@@ -43,6 +43,11 @@ int zc_bulk_probe(int32_t device, uint64_t bytes, uint32_t chunk, int ctas_per_s
  * pages; 3 mmap + huge pages + cudaHostRegister without prefault. */
 int zc_pin_probe(uint64_t bytes, int mode, int threads, double *alloc_s, double *register_s);
 
+/* Gather roofline of the in-HBM control run: G random 4-byte loads per
+ * second into a `bytes`-sized device array (16 MB = the K27 visited bitmap,
+ * L2-resident); mode 1 adds an atomicOr for 1 load in 16 (the claims). */
+int zc_gather_probe(int32_t device, uint64_t bytes, int mode, double *gloads_per_s);
+
 #ifdef __cplusplus
 }
 #endif

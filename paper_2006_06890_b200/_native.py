@@ -41,7 +41,7 @@ EXPORTED = (
 )
 # every symbol include/zcprobe.h declares (the measurement tool library)
 PROBE_EXPORTED = ("zc_link_probe", "zc_read_probe", "zc_bulk_probe", "zc_vmm_host_probe",
-                  "zc_pin_probe")
+                  "zc_pin_probe", "zc_gather_probe")
 ZC_OPT_TRAFFIC_MODEL, ZC_OPT_HOST_LOOP = 1, 2
 
 
@@ -193,6 +193,7 @@ def probe_lib() -> C.CDLL:
                                             C.POINTER(dbl)]),
                 "zc_bulk_probe": (C.c_int, [i32, u64, u32, C.c_int, C.c_int, C.POINTER(dbl)]),
                 "zc_pin_probe": (C.c_int, [u64, C.c_int, C.c_int, C.POINTER(dbl), C.POINTER(dbl)]),
+                "zc_gather_probe": (C.c_int, [i32, u64, C.c_int, C.POINTER(dbl)]),
                 "zc_vmm_host_probe": (C.c_int, [i32, u64, C.POINTER(u64)]),
             }
             for name, (res, args) in sig.items():

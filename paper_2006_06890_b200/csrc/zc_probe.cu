@@ -563,3 +563,67 @@ extern "C" int zc_pin_probe(uint64_t bytes, int mode, int threads, double* alloc
   }
   return ZC_OK;
 }
+
+// Gather roofline of the HBM control run: its per-edge visited-bitmap probe
+// is a random 4-byte read of a V/8-byte bitmap (16 MB at K27, L2-resident).
+// Every thread issues `per` independent random word loads (counter-hashed
+// indices) into a `words`-word device array and folds them into a sink.
+// mode 0: plain loads; 1: plain loads + atomicOr on 1/16 of them (the claims).
+__global__ void __launch_bounds__(256) k_gather_probe(uint32_t* __restrict__ bm, uint64_t words,
+                                                      uint32_t per, int mode,
+                                                      unsigned long long* sink) {
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint32_t acc = 0;
+  uint64_t h = t * 0x9e3779b97f4a7c15ull + 1;
+  for (uint32_t i = 0; i < per; i += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      h ^= h >> 33;
+      h *= 0xff51afd7ed558ccdull;
+      h ^= h >> 29;
+      v[u] = bm[h % words];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc += v[u];
+      if (mode == 1 && ((h >> (u * 4)) & 15) == 0) atomicOr(bm + ((h >> 7) % words), 1u << u);
+    }
+  }
+  if (acc == 0x12345678u) atomicAdd(sink, 1ull);
+}
+
+extern "C" int zc_gather_probe(int32_t device, uint64_t bytes, int mode, double* gloads_per_s) {
+  using namespace zc;
+  cudaSetDevice(device);
+  const uint64_t words = std::max<uint64_t>(bytes / 4, 1024);
+  uint32_t* bm = nullptr;
+  unsigned long long* sink = nullptr;
+  ZC_CUDA_TRY(cudaMalloc(&bm, words * 4));
+  ZC_CUDA_TRY(cudaMemset(bm, 0, words * 4));
+  ZC_CUDA_TRY(cudaMalloc(&sink, sizeof(*sink)));
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  const int grid = nsm * 8;
+  const uint32_t per = 512;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k_gather_probe<<<grid, 256>>>(bm, words, per, mode, sink);  // warm L2
+  cudaEventRecord(a);
+  for (int r = 0; r < 5; ++r) k_gather_probe<<<grid, 256>>>(bm, words, per, mode, sink);
+  cudaEventRecord(b);
+  cudaError_t e = cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaFree(bm);
+  cudaFree(sink);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (e != cudaSuccess) {
+    set_error(std::string("gather probe: ") + cudaGetErrorString(e));
+    return ZC_ECUDA;
+  }
+  *gloads_per_s = 5.0 * grid * 256.0 * per / (ms * 1e-3) / 1e9;
+  return ZC_OK;
+}
