@@ -599,8 +599,18 @@ def variants_placements(zc, args, g, sources, device, oc, parity, step_srcs) -> 
             del ballast
             torch.cuda.empty_cache()
         h.close()
+    # the HBM control is gather-bound (a random visited-bitmap probe per edge),
+    # not HBM-bandwidth bound: its roofline is the L2 random-load rate
+    from paper_2006_06890_b200.device import gather_probe
     hbm = out["hbm/merged-aligned"]
-    hbm["roofline_hbm_gbs"] = None  # HBM control: gather-bound (visited-bitmap probes), see DESIGN
+    bitmap = (g.num_vertices + 7) // 8
+    ceil = {m: gather_probe(bitmap, m, device) for m in (0, 1)}
+    probes = hbm["gteps"] * hbm["kernel_ms"] / hbm["expand_ms"]  # G probes/s in the sweeps
+    hbm["gather_roofline"] = {"g_loads_per_s": ceil[0], "g_loads_per_s_with_claims": ceil[1],
+                              "bitmap_bytes": bitmap, "sweep_g_probes_per_s": probes,
+                              "frac": probes / ceil[1],
+                              "probe": "zc_gather_probe: random 4-byte loads into a bitmap-sized "
+                                       "device array (mode 1 adds the claims' atomicOr)"}
     return out
 
 

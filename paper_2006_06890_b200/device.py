@@ -459,6 +459,14 @@ def read_probe(nbytes: int, chunk_bytes: int, random, alloc: str = "pinned",
     return out.value
 
 
+def gather_probe(nbytes: int = 16 << 20, mode: int = 1, device: int = 0) -> float:
+    """G random 4-byte loads/s into an nbytes device array (mode 1: with an
+    atomicOr per 16 loads) -- the in-HBM control run's gather roofline."""
+    out = C.c_double()
+    N.check(N.probe_lib().zc_gather_probe(device, nbytes, mode, C.byref(out)))
+    return out.value
+
+
 def link_probe(device: int = 0, nbytes: int = 1 << 30, iters: int = 5) -> dict:
     """Measured host-link and HBM read bandwidths (GB/s)."""
     m, z, h = C.c_double(), C.c_double(), C.c_double()
