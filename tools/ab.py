@@ -10,11 +10,13 @@ ap.add_argument("--specs", default=";unroll=8")
 ap.add_argument("--sources", type=int, default=6)
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--algo", default="bfs")
+ap.add_argument("--placement", default="zerocopy")
 a = ap.parse_args()
 if a.algo == "sssp":
-    dg = zc.generate_uniform_device(1 << a.scale, 16, 16, seed=27, weights=(8, 72))
+    dg = zc.generate_uniform_device(1 << a.scale, 16, 16, seed=27, weights=(8, 72),
+                                    placement=a.placement)
 else:
-    dg = zc.generate_rmat(a.scale, 16, seed=27, symmetrize=a.algo == "cc")
+    dg = zc.generate_rmat(a.scale, 16, seed=27, symmetrize=a.algo == "cc", placement=a.placement)
 srcs = [int(s) for s in zc.pick_sources(dg.as_csr(), 64, seed=7)[:a.sources]]
 if a.algo == "cc":
     srcs = srcs[:1]
