@@ -949,17 +949,37 @@ def main_partitioned(args, rank, world, device):
     e2e = _part_series(part, "bfs", sources, strat, args.steps, 0, world, device,
                        exchange=args.exchange, bufs=bufs, stage=stage, fetch=True)
     d2h = sum_over_ranks(sum(r.values.nbytes for r in e2e["_results"]), world, device)
-    crc_a = _gather_values_crc(e2e["_results"][0], world, device)
+    ra = e2e["_results"][0]  # sources[0] (e2e runs without warm-up)
+    crc_a = _gather_values_crc(ra, world, device)
     if fused_error is None:
         r_alt = _part_series(part, "bfs", sources[:1], strat, 1, 0, world, device,
                              exchange=other, bufs=bufs, stage=stage,
                              fetch=True)  # e2e's first run: sources[0]
         crc_b = _gather_values_crc(r_alt["_results"][0], world, device)
-        ra, rb = e2e["_results"][0], r_alt["_results"][0]
+        rb = r_alt["_results"][0]
         parity[f"kron{scale}/fused_vs_reduce_scatter"] = bool(
             crc_a == crc_b and ra.iterations == rb.iterations
             and list(ra.traversed_edges) == list(rb.traversed_edges))
     e2e_value = e2e["_trav"] / e2e["wall_s"] / 1e9
+    # B200 store extension at N>1: direction-optimizing partitions (compressed
+    # out-lists, per-rank generated in-lists, bottom-up steps against the
+    # all-reduced frontier bitmap), same graph and sources; build time apart
+    dobfs = None
+    if not args.no_variants:
+        t0 = time.time()
+        part.build_stores()
+        build_s = max_over_ranks(time.time() - t0, world, device)
+        d = _part_series(part, "bfs", sources, "direction-optimizing", min(args.steps, 5), 1,
+                         world, device, exchange=args.exchange, bufs=bufs, stage=stage)
+        dobfs = dict(_strip(d), build_s=build_s)
+        # the same levels, iterations and work as merged-aligned from sources[0]
+        r_do = _part_series(part, "bfs", sources[:1], "direction-optimizing", 1, 0, world,
+                            device, exchange=args.exchange, bufs=bufs, stage=stage,
+                            fetch=True)["_results"][0]
+        parity[f"kron{scale}/direction-optimizing_vs_merged-aligned"] = bool(
+            _gather_values_crc(r_do, world, device) == crc_a
+            and r_do.iterations == ra.iterations
+            and list(r_do.traversed_edges) == list(ra.traversed_edges))
     part_arcs = part.graph_view().num_edges
     part.close()
     del bufs
@@ -1002,7 +1022,7 @@ def main_partitioned(args, rank, world, device):
                      "bytes_per_level": head["exchange_bytes_per_step"] / max(head["iterations"], 1),
                      "kind": args.exchange,
                      other.replace("-", "_") + "_bytes_per_step": alt["exchange_bytes_per_step"]},
-        "variants": {other: _strip(alt)},
+        "variants": {other: _strip(alt), "direction-optimizing": dobfs},
         "fused_error": fused_error,
         "headline": _strip(head),
         "graph": {"vertices": 1 << scale, "arcs": args.edge_factor << scale,

@@ -235,6 +235,13 @@ class CudaPartition:
         N.check(N.lib().zc_part_apply(self._h, ptr, C.byref(n), C.byref(t)))
         return n.value, t.value
 
+    def build_stores(self) -> None:
+        """The compressed out-lists and the owned vertices' in-lists the
+        direction-optimizing strategy reads (built on first use otherwise)."""
+        nb = C.c_uint64()
+        N.check(N.lib().zc_graph_build_compressed(self._h, C.byref(nb)))
+        N.check(N.lib().zc_part_build_in_lists(self._h, C.byref(nb)))
+
     def launches(self) -> int:
         """Kernels launched since the last begin (this rank)."""
         return self.run_stats()["launches"]
