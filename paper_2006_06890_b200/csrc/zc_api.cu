@@ -1731,11 +1731,11 @@ static int part_expand_impl(zc_graph* g, void* exch, int mode) {
     return ZC_ESTATE;
   }
   const bool fused = mode == kExchStore;
-  if (fused && (!g->d_peers || g->fused_algo != g->p_algo)) {
+  if (fused && (!g->peers_ready || g->fused_algo != g->p_algo)) {
     set_error("fused exchange not initialised for this algorithm (zc_part_fused_init/connect)");
     return ZC_ESTATE;
   }
-  if (mode == kExchBitmap && (!g->d_peer_sent || g->p_algo != kBfs)) {
+  if (mode == kExchBitmap && (!g->peer_sent_ready || g->p_algo != kBfs)) {
     set_error("bitmap exchange: a bfs run and zc_part_bitmap_init/connect first");
     return ZC_ESTATE;
   }
@@ -1856,6 +1856,7 @@ int zc_part_fused_connect(zc_graph* g, const void* handles, void* const* ptrs) {
     return ZC_ESTATE;
   }
   DeviceGuard dg(g->device);
+  g->peers_ready = false;
   for (void* p : g->ipc_opened) cudaIpcCloseMemHandle(p);
   g->ipc_opened.clear();
   std::vector<void*> peers(g->nparts);
@@ -1875,6 +1876,7 @@ int zc_part_fused_connect(zc_graph* g, const void* handles, void* const* ptrs) {
   }
   ZC_CUDA_TRY(cudaMemcpy(g->d_peers, peers.data(), g->nparts * sizeof(void*),
                          cudaMemcpyHostToDevice));
+  g->peers_ready = true;
   return ZC_OK;
 }
 
@@ -1972,6 +1974,7 @@ int zc_part_bitmap_connect(zc_graph* g, const void* handles, void* const* ptrs) 
     return ZC_ESTATE;
   }
   DeviceGuard dg(g->device);
+  g->peer_sent_ready = false;
   for (void* p : g->ipc_opened_sent) cudaIpcCloseMemHandle(p);
   g->ipc_opened_sent.clear();
   std::vector<const void*> peers(g->nparts);
@@ -1991,13 +1994,14 @@ int zc_part_bitmap_connect(zc_graph* g, const void* handles, void* const* ptrs) 
   }
   ZC_CUDA_TRY(cudaMemcpy(g->d_peer_sent, peers.data(), g->nparts * sizeof(void*),
                          cudaMemcpyHostToDevice));
+  g->peer_sent_ready = true;
   return ZC_OK;
 }
 
 int zc_part_bitmap_expand(zc_graph* g) { return part_expand_impl(g, nullptr, kExchBitmap); }
 
 int zc_part_bitmap_apply(zc_graph* g, uint64_t* n_next, uint64_t* trav_next) {
-  if (!g || !g->d_peer_sent) {
+  if (!g || !g->peer_sent_ready) {
     set_error("zc_part_bitmap_init / connect first");
     return ZC_ESTATE;
   }

@@ -135,6 +135,8 @@ struct zc_graph {
   // BFS bitmap exchange: the ranks' `sent` bitmaps (device array of nparts
   // pointers; peers' through CUDA IPC), read by each owner for its range
   const uint32_t** d_peer_sent = nullptr;
+  bool peer_sent_ready = false;  // zc_part_bitmap_connect done
+  bool peers_ready = false;      // zc_part_fused_connect done
   std::vector<void*> ipc_opened_sent;
   void* d_lbest = nullptr;     // SSSP / CC: best candidate sent per global vertex this iteration
   std::vector<void*> ipc_opened;

@@ -832,3 +832,28 @@ def test_schedule_argument_errors():
         zc.sssp(g, 0, schedule="near-far", collect_traffic=True)
     with pytest.raises(ValueError, match="undirected"):
         zc.cc(g, schedule="afforest")
+
+
+def test_partition_exchange_call_order_errors():
+    """The fused / bitmap exchanges refuse to run before their peers are
+    connected, and the bitmap exchange is BFS-only (zc_part_* return
+    ZC_ESTATE -> RuntimeError)."""
+    g = zc.symmetrized(zc.generate_uniform(2000, 1, 6, seed=9))
+    b = edge_balanced_bounds(g.offsets, 2)
+    e = CudaPartition(local_part(g, b, 0), b, 0)
+    e.begin("bfs", 0, "merged-aligned")
+    with pytest.raises(RuntimeError, match="bitmap"):
+        e.bitmap_expand()
+    with pytest.raises(RuntimeError, match="fused"):
+        e.fused_expand()
+    e.bitmap_init()  # exported, but the peers are not connected yet
+    with pytest.raises(RuntimeError, match="bitmap"):
+        e.bitmap_expand()
+    e.fused_init("bfs")
+    with pytest.raises(RuntimeError, match="fused"):
+        e.fused_expand()
+    e.bitmap_connect(ptrs=[e.bitmap_init()[1]] * 2)
+    e.begin("cc", 0, "merged-aligned")
+    with pytest.raises(RuntimeError, match="bitmap"):  # BFS only
+        e.bitmap_expand()
+    e.close()

@@ -105,3 +105,15 @@ def test_pull_rule():
     assert DO_ALPHA == 2.0
     assert not pull_now(1, 10**9, 1)          # never the source's own expansion
     assert pull_now(2, 600, 1000) and not pull_now(2, 400, 1000)
+
+
+def test_driver_argument_errors_and_accounting():
+    from paper_2006_06890_b200.multi import allreduce_send_bytes, run_partition
+    with pytest.raises(ValueError, match="bfs_exchange"):
+        run_partition(None, "bfs", 0, "merged-aligned", bfs_exchange="ring")
+    with pytest.raises(ValueError, match="unknown algorithm"):
+        run_partition(None, "pagerank", 0, "merged-aligned")
+    # a ring all-reduce sends 2 (p - 1) / p of the buffer per rank; nothing alone
+    assert allreduce_send_bytes(1000, 1) == 0
+    assert allreduce_send_bytes(1000, 2) == 1000
+    assert allreduce_send_bytes(800, 4) == 1200
