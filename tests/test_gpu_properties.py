@@ -65,3 +65,29 @@ def test_random_graphs_match_oracle(case):
         assert _same(r, ref_b) and len(r.per_iteration_traffic) == r.iterations
     zc.release(g)
     zc.release(gu)
+
+
+@settings(max_examples=int(__import__("os").environ.get("ZC_HYP_EXAMPLES", "200")) // 4,
+          deadline=None, suppress_health_check=list(HealthCheck))
+@given(graphs(), st.integers(1, 4), st.sampled_from(["merged-aligned", "packed"]),
+       st.sampled_from([(False, "bitmap"), (True, "bitmap"), (True, "store")]))
+def test_random_partitions_match_oracle(case, nparts, strategy, exchange):
+    """Vertex-range partitions of arbitrary graphs (ranges may be empty) with
+    every exchange: identical values, iterations and traversed edges."""
+    from paper_2006_06890_b200.multi import (CudaPartition, edge_balanced_bounds, local_part,
+                                             run_partitions_local)
+    g, src = case
+    g = zc.CsrGraph(g.num_vertices, g.num_edges, g.offsets, g.edges,
+                    np.minimum(np.asarray(g.weights), 2 ** 31), g.edge_elem_bytes, 4, True)
+    gu = zc.symmetrized(g)
+    fused, bx = exchange
+    for algo, graph in (("bfs", g), ("sssp", g), ("cc", gu)):
+        ref = oracle.run(algo, graph, src)
+        b = edge_balanced_bounds(graph.offsets, nparts)
+        engines = [CudaPartition(local_part(graph, b, k), b, k) for k in range(nparts)]
+        vals, iters, trav = run_partitions_local(engines, algo, src, strategy, fused=fused,
+                                                 bfs_exchange=bx)
+        assert np.array_equal(vals, ref.values), (algo, nparts, strategy, exchange)
+        assert iters == ref.iterations and trav == ref.traversed_edges
+        for e in engines:
+            e.close()
