@@ -802,6 +802,7 @@ def _part_series(part, algo, sources, strat, steps, warmup, world, device, *, ex
     ev1 = torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
     ev0.record()
+    d2h = 0
     for i in range(steps):
         r = one(warmup + i)
         trav += r.total_traversed_edges
@@ -810,7 +811,11 @@ def _part_series(part, algo, sources, strat, steps, warmup, world, device, *, ex
         xbytes += r.exchange_bytes
         bu += r.bottom_up_steps
         launches += part.launches()
-        results.append(r)
+        if r.values is not None:
+            d2h += r.values.nbytes
+        # keep the first result only: a rank's int64 slice is 1 GiB at K30 / 8
+        if not results:
+            results.append(r)
     ev1.record()
     torch.cuda.synchronize(device)
     wall = time.perf_counter() - t0
@@ -828,7 +833,7 @@ def _part_series(part, algo, sources, strat, steps, warmup, world, device, *, ex
             "bottom_up_steps_per_step": bu / steps,
             "gpu_launches": int(sum_over_ranks(launches, world, device)),
             "wall_s": max_over_ranks(wall, world, device), "_results": results,
-            "_trav": trav}
+            "_trav": trav, "_d2h": d2h}
 
 
 def _gather_values_crc(r, world, device) -> str:
@@ -896,13 +901,14 @@ def main_partitioned(args, rank, world, device):
 
     headline  weak scaling: directed Kronecker scale 27 + log2(N) (2^31 arcs
               per rank, as the N=1 line; K29 at N=4), BFS merged+aligned, the
-              fused exchange (discoveries stored straight into the owner's
-              buffer over NVLink, deduplicated per rank and level); the NCCL
-              reduce-scatter exchange timed beside it
+              fused bitmap exchange (every rank marks its discoveries in its
+              own bitmap, each owner ORs the ranks' words over its range
+              through peer memory / NVLink); the NCCL reduce-scatter exchange
+              and direction-optimizing partitions timed beside it
     configs4  fixed size: Kronecker 29 symmetrized (2^34 arcs) BFS and CC
     parity    small-scale BFS / CC against the oracle for both exchanges;
-              full size: both exchanges give the same levels (crc), iterations
-              and traversed edges"""
+              full size: the exchanges and direction-optimizing give the same
+              levels (per-rank crcs), iterations and traversed edges"""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -948,7 +954,7 @@ def main_partitioned(args, rank, world, device):
     # e2e: the public partitioned API with every rank's int64 levels downloaded
     e2e = _part_series(part, "bfs", sources, strat, args.steps, 0, world, device,
                        exchange=args.exchange, bufs=bufs, stage=stage, fetch=True)
-    d2h = sum_over_ranks(sum(r.values.nbytes for r in e2e["_results"]), world, device)
+    d2h = sum_over_ranks(e2e["_d2h"], world, device)
     ra = e2e["_results"][0]  # sources[0] (e2e runs without warm-up)
     crc_a = _gather_values_crc(ra, world, device)
     if fused_error is None:
