@@ -971,7 +971,11 @@ def main_partitioned(args, rank, world, device):
     # out-lists, per-rank generated in-lists, bottom-up steps against the
     # all-reduced frontier bitmap), same graph and sources; build time apart
     dobfs = None
-    if not args.no_variants:
+    ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    lists = (args.edge_factor << scale) * 4  # all ranks' raw lists, on this node
+    if not args.no_variants and ram < 3 * lists:  # + ~1.5x for the two line streams
+        dobfs = {"skipped": f"host memory {ram >> 30} GiB < 3 x the {lists >> 30} GiB of lists"}
+    elif not args.no_variants:
         t0 = time.time()
         part.build_stores()
         build_s = max_over_ranks(time.time() - t0, world, device)
