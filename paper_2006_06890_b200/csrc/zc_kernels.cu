@@ -1170,15 +1170,24 @@ __global__ void __launch_bounds__(1024) k_tile_scan(CompactArgs c) {
   }
 }
 
+// One tile (kTileVerts vertices) per iteration: the marked vertices' tile
+// offsets are staged in shared memory in vertex order (a block prefix over
+// the threads' 16-flag groups), then the block writes the tile's frontier
+// entries with consecutive threads on consecutive positions -- coalesced
+// stores, and coalesced offset gathers for the sorted ids -- instead of each
+// thread scattering its own 16 vertices' entries.
 template <int ALGO>
 __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
+  __shared__ uint16_t sh_v[kTileVerts];  // tile offsets of the marked vertices
   __shared__ uint32_t warp_tot[kTileThreads / 32];
   __shared__ unsigned long long deg_sh[kTileThreads / 32], indeg_sh[kTileThreads / 32];
+  static_assert(kTileVerts <= 65536, "tile offsets are u16");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (uint64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
     uint4* fp = reinterpret_cast<uint4*>(c.flags) + t * kTileThreads + threadIdx.x;
     const uint4 f_all = *fp;
-    const uint4 f = select_near(f_all, t * kTileVerts + static_cast<uint64_t>(threadIdx.x) * 16, c);
+    const uint64_t tile0 = t * kTileVerts;
+    const uint4 f = select_near(f_all, tile0 + static_cast<uint64_t>(threadIdx.x) * 16, c);
     const uint32_t words[4] = {f.x, f.y, f.z, f.w};
     const uint32_t cnt = __popc(f.x) + __popc(f.y) + __popc(f.z) + __popc(f.w);
     uint32_t incl = cnt;
@@ -1189,29 +1198,34 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_write(CompactArgs c) {
     }
     if (lane == 31) warp_tot[wid] = incl;
     __syncthreads();
-    uint32_t before = 0;
-    for (int w = 0; w < wid; ++w) before += warp_tot[w];
-    uint64_t pos = static_cast<uint64_t>(c.tiles[t]) + before + incl - cnt;
-    unsigned long long deg = 0, indeg = 0;
-    if (cnt) {
-      const uint64_t v0 = t * kTileVerts + static_cast<uint64_t>(threadIdx.x) * 16;
+    uint32_t before = 0, total = 0;
 #pragma unroll
-      for (int b = 0; b < 16; ++b) {
-        if ((words[b >> 2] >> ((b & 3) * 8)) & 0xffu) {
-          const uint64_t v = v0 + b;
-          const uint64_t s0 = c.off[v], d0 = c.off[v + 1] - s0;
-          c.front_out[pos] = static_cast<uint32_t>(v);
-          c.fs_out[pos] = s0;
-          c.fd_out[pos] = static_cast<uint32_t>(d0);
-          if (ALGO == kSssp) c.fval_out[pos] = static_cast<const uint64_t*>(c.state)[v];
-          if (ALGO == kCc) c.fval_out[pos] = static_cast<const uint32_t*>(c.state)[v];
-          deg += d0;
-          if (c.in_off) indeg += c.in_off[v + 1] - c.in_off[v];
-          ++pos;
-        }
-      }
+    for (int w = 0; w < kTileThreads / 32; ++w) {
+      before += w < wid ? warp_tot[w] : 0u;
+      total += warp_tot[w];
+    }
+    if (cnt) {
+      uint32_t lpos = before + incl - cnt;
+#pragma unroll
+      for (int b = 0; b < 16; ++b)
+        if ((words[b >> 2] >> ((b & 3) * 8)) & 0xffu)
+          sh_v[lpos++] = static_cast<uint16_t>(threadIdx.x * 16 + b);
       // selected marks are consumed; far-pile marks (near-far SSSP) stay
       *fp = make_uint4(f_all.x ^ f.x, f_all.y ^ f.y, f_all.z ^ f.z, f_all.w ^ f.w);
+    }
+    __syncthreads();
+    const uint64_t base = c.tiles[t];
+    unsigned long long deg = 0, indeg = 0;
+    for (uint32_t i = threadIdx.x; i < total; i += kTileThreads) {
+      const uint64_t v = tile0 + sh_v[i], pos = base + i;
+      const uint64_t s0 = c.off[v], d0 = c.off[v + 1] - s0;
+      c.front_out[pos] = static_cast<uint32_t>(v);
+      c.fs_out[pos] = s0;
+      c.fd_out[pos] = static_cast<uint32_t>(d0);
+      if (ALGO == kSssp) c.fval_out[pos] = static_cast<const uint64_t*>(c.state)[v];
+      if (ALGO == kCc) c.fval_out[pos] = static_cast<const uint32_t*>(c.state)[v];
+      deg += d0;
+      if (c.in_off) indeg += c.in_off[v + 1] - c.in_off[v];
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
