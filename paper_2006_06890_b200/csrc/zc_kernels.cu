@@ -1132,10 +1132,20 @@ __global__ void __launch_bounds__(1024) k_tile_scan(CompactArgs c) {
   __shared__ uint64_t warp_sums[32];
   const int tid = threadIdx.x;
   const uint64_t n = c.ntiles;
-  const uint64_t chunk = (n + blockDim.x - 1) / blockDim.x;
+  // chunks of whole uint4 groups: the per-thread sums read 16 bytes at a time
+  const uint64_t chunk = (n + blockDim.x * 4 - 1) / (blockDim.x * 4) * 4;
   const uint64_t lo = min(n, tid * chunk), hi = min(n, lo + chunk);
   uint64_t sum = 0;
-  for (uint64_t k = lo; k < hi; ++k) sum += c.tiles[k];
+  if (hi - lo == chunk) {
+    const uint4* q = reinterpret_cast<const uint4*>(c.tiles + lo);
+#pragma unroll 4
+    for (uint64_t k = 0; k < chunk / 4; ++k) {
+      const uint4 x = q[k];
+      sum += static_cast<uint64_t>(x.x) + x.y + x.z + x.w;
+    }
+  } else {
+    for (uint64_t k = lo; k < hi; ++k) sum += c.tiles[k];
+  }
   uint64_t incl = sum;
   const int lane = tid & 31, wid = tid >> 5;
 #pragma unroll
@@ -1163,10 +1173,25 @@ __global__ void __launch_bounds__(1024) k_tile_scan(CompactArgs c) {
   }
   __syncthreads();
   uint64_t run = warp_sums[wid] + incl - sum;
-  for (uint64_t k = lo; k < hi; ++k) {
-    const uint32_t cnt = c.tiles[k];
-    c.tiles[k] = static_cast<uint32_t>(run);  // frontier positions fit u32 (V < 2^32)
-    run += cnt;
+  if (hi - lo == chunk) {  // frontier positions fit u32 (V < 2^32)
+    uint4* q = reinterpret_cast<uint4*>(c.tiles + lo);
+#pragma unroll 4
+    for (uint64_t k = 0; k < chunk / 4; ++k) {
+      const uint4 x = q[k];
+      uint4 y;
+      y.x = static_cast<uint32_t>(run);
+      y.y = static_cast<uint32_t>(run += x.x);
+      y.z = static_cast<uint32_t>(run += x.y);
+      y.w = static_cast<uint32_t>(run += x.z);
+      run += x.w;
+      q[k] = y;
+    }
+  } else {
+    for (uint64_t k = lo; k < hi; ++k) {
+      const uint32_t cnt = c.tiles[k];
+      c.tiles[k] = static_cast<uint32_t>(run);
+      run += cnt;
+    }
   }
 }
 
