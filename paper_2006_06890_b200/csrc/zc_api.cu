@@ -275,7 +275,8 @@ __attribute__((target("avx2"))) static void widen_levels_avx2(const uint8_t* src
   _mm_sfence();
 }
 
-static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n, bool overlapped) {
+static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n, bool overlapped,
+                         int threads = 0) {
   static const bool avx2 = __builtin_cpu_supports("avx2");
   // Overlapped (pipelined) widens run on four threads: they share the host's
   // memory bandwidth with the next traversal's zero-copy reads -- more
@@ -284,7 +285,8 @@ static void widen_levels(const uint8_t* src, int64_t* out, uint64_t n, bool over
   // all cores but two.
   static const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
   static const unsigned spare_overlap = hc > 4 ? hc - 4 : 0u;
-  const unsigned spare = overlapped ? spare_overlap : 2u;
+  unsigned spare = overlapped ? spare_overlap : 2u;
+  if (threads > 0) spare = hc > static_cast<unsigned>(threads) ? hc - threads : 0u;
   parallel_for(
       n,
       [&](uint64_t lo, uint64_t hi) {
@@ -1074,6 +1076,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
     const uint8_t* src8 = g->h_stage[b];
     const uint64_t nv = g->nv;
     const int dev = g->device;
+    const int wthreads = g->tune.widen;
     int* err = &g->widen_err;
     g->widen_th[b] = std::thread([=] {  // widens while the caller starts the next traversal
       cudaSetDevice(dev);
@@ -1081,7 +1084,7 @@ int run(zc_graph* g, int algo, uint64_t src, int strategy, int64_t* out, zc_stat
         *err = ZC_ECUDA;
         return;
       }
-      widen_levels(src8, out, nv, true);
+      widen_levels(src8, out, nv, true, wthreads);
     });
     ZC_CUDA_TRY(cudaEventSynchronize(g->ev[1]));
   } else if (narrow) {
@@ -2515,6 +2518,7 @@ int zc_set_tuning(zc_graph* g, const char* spec) {
     else if (k == "do_alpha" && atof(v.c_str()) > 0) t.do_alpha = atof(v.c_str());
     else if (k == "ld" && v.size() == 1 && v[0] >= '0' && v[0] <= '3') t.ld = v[0] - '0';
     else if (k == "pairs" && (v == "0" || v == "1")) t.pairs = v == "1";
+    else if (k == "widen" && atoi(v.c_str()) > 0 && atoi(v.c_str()) <= 256) t.widen = atoi(v.c_str());
     else if (k == "carveout" && !v.empty() && atoi(v.c_str()) >= 0 && atoi(v.c_str()) <= 100)
       t.carveout = atoi(v.c_str());
     else {
