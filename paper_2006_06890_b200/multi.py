@@ -3,18 +3,27 @@
 One process per GPU (``torch.distributed``, NCCL over NVLink).  Rank k owns
 the global vertices [bounds[k], bounds[k+1]) -- ranges cut so every rank
 holds ~E/p edges -- and keeps only their lists in its pinned host memory, so
-each GPU streams its own edge slice over its own host link.  Per iteration:
+each GPU streams its own edge slice over its own host link.  Per iteration the
+rank's CUDA kernels read its frontier's lists (zero-copy) and produce a
+candidate for every touched global vertex, delivered to the owners by one of:
 
-1. ``expand``: the rank's CUDA kernels read its frontier's lists (zero-copy)
-   and write a candidate for every touched global vertex into a dense
-   exchange buffer of ``nparts * stride`` slots (BFS: u8 "discovered" flags;
-   SSSP: int64 candidate distances; CC: int32 candidate labels);
-2. ``reduce_scatter`` (MAX for the flags -- NCCL has no bitwise OR --, MIN
-   for distances / labels) delivers to every owner the merged candidates of
-   its own range;
-3. ``apply``: the owner merges them into its state (Jacobi: candidates were
-   computed from start-of-iteration values) and compacts its next frontier;
-4. ``all_reduce`` of (frontier size, traversed edges) decides termination.
+* ``fused=True`` (no collective on the data path; CUDA-IPC peer pointers,
+  NVLink between GPUs):
+  - BFS, ``bfs_exchange="bitmap"`` (default): every rank marks its
+    discoveries in its own global bitmap; after a barrier each owner ORs the
+    ranks' words over its range and applies them (V/8 bytes read per rank);
+  - BFS ``"store"`` / SSSP / CC: the expansion stores each discovery, or
+    atomicMin's each candidate that improves the rank's local best, straight
+    into the owner's buffer;
+* ``fused=False``: a dense exchange buffer of ``nparts * stride`` slots and a
+  ``reduce_scatter`` (MAX on u8 flags for BFS -- NCCL has no bitwise OR --,
+  MIN on int64 distances / int32 labels).
+
+The owner merges its candidates into its state (Jacobi: computed from
+start-of-iteration values) and compacts its next frontier; an ``all_reduce``
+of (frontier size, traversed edges, unvisited in-edges) decides termination
+and, for direction-optimizing BFS, the step direction (bottom-up steps
+all-reduce the owned frontiers' disjoint bitmaps and scan owned in-lists).
 
 Because every step is the reference's level-synchronous / Jacobi iteration
 (traversal.py:98-179), values, iteration counts and per-iteration traversed
