@@ -665,6 +665,9 @@ def other_configs(zc, args, device, oc, parity) -> dict:
     u.set_tuning("")
     out[f"{tag}/cpu_port_work_gteps"] = (sum(ref.traversed_edges)
                                          / oc.seconds[("u27", "sssp", src)] / 1e9)
+    link = load_ncu_summary().get("link_utilisation_r02", {})
+    if f"{tag}/merged-aligned" in out and "sssp_u27_merged_aligned_pairs" in link:
+        out[f"{tag}/merged-aligned"]["pcie_read_frac_ncu"] = link["sssp_u27_merged_aligned_pairs"]
     u.close()
     t0 = time.time()
     k = zc.generate_rmat(args.scale, args.edge_factor, seed=args.seed, symmetrize=True,
@@ -684,6 +687,8 @@ def other_configs(zc, args, device, oc, parity) -> dict:
         parity[key] = same(r, ref) if sched is None else same_values(r, ref)
     out[f"{tag}/cpu_port_work_gteps"] = (sum(ref.traversed_edges)
                                          / oc.seconds[("kron_sym", "cc", 0)] / 1e9)
+    if f"{tag}/merged-aligned" in out and "cc_k27sym_merged_aligned" in link:
+        out[f"{tag}/merged-aligned"]["pcie_read_frac_ncu"] = link["cc_k27sym_merged_aligned"]
     # PageRank streams the whole zero-copy list every
     # iteration (5 iterations timed; parity is pinned on the reference's
     # PageRank fixtures in the GPU tests, not at this size)
