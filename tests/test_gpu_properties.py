@@ -39,7 +39,8 @@ def _same(r, ref, full=True):
     return ok
 
 
-@settings(max_examples=int(__import__("os").environ.get("ZC_HYP_EXAMPLES", "200")), deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=int(__import__("os").environ.get("ZC_HYP_EXAMPLES", "200")), deadline=None, derandomize=True,
+          suppress_health_check=list(HealthCheck))
 @given(graphs())
 def test_random_graphs_match_oracle(case):
     g, src = case
@@ -68,7 +69,8 @@ def test_random_graphs_match_oracle(case):
 
 
 @settings(max_examples=int(__import__("os").environ.get("ZC_HYP_EXAMPLES", "200")) // 4,
-          deadline=None, suppress_health_check=list(HealthCheck))
+          deadline=None, derandomize=True,
+          suppress_health_check=list(HealthCheck))
 @given(graphs(), st.integers(1, 4), st.sampled_from(["merged-aligned", "packed"]),
        st.sampled_from([(False, "bitmap"), (True, "bitmap"), (True, "store")]))
 def test_random_partitions_match_oracle(case, nparts, strategy, exchange):
