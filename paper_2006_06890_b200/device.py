@@ -368,6 +368,7 @@ def is_multigraph(dg: "DeviceGraph") -> bool:
 
 _CACHE: dict = {}
 _CACHE_LOCK = threading.Lock()
+HANDLES_PER_GRAPH = 2
 
 
 def _drop(gid: int) -> None:
@@ -394,11 +395,15 @@ def device_graph(g, placement: str = "zerocopy", device: int = 0) -> DeviceGraph
             entry = (weakref.ref(g, lambda _r, gid=gid: _drop(gid)), {})
             _CACHE[gid] = entry
         per = entry[1]
-        dg = per.get(key)
+        dg = per.pop(key, None)
         if dg is None:
+            # at most HANDLES_PER_GRAPH live handles per graph object (each holds
+            # a full copy of the lists): switching back and forth between two
+            # placements does not re-pin, a third evicts the least recent
+            while len(per) >= HANDLES_PER_GRAPH:
+                per.pop(next(iter(per))).close()
             dg = DeviceGraph(g, placement, device)
-            per.clear()  # one live handle per graph object (memory is large)
-            per[key] = dg
+        per[key] = dg  # most recently used last
     return dg
 
 

@@ -857,3 +857,19 @@ def test_partition_exchange_call_order_errors():
     with pytest.raises(RuntimeError, match="bitmap"):  # BFS only
         e.bitmap_expand()
     e.close()
+
+
+def test_device_graph_cache_keeps_two_placements():
+    """Alternating two placements reuses both handles (no re-pinning); a third
+    placement evicts the least recently used one."""
+    g = zc.generate_uniform(3000, 1, 8, seed=21)
+    a = zc.device_graph(g, "zerocopy")
+    b = zc.device_graph(g, "hbm")
+    assert zc.device_graph(g, "zerocopy") is a and zc.device_graph(g, "hbm") is b
+    c = zc.device_graph(g, "uvm")  # evicts "zerocopy", the least recent
+    assert zc.device_graph(g, "hbm") is b and zc.device_graph(g, "uvm") is c
+    assert zc.device_graph(g, "zerocopy") is not a
+    ref = oracle.bfs(g, 0)
+    for p in ("zerocopy", "hbm", "uvm"):
+        assert np.array_equal(zc.bfs(g, 0, placement=p, collect_traffic=False).values, ref.values)
+    zc.release(g)
