@@ -39,7 +39,7 @@ def _same(r, ref, full=True):
     return ok
 
 
-@settings(max_examples=int(__import__("os").environ.get("ZC_HYP_EXAMPLES", "200")), deadline=None, derandomize=True,
+@settings(max_examples=int(__import__("os").environ.get("ZC_HYP_EXAMPLES", "200")), deadline=None, derandomize=__import__("os").environ.get("ZC_HYP_RANDOM") != "1",
           suppress_health_check=list(HealthCheck))
 @given(graphs())
 def test_random_graphs_match_oracle(case):
@@ -69,7 +69,7 @@ def test_random_graphs_match_oracle(case):
 
 
 @settings(max_examples=int(__import__("os").environ.get("ZC_HYP_EXAMPLES", "200")) // 4,
-          deadline=None, derandomize=True,
+          deadline=None, derandomize=__import__("os").environ.get("ZC_HYP_RANDOM") != "1",
           suppress_health_check=list(HealthCheck))
 @given(graphs(), st.integers(1, 4), st.sampled_from(["merged-aligned", "packed"]),
        st.sampled_from([(False, "bitmap"), (True, "bitmap"), (True, "store")]))
