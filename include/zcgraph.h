@@ -178,7 +178,9 @@ int zc_cc(zc_graph *g, int strategy, int64_t *out, zc_stats *stats);
  *     the near set runs dry the threshold moves to the smallest waiting
  *     distance + delta (delta = 0: the default, 16).
  *   zc_cc_afforest: union-find (Afforest's schedule): pass 1 unions every
- *     vertex with the neighbours of its list's first window, pass 2 only the
+ *     vertex with the neighbours of its list's first window (compressed: the
+ *     first 4 elements of a short list, 32 samples of a long list's first
+ *     line), pass 2 only the
  *     vertices outside the largest component whose lists reach further;
  *     iterations = passes.  Strategies naive .. compressed. */
 int zc_sssp_nearfar(zc_graph *g, uint64_t source, int strategy, uint64_t delta, int64_t *out,
@@ -274,7 +276,9 @@ int zc_set_options(zc_graph *g, uint32_t options);
  * preferred shared-memory carveout; no measurable effect on K27 BFS),
  * "widen=N" (host threads widening a pipelined result; more slow the next
  * traversal's zero-copy reads: K27, 2 / 4 / 8 / 12 threads, e2e 45.8 / 45.6 /
- * 45.5 / 45.0 GTEPS direction-optimizing).
+ * 45.5 / 45.0 GTEPS direction-optimizing), "uf_sample=N" (afforest's
+ * sampling pass over compressed lists: elements per short list, default 4;
+ * >= 96 reads short lists and long lists' first lines whole).
  * "unroll" also takes 16 (merged / merged-aligned BFS and CC).  NULL or "" resets the
  * defaults; an unknown entry is ZC_EINVAL.  Read by the run path; nothing is
  * taken from the environment. */

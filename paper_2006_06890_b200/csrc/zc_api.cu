@@ -85,6 +85,7 @@ void tune_params(ExpandArgs* a, const zc_graph* g) {
   a->chunk_sched = g->tune.sched;
   a->carveout = g->tune.carveout;
   a->ld = g->tune.ld;
+  a->uf_sample = g->tune.uf_sample ? static_cast<uint32_t>(g->tune.uf_sample) : kUfSample;
 }
 
 // ---------------------------------------------------------- pinned lists
@@ -1284,8 +1285,8 @@ int run_afforest(zc_graph* g, int strategy, int64_t* out, zc_stats* stats) {
       }
       i = j;
     }
-    ZC_CUDA_TRY(launch_uf_marks(parent, g->d_off, g->d_cpos, g->nv, giant, s1, g->eb, g->d_flags,
-                                st, &launches));
+    ZC_CUDA_TRY(launch_uf_marks(parent, g->d_off, g->d_cpos, g->nv, giant, s1, g->eb,
+                                args(0, 1).uf_sample, g->d_flags, st, &launches));
     CompactArgs c{};
     c.flags = g->d_flags;
     c.nv = g->nv;
@@ -2519,6 +2520,8 @@ int zc_set_tuning(zc_graph* g, const char* spec) {
     else if (k == "ld" && v.size() == 1 && v[0] >= '0' && v[0] <= '3') t.ld = v[0] - '0';
     else if (k == "pairs" && (v == "0" || v == "1")) t.pairs = v == "1";
     else if (k == "widen" && atoi(v.c_str()) > 0 && atoi(v.c_str()) <= 256) t.widen = atoi(v.c_str());
+    else if (k == "uf_sample" && atoi(v.c_str()) > 0 && atoi(v.c_str()) <= 1024)
+      t.uf_sample = atoi(v.c_str());
     else if (k == "carveout" && !v.empty() && atoi(v.c_str()) >= 0 && atoi(v.c_str()) <= 100)
       t.carveout = atoi(v.c_str());
     else {

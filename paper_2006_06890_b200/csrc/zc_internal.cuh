@@ -77,6 +77,10 @@ constexpr uint32_t kCmpMaxCount = 256;
 constexpr uint32_t kLineWords = 32;
 constexpr uint32_t kLineBits = 1024;
 constexpr uint32_t kCmpShortMaxDeg = 96;
+// Afforest's sampling pass over compressed lists reads this many elements of
+// each short list and one per lane of a long list's first line (the rest of a
+// list outside the giant component is read by the second pass).
+constexpr uint32_t kUfSample = 4;
 // Short lists are packed into 256-byte spans (two lines) and never straddle
 // one: a U27 SSSP list (540 bits) then shares its span with two others.
 constexpr uint32_t kShortSpanBits = 2 * kLineBits;
@@ -199,6 +203,11 @@ struct ExpandArgs {
   // lines of the long in-lists still without a parent (0: one pass, all)
   const uint32_t* fbits;
   uint32_t pull_pass;
+  // union-find sampling pass (kCcUf, pull_pass 1) over compressed lists:
+  // elements read per short list, and per lane of a long list's first line
+  // when below kCmpShortMaxDeg (>= kCmpShortMaxDeg: short lists and the first
+  // line whole)
+  uint32_t uf_sample;
 };
 
 // Expansion tuning knobs of a handle (zc_set_tuning "unroll=8,ctas=6,sched=chunk").
@@ -284,7 +293,8 @@ cudaError_t launch_uf_sample(const uint32_t* parent, uint64_t nv, uint32_t* out,
                              cudaStream_t st, uint64_t* launches);
 cudaError_t launch_uf_marks(const uint32_t* parent, const uint64_t* off, const uint64_t* cpos,
                             uint64_t nv, uint32_t giant, int strategy, int edge_bytes,
-                            uint8_t* flags, cudaStream_t st, uint64_t* launches);
+                            uint32_t uf_sample, uint8_t* flags, cudaStream_t st,
+                            uint64_t* launches);
 cudaError_t launch_fval_ids(const uint32_t* front, uint64_t* fval, uint64_t n, cudaStream_t st,
                             uint64_t* launches);
 // BFS levels (all below 255) as u8, 0xff = unreached.

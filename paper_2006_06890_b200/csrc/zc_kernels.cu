@@ -646,14 +646,17 @@ __device__ __forceinline__ uint32_t visit_line(const ExpandArgs& a, uint32_t x, 
   }
   uint32_t val = incl - run;
   const uint32_t wb = kCmpHdrBits + (cnt - 1) * w;
-  for (uint32_t e = e0; e < e1; ++e) {
+  uint32_t e1v = e1;  // union-find sampling pass: one element per lane
+  if constexpr (ALGO == kCcUf)
+    if (a.pull_pass == 1 && a.uf_sample < kCmpShortMaxDeg) e1v = min(e1, e0 + 1);
+  for (uint32_t e = e0; e < e1v; ++e) {
     val += e == 0 ? L[0] : line_bits(L, kCmpHdrBits + (e - 1) * w, w);
     uint64_t wt = 0;
     if constexpr (AlgoTraits<ALGO>::weighted) wt = a.cmp_wmin + line_bits(L, wb + e * a.cmp_ww, a.cmp_ww);
     Visit<ALGO>::apply(a, val, wt, sval);
   }
   __syncwarp();
-  return e1 > e0 ? e1 - e0 : 0u;  // elements this lane visited
+  return e1v > e0 ? e1v - e0 : 0u;  // elements this lane visited
 }
 
 // Decode the short lists of staged slots [k0, k1) from their shared line
@@ -679,7 +682,10 @@ __device__ __forceinline__ uint32_t visit_short(const ExpandArgs& a, uint32_t x,
     const uint32_t w = d ? line_bits(L, p, kCmpShortWidthBits) : 0;
     uint32_t val = d ? line_bits(L, p + kCmpShortWidthBits, a.cmp_b0) : 0;
     const uint32_t wb = p + hdr + (d - 1) * w;
-    for (uint32_t e = 0; e < d; ++e) {
+    uint32_t dv = d;  // union-find sampling pass: the first uf_sample elements
+    if constexpr (ALGO == kCcUf)
+      if (a.pull_pass == 1) dv = min(d, a.uf_sample);
+    for (uint32_t e = 0; e < dv; ++e) {
       // bottom-up: stop at the first parent (or a candidate found elsewhere)
       if (AlgoTraits<ALGO>::pull && is_visited(a, sval)) break;
       if (e) val += line_bits(L, p + hdr + (e - 1) * w, w);
@@ -1324,14 +1330,19 @@ __global__ void k_uf_sample(const uint32_t* parent, uint64_t nv, uint32_t* out, 
 // elements beyond the window(s) pass 1 read (the first window; for the
 // compressed stream the first line of a long list, short lists whole).
 __global__ void k_uf_marks(const uint32_t* parent, const uint64_t* off, const uint64_t* cpos,
-                           uint64_t nv, uint32_t giant, int strategy, int eb, uint8_t* flags) {
+                           uint64_t nv, uint32_t giant, int strategy, int eb,
+                           uint32_t uf_sample, uint8_t* flags) {
   for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv;
        v += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t s = off[v], e = off[v + 1];
     bool rest;
     if (strategy == kCompressed) {
+      // the sampling pass read uf_sample elements of a short list, one per
+      // lane of a long list's first line (uf_sample >= kCmpShortMaxDeg: short
+      // lists and the first line whole)
       const uint64_t c = cpos[v];
-      rest = (c & kCmpLong) && cmp_lines(c) > 1;
+      rest = uf_sample < kCmpShortMaxDeg ? (c & kCmpLong) || e - s > uf_sample
+                                         : (c & kCmpLong) && cmp_lines(c) > 1;
     } else if (strategy == kNaive) {
       rest = false;  // the naive sweep reads whole lists in pass 1
     } else {
@@ -2002,10 +2013,11 @@ cudaError_t launch_uf_sample(const uint32_t* parent, uint64_t nv, uint32_t* out,
 
 cudaError_t launch_uf_marks(const uint32_t* parent, const uint64_t* off, const uint64_t* cpos,
                             uint64_t nv, uint32_t giant, int strategy, int edge_bytes,
-                            uint8_t* flags, cudaStream_t st, uint64_t* launches) {
+                            uint32_t uf_sample, uint8_t* flags, cudaStream_t st,
+                            uint64_t* launches) {
   if (!nv) return cudaSuccess;
   k_uf_marks<<<grid_for(nv, 256, 148, 8), 256, 0, st>>>(parent, off, cpos, nv, giant, strategy,
-                                                        edge_bytes, flags);
+                                                        edge_bytes, uf_sample, flags);
   *launches += 1;
   return cudaGetLastError();
 }

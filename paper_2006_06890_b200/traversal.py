@@ -172,8 +172,8 @@ def cc(g, strategy=AccessStrategy.MERGED_ALIGNED, *, collect_traffic: Optional[b
     ``schedule="afforest"`` (B200 extension) computes the same labels by
     union-find in at most two passes over the lists (iterations = passes;
     ``traversed_edges[k]`` = the list elements pass k read: the first window
-    of every list, then the whole lists of the vertices outside the giant
-    component)."""
+    of every list (compressed: a sample, ``DeviceGraph.set_tuning("uf_sample=N")``),
+    then the whole lists of the vertices outside the giant component)."""
     if g.directed:
         raise ValueError("connected components require an undirected graph "
                          "(load with directed=False or symmetrize first)")

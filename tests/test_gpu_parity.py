@@ -822,6 +822,27 @@ def test_work_efficient_schedules_rmat():
         assert np.array_equal(r.values, ref.values), delta
 
 
+def test_afforest_compressed_sampling_widths():
+    """Afforest's sampling pass over compressed lists reads uf_sample elements
+    per short list (one per lane of a long list's first line); the second
+    pass completes every list outside the giant component, so the labels do
+    not depend on the width (>= 96: short lists and first lines whole)."""
+    for scale, seed in ((16, 3), (17, 11)):
+        k = zc.generate_rmat(scale, 16, seed=seed, symmetrize=True)
+        gk = k.as_csr()
+        ref = oracle.cc(gk, threads=8)
+        work = {}
+        for w in (1, 4, 16, 96):
+            k.set_tuning(f"uf_sample={w}")
+            r = zc.cc(k, "compressed", schedule="afforest")
+            assert np.array_equal(r.values, ref.values), (scale, w)
+            assert r.iterations <= 2
+            work[w] = r.traversed_edges[0]
+        assert work[1] < work[4] < work[16] <= work[96] < gk.num_edges, work
+        k.set_tuning("")
+        k.close()
+
+
 def test_schedule_argument_errors():
     g = zc.with_uniform_weights(zc.generate_uniform(64, 1, 4, seed=1))
     with pytest.raises(ValueError, match="schedule"):
