@@ -141,7 +141,21 @@ void* pinned_list_alloc(int device, size_t bytes) {
   bytes = std::max<size_t>(bytes, 1);
   if (bytes >= (64ull << 20)) {
     const int node = numa_disabled() ? -1 : gpu_numa_node(device);
-    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    // a 2 MiB-aligned mapping of whole 2 MiB pages: an unaligned one is only
+    // partly backed by huge pages, and registering 4 KiB pages is slow (a
+    // 6.2 GB stream took 0.4-0.9 s in cudaHostRegister instead of ~0.15 s)
+    constexpr size_t kHuge = 2ull << 20;
+    bytes = (bytes + kHuge - 1) & ~(kHuge - 1);
+    void* p = MAP_FAILED;
+    void* raw = mmap(nullptr, bytes + kHuge, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS,
+                     -1, 0);
+    if (raw != MAP_FAILED) {
+      const uintptr_t r = reinterpret_cast<uintptr_t>(raw);
+      const uintptr_t a = (r + kHuge - 1) & ~(kHuge - 1);
+      if (a > r) munmap(raw, a - r);
+      if (r + kHuge > a) munmap(reinterpret_cast<void*>(a + bytes), r + kHuge - a);
+      p = reinterpret_cast<void*>(a);
+    }
     if (p != MAP_FAILED) {
       bool ok = true;
       if (node >= 0 && node < 64) {

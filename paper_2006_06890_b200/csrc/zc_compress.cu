@@ -282,11 +282,20 @@ __global__ void k_in_scatter(uint64_t nv, const uint64_t* off, const uint32_t* e
 // device temporaries are released on every path
 struct DevBuf {
   void* p = nullptr;
-  ~DevBuf() { cudaFree(p); }
-  void* release() {
+  ~DevBuf() { reset(); }
+  cudaError_t scratch(size_t bytes) { return cudaMalloc(&p, bytes); }
+  void reset() {
+    cudaFree(p);
+    p = nullptr;
+  }
+  void* release() {  // the buffer changes owner
     void* q = p;
     p = nullptr;
     return q;
+  }
+  void take(DevBuf* o) {
+    reset();
+    p = o->release();
   }
 };
 
@@ -299,16 +308,19 @@ uint32_t first_element_bits(const zc_graph* g) {
   return maxid > 1 ? 64 - __builtin_clzll(maxid - 1) : 1;
 }
 
+// enc_kept: the stream stays in HBM (an HBM-placed handle keeps it), else it
+// is scratch until copied to host memory.  The encode is left running: the
+// caller's host-side allocation overlaps it.
 int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t ww, uint32_t b0,
-                  DevBuf* cpos, DevBuf* enc, size_t* bytes) {
+                  bool enc_kept, DevBuf* cpos, DevBuf* enc, size_t* bytes) {
   DevBuf size, blk, tmp, err;
   const uint64_t nb = (nv + kPlaceBlock - 1) / kPlaceBlock;
-  ZC_CUDA_TRY(cudaMalloc(&size.p, std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
+  ZC_CUDA_TRY(size.scratch(std::max<uint64_t>(nv, 1) * sizeof(uint32_t)));
   k_cmp_size<<<kCmpGrid, 256>>>(nv, d_off, x, ww, b0, static_cast<uint32_t*>(size.p));
   ZC_CUDA_TRY(cudaGetLastError());
   ZC_CUDA_TRY(cudaMalloc(&cpos->p, (nv + 1) * sizeof(uint64_t)));
-  ZC_CUDA_TRY(cudaMalloc(&blk.p, (nb + 1) * 2 * sizeof(uint64_t)));  // sizes, then bases
-  ZC_CUDA_TRY(cudaMalloc(&err.p, sizeof(unsigned)));
+  ZC_CUDA_TRY(blk.scratch((nb + 1) * 2 * sizeof(uint64_t)));  // sizes, then bases
+  ZC_CUDA_TRY(err.scratch(sizeof(unsigned)));
   ZC_CUDA_TRY(cudaMemset(err.p, 0, sizeof(unsigned)));
   uint64_t* bbits = static_cast<uint64_t*>(blk.p);
   uint64_t* bbase = bbits + nb + 1;
@@ -319,7 +331,7 @@ int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t w
   ZC_CUDA_TRY(cudaGetLastError());
   size_t tb = 0;
   ZC_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, bbits, bbase, nb + 1));
-  ZC_CUDA_TRY(cudaMalloc(&tmp.p, std::max<size_t>(tb, 1)));
+  ZC_CUDA_TRY(tmp.scratch(std::max<size_t>(tb, 1)));
   ZC_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tb, bbits, bbase, nb + 1));
   k_cmp_place_add<<<kCmpGrid, 256>>>(nv, static_cast<uint64_t*>(cpos->p), bbase);
   ZC_CUDA_TRY(cudaGetLastError());
@@ -338,11 +350,12 @@ int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t w
   }
   const uint64_t lines = end / kLineBits;  // span-aligned, so whole lines
   *bytes = std::max<uint64_t>(lines, 1) * kLineBytes;
-  ZC_CUDA_TRY(cudaMalloc(&enc->p, *bytes));
-  ZC_CUDA_TRY(cudaMemset(enc->p, 0, *bytes));
+  if (enc_kept) ZC_CUDA_TRY(cudaMalloc(&enc->p, *bytes));
+  else ZC_CUDA_TRY(enc->scratch(*bytes));
+  ZC_CUDA_TRY(cudaMemsetAsync(enc->p, 0, *bytes, 0));
   k_cmp_encode<<<kCmpGrid, 256>>>(nv, d_off, x, ww, b0, static_cast<uint64_t*>(cpos->p),
                                   static_cast<uint32_t*>(enc->p));
-  ZC_CUDA_TRY(cudaDeviceSynchronize());
+  ZC_CUDA_TRY(cudaGetLastError());
   return ZC_OK;
 }
 
@@ -370,7 +383,7 @@ int place_stream(zc_graph* g, DevBuf* enc, size_t bytes, void** host_out, const 
       set_error("cannot allocate host memory for the compressed lists");
       return ZC_ENOMEM;
     }
-    build_mark(g, "pin_alloc");
+    build_mark(g, "encode+pin_alloc");  // the host allocation overlaps the encode
     const void* d = nullptr;
     if (cudaMemcpy(host, enc->p, bytes, cudaMemcpyDefault) != cudaSuccess ||
         (g->placement != ZC_PLACE_HBM && host_list_device_ptr(host, &d) != ZC_OK)) {
@@ -396,9 +409,10 @@ int install_in_lists(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted) {
   DevBuf enc, cpos;
   Elems x{d_in_sorted, nullptr, 0};
   size_t bytes = 0;
-  int rc = encode_stream(g->nv, d_in_off, x, 0, first_element_bits(g), &cpos, &enc, &bytes);
+  int rc = encode_stream(g->nv, d_in_off, x, 0, first_element_bits(g),
+                         g->placement == ZC_PLACE_HBM, &cpos, &enc, &bytes);
   if (rc) return rc;
-  build_mark(g, "in:size_place_encode");
+  build_mark(g, "in:size_place");
   void* host = nullptr;
   const void* dev = nullptr;
   void* hbm = nullptr;
@@ -451,9 +465,9 @@ int build_out_stream(zc_graph* g, DevBuf* keep_lists) {
   Elems x{nullptr, nullptr, 0};
   uint32_t ww = 0;
   if (weighted) {
-    ZC_CUDA_TRY(cudaMalloc(&sorted.p, std::max<uint64_t>(ne, 1) * 8));
-    ZC_CUDA_TRY(cudaMalloc(&wtmp.p, std::max<uint64_t>(ne, 1) * 8));
-    ZC_CUDA_TRY(cudaMalloc(&range.p, 2 * sizeof(unsigned)));
+    ZC_CUDA_TRY(sorted.scratch(std::max<uint64_t>(ne, 1) * 8));
+    ZC_CUDA_TRY(wtmp.scratch(std::max<uint64_t>(ne, 1) * 8));
+    ZC_CUDA_TRY(range.scratch(2 * sizeof(unsigned)));
     const unsigned init[2] = {0xffffffffu, 0u};
     ZC_CUDA_TRY(cudaMemcpy(range.p, init, sizeof(init), cudaMemcpyHostToDevice));
     uint32_t* de = static_cast<uint32_t*>(wtmp.p);
@@ -465,7 +479,7 @@ int build_out_stream(zc_graph* g, DevBuf* keep_lists) {
     ZC_CUDA_TRY(cudaGetLastError());
     unsigned hr[2];
     ZC_CUDA_TRY(cudaMemcpy(hr, r, sizeof(hr), cudaMemcpyDeviceToHost));
-    cudaFree(wtmp.release());
+    wtmp.reset();
     if (!ne) hr[0] = hr[1] = 0;
     x.e64 = static_cast<const uint64_t*>(sorted.p);
     x.wmin = hr[0];
@@ -474,7 +488,7 @@ int build_out_stream(zc_graph* g, DevBuf* keep_lists) {
     const int rc = sort_lists_device(8, nv, g->d_off, sorted.p);
     if (rc) return rc;
   } else {
-    ZC_CUDA_TRY(cudaMalloc(&sorted.p, std::max<uint64_t>(ne, 1) * 4));
+    ZC_CUDA_TRY(sorted.scratch(std::max<uint64_t>(ne, 1) * 4));
     ZC_CUDA_TRY(cudaMemcpy(sorted.p, g->h_edges, ne * 4, cudaMemcpyDefault));
     build_mark(g, "out:h2d_copy");
     const int rc = sort_lists_device(4, nv, g->d_off, sorted.p);
@@ -482,13 +496,15 @@ int build_out_stream(zc_graph* g, DevBuf* keep_lists) {
     x.e32 = static_cast<const uint32_t*>(sorted.p);
   }
   build_mark(g, "out:sort");
+  g->build_log.emplace_back("out:sort[gpu]", last_sort_gpu_ms());
   size_t bytes = 0;
   const uint32_t b0 = first_element_bits(g);
-  int rc = encode_stream(nv, g->d_off, x, ww, b0, &cpos, &enc, &bytes);
+  int rc = encode_stream(nv, g->d_off, x, ww, b0, g->placement == ZC_PLACE_HBM, &cpos, &enc,
+                         &bytes);
   if (rc) return rc;
-  if (keep_lists && !weighted) keep_lists->p = sorted.release();
-  cudaFree(sorted.release());
-  build_mark(g, "out:size_place_encode");
+  if (keep_lists && !weighted) keep_lists->take(&sorted);
+  sorted.reset();
+  build_mark(g, "out:size_place");
   void* host = nullptr;
   const void* dev = nullptr;
   void* hbm = nullptr;
@@ -556,33 +572,34 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
   } else {
     DevBuf in_e, deg, in_off, tmp;
     if (!out_e.p) {
-      ZC_CUDA_TRY(cudaMalloc(&out_e.p, std::max<uint64_t>(ne, 1) * 4));
+      ZC_CUDA_TRY(out_e.scratch(std::max<uint64_t>(ne, 1) * 4));
       ZC_CUDA_TRY(cudaMemcpy(out_e.p, g->h_edges, ne * 4, cudaMemcpyDefault));
       build_mark(g, "in:h2d_copy");
     }
-    ZC_CUDA_TRY(cudaMalloc(&deg.p, std::max<uint64_t>(nv, 1) * 4));
+    ZC_CUDA_TRY(deg.scratch(std::max<uint64_t>(nv, 1) * 4));
     ZC_CUDA_TRY(cudaMemset(deg.p, 0, std::max<uint64_t>(nv, 1) * 4));
     k_in_count<<<kCmpGrid, 256>>>(ne, static_cast<uint32_t*>(out_e.p),
                                   static_cast<uint32_t*>(deg.p));
     ZC_CUDA_TRY(cudaGetLastError());
     ZC_CUDA_TRY(cudaMalloc(&in_off.p, (nv + 1) * sizeof(uint64_t)));
     const size_t tb = scan_tmp_bytes(nv);
-    ZC_CUDA_TRY(cudaMalloc(&tmp.p, tb));
+    ZC_CUDA_TRY(tmp.scratch(tb));
     ZC_CUDA_TRY(scan_u32_to_u64(static_cast<uint32_t*>(deg.p), static_cast<uint64_t*>(in_off.p),
                                 nv, tmp.p, tb, 0));
-    cudaFree(tmp.release());
+    tmp.reset();
     ZC_CUDA_TRY(cudaMemset(deg.p, 0, std::max<uint64_t>(nv, 1) * 4));  // now the cursors
-    ZC_CUDA_TRY(cudaMalloc(&in_e.p, std::max<uint64_t>(ne, 1) * 4));
+    ZC_CUDA_TRY(in_e.scratch(std::max<uint64_t>(ne, 1) * 4));
     k_in_scatter<<<kCmpGrid, 256>>>(nv, g->d_off, static_cast<uint32_t*>(out_e.p),
                                     static_cast<uint64_t*>(in_off.p),
                                     static_cast<uint32_t*>(deg.p), static_cast<uint32_t*>(in_e.p));
     ZC_CUDA_TRY(cudaGetLastError());
-    cudaFree(out_e.release());
-    cudaFree(deg.release());
+    out_e.reset();
+    deg.reset();
     build_mark(g, "in:transpose");
     rc = sort_lists_device(4, nv, static_cast<uint64_t*>(in_off.p), in_e.p);
     if (rc) return rc;
     build_mark(g, "in:sort");
+    g->build_log.emplace_back("in:sort[gpu]", last_sort_gpu_ms());
     if ((rc = install_in_lists(g, static_cast<uint64_t*>(in_off.p),
                                static_cast<uint32_t*>(in_e.p))))
       return rc;

@@ -313,6 +313,23 @@ int offsets_from_degrees(zc_graph* g, uint32_t* d_deg, uint64_t nv, uint64_t** d
   return ZC_OK;
 }
 
+// Any list not ascending?  A warp per list, lanes compare neighbours.
+template <typename ET>
+__global__ void k_lists_unsorted(uint64_t nv, const uint64_t* off, const ET* edges,
+                                 unsigned* bad) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t v = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) / 32; v < nv; v += warps) {
+    const uint64_t s = off[v], e = off[v + 1];
+    bool b = false;
+    for (uint64_t i = s + 1 + lane; i < e && !b; i += 32) b = edges[i - 1] > edges[i];
+    if (__any_sync(0xffffffffu, b)) {
+      if (lane == 0) atomicOr(bad, 1u);
+      return;
+    }
+  }
+}
+
 // Offsets of a batch of lists relative to its first element (CUB takes int).
 __global__ void k_rel_offsets(uint64_t n, const uint64_t* off, uint64_t base, int* rel) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n;
@@ -323,10 +340,26 @@ __global__ void k_rel_offsets(uint64_t n, const uint64_t* off, uint64_t base, in
 // Sort every list ascending: CUB's segmented sort (segments partitioned by
 // size into sub-warp / warp / CTA sorts) over batches of consecutive lists
 // holding at most 2^30 keys (CUB takes int sizes), out of place into a batch
-// buffer, copied back.
+// buffer, copied back; lists already ascending are left as they are.
+// t_sort_gpu_ms: the GPU time of this thread's last call's sorts and copies
+// (CUDA events; the rest of its wall time is allocation and batching).
+thread_local float t_sort_gpu_ms = 0;
+
 template <typename ET>
 int sort_lists(uint64_t nv, const uint64_t* d_off, ET* edges) {
+  t_sort_gpu_ms = 0;
   if (nv == 0) return ZC_OK;
+  {  // already ascending (graphs built by a lexsort, symmetrized ones): done
+    unsigned* bad = nullptr;
+    ZC_CUDA_TRY(cudaMalloc(&bad, sizeof(unsigned)));
+    unsigned h = 1;
+    cudaMemset(bad, 0, sizeof(unsigned));
+    k_lists_unsorted<ET><<<kGenGrid, 256>>>(nv, d_off, edges, bad);
+    const cudaError_t e = cudaMemcpy(&h, bad, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(bad);
+    ZC_CUDA_TRY(e);
+    if (!h) return ZC_OK;
+  }
   std::vector<uint64_t> cut{0};
   auto off_at = [&](uint64_t v, uint64_t* x) {
     return cudaMemcpy(x, d_off + v, sizeof(*x), cudaMemcpyDeviceToHost);
@@ -380,6 +413,10 @@ int sort_lists(uint64_t nv, const uint64_t* d_off, ET* edges) {
     }
     span -= base;
     if (span == 0) continue;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, 0);
     k_rel_offsets<<<kGenGrid, 256>>>(n, d_off + v0, base, rel);
     size_t need = 0;
     cub::DeviceSegmentedSort::SortKeys(nullptr, need, edges + base, out, static_cast<int>(span),
@@ -397,11 +434,17 @@ int sort_lists(uint64_t nv, const uint64_t* d_off, ET* edges) {
     if (cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, edges + base, out,
                                            static_cast<int>(span), static_cast<int>(n), rel,
                                            rel + 1) != cudaSuccess ||
-        cudaMemcpy(edges + base, out, span * sizeof(ET), cudaMemcpyDeviceToDevice) !=
+        cudaMemcpyAsync(edges + base, out, span * sizeof(ET), cudaMemcpyDeviceToDevice, 0) !=
             cudaSuccess) {
       rc = ZC_ECUDA;
       set_error(std::string("list sort: ") + cudaGetErrorString(cudaGetLastError()));
     }
+    cudaEventRecord(e1, 0);
+    float ms = 0;
+    if (cudaEventSynchronize(e1) == cudaSuccess && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess)
+      t_sort_gpu_ms += ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   }
   cudaFree(rel);
   cudaFree(out);
@@ -827,6 +870,8 @@ int generate_uniform(uint64_t nv, uint32_t dmin, uint32_t dmax, uint64_t seed, i
 }  // namespace
 
 int part_in_lists(zc_graph* g) { return rmat_part_in_lists(g); }
+
+float last_sort_gpu_ms() { return t_sort_gpu_ms; }
 
 int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, void* edges) {
   int rc = elem_bytes == 4 ? sort_lists<uint32_t>(nv, d_off, static_cast<uint32_t*>(edges))

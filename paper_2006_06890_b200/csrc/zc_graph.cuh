@@ -174,6 +174,7 @@ int finish_create(zc_graph* g);  // prefetch (UVM) + sync
 int init_partition(zc_graph* g, const zc_part_info* info);
 // pinned mapped list buffers, NUMA-local to the GPU when the host has several nodes
 void* pinned_list_alloc(int device, size_t bytes);
+
 void pinned_list_free(void* p);
 // Host-side list buffer of a handle: pinned (ZEROCOPY, and the HBM run's
 // shadow) or host-resident managed memory (ZEROCOPY_MANAGED).  Freed with

@@ -237,7 +237,8 @@ class DeviceGraph:
 
     def build_log(self) -> list:
         """[(phase, wall ms)] of this handle's one-time builds (compressed out /
-        in-list streams), in order (zc_graph_build_log)."""
+        in-list streams), in order (zc_graph_build_log); "…[gpu]" entries are
+        the GPU time inside the phase before them, not phases of their own."""
         need = N.lib().zc_graph_build_log(self.handle, None, 0)
         if need < 0:
             N.check(need)
