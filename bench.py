@@ -691,18 +691,32 @@ def other_configs(zc, args, device, oc, parity) -> dict:
         out[f"{tag}/merged-aligned"]["pcie_read_frac_ncu"] = link["cc_k27sym_merged_aligned"]
     # PageRank streams the whole zero-copy list every
     # iteration (5 iterations timed; parity is pinned on the reference's
-    # PageRank fixtures in the GPU tests, not at this size)
+    # PageRank fixtures in the GPU tests; here against the oracle's threaded
+    # C pull: float64 sums against the library's 2^-62 fixed-point sums, so
+    # |gpu - oracle| <= 1e-9 rank + 1e-16 per vertex (1e-16 ~ 450 quanta; the
+    # smallest ranks, ~1e-9 at K27, carry a few quanta per summed element)
+    import oracle
     import warnings
+    t0 = time.perf_counter()
+    pr_ref = oracle.pagerank_c(gk, 0.85, 5, 1e-30, threads=oc.threads, symmetric=True)
+    pr_s = time.perf_counter() - t0
+    tag = f"pagerank_kron{args.scale}_sym"
     for s in ("merged-aligned", "compressed"):
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")  # the multigraph note (duplicates are kept)
             zc.pagerank(k, s, max_iters=1, tol=1e-30, collect_traffic=False)
             r = zc.pagerank(k, s, max_iters=5, tol=1e-30, collect_traffic=False)
         t = r.kernel_ms * 1e-3
-        out[f"pagerank_kron{args.scale}_sym/{s}"] = {
+        err = np.abs(r.values - pr_ref.values)
+        out[f"{tag}/{s}"] = {
             "iterations": r.iterations, "kernel_ms": r.kernel_ms,
             "edge_gteps": r.total_traversed_edges / t / 1e9,
-            "link_gbs_8d": r.total_traversed_edges * 4 / (r.expand_ms * 1e-3) / 1e9}
+            "link_gbs_8d": r.total_traversed_edges * 4 / (r.expand_ms * 1e-3) / 1e9,
+            "max_abs_err_vs_oracle": float(err.max()),
+            "max_rel_err_vs_oracle": float(np.max(err / pr_ref.values))}
+        parity[f"{tag}/{s}"] = bool(r.iterations == pr_ref.iterations
+                                    and np.all(err <= 1e-9 * pr_ref.values + 1e-16))
+    out[f"{tag}/cpu_port_edge_gteps"] = sum(pr_ref.traversed_edges) / pr_s / 1e9
     k.close()
     return out
 

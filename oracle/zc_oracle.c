@@ -16,6 +16,14 @@
  *   zco_cc    <- cc    traversal.py:154-179 (Jacobi min-label propagation,
  *                all vertices active first)
  *   traversed[k] = sum of frontier degrees of iteration k (traversal.py:63-65)
+ *   zco_pagerank <- pagerank traversal.py:191-249 (synchronous power
+ *                iteration, dangling mass spread uniformly, L1 stopping
+ *                rule, final normalisation) as a pull over in-lists -- the
+ *                out-lists themselves for an undirected graph; float64 sums
+ *                in a different order than the reference's bincount, so
+ *                results agree to rounding, not bit for bit (the numpy
+ *                restatement oracle.pagerank is the one pinned bit-close to
+ *                the reference fixtures; tests check this one against it)
  *
  * Pinning: tests/test_oracle_golden.py checks this file against fixtures
  * produced by the reference itself (tests/golden/make_golden.py): 406 small
@@ -29,6 +37,7 @@
  */
 #include <stdint.h>
 #include <stdlib.h>
+#include <math.h>
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
@@ -198,5 +207,85 @@ int64_t zco_cc(uint64_t nv, const int64_t *off, const void *edges, int eb, int64
     n = collect(nv, off, s.mark, s.front, &t, nt);
   }
   free_scratch(&s);
+  return (int64_t)it;
+}
+
+/* ranks: float64[nv] out.  Returns the iteration count, -1 on allocation
+ * failure.  symmetric != 0: the lists are their own transpose. */
+int64_t zco_pagerank(uint64_t nv, const int64_t *off, const void *edges, int eb, int symmetric,
+                     double damping, uint64_t max_iters, double tol, double *ranks,
+                     int nthreads) {
+  int nt = nthreads > 0 ? nthreads : 1;
+  if (nv == 0) return 0;
+  const int64_t *ioff = off;
+  const uint32_t *iedges = NULL;
+  int64_t *toff = NULL;
+  uint32_t *tedges = NULL;
+  if (!symmetric) {  /* counting transpose: in-list of v = the sources of arcs into v */
+    const uint64_t ne = (uint64_t)off[nv];
+    toff = calloc(nv + 1, sizeof(int64_t));
+    tedges = malloc((ne ? ne : 1) * sizeof(uint32_t));
+    uint64_t *cur = calloc(nv, sizeof(uint64_t));
+    if (!toff || !tedges || !cur) {
+      free(toff);
+      free(tedges);
+      free(cur);
+      return -1;
+    }
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (uint64_t k = 0; k < ne; ++k)
+      __atomic_fetch_add(&toff[ld_elem(edges, eb, k) + 1], 1, __ATOMIC_RELAXED);
+    for (uint64_t v = 0; v < nv; ++v) toff[v + 1] += toff[v];
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1024)
+    for (uint64_t u = 0; u < nv; ++u)
+      for (int64_t k = off[u]; k < off[u + 1]; ++k) {
+        const uint64_t w = ld_elem(edges, eb, (uint64_t)k);
+        tedges[toff[w] + __atomic_fetch_add(&cur[w], 1, __ATOMIC_RELAXED)] = (uint32_t)u;
+      }
+    free(cur);
+    ioff = toff;
+    iedges = tedges;
+  }
+  double *contrib = malloc(nv * sizeof(double)), *next = malloc(nv * sizeof(double));
+  if (!contrib || !next) {
+    free(contrib);
+    free(next);
+    free(toff);
+    free(tedges);
+    return -1;
+  }
+  for (uint64_t v = 0; v < nv; ++v) ranks[v] = 1.0 / (double)nv;
+  uint64_t it = 0;
+  while (it < max_iters) {
+    ++it;
+    double dang = 0;
+#pragma omp parallel for num_threads(nt) schedule(static) reduction(+ : dang)
+    for (uint64_t u = 0; u < nv; ++u) {
+      const int64_t d = off[u + 1] - off[u];
+      contrib[u] = d ? ranks[u] / (double)d : 0.0;
+      if (!d) dang += ranks[u];
+    }
+    const double base = (1.0 - damping) / (double)nv + damping * dang / (double)nv;
+    double delta = 0;
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 1024) reduction(+ : delta)
+    for (uint64_t v = 0; v < nv; ++v) {
+      double acc = 0;
+      if (iedges)
+        for (int64_t k = ioff[v]; k < ioff[v + 1]; ++k) acc += contrib[iedges[k]];
+      else
+        for (int64_t k = ioff[v]; k < ioff[v + 1]; ++k) acc += contrib[ld_elem(edges, eb, (uint64_t)k)];
+      next[v] = base + damping * acc;
+      delta += fabs(next[v] - ranks[v]);
+    }
+    memcpy(ranks, next, nv * sizeof(double));
+    if (delta < tol) break;
+  }
+  double sum = 0;
+  for (uint64_t v = 0; v < nv; ++v) sum += ranks[v];
+  for (uint64_t v = 0; v < nv; ++v) ranks[v] /= sum;
+  free(contrib);
+  free(next);
+  free(toff);
+  free(tedges);
   return (int64_t)it;
 }
