@@ -278,7 +278,11 @@ int zc_set_options(zc_graph *g, uint32_t options);
  * traversal's zero-copy reads: K27, 2 / 4 / 8 / 12 threads, e2e 45.8 / 45.6 /
  * 45.5 / 45.0 GTEPS direction-optimizing), "uf_sample=N" (afforest's
  * sampling pass over compressed lists: elements per short list, default 4;
- * >= 96 reads short lists and long lists' first lines whole).
+ * >= 96 reads short lists and long lists' first lines whole), "sort=radix|
+ * segmented" (compressed builds sort the lists by two stable radix-sort
+ * transposes, which also yield the in-lists, or -- the fallback when their four
+ * edge-sized device buffers do not fit -- a count / scatter transpose and a
+ * segmented sort).
  * "unroll" also takes 16 (merged / merged-aligned BFS and CC).  NULL or "" resets the
  * defaults; an unknown entry is ZC_EINVAL.  Read by the run path; nothing is
  * taken from the environment. */

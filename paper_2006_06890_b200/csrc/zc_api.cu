@@ -2536,6 +2536,7 @@ int zc_set_tuning(zc_graph* g, const char* spec) {
     else if (k == "widen" && atoi(v.c_str()) > 0 && atoi(v.c_str()) <= 256) t.widen = atoi(v.c_str());
     else if (k == "uf_sample" && atoi(v.c_str()) > 0 && atoi(v.c_str()) <= 1024)
       t.uf_sample = atoi(v.c_str());
+    else if (k == "sort" && (v == "radix" || v == "segmented")) t.seg_sort = v == "segmented";
     else if (k == "carveout" && !v.empty() && atoi(v.c_str()) >= 0 && atoi(v.c_str()) <= 100)
       t.carveout = atoi(v.c_str());
     else {

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -277,6 +278,31 @@ __global__ void k_in_scatter(uint64_t nv, const uint64_t* off, const uint32_t* e
     }
 }
 
+// The owning list of every element: src[k] = v for off[v] <= k < off[v+1]
+// (warp per list; a hub list's warp streams its stores).
+__global__ void k_arc_sources(uint64_t nv, const uint64_t* off, uint32_t* src) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t v = gw; v < nv; v += nw) {
+    const uint64_t s = off[v], e = off[v + 1];
+    for (uint64_t k = s + lane; k < e; k += 32) src[k] = static_cast<uint32_t>(v);
+  }
+}
+
+// List offsets from sorted keys: off[j] = first i with keys[i] >= j, for
+// j in [0, nk]; thread i fills the offsets of the keys between keys[i-1] and
+// keys[i] (i == ne: up to nk), so every offset is written once.
+__global__ void k_offsets_from_sorted(uint64_t ne, const uint32_t* keys, uint64_t nk,
+                                      uint64_t* off) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= ne;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t lo = i ? static_cast<uint64_t>(keys[i - 1]) + 1 : 0;
+    const uint64_t hi = i < ne ? static_cast<uint64_t>(keys[i]) : nk;
+    for (uint64_t j = lo; j <= hi; ++j) off[j] = i;
+  }
+}
+
 }  // namespace
 
 // device temporaries are released on every path
@@ -298,6 +324,68 @@ struct DevBuf {
     p = o->release();
   }
 };
+
+namespace {
+// Transpose by a stable device radix sort: the nl lists (offsets d_off) of
+// element ids < nk become nk lists of list ids, ascending inside each list
+// (keys = elements, values = owning list ids in ascending order; LSD radix
+// sorting is stable).  Two transposes sort every list of a graph; one turns
+// sorted or unsorted out-lists into sorted in-lists.  Replaces a count /
+// atomic-cursor scatter followed by a segmented sort (~0.9 s at 2^31 arcs).
+// e (ne elements) is consumed; t_e / t_off (nk + 1 offsets) receive the
+// result (known_off: the result's offsets, when the caller has them; else
+// they come from the sorted keys).  Returns ZC_ENOMEM with e intact and
+// nothing allocated when the four ne-element buffers do not fit (callers
+// fall back).
+int radix_transpose(uint64_t nl, const uint64_t* d_off, DevBuf* e, uint64_t ne, uint64_t nk,
+                    DevBuf* t_e, DevBuf* t_off, zc_graph* g, const char* tag,
+                    const uint64_t* known_off = nullptr) {
+  auto mark = [&](const char* what) {
+    if (g) build_mark(g, (std::string(tag) + what).c_str());
+  };
+  const uint32_t bits = nk > 1 ? 64 - __builtin_clzll(nk - 1) : 1;
+  const size_t nb = std::max<uint64_t>(ne, 1) * sizeof(uint32_t);
+  DevBuf src, kalt, valt, off, tmp;
+  cub::DoubleBuffer<uint32_t> probe_k(nullptr, nullptr), probe_v(nullptr, nullptr);
+  size_t tb = 0;
+  ZC_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, probe_k, probe_v, ne, 0,
+                                              static_cast<int>(bits)));
+  if (src.scratch(nb) != cudaSuccess || kalt.scratch(nb) != cudaSuccess ||
+      valt.scratch(nb) != cudaSuccess || off.scratch((nk + 1) * sizeof(uint64_t)) != cudaSuccess ||
+      tmp.scratch(tb) != cudaSuccess) {
+    cudaGetLastError();  // the failed allocation is not sticky
+    return ZC_ENOMEM;
+  }
+  mark(":alloc");
+  uint32_t* ke = static_cast<uint32_t*>(e->p);
+  k_arc_sources<<<kCmpGrid, 256>>>(nl, d_off, static_cast<uint32_t*>(src.p));
+  ZC_CUDA_TRY(cudaGetLastError());
+  mark(":sources");
+  cub::DoubleBuffer<uint32_t> keys(ke, static_cast<uint32_t*>(kalt.p));
+  cub::DoubleBuffer<uint32_t> vals(static_cast<uint32_t*>(src.p), static_cast<uint32_t*>(valt.p));
+  ZC_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys, vals, ne, 0,
+                                              static_cast<int>(bits)));
+  if (known_off) {
+    ZC_CUDA_TRY(cudaMemcpyAsync(off.p, known_off, (nk + 1) * sizeof(uint64_t),
+                                cudaMemcpyDeviceToDevice, 0));
+  } else {
+    k_offsets_from_sorted<<<kCmpGrid, 256>>>(ne, keys.Current(), nk,
+                                             static_cast<uint64_t*>(off.p));
+    ZC_CUDA_TRY(cudaGetLastError());
+  }
+  mark(":radix");
+  DevBuf* held = vals.Current() == src.p ? &src : &valt;
+  t_e->take(held);
+  t_off->take(&off);
+  e->reset();
+  src.reset();
+  kalt.reset();
+  valt.reset();
+  tmp.reset();
+  mark(":free");
+  return ZC_OK;
+}
+}  // namespace
 
 // Sorted lists (x) over offsets d_off -> the line stream in device memory
 // (enc) and the per-vertex bit positions (cpos).
@@ -454,7 +542,60 @@ namespace {
 // The out-list stream.  keep_lists (unweighted graphs): hand the sorted device
 // copy of the raw lists to the caller (the in-list transpose reads it instead
 // of copying the lists from host memory again).
-int build_out_stream(zc_graph* g, DevBuf* keep_lists) {
+// Sort the out-lists in place (sorted: the device copy, offsets g->d_off):
+// two radix transposes, or the segmented sort when they do not fit.  With
+// keep_in_e, the first transpose's sorted in-lists are handed over too
+// (directed, unpartitioned graphs; left empty otherwise).
+int sort_out_lists(zc_graph* g, DevBuf* sorted, DevBuf* keep_in_e, DevBuf* keep_in_off) {
+  const uint64_t nv = g->nv, ne = g->ne;
+  const uint64_t nk = g->nparts ? g->global_nv : nv;
+  bool asc = false;
+  ZC_CUDA_TRY(lists_ascending(nv, g->d_off, static_cast<const uint32_t*>(sorted->p), &asc));
+  set_sort_gpu_ms(0);
+  if (asc) return ZC_OK;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, 0);
+  DevBuf tin, toff, oo;
+  int rc = g->tune.seg_sort ? ZC_ENOMEM : radix_transpose(nv, g->d_off, sorted, ne, nk, &tin, &toff, g, "out:t1");
+  if (rc == ZC_ENOMEM) {  // sorted is intact
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return sort_lists_device(4, nv, g->d_off, sorted->p);
+  }
+  const bool keep = keep_in_e && !g->nparts && (g->flags & ZC_F_DIRECTED);
+  DevBuf copy;
+  if (rc == ZC_OK && keep) {  // the second transpose consumes its input
+    if (copy.scratch(std::max<uint64_t>(ne, 1) * 4) == cudaSuccess) {
+      ZC_CUDA_TRY(cudaMemcpyAsync(copy.p, tin.p, ne * 4, cudaMemcpyDeviceToDevice, 0));
+    } else {
+      cudaGetLastError();
+    }
+  }
+  if (rc == ZC_OK)
+    rc = radix_transpose(nk, static_cast<uint64_t*>(toff.p), &tin, ne, nv, sorted, &oo, g, "out:t2",
+                         g->d_off);
+  if (rc == ZC_ENOMEM) {  // the in-lists fit but not the second transpose: sort them back
+    set_error("out of device memory (list transpose)");
+  }
+  cudaEventRecord(e1, 0);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  set_sort_gpu_ms(ms);
+  if (rc) return rc;
+  if (keep && copy.p) {
+    keep_in_e->take(&copy);
+    keep_in_off->take(&toff);
+  }
+  return ZC_OK;
+}
+
+int build_out_stream(zc_graph* g, DevBuf* keep_lists, DevBuf* keep_in_e = nullptr,
+                     DevBuf* keep_in_off = nullptr) {
   cudaSetDevice(g->device);
   ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
   build_start(g);
@@ -491,7 +632,7 @@ int build_out_stream(zc_graph* g, DevBuf* keep_lists) {
     ZC_CUDA_TRY(sorted.scratch(std::max<uint64_t>(ne, 1) * 4));
     ZC_CUDA_TRY(cudaMemcpy(sorted.p, g->h_edges, ne * 4, cudaMemcpyDefault));
     build_mark(g, "out:h2d_copy");
-    const int rc = sort_lists_device(4, nv, g->d_off, sorted.p);
+    const int rc = sort_out_lists(g, &sorted, keep_in_e, keep_in_off);
     if (rc) return rc;
     x.e32 = static_cast<const uint32_t*>(sorted.p);
   }
@@ -539,6 +680,18 @@ extern "C" int zc_graph_build_compressed(zc_graph* g, uint64_t* compressed_bytes
   return ZC_OK;
 }
 
+namespace {
+// Sorted in-lists (device, offsets in_off) -> the handle's in-list stream.
+int finish_in_lists(zc_graph* g, DevBuf* in_e, DevBuf* in_off, uint64_t* compressed_bytes) {
+  int rc = install_in_lists(g, static_cast<uint64_t*>(in_off->p), static_cast<uint32_t*>(in_e->p));
+  if (rc) return rc;
+  in_off->release();  // owned by the handle now
+  if ((rc = alloc_pull_state(g))) return rc;
+  if (compressed_bytes) *compressed_bytes = g->cmp_in_bytes;
+  return ZC_OK;
+}
+}  // namespace
+
 extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) {
   if (!g) {
     set_error("null graph handle");
@@ -558,8 +711,12 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
   }
   const bool transpose = (g->flags & ZC_F_DIRECTED) != 0;
   DevBuf out_e;  // the raw lists on the device (any order inside a list)
+  DevBuf kin_e, kin_off;  // or the out-list sort's transpose: the sorted in-lists
   int rc = ZC_OK;
-  if (!g->h_cmp && (rc = build_out_stream(g, transpose ? &out_e : nullptr))) return rc;
+  if (!g->h_cmp &&
+      (rc = build_out_stream(g, transpose ? &out_e : nullptr, transpose ? &kin_e : nullptr,
+                             transpose ? &kin_off : nullptr)))
+    return rc;
   cudaSetDevice(g->device);
   build_start(g);
   const uint64_t nv = g->nv, ne = g->ne;
@@ -571,11 +728,35 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
     g->in_alias = true;
   } else {
     DevBuf in_e, deg, in_off, tmp;
+    if (kin_e.p) {  // transposed while sorting the out-lists
+      in_e.take(&kin_e);
+      in_off.take(&kin_off);
+      out_e.reset();
+      return finish_in_lists(g, &in_e, &in_off, compressed_bytes);
+    }
     if (!out_e.p) {
       ZC_CUDA_TRY(out_e.scratch(std::max<uint64_t>(ne, 1) * 4));
       ZC_CUDA_TRY(cudaMemcpy(out_e.p, g->h_edges, ne * 4, cudaMemcpyDefault));
       build_mark(g, "in:h2d_copy");
     }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, 0);
+    rc = g->tune.seg_sort ? ZC_ENOMEM : radix_transpose(nv, g->d_off, &out_e, ne, nv, &in_e, &in_off, g, "in:t");
+    cudaEventRecord(e1, 0);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (rc == ZC_OK) {
+      build_mark(g, "in:transpose");
+      g->build_log.emplace_back("in:transpose[gpu]", ms);
+      return finish_in_lists(g, &in_e, &in_off, compressed_bytes);
+    }
+    if (rc != ZC_ENOMEM) return rc;
+    // the radix transpose's buffers do not fit: count, scatter, segmented sort
     ZC_CUDA_TRY(deg.scratch(std::max<uint64_t>(nv, 1) * 4));
     ZC_CUDA_TRY(cudaMemset(deg.p, 0, std::max<uint64_t>(nv, 1) * 4));
     k_in_count<<<kCmpGrid, 256>>>(ne, static_cast<uint32_t*>(out_e.p),

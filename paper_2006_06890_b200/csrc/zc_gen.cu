@@ -872,6 +872,22 @@ int generate_uniform(uint64_t nv, uint32_t dmin, uint32_t dmax, uint64_t seed, i
 int part_in_lists(zc_graph* g) { return rmat_part_in_lists(g); }
 
 float last_sort_gpu_ms() { return t_sort_gpu_ms; }
+void set_sort_gpu_ms(float ms) { t_sort_gpu_ms = ms; }
+
+cudaError_t lists_ascending(uint64_t nv, const uint64_t* d_off, const uint32_t* edges, bool* yes) {
+  *yes = true;
+  if (nv == 0) return cudaSuccess;
+  unsigned* bad = nullptr;
+  cudaError_t e = cudaMalloc(&bad, sizeof(unsigned));
+  if (e != cudaSuccess) return e;
+  unsigned h = 1;
+  cudaMemset(bad, 0, sizeof(unsigned));
+  k_lists_unsorted<uint32_t><<<kGenGrid, 256>>>(nv, d_off, edges, bad);
+  e = cudaMemcpy(&h, bad, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(bad);
+  *yes = h == 0;
+  return e;
+}
 
 int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, void* edges) {
   int rc = elem_bytes == 4 ? sort_lists<uint32_t>(nv, d_off, static_cast<uint32_t*>(edges))

@@ -118,6 +118,7 @@ struct zc_graph {
     int carveout = -1;  // sweep kernels' preferred shared-memory carveout (%, -1: default)
     int widen = 0;      // host threads of an overlapped result widen (0: 4)
     int uf_sample = 0;  // afforest sampling pass on compressed lists (0: kUfSample)
+    int seg_sort = 0;   // 1: compressed builds sort by count/scatter + segmented sort, not radix transposes
   } tune;
   int multigraph = -1;  // cached duplicate-arc check (-1 unknown)
   // one-time builds (compressed streams, pairs): wall ms per phase, in order

@@ -319,6 +319,9 @@ cudaError_t launch_dup_flags(const void* sorted, int elem_bytes, const uint64_t*
 // Sort every list ascending in place (device array, zc_gen.cu).
 int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, void* edges);
 float last_sort_gpu_ms();  // GPU time of this thread's last list sort
+void set_sort_gpu_ms(float ms);
+// *yes = every list (offsets d_off, device) ascending
+cudaError_t lists_ascending(uint64_t nv, const uint64_t* d_off, const uint32_t* edges, bool* yes);
 
 // Exclusive scan of u32 counts into u64 offsets (n+1 outputs), device-wide.
 cudaError_t scan_u32_to_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp,

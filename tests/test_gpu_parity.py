@@ -894,3 +894,38 @@ def test_device_graph_cache_keeps_two_placements():
     for p in ("zerocopy", "hbm", "uvm"):
         assert np.array_equal(zc.bfs(g, 0, placement=p, collect_traffic=False).values, ref.values)
     zc.release(g)
+
+
+def test_compressed_build_radix_vs_segmented_sort():
+    """The compressed builds sort lists by two stable radix-sort transposes
+    (the first one's output is the sorted in-lists); the count / scatter /
+    segmented-sort path is the fallback (tuning sort=segmented).  Both yield
+    the same streams: equal out-list index and stream sizes, and
+    direction-optimizing BFS equal to the oracle through the in-lists."""
+    for make in (lambda: zc.generate_rmat(15, 16, seed=5),
+                 lambda: zc.generate_uniform_device(20000, 0, 40, seed=9)):
+        built = {}
+        for mode in ("radix", "segmented"):
+            k = make()
+            k.set_tuning(f"sort={mode}")
+            out_b = k.build_compressed()
+            in_b = k.build_in_lists()
+            built[mode] = (out_b, in_b, k.compressed_index())
+            gk = k.as_csr()
+            for src in zc.pick_sources(gk, 3, seed=2):
+                r = zc.bfs(k, int(src), "direction-optimizing")
+                ref = oracle.bfs(gk, int(src))
+                assert np.array_equal(r.values, ref.values), (mode, int(src))
+                assert r.traversed_edges == ref.traversed_edges
+            k.close()
+        assert built["radix"][0] == built["segmented"][0]
+        assert built["radix"][1] == built["segmented"][1]
+        assert np.array_equal(built["radix"][2], built["segmented"][2])
+    # in-lists built after the out-lists (a second radix transpose of the raw lists)
+    k = zc.generate_rmat(14, 16, seed=8)
+    k.build_compressed()
+    k.build_in_lists()
+    gk = k.as_csr()
+    src = int(zc.pick_sources(gk, 1, seed=1)[0])
+    assert np.array_equal(zc.bfs(k, src, "direction-optimizing").values, oracle.bfs(gk, src).values)
+    k.close()

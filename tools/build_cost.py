@@ -24,3 +24,15 @@ for nbytes in (nb, ni):
     t = time.time()
     N.lib().zc_host_free(p)
     print(f"zc_host_alloc({nbytes}) {ta:.2f}s free {time.time() - t:.2f}s", flush=True)
+dg.close()
+# a fresh graph's direction-optimizing build in one call: the out-list sort's
+# first radix transpose is kept as the in-lists (no second transpose)
+for tune in ("", "sort=segmented"):
+    dg = zc.generate_rmat(scale, 16, seed=27)
+    dg.set_tuning(tune)
+    t = time.time()
+    ni = dg.build_in_lists()
+    print(f"[{tune or 'sort=radix'}] fresh build_in_lists (out + in) {time.time() - t:.2f}s "
+          f"bytes={ni}", flush=True)
+    print("phases (ms):", " ".join(f"{k}={v:.0f}" for k, v in dg.build_log()), flush=True)
+    dg.close()
