@@ -137,49 +137,64 @@ static void prefault(void* p, size_t bytes) {
 
 static bool numa_disabled();
 
-void* pinned_list_alloc(int device, size_t bytes) {
+HostMap pinned_list_map(int device, size_t bytes) {
+  HostMap m;
   bytes = std::max<size_t>(bytes, 1);
-  if (bytes >= (64ull << 20)) {
-    const int node = numa_disabled() ? -1 : gpu_numa_node(device);
-    // a 2 MiB-aligned mapping of whole 2 MiB pages: an unaligned one is only
-    // partly backed by huge pages, and registering 4 KiB pages is slow (a
-    // 6.2 GB stream took 0.4-0.9 s in cudaHostRegister instead of ~0.15 s)
-    constexpr size_t kHuge = 2ull << 20;
-    bytes = (bytes + kHuge - 1) & ~(kHuge - 1);
-    void* p = MAP_FAILED;
-    void* raw = mmap(nullptr, bytes + kHuge, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS,
-                     -1, 0);
-    if (raw != MAP_FAILED) {
-      const uintptr_t r = reinterpret_cast<uintptr_t>(raw);
-      const uintptr_t a = (r + kHuge - 1) & ~(kHuge - 1);
-      if (a > r) munmap(raw, a - r);
-      if (r + kHuge > a) munmap(reinterpret_cast<void*>(a + bytes), r + kHuge - a);
-      p = reinterpret_cast<void*>(a);
-    }
-    if (p != MAP_FAILED) {
-      bool ok = true;
-      if (node >= 0 && node < 64) {
-        unsigned long mask = 1ul << node;
-        ok = syscall(SYS_mbind, p, bytes, 2 /* MPOL_BIND */, &mask, 64, 0) == 0;
-      }
-      madvise(p, bytes, MADV_HUGEPAGE);
-      if (ok) prefault(p, bytes);
-      if (ok && cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) ==
-                    cudaSuccess) {
-        std::lock_guard<std::mutex> lk(g_map_mu);
-        g_mapped[p] = bytes;
-        return p;
-      }
-      cudaGetLastError();
+  if (bytes < (64ull << 20)) return m;
+  const int node = numa_disabled() ? -1 : gpu_numa_node(device);
+  // a 2 MiB-aligned mapping of whole 2 MiB pages: an unaligned one is only
+  // partly backed by huge pages, and registering 4 KiB pages is slow (a
+  // 6.2 GB stream took 0.4-0.9 s in cudaHostRegister instead of ~0.15 s)
+  constexpr size_t kHuge = 2ull << 20;
+  bytes = (bytes + kHuge - 1) & ~(kHuge - 1);
+  void* raw = mmap(nullptr, bytes + kHuge, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS,
+                   -1, 0);
+  if (raw == MAP_FAILED) return m;
+  const uintptr_t r = reinterpret_cast<uintptr_t>(raw);
+  const uintptr_t a = (r + kHuge - 1) & ~(kHuge - 1);
+  if (a > r) munmap(raw, a - r);
+  if (r + kHuge > a) munmap(reinterpret_cast<void*>(a + bytes), r + kHuge - a);
+  void* p = reinterpret_cast<void*>(a);
+  if (node >= 0 && node < 64) {
+    unsigned long mask = 1ul << node;
+    if (syscall(SYS_mbind, p, bytes, 2 /* MPOL_BIND */, &mask, 64, 0) != 0) {
       munmap(p, bytes);
+      return m;
     }
   }
+  madvise(p, bytes, MADV_HUGEPAGE);
+  prefault(p, bytes);
+  m.p = p;
+  m.bytes = bytes;
+  return m;
+}
+
+void pinned_list_unmap(HostMap m) {
+  if (m.p) munmap(m.p, m.bytes);
+}
+
+void* pinned_list_finish(HostMap m, size_t bytes) {
+  if (m.p) {
+    if (cudaHostRegister(m.p, m.bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) ==
+        cudaSuccess) {
+      std::lock_guard<std::mutex> lk(g_map_mu);
+      g_mapped[m.p] = m.bytes;
+      return m.p;
+    }
+    cudaGetLastError();
+    munmap(m.p, m.bytes);
+  }
   void* p = nullptr;
-  if (cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+  if (cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocMapped | cudaHostAllocPortable) !=
+      cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
   return p;
+}
+
+void* pinned_list_alloc(int device, size_t bytes) {
+  return pinned_list_finish(pinned_list_map(device, bytes), bytes);
 }
 
 static bool numa_disabled() {

@@ -24,6 +24,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <future>
 #include <string>
 #include <vector>
 
@@ -452,7 +453,7 @@ int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t w
 // Place an encoded stream like the handle's lists: host (pinned / managed,
 // read zero-copy), managed (UVM) or HBM (with a host shadow).
 int place_stream(zc_graph* g, DevBuf* enc, size_t bytes, void** host_out, const void** dev_out,
-                 void** hbm_out) {
+                 void** hbm_out, std::future<HostMap>* pre = nullptr) {
   void* host = nullptr;
   const void* dev = nullptr;
   void* hbm = nullptr;
@@ -466,7 +467,8 @@ int place_stream(zc_graph* g, DevBuf* enc, size_t bytes, void** host_out, const 
     }
     dev = host;
   } else {
-    host = host_list_alloc(g, bytes);  // the stream, or the HBM run's host shadow
+    // the stream, or the HBM run's host shadow (pre: allocated in the background)
+    host = pre && pre->valid() ? pinned_list_finish(pre->get(), bytes) : host_list_alloc(g, bytes);
     if (!host) {
       set_error("cannot allocate host memory for the compressed lists");
       return ZC_ENOMEM;
@@ -493,27 +495,58 @@ int place_stream(zc_graph* g, DevBuf* enc, size_t bytes, void** host_out, const 
   return ZC_OK;
 }
 
-int install_in_lists(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted) {
+// An in-list stream encoded ahead of its placement: a fresh direction-
+// optimizing build encodes the in-lists right after the out-list sort and
+// allocates their pinned host stream on a background thread while the
+// out-list stream is encoded and placed.
+struct InPrep {
+  DevBuf in_e, in_off;  // sorted in-lists (device) and their offsets
   DevBuf enc, cpos;
-  Elems x{d_in_sorted, nullptr, 0};
   size_t bytes = 0;
+  std::future<HostMap> host;  // the host stream's mapping, prefaulted in the background
+  ~InPrep() {
+    if (host.valid()) pinned_list_unmap(host.get());
+  }
+};
+
+int prepare_in_stream(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted, InPrep* p,
+                      bool background_alloc) {
+  Elems x{d_in_sorted, nullptr, 0};
   int rc = encode_stream(g->nv, d_in_off, x, 0, first_element_bits(g),
-                         g->placement == ZC_PLACE_HBM, &cpos, &enc, &bytes);
+                         g->placement == ZC_PLACE_HBM, &p->cpos, &p->enc, &p->bytes);
   if (rc) return rc;
+  if (background_alloc && (g->placement == ZC_PLACE_ZEROCOPY || g->placement == ZC_PLACE_HBM)) {
+    // only the mapping and first touch: registering pins pages under a driver
+    // lock that would stall this thread's device calls (measured: slower)
+    const size_t bytes = p->bytes;
+    const int dev = g->device;
+    p->host = std::async(std::launch::async, [dev, bytes] { return pinned_list_map(dev, bytes); });
+  }
   build_mark(g, "in:size_place");
+  return ZC_OK;
+}
+
+int place_in_stream(zc_graph* g, uint64_t* d_in_off, InPrep* p) {
   void* host = nullptr;
   const void* dev = nullptr;
   void* hbm = nullptr;
-  if ((rc = place_stream(g, &enc, bytes, &host, &dev, &hbm))) return rc;
+  int rc = place_stream(g, &p->enc, p->bytes, &host, &dev, &hbm, &p->host);
+  if (rc) return rc;
   g->h_cmp_in = host;
   g->d_cmp_in = dev;
   g->hbm_cmp_in = hbm;
-  g->d_cpos_in = static_cast<uint64_t*>(cpos.release());
+  g->d_cpos_in = static_cast<uint64_t*>(p->cpos.release());
   g->d_in_off = d_in_off;
-  g->cmp_in_bytes = bytes;
+  g->cmp_in_bytes = p->bytes;
   rc = alloc_pull_state(g);
   build_mark(g, "in:pull_state");
   return rc;
+}
+
+int install_in_lists(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted) {
+  InPrep p;
+  int rc = prepare_in_stream(g, d_in_off, d_in_sorted, &p, false);
+  return rc ? rc : place_in_stream(g, d_in_off, &p);
 }
 
 int alloc_pull_state(zc_graph* g) {
@@ -594,8 +627,7 @@ int sort_out_lists(zc_graph* g, DevBuf* sorted, DevBuf* keep_in_e, DevBuf* keep_
   return ZC_OK;
 }
 
-int build_out_stream(zc_graph* g, DevBuf* keep_lists, DevBuf* keep_in_e = nullptr,
-                     DevBuf* keep_in_off = nullptr) {
+int build_out_stream(zc_graph* g, DevBuf* keep_lists, InPrep* prep = nullptr) {
   cudaSetDevice(g->device);
   ZC_CUDA_TRY(cudaStreamSynchronize(g->stream));
   build_start(g);
@@ -632,9 +664,14 @@ int build_out_stream(zc_graph* g, DevBuf* keep_lists, DevBuf* keep_in_e = nullpt
     ZC_CUDA_TRY(sorted.scratch(std::max<uint64_t>(ne, 1) * 4));
     ZC_CUDA_TRY(cudaMemcpy(sorted.p, g->h_edges, ne * 4, cudaMemcpyDefault));
     build_mark(g, "out:h2d_copy");
-    const int rc = sort_out_lists(g, &sorted, keep_in_e, keep_in_off);
+    int rc = sort_out_lists(g, &sorted, prep ? &prep->in_e : nullptr,
+                            prep ? &prep->in_off : nullptr);
     if (rc) return rc;
     x.e32 = static_cast<const uint32_t*>(sorted.p);
+    if (prep && prep->in_e.p &&  // the in-lists came with the sort: encode them now
+        (rc = prepare_in_stream(g, static_cast<uint64_t*>(prep->in_off.p),
+                                static_cast<uint32_t*>(prep->in_e.p), prep, true)))
+      return rc;
   }
   build_mark(g, "out:sort");
   g->build_log.emplace_back("out:sort[gpu]", last_sort_gpu_ms());
@@ -711,11 +748,10 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
   }
   const bool transpose = (g->flags & ZC_F_DIRECTED) != 0;
   DevBuf out_e;  // the raw lists on the device (any order inside a list)
-  DevBuf kin_e, kin_off;  // or the out-list sort's transpose: the sorted in-lists
+  InPrep prep;  // or the out-list sort's transpose: the sorted, encoded in-lists
   int rc = ZC_OK;
   if (!g->h_cmp &&
-      (rc = build_out_stream(g, transpose ? &out_e : nullptr, transpose ? &kin_e : nullptr,
-                             transpose ? &kin_off : nullptr)))
+      (rc = build_out_stream(g, transpose ? &out_e : nullptr, transpose ? &prep : nullptr)))
     return rc;
   cudaSetDevice(g->device);
   build_start(g);
@@ -728,11 +764,12 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
     g->in_alias = true;
   } else {
     DevBuf in_e, deg, in_off, tmp;
-    if (kin_e.p) {  // transposed while sorting the out-lists
-      in_e.take(&kin_e);
-      in_off.take(&kin_off);
+    if (prep.enc.p) {  // transposed and encoded while the out-lists were built
       out_e.reset();
-      return finish_in_lists(g, &in_e, &in_off, compressed_bytes);
+      if ((rc = place_in_stream(g, static_cast<uint64_t*>(prep.in_off.p), &prep))) return rc;
+      prep.in_off.release();  // owned by the handle now
+      if (compressed_bytes) *compressed_bytes = g->cmp_in_bytes;
+      return ZC_OK;
     }
     if (!out_e.p) {
       ZC_CUDA_TRY(out_e.scratch(std::max<uint64_t>(ne, 1) * 4));

@@ -175,6 +175,16 @@ int finish_create(zc_graph* g);  // prefetch (UVM) + sync
 int init_partition(zc_graph* g, const zc_part_info* info);
 // pinned mapped list buffers, NUMA-local to the GPU when the host has several nodes
 void* pinned_list_alloc(int device, size_t bytes);
+// pinned_list_alloc in two halves: the prefaulted huge-page mapping (no CUDA
+// calls, so another thread can run it beside device work; p == nullptr when
+// small or failed), then its registration (cudaHostAlloc on any failure).
+struct HostMap {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+HostMap pinned_list_map(int device, size_t bytes);
+void* pinned_list_finish(HostMap m, size_t bytes);
+void pinned_list_unmap(HostMap m);
 
 void pinned_list_free(void* p);
 // Host-side list buffer of a handle: pinned (ZEROCOPY, and the HBM run's
