@@ -695,9 +695,13 @@ def other_configs(zc, args, device, oc, parity) -> dict:
     # PageRank streams the whole zero-copy list every
     # iteration (5 iterations timed; parity is pinned on the reference's
     # PageRank fixtures in the GPU tests; here against the oracle's threaded
-    # C pull: float64 sums against the library's 2^-62 fixed-point sums, so
-    # |gpu - oracle| <= 1e-9 rank + 1e-16 per vertex (1e-16 ~ 450 quanta; the
-    # smallest ranks, ~1e-9 at K27, carry a few quanta per summed element)
+    # C pull: float64 sums against the library's 2^-62 fixed-point sums.  Each
+    # iteration quantises every summed contribution (round to nearest, <= 2^-63
+    # each), so vertex v's sum is off by <= deg(v) 2^-63 per iteration, and
+    # errors of earlier iterations reach it damped (x 0.85 per hop, spread over
+    # the neighbours' degrees): after k iterations <= k(k+1)/2 (deg(v)+1) 2^-62.
+    # The check: |gpu - oracle| <= that + 1e-9 rank + 1e-16 per vertex (a hub of
+    # degree ~1e6 carries ~1e-12 absolute, ~3e-9 relative, at K27)
     import oracle
     import warnings
     t0 = time.perf_counter()
@@ -711,6 +715,8 @@ def other_configs(zc, args, device, oc, parity) -> dict:
             r = zc.pagerank(k, s, max_iters=5, tol=1e-30, collect_traffic=False)
         t = r.kernel_ms * 1e-3
         err = np.abs(r.values - pr_ref.values)
+        fx = (r.iterations * (r.iterations + 1) / 2) * (np.diff(np.asarray(gk.offsets)) + 1.0) \
+            * 2.0 ** -62
         out[f"{tag}/{s}"] = {
             "iterations": r.iterations, "kernel_ms": r.kernel_ms,
             "edge_gteps": r.total_traversed_edges / t / 1e9,
@@ -718,7 +724,9 @@ def other_configs(zc, args, device, oc, parity) -> dict:
             "max_abs_err_vs_oracle": float(err.max()),
             "max_rel_err_vs_oracle": float(np.max(err / pr_ref.values))}
         parity[f"{tag}/{s}"] = bool(r.iterations == pr_ref.iterations
-                                    and np.all(err <= 1e-9 * pr_ref.values + 1e-16))
+                                    and np.all(err <= 1e-9 * pr_ref.values + 1e-16 + fx))
+        out[f"{tag}/{s}"]["max_err_over_fixed_point_bound"] = float(
+            np.max(err / (1e-9 * pr_ref.values + 1e-16 + fx)))
     out[f"{tag}/cpu_port_edge_gteps"] = sum(pr_ref.traversed_edges) / pr_s / 1e9
     k.close()
     return out
