@@ -388,6 +388,52 @@ int radix_transpose(uint64_t nl, const uint64_t* d_off, DevBuf* e, uint64_t ne, 
 }
 }  // namespace
 
+// Every list (offsets d_off, u32 elements < nk) sorted in place by two radix
+// transposes through three scratch buffers: the first leaves the transposed
+// lists in one of them, the second writes the sorted lists back (into
+// `edges` itself, or a copy).  ZC_ENOMEM, lists untouched, when the scratch
+// does not fit.  sort_lists (zc_gen.cu) takes it before its segmented sort.
+int sort_lists_radix(uint64_t nv, const uint64_t* d_off, uint32_t* edges, uint64_t ne,
+                     uint64_t nk) {
+  const uint32_t bits_k = nk > 1 ? 64 - __builtin_clzll(nk - 1) : 1;
+  const uint32_t bits_v = nv > 1 ? 64 - __builtin_clzll(nv - 1) : 1;
+  const size_t nb = std::max<uint64_t>(ne, 1) * sizeof(uint32_t);
+  DevBuf K, S, V, toff, tmp;
+  cub::DoubleBuffer<uint32_t> pk(nullptr, nullptr), pv(nullptr, nullptr);
+  size_t tb = 0;
+  ZC_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, pk, pv, ne, 0,
+                                              static_cast<int>(std::max(bits_k, bits_v))));
+  if (K.scratch(nb) != cudaSuccess || S.scratch(nb) != cudaSuccess ||
+      V.scratch(nb) != cudaSuccess || toff.scratch((nk + 1) * sizeof(uint64_t)) != cudaSuccess ||
+      tmp.scratch(tb) != cudaSuccess) {
+    cudaGetLastError();
+    return ZC_ENOMEM;
+  }
+  uint32_t* E = edges;
+  uint32_t* k = static_cast<uint32_t*>(K.p);
+  uint32_t* sp = static_cast<uint32_t*>(S.p);
+  uint32_t* vp = static_cast<uint32_t*>(V.p);
+  // 1: keys = elements, values = owning lists (ascending) -> transposed lists
+  k_arc_sources<<<kCmpGrid, 256>>>(nv, d_off, sp);
+  cub::DoubleBuffer<uint32_t> keys(E, k), vals(sp, vp);
+  ZC_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys, vals, ne, 0,
+                                              static_cast<int>(bits_k)));
+  k_offsets_from_sorted<<<kCmpGrid, 256>>>(ne, keys.Current(), nk,
+                                           static_cast<uint64_t*>(toff.p));
+  ZC_CUDA_TRY(cudaGetLastError());
+  uint32_t* T = vals.Current();
+  uint32_t* U = T == sp ? vp : sp;
+  // 2: keys = transposed elements (list ids), values = their owners -> sorted lists
+  k_arc_sources<<<kCmpGrid, 256>>>(nk, static_cast<uint64_t*>(toff.p), k);
+  cub::DoubleBuffer<uint32_t> keys2(T, U), vals2(k, E);
+  ZC_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys2, vals2, ne, 0,
+                                              static_cast<int>(bits_v)));
+  if (vals2.Current() != E)
+    ZC_CUDA_TRY(cudaMemcpyAsync(E, vals2.Current(), nb, cudaMemcpyDeviceToDevice, 0));
+  ZC_CUDA_TRY(cudaGetLastError());
+  return ZC_OK;
+}
+
 // Sorted lists (x) over offsets d_off -> the line stream in device memory
 // (enc) and the per-vertex bit positions (cpos).
 namespace {
@@ -591,11 +637,13 @@ int sort_out_lists(zc_graph* g, DevBuf* sorted, DevBuf* keep_in_e, DevBuf* keep_
   cudaEventCreate(&e1);
   cudaEventRecord(e0, 0);
   DevBuf tin, toff, oo;
-  int rc = g->tune.seg_sort ? ZC_ENOMEM : radix_transpose(nv, g->d_off, sorted, ne, nk, &tin, &toff, g, "out:t1");
+  int rc = g->tune.seg_sort
+               ? ZC_ENOMEM
+               : radix_transpose(nv, g->d_off, sorted, ne, nk, &tin, &toff, g, "out:t1");
   if (rc == ZC_ENOMEM) {  // sorted is intact
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    return sort_lists_device(4, nv, g->d_off, sorted->p);
+    return sort_lists_device(4, nv, g->d_off, sorted->p, !g->tune.seg_sort);
   }
   const bool keep = keep_in_e && !g->nparts && (g->flags & ZC_F_DIRECTED);
   DevBuf copy;
@@ -607,10 +655,19 @@ int sort_out_lists(zc_graph* g, DevBuf* sorted, DevBuf* keep_in_e, DevBuf* keep_
     }
   }
   if (rc == ZC_OK)
-    rc = radix_transpose(nk, static_cast<uint64_t*>(toff.p), &tin, ne, nv, sorted, &oo, g, "out:t2",
-                         g->d_off);
-  if (rc == ZC_ENOMEM) {  // the in-lists fit but not the second transpose: sort them back
-    set_error("out of device memory (list transpose)");
+    rc = radix_transpose(nk, static_cast<uint64_t*>(toff.p), &tin, ne, nv, sorted, &oo, g,
+                         "out:t2", g->d_off);
+  if (rc == ZC_ENOMEM) {  // the first transpose fit, the second did not (the keep copy
+    // holds memory): drop both, copy the lists again and take the segmented sort
+    tin.reset();
+    toff.reset();
+    copy.reset();
+    if (sorted->scratch(std::max<uint64_t>(ne, 1) * 4) != cudaSuccess ||
+        cudaMemcpy(sorted->p, g->h_edges, ne * 4, cudaMemcpyDefault) != cudaSuccess) {
+      set_error("out of device memory (list sort)");
+    } else {
+      rc = sort_lists_device(4, nv, g->d_off, sorted->p, !g->tune.seg_sort);
+    }
   }
   cudaEventRecord(e1, 0);
   cudaEventSynchronize(e1);
@@ -620,7 +677,7 @@ int sort_out_lists(zc_graph* g, DevBuf* sorted, DevBuf* keep_in_e, DevBuf* keep_
   cudaEventDestroy(e1);
   set_sort_gpu_ms(ms);
   if (rc) return rc;
-  if (keep && copy.p) {
+  if (keep && copy.p && toff.p) {
     keep_in_e->take(&copy);
     keep_in_off->take(&toff);
   }
@@ -780,7 +837,9 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, 0);
-    rc = g->tune.seg_sort ? ZC_ENOMEM : radix_transpose(nv, g->d_off, &out_e, ne, nv, &in_e, &in_off, g, "in:t");
+    rc = g->tune.seg_sort
+             ? ZC_ENOMEM
+             : radix_transpose(nv, g->d_off, &out_e, ne, nv, &in_e, &in_off, g, "in:t");
     cudaEventRecord(e1, 0);
     cudaEventSynchronize(e1);
     float ms = 0;
@@ -814,7 +873,7 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
     out_e.reset();
     deg.reset();
     build_mark(g, "in:transpose");
-    rc = sort_lists_device(4, nv, static_cast<uint64_t*>(in_off.p), in_e.p);
+    rc = sort_lists_device(4, nv, static_cast<uint64_t*>(in_off.p), in_e.p, !g->tune.seg_sort);
     if (rc) return rc;
     build_mark(g, "in:sort");
     g->build_log.emplace_back("in:sort[gpu]", last_sort_gpu_ms());

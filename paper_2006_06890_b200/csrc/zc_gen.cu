@@ -22,10 +22,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cub/device/device_reduce.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "zc_graph.cuh"
@@ -346,7 +348,7 @@ __global__ void k_rel_offsets(uint64_t n, const uint64_t* off, uint64_t base, in
 thread_local float t_sort_gpu_ms = 0;
 
 template <typename ET>
-int sort_lists(uint64_t nv, const uint64_t* d_off, ET* edges) {
+int sort_lists(uint64_t nv, const uint64_t* d_off, ET* edges, bool radix = true) {
   t_sort_gpu_ms = 0;
   if (nv == 0) return ZC_OK;
   {  // already ascending (graphs built by a lexsort, symmetrized ones): done
@@ -359,6 +361,38 @@ int sort_lists(uint64_t nv, const uint64_t* d_off, ET* edges) {
     cudaFree(bad);
     ZC_CUDA_TRY(e);
     if (!h) return ZC_OK;
+  }
+  if constexpr (std::is_same<ET, uint32_t>::value) {  // radix transposes when they fit
+    uint64_t ne = 0;
+    ZC_CUDA_TRY(cudaMemcpy(&ne, d_off + nv, sizeof(ne), cudaMemcpyDeviceToHost));
+    if (radix && ne > 0) {
+      uint32_t* mx = nullptr;
+      void* tmp = nullptr;
+      size_t tb = 0;
+      uint32_t hmx = 0;
+      ZC_CUDA_TRY(cub::DeviceReduce::Max(nullptr, tb, edges, mx, ne));
+      ZC_CUDA_TRY(cudaMalloc(&mx, 256 + tb));
+      tmp = reinterpret_cast<char*>(mx) + 256;
+      cudaError_t e = cub::DeviceReduce::Max(tmp, tb, edges, mx, ne);
+      if (e == cudaSuccess) e = cudaMemcpy(&hmx, mx, sizeof(hmx), cudaMemcpyDeviceToHost);
+      cudaFree(mx);
+      ZC_CUDA_TRY(e);
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, 0);
+      const int rc = sort_lists_radix(nv, d_off, edges, ne, static_cast<uint64_t>(hmx) + 1);
+      cudaEventRecord(e1, 0);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      if (rc != ZC_ENOMEM) {
+        t_sort_gpu_ms = ms;
+        return rc;
+      }
+    }
   }
   std::vector<uint64_t> cut{0};
   auto off_at = [&](uint64_t v, uint64_t* x) {
@@ -889,8 +923,9 @@ cudaError_t lists_ascending(uint64_t nv, const uint64_t* d_off, const uint32_t* 
   return e;
 }
 
-int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, void* edges) {
-  int rc = elem_bytes == 4 ? sort_lists<uint32_t>(nv, d_off, static_cast<uint32_t*>(edges))
+int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, void* edges,
+                      bool radix) {
+  int rc = elem_bytes == 4 ? sort_lists<uint32_t>(nv, d_off, static_cast<uint32_t*>(edges), radix)
                            : sort_lists<uint64_t>(nv, d_off, static_cast<uint64_t*>(edges));
   if (rc) return rc;
   ZC_CUDA_TRY(cudaDeviceSynchronize());

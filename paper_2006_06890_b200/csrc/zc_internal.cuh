@@ -317,9 +317,15 @@ cudaError_t launch_pr_normalize(double* rank, uint64_t nv, uint64_t* ctr, bool d
 cudaError_t launch_dup_flags(const void* sorted, int elem_bytes, const uint64_t* off, uint64_t nv,
                              uint64_t* ctr, cudaStream_t st);
 // Sort every list ascending in place (device array, zc_gen.cu).
-int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, void* edges);
+// (u32 lists: radix transposes first unless radix == false, then the segmented sort)
+int sort_lists_device(int elem_bytes, uint64_t nv, const uint64_t* d_off, void* edges,
+                      bool radix = true);
 float last_sort_gpu_ms();  // GPU time of this thread's last list sort
 void set_sort_gpu_ms(float ms);
+// Lists sorted in place by two radix transposes (zc_compress.cu); ZC_ENOMEM
+// (untouched) when the three edge-sized scratch buffers do not fit.
+int sort_lists_radix(uint64_t nv, const uint64_t* d_off, uint32_t* edges, uint64_t ne,
+                     uint64_t nk);
 // *yes = every list (offsets d_off, device) ascending
 cudaError_t lists_ascending(uint64_t nv, const uint64_t* d_off, const uint32_t* edges, bool* yes);
 
