@@ -499,7 +499,7 @@ int encode_stream(uint64_t nv, const uint64_t* d_off, const Elems& x, uint32_t w
 // Place an encoded stream like the handle's lists: host (pinned / managed,
 // read zero-copy), managed (UVM) or HBM (with a host shadow).
 int place_stream(zc_graph* g, DevBuf* enc, size_t bytes, void** host_out, const void** dev_out,
-                 void** hbm_out, std::future<HostMap>* pre = nullptr) {
+                 void** hbm_out, std::future<HostMap>* pre = nullptr, const char* tag = "out") {
   void* host = nullptr;
   const void* dev = nullptr;
   void* hbm = nullptr;
@@ -519,7 +519,7 @@ int place_stream(zc_graph* g, DevBuf* enc, size_t bytes, void** host_out, const 
       set_error("cannot allocate host memory for the compressed lists");
       return ZC_ENOMEM;
     }
-    build_mark(g, "encode+pin_alloc");  // the host allocation overlaps the encode
+    build_mark(g, (std::string(tag) + ":encode+pin_alloc").c_str());  // overlaps the encode
     const void* d = nullptr;
     if (cudaMemcpy(host, enc->p, bytes, cudaMemcpyDefault) != cudaSuccess ||
         (g->placement != ZC_PLACE_HBM && host_list_device_ptr(host, &d) != ZC_OK)) {
@@ -534,7 +534,7 @@ int place_stream(zc_graph* g, DevBuf* enc, size_t bytes, void** host_out, const 
       dev = d;
     }
   }
-  build_mark(g, "d2h_copy");
+  build_mark(g, (std::string(tag) + ":d2h_copy").c_str());
   *host_out = host;
   *dev_out = dev;
   *hbm_out = hbm;
@@ -550,6 +550,7 @@ struct InPrep {
   DevBuf enc, cpos;
   size_t bytes = 0;
   std::future<HostMap> host;  // the host stream's mapping, prefaulted in the background
+  bool placed = false;        // installed in the handle (place_in_stream)
   ~InPrep() {
     if (host.valid()) pinned_list_unmap(host.get());
   }
@@ -576,7 +577,7 @@ int place_in_stream(zc_graph* g, uint64_t* d_in_off, InPrep* p) {
   void* host = nullptr;
   const void* dev = nullptr;
   void* hbm = nullptr;
-  int rc = place_stream(g, &p->enc, p->bytes, &host, &dev, &hbm, &p->host);
+  int rc = place_stream(g, &p->enc, p->bytes, &host, &dev, &hbm, &p->host, "in");
   if (rc) return rc;
   g->h_cmp_in = host;
   g->d_cmp_in = dev;
@@ -740,10 +741,24 @@ int build_out_stream(zc_graph* g, DevBuf* keep_lists, InPrep* prep = nullptr) {
   if (keep_lists && !weighted) keep_lists->take(&sorted);
   sorted.reset();
   build_mark(g, "out:size_place");
+  std::future<HostMap> out_map;
+  if (prep && prep->enc.p) {
+    // a fresh direction-optimizing build: map this stream's host memory in the
+    // background while the in-list stream (mapped during the sorts) is placed
+    if (g->placement == ZC_PLACE_ZEROCOPY || g->placement == ZC_PLACE_HBM) {
+      const int dv = g->device;
+      out_map = std::async(std::launch::async, [dv, bytes] { return pinned_list_map(dv, bytes); });
+    }
+    if ((rc = place_in_stream(g, static_cast<uint64_t*>(prep->in_off.p), prep))) return rc;
+    prep->in_off.release();  // owned by the handle now
+    prep->placed = true;
+  }
   void* host = nullptr;
   const void* dev = nullptr;
   void* hbm = nullptr;
-  if ((rc = place_stream(g, &enc, bytes, &host, &dev, &hbm))) return rc;
+  rc = place_stream(g, &enc, bytes, &host, &dev, &hbm, out_map.valid() ? &out_map : nullptr);
+  if (out_map.valid()) pinned_list_unmap(out_map.get());  // place_stream failed before using it
+  if (rc) return rc;
   g->h_cmp = host;
   g->d_cmp = dev;
   g->hbm_cmp = hbm;
@@ -821,10 +836,7 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
     g->in_alias = true;
   } else {
     DevBuf in_e, deg, in_off, tmp;
-    if (prep.enc.p) {  // transposed and encoded while the out-lists were built
-      out_e.reset();
-      if ((rc = place_in_stream(g, static_cast<uint64_t*>(prep.in_off.p), &prep))) return rc;
-      prep.in_off.release();  // owned by the handle now
+    if (prep.placed) {  // transposed, encoded and placed while the out-lists were built
       if (compressed_bytes) *compressed_bytes = g->cmp_in_bytes;
       return ZC_OK;
     }
