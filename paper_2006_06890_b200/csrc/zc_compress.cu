@@ -550,7 +550,6 @@ struct InPrep {
   DevBuf enc, cpos;
   size_t bytes = 0;
   std::future<HostMap> host;  // the host stream's mapping, prefaulted in the background
-  bool placed = false;        // installed in the handle (place_in_stream)
   ~InPrep() {
     if (host.valid()) pinned_list_unmap(host.get());
   }
@@ -741,24 +740,10 @@ int build_out_stream(zc_graph* g, DevBuf* keep_lists, InPrep* prep = nullptr) {
   if (keep_lists && !weighted) keep_lists->take(&sorted);
   sorted.reset();
   build_mark(g, "out:size_place");
-  std::future<HostMap> out_map;
-  if (prep && prep->enc.p) {
-    // a fresh direction-optimizing build: map this stream's host memory in the
-    // background while the in-list stream (mapped during the sorts) is placed
-    if (g->placement == ZC_PLACE_ZEROCOPY || g->placement == ZC_PLACE_HBM) {
-      const int dv = g->device;
-      out_map = std::async(std::launch::async, [dv, bytes] { return pinned_list_map(dv, bytes); });
-    }
-    if ((rc = place_in_stream(g, static_cast<uint64_t*>(prep->in_off.p), prep))) return rc;
-    prep->in_off.release();  // owned by the handle now
-    prep->placed = true;
-  }
   void* host = nullptr;
   const void* dev = nullptr;
   void* hbm = nullptr;
-  rc = place_stream(g, &enc, bytes, &host, &dev, &hbm, out_map.valid() ? &out_map : nullptr);
-  if (out_map.valid()) pinned_list_unmap(out_map.get());  // place_stream failed before using it
-  if (rc) return rc;
+  if ((rc = place_stream(g, &enc, bytes, &host, &dev, &hbm))) return rc;
   g->h_cmp = host;
   g->d_cmp = dev;
   g->hbm_cmp = hbm;
@@ -836,7 +821,10 @@ extern "C" int zc_graph_build_in_lists(zc_graph* g, uint64_t* compressed_bytes) 
     g->in_alias = true;
   } else {
     DevBuf in_e, deg, in_off, tmp;
-    if (prep.placed) {  // transposed, encoded and placed while the out-lists were built
+    if (prep.enc.p) {  // transposed and encoded while the out-lists were built
+      out_e.reset();
+      if ((rc = place_in_stream(g, static_cast<uint64_t*>(prep.in_off.p), &prep))) return rc;
+      prep.in_off.release();  // owned by the handle now
       if (compressed_bytes) *compressed_bytes = g->cmp_in_bytes;
       return ZC_OK;
     }
