@@ -97,31 +97,68 @@ __host__ __device__ __forceinline__ uint64_t short_bits(uint64_t d, uint32_t w, 
   return kCmpShortWidthBits + b0 + (d - 1) * w + d * ww;
 }
 
+// Lists of at most kLaneList elements are sized / encoded by one lane each
+// (32 lists per warp in flight: the warp-per-list loop was latency-bound,
+// 15-25 % SM throughput, long-scoreboard stalls); longer lists, and the rare
+// short-degree list too wide for a span, take the warp-cooperative path.
+constexpr uint32_t kLaneList = 32;
+
+// Largest delta of a list of 1 <= d <= kLaneList elements, one lane.
+__device__ __forceinline__ uint32_t lane_max_delta(const Elems& x, uint64_t s, uint32_t d) {
+  uint32_t prev = x.dst(s), mx = 0;
+#pragma unroll 4
+  for (uint32_t k = 1; k < d; ++k) {
+    const uint32_t c = x.dst(s + k);
+    mx = max(mx, c - prev);
+    prev = c;
+  }
+  return mx;
+}
+
+// Size word of list [s, s + d), warp-cooperative (any d >= 1).
+__device__ uint32_t size_list_warp(const Elems& x, uint64_t s, uint64_t d, uint32_t ww,
+                                   uint32_t b0, int lane) {
+  const uint64_t sb = short_bits(d, list_width(x, s, d, lane), ww, b0);
+  if (sb <= kShortSpanBits && d <= kCmpShortMaxDeg)  // one lane decodes a short list
+    return static_cast<uint32_t>(sb);
+  uint32_t n = 0;
+  for (uint64_t p = 0; p < d; ++n) {
+    uint32_t cnt, w;
+    line_fill(x, s, d, p, ww, lane, &cnt, &w);
+    p += cnt;
+  }
+  return kLongSize | n;
+}
+
 // Size word of every list: 0 (empty), its bit length (short), or
-// kLongSize | lines (long).
+// kLongSize | lines (long).  A warp takes 32 consecutive lists at a time.
 __global__ void k_cmp_size(uint64_t nv, const uint64_t* off, Elems x, uint32_t ww, uint32_t b0,
                            uint32_t* size) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t v = gw; v < nv; v += nw) {
-    const uint64_t s = off[v], d = off[v + 1] - s;
-    uint32_t out = 0;
-    if (d) {
-      const uint64_t sb = short_bits(d, list_width(x, s, d, lane), ww, b0);
-      if (sb <= kShortSpanBits && d <= kCmpShortMaxDeg) {  // one lane decodes a short list
-        out = static_cast<uint32_t>(sb);
-      } else {
-        uint32_t n = 0;
-        for (uint64_t p = 0; p < d; ++n) {
-          uint32_t cnt, w;
-          line_fill(x, s, d, p, ww, lane, &cnt, &w);
-          p += cnt;
-        }
-        out = kLongSize | n;
-      }
+  for (uint64_t base = gw * 32; base < nv; base += nw * 32) {
+    const uint64_t v = base + lane;
+    uint64_t s = 0, d = 0;
+    if (v < nv) {
+      s = off[v];
+      d = off[v + 1] - s;
     }
-    if (lane == 0) size[v] = out;
+    uint32_t out = 0;
+    bool warp_path = d > kLaneList;
+    if (d && d <= kLaneList) {
+      const uint64_t sb = short_bits(d, bits_of(lane_max_delta(x, s, static_cast<uint32_t>(d))),
+                                     ww, b0);
+      if (sb <= kShortSpanBits) out = static_cast<uint32_t>(sb);
+      else warp_path = true;
+    }
+    for (unsigned m = __ballot_sync(kFullMask, warp_path); m; m &= m - 1) {
+      const int l = __ffs(m) - 1;
+      const uint32_t o = size_list_warp(x, __shfl_sync(kFullMask, s, l),
+                                        __shfl_sync(kFullMask, d, l), ww, b0, lane);
+      if (lane == l) out = o;
+    }
+    if (v < nv) size[v] = out;
   }
 }
 
@@ -135,8 +172,83 @@ __device__ __forceinline__ void put_bits(uint32_t* out, uint64_t bit, uint32_t v
   if (sh + nbits > 32) atomicOr(out + (bit >> 5) + 1, val >> (32 - sh));
 }
 
-// Encode: warp per list.  Short lists OR their fields into shared lines;
-// long lists build each line in a shared-memory buffer and store it whole.
+// Short list [s, s + d) at bit `pos`, one lane: width, first element, deltas,
+// weights.  Lists share words at their ends, hence the OR atomics.
+__device__ __forceinline__ void encode_short_lane(const Elems& x, uint64_t s, uint32_t d,
+                                                  uint32_t ww, uint32_t b0, uint64_t pos,
+                                                  uint32_t* out) {
+  const uint32_t w = bits_of(lane_max_delta(x, s, d));
+  const uint64_t hdr = pos + kCmpShortWidthBits + b0, wbase = hdr + (d - 1) * w;
+  uint32_t prev = x.dst(s);
+  put_bits(out, pos, w, kCmpShortWidthBits);
+  put_bits(out, pos + kCmpShortWidthBits, prev, b0);
+  put_bits(out, wbase, x.wt(s), ww);
+#pragma unroll 4
+  for (uint32_t k = 1; k < d; ++k) {
+    const uint32_t c = x.dst(s + k);
+    put_bits(out, hdr + (k - 1) * w, c - prev, w);
+    put_bits(out, wbase + k * ww, x.wt(s + k), ww);
+    prev = c;
+  }
+}
+
+// List [s, s + d) with index word c, warp-cooperative (any d >= 1).  Short
+// lists OR their fields into shared lines; long lists build each line in a
+// shared-memory buffer (L, this warp's) and store it whole.
+__device__ void encode_list_warp(const Elems& x, uint64_t s, uint64_t d, uint64_t c, uint32_t ww,
+                                 uint32_t b0, uint32_t* out, uint32_t* L, int lane) {
+  const uint64_t pos = cmp_pos(c);
+  if (!(c & kCmpLong)) {
+    const uint32_t w = list_width(x, s, d, lane);
+    const uint64_t hdr = kCmpShortWidthBits + b0;
+    if (lane == 0) {
+      put_bits(out, pos, w, kCmpShortWidthBits);
+      put_bits(out, pos + kCmpShortWidthBits, x.dst(s), b0);
+    }
+    const uint64_t wbase = pos + hdr + (d - 1) * w;
+    for (uint64_t k = lane; k < d; k += 32) {
+      if (k) put_bits(out, pos + hdr + (k - 1) * w, x.dst(s + k) - x.dst(s + k - 1), w);
+      put_bits(out, wbase + k * ww, x.wt(s + k), ww);
+    }
+    return;
+  }
+  const uint64_t l0 = pos / kLineBits, nl = cmp_lines(c);
+  uint64_t p = 0;
+  for (uint64_t t = 0; t < nl; ++t) {
+    uint32_t cnt, w;
+    line_fill(x, s, d, p, ww, lane, &cnt, &w);
+    L[lane] = 0;
+    if (lane < 2) L[kLineWords + lane] = 0;
+    __syncwarp();
+    const uint32_t wb = kCmpHdrBits + (cnt - 1) * w;
+    for (uint32_t k = lane; k < cnt; k += 32) {
+      if (k && w) {
+        const uint32_t dl = x.dst(s + p + k) - x.dst(s + p + k - 1);
+        const uint32_t bit = kCmpHdrBits + (k - 1) * w;
+        atomicOr(&L[bit >> 5], dl << (bit & 31));
+        if ((bit & 31) + w > 32) atomicOr(&L[(bit >> 5) + 1], dl >> (32 - (bit & 31)));
+      }
+      if (ww) {
+        const uint32_t wv = x.wt(s + p + k) & (ww < 32 ? (1u << ww) - 1 : ~0u);
+        const uint32_t bit = wb + k * ww;
+        atomicOr(&L[bit >> 5], wv << (bit & 31));
+        if ((bit & 31) + ww > 32) atomicOr(&L[(bit >> 5) + 1], wv >> (32 - (bit & 31)));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      L[0] = x.dst(s + p);
+      L[1] |= w | ((cnt - 1) << 6);
+    }
+    __syncwarp();
+    out[(l0 + t) * kLineWords + lane] = L[lane];
+    __syncwarp();
+    p += cnt;
+  }
+}
+
+// Encode: a warp takes 32 consecutive lists at a time, the short ones of at
+// most kLaneList elements a lane each, the rest one by one together.
 __global__ void __launch_bounds__(256) k_cmp_encode(uint64_t nv, const uint64_t* off, Elems x,
                                                     uint32_t ww, uint32_t b0, const uint64_t* cpos,
                                                     uint32_t* out) {
@@ -145,56 +257,20 @@ __global__ void __launch_bounds__(256) k_cmp_encode(uint64_t nv, const uint64_t*
   uint32_t* L = buf[threadIdx.x >> 5];
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t v = gw; v < nv; v += nw) {
-    const uint64_t s = off[v], d = off[v + 1] - s;
-    if (!d) continue;
-    const uint64_t c = cpos[v], pos = cmp_pos(c);
-    if (!(c & kCmpLong)) {
-      const uint32_t w = list_width(x, s, d, lane);
-      const uint64_t hdr = kCmpShortWidthBits + b0;
-      if (lane == 0) {
-        put_bits(out, pos, w, kCmpShortWidthBits);
-        put_bits(out, pos + kCmpShortWidthBits, x.dst(s), b0);
-      }
-      const uint64_t wbase = pos + hdr + (d - 1) * w;
-      for (uint64_t k = lane; k < d; k += 32) {
-        if (k) put_bits(out, pos + hdr + (k - 1) * w, x.dst(s + k) - x.dst(s + k - 1), w);
-        put_bits(out, wbase + k * ww, x.wt(s + k), ww);
-      }
-      continue;
+  for (uint64_t base = gw * 32; base < nv; base += nw * 32) {
+    const uint64_t v = base + lane;
+    uint64_t s = 0, d = 0, c = 0;
+    if (v < nv) {
+      s = off[v];
+      d = off[v + 1] - s;
+      if (d) c = cpos[v];
     }
-    const uint64_t l0 = pos / kLineBits, nl = cmp_lines(c);
-    uint64_t p = 0;
-    for (uint64_t t = 0; t < nl; ++t) {
-      uint32_t cnt, w;
-      line_fill(x, s, d, p, ww, lane, &cnt, &w);
-      L[lane] = 0;
-      if (lane < 2) L[kLineWords + lane] = 0;
-      __syncwarp();
-      const uint32_t wb = kCmpHdrBits + (cnt - 1) * w;
-      for (uint32_t k = lane; k < cnt; k += 32) {
-        if (k && w) {
-          const uint32_t dl = x.dst(s + p + k) - x.dst(s + p + k - 1);
-          const uint32_t bit = kCmpHdrBits + (k - 1) * w;
-          atomicOr(&L[bit >> 5], dl << (bit & 31));
-          if ((bit & 31) + w > 32) atomicOr(&L[(bit >> 5) + 1], dl >> (32 - (bit & 31)));
-        }
-        if (ww) {
-          const uint32_t wv = x.wt(s + p + k) & (ww < 32 ? (1u << ww) - 1 : ~0u);
-          const uint32_t bit = wb + k * ww;
-          atomicOr(&L[bit >> 5], wv << (bit & 31));
-          if ((bit & 31) + ww > 32) atomicOr(&L[(bit >> 5) + 1], wv >> (32 - (bit & 31)));
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        L[0] = x.dst(s + p);
-        L[1] |= w | ((cnt - 1) << 6);
-      }
-      __syncwarp();
-      out[(l0 + t) * kLineWords + lane] = L[lane];
-      __syncwarp();
-      p += cnt;
+    const bool mine = d && d <= kLaneList && !(c & kCmpLong);
+    if (mine) encode_short_lane(x, s, static_cast<uint32_t>(d), ww, b0, cmp_pos(c), out);
+    for (unsigned m = __ballot_sync(kFullMask, d && !mine); m; m &= m - 1) {
+      const int l = __ffs(m) - 1;
+      encode_list_warp(x, __shfl_sync(kFullMask, s, l), __shfl_sync(kFullMask, d, l),
+                       __shfl_sync(kFullMask, c, l), ww, b0, out, L, lane);
     }
   }
 }
