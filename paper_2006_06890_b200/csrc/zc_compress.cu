@@ -55,31 +55,49 @@ struct Elems {
 
 // Greedy fill of one long-list line starting at element p of the list [0, d):
 // the largest K <= min(255, d-1-p) with 48 + K * max(bits(delta 1..K)) +
-// (K + 1) * ww <= 1024.  Warp-cooperative; returns count = K + 1 and width.
+// (K + 1) * ww <= 1024.  Warp-cooperative, in one pass: lane l loads elements
+// 8l .. 8l+8 of the line's window (all 256 candidate deltas in flight at once;
+// a 32-delta chunk loop serialised ~5 load round trips per line, which set
+// the build's tail on hub lists), a warp prefix-max gives every delta's
+// running width, and the fitting deltas are a prefix (the cost grows with k).
+// Returns count = K + 1 and width = max bits(delta 1..K).
 __device__ __forceinline__ void line_fill(const Elems& x, uint64_t s, uint64_t d, uint64_t p,
                                           uint32_t ww, int lane, uint32_t* count,
                                           uint32_t* width) {
   const uint64_t rest = d - 1 - p;
   const uint32_t kmax = static_cast<uint32_t>(rest < kCmpMaxCount - 1 ? rest : kCmpMaxCount - 1);
-  uint32_t K = 0, m = 0;
-  for (uint32_t c = 0; c < kmax; c += 32) {
-    const uint32_t k = c + lane + 1;
-    uint32_t pm = m;
-    if (k <= kmax) pm = max(pm, bits_of(x.dst(s + p + k) - x.dst(s + p + k - 1)));
+  const uint32_t k0 = static_cast<uint32_t>(lane) * 8;  // this lane's deltas k0+1 .. k0+8
+  uint32_t e[9];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(kFullMask, pm, o);
-      if (lane >= o) pm = max(pm, t);
-    }
-    // the bit count is non-decreasing in the lane: the fitting lanes are a prefix
-    const bool ok = k <= kmax && kCmpHdrBits + k * pm + (k + 1) * ww <= kLineBits;
-    const int nok = __popc(__ballot_sync(kFullMask, ok));
-    if (nok) m = __shfl_sync(kFullMask, pm, nok - 1);
-    K = c + nok;
-    if (nok < 32) break;
+  for (int j = 0; j < 9; ++j) e[j] = k0 + j <= kmax ? x.dst(s + p + k0 + j) : 0u;
+  uint32_t b[8], lm = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    b[j] = k0 + j + 1 <= kmax ? bits_of(e[j + 1] - e[j]) : 0u;
+    lm = max(lm, b[j]);
   }
+  uint32_t inc = lm;  // inclusive prefix max over lanes, then exclusive
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFullMask, inc, o);
+    if (lane >= o) inc = max(inc, t);
+  }
+  uint32_t pm = __shfl_up_sync(kFullMask, inc, 1);
+  if (lane == 0) pm = 0;
+  uint32_t n = 0, mlast = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t k = k0 + j + 1;
+    pm = max(pm, b[j]);
+    if (k <= kmax && kCmpHdrBits + k * pm + (k + 1) * ww <= kLineBits) {
+      ++n;
+      mlast = pm;
+    }
+  }
+  const uint32_t K = __reduce_add_sync(kFullMask, n);
+  const uint32_t m = __shfl_sync(kFullMask, mlast, K ? (K - 1) / 8 : 0);
   *count = K + 1;
-  *width = m;
+  *width = K ? m : 0u;
 }
 
 // Width of the widest delta of the whole list (warp-cooperative).
