@@ -660,7 +660,10 @@ int prepare_in_stream(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted, In
     // lock that would stall this thread's device calls (measured: slower)
     const size_t bytes = p->bytes;
     const int dev = g->device;
-    p->host = std::async(std::launch::async, [dev, bytes] { return pinned_list_map(dev, bytes); });
+    try {
+      p->host = std::async(std::launch::async, [dev, bytes] { return pinned_list_map(dev, bytes); });
+    } catch (...) {  // no thread: place_stream allocates on this one
+    }
   }
   build_mark(g, "in:size_place");
   return ZC_OK;
