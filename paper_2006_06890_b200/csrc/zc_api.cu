@@ -42,11 +42,12 @@ static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
 // Run fn(lo, hi) over [0, n) on all host cores but `spare`.
+// `serial_below`: item counts under it run on the calling thread.
 template <typename F>
-static void parallel_for(uint64_t n, F fn, unsigned spare = 0) {
+static void parallel_for(uint64_t n, F fn, unsigned spare = 0, uint64_t serial_below = 1u << 16) {
   const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
   unsigned nt = hc > spare + 1 ? hc - spare : 1;
-  if (n < (1u << 16)) nt = 1;
+  if (n < serial_below) nt = 1;
   if (nt == 1) {
     fn(uint64_t(0), n);
     return;
@@ -1472,7 +1473,7 @@ int pread_all(int fd, void* dst, uint64_t bytes, uint64_t off) {
         done += static_cast<uint64_t>(r);
       }
     }
-  });
+  }, 0, 2);  // 64 MiB chunks on every core: page-cache copies scale with threads
   return bad ? ZC_EINVAL : ZC_OK;
 }
 
