@@ -257,6 +257,12 @@ int zc_run_profile(const zc_graph *g, double *expand_ms, uint64_t capacity);
  * starts cold (the paper's UVM timing).  No-op otherwise. */
 int zc_graph_evict(zc_graph *g);
 
+/* UVM placement: migrate the lists to the device now (cudaMemPrefetchAsync on
+ * the handle's stream; the lists stay read-mostly) -- the paper's UVM
+ * comparison with prefetch, after zc_graph_evict for a cold start.  *ms (may
+ * be NULL) = the migration's device time.  No-op (ms 0) on other placements. */
+int zc_graph_prefetch(zc_graph *g, float *ms);
+
 /* Per-handle run options. */
 #define ZC_OPT_TRAFFIC_MODEL 1u /* also evaluate the reference's request model
                                    (coalesce.py:165-207) on every frontier */

@@ -28,7 +28,7 @@ EXPORTED = (
     "zc_cc", "zc_run_log", "zc_host_alloc", "zc_host_free", "zc_generate_rmat",
     "zc_generate_uniform", "zc_set_options", "zc_set_tuning", "zc_run_traffic",
     "zc_graph_build_log",
-    "zc_run_profile", "zc_graph_evict", "zc_part_create",
+    "zc_run_profile", "zc_graph_evict", "zc_graph_prefetch", "zc_part_create",
     "zc_part_exchange_elem_bytes", "zc_part_begin", "zc_part_expand", "zc_part_apply",
     "zc_part_result", "zc_generate_rmat_part", "zc_pagerank", "zc_graph_multigraph",
     "zc_part_fused_init", "zc_part_fused_connect", "zc_part_fused_reset", "zc_part_fused_expand",
@@ -117,6 +117,7 @@ def _declare(lib: C.CDLL) -> None:
         "zc_set_tuning": (C.c_int, [P, C.c_char_p]),
         "zc_run_profile": (C.c_int, [P, P, u64]),
         "zc_graph_evict": (C.c_int, [P]),
+        "zc_graph_prefetch": (C.c_int, [P, C.POINTER(C.c_float)]),
         "zc_run_traffic": (C.c_int, [P, P, u64]),
         "zc_host_alloc": (P, [C.c_size_t]),
         "zc_host_free": (None, [P]),

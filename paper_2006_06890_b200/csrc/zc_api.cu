@@ -2525,6 +2525,36 @@ int zc_graph_evict(zc_graph* g) {
   return rc;
 }
 
+int zc_graph_prefetch(zc_graph* g, float* ms) {
+  if (!g) {
+    set_error("null graph handle");
+    return ZC_ESTATE;
+  }
+  if (ms) *ms = 0;
+  if (g->placement != ZC_PLACE_UVM || !g->ne) return ZC_OK;
+  DeviceGuard dg(g->device);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ZC_CUDA_TRY(cudaEventCreate(&e0));
+  if (cudaEventCreate(&e1) != cudaSuccess) {
+    cudaEventDestroy(e0);
+    set_error("cudaEventCreate failed");
+    return ZC_ECUDA;
+  }
+  cudaError_t e = cudaEventRecord(e0, g->stream);
+  if (e == cudaSuccess) e = cudaMemPrefetchAsync(g->h_edges, g->ne * g->eb, g->device, g->stream);
+  if (e == cudaSuccess && g->h_weights)
+    e = cudaMemPrefetchAsync(g->h_weights, g->ne * g->wb, g->device, g->stream);
+  if (e == cudaSuccess) e = cudaEventRecord(e1, g->stream);
+  if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+  float t = 0;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&t, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ZC_CUDA_TRY(e);
+  if (ms) *ms = t;
+  return ZC_OK;
+}
+
 int zc_set_tuning(zc_graph* g, const char* spec) {
   if (!g) {
     set_error("null graph handle");

@@ -194,6 +194,14 @@ class DeviceGraph:
         """UVM: move the lists back to host memory so the next run is cold."""
         N.check(N.lib().zc_graph_evict(self.handle))
 
+    def prefetch(self) -> float:
+        """UVM: migrate the lists to the GPU now (cudaMemPrefetchAsync; the
+        paper's UVM-with-prefetch comparison, after evict() for a cold
+        start).  Returns the migration's device time in ms (0 otherwise)."""
+        ms = C.c_float(0)
+        N.check(N.lib().zc_graph_prefetch(self.handle, C.byref(ms)))
+        return float(ms.value)
+
     def build_sssp_pairs(self) -> None:
         """Interleave (dst, weight) into one 8-byte stream for SSSP (extra
         8 B/edge of host memory); results are identical."""

@@ -929,3 +929,21 @@ def test_compressed_build_radix_vs_segmented_sort():
     src = int(zc.pick_sources(gk, 1, seed=1)[0])
     assert np.array_equal(zc.bfs(k, src, "direction-optimizing").values, oracle.bfs(gk, src).values)
     k.close()
+
+
+def test_uvm_prefetch_cold_then_migrated():
+    """UVM with prefetch (zc_graph_prefetch): after evict() the lists are
+    migrated back to the GPU in one call (device time > 0), the traversal
+    equals the oracle; other placements are a no-op."""
+    k = zc.generate_rmat(16, 16, seed=4, placement="uvm")
+    gk = k.as_csr()
+    src = int(zc.pick_sources(gk, 1, seed=3)[0])
+    ref = oracle.bfs(gk, src)
+    k.evict()
+    assert k.prefetch() > 0
+    r = zc.bfs(k, src, "merged-aligned")
+    assert np.array_equal(r.values, ref.values) and r.traversed_edges == ref.traversed_edges
+    k.close()
+    z = zc.generate_rmat(12, 16, seed=4)
+    assert z.prefetch() == 0
+    z.close()
