@@ -62,4 +62,20 @@ run_partitions_local(sp, "cc", 0, "merged-aligned", fused=True)
 run_partitions_local(sp, "bfs", 1, "merged-aligned", fused=True)
 wp = [generate_rmat_part(12, 2, k, seed=3, weights=(1, 9)) for k in range(2)]
 run_partitions_local(wp, "sssp", 1, "merged-aligned", fused=True)
+# round 2 (late): the radix-sort transposes on unsorted lists (directed
+# R-MAT: the fresh out + in build hands the first transpose over as the
+# in-lists; then the in-lists of a second handle built after its out-lists;
+# sort=segmented for the fallback), the lane-per-list encode, UVM prefetch
+q = hl(zc.generate_rmat(13, 16, seed=9))
+zc.bfs(q, 1, "direction-optimizing", collect_traffic=False)
+q2 = hl(zc.generate_rmat(13, 16, seed=9))
+q2.build_compressed()
+zc.bfs(q2, 1, "direction-optimizing", collect_traffic=False)
+q3 = hl(zc.generate_rmat(13, 16, seed=9))
+q3.set_tuning("loop=host,sort=segmented")
+zc.bfs(q3, 1, "direction-optimizing", collect_traffic=False)
+u = hl(zc.generate_rmat(12, 16, seed=2, placement="uvm"))
+u.evict()
+u.prefetch()
+zc.bfs(u, 1, "merged-aligned", collect_traffic=False)
 print("sanitize run ok")
