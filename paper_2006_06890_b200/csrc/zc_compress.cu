@@ -482,13 +482,19 @@ int radix_transpose(uint64_t nl, const uint64_t* d_off, DevBuf* e, uint64_t ne, 
 }
 }  // namespace
 
+namespace {
 // Every list (offsets d_off, u32 elements < nk) sorted in place by two radix
-// transposes through three scratch buffers: the first leaves the transposed
-// lists in one of them, the second writes the sorted lists back (into
-// `edges` itself, or a copy).  ZC_ENOMEM, lists untouched, when the scratch
-// does not fit.  sort_lists (zc_gen.cu) takes it before its segmented sort.
-int sort_lists_radix(uint64_t nv, const uint64_t* d_off, uint32_t* edges, uint64_t ne,
-                     uint64_t nk) {
+// transposes through three scratch buffers allocated once: the first leaves
+// the transposed lists (the graph's in-lists, ascending) in one of them, the
+// second writes the sorted lists back (into `edges` itself, or a copy).
+// keep_e / keep_off (optional) receive a copy of the first transpose and its
+// offsets.  ZC_ENOMEM, lists untouched, when the scratch does not fit.  g
+// (optional) takes the phase marks.
+int sort_lists_radix_keep(zc_graph* g, uint64_t nv, const uint64_t* d_off, uint32_t* edges,
+                          uint64_t ne, uint64_t nk, DevBuf* keep_e, DevBuf* keep_off) {
+  auto mark = [&](const char* what) {
+    if (g) build_mark(g, what);
+  };
   const uint32_t bits_k = nk > 1 ? 64 - __builtin_clzll(nk - 1) : 1;
   const uint32_t bits_v = nv > 1 ? 64 - __builtin_clzll(nv - 1) : 1;
   const size_t nb = std::max<uint64_t>(ne, 1) * sizeof(uint32_t);
@@ -503,6 +509,7 @@ int sort_lists_radix(uint64_t nv, const uint64_t* d_off, uint32_t* edges, uint64
     cudaGetLastError();
     return ZC_ENOMEM;
   }
+  mark("out:sort:alloc");
   uint32_t* E = edges;
   uint32_t* k = static_cast<uint32_t*>(K.p);
   uint32_t* sp = static_cast<uint32_t*>(S.p);
@@ -517,6 +524,14 @@ int sort_lists_radix(uint64_t nv, const uint64_t* d_off, uint32_t* edges, uint64
   ZC_CUDA_TRY(cudaGetLastError());
   uint32_t* T = vals.Current();
   uint32_t* U = T == sp ? vp : sp;
+  DevBuf copy;
+  if (keep_e) {  // the second transpose overwrites T's buffer pair
+    if (copy.scratch(nb) == cudaSuccess)
+      ZC_CUDA_TRY(cudaMemcpyAsync(copy.p, T, nb, cudaMemcpyDeviceToDevice, 0));
+    else
+      cudaGetLastError();  // no copy: the caller transposes again later
+  }
+  mark("out:sort:t1");
   // 2: keys = transposed elements (list ids), values = their owners -> sorted lists
   k_arc_sources<<<kCmpGrid, 256>>>(nk, static_cast<uint64_t*>(toff.p), k);
   cub::DoubleBuffer<uint32_t> keys2(T, U), vals2(k, E);
@@ -525,7 +540,18 @@ int sort_lists_radix(uint64_t nv, const uint64_t* d_off, uint32_t* edges, uint64
   if (vals2.Current() != E)
     ZC_CUDA_TRY(cudaMemcpyAsync(E, vals2.Current(), nb, cudaMemcpyDeviceToDevice, 0));
   ZC_CUDA_TRY(cudaGetLastError());
+  mark("out:sort:t2");
+  if (keep_e && copy.p) {
+    keep_e->take(&copy);
+    keep_off->take(&toff);
+  }
   return ZC_OK;
+}
+}  // namespace
+
+int sort_lists_radix(uint64_t nv, const uint64_t* d_off, uint32_t* edges, uint64_t ne,
+                     uint64_t nk) {
+  return sort_lists_radix_keep(nullptr, nv, d_off, edges, ne, nk, nullptr, nullptr);
 }
 
 // Sorted lists (x) over offsets d_off -> the line stream in device memory
@@ -729,43 +755,18 @@ int sort_out_lists(zc_graph* g, DevBuf* sorted, DevBuf* keep_in_e, DevBuf* keep_
   ZC_CUDA_TRY(lists_ascending(nv, g->d_off, static_cast<const uint32_t*>(sorted->p), &asc));
   set_sort_gpu_ms(0);
   if (asc) return ZC_OK;
+  const bool keep = keep_in_e && !g->nparts && (g->flags & ZC_F_DIRECTED);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, 0);
-  DevBuf tin, toff, oo;
   int rc = g->tune.seg_sort
                ? ZC_ENOMEM
-               : radix_transpose(nv, g->d_off, sorted, ne, nk, &tin, &toff, g, "out:t1");
-  if (rc == ZC_ENOMEM) {  // sorted is intact
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return sort_lists_device(4, nv, g->d_off, sorted->p, !g->tune.seg_sort);
-  }
-  const bool keep = keep_in_e && !g->nparts && (g->flags & ZC_F_DIRECTED);
-  DevBuf copy;
-  if (rc == ZC_OK && keep) {  // the second transpose consumes its input
-    if (copy.scratch(std::max<uint64_t>(ne, 1) * 4) == cudaSuccess) {
-      ZC_CUDA_TRY(cudaMemcpyAsync(copy.p, tin.p, ne * 4, cudaMemcpyDeviceToDevice, 0));
-    } else {
-      cudaGetLastError();
-    }
-  }
-  if (rc == ZC_OK)
-    rc = radix_transpose(nk, static_cast<uint64_t*>(toff.p), &tin, ne, nv, sorted, &oo, g,
-                         "out:t2", g->d_off);
-  if (rc == ZC_ENOMEM) {  // the first transpose fit, the second did not (the keep copy
-    // holds memory): drop both, copy the lists again and take the segmented sort
-    tin.reset();
-    toff.reset();
-    copy.reset();
-    if (sorted->scratch(std::max<uint64_t>(ne, 1) * 4) != cudaSuccess ||
-        cudaMemcpy(sorted->p, g->h_edges, ne * 4, cudaMemcpyDefault) != cudaSuccess) {
-      set_error("out of device memory (list sort)");
-    } else {
-      rc = sort_lists_device(4, nv, g->d_off, sorted->p, !g->tune.seg_sort);
-    }
-  }
+               : sort_lists_radix_keep(g, nv, g->d_off, static_cast<uint32_t*>(sorted->p), ne,
+                                       nk, keep ? keep_in_e : nullptr,
+                                       keep ? keep_in_off : nullptr);
+  if (rc == ZC_ENOMEM)  // the lists are intact: the segmented sort
+    rc = sort_lists_device(4, nv, g->d_off, sorted->p, false);
   cudaEventRecord(e1, 0);
   cudaEventSynchronize(e1);
   float ms = 0;
@@ -773,12 +774,7 @@ int sort_out_lists(zc_graph* g, DevBuf* sorted, DevBuf* keep_in_e, DevBuf* keep_
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   set_sort_gpu_ms(ms);
-  if (rc) return rc;
-  if (keep && copy.p && toff.p) {
-    keep_in_e->take(&copy);
-    keep_in_off->take(&toff);
-  }
-  return ZC_OK;
+  return rc;
 }
 
 int build_out_stream(zc_graph* g, DevBuf* keep_lists, InPrep* prep = nullptr) {
