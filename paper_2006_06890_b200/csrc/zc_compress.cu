@@ -424,17 +424,15 @@ namespace {
 // Transpose by a stable device radix sort: the nl lists (offsets d_off) of
 // element ids < nk become nk lists of list ids, ascending inside each list
 // (keys = elements, values = owning list ids in ascending order; LSD radix
-// sorting is stable).  Two transposes sort every list of a graph; one turns
-// sorted or unsorted out-lists into sorted in-lists.  Replaces a count /
-// atomic-cursor scatter followed by a segmented sort (~0.9 s at 2^31 arcs).
-// e (ne elements) is consumed; t_e / t_off (nk + 1 offsets) receive the
-// result (known_off: the result's offsets, when the caller has them; else
-// they come from the sorted keys).  Returns ZC_ENOMEM with e intact and
+// sorting is stable) -- sorted in-lists from sorted or unsorted out-lists
+// (two transposes sort every list: sort_lists_radix_keep).  Replaces a count
+// / atomic-cursor scatter followed by a segmented sort (~0.55 s at 2^31
+// arcs).  e (ne elements) is consumed; t_e / t_off (nk + 1 offsets, from the
+// sorted keys) receive the result.  Returns ZC_ENOMEM with e intact and
 // nothing allocated when the four ne-element buffers do not fit (callers
 // fall back).
 int radix_transpose(uint64_t nl, const uint64_t* d_off, DevBuf* e, uint64_t ne, uint64_t nk,
-                    DevBuf* t_e, DevBuf* t_off, zc_graph* g, const char* tag,
-                    const uint64_t* known_off = nullptr) {
+                    DevBuf* t_e, DevBuf* t_off, zc_graph* g, const char* tag) {
   auto mark = [&](const char* what) {
     if (g) build_mark(g, (std::string(tag) + what).c_str());
   };
@@ -460,14 +458,8 @@ int radix_transpose(uint64_t nl, const uint64_t* d_off, DevBuf* e, uint64_t ne, 
   cub::DoubleBuffer<uint32_t> vals(static_cast<uint32_t*>(src.p), static_cast<uint32_t*>(valt.p));
   ZC_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys, vals, ne, 0,
                                               static_cast<int>(bits)));
-  if (known_off) {
-    ZC_CUDA_TRY(cudaMemcpyAsync(off.p, known_off, (nk + 1) * sizeof(uint64_t),
-                                cudaMemcpyDeviceToDevice, 0));
-  } else {
-    k_offsets_from_sorted<<<kCmpGrid, 256>>>(ne, keys.Current(), nk,
-                                             static_cast<uint64_t*>(off.p));
-    ZC_CUDA_TRY(cudaGetLastError());
-  }
+  k_offsets_from_sorted<<<kCmpGrid, 256>>>(ne, keys.Current(), nk, static_cast<uint64_t*>(off.p));
+  ZC_CUDA_TRY(cudaGetLastError());
   mark(":radix");
   DevBuf* held = vals.Current() == src.p ? &src : &valt;
   t_e->take(held);
@@ -687,7 +679,8 @@ int prepare_in_stream(zc_graph* g, uint64_t* d_in_off, uint32_t* d_in_sorted, In
     const size_t bytes = p->bytes;
     const int dev = g->device;
     try {
-      p->host = std::async(std::launch::async, [dev, bytes] { return pinned_list_map(dev, bytes); });
+      p->host = std::async(std::launch::async,
+                           [dev, bytes] { return pinned_list_map(dev, bytes); });
     } catch (...) {  // no thread: place_stream allocates on this one
     }
   }
