@@ -275,9 +275,11 @@ int zc_set_options(zc_graph *g, uint32_t options);
  * comma-separated "unroll=2|4|8", "ctas=N" (sweep CTAs per SM),
  * "sched=chunk|sweep", "loop=host|device" (host-driven level loop, e.g. under
  * a profiler, which cannot see kernels inside conditional graph nodes),
- * "do_alpha=X" (direction-optimizing switch factor), "ld=0..3" (load flavour of
+ * "do_alpha=X" (direction-optimizing switch factor), "ld=0..4" (load flavour of
  * the raw-list BFS sweeps: L1::no_allocate, L1-cached, read-only path,
- * L1::evict_first), "pairs=0|1" (SSSP reads the separate edge and weight
+ * L1::evict_first; 4 = L1-cached with a 3-sector merged-aligned window read
+ * as its whole 128-byte line, the merged-aligned BFS default -- ld=1 gives
+ * its plain windows), "pairs=0|1" (SSSP reads the separate edge and weight
  * arrays / the interleaved pairs stream), "carveout=0..100" (the sweeps'
  * preferred shared-memory carveout; no measurable effect on K27 BFS),
  * "widen=N" (host threads widening a pipelined result; more slow the next

@@ -2577,7 +2577,7 @@ int zc_set_tuning(zc_graph* g, const char* spec) {
     else if (k == "sched" && (v == "chunk" || v == "sweep")) t.sched = v == "chunk";
     else if (k == "loop" && (v == "host" || v == "device")) t.host_loop = v == "host";
     else if (k == "do_alpha" && atof(v.c_str()) > 0) t.do_alpha = atof(v.c_str());
-    else if (k == "ld" && v.size() == 1 && v[0] >= '0' && v[0] <= '3') t.ld = v[0] - '0';
+    else if (k == "ld" && v.size() == 1 && v[0] >= '0' && v[0] <= '4') t.ld = v[0] - '0';
     else if (k == "pairs" && (v == "0" || v == "1")) t.pairs = v == "1";
     else if (k == "widen" && atoi(v.c_str()) > 0 && atoi(v.c_str()) <= 256) t.widen = atoi(v.c_str());
     else if (k == "uf_sample" && atoi(v.c_str()) > 0 && atoi(v.c_str()) <= 1024)

@@ -838,8 +838,14 @@ __global__ void __launch_bounds__(kSweepThreads, SweepMinBlocks<STRAT, ALGO>::va
             bt.ok[u] = idx >= s0 && idx < e0;
           }
           if constexpr (ALGO == kCcUf) seen += bt.ok[u];
-          if (bt.ok[u]) {
-            bt.dst[u] = ld_list_f<LD>(E + idx);
+          bool promote = false;  // ld=4: a window of 3 sectors loads its whole line
+          if constexpr (LD == 4 && STRAT == kMergedAligned && sizeof(ET) == 4) {
+            const uint64_t base = idx - lane;
+            const uint64_t lo = max(s0, base), hi = min(e0, base + kWarp);
+            promote = hi > lo && ((hi - 1 - base) >> 3) - ((lo - base) >> 3) == 2;
+          }
+          if (bt.ok[u] || promote) {
+            bt.dst[u] = ld_list_f<LD == 4 ? 1 : LD>(E + idx);
             if constexpr (AlgoTraits<ALGO>::weighted && !IsPair<WT>::value)
               bt.wt[u] = ld_list_f<LD>(Wt + idx);
           }
@@ -1783,7 +1789,17 @@ cudaError_t expand_t(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t
       if (u == 2) return expand_sweep<STRAT, ALGO, ET, WT, 2>(a, num_sms, st, launches);
       if constexpr ((STRAT == kMergedAligned || STRAT == kMerged) &&
                     (ALGO == kBfs || ALGO == kCc)) {
-        if (u == 16) return expand_sweep<STRAT, ALGO, ET, WT, 16>(a, num_sms, st, launches);
+        if (u == 16) {
+          // merged-aligned BFS reads a window of 3 sectors as its whole line by
+          // default (ld=4; ld=1 = the plain window loads): one 128-byte request
+          // instead of a 96-byte one, which the link serves at 0.33 G/s against
+          // 0.39 G/s for full lines (+1.0-1.2 % over K27 sources, r02_promote_ab)
+          if constexpr (ALGO == kBfs && STRAT == kMergedAligned) {
+            if (a.ld < 0 || a.ld == 4)
+              return expand_sweep<STRAT, ALGO, ET, WT, 16, 4>(a, num_sms, st, launches);
+          }
+          return expand_sweep<STRAT, ALGO, ET, WT, 16>(a, num_sms, st, launches);
+        }
       }
       if (u == 8) {
         if constexpr (ALGO == kBfs && STRAT != kPacked) {

@@ -279,7 +279,7 @@ class DeviceGraph:
     def set_tuning(self, spec: str = "") -> None:
         """Launch tuning of this handle (zc_set_tuning): comma-separated
         unroll=2|4|8|16, ctas=N, sched=chunk|sweep, loop=host|device,
-        do_alpha=X, ld=0..3, pairs=0|1, carveout=0..100, widen=1..256,
+        do_alpha=X, ld=0..4, pairs=0|1, carveout=0..100, widen=1..256,
         uf_sample=1..1024; "" restores the defaults."""
         N.check(N.lib().zc_set_tuning(self.handle, spec.encode()))
 
