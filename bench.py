@@ -438,8 +438,9 @@ def main():
             "bound": "host-link", "achieved": achieved, "peak": PCIE_GEN5_X16_GBS,
             "unit": "GB/s", "frac": achieved / PCIE_GEN5_X16_GBS,
             "traffic": ncu.get("sysmem_bytes_per_launch"),
-            "traffic_kind": "ncu syslts__d_sectors_fill_sysmem x 32 B of the main-level launch "
-                            "(host-link read bytes)",
+            "traffic_kind": "ncu syslts__t_sectors_srcunit_tex_aperture_sysmem_op_read_lookup_miss "
+                            "x 32 B of the main-level launch (host-link read bytes the L2 "
+                            "fetched)",
             "traffic_algorithmic_bytes": ncu.get("algorithmic_bytes_per_launch"),
             "traffic_pcie_read_bytes": ncu.get("pcie_read_bytes_per_launch"),
             "traffic_hbm_dram_bytes": ncu.get("dram_bytes_per_launch"),
