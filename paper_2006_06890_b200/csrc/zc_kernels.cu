@@ -1802,6 +1802,10 @@ cudaError_t expand_t(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t
         }
       }
       if (u == 8) {
+        if constexpr (ALGO == kCc && STRAT == kMergedAligned) {  // whole-line 3-sector windows
+          if (a.ld < 0 || a.ld == 4)
+            return expand_sweep<STRAT, ALGO, ET, WT, 8, 4>(a, num_sms, st, launches);
+        }
         if constexpr (ALGO == kBfs && STRAT != kPacked) {
           if (a.ld == 0) return expand_sweep<STRAT, ALGO, ET, WT, 8, 0>(a, num_sms, st, launches);
           if (a.ld == 2) return expand_sweep<STRAT, ALGO, ET, WT, 8, 2>(a, num_sms, st, launches);
