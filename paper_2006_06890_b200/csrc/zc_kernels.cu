@@ -1736,6 +1736,11 @@ cudaError_t expand_sweep(const ExpandArgs& a, int num_sms, cudaStream_t st,
 
 template <int STRAT, int ALGO, typename ET, typename WT, int U>
 cudaError_t expand_u(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t* launches) {
+  if constexpr (ALGO == kPr && STRAT == kMergedAligned && sizeof(ET) == 4) {
+    // PageRank's full-list passes: whole-line 3-sector windows like BFS / CC
+    if (!a.chunk_sched && (a.ld < 0 || a.ld == 4))
+      return expand_sweep<STRAT, ALGO, ET, WT, U, 4>(a, num_sms, st, launches);
+  }
   if (!a.chunk_sched || STRAT == kPacked)
     return expand_sweep<STRAT, ALGO, ET, WT, U>(a, num_sms, st, launches);
   // default: 8 resident 256-thread CTAs per SM = 64 warps/SM (register-limited below)
