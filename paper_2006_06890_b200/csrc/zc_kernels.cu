@@ -1784,7 +1784,7 @@ cudaError_t expand_t(const ExpandArgs& a, int num_sms, cudaStream_t st, uint64_t
   // per warp, and adjacent lists' windows (which share lines) issued back to
   // back by one warp, so the L1 / L2 merge more of the reference's duplicate
   // line requests (profiles/r02_unroll_ab.txt, K27 BFS merged-aligned: 4 -> 8
-  // +1.8 %, 8 -> 16 +2.1 % (108 registers, 2 CTAs / SM); merged +8 %, +7 %;
+  // +1.8 %, 8 -> 16 +2.1 % (108 registers then, 127-128 now; 2 CTAs / SM); merged +8 %, +7 %;
   // CC-K27-sym merged-aligned 4 -> 8 +2.3 %, 8 -> 16 -0.9 %; SSSP and packed
   // unchanged or slower above 4).  zc_set_tuning unroll=2|4|8|16 and ld=0..3
   // are A/B variants.
