@@ -840,9 +840,13 @@ __global__ void __launch_bounds__(kSweepThreads, SweepMinBlocks<STRAT, ALGO>::va
           if constexpr (ALGO == kCcUf) seen += bt.ok[u];
           bool promote = false;  // ld=4: a window of 3 sectors loads its whole line
           if constexpr (LD == 4 && STRAT == kMergedAligned && sizeof(ET) == 4) {
+            // only over a 128-byte-aligned list array (every allocation here;
+            // a caller-registered buffer may not be): then the window is one
+            // memory line holding list elements, inside mapped pages
             const uint64_t base = idx - lane;
             const uint64_t lo = max(s0, base), hi = min(e0, base + kWarp);
-            promote = hi > lo && ((hi - 1 - base) >> 3) - ((lo - base) >> 3) == 2;
+            promote = (reinterpret_cast<uintptr_t>(E) & 127) == 0 && hi > lo &&
+                      ((hi - 1 - base) >> 3) - ((lo - base) >> 3) == 2;
           }
           if (bt.ok[u] || promote) {
             bt.dst[u] = ld_list_f<LD == 4 ? 1 : LD>(E + idx);
